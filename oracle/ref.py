@@ -1,0 +1,198 @@
+"""TEST INFRASTRUCTURE ONLY -- ctypes front end of oracle/_ref/libtpref.so.
+
+libtpref.so is the reference's own solver templates (tpfem, compiled from
+/root/reference/proj/include by oracle/Makefile with the shim SparseSolver)
+driving the BASELINE grid physics (oracle/grid_problem.hpp).  Only tests/,
+__graft_entry__.smoke() and bench.py's CPU legs may use this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from paper_2502_21013_b200.abi import (TP_OK, TpProblemDesc, TpSolverCfg, default_cfg)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "_ref", "libtpref.so")
+_lib = None
+
+
+class RefError(RuntimeError):
+    def __init__(self, code, msg, residual):
+        super().__init__(f"[{code}] {msg}")
+        self.code, self.residual = code, residual
+
+
+def available() -> bool:
+    return os.path.exists(LIB_PATH)
+
+
+def lib():
+    global _lib
+    if _lib is None:
+        if not available():
+            raise FileNotFoundError(f"{LIB_PATH} missing: run `make -C oracle` where /root/reference exists")
+        L = C.CDLL(LIB_PATH)
+        dp = C.POINTER(C.c_double)
+        ip = C.POINTER(C.c_int32)
+        D = C.POINTER(TpProblemDesc)
+        G = C.POINTER(TpSolverCfg)
+        L.tpref_last_error.argtypes = [C.c_char_p, C.c_size_t, dp]
+        L.tpref_desc_baseline.argtypes = [C.c_int32, D]
+        L.tpref_hardware_threads.argtypes = []
+        L.tpref_sizes.argtypes = [D, ip, ip, dp]
+        L.tpref_loads.argtypes = [D, dp]
+        L.tpref_mass.argtypes = [D, dp]
+        L.tpref_sigma.argtypes = [D, dp]
+        L.tpref_apply_k.argtypes = [D, dp, dp, C.c_int32]
+        L.tpref_jacobian_apply.argtypes = [D, dp, dp, dp]
+        L.tpref_static_init.argtypes = [D, G, dp, ip]
+        L.tpref_choose_nu_hat.argtypes = [D, G, dp, dp, dp]
+        L.tpref_residual.argtypes = [D, dp, dp, dp, C.c_int32]
+        L.tpref_periodic_solve.argtypes = [D, G, dp, dp, dp]
+        L.tpref_solve_m1.argtypes = [D, G, dp, C.c_double, dp, dp, dp, dp, C.c_int32, ip, ip, dp,
+                                     C.c_int32, dp]
+        _lib = L
+    return _lib
+
+
+def _ptr(a):
+    if a is None:
+        return None
+    return a.ctypes.data_as(C.POINTER(C.c_double if a.dtype == np.float64 else C.c_int32))
+
+
+def _check(code):
+    if code != TP_OK:
+        buf = C.create_string_buffer(1024)
+        res = C.c_double()
+        lib().tpref_last_error(buf, 1024, C.byref(res))
+        raise RefError(code, buf.value.decode(), res.value)
+
+
+def baseline_desc(config: int) -> TpProblemDesc:
+    d = TpProblemDesc()
+    _check(lib().tpref_desc_baseline(config, C.byref(d)))
+    return d
+
+
+def hardware_threads() -> int:
+    return int(lib().tpref_hardware_threads())
+
+
+def sizes(desc):
+    n, N, tau = C.c_int32(), C.c_int32(), C.c_double()
+    _check(lib().tpref_sizes(C.byref(desc), C.byref(n), C.byref(N), C.byref(tau)))
+    return n.value, N.value, tau.value
+
+
+def loads(desc):
+    n, N, _ = sizes(desc)
+    F = np.zeros((N, n))
+    _check(lib().tpref_loads(C.byref(desc), _ptr(F)))
+    return F
+
+
+def mass(desc):
+    n, _, _ = sizes(desc)
+    m = np.zeros(n)
+    _check(lib().tpref_mass(C.byref(desc), _ptr(m)))
+    return m
+
+
+def sigma(desc):
+    c = desc.cells
+    s = np.zeros(2 * c * c)
+    _check(lib().tpref_sigma(C.byref(desc), _ptr(s)))
+    return s
+
+
+def apply_k(desc, U):
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    out = np.zeros_like(U)
+    cnt = 1 if U.ndim == 1 else U.shape[0]
+    _check(lib().tpref_apply_k(C.byref(desc), _ptr(U), _ptr(out), cnt))
+    return out
+
+
+def jacobian_apply(desc, u, v):
+    u = np.ascontiguousarray(u, dtype=np.float64)
+    v = np.ascontiguousarray(v, dtype=np.float64)
+    y = np.zeros_like(v)
+    _check(lib().tpref_jacobian_apply(C.byref(desc), _ptr(u), _ptr(v), _ptr(y)))
+    return y
+
+
+def static_init(desc, cfg: TpSolverCfg | None = None):
+    cfg = cfg or default_cfg()
+    n, N, _ = sizes(desc)
+    U0 = np.zeros((N, n))
+    counts = np.zeros(N, dtype=np.int32)
+    _check(lib().tpref_static_init(C.byref(desc), C.byref(cfg), _ptr(U0), _ptr(counts)))
+    return U0, counts
+
+
+def choose_nu_hat(desc, U0, cfg: TpSolverCfg | None = None):
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    nu = np.zeros(5)
+    q = C.c_double()
+    _check(lib().tpref_choose_nu_hat(C.byref(desc), C.byref(cfg), _ptr(U0), _ptr(nu), C.byref(q)))
+    return nu, q.value
+
+
+def residual(desc, U, threads=0):
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    R = np.zeros_like(U)
+    nrm = C.c_double()
+    _check(lib().tpref_residual(C.byref(desc), _ptr(U), _ptr(R), C.byref(nrm),
+                                threads or hardware_threads()))
+    return R, nrm.value
+
+
+def periodic_solve(desc, nu_hat, G, cfg: TpSolverCfg | None = None):
+    cfg = cfg or default_cfg()
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    U = np.zeros_like(G)
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(lib().tpref_periodic_solve(C.byref(desc), C.byref(cfg), _ptr(nu), _ptr(G), _ptr(U)))
+    return U
+
+
+@dataclass
+class RefM1Result:
+    U: np.ndarray
+    history: np.ndarray
+    contraction: np.ndarray
+    iterations: int
+    status: int
+    iterates: np.ndarray | None = None
+    wall_time: float = 0.0
+    setup_time: float = 0.0
+
+
+def solve_m1(desc, nu_hat, q, U0, cfg: TpSolverCfg | None = None, keep_iterates=False,
+             cache=0) -> RefM1Result:
+    """tpfem::solve_m1_fixed_point on the grid problem (solvers.hpp:301-369)."""
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    cap = cfg.m1_max_outer + 1
+    hist = np.zeros(cap)
+    contr = np.zeros(cap)
+    it = C.c_int32()
+    st = C.c_int32()
+    U = np.zeros_like(U0)
+    its = np.zeros((cap,) + U0.shape) if keep_iterates else None
+    times = np.zeros(2)
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(lib().tpref_solve_m1(C.byref(desc), C.byref(cfg), _ptr(nu), q, _ptr(U0), _ptr(U),
+                                _ptr(hist), _ptr(contr), cap, C.byref(it), C.byref(st),
+                                _ptr(its), cache, _ptr(times)))
+    k = it.value
+    return RefM1Result(U=U, history=hist[:k + 1].copy(), contraction=contr[:k].copy(),
+                       iterations=k, status=st.value,
+                       iterates=None if its is None else its[:k + 1].copy(),
+                       wall_time=float(times[0]), setup_time=float(times[1]))

@@ -1,0 +1,240 @@
+// TEST INFRASTRUCTURE ONLY -- C ABI over the reference's own solver templates
+// (built by oracle/Makefile into oracle/_ref/libtpref.so; never linked into
+// the product).  Used by tests/ as the parity checker, by bench.py's
+// cpu_baseline leg and by `bench.py --impl reference`.
+//
+// Every entry point drives reference code unchanged:
+//   tpref_static_init   -> tpfem::static_init            (solvers.hpp:276-296)
+//   tpref_solve_m1      -> tpfem::solve_m1_fixed_point   (solvers.hpp:301-369)
+//   tpref_periodic_solve-> tpfem::PeriodicSolver::solve  (periodic.hpp:154-198)
+//   tpref_residual      -> tpfem::residual + block_l2    (periodic.hpp:35-67)
+// with tporacle::GridProblem (grid_problem.hpp) supplying the BASELINE physics.
+#include <chrono>
+#include <cstring>
+#include <string>
+#include <thread>
+
+#include "grid_problem.hpp"
+#include "tpfem/periodic.hpp"
+#include "tpfem/solvers.hpp"
+#include "../include/tpgpu_baseline.h"
+
+namespace {
+
+thread_local std::string g_err;
+thread_local double g_err_res = -1;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TP_OK;
+  } catch (const tpfem::SolveError& e) {
+    g_err = e.what();
+    g_err_res = e.residual();
+    return TP_ESOLVE;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    g_err_res = -1;
+    return TP_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_err_res = -1;
+    return TP_EINVAL;
+  }
+}
+
+tpfem::SolverConfig to_ref(const tp_solver_cfg* c) {
+  tpfem::SolverConfig s;
+  if (!c) return s;
+  s.tol = c->tol;
+  s.m1_max_outer = c->m1_max_outer;
+  s.armijo.slope = c->armijo_slope;
+  s.armijo.backtrack = c->armijo_backtrack;
+  s.armijo.max_halvings = c->armijo_max_halvings;
+  s.nu_hat_mode = c->nu_hat_mode == TP_NU_HAT_THEORY ? tpfem::NuHatMode::theory
+                                                     : tpfem::NuHatMode::frozen_field;
+  s.imag_tol = c->imag_tol;
+  s.static_tol = c->static_tol;
+  s.static_max_newton = c->static_max_newton;
+  s.threads = c->threads > 0 ? c->threads
+                             : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
+  return s;
+}
+
+tpfem::PeriodicState state_from(const tporacle::GridProblem& p, const double* U) {
+  tpfem::PeriodicState s(p.steps(), p.n_dof(), p.tau());
+  std::memcpy(s.data.data(), U, s.data.size() * sizeof(double));
+  return s;
+}
+
+std::array<double, tpfem::kNumRegions> nu_array(const double* nu_hat) {
+  std::array<double, tpfem::kNumRegions> a{};
+  for (int r = 0; r < tpfem::kNumRegions; ++r) a[static_cast<std::size_t>(r)] = nu_hat[r];
+  return a;
+}
+
+}  // namespace
+
+extern "C" {
+
+int tpref_last_error(char* buf, size_t cap, double* achieved) {
+  if (buf && cap) {
+    std::strncpy(buf, g_err.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  if (achieved) *achieved = g_err_res;
+  return TP_OK;
+}
+
+int tpref_desc_baseline(int32_t config, tp_problem_desc* d) {
+  return tp_baseline_desc_fill(config, d) == 0 ? TP_OK : TP_EINVAL;
+}
+
+int tpref_hardware_threads(void) { return static_cast<int>(std::thread::hardware_concurrency()); }
+
+int tpref_sizes(const tp_problem_desc* d, int32_t* n, int32_t* N, double* tau) {
+  return guarded([&] {
+    tporacle::validate_desc(*d);
+    if (n) *n = (d->cells - 1) * (d->cells - 1);
+    if (N) *N = d->steps;
+    if (tau) *tau = d->period / d->steps;
+  });
+}
+
+int tpref_loads(const tp_problem_desc* d, double* F) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::BlockRhs f = p.loads();
+    std::memcpy(F, f.data.data(), f.data.size() * sizeof(double));
+  });
+}
+
+int tpref_mass(const tp_problem_desc* d, double* m) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    std::vector<double> ones(static_cast<std::size_t>(p.n_dof()), 1.0);
+    p.mass().multiply(ones.data(), m);
+  });
+}
+
+int tpref_sigma(const tp_problem_desc* d, double* sigma) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    std::memcpy(sigma, p.sigma().data(), p.sigma().size() * sizeof(double));
+  });
+}
+
+int tpref_apply_k(const tp_problem_desc* d, const double* U, double* out, int32_t count) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const std::size_t n = static_cast<std::size_t>(p.n_dof());
+    for (int i = 0; i < count; ++i) p.apply_k(U + i * n, out + i * n);
+  });
+}
+
+/// y = J(u) v for one slice (Jacobian KAT support).
+int tpref_jacobian_apply(const tp_problem_desc* d, const double* u, const double* v, double* y) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    p.jacobian_k(u).multiply(v, y);
+  });
+}
+
+int tpref_static_init(const tp_problem_desc* d, const tp_solver_cfg* c, double* U0,
+                      int32_t* newton_counts) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::BlockRhs F = p.loads();
+    std::vector<int> counts;
+    const tpfem::PeriodicState U = tpfem::static_init(p, F, p.tau(), to_ref(c), &counts);
+    std::memcpy(U0, U.data.data(), U.data.size() * sizeof(double));
+    if (newton_counts)
+      for (std::size_t i = 0; i < counts.size(); ++i) newton_counts[i] = counts[i];
+  });
+}
+
+int tpref_choose_nu_hat(const tp_problem_desc* d, const tp_solver_cfg* c, const double* U0,
+                        double* nu_hat, double* q) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const int samples = (c && c->nu_hat_samples > 1) ? c->nu_hat_samples : 2000;
+    const tpfem::NuHatChoice ch = p.choose_nu_hat(cfg.nu_hat_mode, state_from(p, U0), samples);
+    for (int r = 0; r < tpfem::kNumRegions; ++r) nu_hat[r] = ch.nu_hat[static_cast<std::size_t>(r)];
+    if (q) *q = ch.q;
+  });
+}
+
+int tpref_residual(const tp_problem_desc* d, const double* U, double* R, double* norm,
+                   int32_t threads) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::BlockRhs F = p.loads();
+    const tpfem::BlockRhs res = tpfem::residual(p, state_from(p, U), F, std::max(1, threads));
+    if (R) std::memcpy(R, res.data.data(), res.data.size() * sizeof(double));
+    if (norm) *norm = tpfem::block_l2(res);
+  });
+}
+
+int tpref_periodic_solve(const tp_problem_desc* d, const tp_solver_cfg* c, const double* nu_hat,
+                         const double* G, double* U) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const tpfem::SparseMatrix<double> K = p.stiffness_frozen(nu_array(nu_hat));
+    tpfem::PeriodicSolverOptions opts = tpfem::make_periodic_options(cfg);
+    opts.cache = tpfem::CachePolicy::never;
+    const tpfem::PeriodicSolver solver(p.mass(), K, p.tau(), p.steps(), opts);
+    tpfem::BlockRhs g(p.steps(), p.n_dof());
+    std::memcpy(g.data.data(), G, g.data.size() * sizeof(double));
+    const tpfem::PeriodicState u = solver.solve(g);
+    std::memcpy(U, u.data.data(), u.data.size() * sizeof(double));
+  });
+}
+
+/// solve_m1_fixed_point on the grid problem.  cache: 0 automatic, 1 always,
+/// 2 never.  iterates (may be NULL): (cap) x N x n, iterate k at offset k*N*n.
+/// times[0] = wall seconds of the call, times[1] = PeriodicSolver setup +
+/// initial residual seconds (measured separately on the same inputs).
+int tpref_solve_m1(const tp_problem_desc* d, const tp_solver_cfg* c, const double* nu_hat,
+                   double q, const double* U0, double* U_out, double* history,
+                   double* contraction, int32_t cap, int32_t* iterations, int32_t* status,
+                   double* iterates, int32_t cache, double* times) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    tpfem::SolverConfig cfg = to_ref(c);
+    cfg.cache = cache == 1 ? tpfem::CachePolicy::always
+                           : cache == 2 ? tpfem::CachePolicy::never : tpfem::CachePolicy::automatic;
+    const tpfem::BlockRhs F = p.loads();
+    const tpfem::SparseMatrix<double> K = p.stiffness_frozen(nu_array(nu_hat));
+    const tpfem::PeriodicState U0s = state_from(p, U0);
+    std::vector<tpfem::PeriodicState> log;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [U, rep] = tpfem::solve_m1_fixed_point(p, K, F, U0s, cfg, q, iterates ? &log : nullptr);
+    const auto t1 = std::chrono::steady_clock::now();
+    if (times) {
+      times[0] = std::chrono::duration<double>(t1 - t0).count();
+      const auto s0 = std::chrono::steady_clock::now();
+      const tpfem::PeriodicSolver setup(p.mass(), K, p.tau(), p.steps(), tpfem::make_periodic_options(cfg));
+      const tpfem::BlockRhs R0 = tpfem::residual(p, U0s, F, cfg.threads);
+      (void)tpfem::block_l2(R0);
+      times[1] = std::chrono::duration<double>(std::chrono::steady_clock::now() - s0).count();
+    }
+    if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
+    for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)
+      history[k] = rep.residual_history[k];
+    if (contraction)
+      for (std::size_t k = 0; k < rep.contraction_history.size() && static_cast<int>(k) < cap; ++k)
+        contraction[k] = rep.contraction_history[k];
+    if (iterations) *iterations = rep.iterations;
+    if (status) *status = static_cast<int32_t>(rep.status);
+    if (iterates) {
+      const std::size_t sz = U.data.size();
+      for (std::size_t k = 0; k < log.size() && static_cast<int>(k) < cap; ++k)
+        std::memcpy(iterates + k * sz, log[k].data.data(), sz * sizeof(double));
+    }
+  });
+}
+
+}  // extern "C"

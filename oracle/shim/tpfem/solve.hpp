@@ -1,0 +1,499 @@
+// TEST INFRASTRUCTURE ONLY -- stand-in for the reference's tpfem/solve.hpp.
+//
+// The reference (/root/reference/proj/include/tpfem/solve.hpp:1-159) wraps
+// Eigen (SimplicialLDLT / SparseLU / PartialPivLU).  Eigen is not installed
+// in this image, so oracle/Makefile puts this directory first on the include
+// path and the reference headers (periodic.hpp, solvers.hpp, ...) compile
+// unchanged against it.  The interface is the reference's, line for line:
+//   SolveError                      solve.hpp:17-26
+//   SparseSolver<Scalar>            solve.hpp:51-126  (kResidualTol, solve with
+//                                   residual contract, clone, factor_bytes, size,
+//                                   matrix)
+//   solve_sparse                    solve.hpp:128-131
+//   solve_dense                     solve.hpp:135-157 (same backward-error test)
+// The arithmetic behind it is a self-written sparse direct method:
+//   * fill-reducing nested-dissection ordering (BFS level-set separators on the
+//     graph of A + A^T),
+//   * up-looking simplicial LDL^T (elimination tree + row patterns), used for
+//     every symmetric-flagged matrix -- real SPD blocks and the complex
+//     symmetric (NOT Hermitian, no conjugation) frequency blocks
+//     lambda_k M + K_hat, whose Hermitian part is SPD,
+//   * dense LU with partial pivoting for non-symmetric matrices and as the
+//     fallback when LDL^T meets a zero pivot (small n only),
+//   * up to three steps of iterative refinement against the original matrix.
+// Results therefore agree with Eigen's to rounding, not bitwise (SURVEY.md
+// §8(c): "bitwise parity with Eigen's factorizations is unpinned").  The shim
+// itself is pinned by compiling the reference's own test_solve.cpp,
+// test_periodic.cpp (DFT solve vs monolithic all-at-once solve) and
+// test_solvers.cpp against it (oracle/Makefile target `reftests`).
+#pragma once
+
+#include <algorithm>
+#include <cmath>
+#include <complex>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <type_traits>
+#include <vector>
+
+#include "tpfem/sparse.hpp"
+
+namespace tpfem {
+
+/// Thrown when a linear solve cannot meet its residual contract.
+class SolveError : public std::runtime_error {
+ public:
+  explicit SolveError(const std::string& what, double residual = -1.0)
+      : std::runtime_error(what), residual_(residual) {}
+  double residual() const { return residual_; }
+
+ private:
+  double residual_;
+};
+
+namespace shim {
+
+inline double abs2(double x) { return x * x; }
+inline double abs2(const std::complex<double>& x) { return std::norm(x); }
+
+/// Nested-dissection permutation of the symmetric pattern `adj` (CSR, no
+/// diagonal).  Returns perm with perm[new] = old.
+inline std::vector<Index> nested_dissection(Index n, const std::vector<Index>& ptr,
+                                            const std::vector<Index>& adj) {
+  std::vector<Index> perm;
+  perm.reserve(static_cast<std::size_t>(n));
+  std::vector<Index> owner(static_cast<std::size_t>(n), 0);  // subset id of each vertex
+  std::vector<Index> level(static_cast<std::size_t>(n), -1);
+  std::vector<Index> queue(static_cast<std::size_t>(n));
+  Index next_id = 1;
+  // BFS inside subset `id` from `src`; returns number reached, fills queue.
+  const auto bfs = [&](Index src, Index id, Index& reached) {
+    Index head = 0, tail = 0;
+    queue[static_cast<std::size_t>(tail++)] = src;
+    level[static_cast<std::size_t>(src)] = 0;
+    Index last = src;
+    while (head < tail) {
+      const Index v = queue[static_cast<std::size_t>(head++)];
+      last = v;
+      for (Index p = ptr[static_cast<std::size_t>(v)]; p < ptr[static_cast<std::size_t>(v) + 1]; ++p) {
+        const Index w = adj[static_cast<std::size_t>(p)];
+        if (owner[static_cast<std::size_t>(w)] != id || level[static_cast<std::size_t>(w)] >= 0) continue;
+        level[static_cast<std::size_t>(w)] = level[static_cast<std::size_t>(v)] + 1;
+        queue[static_cast<std::size_t>(tail++)] = w;
+      }
+    }
+    reached = tail;
+    return last;
+  };
+  struct Task {
+    std::vector<Index> nodes;
+    Index id;
+  };
+  // Explicit stack; emit order: part A, part B, then separator.  We push the
+  // separator as a "leaf" task after the two halves so it is emitted last.
+  struct Item {
+    std::vector<Index> nodes;
+    bool leaf;
+  };
+  std::vector<Item> stack;
+  {
+    std::vector<Index> all(static_cast<std::size_t>(n));
+    for (Index i = 0; i < n; ++i) all[static_cast<std::size_t>(i)] = i;
+    stack.push_back({std::move(all), false});
+  }
+  while (!stack.empty()) {
+    Item item = std::move(stack.back());
+    stack.pop_back();
+    std::vector<Index>& nodes = item.nodes;
+    if (item.leaf || nodes.size() <= 64) {
+      perm.insert(perm.end(), nodes.begin(), nodes.end());
+      continue;
+    }
+    const Index id = next_id++;
+    for (Index v : nodes) {
+      owner[static_cast<std::size_t>(v)] = id;
+      level[static_cast<std::size_t>(v)] = -1;
+    }
+    Index reached = 0;
+    Index far = bfs(nodes.front(), id, reached);
+    if (reached < static_cast<Index>(nodes.size())) {
+      // Disconnected: split off the component (no separator needed).
+      std::vector<Index> comp, rest;
+      for (Index v : nodes)
+        (level[static_cast<std::size_t>(v)] >= 0 ? comp : rest).push_back(v);
+      stack.push_back({std::move(rest), false});
+      stack.push_back({std::move(comp), false});
+      continue;
+    }
+    // Two sweeps towards a pseudo-peripheral vertex.
+    for (int sweep = 0; sweep < 2; ++sweep) {
+      for (Index v : nodes) level[static_cast<std::size_t>(v)] = -1;
+      far = bfs(far, id, reached);
+    }
+    for (Index v : nodes) level[static_cast<std::size_t>(v)] = -1;
+    bfs(far, id, reached);
+    Index depth = 0;
+    for (Index v : nodes) depth = std::max(depth, level[static_cast<std::size_t>(v)]);
+    if (depth < 2) {
+      perm.insert(perm.end(), nodes.begin(), nodes.end());
+      continue;
+    }
+    std::vector<Index> count(static_cast<std::size_t>(depth) + 1, 0);
+    for (Index v : nodes) ++count[static_cast<std::size_t>(level[static_cast<std::size_t>(v)])];
+    Index cum = 0, mid = 1;
+    const Index half = static_cast<Index>(nodes.size()) / 2;
+    for (Index l = 0; l <= depth; ++l) {
+      cum += count[static_cast<std::size_t>(l)];
+      if (cum >= half) {
+        mid = l;
+        break;
+      }
+    }
+    mid = std::clamp<Index>(mid, 1, depth - 1);
+    std::vector<Index> a, b, sep;
+    for (Index v : nodes) {
+      const Index l = level[static_cast<std::size_t>(v)];
+      (l < mid ? a : (l > mid ? b : sep)).push_back(v);
+    }
+    stack.push_back({std::move(sep), true});
+    stack.push_back({std::move(b), false});
+    stack.push_back({std::move(a), false});
+  }
+  return perm;
+}
+
+/// Up-looking simplicial LDL^T of a symmetric (or complex symmetric) matrix,
+/// after the Davis LDL algorithm: elimination tree, then row k of L from a
+/// sparse triangular solve along the tree.  No conjugation anywhere.
+template <class Scalar>
+class Ldlt {
+ public:
+  bool factor(const SparseMatrix<Scalar>& A) {
+    const Index n = A.rows();
+    n_ = n;
+    // Symmetric pattern of A (off-diagonal) for the ordering.
+    std::vector<std::vector<Index>> nb(static_cast<std::size_t>(n));
+    for (Index r = 0; r < n; ++r)
+      for (Index p = A.row_offsets()[static_cast<std::size_t>(r)];
+           p < A.row_offsets()[static_cast<std::size_t>(r) + 1]; ++p) {
+        const Index c = A.col_indices()[static_cast<std::size_t>(p)];
+        if (c == r) continue;
+        nb[static_cast<std::size_t>(r)].push_back(c);
+        nb[static_cast<std::size_t>(c)].push_back(r);
+      }
+    std::vector<Index> ptr(static_cast<std::size_t>(n) + 1, 0), adj;
+    for (Index r = 0; r < n; ++r) {
+      auto& v = nb[static_cast<std::size_t>(r)];
+      std::sort(v.begin(), v.end());
+      v.erase(std::unique(v.begin(), v.end()), v.end());
+      ptr[static_cast<std::size_t>(r) + 1] = ptr[static_cast<std::size_t>(r)] + static_cast<Index>(v.size());
+      adj.insert(adj.end(), v.begin(), v.end());
+    }
+    perm_ = nested_dissection(n, ptr, adj);
+    pinv_.assign(static_cast<std::size_t>(n), 0);
+    for (Index k = 0; k < n; ++k) pinv_[static_cast<std::size_t>(perm_[static_cast<std::size_t>(k)])] = k;
+    // Upper triangle (row <= col) of P A P^T, by columns.
+    std::vector<Index> cp(static_cast<std::size_t>(n) + 1, 0);
+    for (Index r = 0; r < n; ++r)
+      for (Index p = A.row_offsets()[static_cast<std::size_t>(r)];
+           p < A.row_offsets()[static_cast<std::size_t>(r) + 1]; ++p) {
+        const Index pr = pinv_[static_cast<std::size_t>(r)];
+        const Index pc = pinv_[static_cast<std::size_t>(A.col_indices()[static_cast<std::size_t>(p)])];
+        if (pr <= pc) ++cp[static_cast<std::size_t>(pc) + 1];
+      }
+    for (Index k = 0; k < n; ++k) cp[static_cast<std::size_t>(k) + 1] += cp[static_cast<std::size_t>(k)];
+    std::vector<Index> ci(static_cast<std::size_t>(cp.back()));
+    std::vector<Scalar> cx(static_cast<std::size_t>(cp.back()));
+    {
+      std::vector<Index> fill(cp.begin(), cp.end() - 1);
+      for (Index r = 0; r < n; ++r)
+        for (Index p = A.row_offsets()[static_cast<std::size_t>(r)];
+             p < A.row_offsets()[static_cast<std::size_t>(r) + 1]; ++p) {
+          const Index pr = pinv_[static_cast<std::size_t>(r)];
+          const Index pc = pinv_[static_cast<std::size_t>(A.col_indices()[static_cast<std::size_t>(p)])];
+          if (pr > pc) continue;
+          const Index q = fill[static_cast<std::size_t>(pc)]++;
+          ci[static_cast<std::size_t>(q)] = pr;
+          cx[static_cast<std::size_t>(q)] = A.values()[static_cast<std::size_t>(p)];
+        }
+    }
+    // Symbolic.
+    std::vector<Index> parent(static_cast<std::size_t>(n)), flag(static_cast<std::size_t>(n)),
+        lnz(static_cast<std::size_t>(n));
+    for (Index k = 0; k < n; ++k) {
+      parent[static_cast<std::size_t>(k)] = -1;
+      flag[static_cast<std::size_t>(k)] = k;
+      lnz[static_cast<std::size_t>(k)] = 0;
+      for (Index p = cp[static_cast<std::size_t>(k)]; p < cp[static_cast<std::size_t>(k) + 1]; ++p) {
+        Index i = ci[static_cast<std::size_t>(p)];
+        for (; i < k && flag[static_cast<std::size_t>(i)] != k; i = parent[static_cast<std::size_t>(i)]) {
+          if (parent[static_cast<std::size_t>(i)] == -1) parent[static_cast<std::size_t>(i)] = k;
+          ++lnz[static_cast<std::size_t>(i)];
+          flag[static_cast<std::size_t>(i)] = k;
+        }
+      }
+    }
+    lp_.assign(static_cast<std::size_t>(n) + 1, 0);
+    for (Index k = 0; k < n; ++k)
+      lp_[static_cast<std::size_t>(k) + 1] = lp_[static_cast<std::size_t>(k)] + lnz[static_cast<std::size_t>(k)];
+    li_.assign(static_cast<std::size_t>(lp_.back()), 0);
+    lx_.assign(static_cast<std::size_t>(lp_.back()), Scalar{});
+    d_.assign(static_cast<std::size_t>(n), Scalar{});
+    // Numeric.
+    std::vector<Scalar> y(static_cast<std::size_t>(n), Scalar{});
+    std::vector<Index> pattern(static_cast<std::size_t>(n));
+    double dmax = 0;
+    for (Index k = 0; k < n; ++k) {
+      y[static_cast<std::size_t>(k)] = Scalar{};
+      Index top = n;
+      flag[static_cast<std::size_t>(k)] = k;
+      lnz[static_cast<std::size_t>(k)] = 0;
+      for (Index p = cp[static_cast<std::size_t>(k)]; p < cp[static_cast<std::size_t>(k) + 1]; ++p) {
+        Index i = ci[static_cast<std::size_t>(p)];
+        y[static_cast<std::size_t>(i)] += cx[static_cast<std::size_t>(p)];
+        Index len = 0;
+        for (; flag[static_cast<std::size_t>(i)] != k; i = parent[static_cast<std::size_t>(i)]) {
+          pattern[static_cast<std::size_t>(len++)] = i;
+          flag[static_cast<std::size_t>(i)] = k;
+        }
+        while (len > 0) pattern[static_cast<std::size_t>(--top)] = pattern[static_cast<std::size_t>(--len)];
+      }
+      Scalar dk = y[static_cast<std::size_t>(k)];
+      y[static_cast<std::size_t>(k)] = Scalar{};
+      for (; top < n; ++top) {
+        const Index i = pattern[static_cast<std::size_t>(top)];
+        const Scalar yi = y[static_cast<std::size_t>(i)];
+        y[static_cast<std::size_t>(i)] = Scalar{};
+        const Index p2 = lp_[static_cast<std::size_t>(i)] + lnz[static_cast<std::size_t>(i)];
+        for (Index p = lp_[static_cast<std::size_t>(i)]; p < p2; ++p)
+          y[static_cast<std::size_t>(li_[static_cast<std::size_t>(p)])] -= lx_[static_cast<std::size_t>(p)] * yi;
+        const Scalar l_ki = yi / d_[static_cast<std::size_t>(i)];
+        dk -= l_ki * yi;
+        li_[static_cast<std::size_t>(p2)] = k;
+        lx_[static_cast<std::size_t>(p2)] = l_ki;
+        ++lnz[static_cast<std::size_t>(i)];
+      }
+      d_[static_cast<std::size_t>(k)] = dk;
+      dmax = std::max(dmax, std::sqrt(abs2(dk)));
+      if (!(std::sqrt(abs2(dk)) > 1e-14 * dmax) || !std::isfinite(std::sqrt(abs2(dk)))) return false;
+    }
+    return true;
+  }
+
+  void solve(std::vector<Scalar>& x) const {
+    const Index n = n_;
+    std::vector<Scalar> w(static_cast<std::size_t>(n));
+    for (Index k = 0; k < n; ++k) w[static_cast<std::size_t>(k)] = x[static_cast<std::size_t>(perm_[static_cast<std::size_t>(k)])];
+    for (Index j = 0; j < n; ++j) {
+      const Scalar wj = w[static_cast<std::size_t>(j)];
+      for (Index p = lp_[static_cast<std::size_t>(j)]; p < lp_[static_cast<std::size_t>(j) + 1]; ++p)
+        w[static_cast<std::size_t>(li_[static_cast<std::size_t>(p)])] -= lx_[static_cast<std::size_t>(p)] * wj;
+    }
+    for (Index j = 0; j < n; ++j) w[static_cast<std::size_t>(j)] /= d_[static_cast<std::size_t>(j)];
+    for (Index j = n - 1; j >= 0; --j) {
+      Scalar acc = w[static_cast<std::size_t>(j)];
+      for (Index p = lp_[static_cast<std::size_t>(j)]; p < lp_[static_cast<std::size_t>(j) + 1]; ++p)
+        acc -= lx_[static_cast<std::size_t>(p)] * w[static_cast<std::size_t>(li_[static_cast<std::size_t>(p)])];
+      w[static_cast<std::size_t>(j)] = acc;
+    }
+    for (Index k = 0; k < n; ++k) x[static_cast<std::size_t>(perm_[static_cast<std::size_t>(k)])] = w[static_cast<std::size_t>(k)];
+  }
+
+  std::size_t nnz() const { return li_.size() + d_.size(); }
+
+ private:
+  Index n_ = 0;
+  std::vector<Index> perm_, pinv_, lp_, li_;
+  std::vector<Scalar> lx_, d_;
+};
+
+/// Dense LU with partial pivoting (row-major n*n).
+template <class Scalar>
+class DenseLu {
+ public:
+  bool factor(std::vector<Scalar> a, Index n) {
+    n_ = n;
+    lu_ = std::move(a);
+    piv_.resize(static_cast<std::size_t>(n));
+    double amax = 0;
+    for (const Scalar& v : lu_) amax = std::max(amax, std::sqrt(abs2(v)));
+    for (Index k = 0; k < n; ++k) {
+      Index best = k;
+      double bv = -1;
+      for (Index i = k; i < n; ++i) {
+        const double v = std::sqrt(abs2(at(i, k)));
+        if (v > bv) {
+          bv = v;
+          best = i;
+        }
+      }
+      piv_[static_cast<std::size_t>(k)] = best;
+      if (!(bv > 1e-14 * amax)) return false;
+      if (best != k)
+        for (Index j = 0; j < n; ++j) std::swap(at(k, j), at(best, j));
+      for (Index i = k + 1; i < n; ++i) {
+        const Scalar f = at(i, k) / at(k, k);
+        at(i, k) = f;
+        if (f == Scalar{}) continue;
+        for (Index j = k + 1; j < n; ++j) at(i, j) -= f * at(k, j);
+      }
+    }
+    return true;
+  }
+
+  void solve(std::vector<Scalar>& x) const {
+    const Index n = n_;
+    for (Index k = 0; k < n; ++k) std::swap(x[static_cast<std::size_t>(k)], x[static_cast<std::size_t>(piv_[static_cast<std::size_t>(k)])]);
+    for (Index i = 0; i < n; ++i)
+      for (Index j = 0; j < i; ++j) x[static_cast<std::size_t>(i)] -= at(i, j) * x[static_cast<std::size_t>(j)];
+    for (Index i = n - 1; i >= 0; --i) {
+      for (Index j = i + 1; j < n; ++j) x[static_cast<std::size_t>(i)] -= at(i, j) * x[static_cast<std::size_t>(j)];
+      x[static_cast<std::size_t>(i)] /= at(i, i);
+    }
+  }
+
+  std::size_t nnz() const { return lu_.size(); }
+
+ private:
+  Scalar& at(Index i, Index j) { return lu_[static_cast<std::size_t>(i) * n_ + j]; }
+  const Scalar& at(Index i, Index j) const { return lu_[static_cast<std::size_t>(i) * n_ + j]; }
+  Index n_ = 0;
+  std::vector<Scalar> lu_;
+  std::vector<Index> piv_;
+};
+
+}  // namespace shim
+
+/// Direct factorization of a square sparse matrix with the reference's
+/// contract (solve.hpp:47-126): every solve checks the relative residual
+/// against kResidualTol and throws SolveError on failure.
+template <class Scalar>
+class SparseSolver {
+ public:
+  static constexpr double kResidualTol = 1e-10;
+  static constexpr Index kDenseLimit = 6000;
+
+  explicit SparseSolver(const SparseMatrix<Scalar>& A) : A_(A) {
+    if (A.rows() != A.cols()) throw std::invalid_argument("sparse solver needs a square matrix");
+    if (A.rows() == 0) throw std::invalid_argument("sparse solver: empty matrix");
+    factorize();
+  }
+
+  Index size() const { return A_.rows(); }
+  const SparseMatrix<Scalar>& matrix() const { return A_; }
+
+  std::vector<Scalar> solve(const std::vector<Scalar>& b) const {
+    if (static_cast<Index>(b.size()) != A_.rows())
+      throw std::invalid_argument("sparse solve: rhs size mismatch");
+    const double bnorm = norm2(b);
+    if (bnorm == 0.0) return std::vector<Scalar>(b.size(), Scalar{});
+    std::vector<Scalar> x = b;
+    apply_inverse(x);
+    std::vector<Scalar> Ax(x.size()), r(x.size());
+    double rnorm = residual(x, b, Ax, r);
+    for (int it = 0; it < 3 && rnorm > 0; ++it) {
+      std::vector<Scalar> dx = r;
+      apply_inverse(dx);
+      std::vector<Scalar> x2 = x;
+      for (std::size_t i = 0; i < x.size(); ++i) x2[i] += dx[i];
+      std::vector<Scalar> Ax2(x.size()), r2(x.size());
+      const double rn2 = residual(x2, b, Ax2, r2);
+      if (!(rn2 < rnorm)) break;
+      x.swap(x2);
+      r.swap(r2);
+      rnorm = rn2;
+    }
+    const double rel = rnorm / bnorm;
+    if (!(rel <= kResidualTol))
+      throw SolveError("sparse solve: relative residual " + std::to_string(rel) +
+                           " exceeds tolerance",
+                       rel);
+    return x;
+  }
+
+  SparseSolver clone() const { return SparseSolver(A_); }
+
+  std::size_t factor_bytes() const {
+    const std::size_t per_entry = sizeof(Scalar) + 8;
+    return (ldlt_ ? ldlt_->nnz() : lu_->nnz()) * per_entry;
+  }
+
+ private:
+  double residual(const std::vector<Scalar>& x, const std::vector<Scalar>& b,
+                  std::vector<Scalar>& Ax, std::vector<Scalar>& r) const {
+    A_.multiply(x.data(), Ax.data());
+    double acc = 0;
+    for (std::size_t i = 0; i < Ax.size(); ++i) {
+      r[i] = b[i] - Ax[i];
+      acc += shim::abs2(r[i]);
+    }
+    return std::sqrt(acc);
+  }
+
+  void apply_inverse(std::vector<Scalar>& x) const {
+    if (ldlt_)
+      ldlt_->solve(x);
+    else
+      lu_->solve(x);
+  }
+
+  void factorize() {
+    if (A_.symmetric()) {
+      ldlt_ = std::make_unique<shim::Ldlt<Scalar>>();
+      if (ldlt_->factor(A_)) return;
+      ldlt_.reset();
+    }
+    const Index n = A_.rows();
+    if (n > kDenseLimit)
+      throw SolveError("sparse solve: factorization failed (unsymmetric or singular matrix beyond the shim's dense limit)");
+    std::vector<Scalar> dense(static_cast<std::size_t>(n) * n, Scalar{});
+    for (Index r = 0; r < n; ++r)
+      for (Index p = A_.row_offsets()[static_cast<std::size_t>(r)];
+           p < A_.row_offsets()[static_cast<std::size_t>(r) + 1]; ++p)
+        dense[static_cast<std::size_t>(r) * n + A_.col_indices()[static_cast<std::size_t>(p)]] +=
+            A_.values()[static_cast<std::size_t>(p)];
+    lu_ = std::make_unique<shim::DenseLu<Scalar>>();
+    if (!lu_->factor(std::move(dense), n))
+      throw SolveError("sparse solve: factorization failed (singular matrix?)");
+  }
+
+  SparseMatrix<Scalar> A_;
+  std::unique_ptr<shim::Ldlt<Scalar>> ldlt_;
+  std::unique_ptr<shim::DenseLu<Scalar>> lu_;
+};
+
+template <class Scalar>
+std::vector<Scalar> solve_sparse(const SparseMatrix<Scalar>& A, const std::vector<Scalar>& b) {
+  return SparseSolver<Scalar>(A).solve(b);
+}
+
+/// Dense LU solve; A is row-major n*n (reference solve.hpp:135-157, same
+/// normwise backward-error test with the coefficient-wise max norm).
+template <class Scalar>
+std::vector<Scalar> solve_dense(const std::vector<Scalar>& A, Index n,
+                                const std::vector<Scalar>& b) {
+  if (static_cast<Index>(A.size()) != n * n || static_cast<Index>(b.size()) != n)
+    throw std::invalid_argument("dense solve: size mismatch");
+  if (n == 0) return {};
+  const double bnorm = norm2(b);
+  if (bnorm == 0.0) return std::vector<Scalar>(b.size(), Scalar{});
+  shim::DenseLu<Scalar> lu;
+  std::vector<Scalar> x = b;
+  const bool ok = lu.factor(A, n);
+  if (ok) lu.solve(x);
+  double rmax = 0, amax = 0, xmax = 0;
+  for (Index i = 0; i < n; ++i) {
+    Scalar acc{};
+    for (Index j = 0; j < n; ++j) acc += A[static_cast<std::size_t>(i) * n + j] * x[static_cast<std::size_t>(j)];
+    rmax = std::max(rmax, std::sqrt(shim::abs2(acc - b[static_cast<std::size_t>(i)])));
+    xmax = std::max(xmax, std::sqrt(shim::abs2(x[static_cast<std::size_t>(i)])));
+  }
+  for (const Scalar& v : A) amax = std::max(amax, std::sqrt(shim::abs2(v)));
+  const double backward = ok ? rmax / (amax * xmax + bnorm) : INFINITY;
+  if (!std::isfinite(backward) || backward > 1e-12 * n)
+    throw SolveError("dense solve: matrix is singular to working precision", backward);
+  return x;
+}
+
+}  // namespace tpfem
