@@ -1,0 +1,304 @@
+"""Python mirror of the reference interface over the C ABI (include/tpgpu.h).
+
+Names and semantics follow tpfem (/root/reference/proj/include/tpfem):
+  Problem.static_init          static_init            solvers.hpp:276-296
+  Problem.choose_nu_hat        choose_nu_hat          assembly.hpp:254-303
+  Problem.solve_m1_fixed_point solve_m1_fixed_point   solvers.hpp:301-369
+  Problem.periodic_solve       PeriodicSolver::solve  periodic.hpp:154-198
+  Problem.residual / block_l2  residual, block_l2     periodic.hpp:35-67
+  Problem.apply_k              NonlinearOperator::apply assembly.hpp:126-140
+  stopping_check               stopping_check         solvers.hpp:100-103
+  SolveError                   SolveError             solve.hpp:17-26
+Errors raise like the reference: ValueError for invalid arguments
+(std::invalid_argument), SolveError for numerical failure, and RuntimeError
+for CUDA failures.  There is no CPU fallback: without the built library or a
+GPU every call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass, field
+
+import numpy as np
+
+from .abi import (TP_CONVERGED, TP_EINVAL, TP_ESOLVE, TP_ITERATE_CB, TP_OK, STATUS_NAMES,
+                  TpProblemDesc, TpReport, TpSolverCfg, default_cfg)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libtpgpu.so")
+_lib = None
+
+EXPORTS = [
+    "tp_version", "tp_last_error", "tp_solver_cfg_default", "tp_problem_desc_baseline",
+    "tp_problem_create", "tp_problem_destroy", "tp_problem_sizes", "tp_problem_loads",
+    "tp_problem_mass", "tp_apply_k", "tp_residual", "tp_static_init", "tp_set_state",
+    "tp_get_state", "tp_choose_nu_hat", "tp_set_nu_hat", "tp_periodic_solve", "tp_solve_m1",
+    "tp_m1_begin", "tp_m1_sweep", "tp_problem_stream", "tp_problem_launches",
+]
+
+
+class SolveError(RuntimeError):
+    """Numerical failure with the achieved relative residual (solve.hpp:17-26)."""
+
+    def __init__(self, msg, residual=-1.0):
+        super().__init__(msg)
+        self.residual = residual
+
+
+def lib():
+    """Load libtpgpu.so (raises if it has not been built -- no fallback)."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise FileNotFoundError(f"{LIB_PATH} missing: run `python -m paper_2502_21013_b200.build`")
+        L = C.CDLL(LIB_PATH)
+        dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+        vp = C.c_void_p
+        D, G = C.POINTER(TpProblemDesc), C.POINTER(TpSolverCfg)
+        L.tp_version.restype = C.c_int
+        L.tp_last_error.argtypes = [C.c_char_p, C.c_size_t, dp]
+        L.tp_solver_cfg_default.argtypes = [G]
+        L.tp_solver_cfg_default.restype = None
+        L.tp_problem_desc_baseline.argtypes = [C.c_int32, D]
+        L.tp_problem_create.argtypes = [D, C.c_int32, C.POINTER(vp)]
+        L.tp_problem_destroy.argtypes = [vp]
+        L.tp_problem_destroy.restype = None
+        L.tp_problem_sizes.argtypes = [vp, ip, ip, dp]
+        L.tp_problem_loads.argtypes = [vp, dp]
+        L.tp_problem_mass.argtypes = [vp, dp]
+        L.tp_apply_k.argtypes = [vp, dp, dp, C.c_int32]
+        L.tp_residual.argtypes = [vp, dp, dp, dp]
+        L.tp_static_init.argtypes = [vp, G, dp, ip]
+        L.tp_set_state.argtypes = [vp, dp]
+        L.tp_get_state.argtypes = [vp, dp]
+        L.tp_choose_nu_hat.argtypes = [vp, G, dp, dp]
+        L.tp_set_nu_hat.argtypes = [vp, dp, C.c_double]
+        L.tp_periodic_solve.argtypes = [vp, G, dp, dp]
+        L.tp_solve_m1.argtypes = [vp, G, dp, dp, C.POINTER(TpReport), dp, dp, C.c_int32,
+                                  TP_ITERATE_CB, vp]
+        L.tp_m1_begin.argtypes = [vp, G, dp]
+        L.tp_m1_sweep.argtypes = [vp, dp, ip]
+        L.tp_problem_stream.argtypes = [vp]
+        L.tp_problem_stream.restype = vp
+        L.tp_problem_launches.argtypes = [vp]
+        L.tp_problem_launches.restype = C.c_int64
+        _lib = L
+    return _lib
+
+
+def _check(code):
+    if code == TP_OK:
+        return
+    buf = C.create_string_buffer(2048)
+    res = C.c_double()
+    lib().tp_last_error(buf, 2048, C.byref(res))
+    msg = buf.value.decode()
+    if code == TP_EINVAL:
+        raise ValueError(msg)
+    if code == TP_ESOLVE:
+        raise SolveError(msg, res.value)
+    raise RuntimeError(msg)
+
+
+def _dp(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_double))
+
+
+def _ip(a):
+    return None if a is None else a.ctypes.data_as(C.POINTER(C.c_int32))
+
+
+def baseline_desc(config: int) -> TpProblemDesc:
+    d = TpProblemDesc()
+    _check(lib().tp_problem_desc_baseline(config, C.byref(d)))
+    return d
+
+
+def stopping_check(history, tol) -> bool:
+    """last <= tol * first, boundary inclusive (solvers.hpp:100-103)."""
+    if len(history) == 0:
+        raise ValueError("stopping check: empty history")
+    return history[-1] <= tol * history[0]
+
+
+def block_l2(R) -> float:
+    return float(np.sqrt(np.sum(np.square(R))))
+
+
+@dataclass
+class SolveReport:
+    """SolveReport (solvers.hpp:88-96) plus device counters."""
+    method: str = "m1"
+    iterations: int = 0
+    residual_history: list = field(default_factory=list)
+    contraction_history: list = field(default_factory=list)
+    q_estimate: float = float("nan")
+    wall_time: float = 0.0
+    status: str = "converged"
+    setup_time: float = 0.0
+    sweep_time: float = 0.0
+    inner_iterations: int = 0
+
+
+class Problem:
+    """One BASELINE-style grid problem resident on one CUDA device."""
+
+    def __init__(self, desc: TpProblemDesc, device: int = 0):
+        self._h = C.c_void_p()
+        self.desc = desc
+        _check(lib().tp_problem_create(C.byref(desc), device, C.byref(self._h)))
+        n, N, tau = C.c_int32(), C.c_int32(), C.c_double()
+        _check(lib().tp_problem_sizes(self._h, C.byref(n), C.byref(N), C.byref(tau)))
+        self.n_dof, self.steps, self.tau = n.value, N.value, tau.value
+
+    @classmethod
+    def baseline(cls, config: int, device: int = 0) -> "Problem":
+        return cls(baseline_desc(config), device)
+
+    def close(self):
+        if self._h:
+            lib().tp_problem_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def __enter__(self):
+        return self
+
+    def __exit__(self, *a):
+        self.close()
+
+    @property
+    def shape(self):
+        return (self.steps, self.n_dof)
+
+    def _state(self, U):
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        if U.shape != self.shape:
+            raise ValueError(f"state shape {U.shape} != {self.shape}")
+        return U
+
+    # ---- setup products
+    def loads(self) -> np.ndarray:
+        F = np.zeros(self.shape)
+        _check(lib().tp_problem_loads(self._h, _dp(F)))
+        return F
+
+    def mass(self) -> np.ndarray:
+        m = np.zeros(self.n_dof)
+        _check(lib().tp_problem_mass(self._h, _dp(m)))
+        return m
+
+    # ---- Problem concept
+    def apply_k(self, U) -> np.ndarray:
+        U = np.ascontiguousarray(U, dtype=np.float64)
+        cnt = 1 if U.ndim == 1 else U.shape[0]
+        if U.size != cnt * self.n_dof:
+            raise ValueError("apply_k: size mismatch")
+        out = np.zeros_like(U)
+        _check(lib().tp_apply_k(self._h, _dp(U), _dp(out), cnt))
+        return out
+
+    def residual(self, U):
+        U = self._state(U)
+        R = np.zeros_like(U)
+        nrm = C.c_double()
+        _check(lib().tp_residual(self._h, _dp(U), _dp(R), C.byref(nrm)))
+        return R, nrm.value
+
+    # ---- methods
+    def static_init(self, cfg: TpSolverCfg | None = None, want_state=True):
+        cfg = cfg or default_cfg()
+        U0 = np.zeros(self.shape) if want_state else None
+        counts = np.zeros(self.steps, dtype=np.int32)
+        _check(lib().tp_static_init(self._h, C.byref(cfg), _dp(U0), _ip(counts)))
+        return U0, counts
+
+    def set_state(self, U):
+        U = self._state(U)
+        _check(lib().tp_set_state(self._h, _dp(U)))
+
+    def get_state(self):
+        U = np.zeros(self.shape)
+        _check(lib().tp_get_state(self._h, _dp(U)))
+        return U
+
+    def choose_nu_hat(self, cfg: TpSolverCfg | None = None):
+        cfg = cfg or default_cfg()
+        nu = np.zeros(5)
+        q = C.c_double()
+        _check(lib().tp_choose_nu_hat(self._h, C.byref(cfg), _dp(nu), C.byref(q)))
+        return nu, q.value
+
+    def set_nu_hat(self, nu_hat, q=float("nan")):
+        nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+        if nu.shape != (5,):
+            raise ValueError("nu_hat must have 5 entries")
+        _check(lib().tp_set_nu_hat(self._h, _dp(nu), q))
+
+    def periodic_solve(self, G, cfg: TpSolverCfg | None = None) -> np.ndarray:
+        cfg = cfg or default_cfg()
+        G = self._state(G)
+        U = np.zeros_like(G)
+        _check(lib().tp_periodic_solve(self._h, C.byref(cfg), _dp(G), _dp(U)))
+        return U
+
+    def solve_m1_fixed_point(self, U0=None, cfg: TpSolverCfg | None = None, iterate_log=None,
+                             callback=None):
+        """Returns (U, SolveReport).  iterate_log: list to receive every iterate
+        (solvers.hpp:306); callback(k, U, residual) -> truthy aborts."""
+        cfg = cfg or default_cfg()
+        U0a = None if U0 is None else self._state(U0)
+        cap = cfg.m1_max_outer + 1
+        hist = np.zeros(cap)
+        contr = np.zeros(cap)
+        U = np.zeros(self.shape)
+        rep = TpReport()
+
+        want = iterate_log is not None or callback is not None
+
+        def _cb(k, ptr, res, user):
+            if iterate_log is not None:
+                arr = np.ctypeslib.as_array(ptr, shape=(self.steps * self.n_dof,))
+                iterate_log.append(arr.reshape(self.shape).copy())
+            if callback is not None:
+                arr = np.ctypeslib.as_array(ptr, shape=(self.steps * self.n_dof,))
+                return 1 if callback(k, arr.reshape(self.shape), res) else 0
+            return 0
+
+        cb = TP_ITERATE_CB(_cb) if want else TP_ITERATE_CB()
+        _check(lib().tp_solve_m1(self._h, C.byref(cfg), _dp(U0a), _dp(U), C.byref(rep), _dp(hist),
+                                 _dp(contr), cap, cb, None))
+        k = rep.history_len
+        report = SolveReport(iterations=rep.iterations, residual_history=hist[:k].tolist(),
+                             contraction_history=contr[:max(k - 1, 0)].tolist(),
+                             q_estimate=rep.q_estimate, wall_time=rep.wall_time,
+                             status=STATUS_NAMES[rep.status], setup_time=rep.setup_time,
+                             sweep_time=rep.sweep_time, inner_iterations=rep.inner_iterations)
+        return U, report
+
+    # ---- device-resident sweeps
+    def m1_begin(self, cfg: TpSolverCfg | None = None) -> float:
+        cfg = cfg or default_cfg()
+        r0 = C.c_double()
+        _check(lib().tp_m1_begin(self._h, C.byref(cfg), C.byref(r0)))
+        return r0.value
+
+    def m1_sweep(self):
+        r = C.c_double()
+        it = C.c_int32()
+        _check(lib().tp_m1_sweep(self._h, C.byref(r), C.byref(it)))
+        return r.value, it.value
+
+    @property
+    def stream(self) -> int:
+        return lib().tp_problem_stream(self._h) or 0
+
+    @property
+    def launches(self) -> int:
+        return int(lib().tp_problem_launches(self._h))

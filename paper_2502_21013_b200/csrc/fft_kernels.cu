@@ -1,0 +1,259 @@
+// Time-axis DFTs of the periodic solve (reference: PeriodicSolver::solve,
+// periodic.hpp:159-198, and DftPlan, fft.hpp:19-99).
+//
+// Forward: G (N x n, slice-major, real) -> Ghat (K x n, frequency-major,
+// K = N/2+1 half spectrum; X_k = sum_i g_i e^{-2 pi i ik/N}, unnormalised).
+// Inverse: Uhat (K x n) -> U (N x n), x_i = (1/N) sum_k X_k e^{+2 pi i ik/N}
+// over the Hermitian extension X_{N-k} = conj(X_k) -- the reference's
+// conjugate mirroring (periodic.hpp:285-288) made implicit.
+//
+// A block owns C = 2P consecutive dof columns and all N slices: the slice
+// rows are read/written as C contiguous doubles (coalesced), two real columns
+// are packed into one complex column, and each column is transformed in
+// shared memory by the reference's own iterative radix-2 DIT (bit-reversed
+// load, len = 2..N butterflies, fft.hpp:61-79) or, for non-power-of-two N, the
+// direct O(N^2) transform (fft.hpp:81-93).
+//
+// The inverse also returns the partial sums behind the reference's
+// imaginary-residue guard (periodic.hpp:172-196): sum Re^2 and the imaginary
+// energy (Im X_0^2 + Im X_{N/2}^2)/N that the full complex inverse would
+// produce.
+#include <cmath>
+#include <numbers>
+
+#include "tp_internal.cuh"
+
+namespace tpgpu {
+
+namespace {
+
+__device__ __forceinline__ int bitrev(int i, int bits) { return __brev(i) >> (32 - bits); }
+
+__device__ __forceinline__ cplx cmul(cplx a, cplx b) {
+  return {fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
+}
+
+template <bool INVERSE>
+__device__ void transform(cplx* z, cplx* tmp, const cplx* __restrict__ tw, int N, int P, bool pow2) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (pow2) {
+    for (int len = 2; len <= N; len <<= 1) {
+      const int half = len >> 1, stride = N / len;
+      for (int t = tid; t < P * (N >> 1); t += nt) {
+        const int p = t / (N >> 1), bi = t % (N >> 1);
+        const int base = (bi / half) * len, k = bi % half;
+        cplx w = tw[k * stride];
+        if (INVERSE) w.im = -w.im;
+        cplx* a = z + (size_t)p * N;
+        const cplx odd = cmul(a[base + k + half], w);
+        const cplx even = a[base + k];
+        a[base + k] = even + odd;
+        a[base + k + half] = even - odd;
+      }
+      __syncthreads();
+    }
+  } else {
+    for (int t = tid; t < P * N; t += nt) {
+      const int p = t / N, k = t % N;
+      const cplx* a = z + (size_t)p * N;
+      cplx acc{0, 0};
+      for (int j = 0; j < N; ++j) {
+        cplx w = tw[(int)(((long long)k * j) % N)];
+        if (INVERSE) w.im = -w.im;
+        acc = acc + cmul(a[j], w);
+      }
+      tmp[(size_t)p * N + k] = acc;
+    }
+    __syncthreads();
+    for (int t = tid; t < P * N; t += nt) z[t] = tmp[t];
+    __syncthreads();
+  }
+}
+
+__global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N,
+                               int P, int bits, int pow2, const cplx* __restrict__ tw) {
+  extern __shared__ cplx smem[];
+  cplx* z = smem;
+  cplx* tmp = smem + (size_t)P * N;
+  const int C = 2 * P;
+  const size_t j0 = (size_t)blockIdx.x * C;
+  for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
+    const int i = t / C, cc = t % C;
+    const double v = (j0 + cc < n) ? G[(size_t)i * n + j0 + cc] : 0.0;
+    const int pos = pow2 ? bitrev(i, bits) : i;
+    double* zp = reinterpret_cast<double*>(&z[(size_t)(cc >> 1) * N + pos]);
+    zp[cc & 1] = v;
+  }
+  __syncthreads();
+  transform<false>(z, tmp, tw, N, P, pow2);
+  const int K = N / 2 + 1;
+  for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
+    const int k = t / C, cc = t % C;
+    if (j0 + cc >= n) continue;
+    const cplx* a = z + (size_t)(cc >> 1) * N;
+    const cplx Zk = a[k], Zm = conj(a[(N - k) % N]);
+    cplx X;
+    if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
+    else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
+    Ghat[(size_t)k * n + j0 + cc] = X;
+  }
+}
+
+__global__ void k_rdft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N,
+                               int P, int bits, int pow2, const cplx* __restrict__ tw,
+                               double* __restrict__ part) {
+  extern __shared__ cplx smem[];
+  __shared__ double red[2][32];
+  cplx* z = smem;
+  cplx* tmp = smem + (size_t)P * N;
+  const int C = 2 * P;
+  const size_t j0 = (size_t)blockIdx.x * C;
+  const int half = N / 2;
+  const bool even = (N % 2) == 0;
+  double im2 = 0;
+  for (int t = threadIdx.x; t < N * P; t += blockDim.x) {
+    const int k = t / P, p = t % P;
+    const size_t ja = j0 + 2 * p, jb = ja + 1;
+    cplx Xa{0, 0}, Xb{0, 0};
+    const int kk = (k <= half) ? k : N - k;
+    if (ja < n) Xa = Uhat[(size_t)kk * n + ja];
+    if (jb < n) Xb = Uhat[(size_t)kk * n + jb];
+    cplx Z;
+    if (k == 0 || (even && k == half)) {
+      // self-conjugate bins: the real parts form the Hermitian spectrum; the
+      // imaginary parts are what the full inverse would leave as Im(u)
+      Z = {Xa.re, Xb.re};
+      im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
+    } else if (k <= half) {
+      Z = {Xa.re - Xb.im, Xa.im + Xb.re};
+    } else {
+      Z = {Xa.re + Xb.im, -Xa.im + Xb.re};
+    }
+    z[(size_t)p * N + (pow2 ? bitrev(k, bits) : k)] = Z;
+  }
+  __syncthreads();
+  transform<true>(z, tmp, tw, N, P, pow2);
+  const double invN = 1.0 / N;
+  double re2 = 0;
+  for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
+    const int i = t / C, cc = t % C;
+    if (j0 + cc >= n) continue;
+    const cplx v = z[(size_t)(cc >> 1) * N + i];
+    const double x = ((cc & 1) == 0 ? v.re : v.im) * invN;
+    U[(size_t)i * n + j0 + cc] = x;
+    re2 += x * x;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    re2 += __shfl_down_sync(0xffffffffu, re2, o);
+    im2 += __shfl_down_sync(0xffffffffu, im2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = re2;
+    red[1][threadIdx.x >> 5] = im2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+__global__ void k_reduce_pairs(const double* __restrict__ part, int count, double* __restrict__ out) {
+  __shared__ double sh[2][32];
+  double a = 0, b = 0;
+  for (int k = threadIdx.x; k < count; k += blockDim.x) {
+    a += part[2 * k];
+    b += part[2 * k + 1];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_down_sync(0xffffffffu, a, o);
+    b += __shfl_down_sync(0xffffffffu, b, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    sh[0][threadIdx.x >> 5] = a;
+    sh[1][threadIdx.x >> 5] = b;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0, t = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      s += sh[0][w];
+      t += sh[1][w];
+    }
+    out[0] = s;
+    out[1] = t;
+  }
+}
+
+struct FftPlan {
+  int N = 0, P = 0, bits = 0;
+  bool pow2 = false;
+  size_t smem = 0;
+  DevBuf<cplx> tw;
+};
+
+FftPlan& plan_for(Problem& p) {
+  if (p.fft_plan) return *static_cast<FftPlan*>(p.fft_plan.get());
+  auto pl = std::make_shared<FftPlan>();
+  const int N = p.N;
+  pl->N = N;
+  pl->pow2 = (N & (N - 1)) == 0;
+  while ((1 << pl->bits) < N) ++pl->bits;
+  int P = 8192 / N;
+  P = std::max(1, std::min(16, P));
+  const size_t bufs = pl->pow2 ? 1 : 2;
+  while (P > 1 && (size_t)P * N * sizeof(cplx) * bufs > 160 * 1024) P >>= 1;
+  require((size_t)P * N * sizeof(cplx) * bufs <= 200 * 1024, "dft: N too large for the shared-memory transform");
+  pl->P = P;
+  pl->smem = (size_t)P * N * sizeof(cplx) * bufs;
+  std::vector<cplx> h(N);
+  for (int k = 0; k < N; ++k) {
+    const double a = -2.0 * std::numbers::pi * k / N;  // std::polar(1, a), fft.hpp:27-28
+    h[k] = {std::cos(a), std::sin(a)};
+  }
+  pl->tw.alloc(N);
+  TP_CUDA(cudaMemcpy(pl->tw.get(), h.data(), N * sizeof(cplx), cudaMemcpyHostToDevice));
+  TP_CUDA(cudaFuncSetAttribute(k_rdft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+  TP_CUDA(cudaFuncSetAttribute(k_rdft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+  p.fft_plan = pl;
+  return *pl;
+}
+
+}  // namespace
+
+void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat) {
+  FftPlan& pl = plan_for(p);
+  const size_t n = p.n;
+  const int C = 2 * pl.P;
+  const int blocks = (int)((n + C - 1) / C);
+  k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2,
+                                                     pl.tw.get());
+  TP_LAUNCHED(&p);
+}
+
+void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2) {
+  FftPlan& pl = plan_for(p);
+  const size_t n = p.n;
+  const int C = 2 * pl.P;
+  const int blocks = (int)((n + C - 1) / C);
+  p.part.ensure((size_t)2 * blocks);
+  p.red.ensure(16);
+  k_rdft_inverse<<<blocks, 256, pl.smem, p.stream>>>(Uhat, U, n, pl.N, pl.P, pl.bits, pl.pow2,
+                                                     pl.tw.get(), p.part.get());
+  TP_LAUNCHED(&p);
+  k_reduce_pairs<<<1, 1024, 0, p.stream>>>(p.part.get(), blocks, p.red.get());
+  TP_LAUNCHED(&p);
+  if (re2 || im2) {
+    TP_CUDA(cudaMemcpyAsync(p.h_scalars, p.red.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+    TP_CUDA(cudaStreamSynchronize(p.stream));
+    if (re2) *re2 = p.h_scalars[0];
+    if (im2) *im2 = p.h_scalars[1];
+  }
+}
+
+}  // namespace tpgpu

@@ -1,0 +1,78 @@
+// Batched geometric-multigrid-preconditioned conjugate-gradient solver on the
+// structured P1 grid.  Replaces the reference's per-frequency sparse direct
+// solves (PeriodicSolver::solve_frequency, periodic.hpp:252-289, through
+// SparseSolver, solve.hpp:51-126) and the static-initialisation Newton solves
+// (newton_elliptic, solvers.hpp:156-157).
+//
+//   MODE 0 (frequency): T = cplx, operator lambda_b M + K with shared real
+//     7-point stencils per level, COCG in the bilinear form x^T y -- the
+//     blocks are complex symmetric, not Hermitian (periodic.hpp:124).
+//   MODE 1 (slice): T = double, per-batch real SPD stencils (Jacobians), PCG.
+//
+// Preconditioner: symmetric V(nu,nu) cycle, damped-Jacobi smoothing, P1
+// interpolation on the nested triangulation, Galerkin coarse operators
+// (R = P^T), exact dense solve on the coarsest grid (<= 7x7 nodes).  Batches
+// converge independently (per-batch masks); all reductions are fixed-order.
+#pragma once
+
+#include "tp_internal.cuh"
+
+namespace tpgpu {
+
+struct MGConfig {
+  int pre = 2, post = 2;    // smoothing sweeps
+  double omega = 0.8;       // Jacobi damping
+  double rtol = 1e-13;      // ||r_b|| <= rtol ||b_b||
+  int max_iter = 200;
+};
+
+// Stencils of one level for the whole batch (slice mode) or shared (freq mode).
+struct LevelOp {
+  int m = 0, n = 0;
+  const double* K = nullptr;  // freq: 7n shared ; slice: 7n per batch (stride 7n)
+  const double* M = nullptr;  // freq only
+};
+
+template <int MODE>
+struct BatchSolver {
+  using T = typename std::conditional<MODE == 0, cplx, double>::type;
+  Problem* p = nullptr;
+  MGConfig cfg;
+  int B = 0;                      // batch capacity
+  std::vector<LevelOp> ops;       // per level
+  const T* coarse_inv = nullptr;  // n_L^2 per batch
+  const cplx* lam = nullptr;      // freq mode: per batch symbol (device)
+  const int* ext_mask = nullptr;  // optional: batches with mask 0 are skipped
+  // work
+  std::vector<DevBuf<T>> lb, lz0, lz1;  // per level (level 0: b is external)
+  DevBuf<T> r, p0, p1, q;
+  DevBuf<double> part;
+  DevBuf<T> rho, mu, alpha, beta;
+  DevBuf<double> bn2, rn2;
+  DevBuf<int> active;
+  DevBuf<int> count;
+  int* h_count = nullptr;  // pinned [2]
+  cudaEvent_t ev[2] = {nullptr, nullptr};
+
+  void init(Problem* prob, const std::vector<LevelOp>& levels, int batches, const MGConfig& c);
+  ~BatchSolver();
+  // Solve A_b x_b = b_b for b < nb (<= B).  x holds the initial guess when
+  // `warm`, else is overwritten from zero.  Returns iterations.
+  int solve(const T* b, T* x, int nb, bool warm, SolveStats* st);
+  void set_ops(const std::vector<LevelOp>& levels) { ops = levels; }
+
+ private:
+  void vcycle(int lvl, int nb, T* z_out_level0, bool dot);
+  T* vcycle_level(int lvl, int nb, const T* bl, T* z_first, bool first_done, bool dot);
+};
+
+// Galerkin coarse stencil Ac = P^T Af P for `batches` stencils (stride 7n).
+void launch_rap(Problem& p, const double* Af, int mf, double* Ac, int mc, int batches);
+// Dense inverse of the coarsest operator per batch.
+void launch_coarse_inverse_freq(Problem& p, const double* K, const double* M, int m,
+                                const cplx* lam, cplx* inv, int batches);
+void launch_coarse_inverse_slice(Problem& p, const double* J, int m, double* inv, int batches);
+// Build fine-grid element stencils (K_hat or Jacobians at U, per batch).
+void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches);
+
+}  // namespace tpgpu

@@ -1,0 +1,162 @@
+// Static initialisation on the device: per-slice damped Newton for
+// K(u^s) = f^s from u = 0, batched over a chunk of slices.
+//
+// Reference: static_init (solvers.hpp:276-296) -> newton_elliptic
+// (solvers.hpp:131-182) with mass_scale = 0: the Jacobian J(u)
+// (assembly.hpp:153-177) is assembled as a 7-point stencil per slice, solved
+// by the batched MG-PCG of mg.cu (slice mode; the reference factorises J
+// with SimplicialLDLT), then an Armijo backtracking search per slice
+// (slope, factor, cap from SolverConfig::armijo).  The accept/reject
+// decisions and the stopping tests are made on the host from device-reduced
+// norms, in exactly the reference's order and arithmetic.
+#include <algorithm>
+#include <cmath>
+#include <string>
+
+#include "mg.cuh"
+
+namespace tpgpu {
+
+void newton_residual(Problem& p, const double* Ub, const double* Db, const double* d_alpha, double* Ut,
+                     double* Rt, const int* d_slice_of, const int* d_active, int batches,
+                     double* norms2_host);
+
+namespace {
+__global__ void k_accept(double* __restrict__ Ub, double* __restrict__ Rb, const double* __restrict__ Ut,
+                         const double* __restrict__ Rt, const int* __restrict__ acc, size_t n) {
+  const int b = blockIdx.y;
+  if (!acc[b]) return;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    Ub[b * n + i] = Ut[b * n + i];
+    Rb[b * n + i] = Rt[b * n + i];
+  }
+}
+}  // namespace
+
+void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) {
+  // geometry of the hierarchy
+  std::vector<int> ms;
+  for (int cl = c;; cl /= 2) {
+    ms.push_back(cl - 1);
+    if (cl <= 8) break;
+    require(cl % 2 == 0, "multigrid: cells per side must be 2^k * q with q <= 8");
+  }
+  const int nl = (int)ms.size();
+  const int nL = ms.back() * ms.back();
+  size_t per_slice = 0;  // bytes
+  for (int l = 0; l < nl; ++l) per_slice += (size_t)ms[l] * ms[l] * 8 * (7 + 3);
+  per_slice += (size_t)n * 8 * 9 + (size_t)nL * nL * 8;
+  size_t free_b = 0, total_b = 0;
+  TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  int S = cfg.slice_chunk > 0 ? cfg.slice_chunk : (int)std::min<size_t>(N, (size_t)(0.5 * free_b) / per_slice);
+  S = std::max(1, std::min(S, N));
+
+  DevBuf<double> Ub((size_t)S * n), Rb((size_t)S * n), Db((size_t)S * n), Ut((size_t)S * n), Rt((size_t)S * n);
+  std::vector<DevBuf<double>> J(nl);
+  for (int l = 0; l < nl; ++l) J[l].alloc((size_t)S * 7 * ms[l] * ms[l]);
+  DevBuf<double> inv((size_t)S * nL * nL);
+  DevBuf<int> d_slice(S), d_active(S), d_acc(S);
+  DevBuf<double> d_alpha(S);
+  std::vector<LevelOp> ops(nl);
+  for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], J[l].get(), nullptr};
+  MGConfig mc;
+  mc.rtol = cfg.inner_rtol;
+  mc.max_iter = cfg.inner_max_iter;
+  BatchSolver<1> solver;
+  solver.init(this, ops, S, mc);
+  solver.coarse_inv = inv.get();
+
+  std::vector<int> h_slice(S), h_active(S), h_acc(S), counts(N, 0);
+  std::vector<double> h_alpha(S), rnorm(S), scale(S), nrm2(S);
+  for (int s0 = 0; s0 < N; s0 += S) {
+    const int nb = std::min(S, N - s0);
+    for (int b = 0; b < S; ++b) {
+      h_slice[b] = std::min(s0 + b, N - 1);
+      h_active[b] = b < nb;
+    }
+    TP_CUDA(cudaMemcpyAsync(d_slice.get(), h_slice.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+    TP_CUDA(cudaMemcpyAsync(d_active.get(), h_active.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+    TP_CUDA(cudaMemsetAsync(Ub.get(), 0, Ub.bytes(), stream));
+    // r = f - K(0) = f ; scale = max(||f||, ||r||)  (solvers.hpp:148-152)
+    newton_residual(*this, Ub.get(), nullptr, nullptr, nullptr, Rb.get(), d_slice.get(), d_active.get(), S,
+                    nrm2.data());
+    for (int b = 0; b < nb; ++b) {
+      rnorm[b] = std::sqrt(nrm2[b]);
+      scale[b] = std::max(rnorm[b], rnorm[b]);
+      if (scale[b] == 0 || rnorm[b] <= cfg.static_tol * scale[b]) h_active[b] = 0;
+    }
+    for (int step = 1; step <= cfg.static_max_newton; ++step) {
+      int n_active = 0;
+      for (int b = 0; b < nb; ++b) n_active += h_active[b];
+      if (n_active == 0) break;
+      TP_CUDA(cudaMemcpyAsync(d_active.get(), h_active.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+      // J(u) for the batch, Galerkin hierarchy, coarsest inverses
+      launch_element_stencil(*this, true, Ub.get(), J[0].get(), nb);
+      for (int l = 1; l < nl; ++l) launch_rap(*this, J[l - 1].get(), ms[l - 1], J[l].get(), ms[l], nb);
+      launch_coarse_inverse_slice(*this, J[nl - 1].get(), ms[nl - 1], inv.get(), nb);
+      // delta = J^{-1} r  (masked to the active slices)
+      solver.ext_mask = d_active.get();
+      SolveStats st;
+      solver.solve(Rb.get(), Db.get(), nb, false, &st);
+      solver.ext_mask = nullptr;
+      // Armijo backtracking (solvers.hpp:158-177)
+      for (int b = 0; b < S; ++b) {
+        h_alpha[b] = 1.0;
+        h_acc[b] = 0;
+      }
+      std::vector<int> searching(h_active.begin(), h_active.end());
+      for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
+        int any = 0;
+        for (int b = 0; b < nb; ++b) any += searching[b];
+        if (!any) break;
+        TP_CUDA(cudaMemcpyAsync(d_alpha.get(), h_alpha.data(), S * sizeof(double), cudaMemcpyHostToDevice, stream));
+        TP_CUDA(cudaMemcpyAsync(d_acc.get(), searching.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+        newton_residual(*this, Ub.get(), Db.get(), d_alpha.get(), Ut.get(), Rt.get(), d_slice.get(),
+                        d_acc.get(), S, nrm2.data());
+        std::vector<int> accept(S, 0);
+        for (int b = 0; b < nb; ++b) {
+          if (!searching[b]) continue;
+          const double tnorm = std::sqrt(nrm2[b]);
+          if (tnorm <= (1.0 - cfg.armijo_slope * h_alpha[b]) * rnorm[b]) {
+            accept[b] = 1;
+            rnorm[b] = tnorm;
+            h_acc[b] = 1;
+            searching[b] = 0;
+          } else {
+            h_alpha[b] *= cfg.armijo_backtrack;
+          }
+        }
+        TP_CUDA(cudaMemcpyAsync(d_acc.get(), accept.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+        dim3 g((unsigned)std::min<size_t>((n + 255) / 256, 1024), S);
+        k_accept<<<g, 256, 0, stream>>>(Ub.get(), Rb.get(), Ut.get(), Rt.get(), d_acc.get(), n);
+        TP_LAUNCHED(this);
+        TP_CUDA(cudaStreamSynchronize(stream));
+      }
+      for (int b = 0; b < nb; ++b) {
+        if (!h_active[b]) continue;
+        if (!h_acc[b])
+          throw Error(TP_ESOLVE,
+                      "static init, step " + std::to_string(s0 + b + 1) +
+                          ": newton: line search exhausted at residual " + std::to_string(rnorm[b]),
+                      rnorm[b] / scale[b]);
+        if (rnorm[b] <= cfg.static_tol * scale[b]) {
+          counts[s0 + b] = step;
+          h_active[b] = 0;
+        }
+      }
+    }
+    for (int b = 0; b < nb; ++b)
+      if (h_active[b])
+        throw Error(TP_ESOLVE,
+                    "static init, step " + std::to_string(s0 + b + 1) + ": newton: no convergence within " +
+                        std::to_string(cfg.static_max_newton) + " steps",
+                    rnorm[b] / scale[b]);
+    TP_CUDA(cudaMemcpyAsync(U.get() + (size_t)s0 * n, Ub.get(), (size_t)nb * n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, stream));
+  }
+  TP_CUDA(cudaStreamSynchronize(stream));
+  if (newton_counts)
+    for (int s = 0; s < N; ++s) newton_counts[s] = counts[s];
+}
+
+}  // namespace tpgpu

@@ -1,0 +1,469 @@
+// Nonlinear operator kernels: K(u), the fused residual + fixed-point RHS, and
+// the P1 element-stencil assembly (K_hat and Newton Jacobians).
+//
+// Reference: NonlinearOperator::apply (assembly.hpp:126-140), the M1 RHS
+// lambda (solvers.hpp:326-336), residual (periodic.hpp:35-58),
+// assemble_stiffness_frozen (assembly.hpp:68-84), jacobian (assembly.hpp:153-177).
+//
+// Structured-grid restatement: with h = 1/c, area = h^2/2 and basis gradients
+// c*s_a (s_a in {-1,0,1}^2), the element term nu*area*grad u.grad phi_a is
+// (nu/2) * (dx*sx_a + dy*sy_a) where (dx, dy) are vertex differences -- the
+// h factors cancel.  Each 32x8 node tile stages u (+1 halo) in shared memory,
+// evaluates nu(|grad u|) once per triangle, then every node gathers its six
+// incident triangles (no atomics, deterministic).
+#include "tp_internal.cuh"
+
+namespace tpgpu {
+
+namespace {
+
+constexpr int TX = 32, TY = 8;
+
+__device__ __forceinline__ double nu_of(const MaterialDev& mt, double s2) {
+  if (mt.linear) return mt.nu0;
+  return mt.nu0 + (mt.nu_inf - mt.nu0) * s2 / (s2 + mt.bs2);
+}
+
+// Shared-memory tile: vertices [x0, x0+TX+1] x [y0, y0+TY+1] (vertex coords),
+// cells [x0, x0+TX] x [y0, y0+TY].
+struct Tile {
+  double u[TY + 2][TX + 2];
+  double w[2][TY + 1][TX + 1];   // nu_T / 2 (nonlinear)
+  double wh[2][TY + 1][TX + 1];  // nu_hat_T / 2 (frozen)
+};
+
+// u at vertex (X, Y) of slice `us` (0 on the Dirichlet boundary).
+__device__ __forceinline__ double vertex_u(const double* __restrict__ us, int m, int X, int Y) {
+  return (X >= 1 && X <= m && Y >= 1 && Y <= m) ? us[(size_t)(Y - 1) * m + (X - 1)] : 0.0;
+}
+
+template <bool NEED_NU, bool NEED_HAT>
+__device__ void tile_load(Tile& t, const double* __restrict__ us, const double* __restrict__ ds,
+                          double alpha, int m, int c, int x0, int y0,
+                          const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
+                          const double* __restrict__ nu_hat) {
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  for (int k = tid; k < (TY + 2) * (TX + 2); k += TX * TY) {
+    const int ly = k / (TX + 2), lx = k % (TX + 2);
+    double v = vertex_u(us, m, x0 + lx, y0 + ly);
+    if (ds) v += alpha * vertex_u(ds, m, x0 + lx, y0 + ly);
+    t.u[ly][lx] = v;
+  }
+  __syncthreads();
+  const double c2 = (double)c * (double)c;
+  for (int k = tid; k < (TY + 1) * (TX + 1); k += TX * TY) {
+    const int ly = k / (TX + 1), lx = k % (TX + 1);
+    const int i = x0 + lx, j = y0 + ly;
+    double w1 = 0, w2 = 0, h = 0;
+    if (i < c && j < c) {
+      const MaterialDev mt = mats[cell_mat[(size_t)j * c + i]];
+      if (NEED_NU) {
+        const double u00 = t.u[ly][lx], u10 = t.u[ly][lx + 1];
+        const double u01 = t.u[ly + 1][lx], u11 = t.u[ly + 1][lx + 1];
+        const double ax = u10 - u00, ay = u11 - u10;  // T1
+        const double bx = u11 - u01, by = u01 - u00;  // T2
+        w1 = 0.5 * nu_of(mt, c2 * (ax * ax + ay * ay));
+        w2 = 0.5 * nu_of(mt, c2 * (bx * bx + by * by));
+      }
+      if (NEED_HAT) h = 0.5 * nu_hat[cell_mat[(size_t)j * c + i]];
+    }
+    t.w[0][ly][lx] = w1;
+    t.w[1][ly][lx] = w2;
+    t.wh[0][ly][lx] = h;
+    t.wh[1][ly][lx] = h;
+  }
+  __syncthreads();
+}
+
+// Sum over the six triangles around node (tx, ty) of W_T * (dx*sx + dy*sy).
+template <int WHICH>  // 0: w (nonlinear), 1: wh (frozen)
+__device__ __forceinline__ double gather(const Tile& t, int tx, int ty) {
+  const int lx = tx + 1, ly = ty + 1;  // vertex of the node inside the tile
+  const double uC = t.u[ly][lx], uE = t.u[ly][lx + 1], uW = t.u[ly][lx - 1];
+  const double uN = t.u[ly + 1][lx], uS = t.u[ly - 1][lx];
+  const double uNE = t.u[ly + 1][lx + 1], uSW = t.u[ly - 1][lx - 1];
+  const auto& W = WHICH == 0 ? t.w : t.wh;
+  // cell (X,Y) -> tile cell (lx, ly); (X-1,Y) -> (lx-1, ly); (X-1,Y-1) -> (lx-1, ly-1); (X,Y-1) -> (lx, ly-1)
+  double acc = 0;
+  acc += W[0][ly][lx] * (-(uE - uC));                    // T1(X,Y), local 0
+  acc += W[1][ly][lx] * (-(uN - uC));                    // T2(X,Y), local 0
+  acc += W[0][ly][lx - 1] * ((uC - uW) - (uN - uC));     // T1(X-1,Y), local 1
+  acc += W[0][ly - 1][lx - 1] * (uC - uS);               // T1(X-1,Y-1), local 2
+  acc += W[1][ly - 1][lx - 1] * (uC - uW);               // T2(X-1,Y-1), local 1
+  acc += W[1][ly - 1][lx] * (-(uE - uC) + (uC - uS));    // T2(X,Y-1), local 2
+  (void)uNE;
+  (void)uSW;
+  return acc;
+}
+
+__device__ __forceinline__ double block_sum(double v, double* sh) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  const int tid = threadIdx.y * blockDim.x + threadIdx.x;
+  const int nw = (blockDim.x * blockDim.y) / 32;
+  __syncthreads();
+  if ((tid & 31) == 0) sh[tid >> 5] = v;
+  __syncthreads();
+  double s = 0;
+  if (tid == 0)
+    for (int w = 0; w < nw; ++w) s += sh[w];
+  return s;
+}
+
+// out = K(u) per slice.
+__global__ void __launch_bounds__(TX * TY) k_apply_k(const double* __restrict__ U, double* __restrict__ out,
+                                                     int m, int c, const uint8_t* __restrict__ cell_mat,
+                                                     const MaterialDev* __restrict__ mats) {
+  __shared__ Tile t;
+  const size_t n = (size_t)m * m;
+  const int s = blockIdx.z;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  tile_load<true, false>(t, U + s * n, nullptr, 0.0, m, c, x0, y0, cell_mat, mats, nullptr);
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  if (x < m && y < m) out[s * n + (size_t)y * m + x] = gather<0>(t, threadIdx.x, threadIdx.y);
+}
+
+// One pass over the current iterate U (all N slices):
+//   R^s = F^s - M (u^s - u^{s-1})/tau - K(u^s)           (periodic.hpp:35-58)
+//   G^s = F^s + K_hat u^s - K(u^s)                        (solvers.hpp:326-336)
+// K(u) is evaluated once and shared.  R is never written: per-block partial
+// sums of R^2 go to `part` (block_l2 is reduced deterministically).
+template <bool WANT_G, bool WANT_R>
+__global__ void __launch_bounds__(TX * TY) k_sweep_fused(
+    const double* __restrict__ U, double* __restrict__ G, double* __restrict__ R,
+    double* __restrict__ part, int m, int c, int N, double inv_tau,
+    const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
+    const double* __restrict__ nu_hat, const double* __restrict__ mass,
+    const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
+  __shared__ Tile t;
+  __shared__ double red[32];
+  const size_t n = (size_t)m * m;
+  const int s = blockIdx.z;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  tile_load<true, WANT_G>(t, U + s * n, nullptr, 0.0, m, c, x0, y0, cell_mat, mats, nu_hat);
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  double r2 = 0;
+  if (x < m && y < m) {
+    const size_t i = (size_t)y * m + x;
+    double f = 0;
+    for (int r = 0; r < nsrc; ++r) f += src_time[s * nsrc + r] * src_prof[r * n + i];
+    const double ku = gather<0>(t, threadIdx.x, threadIdx.y);
+    if (WANT_G) {
+      const double khu = gather<1>(t, threadIdx.x, threadIdx.y);
+      G[s * n + i] = f + khu - ku;
+    }
+    const double mi = mass[i];
+    double mdu = 0;
+    if (mi != 0) {
+      const int sp = (s + N - 1) % N;
+      mdu = mi * ((t.u[threadIdx.y + 1][threadIdx.x + 1] - U[sp * n + i]) * inv_tau);
+    }
+    const double res = f - mdu - ku;
+    if (WANT_R && R) R[s * n + i] = res;
+    r2 = res * res;
+  }
+  const double tot = block_sum(r2, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0)
+    part[((size_t)s * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tot;
+}
+
+__global__ void k_reduce_sum(const double* __restrict__ in, int count, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double v = 0;
+  for (int k = threadIdx.x; k < count; k += blockDim.x) v += in[k];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += sh[w];
+    *out = s;
+  }
+}
+
+// Element-stencil assembly: per node, the 7-point row of
+//   sum_T (1/2) s_a^T Q_T s_b,   Q_T = a_T I + b_T g g^T  (g = grad u on T).
+// Frozen stiffness: a_T = nu_hat, b_T = 0.  Newton Jacobian: a_T = nu(s),
+// b_T = nu'(s)/s (0 at s = 0), s = |g|  (assembly.hpp:153-177).
+// Output st[d*n + i] for batch `blockIdx.z` (stride 7n).
+template <bool JAC>
+__global__ void __launch_bounds__(256) k_element_stencil(
+    const double* __restrict__ U, double* __restrict__ st, int m, int c,
+    const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
+    const double* __restrict__ nu_hat) {
+  const size_t n = (size_t)m * m;
+  const int b = blockIdx.z;
+  const size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int x = (int)(i % m), y = (int)(i / m);
+  const int X = x + 1, Y = y + 1;
+  const double* us = JAC ? U + b * n : nullptr;
+  const double cc = (double)c;
+  // triangle list: (cell dx, cell dy, type, local a); sign vectors per type
+  // T1: s0=(-1,0) s1=(1,-1) s2=(0,1);  T2: s0=(0,-1) s1=(1,0) s2=(-1,1)
+  const int tcx[6] = {0, 0, -1, -1, -1, 0};
+  const int tcy[6] = {0, 0, 0, -1, -1, -1};
+  const int ttp[6] = {0, 1, 0, 0, 1, 1};
+  const int tla[6] = {0, 0, 1, 2, 1, 2};
+  double row[7] = {0, 0, 0, 0, 0, 0, 0};
+  for (int k = 0; k < 6; ++k) {
+    const int ci = X + tcx[k], cj = Y + tcy[k];
+    const int tp = ttp[k], a = tla[k];
+    const MaterialDev mt = mats[cell_mat[(size_t)cj * c + ci]];
+    // vertices of the triangle (vertex coords) and their sign vectors
+    int vx[3], vy[3];
+    vx[0] = ci; vy[0] = cj;
+    if (tp == 0) { vx[1] = ci + 1; vy[1] = cj; vx[2] = ci + 1; vy[2] = cj + 1; }
+    else         { vx[1] = ci + 1; vy[1] = cj + 1; vx[2] = ci; vy[2] = cj + 1; }
+    const int sxa[2][3] = {{-1, 1, 0}, {0, 1, -1}};
+    const int sya[2][3] = {{0, -1, 1}, {-1, 0, 1}};
+    double qa, qb = 0, gx = 0, gy = 0;
+    if (JAC) {
+      const double u0 = vertex_u(us, m, vx[0], vy[0]);
+      const double u1 = vertex_u(us, m, vx[1], vy[1]);
+      const double u2 = vertex_u(us, m, vx[2], vy[2]);
+      gx = cc * (sxa[tp][0] * u0 + sxa[tp][1] * u1 + sxa[tp][2] * u2);
+      gy = cc * (sya[tp][0] * u0 + sya[tp][1] * u1 + sya[tp][2] * u2);
+      const double s2 = gx * gx + gy * gy;
+      qa = nu_of(mt, s2);
+      if (!mt.linear && s2 > 0) {
+        // nu'(s)/s = 2 (nu_inf - nu0) Bs^2 / (s^2 + Bs^2)^2
+        const double den = s2 + mt.bs2;
+        qb = 2.0 * (mt.nu_inf - mt.nu0) * mt.bs2 / (den * den);
+      }
+    } else {
+      qa = nu_hat[cell_mat[(size_t)cj * c + ci]];
+    }
+    const double sax = sxa[tp][a], say = sya[tp][a];
+    // area * grad phi_a^T Q grad phi_b with grad phi = c s, area = 1/(2c^2):
+    //   (1/2) [qa (s_a.s_b) + qb (g.s_a)(g.s_b)],  g the true gradient.
+    const double gsa = gx * sax + gy * say;
+    for (int bb = 0; bb < 3; ++bb) {
+      const double sbx = sxa[tp][bb], sby = sya[tp][bb];
+      double v = qa * (sax * sbx + say * sby);
+      if (JAC) v += qb * gsa * (gx * sbx + gy * sby);
+      v *= 0.5;
+      const int ddx = vx[bb] - X, ddy = vy[bb] - Y;
+      int d;
+      if (ddx == 0 && ddy == 0) d = SC;
+      else if (ddx == -1 && ddy == 0) d = SW_;
+      else if (ddx == 1 && ddy == 0) d = SE_;
+      else if (ddx == 0 && ddy == -1) d = SS_;
+      else if (ddx == 0 && ddy == 1) d = SN_;
+      else if (ddx == -1 && ddy == -1) d = SSW;
+      else d = SNE;
+      row[d] += v;
+    }
+  }
+  // drop couplings to Dirichlet vertices
+  for (int d = 1; d < 7; ++d) {
+    const int nx = x + dir_dx(d), ny = y + dir_dy(d);
+    if (nx < 0 || nx >= m || ny < 0 || ny >= m) row[d] = 0;
+  }
+  double* o = st + (size_t)b * 7 * n;
+  for (int d = 0; d < 7; ++d) o[d * n + i] = row[d];
+}
+
+}  // namespace
+
+double reduce_sum(Problem& p, const double* partials, int count) {
+  k_reduce_sum<<<1, 1024, 0, p.stream>>>(partials, count, p.red.get());
+  TP_LAUNCHED(&p);
+  TP_CUDA(cudaMemcpyAsync(p.h_scalars, p.red.get(), sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+  TP_CUDA(cudaStreamSynchronize(p.stream));
+  return p.h_scalars[0];
+}
+
+void Problem::apply_k_dev(const double* u, double* out, int count) {
+  dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, count);
+  k_apply_k<<<grid, dim3(TX, TY), 0, stream>>>(u, out, m, c, d_cell_mat.get(), d_mat.get());
+  TP_LAUNCHED(this);
+}
+
+static size_t sweep_partials(int m, int N) {
+  return (size_t)((m + TX - 1) / TX) * ((m + TY - 1) / TY) * N;
+}
+
+double Problem::residual_and_rhs(bool want_rhs) {
+  dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, N);
+  const size_t np = sweep_partials(m, N);
+  part.ensure(np);
+  const int nsrc = (int)src_mats.size();
+  if (want_rhs) {
+    require(nu_hat_set, "fixed-point sweep: nu_hat not installed");
+    k_sweep_fused<true, false><<<grid, dim3(TX, TY), 0, stream>>>(
+        U.get(), G.get(), nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+  } else {
+    k_sweep_fused<false, false><<<grid, dim3(TX, TY), 0, stream>>>(
+        U.get(), nullptr, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+  }
+  TP_LAUNCHED(this);
+  return std::sqrt(reduce_sum(*this, part.get(), (int)np));
+}
+
+void Problem::residual_dev(const double* u, double* r, int count_slices) {
+  require(count_slices == N, "residual: needs all slices");
+  dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, N);
+  part.ensure(sweep_partials(m, N));
+  k_sweep_fused<false, true><<<grid, dim3(TX, TY), 0, stream>>>(
+      u, nullptr, r, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(), d_nu_hat.get(),
+      d_mass.get(), d_src_prof.get(), d_src_time.get(), (int)src_mats.size());
+  TP_LAUNCHED(this);
+}
+
+void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches) {
+  dim3 grid((p.n + 255) / 256, 1, batches);
+  if (jacobian)
+    k_element_stencil<true><<<grid, 256, 0, p.stream>>>(U, st, p.m, p.c, p.d_cell_mat.get(),
+                                                         p.d_mat.get(), nullptr);
+  else
+    k_element_stencil<false><<<grid, 256, 0, p.stream>>>(nullptr, st, p.m, p.c, p.d_cell_mat.get(),
+                                                          p.d_mat.get(), p.d_nu_hat.get());
+  TP_LAUNCHED(&p);
+}
+
+// ---- Newton helpers (static_init) -------------------------------------
+
+namespace {
+
+// r_s = f_s - K(u_s + alpha_s d_s) for the batch slices listed in `slices`;
+// writes trial u and r, and per-block partial ||r||^2.
+__global__ void __launch_bounds__(TX * TY) k_newton_residual(
+    const double* __restrict__ Ub, const double* __restrict__ Db, const double* __restrict__ alpha,
+    double* __restrict__ Ut, double* __restrict__ Rt, double* __restrict__ part,
+    const int* __restrict__ slice_of, const int* __restrict__ active, int m, int c,
+    const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
+    const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
+  __shared__ Tile t;
+  __shared__ double red[32];
+  const size_t n = (size_t)m * m;
+  const int b = blockIdx.z;
+  const size_t pidx = ((size_t)b * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x;
+  if (!active[b]) {
+    if (threadIdx.x == 0 && threadIdx.y == 0) part[pidx] = 0;
+    return;
+  }
+  const int s = slice_of[b];
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const double a = alpha ? alpha[b] : 0.0;
+  tile_load<true, false>(t, Ub + b * n, Db ? Db + b * n : nullptr, a, m, c, x0, y0, cell_mat, mats,
+                         nullptr);
+  const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
+  double r2 = 0;
+  if (x < m && y < m) {
+    const size_t i = (size_t)y * m + x;
+    double f = 0;
+    for (int r = 0; r < nsrc; ++r) f += src_time[s * nsrc + r] * src_prof[r * n + i];
+    const double res = f - gather<0>(t, threadIdx.x, threadIdx.y);
+    Rt[b * n + i] = res;
+    if (Ut) Ut[b * n + i] = t.u[threadIdx.y + 1][threadIdx.x + 1];
+    r2 = res * res;
+  }
+  const double tot = block_sum(r2, red);
+  if (threadIdx.x == 0 && threadIdx.y == 0) part[pidx] = tot;
+}
+
+// per-batch sums of partials (fixed order)
+__global__ void k_reduce_batches(const double* __restrict__ part, int per, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int b = blockIdx.x;
+  double v = 0;
+  for (int k = threadIdx.x; k < per; k += blockDim.x) v += part[(size_t)b * per + k];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += sh[w];
+    out[b] = s;
+  }
+}
+
+}  // namespace
+
+// Evaluate r = f - K(u + alpha d) for a batch; returns per-batch ||r||^2 into
+// host `norms2` (synchronising).
+void newton_residual(Problem& p, const double* Ub, const double* Db, const double* d_alpha,
+                     double* Ut, double* Rt, const int* d_slice_of, const int* d_active, int batches,
+                     double* norms2_host) {
+  dim3 grid((p.m + TX - 1) / TX, (p.m + TY - 1) / TY, batches);
+  const int per = grid.x * grid.y;
+  p.part.ensure((size_t)per * batches);
+  p.red.ensure(batches + 16);
+  k_newton_residual<<<grid, dim3(TX, TY), 0, p.stream>>>(
+      Ub, Db, d_alpha, Ut, Rt, p.part.get(), d_slice_of, d_active, p.m, p.c, p.d_cell_mat.get(),
+      p.d_mat.get(), p.d_src_prof.get(), p.d_src_time.get(), (int)p.src_mats.size());
+  TP_LAUNCHED(&p);
+  k_reduce_batches<<<batches, 256, 0, p.stream>>>(p.part.get(), per, p.red.get());
+  TP_LAUNCHED(&p);
+  TP_CUDA(cudaMemcpyAsync(norms2_host, p.red.get(), sizeof(double) * batches, cudaMemcpyDeviceToHost,
+                          p.stream));
+  TP_CUDA(cudaStreamSynchronize(p.stream));
+}
+
+// per-material min/max of |grad u| over all slices of the device state
+namespace {
+__global__ void k_field_ranges(const double* __restrict__ U, int m, int c, int N,
+                               const uint8_t* __restrict__ cell_mat, double* __restrict__ lo,
+                               double* __restrict__ hi) {
+  // one thread per cell per slice-group; partial min/max per block per material
+  __shared__ double slo[TP_MAX_MATERIALS][256], shi[TP_MAX_MATERIALS][256];
+  const size_t cells = (size_t)c * c;
+  const size_t n = (size_t)m * m;
+  double mlo[TP_MAX_MATERIALS], mhi[TP_MAX_MATERIALS];
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r) { mlo[r] = INFINITY; mhi[r] = -1.0; }
+  const double cc = (double)c;
+  for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < cells * N;
+       k += (size_t)gridDim.x * blockDim.x) {
+    const int s = (int)(k / cells);
+    const size_t cell = k % cells;
+    const int i = (int)(cell % c), j = (int)(cell / c);
+    const double* us = U + s * n;
+    const double u00 = vertex_u(us, m, i, j), u10 = vertex_u(us, m, i + 1, j);
+    const double u01 = vertex_u(us, m, i, j + 1), u11 = vertex_u(us, m, i + 1, j + 1);
+    const double s1 = hypot(cc * (u10 - u00), cc * (u11 - u10));
+    const double s2 = hypot(cc * (u11 - u01), cc * (u01 - u00));
+    const int r = cell_mat[cell];
+    mlo[r] = fmin(mlo[r], fmin(s1, s2));
+    mhi[r] = fmax(mhi[r], fmax(s1, s2));
+  }
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r) { slo[r][threadIdx.x] = mlo[r]; shi[r][threadIdx.x] = mhi[r]; }
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w)
+      for (int r = 0; r < TP_MAX_MATERIALS; ++r) {
+        slo[r][threadIdx.x] = fmin(slo[r][threadIdx.x], slo[r][threadIdx.x + w]);
+        shi[r][threadIdx.x] = fmax(shi[r][threadIdx.x], shi[r][threadIdx.x + w]);
+      }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0)
+    for (int r = 0; r < TP_MAX_MATERIALS; ++r) {
+      lo[blockIdx.x * TP_MAX_MATERIALS + r] = slo[r][0];
+      hi[blockIdx.x * TP_MAX_MATERIALS + r] = shi[r][0];
+    }
+}
+}  // namespace
+
+void Problem::field_ranges(double* lo, double* hi, int* any) {
+  const int blocks = 2 * num_sms;
+  part.ensure((size_t)2 * blocks * TP_MAX_MATERIALS);
+  k_field_ranges<<<blocks, 256, 0, stream>>>(U.get(), m, c, N, d_cell_mat.get(), part.get(),
+                                            part.get() + blocks * TP_MAX_MATERIALS);
+  TP_LAUNCHED(this);
+  std::vector<double> h(2 * blocks * TP_MAX_MATERIALS);
+  TP_CUDA(cudaMemcpyAsync(h.data(), part.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r) {
+    lo[r] = INFINITY;
+    hi[r] = -1.0;
+    for (int b = 0; b < blocks; ++b) {
+      lo[r] = std::fmin(lo[r], h[b * TP_MAX_MATERIALS + r]);
+      hi[r] = std::fmax(hi[r], h[(blocks + b) * TP_MAX_MATERIALS + r]);
+    }
+    any[r] = hi[r] >= 0.0;
+  }
+}
+
+}  // namespace tpgpu

@@ -1,0 +1,711 @@
+// Host side of libtpgpu.so: problem setup (mesh, materials, sources), the
+// frequency-solver hierarchy, the M1 fixed-point driver and the C ABI.
+//
+// Host code mirrors the reference's control flow line by line where it is
+// control flow (solve_m1_fixed_point, solvers.hpp:301-369; stopping_check,
+// solvers.hpp:100-103; choose_nu_hat, assembly.hpp:254-303); all per-dof
+// arithmetic runs in the CUDA kernels of op_kernels.cu / fft_kernels.cu /
+// mg.cu / newton.cu.  There is no CPU fallback: a missing device is TP_ECUDA.
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstring>
+#include <limits>
+#include <numbers>
+#include <string>
+
+#include "../../include/tpgpu_baseline.h"
+#include "mg.cuh"
+
+namespace tpgpu {
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line) {
+  throw Error(TP_ECUDA, std::string("CUDA error ") + cudaGetErrorName(e) + " (" +
+                            cudaGetErrorString(e) + ") at " + file + ":" + std::to_string(line) +
+                            ": " + what);
+}
+
+namespace {
+
+uint64_t splitmix64(uint64_t& state) {
+  uint64_t z = (state += 0x9e3779b97f4a7c15ULL);
+  z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  z = (z ^ (z >> 27)) * 0x94d049bb133111ebULL;
+  return z ^ (z >> 31);
+}
+
+void validate_desc(const tp_problem_desc& d) {
+  require(d.cells >= 2, "problem: need at least 2 cells per side");
+  require(d.steps >= 1, "problem: need at least one time step");
+  require(d.period > 0, "problem: period must be positive");
+  require(d.n_materials >= 1 && d.n_materials <= TP_MAX_MATERIALS, "problem: material count out of range");
+  require(d.n_rects >= 0 && d.n_rects <= TP_MAX_RECTS, "problem: rectangle count out of range");
+  for (int r = 0; r < d.n_rects; ++r)
+    require(d.rect[r].material >= 0 && d.rect[r].material < d.n_materials,
+            "problem: rectangle material out of range");
+  for (int k = 0; k < d.n_materials; ++k) {
+    const tp_material& mt = d.material[k];
+    require(mt.sigma >= 0, "problem: sigma must be >= 0");
+    require(mt.nu0 > 0 && mt.nu_inf > 0, "problem: nu must be > 0");
+    require(mt.nu0 == mt.nu_inf || mt.bs > 0, "problem: Bs must be > 0");
+    require(mt.n_harmonics >= 0 && mt.n_harmonics <= TP_MAX_HARMONICS, "problem: harmonic count out of range");
+  }
+}
+
+void validate_cfg(const tp_solver_cfg& c) {
+  // validate(), solvers.hpp:71-86 (fields on this path)
+  require(c.tol > 0 && c.tol < 1, "solver config: tol must lie in (0,1)");
+  require(c.armijo_slope > 0 && c.armijo_slope < 1, "solver config: armijo slope must lie in (0,1)");
+  require(c.armijo_backtrack > 0 && c.armijo_backtrack < 1,
+          "solver config: armijo backtracking factor must lie in (0,1)");
+  require(c.armijo_max_halvings >= 0, "solver config: negative armijo halving cap");
+  require(c.m1_max_outer >= 1 && c.static_max_newton >= 1, "solver config: iteration caps must be positive");
+  require(c.static_tol > 0 && c.static_tol < 1, "solver config: inner tolerances must lie in (0,1)");
+  require(c.inner_rtol > 0 && c.inner_rtol < 1e-6, "solver config: inner_rtol must lie in (0,1e-6)");
+  require(c.inner_max_iter >= 1, "solver config: inner_max_iter must be positive");
+}
+
+// nu(s) and nu'(s) on the host, for the flux-bound sampling (materials.hpp:42-57 law swapped).
+double h_nu(const tp_material& m, double s) {
+  if (m.nu0 == m.nu_inf) return m.nu0;
+  const double s2 = s * s;
+  return m.nu0 + (m.nu_inf - m.nu0) * s2 / (s2 + m.bs * m.bs);
+}
+double h_nu_prime(const tp_material& m, double s) {
+  if (m.nu0 == m.nu_inf) return 0;
+  const double den = s * s + m.bs * m.bs;
+  return 2.0 * (m.nu_inf - m.nu0) * s * m.bs * m.bs / (den * den);
+}
+// flux_jacobian_bounds, materials.hpp:112-128
+void flux_bounds(const tp_material& m, double lo, double hi, int samples, double& lam, double& Lam) {
+  require(lo >= 0 && hi >= lo, "flux bounds: need 0 <= s_lo <= s_hi");
+  require(samples >= 2, "flux bounds: need at least 2 samples");
+  lam = std::numeric_limits<double>::infinity();
+  Lam = 0;
+  for (int j = 0; j < samples; ++j) {
+    const double s = lo + (hi - lo) * j / (samples - 1);
+    const double nu = h_nu(m, s);
+    const double gp = nu + h_nu_prime(m, s) * s;
+    lam = std::min({lam, nu, gp});
+    Lam = std::max({Lam, nu, gp});
+  }
+}
+
+}  // namespace
+
+struct Problem::FreqWork {
+  DevBuf<cplx> lam;       // K symbols
+  DevBuf<cplx> inv;       // K * nL^2 coarsest inverses
+  BatchSolver<0> solver;
+  int chunk = 0;
+  int nL = 0;
+};
+
+Problem::Problem(const tp_problem_desc& d, int dev) : desc(d), device(dev) {
+  validate_desc(d);
+  int count = 0;
+  TP_CUDA(cudaGetDeviceCount(&count));
+  require(dev >= 0 && dev < count, "problem: CUDA device index out of range");
+  TP_CUDA(cudaSetDevice(dev));
+  TP_CUDA(cudaDeviceGetAttribute(&num_sms, cudaDevAttrMultiProcessorCount, dev));
+  TP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  TP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_scalars), 4096 * sizeof(double)));
+  c = d.cells;
+  m = c - 1;
+  n = m * m;
+  N = d.steps;
+  K = N / 2 + 1;
+  T = d.period;
+  tau = T / N;
+  // cell materials: painter's order by cell centroid (mesh.hpp:164-177)
+  cell_mat.assign((size_t)c * c, 0);
+  for (int j = 0; j < c; ++j)
+    for (int i = 0; i < c; ++i) {
+      const double cx = (2.0 * i + 1.0) / (2.0 * c), cy = (2.0 * j + 1.0) / (2.0 * c);
+      int mat = 0;
+      for (int r = 0; r < d.n_rects; ++r) {
+        const tp_rect& R = d.rect[r];
+        if (cx >= R.x0 && cx <= R.x1 && cy >= R.y0 && cy <= R.y1) mat = R.material;
+      }
+      cell_mat[(size_t)j * c + i] = (uint8_t)mat;
+    }
+  // per-triangle sigma with the seeded bilinear noise
+  std::vector<double> lattice;
+  const int L = d.noise_lattice >= 2 ? d.noise_lattice : 8;
+  {
+    uint64_t st = d.noise_seed;
+    lattice.resize((size_t)L * L);
+    const double lo = d.noise_lattice >= 2 ? d.noise_lo : 0.5, hi = d.noise_lattice >= 2 ? d.noise_hi : 1.5;
+    for (int b = 0; b < L; ++b)
+      for (int a = 0; a < L; ++a) {
+        const double u = (double)(splitmix64(st) >> 11) * 0x1.0p-53;
+        lattice[(size_t)b * L + a] = lo + (hi - lo) * u;
+      }
+  }
+  auto noise = [&](double x, double y) {
+    const double lo = d.noise_lattice >= 2 ? d.noise_lo : 0.5, hi = d.noise_lattice >= 2 ? d.noise_hi : 1.5;
+    auto coord = [L](double p, double a, double b, int& i0, double& f) {
+      double s = (p - a) / (b - a) * (L - 1);
+      s = std::min(std::max(s, 0.0), (double)(L - 1));
+      i0 = std::min((int)std::floor(s), L - 2);
+      f = s - i0;
+    };
+    int a0, b0;
+    double fx, fy;
+    coord(x, d.noise_box[0], d.noise_box[2], a0, fx);
+    coord(y, d.noise_box[1], d.noise_box[3], b0, fy);
+    auto v = [&](int a, int b) { return lattice[(size_t)b * L + a]; };
+    const double val = (1 - fx) * (1 - fy) * v(a0, b0) + fx * (1 - fy) * v(a0 + 1, b0) +
+                       (1 - fx) * fy * v(a0, b0 + 1) + fx * fy * v(a0 + 1, b0 + 1);
+    return std::min(std::max(val, lo), hi);
+  };
+  tri_sigma.assign((size_t)2 * c * c, 0.0);
+  for (int j = 0; j < c; ++j)
+    for (int i = 0; i < c; ++i) {
+      const tp_material& mt = d.material[cell_mat[(size_t)j * c + i]];
+      for (int t = 0; t < 2; ++t) {
+        double s = mt.sigma;
+        if (mt.sigma_noise) {
+          const bool lower = t == 0;
+          const double x = (3.0 * i + (lower ? 2.0 : 1.0)) / (3.0 * c);
+          const double y = (3.0 * j + (lower ? 1.0 : 2.0)) / (3.0 * c);
+          s = mt.sigma * noise(x, y);
+        }
+        tri_sigma[(size_t)2 * (j * c + i) + t] = s;
+      }
+    }
+  // lumped mass and source profiles: sum over the six triangles of each node
+  const double area = 0.5 / ((double)c * c);
+  for (int r = 0; r < d.n_materials; ++r)
+    if (d.material[r].n_harmonics > 0) src_mats.push_back(r);
+  const int nsrc = (int)src_mats.size();
+  mass.assign(n, 0.0);
+  src_prof.assign((size_t)nsrc * n, 0.0);
+  const int tcx[6] = {0, 0, -1, -1, -1, 0}, tcy[6] = {0, 0, 0, -1, -1, -1}, ttp[6] = {0, 1, 0, 0, 1, 1};
+  for (int y = 0; y < m; ++y)
+    for (int x = 0; x < m; ++x) {
+      const size_t i = (size_t)y * m + x;
+      for (int k = 0; k < 6; ++k) {
+        const int ci = x + 1 + tcx[k], cj = y + 1 + tcy[k];
+        const size_t cell = (size_t)cj * c + ci;
+        mass[i] += tri_sigma[2 * cell + ttp[k]] * area / 3.0;
+        for (int r = 0; r < nsrc; ++r)
+          if (cell_mat[cell] == src_mats[r]) src_prof[(size_t)r * n + i] += area / 3.0;
+      }
+    }
+  src_time.assign((size_t)N * std::max(nsrc, 1), 0.0);
+  for (int s = 0; s < N; ++s) {
+    const double t = (s + 1) * T / N;  // assembly.hpp:95
+    for (int r = 0; r < nsrc; ++r) {
+      const tp_material& mt = d.material[src_mats[r]];
+      double j = 0;
+      for (int h = 0; h < mt.n_harmonics; ++h)
+        j += mt.amp[h] * std::sin(2.0 * std::numbers::pi * mt.harmonic[h] * t / T + mt.phase[h]);
+      src_time[(size_t)s * nsrc + r] = j;
+    }
+  }
+  nu_hat.assign(TP_MAX_MATERIALS, 1.0);
+  upload_constants();
+  U.alloc((size_t)N * n);
+  G.alloc((size_t)N * n);
+  Ghat.alloc((size_t)K * n);
+  Uhat.alloc((size_t)K * n);
+  red.alloc(4096);
+  TP_CUDA(cudaMemsetAsync(U.get(), 0, U.bytes(), stream));
+}
+
+Problem::~Problem() {
+  fw.reset();
+  if (h_scalars) cudaFreeHost(h_scalars);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void Problem::upload_constants() {
+  d_cell_mat.alloc(cell_mat.size());
+  TP_CUDA(cudaMemcpy(d_cell_mat.get(), cell_mat.data(), cell_mat.size(), cudaMemcpyHostToDevice));
+  d_mass.alloc(n);
+  TP_CUDA(cudaMemcpy(d_mass.get(), mass.data(), n * sizeof(double), cudaMemcpyHostToDevice));
+  d_src_prof.alloc(std::max<size_t>(src_prof.size(), 1));
+  if (!src_prof.empty())
+    TP_CUDA(cudaMemcpy(d_src_prof.get(), src_prof.data(), src_prof.size() * sizeof(double), cudaMemcpyHostToDevice));
+  d_src_time.alloc(src_time.size());
+  TP_CUDA(cudaMemcpy(d_src_time.get(), src_time.data(), src_time.size() * sizeof(double), cudaMemcpyHostToDevice));
+  std::vector<MaterialDev> mt(TP_MAX_MATERIALS);
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r) {
+    if (r < desc.n_materials) {
+      const tp_material& x = desc.material[r];
+      mt[r] = {x.nu0, x.nu_inf, x.bs * x.bs, x.nu0 == x.nu_inf ? 1 : 0};
+    } else {
+      mt[r] = {1.0, 1.0, 1.0, 1};
+    }
+  }
+  d_mat.alloc(TP_MAX_MATERIALS);
+  TP_CUDA(cudaMemcpy(d_mat.get(), mt.data(), mt.size() * sizeof(MaterialDev), cudaMemcpyHostToDevice));
+  d_nu_hat.alloc(TP_MAX_MATERIALS);
+  TP_CUDA(cudaMemcpy(d_nu_hat.get(), nu_hat.data(), TP_MAX_MATERIALS * sizeof(double), cudaMemcpyHostToDevice));
+}
+
+void Problem::install_nu_hat(const double* nu, double q) {
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r)
+    require(nu[r] > 0, "frozen stiffness: nu_hat must be positive");  // assembly.hpp:70-71
+  nu_hat.assign(nu, nu + TP_MAX_MATERIALS);
+  q_estimate = q;
+  TP_CUDA(cudaMemcpyAsync(d_nu_hat.get(), nu_hat.data(), TP_MAX_MATERIALS * sizeof(double),
+                          cudaMemcpyHostToDevice, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  nu_hat_set = true;
+  freq_ready = false;
+  uhat_valid = false;
+}
+
+// PeriodicSolver ctor (periodic.hpp:128-139): symbols + multigrid hierarchy
+// for (lambda_k M + K_hat), all frequencies sharing the real stencils.
+void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
+  require(nu_hat_set, "periodic solver: nu_hat not installed");
+  if (freq_ready && fw && (cfg.freq_chunk <= 0 || cfg.freq_chunk == fw->chunk)) {
+    fw->solver.cfg.rtol = cfg.inner_rtol;
+    fw->solver.cfg.max_iter = cfg.inner_max_iter;
+    return;
+  }
+  fw.reset();
+  levels.clear();
+  int cl = c;
+  while (true) {
+    Level L;
+    L.m = cl - 1;
+    L.n = L.m * L.m;
+    levels.push_back(std::move(L));
+    if (cl <= 8) break;
+    require(cl % 2 == 0, "multigrid: cells per side must be 2^k * q with q <= 8");
+    cl /= 2;
+  }
+  const int nl = (int)levels.size();
+  // fine level: K_hat element stencil, lumped M on the diagonal
+  levels[0].K.alloc((size_t)7 * n);
+  levels[0].M.alloc((size_t)7 * n);
+  launch_element_stencil(*this, false, nullptr, levels[0].K.get(), 1);
+  TP_CUDA(cudaMemsetAsync(levels[0].M.get(), 0, levels[0].M.bytes(), stream));
+  TP_CUDA(cudaMemcpyAsync(levels[0].M.get(), d_mass.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  for (int l = 1; l < nl; ++l) {
+    levels[l].K.alloc((size_t)7 * levels[l].n);
+    levels[l].M.alloc((size_t)7 * levels[l].n);
+    launch_rap(*this, levels[l - 1].K.get(), levels[l - 1].m, levels[l].K.get(), levels[l].m, 1);
+    launch_rap(*this, levels[l - 1].M.get(), levels[l - 1].m, levels[l].M.get(), levels[l].m, 1);
+  }
+  fw = std::make_unique<FreqWork>();
+  // symbols lambda_k (periodic.hpp:146-152)
+  std::vector<cplx> lam(K);
+  for (int k = 0; k < K; ++k) {
+    if (k == 0) lam[k] = {0.0, 0.0};
+    else if (2 * k == N) lam[k] = {2.0 / tau, 0.0};
+    else {
+      const double a = -2.0 * std::numbers::pi * k / N;
+      const double rr = std::cos(a), ri = std::sin(a);  // std::polar(1.0, a)
+      lam[k] = {(1.0 - rr) / tau, (0.0 - ri) / tau};
+    }
+  }
+  fw->lam.alloc(K);
+  TP_CUDA(cudaMemcpy(fw->lam.get(), lam.data(), K * sizeof(cplx), cudaMemcpyHostToDevice));
+  const Level& LC = levels.back();
+  fw->nL = LC.n;
+  fw->inv.alloc((size_t)K * LC.n * LC.n);
+  launch_coarse_inverse_freq(*this, LC.K.get(), LC.M.get(), LC.m, fw->lam.get(), fw->inv.get(), K);
+  // chunk: work ~ 7 complex vectors per frequency on the fine level (+1/3 coarse)
+  size_t free_b = 0, total_b = 0;
+  TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double per = 16.0 * 8.5 * n;
+  int chunk = cfg.freq_chunk > 0 ? cfg.freq_chunk : (int)std::min<double>(K, 0.6 * free_b / per);
+  chunk = std::max(1, std::min(chunk, K));
+  fw->chunk = chunk;
+  std::vector<LevelOp> ops(nl);
+  for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get()};
+  MGConfig mc;
+  mc.rtol = cfg.inner_rtol;
+  mc.max_iter = cfg.inner_max_iter;
+  fw->solver.init(this, ops, chunk, mc);
+  TP_CUDA(cudaStreamSynchronize(stream));
+  freq_ready = true;
+  uhat_valid = false;
+}
+
+void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
+  build_frequency_solver(cfg);
+  launch_rdft_forward(*this, G.get(), Ghat.get());
+  const bool warm = cfg.warm_start && uhat_valid;
+  int iters = 0;
+  for (int k0 = 0; k0 < K; k0 += fw->chunk) {
+    const int nb = std::min(fw->chunk, K - k0);
+    fw->solver.lam = fw->lam.get() + k0;
+    fw->solver.coarse_inv = fw->inv.get() + (size_t)k0 * fw->nL * fw->nL;
+    iters = std::max(iters, fw->solver.solve(Ghat.get() + (size_t)k0 * n, Uhat.get() + (size_t)k0 * n,
+                                             nb, warm, st));
+  }
+  last_inner = iters;
+  double re2 = 0, im2 = 0;
+  launch_rdft_inverse(*this, Uhat.get(), U.get(), &re2, &im2);
+  uhat_valid = true;
+  // imaginary-residue guard, periodic.hpp:186-196
+  const double re_norm = std::sqrt(re2), im_norm = std::sqrt(im2);
+  if (im_norm > cfg.imag_tol * std::max(re_norm, 1e-300))
+    throw Error(TP_ESOLVE,
+                "periodic solver: imaginary residue " + std::to_string(im_norm) + " exceeds " +
+                    std::to_string(cfg.imag_tol) + " x " + std::to_string(re_norm),
+                im_norm / std::max(re_norm, 1e-300));
+}
+
+}  // namespace tpgpu
+
+// =================================================================== C ABI
+using tpgpu::Error;
+using tpgpu::Problem;
+
+struct tp_problem {
+  std::unique_ptr<Problem> impl;
+};
+
+namespace {
+thread_local std::string g_err;
+thread_local double g_err_res = -1;
+
+template <class F>
+int guarded(F&& f) {
+  try {
+    f();
+    return TP_OK;
+  } catch (const Error& e) {
+    g_err = e.what();
+    g_err_res = e.residual;
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    g_err = std::string("allocation failed: ") + e.what();
+    g_err_res = -1;
+    return TP_ECUDA;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    g_err_res = -1;
+    return TP_EINVAL;
+  }
+}
+
+Problem& P(tp_problem* p) {
+  tpgpu::require(p && p->impl, "null problem handle");
+  TP_CUDA(cudaSetDevice(p->impl->device));
+  return *p->impl;
+}
+
+tp_solver_cfg cfg_or_default(const tp_solver_cfg* c) {
+  tp_solver_cfg d;
+  tp_solver_cfg_default(&d);
+  return c ? *c : d;
+}
+
+double seconds_since(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+extern "C" {
+
+int tp_version(void) { return TPGPU_VERSION; }
+
+int tp_last_error(char* buf, size_t cap, double* achieved) {
+  if (buf && cap) {
+    std::strncpy(buf, g_err.c_str(), cap - 1);
+    buf[cap - 1] = 0;
+  }
+  if (achieved) *achieved = g_err_res;
+  return TP_OK;
+}
+
+void tp_solver_cfg_default(tp_solver_cfg* c) {
+  std::memset(c, 0, sizeof(*c));
+  c->tol = 1e-4;
+  c->m1_max_outer = 200;
+  c->armijo_max_halvings = 30;
+  c->armijo_slope = 1e-4;
+  c->armijo_backtrack = 0.5;
+  c->nu_hat_mode = TP_NU_HAT_FROZEN_FIELD;
+  c->nu_hat_samples = 2000;
+  c->imag_tol = 1e-9;
+  c->static_tol = 1e-8;
+  c->static_max_newton = 50;
+  c->threads = 1;
+  c->inner_rtol = 1e-13;
+  c->inner_max_iter = 200;
+  c->warm_start = 1;
+}
+
+int tp_problem_desc_baseline(int32_t config, tp_problem_desc* desc) {
+  return guarded([&] {
+    tpgpu::require(desc != nullptr, "null descriptor");
+    tpgpu::require(tp_baseline_desc_fill(config, desc) == 0, "unknown BASELINE config id");
+  });
+}
+
+int tp_problem_create(const tp_problem_desc* desc, int32_t device, tp_problem** out) {
+  return guarded([&] {
+    tpgpu::require(desc && out, "null argument");
+    auto h = std::make_unique<tp_problem>();
+    h->impl = std::make_unique<Problem>(*desc, device);
+    *out = h.release();
+  });
+}
+
+void tp_problem_destroy(tp_problem* p) {
+  if (!p) return;
+  if (p->impl) cudaSetDevice(p->impl->device);
+  delete p;
+}
+
+int tp_problem_sizes(const tp_problem* p, int32_t* n_dof, int32_t* steps, double* tau) {
+  return guarded([&] {
+    tpgpu::require(p && p->impl, "null problem handle");
+    if (n_dof) *n_dof = p->impl->n;
+    if (steps) *steps = p->impl->N;
+    if (tau) *tau = p->impl->tau;
+  });
+}
+
+int tp_problem_loads(tp_problem* h, double* F) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const int nsrc = (int)p.src_mats.size();
+    for (int s = 0; s < p.N; ++s)
+      for (int i = 0; i < p.n; ++i) {
+        double f = 0;
+        for (int r = 0; r < nsrc; ++r) f += p.src_time[(size_t)s * nsrc + r] * p.src_prof[(size_t)r * p.n + i];
+        F[(size_t)s * p.n + i] = f;
+      }
+  });
+}
+
+int tp_problem_mass(tp_problem* h, double* m) {
+  return guarded([&] {
+    Problem& p = P(h);
+    std::memcpy(m, p.mass.data(), p.n * sizeof(double));
+  });
+}
+
+int tp_apply_k(tp_problem* h, const double* U, double* KU, int32_t count) {
+  return guarded([&] {
+    Problem& p = P(h);
+    tpgpu::require(count >= 1, "apply_k: count must be positive");
+    tpgpu::DevBuf<double> du((size_t)count * p.n), dk((size_t)count * p.n);
+    TP_CUDA(cudaMemcpyAsync(du.get(), U, du.bytes(), cudaMemcpyHostToDevice, p.stream));
+    p.apply_k_dev(du.get(), dk.get(), count);
+    TP_CUDA(cudaMemcpyAsync(KU, dk.get(), dk.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    TP_CUDA(cudaStreamSynchronize(p.stream));
+  });
+}
+
+int tp_residual(tp_problem* h, const double* U, double* R, double* norm) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const size_t sz = (size_t)p.N * p.n;
+    tpgpu::DevBuf<double> du(sz), dr(sz);
+    TP_CUDA(cudaMemcpyAsync(du.get(), U, sz * sizeof(double), cudaMemcpyHostToDevice, p.stream));
+    p.residual_dev(du.get(), dr.get(), p.N);
+    const size_t np = p.part.count;
+    (void)np;
+    if (R) TP_CUDA(cudaMemcpyAsync(R, dr.get(), sz * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
+    const int blocks = (int)(((p.m + 31) / 32) * ((p.m + 7) / 8) * (size_t)p.N);
+    const double s = tpgpu::reduce_sum(p, p.part.get(), blocks);
+    if (norm) *norm = std::sqrt(s);
+  });
+}
+
+int tp_set_state(tp_problem* h, const double* U) {
+  return guarded([&] {
+    Problem& p = P(h);
+    TP_CUDA(cudaMemcpyAsync(p.U.get(), U, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+    TP_CUDA(cudaStreamSynchronize(p.stream));
+    p.state_valid = true;
+    p.uhat_valid = false;
+  });
+}
+
+int tp_get_state(tp_problem* h, double* U) {
+  return guarded([&] {
+    Problem& p = P(h);
+    TP_CUDA(cudaMemcpyAsync(U, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    TP_CUDA(cudaStreamSynchronize(p.stream));
+  });
+}
+
+int tp_static_init(tp_problem* h, const tp_solver_cfg* c, double* U0, int32_t* newton_counts) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const tp_solver_cfg cfg = cfg_or_default(c);
+    tpgpu::validate_cfg(cfg);
+    p.static_init_dev(cfg, newton_counts);
+    p.state_valid = true;
+    p.uhat_valid = false;
+    if (U0) {
+      TP_CUDA(cudaMemcpyAsync(U0, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      TP_CUDA(cudaStreamSynchronize(p.stream));
+    }
+  });
+}
+
+// choose_nu_hat (assembly.hpp:254-303) + flux_bounds (materials.hpp:147-155)
+int tp_choose_nu_hat(tp_problem* h, const tp_solver_cfg* c, double* nu_hat, double* q) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const tp_solver_cfg cfg = cfg_or_default(c);
+    const bool theory = cfg.nu_hat_mode == TP_NU_HAT_THEORY;
+    double lo[TP_MAX_MATERIALS], hi[TP_MAX_MATERIALS];
+    int any[TP_MAX_MATERIALS] = {0, 0, 0, 0, 0};
+    if (!theory) {
+      tpgpu::require(p.state_valid, "choose_nu_hat: frozen-field mode needs a state (static_init or set_state)");
+      p.field_ranges(lo, hi, any);
+    }
+    double out[TP_MAX_MATERIALS];
+    double qq = 0;
+    const int samples = cfg.nu_hat_samples > 1 ? cfg.nu_hat_samples : 2000;
+    for (int r = 0; r < TP_MAX_MATERIALS; ++r) {
+      if (r >= p.desc.n_materials) {
+        out[r] = 1.0;
+        continue;
+      }
+      const tp_material& mt = p.desc.material[r];
+      double lf, Lf;
+      tpgpu::flux_bounds(mt, 0.0, p.desc.s_max > 0 ? p.desc.s_max : 3.0,
+                  p.desc.flux_samples > 1 ? p.desc.flux_samples : 10001, lf, Lf);
+      if (theory) {
+        out[r] = 0.5 * (lf + Lf);
+        qq = std::max(qq, (Lf - lf) / (Lf + lf));
+        continue;
+      }
+      if (!any[r]) {
+        out[r] = 0.5 * (lf + Lf);
+        continue;
+      }
+      const double margin = 0.2 * (hi[r] - lo[r]) + 1e-3;
+      double lam, Lam;
+      tpgpu::flux_bounds(mt, std::max(0.0, lo[r] - margin), hi[r] + margin, samples, lam, Lam);
+      out[r] = 0.5 * (lam + Lam);
+      qq = std::max(qq, (Lam - lam) / (Lam + lam));
+    }
+    p.install_nu_hat(out, qq);
+    if (nu_hat) std::memcpy(nu_hat, out, sizeof(out));
+    if (q) *q = qq;
+  });
+}
+
+int tp_set_nu_hat(tp_problem* h, const double* nu_hat, double q) {
+  return guarded([&] { P(h).install_nu_hat(nu_hat, q); });
+}
+
+int tp_periodic_solve(tp_problem* h, const tp_solver_cfg* c, const double* G, double* U) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const tp_solver_cfg cfg = cfg_or_default(c);
+    TP_CUDA(cudaMemcpyAsync(p.G.get(), G, p.G.bytes(), cudaMemcpyHostToDevice, p.stream));
+    p.uhat_valid = false;
+    tpgpu::SolveStats st;
+    p.periodic_solve_dev(cfg, &st);
+    TP_CUDA(cudaMemcpyAsync(U, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    TP_CUDA(cudaStreamSynchronize(p.stream));
+    p.state_valid = true;
+  });
+}
+
+int tp_m1_begin(tp_problem* h, const tp_solver_cfg* c, double* residual0) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const tp_solver_cfg cfg = cfg_or_default(c);
+    tpgpu::validate_cfg(cfg);
+    tpgpu::require(p.state_valid, "m1: no state (static_init or set_state first)");
+    p.build_frequency_solver(cfg);
+    p.uhat_valid = false;
+    const double r0 = p.residual_and_rhs(true);
+    if (residual0) *residual0 = r0;
+  });
+}
+
+int tp_m1_sweep(tp_problem* h, double* residual, int32_t* inner) {
+  return guarded([&] {
+    Problem& p = P(h);
+    tpgpu::require(p.freq_ready, "m1 sweep: call tp_m1_begin first");
+    tp_solver_cfg cfg;
+    tp_solver_cfg_default(&cfg);
+    cfg.inner_rtol = p.fw->solver.cfg.rtol;
+    cfg.inner_max_iter = p.fw->solver.cfg.max_iter;
+    tpgpu::SolveStats st;
+    p.periodic_solve_dev(cfg, &st);
+    const double r = p.residual_and_rhs(true);
+    if (residual) *residual = r;
+    if (inner) *inner = st.iterations;
+  });
+}
+
+// solve_m1_fixed_point, solvers.hpp:301-369
+int tp_solve_m1(tp_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out,
+                tp_report* rep, double* history, double* contraction, int32_t cap, tp_iterate_cb cb,
+                void* user) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const tp_solver_cfg cfg = cfg_or_default(c);
+    tpgpu::validate_cfg(cfg);
+    tpgpu::require(p.nu_hat_set, "m1: nu_hat not installed (tp_choose_nu_hat / tp_set_nu_hat)");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (U0) {
+      TP_CUDA(cudaMemcpyAsync(p.U.get(), U0, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+      p.state_valid = true;
+    }
+    tpgpu::require(p.state_valid, "m1: no initial state");
+    std::vector<double> hist;
+    std::vector<double> host_u;
+    auto callback = [&](int k, double res) {
+      if (!cb) return;
+      host_u.resize((size_t)p.N * p.n);
+      TP_CUDA(cudaMemcpyAsync(host_u.data(), p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      TP_CUDA(cudaStreamSynchronize(p.stream));
+      if (cb(k, host_u.data(), res, user) != 0) throw Error(TP_EINVAL, "m1: aborted by iterate callback");
+    };
+    auto stop = [&]() { return hist.back() <= cfg.tol * hist.front(); };  // solvers.hpp:100-103
+    hist.push_back(p.residual_and_rhs(true));
+    callback(0, hist.back());
+    tp_report r{};
+    r.q_estimate = p.q_estimate;
+    tpgpu::SolveStats st;
+    double setup = 0, sweeps = 0;
+    if (!stop()) {
+      const auto ts = std::chrono::steady_clock::now();
+      p.build_frequency_solver(cfg);
+      p.uhat_valid = false;
+      setup = seconds_since(ts);
+      for (int k = 1; k <= cfg.m1_max_outer; ++k) {
+        const auto tk = std::chrono::steady_clock::now();
+        p.periodic_solve_dev(cfg, &st);
+        r.iterations = k;
+        hist.push_back(p.residual_and_rhs(true));
+        sweeps += seconds_since(tk);
+        callback(k, hist.back());
+        if (stop()) break;
+      }
+    }
+    r.status = stop() ? TP_CONVERGED : TP_MAX_ITER;
+    r.inner_iterations = (int32_t)st.batch_iterations;
+    r.history_len = (int32_t)std::min<size_t>(hist.size(), cap > 0 ? cap : 0);
+    if (history)
+      for (int k = 0; k < r.history_len; ++k) history[k] = hist[k];
+    if (contraction)
+      for (size_t k = 0; k + 1 < hist.size() && (int)k < cap; ++k)
+        contraction[k] = hist[k] > 0 ? hist[k + 1] / hist[k] : 0.0;
+    if (U_out) {
+      TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      TP_CUDA(cudaStreamSynchronize(p.stream));
+    }
+    r.setup_time = setup;
+    r.sweep_time = sweeps;
+    r.wall_time = seconds_since(t0);
+    if (rep) *rep = r;
+  });
+}
+
+void* tp_problem_stream(tp_problem* p) { return (p && p->impl) ? (void*)p->impl->stream : nullptr; }
+
+int64_t tp_problem_launches(const tp_problem* p) { return (p && p->impl) ? p->impl->launches : 0; }
+
+}  // extern "C"

@@ -1,0 +1,204 @@
+// Internal declarations of the B200 fixed-point-sweep library (libtpgpu.so).
+// See DESIGN.md for the data layout and the kernel inventory.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "../../include/tpgpu.h"
+
+namespace tpgpu {
+
+// ---------------------------------------------------------------- errors
+struct Error : std::runtime_error {
+  int code;
+  double residual;
+  Error(int c, const std::string& m, double r = -1.0) : std::runtime_error(m), code(c), residual(r) {}
+};
+
+[[noreturn]] void throw_cuda(cudaError_t e, const char* what, const char* file, int line);
+#define TP_CUDA(x)                                                   \
+  do {                                                               \
+    cudaError_t tp_e_ = (x);                                         \
+    if (tp_e_ != cudaSuccess) ::tpgpu::throw_cuda(tp_e_, #x, __FILE__, __LINE__); \
+  } while (0)
+#define TP_LAUNCHED(p)                                               \
+  do {                                                               \
+    ++(p)->launches;                                                 \
+    cudaError_t tp_e_ = cudaGetLastError();                          \
+    if (tp_e_ != cudaSuccess) ::tpgpu::throw_cuda(tp_e_, "kernel launch", __FILE__, __LINE__); \
+  } while (0)
+
+inline void require(bool ok, const std::string& msg) {
+  if (!ok) throw Error(TP_EINVAL, msg);
+}
+
+// ---------------------------------------------------------------- complex
+struct cplx {
+  double re, im;
+};
+__host__ __device__ inline cplx mk(double r, double i) { return cplx{r, i}; }
+__host__ __device__ inline cplx operator+(cplx a, cplx b) { return {a.re + b.re, a.im + b.im}; }
+__host__ __device__ inline cplx operator-(cplx a, cplx b) { return {a.re - b.re, a.im - b.im}; }
+__host__ __device__ inline cplx operator*(cplx a, cplx b) {
+  return {a.re * b.re - a.im * b.im, a.re * b.im + a.im * b.re};
+}
+__host__ __device__ inline cplx operator*(double s, cplx a) { return {s * a.re, s * a.im}; }
+__host__ __device__ inline cplx conj(cplx a) { return {a.re, -a.im}; }
+__host__ __device__ inline double norm2(cplx a) { return a.re * a.re + a.im * a.im; }
+__host__ __device__ inline double norm2(double a) { return a * a; }
+__host__ __device__ inline cplx cdiv(cplx a, cplx b) {
+  const double d = b.re * b.re + b.im * b.im;
+  return {(a.re * b.re + a.im * b.im) / d, (a.im * b.re - a.re * b.im) / d};
+}
+__host__ __device__ inline double cdiv(double a, double b) { return a / b; }
+
+// ---------------------------------------------------------------- device buffers
+template <class T>
+struct DevBuf {
+  T* ptr = nullptr;
+  size_t count = 0;
+  DevBuf() = default;
+  explicit DevBuf(size_t n) { alloc(n); }
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) { o.ptr = nullptr; o.count = 0; }
+  DevBuf& operator=(DevBuf&& o) noexcept {
+    if (this != &o) { release(); ptr = o.ptr; count = o.count; o.ptr = nullptr; o.count = 0; }
+    return *this;
+  }
+  ~DevBuf() { release(); }
+  void alloc(size_t n) {
+    release();
+    if (n) TP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
+    count = n;
+  }
+  void ensure(size_t n) { if (count < n) alloc(n); }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    count = 0;
+  }
+  T* get() const { return ptr; }
+  size_t bytes() const { return count * sizeof(T); }
+};
+
+// ---------------------------------------------------------------- grid
+// Interior node (x, y), 0 <= x, y < m = cells-1, index y*m + x; it is vertex
+// (x+1, y+1) of the (cells+1)^2 vertex lattice.  Cell (i, j) has triangles
+// T1 = {v(i,j), v(i+1,j), v(i+1,j+1)} and T2 = {v(i,j), v(i+1,j+1), v(i,j+1)}.
+// 7-point stencils are stored SoA: st[d*n + i], d in the order below.
+enum StencilDir { SC = 0, SW_ = 1, SE_ = 2, SS_ = 3, SN_ = 4, SSW = 5, SNE = 6 };
+constexpr int kDirs = 7;
+__host__ __device__ constexpr int dir_dx(int d) { return d == 1 ? -1 : d == 2 ? 1 : d == 5 ? -1 : d == 6 ? 1 : 0; }
+__host__ __device__ constexpr int dir_dy(int d) { return d == 3 ? -1 : d == 4 ? 1 : d == 5 ? -1 : d == 6 ? 1 : 0; }
+
+struct MaterialDev {
+  double nu0, nu_inf, bs2;  // bs2 = Bs^2
+  int linear;
+};
+
+// ---------------------------------------------------------------- multigrid
+// One level of the geometric hierarchy (P1 interpolation on the nested
+// triangulation, Galerkin coarse operators).
+struct Level {
+  int m = 0;          // interior nodes per side
+  int n = 0;          // m*m
+  DevBuf<double> K;   // 7*n real stencil (frequency mode: shared)
+  DevBuf<double> M;   // 7*n real stencil (frequency mode: shared)
+};
+
+class Problem;
+
+// Batched multigrid-preconditioned conjugate-gradient solver.  Frequency mode
+// (T = cplx): operator lambda_b M + K with shared real stencils, COCG (complex
+// symmetric, bilinear form).  Slice mode (T = double): per-batch real SPD
+// stencils (Newton Jacobians), PCG.
+struct SolveStats {
+  int iterations = 0;
+  int64_t batch_iterations = 0;
+  double max_rel_residual = 0;
+};
+
+// ---------------------------------------------------------------- problem
+class Problem {
+ public:
+  Problem(const tp_problem_desc& d, int device);
+  ~Problem();
+
+  // host setup products
+  tp_problem_desc desc;
+  int device = 0;
+  int c = 0, m = 0, n = 0, N = 0, K = 0;  // cells, nodes/side, dofs, steps, frequencies N/2+1
+  double tau = 0, T = 0;
+  std::vector<uint8_t> cell_mat;      // c*c
+  std::vector<double> tri_sigma;      // 2*c*c
+  std::vector<double> mass;           // n (lumped)
+  std::vector<int> src_mats;          // materials with sources
+  std::vector<double> src_prof;       // nsrc * n  (int j(t)=1 phi_i over the material)
+  std::vector<double> src_time;       // N * nsrc  (j_r(t_n))
+  std::vector<double> nu_hat;         // TP_MAX_MATERIALS
+  double q_estimate = 0;
+  bool nu_hat_set = false;
+
+  // device constants
+  cudaStream_t stream = nullptr;
+  int64_t launches = 0;
+  int num_sms = 148;
+  DevBuf<uint8_t> d_cell_mat;
+  DevBuf<double> d_mass;
+  DevBuf<double> d_src_prof;
+  DevBuf<double> d_src_time;
+  DevBuf<MaterialDev> d_mat;
+  DevBuf<double> d_nu_hat;
+  // device state
+  DevBuf<double> U;     // N*n current iterate (slice-major)
+  DevBuf<double> G;     // N*n right-hand side of the next sweep
+  DevBuf<cplx> Ghat;    // K*n  (frequency-major)
+  DevBuf<cplx> Uhat;    // K*n  (frequency-major)
+  DevBuf<double> part;  // reduction partials
+  DevBuf<double> red;   // reduced scalars
+  bool state_valid = false;
+  bool uhat_valid = false;
+
+  // frequency-solver hierarchy
+  std::vector<Level> levels;
+  bool freq_ready = false;
+  int freq_chunk = 0;
+  struct FreqWork;
+  std::unique_ptr<FreqWork> fw;
+
+  std::shared_ptr<void> fft_plan;
+
+  // pinned host scratch
+  double* h_scalars = nullptr;  // pinned, 4096 doubles
+
+  // ---- operations (defined across the .cu files)
+  void upload_constants();
+  void install_nu_hat(const double* nu, double q);
+  void build_frequency_solver(const tp_solver_cfg& cfg);
+  // K(u) for `count` slices of `u` into `out` (device pointers)
+  void apply_k_dev(const double* u, double* out, int count);
+  // fused residual + next RHS over the device state: returns ||R||
+  double residual_and_rhs(bool want_rhs);
+  // residual only (host-facing)
+  void residual_dev(const double* u, double* r, int count_slices);
+  // periodic linear solve of the device G into the device U
+  void periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st);
+  void static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts);
+  void field_ranges(double* lo, double* hi, int* any);
+  int last_inner = 0;
+};
+
+// kernels / helpers implemented in the .cu files
+void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat);
+// returns imaginary-residue norm^2 partial sum and real norm^2 (host)
+void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2);
+double reduce_sum(Problem& p, const double* partials, int count);
+
+}  // namespace tpgpu

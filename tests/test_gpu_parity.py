@@ -1,0 +1,137 @@
+"""GPU parity: libtpgpu.so (CUDA, sm_100a) against the compiled reference
+(oracle/_ref/libtpref.so = tpfem's own static_init / solve_m1_fixed_point /
+PeriodicSolver on the BASELINE grid physics), same seeded inputs.
+
+Tolerances (BASELINE.json north_star): every fixed-point iterate within a
+relative l2 error of 1e-10, identical fixed-point iteration counts, identical
+Newton counts; setup vectors (loads, mass) and K(u) within 1e-13 relative.
+"""
+import numpy as np
+import pytest
+
+from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg
+from paper_2502_21013_b200.abi import TpProblemDesc
+
+pytestmark = pytest.mark.gpu
+
+ITERATE_TOL = 1e-10
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-300))
+
+
+def small_desc(cells=16, steps=16, config=0):
+    d = baseline_desc(config)
+    d.cells = cells
+    d.steps = steps
+    return d
+
+
+@pytest.fixture(scope="module")
+def cfg0_ref(ref):
+    d = ref.baseline_desc(0)
+    cfg = default_cfg(tol=1e-8)
+    U0, counts = ref.static_init(d, cfg)
+    nu, q = ref.choose_nu_hat(d, U0, cfg)
+    m1 = ref.solve_m1(d, nu, q, U0, cfg, keep_iterates=True)
+    return dict(desc=d, cfg=cfg, U0=U0, counts=counts, nu=nu, q=q, m1=m1)
+
+
+@pytest.mark.parametrize("config", [0, 1])
+def test_setup_vectors_match_reference(ref, config):
+    d = baseline_desc(config)
+    with Problem(d) as p:
+        assert p.shape == ref.sizes(d)[1::-1]
+        F, Fr = p.loads(), ref.loads(d)
+        assert rel(F, Fr) <= 1e-13
+        assert rel(p.mass(), ref.mass(d)) <= 1e-13
+
+
+@pytest.mark.parametrize("config,slices", [(0, 8), (1, 3), (2, 1)])
+def test_apply_k_matches_reference(ref, config, slices):
+    d = baseline_desc(config)
+    with Problem(d) as p:
+        rng = np.random.default_rng(100 + config)
+        U = rng.standard_normal((slices, p.n_dof)) * 0.05
+        out = p.apply_k(U)
+        assert rel(out, ref.apply_k(d, U)) <= 1e-13
+
+
+def test_residual_matches_reference(ref):
+    d = baseline_desc(0)
+    with Problem(d) as p:
+        rng = np.random.default_rng(7)
+        U = rng.standard_normal(p.shape) * 0.02
+        R, nrm = p.residual(U)
+        Rr, nr = ref.residual(d, U)
+        assert rel(R, Rr) <= 1e-13
+        assert abs(nrm - nr) <= 1e-13 * nr
+
+
+def test_static_init_matches_reference(cfg0_ref):
+    r = cfg0_ref
+    with Problem(r["desc"]) as p:
+        U0, counts = p.static_init(r["cfg"])
+        assert np.array_equal(counts, r["counts"])
+        assert rel(U0, r["U0"]) <= ITERATE_TOL
+        nu, q = p.choose_nu_hat(r["cfg"])
+        assert np.allclose(nu, r["nu"], rtol=1e-12, atol=0)
+        assert abs(q - r["q"]) <= 1e-12
+
+
+def test_periodic_solve_matches_reference(ref, cfg0_ref):
+    r = cfg0_ref
+    d = r["desc"]
+    with Problem(d) as p:
+        p.set_nu_hat(r["nu"], r["q"])
+        rng = np.random.default_rng(11)
+        G = rng.standard_normal(p.shape)
+        U = p.periodic_solve(G, r["cfg"])
+        Ur = ref.periodic_solve(d, r["nu"], G, r["cfg"])
+        assert rel(U, Ur) <= 1e-11
+
+
+@pytest.mark.parametrize("cells,steps", [(8, 5), (8, 8), (16, 7), (32, 12)])
+def test_periodic_solve_odd_sizes(ref, cells, steps):
+    """Single-level (dense) and multi-level hierarchies, odd N (direct DFT)."""
+    d = small_desc(cells, steps)
+    with Problem(d) as p:
+        nu = np.array([3.0, 2.0, 5.0, 1.0, 1.0])
+        p.set_nu_hat(nu)
+        G = np.random.default_rng(cells * 100 + steps).standard_normal(p.shape)
+        U = p.periodic_solve(G)
+        Ur = ref.periodic_solve(d, nu, G)
+        assert rel(U, Ur) <= 1e-11
+
+
+def test_m1_fixed_point_matches_reference(cfg0_ref):
+    """Iteration count identical; every iterate within 1e-10 relative."""
+    r = cfg0_ref
+    m1 = r["m1"]
+    with Problem(r["desc"]) as p:
+        p.set_nu_hat(r["nu"], r["q"])
+        log = []
+        U, rep = p.solve_m1_fixed_point(r["U0"], r["cfg"], iterate_log=log)
+        assert rep.status == "converged"
+        assert rep.iterations == m1.iterations
+        assert len(log) == m1.iterations + 1
+        errs = [rel(a, b) for a, b in zip(log, m1.iterates)]
+        assert max(errs) <= ITERATE_TOL, max(errs)
+        h, hr = np.array(rep.residual_history), m1.history
+        assert np.all(np.abs(h - hr) <= 1e-10 * hr[0] + 1e-6 * hr)
+        assert rel(U, m1.U) <= ITERATE_TOL
+
+
+def test_linear_control_converges_in_one_sweep(ref):
+    """nu == nu0 everywhere: frozen nu_hat == nu, K_hat == K, one sweep."""
+    d = baseline_desc(5)
+    d.cells, d.steps = 32, 32
+    cfg = default_cfg(tol=1e-8)
+    with Problem(d) as p:
+        p.static_init(cfg, want_state=False)
+        nu, q = p.choose_nu_hat(cfg)
+        assert q == 0.0
+        U, rep = p.solve_m1_fixed_point(None, cfg)
+        assert rep.iterations == 1 and rep.status == "converged"
