@@ -1,0 +1,307 @@
+#!/usr/bin/env python3
+"""Benchmark: space-time DoF/s per fixed-point sweep (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
+                    [--config 1] [--no-cpu-baseline]
+
+One step = one fixed-point sweep over all N time slices of the workload
+(solvers.hpp:326-342: RHS f + K_hat u - K(u), DFT along time, the N/2+1
+frequency-block solves, inverse DFT, residual + norm).  Default workload:
+BASELINE.json configs[1] (256x256 cells, 65,025 dofs, N = 256, fp64).
+
+Timing: W untimed warm-up sweeps, then exactly K sweeps bracketed by a
+barrier + cudaDeviceSynchronize and CUDA events on the library's stream,
+max over ranks.  Every sweep streams U, G, Ghat, Uhat (133 MB each, > L2).
+`e2e` goes through the C ABI with pinned HOST buffers: each step uploads U,
+runs one sweep (tp_solve_m1 with m1_max_outer = 1) and downloads U.
+
+Multi-GPU (torchrun): each rank runs the workload on its own GPU (weak
+scaling, replicas); the N>1 sharded solver is not wired into the bench yet.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "space-time DoF/s per fixed-point sweep"
+UNIT = "DoF/s"
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            pk = json.load(f)
+        return float(pk["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, device: int):
+        self.device = device
+        self.rows = []
+        self._stop = threading.Event()
+        self._t = None
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                out = subprocess.run(["nvidia-smi", "-i", str(self.device), f"--query-gpu={self.Q}",
+                                      "--format=csv,noheader,nounits"], capture_output=True,
+                                     text=True, timeout=5).stdout.strip()
+                if out:
+                    self.rows.append([x.strip() for x in out.split(",")])
+            except Exception:
+                pass
+            self._stop.wait(0.2)
+
+    def __enter__(self):
+        self._t = threading.Thread(target=self._run, daemon=True)
+        self._t.start()
+        return self
+
+    def __exit__(self, *a):
+        self._stop.set()
+        self._t.join(timeout=10)
+
+    def summary(self):
+        if not self.rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[k] for r in self.rows for k in range(4)
+                          if len(r) > 5 + k and r[5 + k].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+                "samples": len(self.rows)}
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    pg = None
+    if world > 1:
+        import torch.distributed as dist
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        dist.init_process_group("gloo", rank=rank, world_size=world)
+        pg = dist
+    return world, rank, local, pg
+
+
+def allreduce_max(pg, x: float) -> float:
+    if pg is None:
+        return x
+    import torch
+    t = torch.tensor([x], dtype=torch.float64)
+    pg.all_reduce(t, op=pg.ReduceOp.MAX)
+    return float(t.item())
+
+
+def barrier(pg):
+    if pg is not None:
+        pg.barrier()
+
+
+def cudart():
+    import torch  # noqa: F401  (loads the CUDA runtime for event timing)
+    return torch
+
+
+def workload_config(desc, world):
+    n = (desc.cells - 1) ** 2
+    D = n * desc.steps
+    return D, {
+        "workload": f"BASELINE configs[1]: {desc.cells}x{desc.cells} cells ({n} dofs) x N={desc.steps} "
+                    "slices, fp64, U0 = static_init, frozen-field nu_hat",
+        "cells": desc.cells, "steps": desc.steps, "space_time_dof": D,
+        "l2": "inputs larger than L2 (U, G, Ghat, Uhat 133 MB each, streamed every sweep)",
+        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+    }
+
+
+# ----------------------------------------------------------------- b200 arm
+def run_b200(args):
+    world, rank, local, pg = dist_setup()
+    torch = cudart()
+    torch.cuda.set_device(local)
+    from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg
+
+    desc = baseline_desc(args.config)
+    D, config = workload_config(desc, world)
+    cfg = default_cfg(tol=1e-8)
+    p = Problem(desc, device=local)
+    t0 = time.perf_counter()
+    U0, counts = p.static_init(cfg)
+    nu, q = p.choose_nu_hat(cfg)
+    init_s = time.perf_counter() - t0
+    t0 = time.perf_counter()
+    r0 = p.m1_begin(cfg)
+    setup_s = time.perf_counter() - t0
+    history = [r0]
+    for _ in range(args.warmup):
+        history.append(p.m1_sweep()[0])
+    stream = torch.cuda.ExternalStream(p.stream, device=local)
+    evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
+    inner = []
+    launches0 = p.launches
+    barrier(pg)
+    torch.cuda.synchronize()
+    with ClockSampler(local) as clk:
+        evs[0].record(stream)
+        for k in range(args.steps):
+            r, it = p.m1_sweep()
+            history.append(r)
+            inner.append(it)
+            evs[k + 1].record(stream)
+        torch.cuda.synchronize()
+    barrier(pg)
+    launches = p.launches - launches0
+    per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
+    total_ms = evs[0].elapsed_time(evs[-1])
+    total_ms = allreduce_max(pg, total_ms)
+    value = D * args.steps * world / (total_ms / 1e3)
+
+    # e2e through the C ABI with pinned host buffers (one sweep per call)
+    e2e = None
+    if args.e2e_steps > 0:
+        Uh = torch.empty(p.shape, dtype=torch.float64, pin_memory=True).numpy()
+        Uo = torch.empty(p.shape, dtype=torch.float64, pin_memory=True).numpy()
+        Uh[:] = U0
+        c1 = default_cfg(tol=1e-300 if False else 1e-12, m1_max_outer=1)
+        p.solve_m1_fixed_point(Uh, c1)  # warm (hierarchy cached)
+        times = []
+        for _ in range(args.e2e_steps):
+            barrier(pg)
+            t = time.perf_counter()
+            Uo[:], _rep = p.solve_m1_fixed_point(Uh, c1)
+            times.append(time.perf_counter() - t)
+        e2e_s = allreduce_max(pg, float(np.median(times)))
+        e2e = {"value": D * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Uh.nbytes),
+               "d2h_bytes_per_step": int(Uo.nbytes),
+               "note": "tp_solve_m1 per step: H2D U0, initial residual, one sweep (cold inner start), D2H U"}
+
+    hbm, src = peaks()
+    # Sweep-level algorithmic bytes: 72 D fixed + inner traffic
+    # S = 26.5 complex-vector streams per inner iteration per (node, frequency).
+    K = desc.steps // 2 + 1
+    n = (desc.cells - 1) ** 2
+    mean_inner = float(np.mean(inner)) if inner else 0.0
+    b_alg = 72.0 * D + 16.0 * n * 26.5 * K * mean_inner
+    t_sweep = total_ms / 1e3 / args.steps
+    roofline = {"bound": "hbm", "scope": "whole sweep (kernel-level figure in profiles/)",
+                "achieved": b_alg / t_sweep / 1e9, "peak": hbm, "unit": "GB/s",
+                "frac": b_alg / t_sweep / 1e9 / hbm, "traffic": None, "peak_source": src,
+                "bytes_per_sweep": b_alg, "inner_iterations_mean": mean_inner}
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "data": "synthetic (BASELINE.json configs[1] physics, seeded sigma noise)",
+           "config": config, "impl": "b200", "clocks": clk.summary(),
+           "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
+           "sweep_ms": {"median": float(np.median(per)), "min": float(np.min(per)),
+                        "max": float(np.max(per))},
+           "inner_iterations": inner, "init_s": init_s, "setup_s": setup_s,
+           "residual_last": history[-1], "residual_first": history[0]}
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(desc, U0, nu, q)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    p.close()
+
+
+def cpu_baseline(desc, U0, nu, q):
+    """The reference's own sweep (oracle/_ref/libtpref.so) on the host cores."""
+    from oracle import ref
+    from paper_2502_21013_b200.abi import default_cfg
+    if not ref.available():
+        return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
+                "sample": "oracle/_ref/libtpref.so not built"}
+    cores = ref.hardware_threads()
+    cfg = default_cfg(tol=1e-12, m1_max_outer=1, threads=cores)
+    r = ref.solve_m1(desc, nu, q, U0, cfg, cache=0)
+    sweep_s = max(r.wall_time - r.setup_time, 1e-9)
+    D = (desc.cells - 1) ** 2 * desc.steps
+    return {"value": D / sweep_s, "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": f"one full sweep of the same workload (tpfem solve_m1_fixed_point, "
+                      f"m1_max_outer=1, cache=automatic, {cores} threads, shim sparse LDL^T); "
+                      f"{sweep_s:.2f} s per sweep"}
+
+
+# ------------------------------------------------------------ reference arm
+def run_reference(args):
+    world, rank, local, pg = dist_setup()
+    if rank != 0:
+        return
+    from oracle import ref
+    from paper_2502_21013_b200.abi import default_cfg
+    desc = ref.baseline_desc(args.config)
+    D, config = workload_config(desc, world)
+    if not ref.available():
+        print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtpref.so not built"}))
+        return
+    cores = ref.hardware_threads()
+    cfg = default_cfg(tol=1e-8, threads=cores)
+    U0 = np.load(args.ref_u0) if args.ref_u0 else ref.static_init(desc, cfg)[0]
+    nu, q = ref.choose_nu_hat(desc, U0, cfg)
+    one = default_cfg(tol=1e-12, m1_max_outer=1, threads=cores)
+    times = []
+    U = U0
+    for k in range(args.warmup + args.steps):
+        r = ref.solve_m1(desc, nu, q, U, one, cache=0)
+        if k >= args.warmup:
+            times.append(max(r.wall_time - r.setup_time, 1e-9))
+        U = r.U
+    tot = float(np.sum(times))
+    value = D * len(times) / tot
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3, "higher_is_better": True,
+           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+           "config": config, "impl": "reference",
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                            "sample": "full sweeps of the workload, tpfem compiled from "
+                                      "/root/reference with the shim sparse LDL^T"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--config", type=int, default=1)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ref-u0", default=None, help="reference arm: precomputed U0 (.npy)")
+    args = ap.parse_args()
+    if args.warmup < 3 and args.impl == "b200":
+        args.warmup = 3
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_b200(args)
+
+
+if __name__ == "__main__":
+    main()
