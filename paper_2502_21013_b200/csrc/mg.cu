@@ -1,11 +1,22 @@
 // Batched multigrid-preconditioned CG/COCG -- see mg.cuh.
 //
-// Traffic notes (per fine node, per batch, per Krylov iteration; 16 B per
-// complex value): apply+dot (read z, p; write p, q), update (read x, p, r, q;
-// write x, r, z), one extra pre-smooth, residual+restrict, prolong+smooth,
-// last smooth+dot: ~22 streams on the fine level, ~1/3 more on the coarse
-// levels.  The kernels keep one thread per node and loop over BPT batches so
-// the shared frequency-mode stencil is loaded once per node.
+// Kernel layout: a block owns a 32x8 tile of nodes of one level and walks the
+// active batches (frequencies or slices) of its batch group.  In frequency
+// mode the tile's shared real stencils (K, M: 14 doubles per node) are staged
+// once per block in shared memory and combined with lambda_b on the fly, so
+// the operator costs no HBM traffic per batch and few registers.  Vector
+// tiles (+1 halo) are staged in shared memory and the next batch's tile is
+// prefetched into registers while the current one is computed (two batches
+// of loads in flight per block).  Restriction forms the fine residual tile in
+// shared memory and gathers P^T from it; prolongation interpolates the coarse
+// correction into the shared tile before smoothing.  32-bit node indices
+// within a level, 64-bit batch offsets.
+//
+// Per fine node and batch (16 B complex) one Krylov iteration streams:
+// apply+dot (read z, p; write p, q), update (read x, p, r, q; write x, r, z),
+// pre-smooth (read z, r; write z), residual+restrict (read z, r), prolong +
+// smooth (read z, r; write z), smooth+dot (read z, r; write z) = 22 vector
+// streams on the fine level, ~1/3 of that again on the coarse levels.
 #include <algorithm>
 #include <cmath>
 
@@ -15,48 +26,8 @@ namespace tpgpu {
 
 namespace {
 
-constexpr int NT = 256;
-
-template <int MODE>
-struct Op;
-
-template <>
-struct Op<0> {
-  const double* K;
-  const double* M;
-  const cplx* lam;
-  size_t n;
-  int m;
-  struct Pre {
-    double k[7], mm[7];
-  };
-  __device__ __forceinline__ void pre(size_t i, Pre& P) const {
-#pragma unroll
-    for (int d = 0; d < 7; ++d) {
-      P.k[d] = K[d * n + i];
-      P.mm[d] = M[d * n + i];
-    }
-  }
-  __device__ __forceinline__ void coef(const Pre& P, int b, size_t, cplx a[7]) const {
-    const cplx l = lam[b];
-#pragma unroll
-    for (int d = 0; d < 7; ++d) a[d] = {fma(l.re, P.mm[d], P.k[d]), l.im * P.mm[d]};
-  }
-};
-
-template <>
-struct Op<1> {
-  const double* J;
-  size_t n;
-  int m;
-  struct Pre {};
-  __device__ __forceinline__ void pre(size_t, Pre&) const {}
-  __device__ __forceinline__ void coef(const Pre&, int b, size_t i, double a[7]) const {
-    const double* s = J + (size_t)b * 7 * n;
-#pragma unroll
-    for (int d = 0; d < 7; ++d) a[d] = s[d * n + i];
-  }
-};
+constexpr int TX = 32, TY = 8, NT = TX * TY;
+constexpr int HX = TX + 2, HY = TY + 2, HN = HX * HY;  // halo tile: 340 values
 
 template <int MODE>
 using TT = typename std::conditional<MODE == 0, cplx, double>::type;
@@ -73,224 +44,117 @@ __device__ __forceinline__ void add_dot(double (&v)[2], cplx a, cplx b) {
   v[1] += t.im;
 }
 __device__ __forceinline__ void add_dot(double (&v)[2], double a, double b) { v[0] += a * b; }
-__device__ __forceinline__ cplx inv_of(cplx a) { return cdiv(cplx{1, 0}, a); }
+__device__ __forceinline__ cplx inv_of(cplx a) {
+  const double d = 1.0 / fma(a.re, a.re, a.im * a.im);
+  return {a.re * d, -a.im * d};
+}
 __device__ __forceinline__ double inv_of(double a) { return 1.0 / a; }
 
-struct Nbr {
-  long off[7];
-  bool ok[7];
+// Level operator.  MODE 0: lambda_b M + K with shared stencils; MODE 1:
+// per-batch stencil J_b.
+template <int MODE>
+struct Op;
+
+template <>
+struct Op<0> {
+  const double* K;
+  const double* M;
+  const cplx* lam;
+  int n, m;
 };
 
-__device__ __forceinline__ void neighbours(size_t i, int m, Nbr& nb) {
-  const int x = (int)(i % m), y = (int)(i / m);
-  nb.off[0] = 0; nb.ok[0] = true;
-  nb.off[1] = -1; nb.ok[1] = x > 0;
-  nb.off[2] = 1; nb.ok[2] = x < m - 1;
-  nb.off[3] = -m; nb.ok[3] = y > 0;
-  nb.off[4] = m; nb.ok[4] = y < m - 1;
-  nb.off[5] = -m - 1; nb.ok[5] = x > 0 && y > 0;
-  nb.off[6] = m + 1; nb.ok[6] = x < m - 1 && y < m - 1;
+template <>
+struct Op<1> {
+  const double* J;
+  int n, m;
+};
+
+// Per-block stencil staging (frequency mode): st[d][tid] (K), st[7+d][tid] (M).
+struct StageF {
+  double v[14][NT];
+};
+
+template <int MODE>
+struct Stencil;
+
+template <>
+struct Stencil<0> {
+  const StageF* s;
+  cplx l;
+  int tid;
+  __device__ __forceinline__ cplx operator()(int d) const {
+    const double mm = s->v[7 + d][tid];
+    return {fma(l.re, mm, s->v[d][tid]), l.im * mm};
+  }
+};
+
+template <>
+struct Stencil<1> {
+  const double* J;  // batch stencil base
+  int n, i;
+  __device__ __forceinline__ double operator()(int d) const { return __ldg(J + (size_t)d * n + i); }
+};
+
+__device__ __forceinline__ void stage_stencil(const Op<0>& op, StageF& st, int i, bool in, int tid) {
+#pragma unroll
+  for (int d = 0; d < 7; ++d) {
+    st.v[d][tid] = in ? __ldg(op.K + (size_t)d * op.n + i) : 0.0;
+    st.v[7 + d][tid] = in ? __ldg(op.M + (size_t)d * op.n + i) : 0.0;
+  }
 }
 
-template <class T>
-__device__ __forceinline__ T apply7(const T a[7], const T* __restrict__ v, size_t i, const Nbr& nb) {
-  T acc = mul(a[0], v[i]);
-#pragma unroll
-  for (int d = 1; d < 7; ++d)
-    if (nb.ok[d]) acc = acc + mul(a[d], v[i + nb.off[d]]);
+template <int MODE>
+__device__ __forceinline__ Stencil<MODE> stencil_of(const Op<MODE>& op, const StageF* st, int b, int i, int tid);
+template <>
+__device__ __forceinline__ Stencil<0> stencil_of<0>(const Op<0>& op, const StageF* st, int b, int, int tid) {
+  return Stencil<0>{st, op.lam[b], tid};
+}
+template <>
+__device__ __forceinline__ Stencil<1> stencil_of<1>(const Op<1>& op, const StageF*, int b, int i, int) {
+  return Stencil<1>{op.J + (size_t)b * 7 * op.n, op.n, i};
+}
+
+// 7-point application from the halo tile
+template <class T, class S>
+__device__ __forceinline__ T apply_tile(const S& a, const T (*s)[HX], int tx, int ty) {
+  const int lx = tx + 1, ly = ty + 1;
+  T acc = mul(a(0), s[ly][lx]);
+  acc = acc + mul(a(1), s[ly][lx - 1]);
+  acc = acc + mul(a(2), s[ly][lx + 1]);
+  acc = acc + mul(a(3), s[ly - 1][lx]);
+  acc = acc + mul(a(4), s[ly + 1][lx]);
+  acc = acc + mul(a(5), s[ly - 1][lx - 1]);
+  acc = acc + mul(a(6), s[ly + 1][lx + 1]);
   return acc;
 }
 
-template <int BPT>
-__device__ __forceinline__ void block_partials(double (&v)[BPT][2], double* __restrict__ part, int b0,
-                                               int nb, int per) {
-  __shared__ double sh[BPT][2][NT / 32];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-#pragma unroll
-  for (int k = 0; k < BPT; ++k)
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      double x = v[k][c];
-      for (int o = 16; o > 0; o >>= 1) x += __shfl_down_sync(0xffffffffu, x, o);
-      if (lane == 0) sh[k][c][w] = x;
-    }
+// Block-wide reduction of one batch's pair into part[(b*tiles + tile)*2 + c].
+__device__ __forceinline__ void block_pair(double v0, double v1, double* __restrict__ part, int b) {
+  __shared__ double sh[2][NT / 32];
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  for (int o = 16; o > 0; o >>= 1) {
+    v0 += __shfl_down_sync(0xffffffffu, v0, o);
+    v1 += __shfl_down_sync(0xffffffffu, v1, o);
+  }
+  if ((tid & 31) == 0) {
+    sh[0][tid >> 5] = v0;
+    sh[1][tid >> 5] = v1;
+  }
   __syncthreads();
-  if ((int)threadIdx.x < BPT * 2) {
-    const int k = threadIdx.x >> 1, c = threadIdx.x & 1;
-    double s = 0;
-    for (int ww = 0; ww < NT / 32; ++ww) s += sh[k][c][ww];
-    const int b = b0 + k;
-    if (b < nb) part[((size_t)b * gridDim.x + blockIdx.x) * 2 + c] = s;
-  }
-}
-
-// r = b - A x (warm) or r = b, x = 0 (cold); partials (||b||^2, ||r||^2).
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_init(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                             TT<MODE>* __restrict__ x, TT<MODE>* __restrict__ r,
-                                             int nb, int warm, double* __restrict__ part) {
-  using T = TT<MODE>;
-  const size_t n = op.n;
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  const int b0 = blockIdx.y * BPT;
-  double v[BPT][2] = {};
-  if (i < n) {
-    typename Op<MODE>::Pre P;
-    Nbr nbr;
-    if (warm) {
-      op.pre(i, P);
-      neighbours(i, op.m, nbr);
+  if (tid == 0) {
+    double a = 0, c = 0;
+    for (int w = 0; w < NT / 32; ++w) {
+      a += sh[0][w];
+      c += sh[1][w];
     }
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      const T bi = bv[(size_t)b * n + i];
-      T ri = bi;
-      if (warm) {
-        T a[7];
-        op.coef(P, b, i, a);
-        ri = bi - apply7(a, x + (size_t)b * n, i, nbr);
-      } else {
-        x[(size_t)b * n + i] = zero_of(bi);
-      }
-      r[(size_t)b * n + i] = ri;
-      v[k][0] += norm2(bi);
-      v[k][1] += norm2(ri);
-    }
-  }
-  block_partials<BPT>(v, part, b0, nb, gridDim.x);
-}
-
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_zero_flagged(TT<MODE>* __restrict__ x, size_t n, int nb,
-                                                     const int* __restrict__ zero) {
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  if (i >= n) return;
-  for (int k = 0; k < BPT; ++k) {
-    const int b = blockIdx.y * BPT + k;
-    if (b >= nb) break;
-    if (zero[b]) x[(size_t)b * n + i] = zero_of(x[0]);
+    const size_t tiles = (size_t)gridDim.x * gridDim.y;
+    const size_t tile = (size_t)blockIdx.y * gridDim.x + blockIdx.x;
+    part[((size_t)b * tiles + tile) * 2] = a;
+    part[((size_t)b * tiles + tile) * 2 + 1] = c;
   }
 }
 
-// p_out = first ? z : z + beta p_in ;  q = A p_out ; partial p^T q
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_apply_dot(Op<MODE> op, const TT<MODE>* __restrict__ z,
-                                                  const TT<MODE>* __restrict__ pin,
-                                                  TT<MODE>* __restrict__ pout, TT<MODE>* __restrict__ q,
-                                                  const TT<MODE>* __restrict__ beta,
-                                                  const int* __restrict__ active, int first, int nb,
-                                                  double* __restrict__ part) {
-  using T = TT<MODE>;
-  const size_t n = op.n;
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  const int b0 = blockIdx.y * BPT;
-  double v[BPT][2] = {};
-  if (i < n) {
-    typename Op<MODE>::Pre P;
-    op.pre(i, P);
-    Nbr nbr;
-    neighbours(i, op.m, nbr);
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      if (!active[b]) continue;
-      const size_t o = (size_t)b * n;
-      T a[7];
-      op.coef(P, b, i, a);
-      const T bt = first ? zero_of(a[0]) : beta[b];
-      T acc = zero_of(a[0]), pi = zero_of(a[0]);
-#pragma unroll
-      for (int d = 0; d < 7; ++d) {
-        if (!nbr.ok[d]) continue;
-        const size_t j = o + i + nbr.off[d];
-        const T pj = first ? z[j] : z[j] + mul(bt, pin[j]);
-        if (d == 0) pi = pj;
-        acc = acc + mul(a[d], pj);
-      }
-      pout[o + i] = pi;
-      q[o + i] = acc;
-      add_dot(v[k], pi, acc);
-    }
-  }
-  block_partials<BPT>(v, part, b0, nb, gridDim.x);
-}
-
-// x += alpha p ; r -= alpha q ; partial ||r||^2 ; z = omega r / a_C
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_update(Op<MODE> op, TT<MODE>* __restrict__ x,
-                                               TT<MODE>* __restrict__ r, const TT<MODE>* __restrict__ p,
-                                               const TT<MODE>* __restrict__ q,
-                                               const TT<MODE>* __restrict__ alpha,
-                                               const int* __restrict__ active, double omega,
-                                               TT<MODE>* __restrict__ z, int nb,
-                                               double* __restrict__ part) {
-  using T = TT<MODE>;
-  const size_t n = op.n;
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  const int b0 = blockIdx.y * BPT;
-  double v[BPT][2] = {};
-  if (i < n) {
-    typename Op<MODE>::Pre P;
-    op.pre(i, P);
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      if (!active[b]) continue;
-      const size_t j = (size_t)b * n + i;
-      const T al = alpha[b];
-      x[j] = x[j] + mul(al, p[j]);
-      const T rj = r[j] - mul(al, q[j]);
-      r[j] = rj;
-      v[k][0] += norm2(rj);
-      if (z) {
-        T a[7];
-        op.coef(P, b, i, a);
-        z[j] = omega * mul(rj, inv_of(a[0]));
-      }
-    }
-  }
-  block_partials<BPT>(v, part, b0, nb, gridDim.x);
-}
-
-// z_out = z_in + omega (b - A z_in)/a_C ; optional partial b^T z_out
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                               const TT<MODE>* __restrict__ zin,
-                                               TT<MODE>* __restrict__ zout,
-                                               const int* __restrict__ active, double omega, int nb,
-                                               int dot, double* __restrict__ part) {
-  using T = TT<MODE>;
-  const size_t n = op.n;
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  const int b0 = blockIdx.y * BPT;
-  double v[BPT][2] = {};
-  if (i < n) {
-    typename Op<MODE>::Pre P;
-    op.pre(i, P);
-    Nbr nbr;
-    neighbours(i, op.m, nbr);
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      if (!active[b]) continue;
-      const size_t o = (size_t)b * n;
-      T a[7];
-      op.coef(P, b, i, a);
-      const T res = bv[o + i] - apply7(a, zin + o, i, nbr);
-      const T zi = zin[o + i] + omega * mul(res, inv_of(a[0]));
-      zout[o + i] = zi;
-      if (dot) add_dot(v[k], bv[o + i], zi);
-    }
-  }
-  if (dot) block_partials<BPT>(v, part, b0, nb, gridDim.x);
-}
-
-// fine node (fx, fy) -> parents in the coarse node grid (mc per side), P1 weights.
+// fine node (fx, fy) -> coarse parents (mc per side), P1 weights.
 __device__ __forceinline__ int parents(int fx, int fy, int mc, int* cx, int* cy, double* w) {
   const int a = fx + 1, b = fy + 1;  // vertex coords on the fine lattice
   int np = 0;
@@ -302,140 +166,436 @@ __device__ __forceinline__ int parents(int fx, int fy, int mc, int* cx, int* cy,
       ++np;
     }
   };
+  const int ah = a >> 1, bh = b >> 1;
   const bool ao = a & 1, bo = b & 1;
-  if (!ao && !bo) add(a / 2, b / 2, 1.0);
-  else if (ao && !bo) { add(a / 2, b / 2, 0.5); add(a / 2 + 1, b / 2, 0.5); }
-  else if (!ao && bo) { add(a / 2, b / 2, 0.5); add(a / 2, b / 2 + 1, 0.5); }
-  else { add(a / 2, b / 2, 0.5); add(a / 2 + 1, b / 2 + 1, 0.5); }
+  if (!ao && !bo) add(ah, bh, 1.0);
+  else if (ao && !bo) { add(ah, bh, 0.5); add(ah + 1, bh, 0.5); }
+  else if (!ao && bo) { add(ah, bh, 0.5); add(ah, bh + 1, 0.5); }
+  else { add(ah, bh, 0.5); add(ah + 1, bh + 1, 0.5); }
   return np;
 }
 
-// bc = P^T (bf - Af zf) ; optionally zc = omega bc / ac_C (first coarse Jacobi sweep)
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_restrict(Op<MODE> opf, Op<MODE> opc,
-                                                 const TT<MODE>* __restrict__ bf,
-                                                 const TT<MODE>* __restrict__ zf,
-                                                 TT<MODE>* __restrict__ bc, TT<MODE>* __restrict__ zc,
-                                                 const int* __restrict__ active, double omega, int nb) {
+// next active batch of this block's group after `b` (uniform), or -1
+__device__ __forceinline__ int next_active(const int* __restrict__ active, int b, int nb, int BB) {
+  const int end = min(nb, (int)(blockIdx.z + 1) * BB);
+  for (int c = b + 1; c < end; ++c)
+    if (!active || active[c]) return c;
+  return -1;
+}
+
+#define TILE_PROLOGUE                                                 \
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;   \
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;               \
+  const int x = x0 + tx, y = y0 + ty;                                 \
+  const int m = op.m, n = op.n;                                       \
+  const bool in = (x < m) && (y < m);                                 \
+  const int i = in ? y * m + x : 0;                                   \
+  const int hk1 = tid + NT; /* second halo element of this thread */  \
+  const bool has1 = hk1 < HN;                                         \
+  (void)tid;                                                          \
+  (void)hk1;                                                          \
+  (void)has1;
+
+// halo element k -> node coords
+__device__ __forceinline__ void halo_xy(int k, int x0, int y0, int& xx, int& yy) {
+  const int ly = k / HX, lx = k - ly * HX;
+  xx = x0 - 1 + lx;
+  yy = y0 - 1 + ly;
+}
+__device__ __forceinline__ void halo_store(int k, cplx (*s)[HX], cplx v) { s[k / HX][k % HX] = v; }
+__device__ __forceinline__ void halo_store(int k, double (*s)[HX], double v) { s[k / HX][k % HX] = v; }
+
+// r = b - A x (warm) or r = b, x = 0 (cold); partials (||b||^2, ||r||^2).
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_init(Op<MODE> op, const TT<MODE>* __restrict__ bv,
+                                             TT<MODE>* __restrict__ x_, TT<MODE>* __restrict__ r,
+                                             int nb, int BB, int warm, double* __restrict__ part) {
   using T = TT<MODE>;
-  const size_t nc = opc.n, nf = opf.n;
-  const int mc = opc.m, mf = opf.m;
-  const size_t ic = (size_t)blockIdx.x * NT + threadIdx.x;
-  if (ic >= nc) return;
-  const int X = (int)(ic % mc), Y = (int)(ic / mc);
-  const int sox[7] = {0, -1, 1, 0, 0, -1, 1}, soy[7] = {0, 0, 0, -1, 1, -1, 1};
-  const double sw[7] = {1.0, 0.5, 0.5, 0.5, 0.5, 0.5, 0.5};
-  const int b0 = blockIdx.y * BPT;
-  T acc[BPT];
-#pragma unroll
-  for (int k = 0; k < BPT; ++k) acc[k] = zero_of(acc[0]);
-  for (int s = 0; s < 7; ++s) {
-    const int fx = 2 * X + 1 + sox[s], fy = 2 * Y + 1 + soy[s];
-    if (fx < 0 || fx >= mf || fy < 0 || fy >= mf) continue;
-    const size_t fi = (size_t)fy * mf + fx;
-    typename Op<MODE>::Pre P;
-    opf.pre(fi, P);
-    Nbr nbr;
-    neighbours(fi, mf, nbr);
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      if (!active[b]) continue;
-      T a[7];
-      opf.coef(P, b, fi, a);
-      const size_t o = (size_t)b * nf;
-      const T res = bf[o + fi] - apply7(a, zf + o, fi, nbr);
-      acc[k] = acc[k] + sw[s] * res;
+  __shared__ T s[HY][HX];
+  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  TILE_PROLOGUE
+  if constexpr (MODE == 0)
+    if (warm) stage_stencil(op, st_[0], i, in, tid);
+  for (int b = next_active(nullptr, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(nullptr, b, nb, BB)) {
+    const size_t o = (size_t)b * n;
+    if (warm) {
+      for (int k = tid; k < HN; k += NT) {
+        int xx, yy;
+        halo_xy(k, x0, y0, xx, yy);
+        halo_store(k, s, (xx >= 0 && xx < m && yy >= 0 && yy < m) ? x_[o + yy * m + xx] : zero_of(s[0][0]));
+      }
     }
-  }
-  typename Op<MODE>::Pre Pc;
-  if (zc) opc.pre(ic, Pc);
-#pragma unroll
-  for (int k = 0; k < BPT; ++k) {
-    const int b = b0 + k;
-    if (b >= nb) break;
-    if (!active[b]) continue;
-    bc[(size_t)b * nc + ic] = acc[k];
-    if (zc) {
-      T a[7];
-      opc.coef(Pc, b, ic, a);
-      zc[(size_t)b * nc + ic] = omega * mul(acc[k], inv_of(a[0]));
+    __syncthreads();
+    double v0 = 0, v1 = 0;
+    if (in) {
+      const T bi = bv[o + i];
+      T ri = bi;
+      if (warm) {
+        ri = bi - apply_tile(stencil_of<MODE>(op, st_, b, i, tid), s, tx, ty);
+      } else {
+        x_[o + i] = zero_of(bi);
+      }
+      r[o + i] = ri;
+      v0 = norm2(bi);
+      v1 = norm2(ri);
     }
+    block_pair(v0, v1, part, b);
+    __syncthreads();
   }
 }
 
-// zc = z_in + P xc (node and neighbours), z_out = zc + omega (b - A zc)/a_C
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_prolong_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_zero_flagged(Op<MODE> op, TT<MODE>* __restrict__ x_, int nb,
+                                                     int BB, const int* __restrict__ zero) {
+  TILE_PROLOGUE
+  if (!in) return;
+  for (int k = 0; k < BB; ++k) {
+    const int b = blockIdx.z * BB + k;
+    if (b >= nb) break;
+    if (zero[b]) x_[(size_t)b * n + i] = zero_of(x_[0]);
+  }
+}
+
+// p_out = first ? z : z + beta p_in ;  q = A p_out ; partial p^T q
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_apply_dot(Op<MODE> op, const TT<MODE>* __restrict__ z,
+                                                  const TT<MODE>* __restrict__ pin,
+                                                  TT<MODE>* __restrict__ pout, TT<MODE>* __restrict__ q,
+                                                  const TT<MODE>* __restrict__ beta,
+                                                  const int* __restrict__ active, int first, int nb,
+                                                  int BB, double* __restrict__ part) {
+  using T = TT<MODE>;
+  __shared__ T s[HY][HX];
+  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  TILE_PROLOGUE
+  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  // prefetch registers: z and p for the (<= 2) halo elements of this thread
+  T z0 = zero_of(T{}), p0 = zero_of(T{}), z1 = zero_of(T{}), p1 = zero_of(T{});
+  int xa, ya, xb, yb;
+  halo_xy(tid, x0, y0, xa, ya);
+  halo_xy(hk1, x0, y0, xb, yb);
+  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
+  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
+  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
+  auto fetch = [&](int b) {
+    const size_t o = (size_t)b * n;
+    if (va) { z0 = z[o + ia]; if (!first) p0 = pin[o + ia]; }
+    if (vb) { z1 = z[o + ib]; if (!first) p1 = pin[o + ib]; }
+  };
+  int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
+  if (b >= 0) fetch(b);
+  while (b >= 0) {
+    const int bn = next_active(active, b, nb, BB);
+    const T bt = first ? zero_of(T{}) : beta[b];
+    halo_store(tid, s, va ? (first ? z0 : z0 + mul(bt, p0)) : zero_of(T{}));
+    if (has1) halo_store(hk1, s, vb ? (first ? z1 : z1 + mul(bt, p1)) : zero_of(T{}));
+    __syncthreads();
+    if (bn >= 0) fetch(bn);
+    double v[2] = {0, 0};
+    if (in) {
+      const size_t o = (size_t)b * n;
+      const T pi = s[ty + 1][tx + 1];
+      const T qi = apply_tile(stencil_of<MODE>(op, st_, b, i, tid), s, tx, ty);
+      pout[o + i] = pi;
+      q[o + i] = qi;
+      add_dot(v, pi, qi);
+    }
+    block_pair(v[0], v[1], part, b);
+    __syncthreads();
+    b = bn;
+  }
+}
+
+// x += alpha p ; r -= alpha q ; partial ||r||^2 ; z = omega r / a_C
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_update(Op<MODE> op, TT<MODE>* __restrict__ x_,
+                                               TT<MODE>* __restrict__ r, const TT<MODE>* __restrict__ p,
+                                               const TT<MODE>* __restrict__ q,
+                                               const TT<MODE>* __restrict__ alpha,
+                                               const int* __restrict__ active, double omega,
+                                               TT<MODE>* __restrict__ z, int nb, int BB,
+                                               double* __restrict__ part) {
+  using T = TT<MODE>;
+  TILE_PROLOGUE
+  double kc = 0, mc = 0;
+  if constexpr (MODE == 0)
+    if (in && z) { kc = __ldg(op.K + i); mc = __ldg(op.M + i); }
+  for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
+    double v0 = 0;
+    if (in) {
+      const size_t j = (size_t)b * n + i;
+      const T al = alpha[b];
+      x_[j] = x_[j] + mul(al, p[j]);
+      const T rj = r[j] - mul(al, q[j]);
+      r[j] = rj;
+      v0 = norm2(rj);
+      if (z) {
+        T d;
+        if constexpr (MODE == 0) { const cplx l = op.lam[b]; d = cplx{fma(l.re, mc, kc), l.im * mc}; }
+        else d = __ldg(op.J + (size_t)b * 7 * n + i);
+        z[j] = omega * mul(rj, inv_of(d));
+      }
+    }
+    block_pair(v0, 0.0, part, b);
+    __syncthreads();
+  }
+}
+
+// z = omega b / a_C (first Jacobi sweep from zero)
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_jacobi0(Op<MODE> op, const TT<MODE>* __restrict__ bv,
+                                                TT<MODE>* __restrict__ z, const int* __restrict__ active,
+                                                double omega, int nb, int BB) {
+  using T = TT<MODE>;
+  TILE_PROLOGUE
+  if (!in) return;
+  double kc = 0, mc = 0;
+  if constexpr (MODE == 0) { kc = __ldg(op.K + i); mc = __ldg(op.M + i); }
+  for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
+    const size_t j = (size_t)b * n + i;
+    T d;
+    if constexpr (MODE == 0) { const cplx l = op.lam[b]; d = cplx{fma(l.re, mc, kc), l.im * mc}; }
+    else d = __ldg(op.J + (size_t)b * 7 * n + i);
+    z[j] = omega * mul(bv[j], inv_of(d));
+  }
+}
+
+// z_out = z_in + omega (b - A z_in)/a_C ; optional partial b^T z_out
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
+                                               const TT<MODE>* __restrict__ zin,
+                                               TT<MODE>* __restrict__ zout,
+                                               const int* __restrict__ active, double omega, int nb,
+                                               int BB, int dot, double* __restrict__ part) {
+  using T = TT<MODE>;
+  __shared__ T s[HY][HX];
+  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  TILE_PROLOGUE
+  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
+  int xa, ya, xb, yb;
+  halo_xy(tid, x0, y0, xa, ya);
+  halo_xy(hk1, x0, y0, xb, yb);
+  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
+  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
+  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
+  auto fetch = [&](int b) {
+    const size_t o = (size_t)b * n;
+    if (va) z0 = zin[o + ia];
+    if (vb) z1 = zin[o + ib];
+    if (in) bo = bv[o + i];
+  };
+  int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
+  if (b >= 0) fetch(b);
+  while (b >= 0) {
+    const int bn = next_active(active, b, nb, BB);
+    halo_store(tid, s, va ? z0 : zero_of(T{}));
+    if (has1) halo_store(hk1, s, vb ? z1 : zero_of(T{}));
+    const T bi = bo;
+    __syncthreads();
+    if (bn >= 0) fetch(bn);
+    double v[2] = {0, 0};
+    if (in) {
+      const auto a = stencil_of<MODE>(op, st_, b, i, tid);
+      const T zi = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx, ty), inv_of(a(0)));
+      zout[(size_t)b * n + i] = zi;
+      if (dot) add_dot(v, bi, zi);
+    }
+    if (dot) block_pair(v[0], v[1], part, b);
+    __syncthreads();
+    b = bn;
+  }
+}
+
+// Fine tile 32x8 -> coarse 16x4: bc = P^T (bf - Af zf); optional first coarse
+// Jacobi sweep zc = omega bc / ac_C.
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_restrict(Op<MODE> op, Op<MODE> opc,
+                                                 const TT<MODE>* __restrict__ bf,
+                                                 const TT<MODE>* __restrict__ zf,
+                                                 TT<MODE>* __restrict__ bc, TT<MODE>* __restrict__ zc,
+                                                 const int* __restrict__ active, double omega, int nb,
+                                                 int BB) {
+  using T = TT<MODE>;
+  __shared__ T s[HY][HX];
+  __shared__ T res[TY + 1][TX + 1];
+  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  TILE_PROLOGUE
+  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  // extra residual nodes: column x0+TX (rows 0..TY-1), row y0+TY (cols 0..TX)
+  int ex = -1, ey = -1;
+  if (tid < TY) { ex = TX; ey = tid; }
+  else if (tid < TY + TX + 1) { ex = tid - TY; ey = TY; }
+  const int gx = x0 + ex, gy = y0 + ey;
+  const bool ein = ex >= 0 && gx < m && gy < m;
+  const int ei = ein ? gy * m + gx : 0;
+  // coarse node of this thread (first 64 threads)
+  const int mcs = opc.m, nc = opc.n;
+  const int cxl = tid & 15, cyl = tid >> 4;
+  const int X = (x0 >> 1) + cxl, Y = (y0 >> 1) + cyl;
+  const bool cin = tid < 64 && X < mcs && Y < mcs;
+  const int ci = cin ? Y * mcs + X : 0;
+  double ckc = 0, cmc = 0;
+  if constexpr (MODE == 0)
+    if (cin && zc) { ckc = __ldg(opc.K + ci); cmc = __ldg(opc.M + ci); }
+  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
+  int xa, ya, xb, yb;
+  halo_xy(tid, x0, y0, xa, ya);
+  halo_xy(hk1, x0, y0, xb, yb);
+  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
+  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
+  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
+  auto fetch = [&](int b) {
+    const size_t o = (size_t)b * n;
+    if (va) z0 = zf[o + ia];
+    if (vb) z1 = zf[o + ib];
+    if (in) bo = bf[o + i];
+  };
+  int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
+  if (b >= 0) fetch(b);
+  while (b >= 0) {
+    const int bn = next_active(active, b, nb, BB);
+    halo_store(tid, s, va ? z0 : zero_of(T{}));
+    if (has1) halo_store(hk1, s, vb ? z1 : zero_of(T{}));
+    const T bi = bo;
+    __syncthreads();
+    if (bn >= 0) fetch(bn);
+    const size_t o = (size_t)b * n;
+    res[ty][tx] = in ? bi - apply_tile(stencil_of<MODE>(op, st_, b, i, tid), s, tx, ty) : zero_of(T{});
+    if (ex >= 0) {
+      T rr = zero_of(T{});
+      if (ein) {
+        T a[7];
+        if constexpr (MODE == 0) {
+          const cplx l = op.lam[b];
+          for (int d = 0; d < 7; ++d) {
+            const double mm = __ldg(op.M + (size_t)d * n + ei);
+            a[d] = cplx{fma(l.re, mm, __ldg(op.K + (size_t)d * n + ei)), l.im * mm};
+          }
+        } else {
+          for (int d = 0; d < 7; ++d) a[d] = __ldg(op.J + (size_t)b * 7 * n + (size_t)d * n + ei);
+        }
+        const T* zz = zf + o;
+        T acc = mul(a[0], zz[ei]);
+        if (gx > 0) acc = acc + mul(a[1], zz[ei - 1]);
+        if (gx < m - 1) acc = acc + mul(a[2], zz[ei + 1]);
+        if (gy > 0) acc = acc + mul(a[3], zz[ei - m]);
+        if (gy < m - 1) acc = acc + mul(a[4], zz[ei + m]);
+        if (gx > 0 && gy > 0) acc = acc + mul(a[5], zz[ei - m - 1]);
+        if (gx < m - 1 && gy < m - 1) acc = acc + mul(a[6], zz[ei + m + 1]);
+        rr = bf[o + ei] - acc;
+      }
+      res[ey][ex] = rr;
+    }
+    __syncthreads();
+    if (cin) {
+      const int fx = 2 * cxl + 1, fy = 2 * cyl + 1;  // local fine centre
+      const T side = res[fy][fx - 1] + res[fy][fx + 1] + res[fy - 1][fx] + res[fy + 1][fx] +
+                     res[fy - 1][fx - 1] + res[fy + 1][fx + 1];
+      const T acc = res[fy][fx] + 0.5 * side;
+      const size_t oc = (size_t)b * nc;
+      bc[oc + ci] = acc;
+      if (zc) {
+        T d;
+        if constexpr (MODE == 0) { const cplx l = opc.lam[b]; d = cplx{fma(l.re, cmc, ckc), l.im * cmc}; }
+        else d = __ldg(opc.J + (size_t)b * 7 * nc + ci);
+        zc[oc + ci] = omega * mul(acc, inv_of(d));
+      }
+    }
+    __syncthreads();
+    b = bn;
+  }
+}
+
+// zc = z_in + P xc on the tile + halo (shared), then z_out = zc + omega (b - A zc)/a_C
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_prolong_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
                                                        const TT<MODE>* __restrict__ zin,
                                                        const TT<MODE>* __restrict__ xc, int mc,
                                                        TT<MODE>* __restrict__ zout,
                                                        const int* __restrict__ active, double omega,
-                                                       int nb, int dot, double* __restrict__ part) {
+                                                       int nb, int BB, int dot, double* __restrict__ part) {
   using T = TT<MODE>;
-  const size_t n = op.n;
-  const size_t ncs = (size_t)mc * mc;
-  const int m = op.m;
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  const int b0 = blockIdx.y * BPT;
-  double v[BPT][2] = {};
-  if (i < n) {
-    typename Op<MODE>::Pre P;
-    op.pre(i, P);
-    Nbr nbr;
-    neighbours(i, m, nbr);
-    const int x = (int)(i % m), y = (int)(i / m);
-    // parents of the node and its neighbours
-    int pcx[7][2], pcy[7][2], np[7];
-    double pw[7][2];
-    for (int d = 0; d < 7; ++d) {
-      np[d] = 0;
-      if (!nbr.ok[d]) continue;
-      np[d] = parents(x + dir_dx(d), y + dir_dy(d), mc, pcx[d], pcy[d], pw[d]);
+  __shared__ T s[HY][HX];
+  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  TILE_PROLOGUE
+  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  const int nc = mc * mc;
+  int xa, ya, xb, yb;
+  halo_xy(tid, x0, y0, xa, ya);
+  halo_xy(hk1, x0, y0, xb, yb);
+  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
+  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
+  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
+  // coarse parents of the two halo elements: linear coarse index, first weight
+  // (1 or 1/2; a second parent, if any, always weighs 1/2)
+  int pa0 = -1, pa1 = -1, pb0 = -1, pb1 = -1;
+  double wa = 0, wb = 0;
+  {
+    int cx[2], cy[2];
+    double w[2];
+    if (va) {
+      const int np = parents(xa, ya, mc, cx, cy, w);
+      if (np > 0) { pa0 = cy[0] * mc + cx[0]; wa = w[0]; }
+      if (np > 1) pa1 = cy[1] * mc + cx[1];
     }
-#pragma unroll
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      if (!active[b]) continue;
-      const size_t o = (size_t)b * n, oc = (size_t)b * ncs;
-      T a[7];
-      op.coef(P, b, i, a);
-      T Az = zero_of(a[0]), zi = zero_of(a[0]);
-#pragma unroll
-      for (int d = 0; d < 7; ++d) {
-        if (!nbr.ok[d]) continue;
-        T zj = zin[o + i + nbr.off[d]];
-        for (int t = 0; t < np[d]; ++t) zj = zj + pw[d][t] * xc[oc + (size_t)pcy[d][t] * mc + pcx[d][t]];
-        if (d == 0) zi = zj;
-        Az = Az + mul(a[d], zj);
-      }
-      const T bi = bv[o + i];
-      const T zo = zi + omega * mul(bi - Az, inv_of(a[0]));
-      zout[o + i] = zo;
-      if (dot) add_dot(v[k], bi, zo);
+    if (vb) {
+      const int np = parents(xb, yb, mc, cx, cy, w);
+      if (np > 0) { pb0 = cy[0] * mc + cx[0]; wb = w[0]; }
+      if (np > 1) pb1 = cy[1] * mc + cx[1];
     }
   }
-  if (dot) block_partials<BPT>(v, part, b0, nb, gridDim.x);
+  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
+  auto fetch = [&](int b) {
+    const size_t o = (size_t)b * n, oc = (size_t)b * nc;
+    if (va) {
+      T v = zin[o + ia];
+      if (pa0 >= 0) v = v + wa * xc[oc + pa0];
+      if (pa1 >= 0) v = v + 0.5 * xc[oc + pa1];
+      z0 = v;
+    }
+    if (vb) {
+      T v = zin[o + ib];
+      if (pb0 >= 0) v = v + wb * xc[oc + pb0];
+      if (pb1 >= 0) v = v + 0.5 * xc[oc + pb1];
+      z1 = v;
+    }
+    if (in) bo = bv[o + i];
+  };
+  int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
+  if (b >= 0) fetch(b);
+  while (b >= 0) {
+    const int bn = next_active(active, b, nb, BB);
+    halo_store(tid, s, va ? z0 : zero_of(T{}));
+    if (has1) halo_store(hk1, s, vb ? z1 : zero_of(T{}));
+    const T bi = bo;
+    __syncthreads();
+    if (bn >= 0) fetch(bn);
+    double v[2] = {0, 0};
+    if (in) {
+      const auto a = stencil_of<MODE>(op, st_, b, i, tid);
+      const T zo = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx, ty), inv_of(a(0)));
+      zout[(size_t)b * n + i] = zo;
+      if (dot) add_dot(v, bi, zo);
+    }
+    if (dot) block_pair(v[0], v[1], part, b);
+    __syncthreads();
+    b = bn;
+  }
 }
 
 // partial b^T z
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_dot(const TT<MODE>* __restrict__ a, const TT<MODE>* __restrict__ z,
-                                            size_t n, const int* __restrict__ active, int nb,
-                                            double* __restrict__ part) {
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  const int b0 = blockIdx.y * BPT;
-  double v[BPT][2] = {};
-  if (i < n)
-    for (int k = 0; k < BPT; ++k) {
-      const int b = b0 + k;
-      if (b >= nb) break;
-      if (!active[b]) continue;
-      add_dot(v[k], a[(size_t)b * n + i], z[(size_t)b * n + i]);
-    }
-  block_partials<BPT>(v, part, b0, nb, gridDim.x);
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_dot(Op<MODE> op, const TT<MODE>* __restrict__ a_,
+                                            const TT<MODE>* __restrict__ z, const int* __restrict__ active,
+                                            int nb, int BB, double* __restrict__ part) {
+  TILE_PROLOGUE
+  for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
+    double v[2] = {0, 0};
+    if (in) add_dot(v, a_[(size_t)b * n + i], z[(size_t)b * n + i]);
+    block_pair(v[0], v[1], part, b);
+    __syncthreads();
+  }
 }
 
 // dense coarsest solve x = inv b, one block per batch
@@ -666,17 +826,33 @@ void launch_coarse_inverse_slice(Problem& p, const double* J, int m, double* inv
 // ---------------------------------------------------------------- solver
 
 template <int MODE>
-static constexpr int bpt() { return MODE == 0 ? 4 : 1; }
-
-template <int MODE>
 static Op<MODE> make_op(const LevelOp& L, const cplx* lam);
 template <>
 Op<0> make_op<0>(const LevelOp& L, const cplx* lam) {
-  return Op<0>{L.K, L.M, lam, (size_t)L.n, L.m};
+  return Op<0>{L.K, L.M, lam, L.n, L.m};
 }
 template <>
 Op<1> make_op<1>(const LevelOp& L, const cplx*) {
-  return Op<1>{L.K, (size_t)L.n, L.m};
+  return Op<1>{L.K, L.n, L.m};
+}
+
+// launch geometry for a level: 32x8 node tiles x batch groups of BB
+struct Geo {
+  dim3 grid;
+  int BB;
+  int tiles;
+};
+
+static Geo geo_for(int m, int nb, int num_sms, int max_bb) {
+  Geo g;
+  const int gx = (m + TX - 1) / TX, gy = (m + TY - 1) / TY;
+  g.tiles = gx * gy;
+  // enough blocks to fill the machine ~4x, then batch loop inside a block
+  int bb = (int)std::max<long>(1, (long)g.tiles * nb / (4L * num_sms));
+  bb = std::min(bb, max_bb);
+  g.BB = bb;
+  g.grid = dim3(gx, gy, (nb + bb - 1) / bb);
+  return g;
 }
 
 template <int MODE>
@@ -701,8 +877,8 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   p0.alloc(n0);
   p1.alloc(n0);
   q.alloc(n0);
-  const size_t per = (levels[0].n + NT - 1) / NT;
-  part.alloc((size_t)B * per * 2 + 64);
+  const size_t tiles = (size_t)((levels[0].m + TX - 1) / TX) * ((levels[0].m + TY - 1) / TY);
+  part.alloc((size_t)B * tiles * 2 + 64);
   rho.alloc(B);
   mu.alloc(B);
   alpha.alloc(B);
@@ -723,77 +899,52 @@ BatchSolver<MODE>::~BatchSolver() {
     if (e) cudaEventDestroy(e);
 }
 
-namespace {
-template <int MODE, int BPT>
-__global__ void __launch_bounds__(NT) k_jacobi0(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                                TT<MODE>* __restrict__ z, const int* __restrict__ active,
-                                                double omega, int nb) {
-  using T = TT<MODE>;
-  const size_t n = op.n;
-  const size_t i = (size_t)blockIdx.x * NT + threadIdx.x;
-  if (i >= n) return;
-  typename Op<MODE>::Pre P;
-  op.pre(i, P);
-  for (int k = 0; k < BPT; ++k) {
-    const int b = blockIdx.y * BPT + k;
-    if (b >= nb) break;
-    if (!active[b]) continue;
-    T a[7];
-    op.coef(P, b, i, a);
-    z[(size_t)b * n + i] = omega * mul(bv[(size_t)b * n + i], inv_of(a[0]));
-  }
-}
-}  // namespace
-
 template <int MODE>
-typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, const T* bl, T* /*unused*/,
-                                                              bool /*unused*/, bool dot) {
-  constexpr int K = bpt<MODE>();
+typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, const T* bl, T*, bool,
+                                                              bool dot) {
   const int L = (int)ops.size();
   const Op<MODE> op = make_op<MODE>(ops[l], lam);
-  const size_t n = ops[l].n;
-  dim3 g((unsigned)((n + NT - 1) / NT), (unsigned)((nb + K - 1) / K));
+  const Geo g = geo_for(ops[l].m, nb, p->num_sms, 8);
   int* act = active.get();
+  cudaStream_t s = p->stream;
   if (L == 1) {
-    k_coarse_solve<T><<<nb, 64, 0, p->stream>>>(coarse_inv, bl, lz0[0].get(), ops[0].n, act);
+    k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, bl, lz0[0].get(), ops[0].n, act);
     TP_LAUNCHED(p);
     if (dot) {
-      k_dot<MODE, K><<<g, NT, 0, p->stream>>>(bl, lz0[0].get(), n, act, nb, part.get());
+      k_dot<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, lz0[0].get(), act, nb, g.BB, part.get());
       TP_LAUNCHED(p);
     }
     return lz0[0].get();
   }
   T* z = lz0[l].get();
   T* o = lz1[l].get();
-  for (int s = 1; s < cfg.pre; ++s) {
-    k_smooth<MODE, K><<<g, NT, 0, p->stream>>>(op, bl, z, o, act, cfg.omega, nb, 0, part.get());
+  for (int k = 1; k < cfg.pre; ++k) {
+    k_smooth<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, 0, part.get());
     TP_LAUNCHED(p);
     std::swap(z, o);
   }
   const bool coarse_next = (l + 1 == L - 1);
   const Op<MODE> opc = make_op<MODE>(ops[l + 1], lam);
-  const size_t nc = ops[l + 1].n;
-  dim3 gc((unsigned)((nc + NT - 1) / NT), (unsigned)((nb + K - 1) / K));
-  k_restrict<MODE, K><<<gc, NT, 0, p->stream>>>(op, opc, bl, z, lb[l + 1].get(),
-                                                 coarse_next ? nullptr : lz0[l + 1].get(), act,
-                                                 cfg.omega, nb);
+  k_restrict<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, opc, bl, z, lb[l + 1].get(),
+                                                   coarse_next ? nullptr : lz0[l + 1].get(), act,
+                                                   cfg.omega, nb, g.BB);
   TP_LAUNCHED(p);
   T* xc;
   if (coarse_next) {
-    k_coarse_solve<T><<<nb, 64, 0, p->stream>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(),
-                                                ops[l + 1].n, act);
+    k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
     TP_LAUNCHED(p);
     xc = lz0[l + 1].get();
   } else {
     xc = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
   }
-  k_prolong_smooth<MODE, K><<<g, NT, 0, p->stream>>>(op, bl, z, xc, ops[l + 1].m, o, act, cfg.omega,
-                                                     nb, (dot && cfg.post == 1) ? 1 : 0, part.get());
+  k_prolong_smooth<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, z, xc, ops[l + 1].m, o, act, cfg.omega,
+                                                         nb, g.BB, (dot && cfg.post == 1) ? 1 : 0,
+                                                         part.get());
   TP_LAUNCHED(p);
   std::swap(z, o);
-  for (int s = 1; s < cfg.post; ++s) {
-    const int d = (dot && s == cfg.post - 1) ? 1 : 0;
-    k_smooth<MODE, K><<<g, NT, 0, p->stream>>>(op, bl, z, o, act, cfg.omega, nb, d, part.get());
+  for (int k = 1; k < cfg.post; ++k) {
+    const int d = (dot && k == cfg.post - 1) ? 1 : 0;
+    k_smooth<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, d, part.get());
     TP_LAUNCHED(p);
     std::swap(z, o);
   }
@@ -802,23 +953,22 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
 
 template <int MODE>
 int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st) {
-  constexpr int K = bpt<MODE>();
   require(nb <= B, "batch solver: too many right-hand sides");
   const Op<MODE> op0 = make_op<MODE>(ops[0], lam);
-  const size_t n0 = ops[0].n;
-  dim3 g0((unsigned)((n0 + NT - 1) / NT), (unsigned)((nb + K - 1) / K));
-  const int per0 = (int)g0.x;
+  const Geo g0 = geo_for(ops[0].m, nb, p->num_sms, 8);
+  const dim3 blk(TX, TY);
+  const int per0 = g0.tiles;
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
   cudaStream_t s = p->stream;
-  k_init<MODE, K><<<g0, NT, 0, s>>>(op0, b, x, r.get(), nb, warm ? 1 : 0, part.get());
+  k_init<MODE><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get());
   TP_LAUNCHED(p);
-  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
-                                  alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
+  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), per0, nb, rtol2, rho.get(), mu.get(), alpha.get(),
+                                  beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
   TP_LAUNCHED(p);
   if (warm) {
-    k_zero_flagged<MODE, K><<<g0, NT, 0, s>>>(x, n0, nb, zero);
+    k_zero_flagged<MODE><<<g0.grid, blk, 0, s>>>(op0, x, nb, g0.BB, zero);
     TP_LAUNCHED(p);
   }
   k_count_active<<<1, 256, 0, s>>>(act, nb, count.get());
@@ -829,7 +979,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int64_t batch_iters = 0;
   int last_active = h_count[0];
   if (last_active > 0) {
-    k_jacobi0<MODE, K><<<g0, NT, 0, s>>>(op0, r.get(), lz0[0].get(), act, cfg.omega, nb);
+    k_jacobi0<MODE><<<g0.grid, blk, 0, s>>>(op0, r.get(), lz0[0].get(), act, cfg.omega, nb, g0.BB);
     TP_LAUNCHED(p);
     T* z = vcycle_level(0, nb, r.get(), nullptr, false, true);
     k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
@@ -839,15 +989,15 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     T* pout = p1.get();
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
-      k_apply_dot<MODE, K><<<g0, NT, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
-                                             it == 1 ? 1 : 0, nb, part.get());
+      k_apply_dot<MODE><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
+                                                it == 1 ? 1 : 0, nb, g0.BB, part.get());
       TP_LAUNCHED(p);
       k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
       TP_LAUNCHED(p);
-      k_update<MODE, K><<<g0, NT, 0, s>>>(op0, x, r.get(), pout, q.get(), alpha.get(), act,
-                                          cfg.omega, ops.size() > 1 ? lz0[0].get() : nullptr, nb,
-                                          part.get());
+      k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, r.get(), pout, q.get(), alpha.get(), act, cfg.omega,
+                                             ops.size() > 1 ? lz0[0].get() : nullptr, nb, g0.BB,
+                                             part.get());
       TP_LAUNCHED(p);
       k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
@@ -863,7 +1013,6 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         last_active = h_count[slot ^ 1];
         if (last_active == 0) {
           iters = it - 1;
-          batch_iters -= 0;
           done = true;
           break;
         }
