@@ -1,16 +1,19 @@
 // Batched multigrid-preconditioned CG/COCG -- see mg.cuh.
 //
 // Kernel layout: a block owns a 32x8 tile of nodes of one level and walks the
-// active batches (frequencies or slices) of its batch group.  In frequency
-// mode the tile's shared real stencils (K, M: 14 doubles per node) are staged
-// once per block in shared memory and combined with lambda_b on the fly, so
-// the operator costs no HBM traffic per batch and few registers.  Vector
-// tiles (+1 halo) are staged in shared memory and the next batch's tile is
-// prefetched into registers while the current one is computed (two batches
-// of loads in flight per block).  Restriction forms the fine residual tile in
-// shared memory and gathers P^T from it; prolongation interpolates the coarse
-// correction into the shared tile before smoothing.  32-bit node indices
-// within a level, 64-bit batch offsets.
+// active batches (frequencies or slices) of its batch group.  Vector tiles
+// (+1 halo) are staged in shared memory (16-byte complex accesses) and the
+// next batch's tile is prefetched into registers while the current one is
+// computed.  Stencil families:
+//   FAM 1  fine level, frequency mode: K_hat is 5-point and M is the lumped
+//          diagonal, so a thread keeps its 5 + 1 real coefficients in
+//          registers and the off-diagonal products are real x complex;
+//   FAM 0  coarse levels, frequency mode: Galerkin 7-point K and M shared by
+//          all frequencies, staged once per block in shared memory;
+//   FAM 2  slice mode (Newton): per-batch 7-point J from global memory.
+// Restriction forms the fine residual tile in shared memory and gathers P^T
+// from it; prolongation interpolates the coarse correction while staging the
+// tile.  32-bit node indices within a level, 64-bit batch offsets.
 //
 // Per fine node and batch (16 B complex) one Krylov iteration streams:
 // apply+dot (read z, p; write p, q), update (read x, p, r, q; write x, r, z),
@@ -28,6 +31,7 @@ namespace {
 
 constexpr int TX = 32, TY = 8, NT = TX * TY;
 constexpr int HX = TX + 2, HY = TY + 2, HN = HX * HY;  // halo tile: 340 values
+constexpr int RX = TX + 3, RY = TY + 3, RN = RX * RY;  // restriction tile: 385 values
 
 template <int MODE>
 using TT = typename std::conditional<MODE == 0, cplx, double>::type;
@@ -49,12 +53,12 @@ __device__ __forceinline__ cplx inv_of(cplx a) {
   return {a.re * d, -a.im * d};
 }
 __device__ __forceinline__ double inv_of(double a) { return 1.0 / a; }
+__device__ __forceinline__ cplx axpy_r(double k, cplx v, cplx acc) { return {fma(k, v.re, acc.re), fma(k, v.im, acc.im)}; }
 
 // Level operator.  MODE 0: lambda_b M + K with shared stencils; MODE 1:
 // per-batch stencil J_b.
 template <int MODE>
 struct Op;
-
 template <>
 struct Op<0> {
   const double* K;
@@ -62,70 +66,141 @@ struct Op<0> {
   const cplx* lam;
   int n, m;
 };
-
 template <>
 struct Op<1> {
   const double* J;
   int n, m;
 };
 
-// Per-block stencil staging (frequency mode): st[d][tid] (K), st[7+d][tid] (M).
+// ---- stencil coefficient families
 struct StageF {
   double v[14][NT];
 };
 
-template <int MODE>
-struct Stencil;
-
-template <>
-struct Stencil<0> {
+struct CoefStaged {  // FAM 0
   const StageF* s;
   cplx l;
   int tid;
-  __device__ __forceinline__ cplx operator()(int d) const {
+  __device__ __forceinline__ cplx c(int d) const {
     const double mm = s->v[7 + d][tid];
     return {fma(l.re, mm, s->v[d][tid]), l.im * mm};
   }
+  __device__ __forceinline__ cplx diag() const { return c(0); }
 };
 
-template <>
-struct Stencil<1> {
-  const double* J;  // batch stencil base
+struct FineRegs {  // FAM 1 per-thread data
+  double k0, kw, ke, ks, kn, m0;
+};
+
+struct CoefFine {
+  FineRegs r;
+  cplx l;
+  __device__ __forceinline__ cplx diag() const { return {fma(l.re, r.m0, r.k0), l.im * r.m0}; }
+};
+
+struct CoefSlice {  // FAM 2
+  const double* J;
   int n, i;
-  __device__ __forceinline__ double operator()(int d) const { return __ldg(J + (size_t)d * n + i); }
+  __device__ __forceinline__ double c(int d) const { return __ldg(J + (size_t)d * n + i); }
+  __device__ __forceinline__ double diag() const { return c(0); }
 };
 
-__device__ __forceinline__ void stage_stencil(const Op<0>& op, StageF& st, int i, bool in, int tid) {
+template <class T, int W>
+__device__ __forceinline__ T apply_tile(const CoefStaged& a, const T (*s)[W], int lx, int ly) {
+  T acc = mul(a.c(0), s[ly][lx]);
+  acc = acc + mul(a.c(1), s[ly][lx - 1]);
+  acc = acc + mul(a.c(2), s[ly][lx + 1]);
+  acc = acc + mul(a.c(3), s[ly - 1][lx]);
+  acc = acc + mul(a.c(4), s[ly + 1][lx]);
+  acc = acc + mul(a.c(5), s[ly - 1][lx - 1]);
+  acc = acc + mul(a.c(6), s[ly + 1][lx + 1]);
+  return acc;
+}
+template <int W>
+__device__ __forceinline__ cplx apply_tile(const CoefFine& a, const cplx (*s)[W], int lx, int ly) {
+  cplx acc = mul(a.diag(), s[ly][lx]);
+  acc = axpy_r(a.r.kw, s[ly][lx - 1], acc);
+  acc = axpy_r(a.r.ke, s[ly][lx + 1], acc);
+  acc = axpy_r(a.r.ks, s[ly - 1][lx], acc);
+  acc = axpy_r(a.r.kn, s[ly + 1][lx], acc);
+  return acc;
+}
+template <class T, int W>
+__device__ __forceinline__ T apply_tile(const CoefSlice& a, const T (*s)[W], int lx, int ly) {
+  T acc = a.c(0) * s[ly][lx];
+  acc = acc + a.c(1) * s[ly][lx - 1];
+  acc = acc + a.c(2) * s[ly][lx + 1];
+  acc = acc + a.c(3) * s[ly - 1][lx];
+  acc = acc + a.c(4) * s[ly + 1][lx];
+  acc = acc + a.c(5) * s[ly - 1][lx - 1];
+  acc = acc + a.c(6) * s[ly + 1][lx + 1];
+  return acc;
+}
+
+// Per-kernel coefficient context
+template <int MODE, int FAM>
+struct Ctx;
+template <>
+struct Ctx<0, 0> {
+  StageF* st;
+  __device__ void init(const Op<0>& op, int i, bool in, int tid) {
 #pragma unroll
-  for (int d = 0; d < 7; ++d) {
-    st.v[d][tid] = in ? __ldg(op.K + (size_t)d * op.n + i) : 0.0;
-    st.v[7 + d][tid] = in ? __ldg(op.M + (size_t)d * op.n + i) : 0.0;
+    for (int d = 0; d < 7; ++d) {
+      st->v[d][tid] = in ? __ldg(op.K + (size_t)d * op.n + i) : 0.0;
+      st->v[7 + d][tid] = in ? __ldg(op.M + (size_t)d * op.n + i) : 0.0;
+    }
   }
+  __device__ CoefStaged at(const Op<0>& op, int b, int, int tid) const { return {st, op.lam[b], tid}; }
+};
+template <>
+struct Ctx<0, 1> {
+  FineRegs r;
+  __device__ void init(const Op<0>& op, int i, bool in, int) {
+    if (in) {
+      const size_t n = op.n;
+      r = {__ldg(op.K + i), __ldg(op.K + n + i), __ldg(op.K + 2 * n + i), __ldg(op.K + 3 * n + i),
+           __ldg(op.K + 4 * n + i), __ldg(op.M + i)};
+    } else {
+      r = {1, 0, 0, 0, 0, 0};
+    }
+  }
+  __device__ CoefFine at(const Op<0>& op, int b, int, int) const { return {r, op.lam[b]}; }
+};
+template <>
+struct Ctx<1, 2> {
+  __device__ void init(const Op<1>&, int, bool, int) {}
+  __device__ CoefSlice at(const Op<1>& op, int b, int i, int) const {
+    return {op.J + (size_t)b * 7 * op.n, op.n, i};
+  }
+};
+
+// coefficients of an arbitrary node (restriction extras): full 7-point
+template <int MODE>
+__device__ __forceinline__ void coef_global(const Op<MODE>& op, int b, int i, TT<MODE> a[7]);
+template <>
+__device__ __forceinline__ void coef_global<0>(const Op<0>& op, int b, int i, cplx a[7]) {
+  const cplx l = op.lam[b];
+  for (int d = 0; d < 7; ++d) {
+    const double mm = __ldg(op.M + (size_t)d * op.n + i);
+    a[d] = cplx{fma(l.re, mm, __ldg(op.K + (size_t)d * op.n + i)), l.im * mm};
+  }
+}
+template <>
+__device__ __forceinline__ void coef_global<1>(const Op<1>& op, int b, int i, double a[7]) {
+  for (int d = 0; d < 7; ++d) a[d] = __ldg(op.J + (size_t)b * 7 * op.n + (size_t)d * op.n + i);
 }
 
 template <int MODE>
-__device__ __forceinline__ Stencil<MODE> stencil_of(const Op<MODE>& op, const StageF* st, int b, int i, int tid);
+__device__ __forceinline__ TT<MODE> diag_global(const Op<MODE>& op, int b, int i);
 template <>
-__device__ __forceinline__ Stencil<0> stencil_of<0>(const Op<0>& op, const StageF* st, int b, int, int tid) {
-  return Stencil<0>{st, op.lam[b], tid};
+__device__ __forceinline__ cplx diag_global<0>(const Op<0>& op, int b, int i) {
+  const cplx l = op.lam[b];
+  const double mm = __ldg(op.M + i);
+  return {fma(l.re, mm, __ldg(op.K + i)), l.im * mm};
 }
 template <>
-__device__ __forceinline__ Stencil<1> stencil_of<1>(const Op<1>& op, const StageF*, int b, int i, int) {
-  return Stencil<1>{op.J + (size_t)b * 7 * op.n, op.n, i};
-}
-
-// 7-point application from the halo tile
-template <class T, class S>
-__device__ __forceinline__ T apply_tile(const S& a, const T (*s)[HX], int tx, int ty) {
-  const int lx = tx + 1, ly = ty + 1;
-  T acc = mul(a(0), s[ly][lx]);
-  acc = acc + mul(a(1), s[ly][lx - 1]);
-  acc = acc + mul(a(2), s[ly][lx + 1]);
-  acc = acc + mul(a(3), s[ly - 1][lx]);
-  acc = acc + mul(a(4), s[ly + 1][lx]);
-  acc = acc + mul(a(5), s[ly - 1][lx - 1]);
-  acc = acc + mul(a(6), s[ly + 1][lx + 1]);
-  return acc;
+__device__ __forceinline__ double diag_global<1>(const Op<1>& op, int b, int i) {
+  return __ldg(op.J + (size_t)b * 7 * op.n + i);
 }
 
 // Block-wide reduction of one batch's pair into part[(b*tiles + tile)*2 + c].
@@ -190,51 +265,56 @@ __device__ __forceinline__ int next_active(const int* __restrict__ active, int b
   const int m = op.m, n = op.n;                                       \
   const bool in = (x < m) && (y < m);                                 \
   const int i = in ? y * m + x : 0;                                   \
-  const int hk1 = tid + NT; /* second halo element of this thread */  \
-  const bool has1 = hk1 < HN;                                         \
-  (void)tid;                                                          \
-  (void)hk1;                                                          \
-  (void)has1;
+  (void)tid;
 
-// halo element k -> node coords
-__device__ __forceinline__ void halo_xy(int k, int x0, int y0, int& xx, int& yy) {
-  const int ly = k / HX, lx = k - ly * HX;
-  xx = x0 - 1 + lx;
-  yy = y0 - 1 + ly;
-}
-__device__ __forceinline__ void halo_store(int k, cplx (*s)[HX], cplx v) { s[k / HX][k % HX] = v; }
-__device__ __forceinline__ void halo_store(int k, double (*s)[HX], double v) { s[k / HX][k % HX] = v; }
+// Two halo elements per thread (k = tid, tid + NT) of a tile of width W and
+// count HNW, origin (x0-1, y0-1).
+template <int W, int HNW>
+struct Halo {
+  int ia, ib;  // linear node index, -1 outside the domain or tile
+  __device__ __forceinline__ void init(int tid, int x0, int y0, int m) {
+    ia = idx(tid, x0, y0, m);
+    ib = (tid + NT < HNW) ? idx(tid + NT, x0, y0, m) : -1;
+  }
+  __device__ __forceinline__ static int idx(int k, int x0, int y0, int m) {
+    const int ly = k / W, lx = k - ly * W;
+    const int xx = x0 - 1 + lx, yy = y0 - 1 + ly;
+    return (xx >= 0 && xx < m && yy >= 0 && yy < m) ? yy * m + xx : -1;
+  }
+  template <class T>
+  __device__ __forceinline__ static void store(T (*s)[W], int k, T v) {
+    const int ly = k / W;
+    s[ly][k - ly * W] = v;
+  }
+};
 
 // r = b - A x (warm) or r = b, x = 0 (cold); partials (||b||^2, ||r||^2).
-template <int MODE>
+template <int MODE, int FAM>
 __global__ void __launch_bounds__(NT, 4) k_init(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                             TT<MODE>* __restrict__ x_, TT<MODE>* __restrict__ r,
-                                             int nb, int BB, int warm, double* __restrict__ part) {
+                                                TT<MODE>* __restrict__ x_, TT<MODE>* __restrict__ r,
+                                                int nb, int BB, int warm, double* __restrict__ part) {
   using T = TT<MODE>;
   __shared__ T s[HY][HX];
-  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
   TILE_PROLOGUE
-  if constexpr (MODE == 0)
-    if (warm) stage_stencil(op, st_[0], i, in, tid);
+  Ctx<MODE, FAM> cx;
+  if constexpr (FAM == 0) cx.st = st_;
+  if (warm) cx.init(op, i, in, tid);
+  Halo<HX, HN> h;
+  h.init(tid, x0, y0, m);
   for (int b = next_active(nullptr, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(nullptr, b, nb, BB)) {
     const size_t o = (size_t)b * n;
     if (warm) {
-      for (int k = tid; k < HN; k += NT) {
-        int xx, yy;
-        halo_xy(k, x0, y0, xx, yy);
-        halo_store(k, s, (xx >= 0 && xx < m && yy >= 0 && yy < m) ? x_[o + yy * m + xx] : zero_of(s[0][0]));
-      }
+      Halo<HX, HN>::store(s, tid, h.ia >= 0 ? x_[o + h.ia] : zero_of(T{}));
+      if (tid + NT < HN) Halo<HX, HN>::store(s, tid + NT, h.ib >= 0 ? x_[o + h.ib] : zero_of(T{}));
     }
     __syncthreads();
     double v0 = 0, v1 = 0;
     if (in) {
       const T bi = bv[o + i];
       T ri = bi;
-      if (warm) {
-        ri = bi - apply_tile(stencil_of<MODE>(op, st_, b, i, tid), s, tx, ty);
-      } else {
-        x_[o + i] = zero_of(bi);
-      }
+      if (warm) ri = bi - apply_tile(cx.at(op, b, i, tid), s, tx + 1, ty + 1);
+      else x_[o + i] = zero_of(bi);
       r[o + i] = ri;
       v0 = norm2(bi);
       v1 = norm2(ri);
@@ -246,7 +326,7 @@ __global__ void __launch_bounds__(NT, 4) k_init(Op<MODE> op, const TT<MODE>* __r
 
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_zero_flagged(Op<MODE> op, TT<MODE>* __restrict__ x_, int nb,
-                                                     int BB, const int* __restrict__ zero) {
+                                                        int BB, const int* __restrict__ zero) {
   TILE_PROLOGUE
   if (!in) return;
   for (int k = 0; k < BB; ++k) {
@@ -257,45 +337,43 @@ __global__ void __launch_bounds__(NT, 4) k_zero_flagged(Op<MODE> op, TT<MODE>* _
 }
 
 // p_out = first ? z : z + beta p_in ;  q = A p_out ; partial p^T q
-template <int MODE>
+template <int MODE, int FAM>
 __global__ void __launch_bounds__(NT, 4) k_apply_dot(Op<MODE> op, const TT<MODE>* __restrict__ z,
-                                                  const TT<MODE>* __restrict__ pin,
-                                                  TT<MODE>* __restrict__ pout, TT<MODE>* __restrict__ q,
-                                                  const TT<MODE>* __restrict__ beta,
-                                                  const int* __restrict__ active, int first, int nb,
-                                                  int BB, double* __restrict__ part) {
+                                                     const TT<MODE>* __restrict__ pin,
+                                                     TT<MODE>* __restrict__ pout, TT<MODE>* __restrict__ q,
+                                                     const TT<MODE>* __restrict__ beta,
+                                                     const int* __restrict__ active, int first, int nb,
+                                                     int BB, double* __restrict__ part) {
   using T = TT<MODE>;
   __shared__ T s[HY][HX];
-  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
   TILE_PROLOGUE
-  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
-  // prefetch registers: z and p for the (<= 2) halo elements of this thread
+  Ctx<MODE, FAM> cx;
+  if constexpr (FAM == 0) cx.st = st_;
+  cx.init(op, i, in, tid);
+  Halo<HX, HN> h;
+  h.init(tid, x0, y0, m);
+  const bool has1 = tid + NT < HN;
   T z0 = zero_of(T{}), p0 = zero_of(T{}), z1 = zero_of(T{}), p1 = zero_of(T{});
-  int xa, ya, xb, yb;
-  halo_xy(tid, x0, y0, xa, ya);
-  halo_xy(hk1, x0, y0, xb, yb);
-  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
-  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
-  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
   auto fetch = [&](int b) {
     const size_t o = (size_t)b * n;
-    if (va) { z0 = z[o + ia]; if (!first) p0 = pin[o + ia]; }
-    if (vb) { z1 = z[o + ib]; if (!first) p1 = pin[o + ib]; }
+    if (h.ia >= 0) { z0 = z[o + h.ia]; if (!first) p0 = pin[o + h.ia]; }
+    if (h.ib >= 0) { z1 = z[o + h.ib]; if (!first) p1 = pin[o + h.ib]; }
   };
   int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
   if (b >= 0) fetch(b);
   while (b >= 0) {
     const int bn = next_active(active, b, nb, BB);
     const T bt = first ? zero_of(T{}) : beta[b];
-    halo_store(tid, s, va ? (first ? z0 : z0 + mul(bt, p0)) : zero_of(T{}));
-    if (has1) halo_store(hk1, s, vb ? (first ? z1 : z1 + mul(bt, p1)) : zero_of(T{}));
+    Halo<HX, HN>::store(s, tid, h.ia >= 0 ? (first ? z0 : z0 + mul(bt, p0)) : zero_of(T{}));
+    if (has1) Halo<HX, HN>::store(s, tid + NT, h.ib >= 0 ? (first ? z1 : z1 + mul(bt, p1)) : zero_of(T{}));
     __syncthreads();
     if (bn >= 0) fetch(bn);
     double v[2] = {0, 0};
     if (in) {
       const size_t o = (size_t)b * n;
       const T pi = s[ty + 1][tx + 1];
-      const T qi = apply_tile(stencil_of<MODE>(op, st_, b, i, tid), s, tx, ty);
+      const T qi = apply_tile(cx.at(op, b, i, tid), s, tx + 1, ty + 1);
       pout[o + i] = pi;
       q[o + i] = qi;
       add_dot(v, pi, qi);
@@ -309,17 +387,14 @@ __global__ void __launch_bounds__(NT, 4) k_apply_dot(Op<MODE> op, const TT<MODE>
 // x += alpha p ; r -= alpha q ; partial ||r||^2 ; z = omega r / a_C
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_update(Op<MODE> op, TT<MODE>* __restrict__ x_,
-                                               TT<MODE>* __restrict__ r, const TT<MODE>* __restrict__ p,
-                                               const TT<MODE>* __restrict__ q,
-                                               const TT<MODE>* __restrict__ alpha,
-                                               const int* __restrict__ active, double omega,
-                                               TT<MODE>* __restrict__ z, int nb, int BB,
-                                               double* __restrict__ part) {
+                                                  TT<MODE>* __restrict__ r, const TT<MODE>* __restrict__ p,
+                                                  const TT<MODE>* __restrict__ q,
+                                                  const TT<MODE>* __restrict__ alpha,
+                                                  const int* __restrict__ active, double omega,
+                                                  TT<MODE>* __restrict__ z, int nb, int BB,
+                                                  double* __restrict__ part) {
   using T = TT<MODE>;
   TILE_PROLOGUE
-  double kc = 0, mc = 0;
-  if constexpr (MODE == 0)
-    if (in && z) { kc = __ldg(op.K + i); mc = __ldg(op.M + i); }
   for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
     double v0 = 0;
     if (in) {
@@ -329,12 +404,7 @@ __global__ void __launch_bounds__(NT, 4) k_update(Op<MODE> op, TT<MODE>* __restr
       const T rj = r[j] - mul(al, q[j]);
       r[j] = rj;
       v0 = norm2(rj);
-      if (z) {
-        T d;
-        if constexpr (MODE == 0) { const cplx l = op.lam[b]; d = cplx{fma(l.re, mc, kc), l.im * mc}; }
-        else d = __ldg(op.J + (size_t)b * 7 * n + i);
-        z[j] = omega * mul(rj, inv_of(d));
-      }
+      if (z) z[j] = omega * mul(rj, inv_of(diag_global<MODE>(op, b, i)));
     }
     block_pair(v0, 0.0, part, b);
     __syncthreads();
@@ -344,60 +414,53 @@ __global__ void __launch_bounds__(NT, 4) k_update(Op<MODE> op, TT<MODE>* __restr
 // z = omega b / a_C (first Jacobi sweep from zero)
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_jacobi0(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                                TT<MODE>* __restrict__ z, const int* __restrict__ active,
-                                                double omega, int nb, int BB) {
-  using T = TT<MODE>;
+                                                   TT<MODE>* __restrict__ z, const int* __restrict__ active,
+                                                   double omega, int nb, int BB) {
   TILE_PROLOGUE
   if (!in) return;
-  double kc = 0, mc = 0;
-  if constexpr (MODE == 0) { kc = __ldg(op.K + i); mc = __ldg(op.M + i); }
   for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
     const size_t j = (size_t)b * n + i;
-    T d;
-    if constexpr (MODE == 0) { const cplx l = op.lam[b]; d = cplx{fma(l.re, mc, kc), l.im * mc}; }
-    else d = __ldg(op.J + (size_t)b * 7 * n + i);
-    z[j] = omega * mul(bv[j], inv_of(d));
+    z[j] = omega * mul(bv[j], inv_of(diag_global<MODE>(op, b, i)));
   }
 }
 
 // z_out = z_in + omega (b - A z_in)/a_C ; optional partial b^T z_out
-template <int MODE>
+template <int MODE, int FAM>
 __global__ void __launch_bounds__(NT, 4) k_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                               const TT<MODE>* __restrict__ zin,
-                                               TT<MODE>* __restrict__ zout,
-                                               const int* __restrict__ active, double omega, int nb,
-                                               int BB, int dot, double* __restrict__ part) {
+                                                  const TT<MODE>* __restrict__ zin,
+                                                  TT<MODE>* __restrict__ zout,
+                                                  const int* __restrict__ active, double omega, int nb,
+                                                  int BB, int dot, double* __restrict__ part) {
   using T = TT<MODE>;
   __shared__ T s[HY][HX];
-  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
   TILE_PROLOGUE
-  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  Ctx<MODE, FAM> cx;
+  if constexpr (FAM == 0) cx.st = st_;
+  cx.init(op, i, in, tid);
+  Halo<HX, HN> h;
+  h.init(tid, x0, y0, m);
+  const bool has1 = tid + NT < HN;
   T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
-  int xa, ya, xb, yb;
-  halo_xy(tid, x0, y0, xa, ya);
-  halo_xy(hk1, x0, y0, xb, yb);
-  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
-  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
-  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
   auto fetch = [&](int b) {
     const size_t o = (size_t)b * n;
-    if (va) z0 = zin[o + ia];
-    if (vb) z1 = zin[o + ib];
+    if (h.ia >= 0) z0 = zin[o + h.ia];
+    if (h.ib >= 0) z1 = zin[o + h.ib];
     if (in) bo = bv[o + i];
   };
   int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
   if (b >= 0) fetch(b);
   while (b >= 0) {
     const int bn = next_active(active, b, nb, BB);
-    halo_store(tid, s, va ? z0 : zero_of(T{}));
-    if (has1) halo_store(hk1, s, vb ? z1 : zero_of(T{}));
+    Halo<HX, HN>::store(s, tid, h.ia >= 0 ? z0 : zero_of(T{}));
+    if (has1) Halo<HX, HN>::store(s, tid + NT, h.ib >= 0 ? z1 : zero_of(T{}));
     const T bi = bo;
     __syncthreads();
     if (bn >= 0) fetch(bn);
     double v[2] = {0, 0};
     if (in) {
-      const auto a = stencil_of<MODE>(op, st_, b, i, tid);
-      const T zi = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx, ty), inv_of(a(0)));
+      const auto a = cx.at(op, b, i, tid);
+      const T zi = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx + 1, ty + 1), inv_of(a.diag()));
       zout[(size_t)b * n + i] = zi;
       if (dot) add_dot(v, bi, zi);
     }
@@ -408,20 +471,26 @@ __global__ void __launch_bounds__(NT, 4) k_smooth(Op<MODE> op, const TT<MODE>* _
 }
 
 // Fine tile 32x8 -> coarse 16x4: bc = P^T (bf - Af zf); optional first coarse
-// Jacobi sweep zc = omega bc / ac_C.
-template <int MODE>
+// Jacobi sweep zc = omega bc / ac_C.  The z tile covers [x0-1, x0+33] x
+// [y0-1, y0+9] so the 33x9 residual region is computed from shared memory.
+template <int MODE, int FAM>
 __global__ void __launch_bounds__(NT, 4) k_restrict(Op<MODE> op, Op<MODE> opc,
-                                                 const TT<MODE>* __restrict__ bf,
-                                                 const TT<MODE>* __restrict__ zf,
-                                                 TT<MODE>* __restrict__ bc, TT<MODE>* __restrict__ zc,
-                                                 const int* __restrict__ active, double omega, int nb,
-                                                 int BB) {
+                                                    const TT<MODE>* __restrict__ bf,
+                                                    const TT<MODE>* __restrict__ zf,
+                                                    TT<MODE>* __restrict__ bc, TT<MODE>* __restrict__ zc,
+                                                    const int* __restrict__ active, double omega, int nb,
+                                                    int BB) {
   using T = TT<MODE>;
-  __shared__ T s[HY][HX];
+  __shared__ T s[RY][RX];
   __shared__ T res[TY + 1][TX + 1];
-  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
   TILE_PROLOGUE
-  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  Ctx<MODE, FAM> cx;
+  if constexpr (FAM == 0) cx.st = st_;
+  cx.init(op, i, in, tid);
+  Halo<RX, RN> h;
+  h.init(tid, x0, y0, m);
+  const bool has1 = tid + NT < RN;
   // extra residual nodes: column x0+TX (rows 0..TY-1), row y0+TY (cols 0..TX)
   int ex = -1, ey = -1;
   if (tid < TY) { ex = TX; ey = tid; }
@@ -435,55 +504,38 @@ __global__ void __launch_bounds__(NT, 4) k_restrict(Op<MODE> op, Op<MODE> opc,
   const int X = (x0 >> 1) + cxl, Y = (y0 >> 1) + cyl;
   const bool cin = tid < 64 && X < mcs && Y < mcs;
   const int ci = cin ? Y * mcs + X : 0;
-  double ckc = 0, cmc = 0;
-  if constexpr (MODE == 0)
-    if (cin && zc) { ckc = __ldg(opc.K + ci); cmc = __ldg(opc.M + ci); }
-  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
-  int xa, ya, xb, yb;
-  halo_xy(tid, x0, y0, xa, ya);
-  halo_xy(hk1, x0, y0, xb, yb);
-  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
-  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
-  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
+  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{}), be = zero_of(T{});
   auto fetch = [&](int b) {
     const size_t o = (size_t)b * n;
-    if (va) z0 = zf[o + ia];
-    if (vb) z1 = zf[o + ib];
+    if (h.ia >= 0) z0 = zf[o + h.ia];
+    if (h.ib >= 0) z1 = zf[o + h.ib];
     if (in) bo = bf[o + i];
+    if (ein) be = bf[o + ei];
   };
   int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
   if (b >= 0) fetch(b);
   while (b >= 0) {
     const int bn = next_active(active, b, nb, BB);
-    halo_store(tid, s, va ? z0 : zero_of(T{}));
-    if (has1) halo_store(hk1, s, vb ? z1 : zero_of(T{}));
-    const T bi = bo;
+    Halo<RX, RN>::store(s, tid, h.ia >= 0 ? z0 : zero_of(T{}));
+    if (has1) Halo<RX, RN>::store(s, tid + NT, h.ib >= 0 ? z1 : zero_of(T{}));
+    const T bi = bo, bei = be;
     __syncthreads();
     if (bn >= 0) fetch(bn);
-    const size_t o = (size_t)b * n;
-    res[ty][tx] = in ? bi - apply_tile(stencil_of<MODE>(op, st_, b, i, tid), s, tx, ty) : zero_of(T{});
+    res[ty][tx] = in ? bi - apply_tile(cx.at(op, b, i, tid), s, tx + 1, ty + 1) : zero_of(T{});
     if (ex >= 0) {
       T rr = zero_of(T{});
       if (ein) {
         T a[7];
-        if constexpr (MODE == 0) {
-          const cplx l = op.lam[b];
-          for (int d = 0; d < 7; ++d) {
-            const double mm = __ldg(op.M + (size_t)d * n + ei);
-            a[d] = cplx{fma(l.re, mm, __ldg(op.K + (size_t)d * n + ei)), l.im * mm};
-          }
-        } else {
-          for (int d = 0; d < 7; ++d) a[d] = __ldg(op.J + (size_t)b * 7 * n + (size_t)d * n + ei);
-        }
-        const T* zz = zf + o;
-        T acc = mul(a[0], zz[ei]);
-        if (gx > 0) acc = acc + mul(a[1], zz[ei - 1]);
-        if (gx < m - 1) acc = acc + mul(a[2], zz[ei + 1]);
-        if (gy > 0) acc = acc + mul(a[3], zz[ei - m]);
-        if (gy < m - 1) acc = acc + mul(a[4], zz[ei + m]);
-        if (gx > 0 && gy > 0) acc = acc + mul(a[5], zz[ei - m - 1]);
-        if (gx < m - 1 && gy < m - 1) acc = acc + mul(a[6], zz[ei + m + 1]);
-        rr = bf[o + ei] - acc;
+        coef_global<MODE>(op, b, ei, a);
+        const int lx = ex + 1, ly = ey + 1;
+        T acc = mul(a[0], s[ly][lx]);
+        acc = acc + mul(a[1], s[ly][lx - 1]);
+        acc = acc + mul(a[2], s[ly][lx + 1]);
+        acc = acc + mul(a[3], s[ly - 1][lx]);
+        acc = acc + mul(a[4], s[ly + 1][lx]);
+        acc = acc + mul(a[5], s[ly - 1][lx - 1]);
+        acc = acc + mul(a[6], s[ly + 1][lx + 1]);
+        rr = bei - acc;
       }
       res[ey][ex] = rr;
     }
@@ -495,12 +547,7 @@ __global__ void __launch_bounds__(NT, 4) k_restrict(Op<MODE> op, Op<MODE> opc,
       const T acc = res[fy][fx] + 0.5 * side;
       const size_t oc = (size_t)b * nc;
       bc[oc + ci] = acc;
-      if (zc) {
-        T d;
-        if constexpr (MODE == 0) { const cplx l = opc.lam[b]; d = cplx{fma(l.re, cmc, ckc), l.im * cmc}; }
-        else d = __ldg(opc.J + (size_t)b * 7 * nc + ci);
-        zc[oc + ci] = omega * mul(acc, inv_of(d));
-      }
+      if (zc) zc[oc + ci] = omega * mul(acc, inv_of(diag_global<MODE>(opc, b, ci)));
     }
     __syncthreads();
     b = bn;
@@ -508,54 +555,53 @@ __global__ void __launch_bounds__(NT, 4) k_restrict(Op<MODE> op, Op<MODE> opc,
 }
 
 // zc = z_in + P xc on the tile + halo (shared), then z_out = zc + omega (b - A zc)/a_C
-template <int MODE>
+template <int MODE, int FAM>
 __global__ void __launch_bounds__(NT, 4) k_prolong_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                                       const TT<MODE>* __restrict__ zin,
-                                                       const TT<MODE>* __restrict__ xc, int mc,
-                                                       TT<MODE>* __restrict__ zout,
-                                                       const int* __restrict__ active, double omega,
-                                                       int nb, int BB, int dot, double* __restrict__ part) {
+                                                          const TT<MODE>* __restrict__ zin,
+                                                          const TT<MODE>* __restrict__ xc, int mc,
+                                                          TT<MODE>* __restrict__ zout,
+                                                          const int* __restrict__ active, double omega,
+                                                          int nb, int BB, int dot, double* __restrict__ part) {
   using T = TT<MODE>;
   __shared__ T s[HY][HX];
-  __shared__ StageF st_[MODE == 0 ? 1 : 0 + 1];
+  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
   TILE_PROLOGUE
-  if constexpr (MODE == 0) stage_stencil(op, st_[0], i, in, tid);
+  Ctx<MODE, FAM> cx;
+  if constexpr (FAM == 0) cx.st = st_;
+  cx.init(op, i, in, tid);
   const int nc = mc * mc;
-  int xa, ya, xb, yb;
-  halo_xy(tid, x0, y0, xa, ya);
-  halo_xy(hk1, x0, y0, xb, yb);
-  const bool va = xa >= 0 && xa < m && ya >= 0 && ya < m;
-  const bool vb = has1 && xb >= 0 && xb < m && yb >= 0 && yb < m;
-  const int ia = va ? ya * m + xa : 0, ib = vb ? yb * m + xb : 0;
+  Halo<HX, HN> h;
+  h.init(tid, x0, y0, m);
+  const bool has1 = tid + NT < HN;
   // coarse parents of the two halo elements: linear coarse index, first weight
   // (1 or 1/2; a second parent, if any, always weighs 1/2)
   int pa0 = -1, pa1 = -1, pb0 = -1, pb1 = -1;
   double wa = 0, wb = 0;
   {
-    int cx[2], cy[2];
+    int cxp[2], cyp[2];
     double w[2];
-    if (va) {
-      const int np = parents(xa, ya, mc, cx, cy, w);
-      if (np > 0) { pa0 = cy[0] * mc + cx[0]; wa = w[0]; }
-      if (np > 1) pa1 = cy[1] * mc + cx[1];
+    if (h.ia >= 0) {
+      const int np = parents(h.ia % m, h.ia / m, mc, cxp, cyp, w);
+      if (np > 0) { pa0 = cyp[0] * mc + cxp[0]; wa = w[0]; }
+      if (np > 1) pa1 = cyp[1] * mc + cxp[1];
     }
-    if (vb) {
-      const int np = parents(xb, yb, mc, cx, cy, w);
-      if (np > 0) { pb0 = cy[0] * mc + cx[0]; wb = w[0]; }
-      if (np > 1) pb1 = cy[1] * mc + cx[1];
+    if (h.ib >= 0) {
+      const int np = parents(h.ib % m, h.ib / m, mc, cxp, cyp, w);
+      if (np > 0) { pb0 = cyp[0] * mc + cxp[0]; wb = w[0]; }
+      if (np > 1) pb1 = cyp[1] * mc + cxp[1];
     }
   }
   T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
   auto fetch = [&](int b) {
     const size_t o = (size_t)b * n, oc = (size_t)b * nc;
-    if (va) {
-      T v = zin[o + ia];
+    if (h.ia >= 0) {
+      T v = zin[o + h.ia];
       if (pa0 >= 0) v = v + wa * xc[oc + pa0];
       if (pa1 >= 0) v = v + 0.5 * xc[oc + pa1];
       z0 = v;
     }
-    if (vb) {
-      T v = zin[o + ib];
+    if (h.ib >= 0) {
+      T v = zin[o + h.ib];
       if (pb0 >= 0) v = v + wb * xc[oc + pb0];
       if (pb1 >= 0) v = v + 0.5 * xc[oc + pb1];
       z1 = v;
@@ -566,15 +612,15 @@ __global__ void __launch_bounds__(NT, 4) k_prolong_smooth(Op<MODE> op, const TT<
   if (b >= 0) fetch(b);
   while (b >= 0) {
     const int bn = next_active(active, b, nb, BB);
-    halo_store(tid, s, va ? z0 : zero_of(T{}));
-    if (has1) halo_store(hk1, s, vb ? z1 : zero_of(T{}));
+    Halo<HX, HN>::store(s, tid, h.ia >= 0 ? z0 : zero_of(T{}));
+    if (has1) Halo<HX, HN>::store(s, tid + NT, h.ib >= 0 ? z1 : zero_of(T{}));
     const T bi = bo;
     __syncthreads();
     if (bn >= 0) fetch(bn);
     double v[2] = {0, 0};
     if (in) {
-      const auto a = stencil_of<MODE>(op, st_, b, i, tid);
-      const T zo = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx, ty), inv_of(a(0)));
+      const auto a = cx.at(op, b, i, tid);
+      const T zo = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx + 1, ty + 1), inv_of(a.diag()));
       zout[(size_t)b * n + i] = zo;
       if (dot) add_dot(v, bi, zo);
     }
@@ -587,8 +633,8 @@ __global__ void __launch_bounds__(NT, 4) k_prolong_smooth(Op<MODE> op, const TT<
 // partial b^T z
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_dot(Op<MODE> op, const TT<MODE>* __restrict__ a_,
-                                            const TT<MODE>* __restrict__ z, const int* __restrict__ active,
-                                            int nb, int BB, double* __restrict__ part) {
+                                               const TT<MODE>* __restrict__ z, const int* __restrict__ active,
+                                               int nb, int BB, double* __restrict__ part) {
   TILE_PROLOGUE
   for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
     double v[2] = {0, 0};
@@ -907,11 +953,23 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   const Geo g = geo_for(ops[l].m, nb, p->num_sms, 8);
   int* act = active.get();
   cudaStream_t s = p->stream;
+  const dim3 blk(TX, TY);
+#define DISPATCH_FAM(lv, CALL)          \
+  if constexpr (MODE == 1) {            \
+    constexpr int FAM = 2;              \
+    CALL;                               \
+  } else if (ops[lv].five) {            \
+    constexpr int FAM = 1;              \
+    CALL;                               \
+  } else {                              \
+    constexpr int FAM = 0;              \
+    CALL;                               \
+  }
   if (L == 1) {
     k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, bl, lz0[0].get(), ops[0].n, act);
     TP_LAUNCHED(p);
     if (dot) {
-      k_dot<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, lz0[0].get(), act, nb, g.BB, part.get());
+      k_dot<MODE><<<g.grid, blk, 0, s>>>(op, bl, lz0[0].get(), act, nb, g.BB, part.get());
       TP_LAUNCHED(p);
     }
     return lz0[0].get();
@@ -919,15 +977,15 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   T* z = lz0[l].get();
   T* o = lz1[l].get();
   for (int k = 1; k < cfg.pre; ++k) {
-    k_smooth<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, 0, part.get());
+    DISPATCH_FAM(l, (k_smooth<MODE, FAM><<<g.grid, blk, 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, 0, part.get())));
     TP_LAUNCHED(p);
     std::swap(z, o);
   }
   const bool coarse_next = (l + 1 == L - 1);
   const Op<MODE> opc = make_op<MODE>(ops[l + 1], lam);
-  k_restrict<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, opc, bl, z, lb[l + 1].get(),
-                                                   coarse_next ? nullptr : lz0[l + 1].get(), act,
-                                                   cfg.omega, nb, g.BB);
+  T* zc0 = coarse_next ? nullptr : lz0[l + 1].get();
+  DISPATCH_FAM(l, (k_restrict<MODE, FAM><<<g.grid, blk, 0, s>>>(op, opc, bl, z, lb[l + 1].get(), zc0, act,
+                                                                cfg.omega, nb, g.BB)));
   TP_LAUNCHED(p);
   T* xc;
   if (coarse_next) {
@@ -937,14 +995,15 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   } else {
     xc = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
   }
-  k_prolong_smooth<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, z, xc, ops[l + 1].m, o, act, cfg.omega,
-                                                         nb, g.BB, (dot && cfg.post == 1) ? 1 : 0,
-                                                         part.get());
+  const int pdot = (dot && cfg.post == 1) ? 1 : 0;
+  const int mcl = ops[l + 1].m;
+  DISPATCH_FAM(l, (k_prolong_smooth<MODE, FAM><<<g.grid, blk, 0, s>>>(op, bl, z, xc, mcl, o, act, cfg.omega,
+                                                                      nb, g.BB, pdot, part.get())));
   TP_LAUNCHED(p);
   std::swap(z, o);
   for (int k = 1; k < cfg.post; ++k) {
     const int d = (dot && k == cfg.post - 1) ? 1 : 0;
-    k_smooth<MODE><<<g.grid, dim3(TX, TY), 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, d, part.get());
+    DISPATCH_FAM(l, (k_smooth<MODE, FAM><<<g.grid, blk, 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, d, part.get())));
     TP_LAUNCHED(p);
     std::swap(z, o);
   }
@@ -962,7 +1021,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int* act = active.get();
   int* zero = active.get() + B;
   cudaStream_t s = p->stream;
-  k_init<MODE><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get());
+  const int l = 0;
+  DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
   TP_LAUNCHED(p);
   k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), per0, nb, rtol2, rho.get(), mu.get(), alpha.get(),
                                   beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
@@ -989,8 +1049,9 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     T* pout = p1.get();
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
-      k_apply_dot<MODE><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
-                                                it == 1 ? 1 : 0, nb, g0.BB, part.get());
+      const int first = it == 1 ? 1 : 0;
+      DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
+                                                                      first, nb, g0.BB, part.get())));
       TP_LAUNCHED(p);
       k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);

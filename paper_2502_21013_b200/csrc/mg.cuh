@@ -31,6 +31,7 @@ struct LevelOp {
   int m = 0, n = 0;
   const double* K = nullptr;  // freq: 7n shared ; slice: 7n per batch (stride 7n)
   const double* M = nullptr;  // freq only
+  bool five = false;          // freq mode: K 5-point and M diagonal (fine level)
 };
 
 template <int MODE>

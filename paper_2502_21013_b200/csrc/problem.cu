@@ -318,7 +318,7 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   chunk = std::max(1, std::min(chunk, K));
   fw->chunk = chunk;
   std::vector<LevelOp> ops(nl);
-  for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get()};
+  for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get(), l == 0};
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
   mc.max_iter = cfg.inner_max_iter;

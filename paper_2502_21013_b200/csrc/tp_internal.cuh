@@ -39,7 +39,7 @@ inline void require(bool ok, const std::string& msg) {
 }
 
 // ---------------------------------------------------------------- complex
-struct cplx {
+struct __align__(16) cplx {
   double re, im;
 };
 __host__ __device__ inline cplx mk(double r, double i) { return cplx{r, i}; }
