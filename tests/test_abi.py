@@ -86,3 +86,19 @@ def test_problem_create_without_gpu_fails_loudly():
         pass
     with pytest.raises(RuntimeError):
         api.Problem(api.baseline_desc(0))
+
+
+def test_tpfem_adapter_compiles_against_reference_headers(tmp_path):
+    """include/tpgpu_tpfem.hpp (the reference-side binding) type-checks
+    against the reference's own headers (shim SparseSolver for Eigen)."""
+    ref_inc = "/root/reference/proj/include"
+    if not os.path.isdir(ref_inc):
+        pytest.skip("reference headers not present")
+    src = tmp_path / "use.cpp"
+    src.write_text('#include "tpgpu_tpfem.hpp"\n'
+                   "int f(){ tp_problem_desc d; tp_problem_desc_baseline(0,&d);"
+                   " tpgpu::GpuProblem p(d); tpfem::SolverConfig c; c.tol=1e-8;"
+                   " auto U0 = tpgpu::static_init(p, c); tpgpu::choose_nu_hat(p, c);"
+                   " auto r = tpgpu::solve_m1_fixed_point(p, U0, c); return r.second.iterations; }\n")
+    subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "oracle", "shim"),
+                    "-I", ref_inc, "-I", os.path.join(ROOT, "include"), str(src)], check=True)
