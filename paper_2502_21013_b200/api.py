@@ -249,7 +249,7 @@ class Problem:
         return U
 
     def solve_m1_fixed_point(self, U0=None, cfg: TpSolverCfg | None = None, iterate_log=None,
-                             callback=None):
+                             callback=None, out=None):
         """Returns (U, SolveReport).  iterate_log: list to receive every iterate
         (solvers.hpp:306); callback(k, U, residual) -> truthy aborts."""
         cfg = cfg or default_cfg()
@@ -257,7 +257,9 @@ class Problem:
         cap = cfg.m1_max_outer + 1
         hist = np.zeros(cap)
         contr = np.zeros(cap)
-        U = np.zeros(self.shape)
+        U = out if out is not None else np.zeros(self.shape)
+        if U.shape != self.shape or U.dtype != np.float64 or not U.flags.c_contiguous:
+            raise ValueError("out must be a C-contiguous float64 array of the state shape")
         rep = TpReport()
 
         want = iterate_log is not None or callback is not None

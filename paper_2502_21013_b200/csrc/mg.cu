@@ -650,10 +650,10 @@ __global__ void k_coarse_solve(const T* __restrict__ inv, const T* __restrict__ 
                                int nL, const int* __restrict__ active) {
   const int b = blockIdx.x;
   if (!active[b]) return;
-  const T* A = inv + (size_t)b * nL * nL;
+  const T* A = inv + (size_t)b * nL * nL;  // transposed: A[j*nL + i] = inv(i, j)
   for (int i = threadIdx.x; i < nL; i += blockDim.x) {
     T acc = zero_of(bc[0]);
-    for (int j = 0; j < nL; ++j) acc = acc + mul(A[(size_t)i * nL + j], bc[(size_t)b * nL + j]);
+    for (int j = 0; j < nL; ++j) acc = acc + mul(A[(size_t)j * nL + i], bc[(size_t)b * nL + j]);
     xc[(size_t)b * nL + i] = acc;
   }
 }
@@ -834,8 +834,10 @@ __global__ void k_dense_inverse(const double* __restrict__ K, const double* __re
       if (i != k) A[(size_t)i * w + k] = zero_of(A[0]);
     __syncthreads();
   }
+  // stored transposed (column j contiguous over rows i) so the coarse solve
+  // reads it coalesced
   for (int t = threadIdx.x; t < n * n; t += blockDim.x) {
-    const int i = t / n, j = t % n;
+    const int j = t / n, i = t % n;
     inv[(size_t)b * n * n + t] = A[(size_t)i * w + n + j];
   }
 }
