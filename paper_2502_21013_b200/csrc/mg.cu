@@ -411,220 +411,330 @@ __global__ void __launch_bounds__(NT, 4) k_update(Op<MODE> op, TT<MODE>* __restr
   }
 }
 
-// z = omega b / a_C (first Jacobi sweep from zero)
-template <int MODE>
-__global__ void __launch_bounds__(NT, 4) k_jacobi0(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                                   TT<MODE>* __restrict__ z, const int* __restrict__ active,
-                                                   double omega, int nb, int BB) {
-  TILE_PROLOGUE
-  if (!in) return;
-  for (int b = next_active(active, blockIdx.z * BB - 1, nb, BB); b >= 0; b = next_active(active, b, nb, BB)) {
-    const size_t j = (size_t)b * n + i;
-    z[j] = omega * mul(bv[j], inv_of(diag_global<MODE>(op, b, i)));
-  }
-}
+// ===================================================================
+// Fused V-cycle passes with halo-2 temporal blocking.
+//
+// k_down (level l): from the level's right-hand side r, two smoothing
+// half-steps from zero (damped Jacobi x2, or one forward red-black
+// Gauss-Seidel sweep on the 5-point fine level), the residual r - A z2 and
+// its restriction P^T to level l+1, in one pass: reads r once (tile + halo 2),
+// writes z2 (tile) and the coarse right-hand side.
+// k_up (level l): z2 + P x_{l+1} on the halo-2 tile, two post-smoothing
+// half-steps (Jacobi x2, or one backward black-red Gauss-Seidel sweep), in
+// one pass: reads z2, r, x_{l+1}; writes z4 (and the partial r^T z4 on the
+// fine level).  Pre and post smoothers are adjoint, restriction is P^T and
+// the coarsest solve is exact, so the V-cycle is a symmetric (in x^T y)
+// preconditioner and COCG's short recurrence holds.
+// Regions in tile-local coordinates (origin x0-2, y0-2): staged grid
+// H2 = 37x13; down pass: z1 on H2, z2 on D = [1,36)x[1,12), residual on
+// Q = [2,35)x[2,11) (tile + the extra column/row the restriction gathers);
+// up pass: z3 on H1 = [1,35)x[1,11), z4 on the tile [2,34)x[2,10).
+constexpr int H2X = TX + 5, H2Y = TY + 5, H2N = H2X * H2Y;  // 481
+constexpr int DX = TX + 3, DY = TY + 3, DN = DX * DY;       // 385
+constexpr int H1X = TX + 2, H1Y = TY + 2, H1N = H1X * H1Y;  // 340
+constexpr int QX = TX + 1, QY = TY + 1, QN = QX * QY;       // 297
+enum { SM_JAC = 0, SM_RB = 1 };
 
-// z_out = z_in + omega (b - A z_in)/a_C ; optional partial b^T z_out
+template <int FAM>
+struct CoefPlanes;
+template <>
+struct CoefPlanes<1> {  // fine: diag K, diag M, 4 real off-diagonals (W, E, S, N)
+  static constexpr int planes = 6;
+};
+template <>
+struct CoefPlanes<0> {  // coarse frequency mode: 7 K + 7 M
+  static constexpr int planes = 14;
+};
+template <>
+struct CoefPlanes<2> {  // slice mode: 7 J (per batch)
+  static constexpr int planes = 7;
+};
+
 template <int MODE, int FAM>
-__global__ void __launch_bounds__(NT, 4) k_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                                  const TT<MODE>* __restrict__ zin,
-                                                  TT<MODE>* __restrict__ zout,
-                                                  const int* __restrict__ active, double omega, int nb,
-                                                  int BB, int dot, double* __restrict__ part) {
-  using T = TT<MODE>;
-  __shared__ T s[HY][HX];
-  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
-  TILE_PROLOGUE
-  Ctx<MODE, FAM> cx;
-  if constexpr (FAM == 0) cx.st = st_;
-  cx.init(op, i, in, tid);
-  Halo<HX, HN> h;
-  h.init(tid, x0, y0, m);
-  const bool has1 = tid + NT < HN;
-  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
-  auto fetch = [&](int b) {
-    const size_t o = (size_t)b * n;
-    if (h.ia >= 0) z0 = zin[o + h.ia];
-    if (h.ib >= 0) z1 = zin[o + h.ib];
-    if (in) bo = bv[o + i];
-  };
-  int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
-  if (b >= 0) fetch(b);
-  while (b >= 0) {
-    const int bn = next_active(active, b, nb, BB);
-    Halo<HX, HN>::store(s, tid, h.ia >= 0 ? z0 : zero_of(T{}));
-    if (has1) Halo<HX, HN>::store(s, tid + NT, h.ib >= 0 ? z1 : zero_of(T{}));
-    const T bi = bo;
-    __syncthreads();
-    if (bn >= 0) fetch(bn);
-    double v[2] = {0, 0};
-    if (in) {
-      const auto a = cx.at(op, b, i, tid);
-      const T zi = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx + 1, ty + 1), inv_of(a.diag()));
-      zout[(size_t)b * n + i] = zi;
-      if (dot) add_dot(v, bi, zi);
+__device__ __forceinline__ void stage_coefs(const Op<MODE>& op, double* cf, int b, int x0, int y0) {
+  const int tid = threadIdx.y * TX + threadIdx.x;
+  const int m = op.m;
+  const size_t n = op.n;
+  for (int k = tid; k < H2N; k += NT) {
+    const int ly = k / H2X, lx = k - ly * H2X;
+    const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
+    const bool in = gx >= 0 && gx < m && gy >= 0 && gy < m;
+    const size_t i = in ? (size_t)gy * m + gx : 0;
+    if constexpr (FAM == 1) {
+      const Op<0>& o = op;
+      cf[0 * H2N + k] = in ? __ldg(o.K + i) : 1.0;
+      cf[1 * H2N + k] = in ? __ldg(o.M + i) : 0.0;
+      for (int d = 1; d <= 4; ++d) cf[(1 + d) * H2N + k] = in ? __ldg(o.K + d * n + i) : 0.0;
+    } else if constexpr (FAM == 0) {
+      const Op<0>& o = op;
+      for (int d = 0; d < 7; ++d) {
+        cf[d * H2N + k] = in ? __ldg(o.K + d * n + i) : (d == 0 ? 1.0 : 0.0);
+        cf[(7 + d) * H2N + k] = in ? __ldg(o.M + d * n + i) : 0.0;
+      }
+    } else {
+      const Op<1>& o = op;
+      const double* J = o.J + (size_t)b * 7 * n;
+      for (int d = 0; d < 7; ++d) cf[d * H2N + k] = in ? __ldg(J + d * n + i) : (d == 0 ? 1.0 : 0.0);
     }
-    if (dot) block_pair(v[0], v[1], part, b);
-    __syncthreads();
-    b = bn;
   }
 }
 
-// Fine tile 32x8 -> coarse 16x4: bc = P^T (bf - Af zf); optional first coarse
-// Jacobi sweep zc = omega bc / ac_C.  The z tile covers [x0-1, x0+33] x
-// [y0-1, y0+9] so the 33x9 residual region is computed from shared memory.
+// diagonal coefficient at H2 index h
 template <int MODE, int FAM>
-__global__ void __launch_bounds__(NT, 4) k_restrict(Op<MODE> op, Op<MODE> opc,
-                                                    const TT<MODE>* __restrict__ bf,
-                                                    const TT<MODE>* __restrict__ zf,
-                                                    TT<MODE>* __restrict__ bc, TT<MODE>* __restrict__ zc,
-                                                    const int* __restrict__ active, double omega, int nb,
-                                                    int BB) {
+__device__ __forceinline__ TT<MODE> cdiag(const double* cf, int h, cplx l) {
+  if constexpr (FAM == 2) {
+    return cf[h];
+  } else if constexpr (FAM == 1) {
+    return cplx{fma(l.re, cf[H2N + h], cf[h]), l.im * cf[H2N + h]};
+  } else {
+    return cplx{fma(l.re, cf[7 * H2N + h], cf[h]), l.im * cf[7 * H2N + h]};
+  }
+}
+
+// off-diagonal part sum_{d>0} a_d v[nbr_d] at H2 position (lx, ly)
+template <int MODE, int FAM>
+__device__ __forceinline__ TT<MODE> coff(const double* cf, const TT<MODE>* v, int lx, int ly, cplx l) {
   using T = TT<MODE>;
-  __shared__ T s[RY][RX];
-  __shared__ T res[TY + 1][TX + 1];
-  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
-  TILE_PROLOGUE
-  Ctx<MODE, FAM> cx;
-  if constexpr (FAM == 0) cx.st = st_;
-  cx.init(op, i, in, tid);
-  Halo<RX, RN> h;
-  h.init(tid, x0, y0, m);
-  const bool has1 = tid + NT < RN;
-  // extra residual nodes: column x0+TX (rows 0..TY-1), row y0+TY (cols 0..TX)
-  int ex = -1, ey = -1;
-  if (tid < TY) { ex = TX; ey = tid; }
-  else if (tid < TY + TX + 1) { ex = tid - TY; ey = TY; }
-  const int gx = x0 + ex, gy = y0 + ey;
-  const bool ein = ex >= 0 && gx < m && gy < m;
-  const int ei = ein ? gy * m + gx : 0;
+  const int h = ly * H2X + lx;
+  const T vw = v[h - 1], ve = v[h + 1], vs = v[h - H2X], vn = v[h + H2X];
+  if constexpr (FAM == 1) {
+    cplx acc = axpy_r(cf[2 * H2N + h], vw, cplx{0, 0});
+    acc = axpy_r(cf[3 * H2N + h], ve, acc);
+    acc = axpy_r(cf[4 * H2N + h], vs, acc);
+    acc = axpy_r(cf[5 * H2N + h], vn, acc);
+    return acc;
+  } else if constexpr (FAM == 2) {
+    const T vsw = v[h - H2X - 1], vne = v[h + H2X + 1];
+    return cf[1 * H2N + h] * vw + cf[2 * H2N + h] * ve + cf[3 * H2N + h] * vs + cf[4 * H2N + h] * vn +
+           cf[5 * H2N + h] * vsw + cf[6 * H2N + h] * vne;
+  } else {
+    const T vsw = v[h - H2X - 1], vne = v[h + H2X + 1];
+    const T vv[6] = {vw, ve, vs, vn, vsw, vne};
+    T acc = zero_of(T{});
+#pragma unroll
+    for (int d = 1; d <= 6; ++d) {
+      const double mm = cf[(7 + d) * H2N + h];
+      acc = acc + mul(cplx{fma(l.re, mm, cf[d * H2N + h]), l.im * mm}, vv[d - 1]);
+    }
+    return acc;
+  }
+}
+
+template <int MODE, int FAM>
+static constexpr size_t fused_smem(bool down) {
+  return (size_t)CoefPlanes<FAM>::planes * H2N * sizeof(double) +
+         (size_t)3 * H2N * sizeof(TT<MODE>) + (down ? (size_t)QN * sizeof(TT<MODE>) : 0);
+}
+
+template <int MODE>
+__device__ __forceinline__ cplx lam_of(const Op<MODE>& op, int b) {
+  if constexpr (MODE == 0) return op.lam[b];
+  else return cplx{0, 0};
+}
+
+template <int MODE, int FAM, int SM>
+__global__ void __launch_bounds__(NT, 3) k_down(Op<MODE> op, Op<MODE> opc, const TT<MODE>* __restrict__ rv,
+                                                TT<MODE>* __restrict__ z2out, TT<MODE>* __restrict__ bc,
+                                                const int* __restrict__ active, double omega, int nb, int BB) {
+  using T = TT<MODE>;
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* cf = reinterpret_cast<double*>(dsm);
+  T* sR = reinterpret_cast<T*>(dsm + (size_t)CoefPlanes<FAM>::planes * H2N * sizeof(double));
+  T* sZ = sR + H2N;
+  T* sW = sZ + H2N;
+  T* sQ = sW + H2N;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int m = op.m, n = op.n;
+  if constexpr (FAM != 2) stage_coefs<MODE, FAM>(op, cf, 0, x0, y0);
+  // my two H2 elements
+  auto h2idx = [&](int k) {
+    const int ly = k / H2X, lx = k - ly * H2X;
+    const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
+    return (k < H2N && gx >= 0 && gx < m && gy >= 0 && gy < m) ? gy * m + gx : -1;
+  };
+  const int ia = h2idx(tid), ib = h2idx(tid + NT);
+  const bool hasb = tid + NT < H2N;
   // coarse node of this thread (first 64 threads)
   const int mcs = opc.m, nc = opc.n;
   const int cxl = tid & 15, cyl = tid >> 4;
   const int X = (x0 >> 1) + cxl, Y = (y0 >> 1) + cyl;
   const bool cin = tid < 64 && X < mcs && Y < mcs;
   const int ci = cin ? Y * mcs + X : 0;
-  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{}), be = zero_of(T{});
+  T ra = zero_of(T{}), rb = zero_of(T{});
   auto fetch = [&](int b) {
     const size_t o = (size_t)b * n;
-    if (h.ia >= 0) z0 = zf[o + h.ia];
-    if (h.ib >= 0) z1 = zf[o + h.ib];
-    if (in) bo = bf[o + i];
-    if (ein) be = bf[o + ei];
+    ra = ia >= 0 ? rv[o + ia] : zero_of(T{});
+    rb = ib >= 0 ? rv[o + ib] : zero_of(T{});
   };
   int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
   if (b >= 0) fetch(b);
   while (b >= 0) {
     const int bn = next_active(active, b, nb, BB);
-    Halo<RX, RN>::store(s, tid, h.ia >= 0 ? z0 : zero_of(T{}));
-    if (has1) Halo<RX, RN>::store(s, tid + NT, h.ib >= 0 ? z1 : zero_of(T{}));
-    const T bi = bo, bei = be;
+    if constexpr (FAM == 2) stage_coefs<MODE, FAM>(op, cf, b, x0, y0);
+    sR[tid] = ra;
+    if (hasb) sR[tid + NT] = rb;
     __syncthreads();
     if (bn >= 0) fetch(bn);
-    res[ty][tx] = in ? bi - apply_tile(cx.at(op, b, i, tid), s, tx + 1, ty + 1) : zero_of(T{});
-    if (ex >= 0) {
-      T rr = zero_of(T{});
-      if (ein) {
-        T a[7];
-        coef_global<MODE>(op, b, ei, a);
-        const int lx = ex + 1, ly = ey + 1;
-        T acc = mul(a[0], s[ly][lx]);
-        acc = acc + mul(a[1], s[ly][lx - 1]);
-        acc = acc + mul(a[2], s[ly][lx + 1]);
-        acc = acc + mul(a[3], s[ly - 1][lx]);
-        acc = acc + mul(a[4], s[ly + 1][lx]);
-        acc = acc + mul(a[5], s[ly - 1][lx - 1]);
-        acc = acc + mul(a[6], s[ly + 1][lx + 1]);
-        rr = bei - acc;
+    const cplx l = lam_of(op, b);
+    // half-step 1 on H2 (from zero)
+    for (int k = tid; k < H2N; k += NT) {
+      const int ly = k / H2X, lx = k - ly * H2X;
+      const T d = cdiag<MODE, FAM>(cf, k, l);
+      T v;
+      if constexpr (SM == SM_RB) {
+        const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
+        v = red ? mul(sR[k], inv_of(d)) : zero_of(T{});
+      } else {
+        v = omega * mul(sR[k], inv_of(d));
       }
-      res[ey][ex] = rr;
+      sZ[k] = v;
+    }
+    __syncthreads();
+    // half-step 2 on D
+    for (int k = tid; k < DN; k += NT) {
+      const int ly = 1 + k / DX, lx = 1 + (k - (ly - 1) * DX);
+      const int h = ly * H2X + lx;
+      const T d = cdiag<MODE, FAM>(cf, h, l);
+      const T off = coff<MODE, FAM>(cf, sZ, lx, ly, l);
+      T v;
+      if constexpr (SM == SM_RB) {
+        const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
+        v = red ? sZ[h] : mul(sR[h] - off, inv_of(d));
+      } else {
+        v = sZ[h] + omega * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
+      }
+      sW[h] = v;
+    }
+    __syncthreads();
+    // residual r - A z2 on [2,35)x[2,11); z2 of the tile to global
+    for (int k = tid; k < QN; k += NT) {
+      const int qy = k / QX, qx = k - qy * QX;
+      const int lx = 2 + qx, ly = 2 + qy, h = ly * H2X + lx;
+      const T z = sW[h];
+      sQ[k] = sR[h] - coff<MODE, FAM>(cf, sW, lx, ly, l) - mul(cdiag<MODE, FAM>(cf, h, l), z);
+      const int gx = x0 + qx, gy = y0 + qy;
+      if (qx < TX && qy < TY && gx < m && gy < m) z2out[(size_t)b * n + gy * m + gx] = z;
     }
     __syncthreads();
     if (cin) {
-      const int fx = 2 * cxl + 1, fy = 2 * cyl + 1;  // local fine centre
-      const T side = res[fy][fx - 1] + res[fy][fx + 1] + res[fy - 1][fx] + res[fy + 1][fx] +
-                     res[fy - 1][fx - 1] + res[fy + 1][fx + 1];
-      const T acc = res[fy][fx] + 0.5 * side;
-      const size_t oc = (size_t)b * nc;
-      bc[oc + ci] = acc;
-      if (zc) zc[oc + ci] = omega * mul(acc, inv_of(diag_global<MODE>(opc, b, ci)));
+      const int fx = 2 * cxl + 1, fy = 2 * cyl + 1;  // local fine centre in sQ
+      const T side = sQ[fy * QX + fx - 1] + sQ[fy * QX + fx + 1] + sQ[(fy - 1) * QX + fx] +
+                     sQ[(fy + 1) * QX + fx] + sQ[(fy - 1) * QX + fx - 1] + sQ[(fy + 1) * QX + fx + 1];
+      bc[(size_t)b * nc + ci] = sQ[fy * QX + fx] + 0.5 * side;
     }
     __syncthreads();
     b = bn;
   }
 }
 
-// zc = z_in + P xc on the tile + halo (shared), then z_out = zc + omega (b - A zc)/a_C
-template <int MODE, int FAM>
-__global__ void __launch_bounds__(NT, 4) k_prolong_smooth(Op<MODE> op, const TT<MODE>* __restrict__ bv,
-                                                          const TT<MODE>* __restrict__ zin,
-                                                          const TT<MODE>* __restrict__ xc, int mc,
-                                                          TT<MODE>* __restrict__ zout,
-                                                          const int* __restrict__ active, double omega,
-                                                          int nb, int BB, int dot, double* __restrict__ part) {
+template <int MODE, int FAM, int SM>
+__global__ void __launch_bounds__(NT, 3) k_up(Op<MODE> op, const TT<MODE>* __restrict__ rv,
+                                              const TT<MODE>* __restrict__ z2in,
+                                              const TT<MODE>* __restrict__ xc, int mc,
+                                              TT<MODE>* __restrict__ zout, const int* __restrict__ active,
+                                              double omega, int nb, int BB, int dot,
+                                              double* __restrict__ part) {
   using T = TT<MODE>;
-  __shared__ T s[HY][HX];
-  __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
-  TILE_PROLOGUE
-  Ctx<MODE, FAM> cx;
-  if constexpr (FAM == 0) cx.st = st_;
-  cx.init(op, i, in, tid);
+  extern __shared__ __align__(16) unsigned char dsm[];
+  double* cf = reinterpret_cast<double*>(dsm);
+  T* sR = reinterpret_cast<T*>(dsm + (size_t)CoefPlanes<FAM>::planes * H2N * sizeof(double));
+  T* sZ = sR + H2N;
+  T* sW = sZ + H2N;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
+  const int m = op.m, n = op.n;
   const int nc = mc * mc;
-  Halo<HX, HN> h;
-  h.init(tid, x0, y0, m);
-  const bool has1 = tid + NT < HN;
-  // coarse parents of the two halo elements: linear coarse index, first weight
-  // (1 or 1/2; a second parent, if any, always weighs 1/2)
-  int pa0 = -1, pa1 = -1, pb0 = -1, pb1 = -1;
+  if constexpr (FAM != 2) stage_coefs<MODE, FAM>(op, cf, 0, x0, y0);
+  int ia = -1, ib = -1, pa0 = -1, pa1 = -1, pb0 = -1, pb1 = -1;
   double wa = 0, wb = 0;
   {
-    int cxp[2], cyp[2];
-    double w[2];
-    if (h.ia >= 0) {
-      const int np = parents(h.ia % m, h.ia / m, mc, cxp, cyp, w);
-      if (np > 0) { pa0 = cyp[0] * mc + cxp[0]; wa = w[0]; }
-      if (np > 1) pa1 = cyp[1] * mc + cxp[1];
-    }
-    if (h.ib >= 0) {
-      const int np = parents(h.ib % m, h.ib / m, mc, cxp, cyp, w);
-      if (np > 0) { pb0 = cyp[0] * mc + cxp[0]; wb = w[0]; }
-      if (np > 1) pb1 = cyp[1] * mc + cxp[1];
-    }
+    auto setup = [&](int k, int& idx, int& p0, int& p1, double& w0) {
+      if (k >= H2N) return;
+      const int ly = k / H2X, lx = k - ly * H2X;
+      const int gx = x0 - 2 + lx, gy = y0 - 2 + ly;
+      if (gx < 0 || gx >= m || gy < 0 || gy >= m) return;
+      idx = gy * m + gx;
+      int cxp[2], cyp[2];
+      double w[2];
+      const int np = parents(gx, gy, mc, cxp, cyp, w);
+      if (np > 0) { p0 = cyp[0] * mc + cxp[0]; w0 = w[0]; }
+      if (np > 1) p1 = cyp[1] * mc + cxp[1];
+    };
+    setup(tid, ia, pa0, pa1, wa);
+    setup(tid + NT, ib, pb0, pb1, wb);
   }
-  T z0 = zero_of(T{}), z1 = zero_of(T{}), bo = zero_of(T{});
+  const bool hasb = tid + NT < H2N;
+  T za = zero_of(T{}), zb = zero_of(T{}), ra = zero_of(T{}), rb = zero_of(T{});
   auto fetch = [&](int b) {
     const size_t o = (size_t)b * n, oc = (size_t)b * nc;
-    if (h.ia >= 0) {
-      T v = zin[o + h.ia];
-      if (pa0 >= 0) v = v + wa * xc[oc + pa0];
-      if (pa1 >= 0) v = v + 0.5 * xc[oc + pa1];
-      z0 = v;
+    za = zero_of(T{});
+    ra = zero_of(T{});
+    if (ia >= 0) {
+      za = z2in[o + ia];
+      if (pa0 >= 0) za = za + wa * xc[oc + pa0];
+      if (pa1 >= 0) za = za + 0.5 * xc[oc + pa1];
+      ra = rv[o + ia];
     }
-    if (h.ib >= 0) {
-      T v = zin[o + h.ib];
-      if (pb0 >= 0) v = v + wb * xc[oc + pb0];
-      if (pb1 >= 0) v = v + 0.5 * xc[oc + pb1];
-      z1 = v;
+    zb = zero_of(T{});
+    rb = zero_of(T{});
+    if (ib >= 0) {
+      zb = z2in[o + ib];
+      if (pb0 >= 0) zb = zb + wb * xc[oc + pb0];
+      if (pb1 >= 0) zb = zb + 0.5 * xc[oc + pb1];
+      rb = rv[o + ib];
     }
-    if (in) bo = bv[o + i];
   };
   int b = next_active(active, blockIdx.z * BB - 1, nb, BB);
   if (b >= 0) fetch(b);
   while (b >= 0) {
     const int bn = next_active(active, b, nb, BB);
-    Halo<HX, HN>::store(s, tid, h.ia >= 0 ? z0 : zero_of(T{}));
-    if (has1) Halo<HX, HN>::store(s, tid + NT, h.ib >= 0 ? z1 : zero_of(T{}));
-    const T bi = bo;
+    if constexpr (FAM == 2) stage_coefs<MODE, FAM>(op, cf, b, x0, y0);
+    sZ[tid] = za;
+    sR[tid] = ra;
+    if (hasb) {
+      sZ[tid + NT] = zb;
+      sR[tid + NT] = rb;
+    }
     __syncthreads();
     if (bn >= 0) fetch(bn);
-    double v[2] = {0, 0};
-    if (in) {
-      const auto a = cx.at(op, b, i, tid);
-      const T zo = s[ty + 1][tx + 1] + omega * mul(bi - apply_tile(a, s, tx + 1, ty + 1), inv_of(a.diag()));
-      zout[(size_t)b * n + i] = zo;
-      if (dot) add_dot(v, bi, zo);
+    const cplx l = lam_of(op, b);
+    // post half-step 1 on H1 (Jacobi, or the black points of a backward sweep)
+    for (int k = tid; k < H1N; k += NT) {
+      const int ly = 1 + k / H1X, lx = 1 + (k - (ly - 1) * H1X);
+      const int h = ly * H2X + lx;
+      const T d = cdiag<MODE, FAM>(cf, h, l);
+      const T off = coff<MODE, FAM>(cf, sZ, lx, ly, l);
+      T v;
+      if constexpr (SM == SM_RB) {
+        const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
+        v = red ? sZ[h] : mul(sR[h] - off, inv_of(d));
+      } else {
+        v = sZ[h] + omega * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
+      }
+      sW[h] = v;
     }
-    if (dot) block_pair(v[0], v[1], part, b);
+    __syncthreads();
+    // post half-step 2 on the tile (Jacobi, or the red points)
+    double vd[2] = {0, 0};
+    {
+      const int lx = tx + 2, ly = ty + 2, h = ly * H2X + lx;
+      const int gx = x0 + tx, gy = y0 + ty;
+      if (gx < m && gy < m) {
+        const T d = cdiag<MODE, FAM>(cf, h, l);
+        const T off = coff<MODE, FAM>(cf, sW, lx, ly, l);
+        T v;
+        if constexpr (SM == SM_RB) {
+          const int red = ((gx + gy) & 1) == 0;
+          v = red ? mul(sR[h] - off, inv_of(d)) : sW[h];
+        } else {
+          v = sW[h] + omega * mul(sR[h] - off - mul(d, sW[h]), inv_of(d));
+        }
+        zout[(size_t)b * n + gy * m + gx] = v;
+        if (dot) add_dot(vd, sR[h], v);
+      }
+    }
+    if (dot) block_pair(vd[0], vd[1], part, b);
     __syncthreads();
     b = bn;
   }
@@ -947,6 +1057,17 @@ BatchSolver<MODE>::~BatchSolver() {
     if (e) cudaEventDestroy(e);
 }
 
+template <int MODE, int FAM, int SM>
+static void set_fused_attrs() {
+  static bool done = false;
+  if (done) return;
+  TP_CUDA(cudaFuncSetAttribute(k_down<MODE, FAM, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)fused_smem<MODE, FAM>(true)));
+  TP_CUDA(cudaFuncSetAttribute(k_up<MODE, FAM, SM>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)fused_smem<MODE, FAM>(false)));
+  done = true;
+}
+
 template <int MODE>
 typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, const T* bl, T*, bool,
                                                               bool dot) {
@@ -976,40 +1097,34 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
     }
     return lz0[0].get();
   }
-  T* z = lz0[l].get();
-  T* o = lz1[l].get();
-  for (int k = 1; k < cfg.pre; ++k) {
-    DISPATCH_FAM(l, (k_smooth<MODE, FAM><<<g.grid, blk, 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, 0, part.get())));
-    TP_LAUNCHED(p);
-    std::swap(z, o);
-  }
-  const bool coarse_next = (l + 1 == L - 1);
   const Op<MODE> opc = make_op<MODE>(ops[l + 1], lam);
-  T* zc0 = coarse_next ? nullptr : lz0[l + 1].get();
-  DISPATCH_FAM(l, (k_restrict<MODE, FAM><<<g.grid, blk, 0, s>>>(op, opc, bl, z, lb[l + 1].get(), zc0, act,
-                                                                cfg.omega, nb, g.BB)));
+  T* z2 = lz0[l].get();
+  T* zo = lz1[l].get();
+  const bool rb = cfg.rb_fine && ops[l].five;
+  // down: smoothing from zero, residual, restriction
+#define LAUNCH_DOWN(SMV)                                                                        \
+  DISPATCH_FAM(l, (set_fused_attrs<MODE, FAM, SMV>(),                                          \
+                   k_down<MODE, FAM, SMV><<<g.grid, blk, fused_smem<MODE, FAM>(true), s>>>(     \
+                       op, opc, bl, z2, lb[l + 1].get(), act, cfg.omega, nb, g.BB)))
+  if (rb) { LAUNCH_DOWN(SM_RB); } else { LAUNCH_DOWN(SM_JAC); }
   TP_LAUNCHED(p);
   T* xc;
-  if (coarse_next) {
+  if (l + 1 == L - 1) {
     k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
     TP_LAUNCHED(p);
     xc = lz0[l + 1].get();
   } else {
     xc = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
   }
-  const int pdot = (dot && cfg.post == 1) ? 1 : 0;
   const int mcl = ops[l + 1].m;
-  DISPATCH_FAM(l, (k_prolong_smooth<MODE, FAM><<<g.grid, blk, 0, s>>>(op, bl, z, xc, mcl, o, act, cfg.omega,
-                                                                      nb, g.BB, pdot, part.get())));
+  const int d = dot ? 1 : 0;
+#define LAUNCH_UP(SMV)                                                                          \
+  DISPATCH_FAM(l, (set_fused_attrs<MODE, FAM, SMV>(),                                          \
+                   k_up<MODE, FAM, SMV><<<g.grid, blk, fused_smem<MODE, FAM>(false), s>>>(      \
+                       op, bl, z2, xc, mcl, zo, act, cfg.omega, nb, g.BB, d, part.get())))
+  if (rb) { LAUNCH_UP(SM_RB); } else { LAUNCH_UP(SM_JAC); }
   TP_LAUNCHED(p);
-  std::swap(z, o);
-  for (int k = 1; k < cfg.post; ++k) {
-    const int d = (dot && k == cfg.post - 1) ? 1 : 0;
-    DISPATCH_FAM(l, (k_smooth<MODE, FAM><<<g.grid, blk, 0, s>>>(op, bl, z, o, act, cfg.omega, nb, g.BB, d, part.get())));
-    TP_LAUNCHED(p);
-    std::swap(z, o);
-  }
-  return z;
+  return zo;
 }
 
 template <int MODE>
@@ -1041,8 +1156,6 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int64_t batch_iters = 0;
   int last_active = h_count[0];
   if (last_active > 0) {
-    k_jacobi0<MODE><<<g0.grid, blk, 0, s>>>(op0, r.get(), lz0[0].get(), act, cfg.omega, nb, g0.BB);
-    TP_LAUNCHED(p);
     T* z = vcycle_level(0, nb, r.get(), nullptr, false, true);
     k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
                                     alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
@@ -1059,7 +1172,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
       TP_LAUNCHED(p);
       k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, r.get(), pout, q.get(), alpha.get(), act, cfg.omega,
-                                             ops.size() > 1 ? lz0[0].get() : nullptr, nb, g0.BB,
+                                             nullptr, nb, g0.BB,
                                              part.get());
       TP_LAUNCHED(p);
       k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per0, nb, rtol2, rho.get(), mu.get(),

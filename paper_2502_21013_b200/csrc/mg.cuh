@@ -24,6 +24,7 @@ struct MGConfig {
   double omega = 0.8;       // Jacobi damping
   double rtol = 1e-13;      // ||r_b|| <= rtol ||b_b||
   int max_iter = 200;
+  bool rb_fine = true;      // red-black Gauss-Seidel on the 5-point fine level
 };
 
 // Stencils of one level for the whole batch (slice mode) or shared (freq mode).

@@ -9,6 +9,7 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <numbers>
@@ -322,6 +323,9 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
   mc.max_iter = cfg.inner_max_iter;
+  // experiment overrides (documented in DESIGN.md §5)
+  if (const char* e = std::getenv("TPGPU_RB_FINE")) mc.rb_fine = std::atoi(e) != 0;
+  if (const char* e = std::getenv("TPGPU_OMEGA")) mc.omega = std::atof(e);
   fw->solver.init(this, ops, chunk, mc);
   TP_CUDA(cudaStreamSynchronize(stream));
   freq_ready = true;
