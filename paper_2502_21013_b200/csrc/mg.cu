@@ -1036,7 +1036,8 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   p1.alloc(n0);
   q.alloc(n0);
   const size_t tiles = (size_t)((levels[0].m + TX - 1) / TX) * ((levels[0].m + TY - 1) / TY);
-  part.alloc((size_t)B * tiles * 2 + 64);
+  const size_t perf = (size_t)fine_partials(levels[0].m, 0) + fine_partials(levels[0].m, 2);
+  part.alloc((size_t)B * (tiles + perf) * 2 + 64);
   rho.alloc(B);
   mu.alloc(B);
   alpha.alloc(B);
@@ -1100,6 +1101,23 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   const Op<MODE> opc = make_op<MODE>(ops[l + 1], lam);
   T* z2 = lz0[l].get();
   T* zo = lz1[l].get();
+  if constexpr (MODE == 0) {
+    if (ops[l].fine.cmat) {
+      FineOp fo = ops[l].fine;
+      fo.lam = lam;
+      launch_fine_down(*p, fo, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, nb);
+      T* xcf;
+      if (l + 1 == L - 1) {
+        k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
+        TP_LAUNCHED(p);
+        xcf = lz0[l + 1].get();
+      } else {
+        xcf = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
+      }
+      launch_fine_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, nb, dot ? 1 : 0, part.get());
+      return zo;
+    }
+  }
   const bool rb = cfg.rb_fine && ops[l].five;
   // down: smoothing from zero, residual, restriction
 #define LAUNCH_DOWN(SMV)                                                                        \
@@ -1133,15 +1151,27 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const Op<MODE> op0 = make_op<MODE>(ops[0], lam);
   const Geo g0 = geo_for(ops[0].m, nb, p->num_sms, 8);
   const dim3 blk(TX, TY);
-  const int per0 = g0.tiles;
+  const bool fine = MODE == 0 && ops[0].fine.cmat != nullptr;
+  FineOp fo = ops[0].fine;
+  fo.lam = reinterpret_cast<const cplx*>(lam);
+  // partials per batch of each producing kernel
+  const int per_t = g0.tiles;
+  const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // init, apply
+  const int per_u = fine ? fine_partials(ops[0].m, 2) : per_t;   // V-cycle dot (up)
+  const int per0 = per_t;
+  (void)per0;
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
   cudaStream_t s = p->stream;
   const int l = 0;
-  DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
-  TP_LAUNCHED(p);
-  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), per0, nb, rtol2, rho.get(), mu.get(), alpha.get(),
+  if (fine && warm) {
+    if constexpr (MODE == 0) launch_fine_apply(*p, fo, b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
+  } else {
+    DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
+    TP_LAUNCHED(p);
+  }
+  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (fine && warm) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(),
                                   beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
   TP_LAUNCHED(p);
   if (warm) {
@@ -1157,7 +1187,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int last_active = h_count[0];
   if (last_active > 0) {
     T* z = vcycle_level(0, nb, r.get(), nullptr, false, true);
-    k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
+    k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
                                     alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
     TP_LAUNCHED(p);
     T* pin = p0.get();
@@ -1165,17 +1195,21 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
-      DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
-                                                                      first, nb, g0.BB, part.get())));
-      TP_LAUNCHED(p);
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
+      if (fine) {
+        if constexpr (MODE == 0) launch_fine_apply(*p, fo, z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false);
+      } else {
+        DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
+                                                                        first, nb, g0.BB, part.get())));
+        TP_LAUNCHED(p);
+      }
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), fine ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
       TP_LAUNCHED(p);
       k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, r.get(), pout, q.get(), alpha.get(), act, cfg.omega,
                                              nullptr, nb, g0.BB,
                                              part.get());
       TP_LAUNCHED(p);
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
       TP_LAUNCHED(p);
       const int slot = it & 1;
@@ -1195,7 +1229,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       }
       iters = it;
       z = vcycle_level(0, nb, r.get(), nullptr, false, true);
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_BETA, part.get(), per0, nb, rtol2, rho.get(), mu.get(),
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
       TP_LAUNCHED(p);
       std::swap(pin, pout);

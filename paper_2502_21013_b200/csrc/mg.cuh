@@ -27,12 +27,23 @@ struct MGConfig {
   bool rb_fine = true;      // red-black Gauss-Seidel on the 5-point fine level
 };
 
+// Fine-level operator data for the streaming kernels (mg_fine.cu): K_hat
+// regenerated from cell materials + nu_hat, lumped mass diagonal.
+struct FineOp {
+  const uint8_t* cmat = nullptr;  // cells*cells
+  const double* nuh = nullptr;    // nu_hat per material
+  const double* mass = nullptr;   // n
+  const cplx* lam = nullptr;      // per batch symbol
+  int m = 0, c = 0, n = 0;
+};
+
 // Stencils of one level for the whole batch (slice mode) or shared (freq mode).
 struct LevelOp {
   int m = 0, n = 0;
   const double* K = nullptr;  // freq: 7n shared ; slice: 7n per batch (stride 7n)
   const double* M = nullptr;  // freq only
   bool five = false;          // freq mode: K 5-point and M diagonal (fine level)
+  FineOp fine;                // freq mode level 0: streaming kernels (cmat != nullptr)
 };
 
 template <int MODE>
@@ -74,6 +85,14 @@ void launch_rap(Problem& p, const double* Af, int mf, double* Ac, int mc, int ba
 void launch_coarse_inverse_freq(Problem& p, const double* K, const double* M, int m,
                                 const cplx* lam, cplx* inv, int batches);
 void launch_coarse_inverse_slice(Problem& p, const double* J, int m, double* inv, int batches);
+// Fine-level streaming kernels (mg_fine.cu).  kind: 0 apply, 1 down, 2 up.
+int fine_partials(int m, int kind);
+void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
+                       const cplx* beta, const int* active, int first, int nb, double* part, bool init);
+void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
+                      const int* active, double omega, int nb);
+void launch_fine_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
+                    cplx* z, const int* active, double omega, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).
 void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches);
 

@@ -58,7 +58,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   DevBuf<int> d_slice(S), d_active(S), d_acc(S);
   DevBuf<double> d_alpha(S);
   std::vector<LevelOp> ops(nl);
-  for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], J[l].get(), nullptr, false};
+  for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], J[l].get(), nullptr, false, {}};
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
   mc.max_iter = cfg.inner_max_iter;

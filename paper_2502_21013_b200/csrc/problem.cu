@@ -319,7 +319,9 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   chunk = std::max(1, std::min(chunk, K));
   fw->chunk = chunk;
   std::vector<LevelOp> ops(nl);
-  for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get(), l == 0};
+  for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get(), l == 0, {}};
+  if (!std::getenv("TPGPU_NO_STREAM_FINE"))
+    ops[0].fine = {d_cell_mat.get(), d_nu_hat.get(), d_mass.get(), nullptr, m, c, n};
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
   mc.max_iter = cfg.inner_max_iter;
