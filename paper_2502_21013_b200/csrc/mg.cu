@@ -1102,7 +1102,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   T* z2 = lz0[l].get();
   T* zo = lz1[l].get();
   if constexpr (MODE == 0) {
-    if (ops[l].fine.cmat) {
+    if (ops[l].fine.we) {
       FineOp fo = ops[l].fine;
       fo.lam = lam;
       launch_fine_down(*p, fo, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, nb);
@@ -1151,7 +1151,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const Op<MODE> op0 = make_op<MODE>(ops[0], lam);
   const Geo g0 = geo_for(ops[0].m, nb, p->num_sms, 8);
   const dim3 blk(TX, TY);
-  const bool fine = MODE == 0 && ops[0].fine.cmat != nullptr;
+  const bool fine = MODE == 0 && ops[0].fine.we != nullptr;
   FineOp fo = ops[0].fine;
   fo.lam = reinterpret_cast<const cplx*>(lam);
   // partials per batch of each producing kernel

@@ -30,8 +30,8 @@ struct MGConfig {
 // Fine-level operator data for the streaming kernels (mg_fine.cu): K_hat
 // regenerated from cell materials + nu_hat, lumped mass diagonal.
 struct FineOp {
-  const uint8_t* cmat = nullptr;  // cells*cells
-  const double* nuh = nullptr;    // nu_hat per material
+  const double* we = nullptr;     // (cells+1)^2 vertex grid: K_hat edge weight (X,Y)-(X+1,Y)
+  const double* wn = nullptr;     // (cells+1)^2 vertex grid: K_hat edge weight (X,Y)-(X,Y+1)
   const double* mass = nullptr;   // n
   const cplx* lam = nullptr;      // per batch symbol
   int m = 0, c = 0, n = 0;
@@ -43,7 +43,7 @@ struct LevelOp {
   const double* K = nullptr;  // freq: 7n shared ; slice: 7n per batch (stride 7n)
   const double* M = nullptr;  // freq only
   bool five = false;          // freq mode: K 5-point and M diagonal (fine level)
-  FineOp fine;                // freq mode level 0: streaming kernels (cmat != nullptr)
+  FineOp fine;                // freq mode level 0: streaming kernels (we != nullptr)
 };
 
 template <int MODE>

@@ -32,10 +32,6 @@ constexpr int RH = 64;     // rows per warp work item
 __device__ __forceinline__ cplx cm(cplx a, cplx b) {
   return {fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
 }
-__device__ __forceinline__ cplx cinv(cplx a) {
-  const double d = 1.0 / fma(a.re, a.re, a.im * a.im);
-  return {a.re * d, -a.im * d};
-}
 __device__ __forceinline__ cplx cs(double s, cplx a) { return {s * a.re, s * a.im}; }
 __device__ __forceinline__ cplx shf_up(cplx v) {
   return {__shfl_up_sync(0xffffffffu, v.re, 1), __shfl_up_sync(0xffffffffu, v.im, 1)};
@@ -44,42 +40,65 @@ __device__ __forceinline__ cplx shf_dn(cplx v) {
   return {__shfl_down_sync(0xffffffffu, v.re, 1), __shfl_down_sync(0xffffffffu, v.im, 1)};
 }
 
-// Per-lane coefficient rows.  Cell row j: A = nu_hat(mat(x+1, j)), B = nu_hat(mat(x, j)).
-struct CellRow {
-  double A, B;
+// Per-row coefficients of the lane's node: K_hat edge weights to E/W/N/S
+// (the diagonal is their sum) and the lumped mass.  op.we / op.wn are
+// (c+1)^2 vertex grids: we[Y][X] = weight of the edge (X,Y)-(X+1,Y),
+// wn[Y][X] = weight of the edge (X,Y)-(X,Y+1); node (x,y) is vertex (x+1,y+1).
+struct RowK {
+  double we, ww, wn, ws, mm;
 };
 
-__device__ __forceinline__ CellRow cell_row(const FineOp& op, int x, int j) {
-  // lanes outside the domain (x < 0 or x >= m) read clamped cells; their
-  // values never reach an owned output (vectors are zero there)
-  const int c = op.c;
-  const int jj = min(max(j, 0), c - 1);
-  const int i1 = min(max(x + 1, 0), c - 1), i0 = min(max(x, 0), c - 1);
-  const uint8_t* row = op.cmat + (size_t)jj * c;
-  return {__ldg(op.nuh + row[i1]), __ldg(op.nuh + row[i0])};
-}
-
-struct Coef {
-  double kc, we, ww, wn, ws, mm;
-};
-
-// node row y uses cell rows y (lower) and y+1 (upper)
-__device__ __forceinline__ Coef coef_of(const CellRow& lo, const CellRow& up, double mass) {
-  Coef k;
-  k.we = 0.5 * (up.A + lo.A);
-  k.ww = 0.5 * (up.B + lo.B);
-  k.wn = 0.5 * (up.A + up.B);
-  k.ws = 0.5 * (lo.A + lo.B);
-  k.kc = (up.A + lo.A) + (up.B + lo.B);
-  k.mm = mass;
+// Load the lane's row-y coefficients; ws comes from the previous row's wn,
+// ww from the west lane's we (warp shuffle, all lanes participate).
+__device__ __forceinline__ RowK row_k(const FineOp& op, int x, int y, double wn_prev) {
+  const int c = op.c, m = op.m;
+  const int X = min(max(x + 1, 0), c), Y = min(max(y + 1, 0), c);
+  const size_t v = (size_t)Y * (c + 1) + X;
+  RowK k;
+  k.we = __ldg(op.we + v);
+  k.wn = __ldg(op.wn + v);
+  k.ww = __shfl_up_sync(0xffffffffu, k.we, 1);
+  k.ws = wn_prev;
+  k.mm = (x >= 0 && x < m && y >= 0 && y < m) ? __ldg(op.mass + (size_t)y * m + x) : 0.0;
   return k;
 }
+// Compact per-row window entry: the lane's own we, wn and mass.
+struct RowW {
+  double we, wn, mm;
+};
+__device__ __forceinline__ RowW row_w(const FineOp& op, int x, int y) {
+  const int c = op.c, m = op.m;
+  const int X = min(max(x + 1, 0), c), Y = min(max(y + 1, 0), c);
+  const size_t v = (size_t)Y * (c + 1) + X;
+  RowW w;
+  w.we = __ldg(op.we + v);
+  w.wn = __ldg(op.wn + v);
+  w.mm = (x >= 0 && x < m && y >= 0 && y < m) ? __ldg(op.mass + (size_t)y * m + x) : 0.0;
+  return w;
+}
+// full coefficients of a row from its window entry and the row below (all lanes call)
+__device__ __forceinline__ RowK expand(const RowW& w, const RowW& below) {
+  return {w.we, __shfl_up_sync(0xffffffffu, w.we, 1), w.wn, below.wn, w.mm};
+}
+// wn of row y-1 for the first row of a chunk
+__device__ __forceinline__ double wn_of(const FineOp& op, int x, int y) {
+  const int c = op.c;
+  const int X = min(max(x + 1, 0), c), Y = min(max(y + 1, 0), c);
+  return __ldg(op.wn + (size_t)Y * (c + 1) + X);
+}
 
-__device__ __forceinline__ cplx diag(const Coef& k, cplx l) { return {fma(l.re, k.mm, k.kc), l.im * k.mm}; }
+__device__ __forceinline__ cplx diag(const RowK& k, cplx l) {
+  const double kc = (k.we + k.ww) + (k.wn + k.ws);
+  return {fma(l.re, k.mm, kc), l.im * k.mm};
+}
+__device__ __forceinline__ cplx rcp(cplx a) {
+  const double d = __drcp_rn(fma(a.re, a.re, a.im * a.im));
+  return {a.re * d, -a.im * d};
+}
 
 // (A v) at a node: d v - wE vE - wW vW - wN vN - wS vS (neighbours of
 // Dirichlet vertices are zero vectors, their edge weights stay on the diagonal)
-__device__ __forceinline__ cplx apply_at(const Coef& k, cplx l, cplx v, cplx vw, cplx ve, cplx vs, cplx vn) {
+__device__ __forceinline__ cplx apply_at(const RowK& k, cplx l, cplx v, cplx vw, cplx ve, cplx vs, cplx vn) {
   cplx acc = cm(diag(k, l), v);
   acc.re -= k.we * ve.re + k.ww * vw.re + k.wn * vn.re + k.ws * vs.re;
   acc.im -= k.we * ve.im + k.ww * vw.im + k.wn * vn.im + k.ws * vs.im;
@@ -113,19 +132,26 @@ __device__ __forceinline__ Item item_of(int m, int own, int nb, const int* __res
   return it;
 }
 
-__device__ __forceinline__ cplx ld(const cplx* __restrict__ v, int x, int y, int m, bool colok) {
-  return (colok && y >= 0 && y < m) ? v[(size_t)y * m + x] : cplx{0, 0};
-}
+
+// Row-streamed vector access: pointer to (row y, lane column), zero outside.
+struct RowPtr {
+  const cplx* p;  // element (y, x) of the current row (clamped column)
+  int m;
+  bool colok;
+  __device__ __forceinline__ cplx at(int y) const {
+    return (colok && y >= 0 && y < m) ? p[(long)y * m] : cplx{0, 0};
+  }
+};
 
 // ---------------------------------------------------------------- apply
 // INIT = 0: p = first ? z : z + beta p_in -> p_out ; q = A p ; part += p^T q
 // INIT = 1: r = b - A x (b in z, x in pin, r to q) ; part += (|b|^2, |r|^2)
 template <int INIT>
-__global__ void __launch_bounds__(WL * WPB) k_fine_apply(FineOp op, const cplx* __restrict__ z,
-                                                         const cplx* __restrict__ pin, cplx* __restrict__ pout,
-                                                         cplx* __restrict__ q, const cplx* __restrict__ beta,
-                                                         const int* __restrict__ active, int first, int nb,
-                                                         double* __restrict__ part) {
+__global__ void __launch_bounds__(WL * WPB, 6) k_fine_apply(FineOp op, const cplx* __restrict__ z,
+                                                            const cplx* __restrict__ pin, cplx* __restrict__ pout,
+                                                            cplx* __restrict__ q, const cplx* __restrict__ beta,
+                                                            const int* __restrict__ active, int first, int nb,
+                                                            double* __restrict__ part) {
   constexpr int H = 1, OWN = WL - 2 * H;
   const int m = op.m;
   const Item it = item_of(m, OWN, nb, INIT ? nullptr : active);
@@ -134,43 +160,42 @@ __global__ void __launch_bounds__(WL * WPB) k_fine_apply(FineOp op, const cplx* 
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
+  const int xc = min(max(x, 0), m - 1);
   const size_t o = (size_t)it.b * op.n;
-  const cplx* zb = z + o;
-  const cplx* pb = pin + o;
+  const RowPtr Z{z + o + xc, m, colok}, P{pin + o + xc, m, colok};
+  cplx* const po = pout + o + xc;
+  cplx* const qo = q + o + xc;
   const cplx l = op.lam[it.b];
   const cplx bt = (INIT || first) ? cplx{0, 0} : beta[it.b];
-  // rows: p at y-1, y, y+1 around the output row y
   auto pval = [&](int y) -> cplx {
-    if (INIT) return ld(pb, x, y, m, colok);  // x (solution) for the residual
-    cplx v = ld(zb, x, y, m, colok);
+    if (INIT) return P.at(y);  // x (solution) for the residual
+    cplx v = Z.at(y);
     if (!first) {
-      const cplx pp = ld(pb, x, y, m, colok);
+      const cplx pp = P.at(y);
       v = {fma(bt.re, pp.re, fma(-bt.im, pp.im, v.re)), fma(bt.re, pp.im, fma(bt.im, pp.re, v.im))};
     }
     return v;
   };
-  CellRow clo = cell_row(op, x, it.ys), cup = cell_row(op, x, it.ys + 1);
+  double wnp = wn_of(op, x, it.ys - 1);
   cplx pm = pval(it.ys - 1), p0 = pval(it.ys), pn = pval(it.ys + 1);
   double s0 = 0, s1 = 0;
   for (int y = it.ys; y < it.ye; ++y) {
-    // prefetch row y+2 and the next upper cell row
-    const cplx pnn = pval(y + 2);
-    const CellRow cnext = cell_row(op, x, y + 2);
-    const double mass = colok ? __ldg(op.mass + (size_t)y * m + x) : 0.0;
-    const Coef k = coef_of(clo, cup, mass);
+    const cplx pnn = pval(y + 2);  // next row in flight during this row's math
+    const RowK k = row_k(op, x, y, wnp);
+    wnp = k.wn;
     const cplx pw = shf_up(p0), pe = shf_dn(p0);
     const cplx Ap = apply_at(k, l, p0, pw, pe, pm, pn);
     if (own) {
-      const size_t i = o + (size_t)y * m + x;
+      const long i = (long)y * m;
       if (INIT) {
-        const cplx bi = zb[(size_t)y * m + x];
+        const cplx bi = Z.p[i];
         const cplx r = {bi.re - Ap.re, bi.im - Ap.im};
-        q[i] = r;
+        qo[i] = r;
         s0 += bi.re * bi.re + bi.im * bi.im;
         s1 += r.re * r.re + r.im * r.im;
       } else {
-        pout[i] = p0;
-        q[i] = Ap;
+        po[i] = p0;
+        qo[i] = Ap;
         const cplx t = cm(p0, Ap);
         s0 += t.re;
         s1 += t.im;
@@ -179,8 +204,6 @@ __global__ void __launch_bounds__(WL * WPB) k_fine_apply(FineOp op, const cplx* 
     pm = p0;
     p0 = pn;
     pn = pnn;
-    clo = cup;
-    cup = cnext;
   }
   warp_pair(s0, s1);
   if (lane == 0) {
@@ -194,9 +217,9 @@ __global__ void __launch_bounds__(WL * WPB) k_fine_apply(FineOp op, const cplx* 
 
 // ---------------------------------------------------------------- down
 __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx* __restrict__ rv,
-                                                        cplx* __restrict__ z2out, cplx* __restrict__ bc,
-                                                        int mc, const int* __restrict__ active, double omega,
-                                                        int nb) {
+                                                           cplx* __restrict__ z2out, cplx* __restrict__ bc,
+                                                           int mc, const int* __restrict__ active, double omega,
+                                                           int nb) {
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
   const int m = op.m;
   const Item it = item_of(m, OWN, nb, active);
@@ -205,75 +228,61 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < H + OWN && colok;
+  const int xc = min(max(x, 0), m - 1);
   const size_t o = (size_t)it.b * op.n;
-  const cplx* rb = rv + o;
+  const RowPtr R{rv + o + xc, m, colok};
+  cplx* const zo = z2out + o + xc;
   const cplx l = op.lam[it.b];
   const int ys = it.ys, ye = it.ye;
-  // pipeline over input rows yi = ys-2 .. ye+2 (z1 rows), z2 rows yi-1, residual rows yi-2
-  // windows
-  cplx r0 = {0, 0}, r1 = {0, 0}, r2 = {0, 0};      // r at yi, yi-1, yi-2
-  cplx a0 = {0, 0}, a1 = {0, 0}, a2 = {0, 0};      // z1 at yi, yi-1, yi-2
-  cplx b1 = {0, 0}, b2 = {0, 0}, b3 = {0, 0};      // z2 at yi-1, yi-2, yi-3
-  cplx q2 = {0, 0}, q3 = {0, 0}, q4 = {0, 0};      // res at yi-2, yi-3, yi-4
-  // cell rows yi+1, yi, yi-1, yi-2 and masses of node rows yi, yi-1, yi-2
-  CellRow cr0 = cell_row(op, x, ys - 1), cr1 = cell_row(op, x, ys - 2), cr2{0, 0}, cr3{0, 0};
-  double ms0 = 0, ms1 = 0, ms2 = 0;
-  cplx rnext = ld(rb, x, ys - 2, m, colok);
+  const bool cown = own && (x & 1) && (x >> 1) < mc;  // coarse centre column
+  cplx* const bco = bc + (size_t)it.b * mc * mc + (x >> 1);
+  // pipeline over input rows yi = ys-2 .. ye+2: z1 at yi, z2 at yi-1,
+  // residual at yi-2, restriction centred on yi-3
+  cplx r0{0, 0}, r1{0, 0}, r2{0, 0};  // r at yi, yi-1, yi-2
+  cplx a0{0, 0}, a1{0, 0}, a2{0, 0};  // z1 at yi, yi-1, yi-2
+  cplx b1{0, 0}, b2{0, 0}, b3{0, 0};  // z2 at yi-1, yi-2, yi-3
+  cplx q2{0, 0}, q3{0, 0}, q4{0, 0};  // res at yi-2, yi-3, yi-4
+  RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
+  cplx rnext = R.at(ys - 2);
   for (int yi = ys - 2; yi <= ye + 2; ++yi) {
     const cplx rcur = rnext;
-    if (yi + 1 <= ye + 2) rnext = ld(rb, x, yi + 1, m, colok);
-    const bool rowok = yi >= 0 && yi < m;
-    // shift windows
-    if (yi > ys - 2) {
-      cr3 = cr2; cr2 = cr1; cr1 = cr0;
-      cr0 = cell_row(op, x, yi + 1);
-    }
-    ms2 = ms1; ms1 = ms0;
-    ms0 = (colok && rowok) ? __ldg(op.mass + (size_t)yi * m + x) : 0.0;
+    rnext = R.at(yi + 1);
     r2 = r1; r1 = r0; r0 = rcur;
+    w3 = w2; w2 = w1; w1 = w0;
+    w0 = row_w(op, x, yi);
+    // z1 = omega r / d at row yi (zero outside the domain: r = 0 there)
     a2 = a1; a1 = a0;
-    a0 = (colok && rowok) ? cs(omega, cm(r0, cinv(diag(coef_of(cr1, cr0, ms0), l)))) : cplx{0, 0};
+    a0 = cs(omega, cm(r0, rcp(diag(expand(w0, w1), l))));
     // z2 at row yi-1
     b3 = b2; b2 = b1;
     {
-      const int y = yi - 1;
       const cplx aw = shf_up(a1), ae = shf_dn(a1);
-      if (colok && y >= 0 && y < m) {
-        const Coef k1 = coef_of(cr2, cr1, ms1);
-        const cplx Aa = apply_at(k1, l, a1, aw, ae, a2, a0);
-        const cplx d = diag(k1, l);
-        const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, cinv(d));
-        b1 = {fma(omega, t.re, a1.re), fma(omega, t.im, a1.im)};
-      } else {
-        b1 = {0, 0};
-      }
-      if (own && y >= ys && y < ye) z2out[o + (size_t)y * m + x] = b1;
+      const RowK k1 = expand(w1, w2);
+      const cplx Aa = apply_at(k1, l, a1, aw, ae, a2, a0);
+      const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, rcp(diag(k1, l)));
+      const int y = yi - 1;
+      const bool in = colok && y >= 0 && y < m;
+      b1 = in ? cplx{fma(omega, t.re, a1.re), fma(omega, t.im, a1.im)} : cplx{0, 0};
+      if (own && y >= ys && y < ye) zo[(long)y * m] = b1;
     }
     // residual at row yi-2
     q4 = q3; q3 = q2;
     {
-      const int y = yi - 2;
       const cplx bw = shf_up(b2), be = shf_dn(b2);
-      if (colok && y >= 0 && y < m) {
-        const cplx Ab = apply_at(coef_of(cr3, cr2, ms2), l, b2, bw, be, b3, b1);
-        q2 = {r2.re - Ab.re, r2.im - Ab.im};
-      } else {
-        q2 = {0, 0};
-      }
+      const cplx Ab = apply_at(expand(w2, w3), l, b2, bw, be, b3, b1);
+      const int y = yi - 2;
+      q2 = (colok && y >= 0 && y < m) ? cplx{r2.re - Ab.re, r2.im - Ab.im} : cplx{0, 0};
     }
-    // restriction: centre row yc = yi-3 (odd fine row 2Y+1 inside the owned rows)
+    // restriction centred on row yc = yi-3 (odd fine row 2Y+1 of the chunk)
     {
       const int yc = yi - 3;
       const cplx qw = shf_up(q3), qe = shf_dn(q3);
       const cplx q4w = shf_up(q4), q2e = shf_dn(q2);
-      if (yc >= ys && yc < ye && (yc & 1) && own && (x & 1)) {
-        const int X = x >> 1, Y = yc >> 1;
-        if (X < mc && Y < mc) {
-          cplx acc = q3;
-          acc.re += 0.5 * (qw.re + qe.re + q4.re + q2.re + q4w.re + q2e.re);
-          acc.im += 0.5 * (qw.im + qe.im + q4.im + q2.im + q4w.im + q2e.im);
-          bc[(size_t)it.b * mc * mc + (size_t)Y * mc + X] = acc;
-        }
+      if (cown && (yc & 1) && yc >= ys && yc < ye && (yc >> 1) < mc) {
+        cplx acc = q3;
+        acc.re += 0.5 * (qw.re + qe.re + q4.re + q2.re + q4w.re + q2e.re);
+        acc.im += 0.5 * (qw.im + qe.im + q4.im + q2.im + q4w.im + q2e.im);
+        bco[(size_t)(yc >> 1) * mc] = acc;
       }
     }
   }
@@ -281,10 +290,10 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
 
 // ---------------------------------------------------------------- up
 __global__ void __launch_bounds__(WL * WPB, 5) k_fine_up(FineOp op, const cplx* __restrict__ rv,
-                                                      const cplx* __restrict__ z2in, const cplx* __restrict__ xc,
-                                                      int mc, cplx* __restrict__ zout,
-                                                      const int* __restrict__ active, double omega, int nb,
-                                                      int dot, double* __restrict__ part) {
+                                                         const cplx* __restrict__ z2in, const cplx* __restrict__ xcv,
+                                                         int mc, cplx* __restrict__ zout,
+                                                         const int* __restrict__ active, double omega, int nb,
+                                                         int dot, double* __restrict__ part) {
   constexpr int H = 2, OWN = WL - 2 * H;  // 28
   const int m = op.m;
   const Item it = item_of(m, OWN, nb, active);
@@ -293,79 +302,68 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_up(FineOp op, const cplx* 
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
+  const int xc = min(max(x, 0), m - 1);
   const size_t o = (size_t)it.b * op.n;
-  const size_t oc = (size_t)it.b * mc * mc;
-  const cplx* rb = rv + o;
-  const cplx* zb = z2in + o;
-  const cplx* xb = xc + oc;
+  const RowPtr R{rv + o + xc, m, colok}, Z2{z2in + o + xc, m, colok};
+  cplx* const zo = zout + o + xc;
+  const cplx* xb = xcv + (size_t)it.b * mc * mc;
   const cplx l = op.lam[it.b];
   const int ys = it.ys, ye = it.ye;
-  // P1 prolongation of the coarse correction at fine node (x, y)
+  // P1 prolongation: fine vertex a = x+1 (column parity fixed per lane)
+  const int a = x + 1, ah = a >> 1;
+  const bool ao = a & 1;
+  auto coarse = [&](int A, int B) -> cplx {
+    return (A >= 1 && A <= mc && B >= 1 && B <= mc) ? xb[(size_t)(B - 1) * mc + (A - 1)] : cplx{0, 0};
+  };
   auto zc_at = [&](int y) -> cplx {
-    if (!colok || y < 0 || y >= m) return {0, 0};
-    cplx v = zb[(size_t)y * m + x];
-    const int a = x + 1, bb = y + 1, ah = a >> 1, bh = bb >> 1;
-    auto add = [&](int A, int B, double w) {
-      if (A >= 1 && A <= mc && B >= 1 && B <= mc) {
-        const cplx c = xb[(size_t)(B - 1) * mc + (A - 1)];
-        v.re = fma(w, c.re, v.re);
-        v.im = fma(w, c.im, v.im);
-      }
-    };
-    const bool ao = a & 1, bo = bb & 1;
-    if (!ao && !bo) add(ah, bh, 1.0);
-    else if (ao && !bo) { add(ah, bh, 0.5); add(ah + 1, bh, 0.5); }
-    else if (!ao && bo) { add(ah, bh, 0.5); add(ah, bh + 1, 0.5); }
-    else { add(ah, bh, 0.5); add(ah + 1, bh + 1, 0.5); }
+    cplx v = Z2.at(y);
+    if (!colok || y < 0 || y >= m) return v;
+    const int bb = y + 1, bh = bb >> 1;
+    cplx c1, c2{0, 0};
+    double w1 = 0.5;
+    if (!ao && !(bb & 1)) { c1 = coarse(ah, bh); w1 = 1.0; }
+    else if (ao && !(bb & 1)) { c1 = coarse(ah, bh); c2 = coarse(ah + 1, bh); }
+    else if (!ao) { c1 = coarse(ah, bh); c2 = coarse(ah, bh + 1); }
+    else { c1 = coarse(ah, bh); c2 = coarse(ah + 1, bh + 1); }
+    v.re = fma(w1, c1.re, fma(0.5, c2.re, v.re));
+    v.im = fma(w1, c1.im, fma(0.5, c2.im, v.im));
     return v;
   };
   // pipeline over input rows yi = ys-2 .. ye+1: zc at yi, z3 at yi-1, z4 at yi-2
-  cplx c0 = {0, 0}, c1 = {0, 0}, c2 = {0, 0};  // zc at yi, yi-1, yi-2
-  cplx r0 = {0, 0}, r1 = {0, 0}, r2 = {0, 0};  // r at yi, yi-1, yi-2
-  cplx e1 = {0, 0}, e2 = {0, 0}, e3 = {0, 0};  // z3 at yi-1, yi-2, yi-3
-  CellRow cr0 = cell_row(op, x, ys - 1), cr1 = cell_row(op, x, ys - 2), cr2{0, 0}, cr3{0, 0};
-  double ms0 = 0, ms1 = 0, ms2 = 0;
-  cplx cnext = zc_at(ys - 2), rnext = ld(rb, x, ys - 2, m, colok);
+  cplx c0{0, 0}, c1{0, 0}, c2{0, 0};  // zc at yi, yi-1, yi-2
+  cplx r0{0, 0}, r1{0, 0}, r2{0, 0};  // r at yi, yi-1, yi-2
+  cplx e1{0, 0}, e2{0, 0}, e3{0, 0};  // z3 at yi-1, yi-2, yi-3
+  RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
+  cplx cnext = zc_at(ys - 2), rnext = R.at(ys - 2);
   double s0 = 0, s1 = 0;
   for (int yi = ys - 2; yi <= ye + 1; ++yi) {
     const cplx ccur = cnext, rcur = rnext;
-    if (yi + 1 <= ye + 1) {
-      cnext = zc_at(yi + 1);
-      rnext = ld(rb, x, yi + 1, m, colok);
-    }
-    const bool rowok = yi >= 0 && yi < m;
-    if (yi > ys - 2) {
-      cr3 = cr2; cr2 = cr1; cr1 = cr0;
-      cr0 = cell_row(op, x, yi + 1);
-    }
-    ms2 = ms1; ms1 = ms0;
-    ms0 = (colok && rowok) ? __ldg(op.mass + (size_t)yi * m + x) : 0.0;
+    cnext = zc_at(yi + 1);
+    rnext = R.at(yi + 1);
     c2 = c1; c1 = c0; c0 = ccur;
     r2 = r1; r1 = r0; r0 = rcur;
+    w3 = w2; w2 = w1; w1 = w0;
+    w0 = row_w(op, x, yi);
     // z3 at row yi-1
     e3 = e2; e2 = e1;
     {
-      const int y = yi - 1;
       const cplx cw = shf_up(c1), ce = shf_dn(c1);
-      if (colok && y >= 0 && y < m) {
-        const Coef k1 = coef_of(cr2, cr1, ms1);
-        const cplx Ac = apply_at(k1, l, c1, cw, ce, c2, c0);
-        const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, cinv(diag(k1, l)));
-        e1 = {fma(omega, t.re, c1.re), fma(omega, t.im, c1.im)};
-      } else {
-        e1 = {0, 0};
-      }
+      const RowK k1 = expand(w1, w2);
+      const cplx Ac = apply_at(k1, l, c1, cw, ce, c2, c0);
+      const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, rcp(diag(k1, l)));
+      const int y = yi - 1;
+      e1 = (colok && y >= 0 && y < m) ? cplx{fma(omega, t.re, c1.re), fma(omega, t.im, c1.im)} : cplx{0, 0};
     }
     // z4 at row yi-2
     {
-      const int y = yi - 2;
       const cplx ew = shf_up(e2), ee = shf_dn(e2);
+      const RowK k2 = expand(w2, w3);
+      const int y = yi - 2;
       if (own && y >= ys && y < ye) {
-        const Coef k2 = coef_of(cr3, cr2, ms2);
         const cplx Ae = apply_at(k2, l, e2, ew, ee, e3, e1);
-        const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, cinv(diag(k2, l)));
+        const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, rcp(diag(k2, l)));
         const cplx z4 = {fma(omega, t.re, e2.re), fma(omega, t.im, e2.im)};
-        zout[o + (size_t)y * m + x] = z4;
+        zo[(long)y * m] = z4;
         if (dot) {
           const cplx pr = cm(r2, z4);
           s0 += pr.re;

@@ -320,8 +320,23 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   fw->chunk = chunk;
   std::vector<LevelOp> ops(nl);
   for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get(), l == 0, {}};
-  if (!std::getenv("TPGPU_NO_STREAM_FINE"))
-    ops[0].fine = {d_cell_mat.get(), d_nu_hat.get(), d_mass.get(), nullptr, m, c, n};
+  if (!std::getenv("TPGPU_NO_STREAM_FINE")) {
+    // K_hat edge weights: we[Y][X] = (nu_hat(cell(X,Y)) + nu_hat(cell(X,Y-1)))/2,
+    // wn[Y][X] = (nu_hat(cell(X,Y)) + nu_hat(cell(X-1,Y)))/2 (the two triangles
+    // sharing the edge, assemble_stiffness_frozen on the right-triangle grid)
+    const int V = c + 1;
+    std::vector<double> we((size_t)V * V, 1.0), wn((size_t)V * V, 1.0);
+    auto nh = [&](int i, int j) { return nu_hat[cell_mat[(size_t)j * c + i]]; };
+    for (int Y = 1; Y <= c - 1; ++Y)
+      for (int X = 0; X <= c - 1; ++X) we[(size_t)Y * V + X] = 0.5 * (nh(X, Y) + nh(X, Y - 1));
+    for (int Y = 0; Y <= c - 1; ++Y)
+      for (int X = 1; X <= c - 1; ++X) wn[(size_t)Y * V + X] = 0.5 * (nh(X, Y) + nh(X - 1, Y));
+    d_we.alloc(we.size());
+    d_wn.alloc(wn.size());
+    TP_CUDA(cudaMemcpy(d_we.get(), we.data(), we.size() * sizeof(double), cudaMemcpyHostToDevice));
+    TP_CUDA(cudaMemcpy(d_wn.get(), wn.data(), wn.size() * sizeof(double), cudaMemcpyHostToDevice));
+    ops[0].fine = {d_we.get(), d_wn.get(), d_mass.get(), nullptr, m, c, n};
+  }
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
   mc.max_iter = cfg.inner_max_iter;

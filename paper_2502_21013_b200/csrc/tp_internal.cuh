@@ -156,6 +156,7 @@ class Problem {
   DevBuf<double> d_src_time;
   DevBuf<MaterialDev> d_mat;
   DevBuf<double> d_nu_hat;
+  DevBuf<double> d_we, d_wn;  // K_hat edge weights on the (c+1)^2 vertex grid (fine streaming kernels)
   // device state
   DevBuf<double> U;     // N*n current iterate (slice-major)
   DevBuf<double> G;     // N*n right-hand side of the next sweep
