@@ -22,6 +22,7 @@
 // streams on the fine level, ~1/3 of that again on the coarse levels.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "mg.cuh"
 
@@ -1158,8 +1159,9 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const int per_t = g0.tiles;
   const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // init, apply
   const int per_u = fine ? fine_partials(ops[0].m, 2) : per_t;   // V-cycle dot (up)
-  const int per0 = per_t;
-  (void)per0;
+  // the smem-tile apply (FAM 1 reads the stored 5-point stencil) keeps more
+  // loads in flight than the streaming one on B200 (measured 102 vs 122 us at cfg 1)
+  static const bool use_stream_apply = std::getenv("TPGPU_STREAM_APPLY") != nullptr;
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
@@ -1195,14 +1197,14 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
-      if (fine) {
+      if (fine && use_stream_apply) {
         if constexpr (MODE == 0) launch_fine_apply(*p, fo, z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false);
       } else {
         DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
                                                                         first, nb, g0.BB, part.get())));
         TP_LAUNCHED(p);
       }
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), fine ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), (fine && use_stream_apply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
       TP_LAUNCHED(p);
       k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, r.get(), pout, q.get(), alpha.get(), act, cfg.omega,
