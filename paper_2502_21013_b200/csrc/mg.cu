@@ -1167,13 +1167,13 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int* zero = active.get() + B;
   cudaStream_t s = p->stream;
   const int l = 0;
-  if (fine && warm) {
+  if (fine && warm && use_stream_apply) {
     if constexpr (MODE == 0) launch_fine_apply(*p, fo, b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
   } else {
     DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
     TP_LAUNCHED(p);
   }
-  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (fine && warm) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(),
+  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (fine && warm && use_stream_apply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(),
                                   beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
   TP_LAUNCHED(p);
   if (warm) {
