@@ -107,7 +107,7 @@ typedef struct tp_solver_cfg {
   int32_t static_max_newton;  /* default 50 */
   int32_t threads;            /* accepted for interface parity; unused on device */
   /* device frequency / Newton inner solver */
-  double inner_rtol;          /* relative residual per block, default 1e-13 */
+  double inner_rtol;          /* relative residual per block, default 1e-12 */
   int32_t inner_max_iter;     /* default 200 */
   int32_t warm_start;         /* start frequency solves from the previous sweep (default 1) */
   int32_t freq_chunk;         /* frequencies per batched solve (0 = automatic) */
@@ -145,6 +145,7 @@ int tp_problem_desc_baseline(int32_t config, tp_problem_desc* desc);
 /* ---- setup (mesh, materials, sources; runner.hpp:46-73 up to static_init) */
 int tp_problem_create(const tp_problem_desc* desc, int32_t device, tp_problem** out);
 void tp_problem_destroy(tp_problem* p);
+/* n_dof: dofs held by this problem (all free dofs; a sharded rank: its strip). */
 int tp_problem_sizes(const tp_problem* p, int32_t* n_dof, int32_t* steps, double* tau);
 /* assemble_loads (assembly.hpp:88-106): F, N x n */
 int tp_problem_loads(tp_problem* p, double* F);
@@ -186,6 +187,36 @@ int tp_m1_begin(tp_problem* p, const tp_solver_cfg* cfg, double* residual0);
 /* One fixed-point sweep (solvers.hpp:326-341) on the device state; returns
  * ||R|| of the new iterate and the inner iteration count of the sweep. */
 int tp_m1_sweep(tp_problem* p, double* residual, int32_t* inner_iterations);
+/* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------
+ * Partition of a sharded problem: node-row strip [row0,row1)
+ * for K(u)/residual/RHS/DFT (all N slices local), frequency block
+ * [freq0,freq1) for the block solves (full grid), slice block [slice0,slice1)
+ * for the static initialisation.  Host state arrays of a sharded problem
+ * (tp_set_state, tp_get_state, tp_static_init, tp_solve_m1, tp_periodic_solve)
+ * are the rank's strip: N x n_local, slice-major. */
+typedef struct tp_shard_plan {
+  int32_t nranks, rank;
+  int32_t row0, row1;
+  int32_t freq0, freq1;
+  int32_t slice0, slice1;
+  int32_t n_local;
+} tp_shard_plan;
+
+typedef struct tp_comm tp_comm;
+
+/* Pure host function (no GPU): the partition every rank computes. */
+int tp_shard_plan_make(int32_t cells, int32_t steps, int32_t nranks, int32_t rank, tp_shard_plan* out);
+/* ncclGetUniqueId on one rank; the caller broadcasts the 128 bytes. */
+int tp_nccl_unique_id(unsigned char id[128]);
+int tp_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device, tp_comm** out);
+void tp_comm_destroy(tp_comm* c);
+void* tp_comm_nccl(tp_comm* c);
+int32_t tp_comm_rank(const tp_comm* c);
+int32_t tp_comm_size(const tp_comm* c);
+int32_t tp_comm_device(const tp_comm* c);
+int tp_problem_create_sharded(const tp_problem_desc* desc, tp_comm* comm, tp_problem** out);
+int tp_problem_shard(const tp_problem* p, tp_shard_plan* out);
+
 /* CUDA stream the problem launches on (cudaStream_t), for event timing. */
 void* tp_problem_stream(tp_problem* p);
 /* Kernel launches issued so far by this problem (for the bench's gpu_launches). */

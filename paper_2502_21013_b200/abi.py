@@ -46,6 +46,12 @@ class TpSolverCfg(C.Structure):
                 ("freq_chunk", C.c_int32), ("slice_chunk", C.c_int32)]
 
 
+class TpShardPlan(C.Structure):
+    _fields_ = [("nranks", C.c_int32), ("rank", C.c_int32), ("row0", C.c_int32), ("row1", C.c_int32),
+                ("freq0", C.c_int32), ("freq1", C.c_int32), ("slice0", C.c_int32),
+                ("slice1", C.c_int32), ("n_local", C.c_int32)]
+
+
 class TpReport(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("status", C.c_int32), ("history_len", C.c_int32),
                 ("inner_iterations", C.c_int32), ("q_estimate", C.c_double),
@@ -70,7 +76,7 @@ def default_cfg(**overrides) -> TpSolverCfg:
     c.static_tol = 1e-8
     c.static_max_newton = 50
     c.threads = 0
-    c.inner_rtol = 1e-13
+    c.inner_rtol = 1e-12
     c.inner_max_iter = 200
     c.warm_start = 1
     c.freq_chunk = 0

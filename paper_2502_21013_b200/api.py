@@ -23,7 +23,7 @@ from dataclasses import dataclass, field
 import numpy as np
 
 from .abi import (TP_CONVERGED, TP_EINVAL, TP_ESOLVE, TP_ITERATE_CB, TP_OK, STATUS_NAMES,
-                  TpProblemDesc, TpReport, TpSolverCfg, default_cfg)
+                  TpProblemDesc, TpReport, TpShardPlan, TpSolverCfg, default_cfg)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(_HERE, "libtpgpu.so")
@@ -35,6 +35,8 @@ EXPORTS = [
     "tp_problem_mass", "tp_apply_k", "tp_residual", "tp_static_init", "tp_set_state",
     "tp_get_state", "tp_choose_nu_hat", "tp_set_nu_hat", "tp_periodic_solve", "tp_solve_m1",
     "tp_m1_begin", "tp_m1_sweep", "tp_problem_stream", "tp_problem_launches",
+    "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
+    "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
 ]
 
 
@@ -83,6 +85,19 @@ def lib():
         L.tp_problem_stream.restype = vp
         L.tp_problem_launches.argtypes = [vp]
         L.tp_problem_launches.restype = C.c_int64
+        SP = C.POINTER(TpShardPlan)
+        L.tp_shard_plan_make.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, SP]
+        L.tp_nccl_unique_id.argtypes = [C.c_char_p]
+        L.tp_comm_create.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
+        L.tp_comm_destroy.argtypes = [vp]
+        L.tp_comm_destroy.restype = None
+        L.tp_comm_nccl.argtypes = [vp]
+        L.tp_comm_nccl.restype = vp
+        for f in ("tp_comm_rank", "tp_comm_size", "tp_comm_device"):
+            getattr(L, f).argtypes = [vp]
+            getattr(L, f).restype = C.c_int32
+        L.tp_problem_create_sharded.argtypes = [D, vp, C.POINTER(vp)]
+        L.tp_problem_shard.argtypes = [vp, SP]
         _lib = L
     return _lib
 
@@ -141,13 +156,63 @@ class SolveReport:
     inner_iterations: int = 0
 
 
-class Problem:
-    """One BASELINE-style grid problem resident on one CUDA device."""
+def shard_plan(cells: int, steps: int, nranks: int, rank: int) -> TpShardPlan:
+    """The partition every rank of a sharded problem uses (no GPU needed)."""
+    p = TpShardPlan()
+    _check(lib().tp_shard_plan_make(cells, steps, nranks, rank, C.byref(p)))
+    return p
 
-    def __init__(self, desc: TpProblemDesc, device: int = 0):
+
+def nccl_unique_id() -> bytes:
+    buf = C.create_string_buffer(128)
+    _check(lib().tp_nccl_unique_id(buf))
+    return buf.raw
+
+
+class Comm:
+    """NCCL communicator of one rank (one process per GPU)."""
+
+    def __init__(self, uid: bytes, nranks: int, rank: int, device: int):
+        self._h = C.c_void_p()
+        _check(lib().tp_comm_create(C.c_char_p(uid), nranks, rank, device, C.byref(self._h)))
+        self.nranks, self.rank, self.device = nranks, rank, device
+
+    @classmethod
+    def from_torch(cls, device: int, group=None) -> "Comm":
+        """Bootstrap over an initialised torch.distributed process group
+        (gloo is enough: it only broadcasts the 128-byte NCCL id)."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+        uid = nccl_unique_id() if rank == 0 else bytes(128)
+        t = torch.tensor(list(uid), dtype=torch.uint8)
+        dist.broadcast(t, src=0, group=group)
+        return cls(bytes(t.tolist()), world, rank, device)
+
+    def close(self):
+        if self._h:
+            lib().tp_comm_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class Problem:
+    """One BASELINE-style grid problem resident on one CUDA device (or one
+    rank's shard of it, see Problem.sharded)."""
+
+    def __init__(self, desc: TpProblemDesc, device: int = 0, comm: "Comm | None" = None):
         self._h = C.c_void_p()
         self.desc = desc
-        _check(lib().tp_problem_create(C.byref(desc), device, C.byref(self._h)))
+        self.comm = comm
+        if comm is None:
+            _check(lib().tp_problem_create(C.byref(desc), device, C.byref(self._h)))
+        else:
+            _check(lib().tp_problem_create_sharded(C.byref(desc), comm._h, C.byref(self._h)))
         n, N, tau = C.c_int32(), C.c_int32(), C.c_double()
         _check(lib().tp_problem_sizes(self._h, C.byref(n), C.byref(N), C.byref(tau)))
         self.n_dof, self.steps, self.tau = n.value, N.value, tau.value
@@ -155,6 +220,15 @@ class Problem:
     @classmethod
     def baseline(cls, config: int, device: int = 0) -> "Problem":
         return cls(baseline_desc(config), device)
+
+    @classmethod
+    def sharded(cls, desc: TpProblemDesc, comm: Comm) -> "Problem":
+        return cls(desc, comm.device, comm)
+
+    def shard(self) -> TpShardPlan:
+        p = TpShardPlan()
+        _check(lib().tp_problem_shard(self._h, C.byref(p)))
+        return p
 
     def close(self):
         if self._h:

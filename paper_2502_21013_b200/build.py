@@ -70,7 +70,7 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
     if force or jobs or _newer(OUT, objs):
         tmp = OUT + ".tmp"
         cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-Xcompiler", "-fPIC",
-                                 "-o", tmp] + objs
+                                 "-o", tmp] + objs + ["-ldl"]
         run(cmd)
         os.replace(tmp, OUT)
     return OUT

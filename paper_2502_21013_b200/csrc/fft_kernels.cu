@@ -228,7 +228,7 @@ FftPlan& plan_for(Problem& p) {
 
 void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat) {
   FftPlan& pl = plan_for(p);
-  const size_t n = p.n;
+  const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
   const int C = 2 * pl.P;
   const int blocks = (int)((n + C - 1) / C);
   k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2,
@@ -238,7 +238,7 @@ void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat) {
 
 void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2) {
   FftPlan& pl = plan_for(p);
-  const size_t n = p.n;
+  const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
   const int C = 2 * pl.P;
   const int blocks = (int)((n + C - 1) / C);
   p.part.ensure((size_t)2 * blocks);

@@ -48,8 +48,9 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   per_slice += (size_t)n * 8 * 9 + (size_t)nL * nL * 8;
   size_t free_b = 0, total_b = 0;
   TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  int S = cfg.slice_chunk > 0 ? cfg.slice_chunk : (int)std::min<size_t>(N, (size_t)(0.5 * free_b) / per_slice);
-  S = std::max(1, std::min(S, N));
+  const int Nr = sh.s1 - sh.s0;
+  int S = cfg.slice_chunk > 0 ? cfg.slice_chunk : (int)std::min<size_t>(Nr, (size_t)(0.5 * free_b) / per_slice);
+  S = std::max(1, std::min(S, Nr));
 
   DevBuf<double> Ub((size_t)S * n), Rb((size_t)S * n), Db((size_t)S * n), Ut((size_t)S * n), Rt((size_t)S * n);
   std::vector<DevBuf<double>> J(nl);
@@ -68,8 +69,12 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
 
   std::vector<int> h_slice(S), h_active(S), h_acc(S), counts(N, 0);
   std::vector<double> h_alpha(S), rnorm(S), scale(S), nrm2(S);
-  for (int s0 = 0; s0 < N; s0 += S) {
-    const int nb = std::min(S, N - s0);
+  // slices of this rank (all of them on a single GPU); sharded problems
+  // solve their slice block on the full grid and redistribute to strips
+  DevBuf<double> Us;
+  if (sharded()) Us.alloc((size_t)(sh.s1 - sh.s0) * n);
+  for (int s0 = sh.s0; s0 < sh.s1; s0 += S) {
+    const int nb = std::min(S, sh.s1 - s0);
     for (int b = 0; b < S; ++b) {
       h_slice[b] = std::min(s0 + b, N - 1);
       h_active[b] = b < nb;
@@ -151,10 +156,11 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
                     "static init, step " + std::to_string(s0 + b + 1) + ": newton: no convergence within " +
                         std::to_string(cfg.static_max_newton) + " steps",
                     rnorm[b] / scale[b]);
-    TP_CUDA(cudaMemcpyAsync(U.get() + (size_t)s0 * n, Ub.get(), (size_t)nb * n * sizeof(double),
-                            cudaMemcpyDeviceToDevice, stream));
+    double* dst = sharded() ? Us.get() + (size_t)(s0 - sh.s0) * n : U.get() + (size_t)s0 * n;
+    TP_CUDA(cudaMemcpyAsync(dst, Ub.get(), (size_t)nb * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
   }
   TP_CUDA(cudaStreamSynchronize(stream));
+  if (sharded()) slices_to_strips(Us.get());
   if (newton_counts)
     for (int s = 0; s < N; ++s) newton_counts[s] = counts[s];
 }

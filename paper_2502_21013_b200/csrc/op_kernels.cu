@@ -37,15 +37,34 @@ __device__ __forceinline__ double vertex_u(const double* __restrict__ us, int m,
   return (X >= 1 && X <= m && Y >= 1 && Y <= m) ? us[(size_t)(Y - 1) * m + (X - 1)] : 0.0;
 }
 
+// A row strip of the node grid held by one rank: node rows [y0, y0+rows) of
+// a slice at `us` (local row-major), plus the halo rows y0-1 (`lo`) and
+// y0+rows (`hi`) from the neighbouring ranks (nullptr: none / boundary).
+struct StripView {
+  const double* lo;
+  const double* hi;
+  int y0, rows;
+};
+
+__device__ __forceinline__ double vertex_u(const double* __restrict__ us, const StripView& sv, int m, int X,
+                                           int Y) {
+  const int x = X - 1, y = Y - 1;
+  if (x < 0 || x >= m || y < 0 || y >= m) return 0.0;
+  const int ly = y - sv.y0;
+  if (ly < 0) return (ly == -1 && sv.lo) ? sv.lo[x] : 0.0;
+  if (ly >= sv.rows) return (ly == sv.rows && sv.hi) ? sv.hi[x] : 0.0;
+  return us[(size_t)ly * m + x];
+}
+
 template <bool NEED_NU, bool NEED_HAT>
-__device__ void tile_load(Tile& t, const double* __restrict__ us, const double* __restrict__ ds,
-                          double alpha, int m, int c, int x0, int y0,
+__device__ void tile_load(Tile& t, const double* __restrict__ us, const StripView& sv,
+                          const double* __restrict__ ds, double alpha, int m, int c, int x0, int y0,
                           const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
                           const double* __restrict__ nu_hat) {
   const int tid = threadIdx.y * TX + threadIdx.x;
   for (int k = tid; k < (TY + 2) * (TX + 2); k += TX * TY) {
     const int ly = k / (TX + 2), lx = k % (TX + 2);
-    double v = vertex_u(us, m, x0 + lx, y0 + ly);
+    double v = vertex_u(us, sv, m, x0 + lx, y0 + ly);
     if (ds) v += alpha * vertex_u(ds, m, x0 + lx, y0 + ly);
     t.u[ly][lx] = v;
   }
@@ -117,7 +136,8 @@ __global__ void __launch_bounds__(TX * TY) k_apply_k(const double* __restrict__ 
   const size_t n = (size_t)m * m;
   const int s = blockIdx.z;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  tile_load<true, false>(t, U + s * n, nullptr, 0.0, m, c, x0, y0, cell_mat, mats, nullptr);
+  const StripView sv{nullptr, nullptr, 0, m};
+  tile_load<true, false>(t, U + s * n, sv, nullptr, 0.0, m, c, x0, y0, cell_mat, mats, nullptr);
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
   if (x < m && y < m) out[s * n + (size_t)y * m + x] = gather<0>(t, threadIdx.x, threadIdx.y);
 }
@@ -127,9 +147,13 @@ __global__ void __launch_bounds__(TX * TY) k_apply_k(const double* __restrict__ 
 //   G^s = F^s + K_hat u^s - K(u^s)                        (solvers.hpp:326-336)
 // K(u) is evaluated once and shared.  R is never written: per-block partial
 // sums of R^2 go to `part` (block_l2 is reduced deterministically).
+// Strip form: the grid covers the local node rows [sy0, sy0+rows) (global
+// coordinates for materials, mass and sources; U, G, R local with slice
+// stride rows*m; halo rows lo/hi with slice stride m).
 template <bool WANT_G, bool WANT_R>
 __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
-    const double* __restrict__ U, double* __restrict__ G, double* __restrict__ R,
+    const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
+    int sy0, int rows, double* __restrict__ G, double* __restrict__ R,
     double* __restrict__ part, int m, int c, int N, double inv_tau,
     const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
     const double* __restrict__ nu_hat, const double* __restrict__ mass,
@@ -137,28 +161,32 @@ __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
   __shared__ Tile t;
   __shared__ double red[32];
   const size_t n = (size_t)m * m;
+  const size_t nl = (size_t)rows * m;
   const int s = blockIdx.z;
-  const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
-  tile_load<true, WANT_G>(t, U + s * n, nullptr, 0.0, m, c, x0, y0, cell_mat, mats, nu_hat);
+  const int x0 = blockIdx.x * TX, y0 = sy0 + blockIdx.y * TY;
+  const StripView sv{halo_lo ? halo_lo + (size_t)s * m : nullptr, halo_hi ? halo_hi + (size_t)s * m : nullptr,
+                     sy0, rows};
+  tile_load<true, WANT_G>(t, U + s * nl, sv, nullptr, 0.0, m, c, x0, y0, cell_mat, mats, nu_hat);
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
   double r2 = 0;
-  if (x < m && y < m) {
-    const size_t i = (size_t)y * m + x;
+  if (x < m && y < sy0 + rows) {
+    const size_t i = (size_t)y * m + x;               // global
+    const size_t il = (size_t)(y - sy0) * m + x;      // local
     double f = 0;
     for (int r = 0; r < nsrc; ++r) f += src_time[s * nsrc + r] * src_prof[r * n + i];
     const double ku = gather<0>(t, threadIdx.x, threadIdx.y);
     if (WANT_G) {
       const double khu = gather<1>(t, threadIdx.x, threadIdx.y);
-      G[s * n + i] = f + khu - ku;
+      G[s * nl + il] = f + khu - ku;
     }
     const double mi = mass[i];
     double mdu = 0;
     if (mi != 0) {
       const int sp = (s + N - 1) % N;
-      mdu = mi * ((t.u[threadIdx.y + 1][threadIdx.x + 1] - U[sp * n + i]) * inv_tau);
+      mdu = mi * ((t.u[threadIdx.y + 1][threadIdx.x + 1] - U[sp * nl + il]) * inv_tau);
     }
     const double res = f - mdu - ku;
-    if (WANT_R && R) R[s * n + i] = res;
+    if (WANT_R && R) R[s * nl + il] = res;
     r2 = res * res;
   }
   const double tot = block_sum(r2, red);
@@ -284,31 +312,36 @@ static size_t sweep_partials(int m, int N) {
 }
 
 double Problem::residual_and_rhs(bool want_rhs) {
-  dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, N);
-  const size_t np = sweep_partials(m, N);
+  const int rows = sh.y1 - sh.y0;
+  if (sharded()) exchange_halo();
+  dim3 grid((m + TX - 1) / TX, (rows + TY - 1) / TY, N);
+  const size_t np = (size_t)grid.x * grid.y * grid.z;
   part.ensure(np);
   const int nsrc = (int)src_mats.size();
+  const double* lo = sharded() ? halo_lo.get() : nullptr;
+  const double* hi = sharded() ? halo_hi.get() : nullptr;
   if (want_rhs) {
     require(nu_hat_set, "fixed-point sweep: nu_hat not installed");
     k_sweep_fused<true, false><<<grid, dim3(TX, TY), 0, stream>>>(
-        U.get(), G.get(), nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
-        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+        U.get(), lo, hi, sh.y0, rows, G.get(), nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(),
+        d_mat.get(), d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   } else {
     k_sweep_fused<false, false><<<grid, dim3(TX, TY), 0, stream>>>(
-        U.get(), nullptr, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
-        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+        U.get(), lo, hi, sh.y0, rows, nullptr, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(),
+        d_mat.get(), d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   }
   TP_LAUNCHED(this);
-  return std::sqrt(reduce_sum(*this, part.get(), (int)np));
+  return std::sqrt(global_sum(reduce_sum(*this, part.get(), (int)np)));
 }
 
 void Problem::residual_dev(const double* u, double* r, int count_slices) {
   require(count_slices == N, "residual: needs all slices");
+  require(!sharded(), "residual of a host state: single-rank problems only");
   dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, N);
   part.ensure(sweep_partials(m, N));
   k_sweep_fused<false, true><<<grid, dim3(TX, TY), 0, stream>>>(
-      u, nullptr, r, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(), d_nu_hat.get(),
-      d_mass.get(), d_src_prof.get(), d_src_time.get(), (int)src_mats.size());
+      u, nullptr, nullptr, 0, m, nullptr, r, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+      d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), (int)src_mats.size());
   TP_LAUNCHED(this);
 }
 
@@ -347,7 +380,8 @@ __global__ void __launch_bounds__(TX * TY) k_newton_residual(
   const int s = slice_of[b];
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const double a = alpha ? alpha[b] : 0.0;
-  tile_load<true, false>(t, Ub + b * n, Db ? Db + b * n : nullptr, a, m, c, x0, y0, cell_mat, mats,
+  const StripView sv{nullptr, nullptr, 0, m};
+  tile_load<true, false>(t, Ub + b * n, sv, Db ? Db + b * n : nullptr, a, m, c, x0, y0, cell_mat, mats,
                          nullptr);
   const int x = x0 + threadIdx.x, y = y0 + threadIdx.y;
   double r2 = 0;
@@ -404,24 +438,29 @@ void newton_residual(Problem& p, const double* Ub, const double* Db, const doubl
 
 // per-material min/max of |grad u| over all slices of the device state
 namespace {
-__global__ void k_field_ranges(const double* __restrict__ U, int m, int c, int N,
-                               const uint8_t* __restrict__ cell_mat, double* __restrict__ lo,
-                               double* __restrict__ hi) {
+// cells of cell rows [cy0, cy1) (vertex rows cy0 .. cy1), u from the strip view
+__global__ void k_field_ranges(const double* __restrict__ U, const double* __restrict__ halo_lo,
+                               const double* __restrict__ halo_hi, int sy0, int rows, int cy0, int cy1,
+                               int m, int c, int N, const uint8_t* __restrict__ cell_mat,
+                               double* __restrict__ lo, double* __restrict__ hi) {
   // one thread per cell per slice-group; partial min/max per block per material
   __shared__ double slo[TP_MAX_MATERIALS][256], shi[TP_MAX_MATERIALS][256];
-  const size_t cells = (size_t)c * c;
-  const size_t n = (size_t)m * m;
+  const size_t cells = (size_t)c * (cy1 - cy0);
+  const size_t nl = (size_t)rows * m;
   double mlo[TP_MAX_MATERIALS], mhi[TP_MAX_MATERIALS];
   for (int r = 0; r < TP_MAX_MATERIALS; ++r) { mlo[r] = INFINITY; mhi[r] = -1.0; }
   const double cc = (double)c;
   for (size_t k = (size_t)blockIdx.x * blockDim.x + threadIdx.x; k < cells * N;
        k += (size_t)gridDim.x * blockDim.x) {
     const int s = (int)(k / cells);
-    const size_t cell = k % cells;
-    const int i = (int)(cell % c), j = (int)(cell / c);
-    const double* us = U + s * n;
-    const double u00 = vertex_u(us, m, i, j), u10 = vertex_u(us, m, i + 1, j);
-    const double u01 = vertex_u(us, m, i, j + 1), u11 = vertex_u(us, m, i + 1, j + 1);
+    const size_t cl = k % cells;
+    const int i = (int)(cl % c), j = cy0 + (int)(cl / c);
+    const size_t cell = (size_t)j * c + i;
+    const double* us = U + s * nl;
+    const StripView sv{halo_lo ? halo_lo + (size_t)s * m : nullptr, halo_hi ? halo_hi + (size_t)s * m : nullptr,
+                       sy0, rows};
+    const double u00 = vertex_u(us, sv, m, i, j), u10 = vertex_u(us, sv, m, i + 1, j);
+    const double u01 = vertex_u(us, sv, m, i, j + 1), u11 = vertex_u(us, sv, m, i + 1, j + 1);
     const double s1 = hypot(cc * (u10 - u00), cc * (u11 - u10));
     const double s2 = hypot(cc * (u11 - u01), cc * (u01 - u00));
     const int r = cell_mat[cell];
@@ -449,8 +488,14 @@ __global__ void k_field_ranges(const double* __restrict__ U, int m, int c, int N
 void Problem::field_ranges(double* lo, double* hi, int* any) {
   const int blocks = 2 * num_sms;
   part.ensure((size_t)2 * blocks * TP_MAX_MATERIALS);
-  k_field_ranges<<<blocks, 256, 0, stream>>>(U.get(), m, c, N, d_cell_mat.get(), part.get(),
-                                            part.get() + blocks * TP_MAX_MATERIALS);
+  // cell row j has vertex rows j, j+1 = node rows j-1, j: rank r owns cell
+  // rows [y0, y1) (the last rank also the top row c-1)
+  const int rows = sh.y1 - sh.y0;
+  const int cy0 = sh.y0, cy1 = (sh.r == sh.P - 1) ? c : sh.y1;
+  if (sharded()) exchange_halo();
+  k_field_ranges<<<blocks, 256, 0, stream>>>(U.get(), sharded() ? halo_lo.get() : nullptr,
+                                            sharded() ? halo_hi.get() : nullptr, sh.y0, rows, cy0, cy1, m, c, N,
+                                            d_cell_mat.get(), part.get(), part.get() + blocks * TP_MAX_MATERIALS);
   TP_LAUNCHED(this);
   std::vector<double> h(2 * blocks * TP_MAX_MATERIALS);
   TP_CUDA(cudaMemcpyAsync(h.data(), part.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
@@ -462,8 +507,9 @@ void Problem::field_ranges(double* lo, double* hi, int* any) {
       lo[r] = std::fmin(lo[r], h[b * TP_MAX_MATERIALS + r]);
       hi[r] = std::fmax(hi[r], h[(blocks + b) * TP_MAX_MATERIALS + r]);
     }
-    any[r] = hi[r] >= 0.0;
   }
+  global_minmax(lo, hi, TP_MAX_MATERIALS);
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r) any[r] = hi[r] >= 0.0;
 }
 
 }  // namespace tpgpu

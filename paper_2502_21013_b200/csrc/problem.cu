@@ -102,7 +102,7 @@ struct Problem::FreqWork {
   int nL = 0;
 };
 
-Problem::Problem(const tp_problem_desc& d, int dev) : desc(d), device(dev) {
+Problem::Problem(const tp_problem_desc& d, int dev, const ShardInfo* shard) : desc(d), device(dev) {
   validate_desc(d);
   int count = 0;
   TP_CUDA(cudaGetDeviceCount(&count));
@@ -207,10 +207,19 @@ Problem::Problem(const tp_problem_desc& d, int dev) : desc(d), device(dev) {
   }
   nu_hat.assign(TP_MAX_MATERIALS, 1.0);
   upload_constants();
-  U.alloc((size_t)N * n);
-  G.alloc((size_t)N * n);
-  Ghat.alloc((size_t)K * n);
-  Uhat.alloc((size_t)K * n);
+  if (shard) {
+    sh = *shard;
+  } else {
+    make_partition(m, K, N, 1, 0, sh);
+  }
+  U.alloc((size_t)N * sh.nr);
+  G.alloc((size_t)N * sh.nr);
+  Ghat.alloc((size_t)K * sh.nr);
+  Uhat.alloc((size_t)K * sh.nr);
+  if (sharded()) {
+    Ghat_f.alloc((size_t)(sh.k1 - sh.k0) * n);
+    Uhat_f.alloc((size_t)(sh.k1 - sh.k0) * n);
+  }
   red.alloc(4096);
   TP_CUDA(cudaMemsetAsync(U.get(), 0, U.bytes(), stream));
 }
@@ -294,29 +303,32 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
     launch_rap(*this, levels[l - 1].M.get(), levels[l - 1].m, levels[l].M.get(), levels[l].m, 1);
   }
   fw = std::make_unique<FreqWork>();
-  // symbols lambda_k (periodic.hpp:146-152)
-  std::vector<cplx> lam(K);
-  for (int k = 0; k < K; ++k) {
-    if (k == 0) lam[k] = {0.0, 0.0};
-    else if (2 * k == N) lam[k] = {2.0 / tau, 0.0};
+  // symbols lambda_k (periodic.hpp:146-152) of this rank's frequencies
+  const int Kr = sh.k1 - sh.k0;
+  std::vector<cplx> lam(Kr);
+  for (int kk = 0; kk < Kr; ++kk) {
+    const int k = sh.k0 + kk;
+    cplx& lk = lam[kk];
+    if (k == 0) lk = {0.0, 0.0};
+    else if (2 * k == N) lk = {2.0 / tau, 0.0};
     else {
       const double a = -2.0 * std::numbers::pi * k / N;
       const double rr = std::cos(a), ri = std::sin(a);  // std::polar(1.0, a)
-      lam[k] = {(1.0 - rr) / tau, (0.0 - ri) / tau};
+      lk = {(1.0 - rr) / tau, (0.0 - ri) / tau};
     }
   }
-  fw->lam.alloc(K);
-  TP_CUDA(cudaMemcpy(fw->lam.get(), lam.data(), K * sizeof(cplx), cudaMemcpyHostToDevice));
+  fw->lam.alloc(Kr);
+  TP_CUDA(cudaMemcpy(fw->lam.get(), lam.data(), Kr * sizeof(cplx), cudaMemcpyHostToDevice));
   const Level& LC = levels.back();
   fw->nL = LC.n;
-  fw->inv.alloc((size_t)K * LC.n * LC.n);
-  launch_coarse_inverse_freq(*this, LC.K.get(), LC.M.get(), LC.m, fw->lam.get(), fw->inv.get(), K);
+  fw->inv.alloc((size_t)Kr * LC.n * LC.n);
+  launch_coarse_inverse_freq(*this, LC.K.get(), LC.M.get(), LC.m, fw->lam.get(), fw->inv.get(), Kr);
   // chunk: work ~ 7 complex vectors per frequency on the fine level (+1/3 coarse)
   size_t free_b = 0, total_b = 0;
   TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double per = 16.0 * 8.5 * n;
-  int chunk = cfg.freq_chunk > 0 ? cfg.freq_chunk : (int)std::min<double>(K, 0.6 * free_b / per);
-  chunk = std::max(1, std::min(chunk, K));
+  int chunk = cfg.freq_chunk > 0 ? cfg.freq_chunk : (int)std::min<double>(Kr, 0.6 * free_b / per);
+  chunk = std::max(1, std::min(chunk, Kr));
   fw->chunk = chunk;
   std::vector<LevelOp> ops(nl);
   for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get(), l == 0, {}};
@@ -352,18 +364,23 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
 void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
   build_frequency_solver(cfg);
   launch_rdft_forward(*this, G.get(), Ghat.get());
+  if (sharded()) alltoall_to_freq();
   const bool warm = cfg.warm_start && uhat_valid;
+  const int Kr = sh.k1 - sh.k0;
   int iters = 0;
-  for (int k0 = 0; k0 < K; k0 += fw->chunk) {
-    const int nb = std::min(fw->chunk, K - k0);
+  for (int k0 = 0; k0 < Kr; k0 += fw->chunk) {
+    const int nb = std::min(fw->chunk, Kr - k0);
     fw->solver.lam = fw->lam.get() + k0;
     fw->solver.coarse_inv = fw->inv.get() + (size_t)k0 * fw->nL * fw->nL;
-    iters = std::max(iters, fw->solver.solve(Ghat.get() + (size_t)k0 * n, Uhat.get() + (size_t)k0 * n,
-                                             nb, warm, st));
+    iters = std::max(iters, fw->solver.solve(spec_in() + (size_t)k0 * n, spec_out() + (size_t)k0 * n, nb,
+                                             warm, st));
   }
   last_inner = iters;
+  if (sharded()) alltoall_from_freq();
   double re2 = 0, im2 = 0;
   launch_rdft_inverse(*this, Uhat.get(), U.get(), &re2, &im2);
+  re2 = global_sum(re2);
+  im2 = global_sum(im2);
   uhat_valid = true;
   // imaginary-residue guard, periodic.hpp:186-196
   const double re_norm = std::sqrt(re2), im_norm = std::sqrt(im2);
@@ -387,6 +404,14 @@ struct tp_problem {
 namespace {
 thread_local std::string g_err;
 thread_local double g_err_res = -1;
+}  // namespace
+
+void tpgpu::set_last_error(const std::string& msg, double residual) {
+  g_err = msg;
+  g_err_res = residual;
+}
+
+namespace {
 
 template <class F>
 int guarded(F&& f) {
@@ -451,7 +476,7 @@ void tp_solver_cfg_default(tp_solver_cfg* c) {
   c->static_tol = 1e-8;
   c->static_max_newton = 50;
   c->threads = 1;
-  c->inner_rtol = 1e-13;
+  c->inner_rtol = 1e-12;
   c->inner_max_iter = 200;
   c->warm_start = 1;
 }
@@ -481,7 +506,7 @@ void tp_problem_destroy(tp_problem* p) {
 int tp_problem_sizes(const tp_problem* p, int32_t* n_dof, int32_t* steps, double* tau) {
   return guarded([&] {
     tpgpu::require(p && p->impl, "null problem handle");
-    if (n_dof) *n_dof = p->impl->n;
+    if (n_dof) *n_dof = p->impl->sh.nr;  // local dofs (all dofs on a single GPU)
     if (steps) *steps = p->impl->N;
     if (tau) *tau = p->impl->tau;
   });
@@ -722,6 +747,35 @@ int tp_solve_m1(tp_problem* h, const tp_solver_cfg* c, const double* U0, double*
     r.sweep_time = sweeps;
     r.wall_time = seconds_since(t0);
     if (rep) *rep = r;
+  });
+}
+
+int tp_problem_create_sharded(const tp_problem_desc* desc, tp_comm* comm, tp_problem** out) {
+  return guarded([&] {
+    tpgpu::require(desc && out && comm, "null argument");
+    const int P = tp_comm_size(comm), r = tp_comm_rank(comm), dev = tp_comm_device(comm);
+    tpgpu::ShardInfo sh;
+    tpgpu::make_partition(desc->cells - 1, desc->steps / 2 + 1, desc->steps, P, r, sh);
+    sh.comm = tp_comm_nccl(comm);
+    auto h = std::make_unique<tp_problem>();
+    h->impl = std::make_unique<Problem>(*desc, dev, &sh);
+    *out = h.release();
+  });
+}
+
+int tp_problem_shard(const tp_problem* p, tp_shard_plan* out) {
+  return guarded([&] {
+    tpgpu::require(p && p->impl && out, "null argument");
+    const tpgpu::ShardInfo& s = p->impl->sh;
+    out->nranks = s.P;
+    out->rank = s.r;
+    out->row0 = s.y0;
+    out->row1 = s.y1;
+    out->freq0 = s.k0;
+    out->freq1 = s.k1;
+    out->slice0 = s.s0;
+    out->slice1 = s.s1;
+    out->n_local = s.nr;
   });
 }
 

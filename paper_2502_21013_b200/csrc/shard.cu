@@ -1,0 +1,343 @@
+// Multi-GPU plumbing: partition, NCCL communicator, and the exchanges of
+// the sharded sweep.
+//
+// An exact time DFT couples all N slices of every dof (periodic.hpp:161-167),
+// so the sweep alternates two layouts:
+//   strips      node rows [y0, y1) x all N slices  -- K(u), residual, RHS,
+//               forward / inverse DFT (all local), one halo row each side;
+//   frequencies k in [k0, k1) x all n dofs          -- the block solves
+//               (periodic.hpp:168-170 decoupling: no communication).
+// Per sweep: one halo exchange (2 rows x N slices to each neighbour), one
+// all-to-all strips -> frequencies before the solves and one back after
+// (grouped ncclSend/ncclRecv; every block is contiguous on one side and
+// strided on the other, handled by cudaMemcpy2DAsync), and scalar norms
+// gathered and summed in rank order (deterministic).  The static
+// initialisation is independent per slice, so it runs slice-sharded on the
+// full grid and is redistributed to strips by one all-to-all.
+#include <dlfcn.h>
+#include <nccl.h>
+
+#include <cstring>
+#include <string>
+
+#include "tp_internal.cuh"
+
+namespace tpgpu {
+
+// NCCL is resolved at run time (dlopen on first use, reusing a libnccl
+// already loaded by the host process, e.g. torch's), so loading libtpgpu.so
+// never pins an NCCL version for the rest of the process.
+struct NcclApi {
+  ncclResult_t (*GetUniqueId)(ncclUniqueId*) = nullptr;
+  ncclResult_t (*CommInitRank)(ncclComm_t*, int, ncclUniqueId, int) = nullptr;
+  ncclResult_t (*CommDestroy)(ncclComm_t) = nullptr;
+  ncclResult_t (*GroupStart)() = nullptr;
+  ncclResult_t (*GroupEnd)() = nullptr;
+  ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*AllGather)(const void*, void*, size_t, ncclDataType_t, ncclComm_t, cudaStream_t) = nullptr;
+  const char* (*GetErrorString)(ncclResult_t) = nullptr;
+  bool ok = false;
+};
+
+static NcclApi& nccl() {
+  static NcclApi api = [] {
+    NcclApi a;
+    void* h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL | RTLD_NOLOAD);
+    if (!h) h = dlopen("libnccl.so.2", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) h = dlopen("libnccl.so", RTLD_NOW | RTLD_GLOBAL);
+    if (!h) return a;
+    a.GetUniqueId = reinterpret_cast<decltype(a.GetUniqueId)>(dlsym(h, "ncclGetUniqueId"));
+    a.CommInitRank = reinterpret_cast<decltype(a.CommInitRank)>(dlsym(h, "ncclCommInitRank"));
+    a.CommDestroy = reinterpret_cast<decltype(a.CommDestroy)>(dlsym(h, "ncclCommDestroy"));
+    a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(dlsym(h, "ncclGroupStart"));
+    a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(dlsym(h, "ncclGroupEnd"));
+    a.Send = reinterpret_cast<decltype(a.Send)>(dlsym(h, "ncclSend"));
+    a.Recv = reinterpret_cast<decltype(a.Recv)>(dlsym(h, "ncclRecv"));
+    a.AllGather = reinterpret_cast<decltype(a.AllGather)>(dlsym(h, "ncclAllGather"));
+    a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(dlsym(h, "ncclGetErrorString"));
+    a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.GroupStart && a.GroupEnd && a.Send && a.Recv &&
+           a.AllGather && a.GetErrorString;
+    return a;
+  }();
+  if (!api.ok) throw Error(TP_ECUDA, "NCCL (libnccl.so.2) could not be loaded");
+  return api;
+}
+
+#define ncclGetUniqueId(...) ::tpgpu::nccl().GetUniqueId(__VA_ARGS__)
+#define ncclCommInitRank(...) ::tpgpu::nccl().CommInitRank(__VA_ARGS__)
+#define ncclCommDestroy(...) ::tpgpu::nccl().CommDestroy(__VA_ARGS__)
+#define ncclGroupStart() ::tpgpu::nccl().GroupStart()
+#define ncclGroupEnd() ::tpgpu::nccl().GroupEnd()
+#define ncclSend(...) ::tpgpu::nccl().Send(__VA_ARGS__)
+#define ncclRecv(...) ::tpgpu::nccl().Recv(__VA_ARGS__)
+#define ncclAllGather(...) ::tpgpu::nccl().AllGather(__VA_ARGS__)
+#define ncclGetErrorString(...) ::tpgpu::nccl().GetErrorString(__VA_ARGS__)
+
+#define TP_NCCL(x)                                                                              \
+  do {                                                                                          \
+    ncclResult_t tp_r_ = (x);                                                                   \
+    if (tp_r_ != ncclSuccess)                                                                   \
+      throw Error(TP_ECUDA, std::string("NCCL error ") + ncclGetErrorString(tp_r_) + " at " +   \
+                                __FILE__ + ":" + std::to_string(__LINE__) + ": " #x);           \
+  } while (0)
+
+void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh) {
+  require(P >= 1 && r >= 0 && r < P, "shard: rank out of range");
+  require(m >= P, "shard: more ranks than grid rows");
+  require(K >= P, "shard: more ranks than frequencies");
+  require(N >= P, "shard: more ranks than time slices");
+  sh.P = P;
+  sh.r = r;
+  sh.ys.resize(P + 1);
+  sh.ks.resize(P + 1);
+  sh.ss.resize(P + 1);
+  for (int q = 0; q <= P; ++q) {
+    sh.ys[q] = (int)((long)m * q / P);
+    sh.ks[q] = (int)((long)K * q / P);
+    sh.ss[q] = (int)((long)N * q / P);
+  }
+  sh.y0 = sh.ys[r];
+  sh.y1 = sh.ys[r + 1];
+  sh.k0 = sh.ks[r];
+  sh.k1 = sh.ks[r + 1];
+  sh.s0 = sh.ss[r];
+  sh.s1 = sh.ss[r + 1];
+  sh.nr = (sh.y1 - sh.y0) * m;
+}
+
+static ncclComm_t comm_of(const Problem& p) { return static_cast<ncclComm_t>(p.sh.comm); }
+
+// Halo rows of all N slices: my first owned row goes to rank r-1 (its hi),
+// my last to rank r+1 (its lo).
+void Problem::exchange_halo() {
+  if (!sharded()) return;
+  const int rows = sh.y1 - sh.y0;
+  const size_t nm = (size_t)N * m;
+  halo_lo.ensure(nm);
+  halo_hi.ensure(nm);
+  halo_send.ensure(2 * nm);
+  // pack first and last rows of every slice (slice stride nr)
+  TP_CUDA(cudaMemcpy2DAsync(halo_send.get(), m * sizeof(double), U.get(), (size_t)sh.nr * sizeof(double),
+                            m * sizeof(double), N, cudaMemcpyDeviceToDevice, stream));
+  TP_CUDA(cudaMemcpy2DAsync(halo_send.get() + nm, m * sizeof(double), U.get() + (size_t)(rows - 1) * m,
+                            (size_t)sh.nr * sizeof(double), m * sizeof(double), N, cudaMemcpyDeviceToDevice,
+                            stream));
+  ncclComm_t c = comm_of(*this);
+  TP_NCCL(ncclGroupStart());
+  if (sh.r > 0) {
+    TP_NCCL(ncclSend(halo_send.get(), nm, ncclDouble, sh.r - 1, c, stream));
+    TP_NCCL(ncclRecv(halo_lo.get(), nm, ncclDouble, sh.r - 1, c, stream));
+  }
+  if (sh.r < sh.P - 1) {
+    TP_NCCL(ncclSend(halo_send.get() + nm, nm, ncclDouble, sh.r + 1, c, stream));
+    TP_NCCL(ncclRecv(halo_hi.get(), nm, ncclDouble, sh.r + 1, c, stream));
+  }
+  TP_NCCL(ncclGroupEnd());
+  // outer boundary ranks: no neighbour -> zero halo (Dirichlet)
+  if (sh.r == 0) TP_CUDA(cudaMemsetAsync(halo_lo.get(), 0, nm * sizeof(double), stream));
+  if (sh.r == sh.P - 1) TP_CUDA(cudaMemsetAsync(halo_hi.get(), 0, nm * sizeof(double), stream));
+}
+
+double Problem::global_sum(double local) {
+  if (!sharded()) return local;
+  red_all.ensure(sh.P + 1);
+  double* d = red_all.get();
+  TP_CUDA(cudaMemcpyAsync(d + sh.P, &local, sizeof(double), cudaMemcpyHostToDevice, stream));
+  TP_NCCL(ncclAllGather(d + sh.P, d, 1, ncclDouble, comm_of(*this), stream));
+  std::vector<double> h(sh.P);
+  TP_CUDA(cudaMemcpyAsync(h.data(), d, sh.P * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  double s = 0;
+  for (int q = 0; q < sh.P; ++q) s += h[q];  // rank order: deterministic
+  return s;
+}
+
+void Problem::global_minmax(double* lo, double* hi, int count) {
+  if (!sharded()) return;
+  red_all.ensure((size_t)2 * count * (sh.P + 1));
+  double* d = red_all.get();
+  std::vector<double> mine(2 * count);
+  for (int i = 0; i < count; ++i) {
+    mine[i] = lo[i];
+    mine[count + i] = hi[i];
+  }
+  double* src = d + (size_t)2 * count * sh.P;
+  TP_CUDA(cudaMemcpyAsync(src, mine.data(), 2 * count * sizeof(double), cudaMemcpyHostToDevice, stream));
+  TP_NCCL(ncclAllGather(src, d, 2 * count, ncclDouble, comm_of(*this), stream));
+  std::vector<double> h((size_t)2 * count * sh.P);
+  TP_CUDA(cudaMemcpyAsync(h.data(), d, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  for (int q = 0; q < sh.P; ++q)
+    for (int i = 0; i < count; ++i) {
+      lo[i] = std::fmin(lo[i], h[(size_t)q * 2 * count + i]);
+      hi[i] = std::fmax(hi[i], h[(size_t)q * 2 * count + count + i]);
+    }
+}
+
+// Ghat (K x nr, my strip) -> Ghat_f ((k1-k0) x n, my frequencies).
+// To rank q: rows [ks[q], ks[q+1]) of my Ghat -- contiguous.  From rank q:
+// its strip of my frequencies, (k1-k0) x n_q, received into staging and
+// scattered into the columns [ys[q]*m, ys[q+1]*m) of Ghat_f.
+void Problem::alltoall_to_freq() {
+  const int Kr = sh.k1 - sh.k0;
+  ncclComm_t c = comm_of(*this);
+  size_t off = 0;
+  std::vector<size_t> soff(sh.P);
+  for (int q = 0; q < sh.P; ++q) {
+    soff[q] = off;
+    off += (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m;
+  }
+  xstage.ensure(off);
+  TP_NCCL(ncclGroupStart());
+  for (int q = 0; q < sh.P; ++q) {
+    const size_t cnt_send = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * 2;  // doubles
+    const size_t cnt_recv = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * 2;
+    TP_NCCL(ncclSend(Ghat.get() + (size_t)sh.ks[q] * sh.nr, cnt_send, ncclDouble, q, c, stream));
+    TP_NCCL(ncclRecv(xstage.get() + soff[q], cnt_recv, ncclDouble, q, c, stream));
+  }
+  TP_NCCL(ncclGroupEnd());
+  for (int q = 0; q < sh.P; ++q) {
+    const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
+    TP_CUDA(cudaMemcpy2DAsync(Ghat_f.get() + (size_t)sh.ys[q] * m, (size_t)n * sizeof(cplx), xstage.get() + soff[q],
+                              nq * sizeof(cplx), nq * sizeof(cplx), Kr, cudaMemcpyDeviceToDevice, stream));
+  }
+}
+
+// Uhat_f ((k1-k0) x n) -> Uhat (K x nr): the reverse of alltoall_to_freq.
+void Problem::alltoall_from_freq() {
+  const int Kr = sh.k1 - sh.k0;
+  ncclComm_t c = comm_of(*this);
+  size_t off = 0;
+  std::vector<size_t> soff(sh.P);
+  for (int q = 0; q < sh.P; ++q) {
+    soff[q] = off;
+    off += (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m;
+  }
+  xstage.ensure(off);
+  for (int q = 0; q < sh.P; ++q) {
+    const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
+    TP_CUDA(cudaMemcpy2DAsync(xstage.get() + soff[q], nq * sizeof(cplx), Uhat_f.get() + (size_t)sh.ys[q] * m,
+                              (size_t)n * sizeof(cplx), nq * sizeof(cplx), Kr, cudaMemcpyDeviceToDevice, stream));
+  }
+  TP_NCCL(ncclGroupStart());
+  for (int q = 0; q < sh.P; ++q) {
+    const size_t cnt_send = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * 2;
+    const size_t cnt_recv = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * 2;
+    TP_NCCL(ncclSend(xstage.get() + soff[q], cnt_send, ncclDouble, q, c, stream));
+    TP_NCCL(ncclRecv(Uhat.get() + (size_t)sh.ks[q] * sh.nr, cnt_recv, ncclDouble, q, c, stream));
+  }
+  TP_NCCL(ncclGroupEnd());
+}
+
+// Us: my static-init slices [s0, s1) on the full grid ((s1-s0) x n).  To
+// rank q: rows of q's strip for my slices (strided, packed); from rank q:
+// its slices of my strip, contiguous at U + ss[q]*nr.
+void Problem::slices_to_strips(const double* Us) {
+  const int Ns = sh.s1 - sh.s0;
+  ncclComm_t c = comm_of(*this);
+  DevBuf<double> pack((size_t)Ns * n);
+  size_t off = 0;
+  std::vector<size_t> soff(sh.P);
+  for (int q = 0; q < sh.P; ++q) {
+    soff[q] = off;
+    const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
+    TP_CUDA(cudaMemcpy2DAsync(pack.get() + off, nq * sizeof(double), Us + (size_t)sh.ys[q] * m, (size_t)n * sizeof(double),
+                              nq * sizeof(double), Ns, cudaMemcpyDeviceToDevice, stream));
+    off += (size_t)Ns * nq;
+  }
+  TP_NCCL(ncclGroupStart());
+  for (int q = 0; q < sh.P; ++q) {
+    const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
+    TP_NCCL(ncclSend(pack.get() + soff[q], (size_t)Ns * nq, ncclDouble, q, c, stream));
+    TP_NCCL(ncclRecv(U.get() + (size_t)sh.ss[q] * sh.nr, (size_t)(sh.ss[q + 1] - sh.ss[q]) * sh.nr, ncclDouble,
+                     q, c, stream));
+  }
+  TP_NCCL(ncclGroupEnd());
+  TP_CUDA(cudaStreamSynchronize(stream));
+}
+
+}  // namespace tpgpu
+
+// =================================================================== C ABI
+struct tp_comm {
+  ncclComm_t comm = nullptr;
+  int nranks = 1, rank = 0, device = 0;
+};
+
+extern "C" {
+
+int tp_shard_plan_make(int32_t cells, int32_t steps, int32_t nranks, int32_t rank, tp_shard_plan* out) {
+  try {
+    tpgpu::require(out != nullptr, "null plan");
+    tpgpu::require(cells >= 2 && steps >= 1, "shard plan: bad sizes");
+    tpgpu::ShardInfo sh;
+    const int m = cells - 1;
+    tpgpu::make_partition(m, steps / 2 + 1, steps, nranks, rank, sh);
+    out->nranks = sh.P;
+    out->rank = sh.r;
+    out->row0 = sh.y0;
+    out->row1 = sh.y1;
+    out->freq0 = sh.k0;
+    out->freq1 = sh.k1;
+    out->slice0 = sh.s0;
+    out->slice1 = sh.s1;
+    out->n_local = sh.nr;
+    return TP_OK;
+  } catch (const std::exception& e) {
+    tpgpu::set_last_error(e.what(), -1.0);
+    return TP_EINVAL;
+  }
+}
+
+int tp_nccl_unique_id(unsigned char id[128]) {
+  try {
+    ncclUniqueId u;
+    if (ncclGetUniqueId(&u) != ncclSuccess) return TP_ECUDA;
+    static_assert(sizeof(u.internal) == 128, "NCCL unique id size");
+    std::memcpy(id, u.internal, 128);
+    return TP_OK;
+  } catch (const std::exception& e) {
+    tpgpu::set_last_error(e.what(), -1.0);
+    return TP_ECUDA;
+  }
+}
+
+int tp_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device, tp_comm** out) {
+  if (!out || nranks < 1 || rank < 0 || rank >= nranks) return TP_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TP_ECUDA;
+  try {
+    ncclUniqueId u;
+    std::memcpy(u.internal, id, 128);
+    auto* c = new tp_comm;
+    c->nranks = nranks;
+    c->rank = rank;
+    c->device = device;
+    if (ncclCommInitRank(&c->comm, nranks, u, rank) != ncclSuccess) {
+      delete c;
+      tpgpu::set_last_error("ncclCommInitRank failed", -1.0);
+      return TP_ECUDA;
+    }
+    *out = c;
+    return TP_OK;
+  } catch (const std::exception& e) {
+    tpgpu::set_last_error(e.what(), -1.0);
+    return TP_ECUDA;
+  }
+}
+
+void tp_comm_destroy(tp_comm* c) {
+  if (!c) return;
+  try {
+    if (c->comm) ncclCommDestroy(c->comm);
+  } catch (...) {
+  }
+  delete c;
+}
+
+void* tp_comm_nccl(tp_comm* c) { return c ? (void*)c->comm : nullptr; }
+int32_t tp_comm_rank(const tp_comm* c) { return c ? c->rank : -1; }
+int32_t tp_comm_size(const tp_comm* c) { return c ? c->nranks : 0; }
+int32_t tp_comm_device(const tp_comm* c) { return c ? c->device : -1; }
+
+}  // extern "C"

@@ -34,6 +34,8 @@ struct Error : std::runtime_error {
     if (tp_e_ != cudaSuccess) ::tpgpu::throw_cuda(tp_e_, "kernel launch", __FILE__, __LINE__); \
   } while (0)
 
+void set_last_error(const std::string& msg, double residual);
+
 inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(TP_EINVAL, msg);
 }
@@ -125,10 +127,26 @@ struct SolveStats {
   double max_rel_residual = 0;
 };
 
+// ---------------------------------------------------------------- sharding
+// One rank of a multi-GPU problem: node-row strip [y0, y1)
+// for the operator / residual / DFT stages (all N slices local), frequency
+// block [k0, k1) for the solves (full grid), slice block [s0, s1) for the
+// static initialisation (full grid).  P == 1 is the single-GPU problem.
+struct ShardInfo {
+  int P = 1, r = 0;
+  int y0 = 0, y1 = 0;
+  int k0 = 0, k1 = 0;
+  int s0 = 0, s1 = 0;
+  int nr = 0;  // local dofs (y1-y0)*m
+  std::vector<int> ys, ks, ss;  // partition points, P+1 each
+  void* comm = nullptr;         // ncclComm_t
+};
+void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh);
+
 // ---------------------------------------------------------------- problem
 class Problem {
  public:
-  Problem(const tp_problem_desc& d, int device);
+  Problem(const tp_problem_desc& d, int device, const ShardInfo* shard = nullptr);
   ~Problem();
 
   // host setup products
@@ -175,6 +193,21 @@ class Problem {
   std::unique_ptr<FreqWork> fw;
 
   std::shared_ptr<void> fft_plan;
+
+  // multi-GPU (P > 1): partition, halo rows, frequency-block spectra
+  ShardInfo sh;
+  bool sharded() const { return sh.comm != nullptr; }
+  DevBuf<double> halo_lo, halo_hi, halo_send;  // N*m each
+  DevBuf<cplx> Ghat_f, Uhat_f, xstage;         // (k1-k0)*n frequency blocks, staging
+  DevBuf<double> red_all;                      // P doubles (allgather)
+  void exchange_halo();
+  double global_sum(double local);
+  void global_minmax(double* lo, double* hi, int count);
+  void alltoall_to_freq();    // Ghat (K x nr) -> Ghat_f ((k1-k0) x n)
+  void alltoall_from_freq();  // Uhat_f -> Uhat (K x nr)
+  void slices_to_strips(const double* Us);  // static-init slices (full grid) -> U strips
+  cplx* spec_in() { return sharded() ? Ghat_f.get() : Ghat.get(); }
+  cplx* spec_out() { return sharded() ? Uhat_f.get() : Uhat.get(); }
 
   // pinned host scratch
   double* h_scalars = nullptr;  // pinned, 4096 doubles

@@ -201,3 +201,30 @@ def test_cfg1_against_golden():
         h = np.array(rep.residual_history)
         assert np.all(np.abs(h - g["history"]) <= 1e-10 * g["history"][0])
         assert np.allclose(U.reshape(-1)[::997], g["U_last_sample"], rtol=1e-9, atol=1e-12)
+
+
+def test_sharded_path_single_rank_matches():
+    """The multi-GPU code path (NCCL communicator, halo exchange, strip <->
+    frequency all-to-alls, slice-sharded static_init, rank-ordered sums) run
+    with one rank must reproduce the single-GPU problem exactly."""
+    from paper_2502_21013_b200 import Comm, nccl_unique_id
+    d = small_desc(32, 16)
+    cfg = default_cfg(tol=1e-8, m1_max_outer=6)
+    with Problem(d) as p:
+        U0, c0 = p.static_init(cfg)
+        nu, q = p.choose_nu_hat(cfg)
+        U, rep = p.solve_m1_fixed_point(None, cfg)
+    comm = Comm(nccl_unique_id(), 1, 0, 0)
+    ps = Problem.sharded(d, comm)
+    plan = ps.shard()
+    assert (plan.nranks, plan.row0, plan.row1, plan.freq0, plan.freq1) == (1, 0, 31, 0, 9)
+    U0s, c0s = ps.static_init(cfg)
+    nus, qs = ps.choose_nu_hat(cfg)
+    Us, reps = ps.solve_m1_fixed_point(None, cfg)
+    ps.close()
+    comm.close()
+    assert np.array_equal(c0, c0s) and np.array_equal(U0, U0s)
+    assert np.array_equal(nu, nus) and q == qs
+    assert reps.iterations == rep.iterations
+    assert np.allclose(reps.residual_history, rep.residual_history, rtol=1e-14, atol=0)
+    assert rel(Us, U) <= 1e-14
