@@ -15,8 +15,12 @@ max over ranks.  Every sweep streams U, G, Ghat, Uhat (133 MB each, > L2).
 `e2e` goes through the C ABI with pinned HOST buffers: each step uploads U,
 runs one sweep (tp_solve_m1 with m1_max_outer = 1) and downloads U.
 
-Multi-GPU (torchrun): each rank runs the workload on its own GPU (weak
-scaling, replicas); the N>1 sharded solver is not wired into the bench yet.
+Multi-GPU (torchrun, one process per GPU): the workload is SHARDED across
+the ranks (strong scaling): node-row strips for K(u) /
+residual / RHS / DFTs, frequency blocks for the solves, NCCL all-to-alls
+between them, halo rows and rank-ordered scalar sums.  torch.distributed
+(gloo) only bootstraps the NCCL communicator; `--replicas` runs independent
+copies instead (weak scaling).
 """
 from __future__ import annotations
 
@@ -126,15 +130,17 @@ def cudart():
     return torch
 
 
-def workload_config(desc, world):
+def workload_config(desc, world, replicas=False):
     n = (desc.cells - 1) ** 2
     D = n * desc.steps
+    par = "single GPU" if world == 1 else (f"replicas x{world}" if replicas else
+                                           f"sharded x{world}: row strips + frequency blocks, NCCL all-to-all")
     return D, {
         "workload": f"BASELINE configs[1]: {desc.cells}x{desc.cells} cells ({n} dofs) x N={desc.steps} "
                     "slices, fp64, U0 = static_init, frozen-field nu_hat",
         "cells": desc.cells, "steps": desc.steps, "space_time_dof": D,
         "l2": "inputs larger than L2 (U, G, Ghat, Uhat 133 MB each, streamed every sweep)",
-        "parallelism": f"replicas x{world}" if world > 1 else "single GPU",
+        "parallelism": par,
     }
 
 
@@ -146,9 +152,16 @@ def run_b200(args):
     from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg
 
     desc = baseline_desc(args.config)
-    D, config = workload_config(desc, world)
+    D, config = workload_config(desc, world, args.replicas)
     cfg = default_cfg(tol=1e-8)
-    p = Problem(desc, device=local)
+    sharded = world > 1 and not args.replicas
+    comm = None
+    if sharded:
+        from paper_2502_21013_b200 import Comm
+        comm = Comm.from_torch(local)
+        p = Problem.sharded(desc, comm)
+    else:
+        p = Problem(desc, device=local)
     t0 = time.perf_counter()
     U0, counts = p.static_init(cfg)
     nu, q = p.choose_nu_hat(cfg)
@@ -179,7 +192,8 @@ def run_b200(args):
     per = [evs[k].elapsed_time(evs[k + 1]) for k in range(args.steps)]
     total_ms = evs[0].elapsed_time(evs[-1])
     total_ms = allreduce_max(pg, total_ms)
-    value = D * args.steps * world / (total_ms / 1e3)
+    jobs = 1 if sharded else world  # sharded: one job over all GPUs; replicas: world jobs
+    value = D * args.steps * jobs / (total_ms / 1e3)
 
     # e2e through the C ABI with pinned host buffers (one sweep per call)
     e2e = None
@@ -196,7 +210,7 @@ def run_b200(args):
             p.solve_m1_fixed_point(Uh, c1, out=Uo)
             times.append(time.perf_counter() - t)
         e2e_s = allreduce_max(pg, float(np.median(times)))
-        e2e = {"value": D * world / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Uh.nbytes),
+        e2e = {"value": D * jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Uh.nbytes),
                "d2h_bytes_per_step": int(Uo.nbytes),
                "note": "tp_solve_m1 per step: H2D U0, initial residual, one sweep (cold inner start), D2H U"}
 
@@ -222,7 +236,7 @@ def run_b200(args):
                 "time_to_residual_s": init_s + t_setup + sum(sw) / 1e3,
                 "init_s": init_s, "setup_s": t_setup, "sweeps_s": sum(sw) / 1e3,
                 "median_sweep_ms": float(np.median(sw)),
-                "median_dof_per_s": D / (float(np.median(sw)) / 1e3),
+                "median_dof_per_s": D * jobs / (allreduce_max(pg, float(np.median(sw))) / 1e3),
                 "inner_iterations_median": float(np.median(its)),
                 "inner_iterations_max": int(max(its)) if its else 0}
 
@@ -241,7 +255,7 @@ def run_b200(args):
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+           "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
            "data": "synthetic (BASELINE.json configs[1] physics, seeded sigma noise)",
            "config": config, "impl": "b200", "clocks": clk.summary(),
            "e2e": e2e, "gpu_launches": launches, "roofline": roofline,
@@ -254,6 +268,8 @@ def run_b200(args):
     if rank == 0:
         print(json.dumps(out), flush=True)
     p.close()
+    if comm is not None:
+        comm.close()
 
 
 def cpu_baseline(desc, U0, nu, q):
@@ -328,6 +344,7 @@ def main():
     ap.add_argument("--e2e-steps", type=int, default=3)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-full-solve", dest="full_solve", action="store_false")
+    ap.add_argument("--replicas", action="store_true", help="N>1: independent copies instead of sharding")
     ap.add_argument("--ref-u0", default=None, help="reference arm: precomputed U0 (.npy)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
