@@ -434,7 +434,7 @@ constexpr int H2X = TX + 5, H2Y = TY + 5, H2N = H2X * H2Y;  // 481
 constexpr int DX = TX + 3, DY = TY + 3, DN = DX * DY;       // 385
 constexpr int H1X = TX + 2, H1Y = TY + 2, H1N = H1X * H1Y;  // 340
 constexpr int QX = TX + 1, QY = TY + 1, QN = QX * QY;       // 297
-enum { SM_JAC = 0, SM_RB = 1 };
+enum { SM_JAC = 0, SM_RB = 1, SM_J1 = 2 };  // J1: one Jacobi step pre and post
 
 template <int FAM>
 struct CoefPlanes;
@@ -536,7 +536,8 @@ __device__ __forceinline__ cplx lam_of(const Op<MODE>& op, int b) {
 template <int MODE, int FAM, int SM>
 __global__ void __launch_bounds__(NT, 3) k_down(Op<MODE> op, Op<MODE> opc, const TT<MODE>* __restrict__ rv,
                                                 TT<MODE>* __restrict__ z2out, TT<MODE>* __restrict__ bc,
-                                                const int* __restrict__ active, double omega, int nb, int BB) {
+                                                const int* __restrict__ active, double omega, double omega2,
+                                                int nb, int BB) {
   using T = TT<MODE>;
   extern __shared__ __align__(16) unsigned char dsm[];
   double* cf = reinterpret_cast<double*>(dsm);
@@ -602,8 +603,12 @@ __global__ void __launch_bounds__(NT, 3) k_down(Op<MODE> op, Op<MODE> opc, const
       if constexpr (SM == SM_RB) {
         const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
         v = red ? sZ[h] : mul(sR[h] - off, inv_of(d));
+      } else if constexpr (SM == SM_J1) {
+        (void)d;
+        (void)off;
+        v = sZ[h];
       } else {
-        v = sZ[h] + omega * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
+        v = sZ[h] + omega2 * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
       }
       sW[h] = v;
     }
@@ -634,7 +639,7 @@ __global__ void __launch_bounds__(NT, 3) k_up(Op<MODE> op, const TT<MODE>* __res
                                               const TT<MODE>* __restrict__ z2in,
                                               const TT<MODE>* __restrict__ xc, int mc,
                                               TT<MODE>* __restrict__ zout, const int* __restrict__ active,
-                                              double omega, int nb, int BB, int dot,
+                                              double omega, double omega2, int nb, int BB, int dot,
                                               double* __restrict__ part) {
   using T = TT<MODE>;
   extern __shared__ __align__(16) unsigned char dsm[];
@@ -710,8 +715,12 @@ __global__ void __launch_bounds__(NT, 3) k_up(Op<MODE> op, const TT<MODE>* __res
       if constexpr (SM == SM_RB) {
         const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
         v = red ? sZ[h] : mul(sR[h] - off, inv_of(d));
+      } else if constexpr (SM == SM_J1) {
+        (void)d;
+        (void)off;
+        v = sZ[h];
       } else {
-        v = sZ[h] + omega * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
+        v = sZ[h] + omega2 * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
       }
       sW[h] = v;
     }
@@ -1106,7 +1115,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
     if (ops[l].fine.we) {
       FineOp fo = ops[l].fine;
       fo.lam = lam;
-      launch_fine_down(*p, fo, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, nb);
+      launch_fine_down(*p, fo, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, cfg.omega2, nb);
       T* xcf;
       if (l + 1 == L - 1) {
         k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
@@ -1115,7 +1124,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
       } else {
         xcf = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
       }
-      launch_fine_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, nb, dot ? 1 : 0, part.get());
+      launch_fine_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
       return zo;
     }
   }
@@ -1124,8 +1133,10 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
 #define LAUNCH_DOWN(SMV)                                                                        \
   DISPATCH_FAM(l, (set_fused_attrs<MODE, FAM, SMV>(),                                          \
                    k_down<MODE, FAM, SMV><<<g.grid, blk, fused_smem<MODE, FAM>(true), s>>>(     \
-                       op, opc, bl, z2, lb[l + 1].get(), act, cfg.omega, nb, g.BB)))
-  if (rb) { LAUNCH_DOWN(SM_RB); } else { LAUNCH_DOWN(SM_JAC); }
+                       op, opc, bl, z2, lb[l + 1].get(), act, cfg.omega, cfg.omega2, nb, g.BB)))
+  static const bool coarse_j1 = std::getenv("TPGPU_COARSE_J1") != nullptr;
+  const bool j1 = coarse_j1 && l > 0;
+  if (rb) { LAUNCH_DOWN(SM_RB); } else if (j1) { LAUNCH_DOWN(SM_J1); } else { LAUNCH_DOWN(SM_JAC); }
   TP_LAUNCHED(p);
   T* xc;
   if (l + 1 == L - 1) {
@@ -1140,8 +1151,8 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
 #define LAUNCH_UP(SMV)                                                                          \
   DISPATCH_FAM(l, (set_fused_attrs<MODE, FAM, SMV>(),                                          \
                    k_up<MODE, FAM, SMV><<<g.grid, blk, fused_smem<MODE, FAM>(false), s>>>(      \
-                       op, bl, z2, xc, mcl, zo, act, cfg.omega, nb, g.BB, d, part.get())))
-  if (rb) { LAUNCH_UP(SM_RB); } else { LAUNCH_UP(SM_JAC); }
+                       op, bl, z2, xc, mcl, zo, act, cfg.omega, cfg.omega2, nb, g.BB, d, part.get())))
+  if (rb) { LAUNCH_UP(SM_RB); } else if (j1) { LAUNCH_UP(SM_J1); } else { LAUNCH_UP(SM_JAC); }
   TP_LAUNCHED(p);
   return zo;
 }

@@ -21,7 +21,10 @@ namespace tpgpu {
 
 struct MGConfig {
   int pre = 2, post = 2;    // smoothing sweeps
-  double omega = 0.8;       // Jacobi damping
+  // Damped-Jacobi steps with a degree-2 Chebyshev pair of weights for D^-1 A
+  // on [1/3, 2] (pre: omega then omega2; post: omega2 then omega -- adjoint)
+  double omega = 0.57;
+  double omega2 = 1.7;
   double rtol = 1e-13;      // ||r_b|| <= rtol ||b_b||
   int max_iter = 200;
   bool rb_fine = true;      // red-black Gauss-Seidel on the 5-point fine level
@@ -90,9 +93,9 @@ int fine_partials(int m, int kind);
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init);
 void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                      const int* active, double omega, int nb);
+                      const int* active, double om1, double om2, int nb);
 void launch_fine_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
-                    cplx* z, const int* active, double omega, int nb, int dot, double* part);
+                    cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).
 void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches);
 

@@ -218,8 +218,8 @@ __global__ void __launch_bounds__(WL * WPB, 6) k_fine_apply(FineOp op, const cpl
 // ---------------------------------------------------------------- down
 __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx* __restrict__ rv,
                                                            cplx* __restrict__ z2out, cplx* __restrict__ bc,
-                                                           int mc, const int* __restrict__ active, double omega,
-                                                           int nb) {
+                                                           int mc, const int* __restrict__ active, double om1,
+                                                           double om2, int nb) {
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
   const int m = op.m;
   const Item it = item_of(m, OWN, nb, active);
@@ -252,7 +252,7 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
     w0 = row_w(op, x, yi);
     // z1 = omega r / d at row yi (zero outside the domain: r = 0 there)
     a2 = a1; a1 = a0;
-    a0 = cs(omega, cm(r0, rcp(diag(expand(w0, w1), l))));
+    a0 = cs(om1, cm(r0, rcp(diag(expand(w0, w1), l))));
     // z2 at row yi-1
     b3 = b2; b2 = b1;
     {
@@ -262,7 +262,7 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
       const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, rcp(diag(k1, l)));
       const int y = yi - 1;
       const bool in = colok && y >= 0 && y < m;
-      b1 = in ? cplx{fma(omega, t.re, a1.re), fma(omega, t.im, a1.im)} : cplx{0, 0};
+      b1 = in ? cplx{fma(om2, t.re, a1.re), fma(om2, t.im, a1.im)} : cplx{0, 0};
       if (own && y >= ys && y < ye) zo[(long)y * m] = b1;
     }
     // residual at row yi-2
@@ -292,7 +292,7 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
 __global__ void __launch_bounds__(WL * WPB, 5) k_fine_up(FineOp op, const cplx* __restrict__ rv,
                                                          const cplx* __restrict__ z2in, const cplx* __restrict__ xcv,
                                                          int mc, cplx* __restrict__ zout,
-                                                         const int* __restrict__ active, double omega, int nb,
+                                                         const int* __restrict__ active, double om1, double om2, int nb,
                                                          int dot, double* __restrict__ part) {
   constexpr int H = 2, OWN = WL - 2 * H;  // 28
   const int m = op.m;
@@ -352,7 +352,7 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_up(FineOp op, const cplx* 
       const cplx Ac = apply_at(k1, l, c1, cw, ce, c2, c0);
       const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, rcp(diag(k1, l)));
       const int y = yi - 1;
-      e1 = (colok && y >= 0 && y < m) ? cplx{fma(omega, t.re, c1.re), fma(omega, t.im, c1.im)} : cplx{0, 0};
+      e1 = (colok && y >= 0 && y < m) ? cplx{fma(om2, t.re, c1.re), fma(om2, t.im, c1.im)} : cplx{0, 0};
     }
     // z4 at row yi-2
     {
@@ -362,7 +362,7 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_up(FineOp op, const cplx* 
       if (own && y >= ys && y < ye) {
         const cplx Ae = apply_at(k2, l, e2, ew, ee, e3, e1);
         const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, rcp(diag(k2, l)));
-        const cplx z4 = {fma(omega, t.re, e2.re), fma(omega, t.im, e2.im)};
+        const cplx z4 = {fma(om1, t.re, e2.re), fma(om1, t.im, e2.im)};
         zo[(long)y * m] = z4;
         if (dot) {
           const cplx pr = cm(r2, z4);
@@ -406,14 +406,14 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
 }
 
 void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                      const int* active, double omega, int nb) {
-  k_fine_down<<<grid_for(op.m, 26, nb), WL * WPB, 0, p.stream>>>(op, r, z2, bc, mc, active, omega, nb);
+                      const int* active, double om1, double om2, int nb) {
+  k_fine_down<<<grid_for(op.m, 26, nb), WL * WPB, 0, p.stream>>>(op, r, z2, bc, mc, active, om1, om2, nb);
   TP_LAUNCHED(&p);
 }
 
 void launch_fine_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
-                    cplx* z, const int* active, double omega, int nb, int dot, double* part) {
-  k_fine_up<<<grid_for(op.m, 28, nb), WL * WPB, 0, p.stream>>>(op, r, z2, xc, mc, z, active, omega, nb, dot,
+                    cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
+  k_fine_up<<<grid_for(op.m, 28, nb), WL * WPB, 0, p.stream>>>(op, r, z2, xc, mc, z, active, om1, om2, nb, dot,
                                                               part);
   TP_LAUNCHED(&p);
 }

@@ -354,7 +354,8 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   mc.max_iter = cfg.inner_max_iter;
   // experiment overrides (documented in DESIGN.md §5)
   if (const char* e = std::getenv("TPGPU_RB_FINE")) mc.rb_fine = std::atoi(e) != 0;
-  if (const char* e = std::getenv("TPGPU_OMEGA")) mc.omega = std::atof(e);
+  if (const char* e = std::getenv("TPGPU_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
+  if (const char* e = std::getenv("TPGPU_OMEGA2")) mc.omega2 = std::atof(e);
   fw->solver.init(this, ops, chunk, mc);
   TP_CUDA(cudaStreamSynchronize(stream));
   freq_ready = true;
