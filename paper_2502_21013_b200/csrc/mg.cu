@@ -443,8 +443,8 @@ struct CoefPlanes<1> {  // fine: diag K, diag M, 4 real off-diagonals (W, E, S, 
   static constexpr int planes = 6;
 };
 template <>
-struct CoefPlanes<0> {  // coarse frequency mode: 7 K + 7 M
-  static constexpr int planes = 14;
+struct CoefPlanes<0> {  // coarse frequency mode, symmetric: K and M at C, E, N, NE
+  static constexpr int planes = 8;
 };
 template <>
 struct CoefPlanes<2> {  // slice mode: 7 J (per batch)
@@ -467,10 +467,13 @@ __device__ __forceinline__ void stage_coefs(const Op<MODE>& op, double* cf, int 
       cf[1 * H2N + k] = in ? __ldg(o.M + i) : 0.0;
       for (int d = 1; d <= 4; ++d) cf[(1 + d) * H2N + k] = in ? __ldg(o.K + d * n + i) : 0.0;
     } else if constexpr (FAM == 0) {
+      // Galerkin operators are symmetric: W(i) = E(i-1), S(i) = N(i-m),
+      // SW(i) = NE(i-m-1), so four planes per matrix describe them
       const Op<0>& o = op;
-      for (int d = 0; d < 7; ++d) {
-        cf[d * H2N + k] = in ? __ldg(o.K + d * n + i) : (d == 0 ? 1.0 : 0.0);
-        cf[(7 + d) * H2N + k] = in ? __ldg(o.M + d * n + i) : 0.0;
+      const int dirs[4] = {SC, SE_, SN_, SNE};
+      for (int q = 0; q < 4; ++q) {
+        cf[q * H2N + k] = in ? __ldg(o.K + dirs[q] * n + i) : (q == 0 ? 1.0 : 0.0);
+        cf[(4 + q) * H2N + k] = in ? __ldg(o.M + dirs[q] * n + i) : 0.0;
       }
     } else {
       const Op<1>& o = op;
@@ -488,7 +491,7 @@ __device__ __forceinline__ TT<MODE> cdiag(const double* cf, int h, cplx l) {
   } else if constexpr (FAM == 1) {
     return cplx{fma(l.re, cf[H2N + h], cf[h]), l.im * cf[H2N + h]};
   } else {
-    return cplx{fma(l.re, cf[7 * H2N + h], cf[h]), l.im * cf[7 * H2N + h]};
+    return cplx{fma(l.re, cf[4 * H2N + h], cf[h]), l.im * cf[4 * H2N + h]};
   }
 }
 
@@ -510,12 +513,16 @@ __device__ __forceinline__ TT<MODE> coff(const double* cf, const TT<MODE>* v, in
            cf[5 * H2N + h] * vsw + cf[6 * H2N + h] * vne;
   } else {
     const T vsw = v[h - H2X - 1], vne = v[h + H2X + 1];
+    // (plane, node) of each neighbour's coefficient: W = E(h-1), E = E(h),
+    // S = N(h-row), N = N(h), SW = NE(h-row-1), NE = NE(h)
+    const int pl[6] = {1, 1, 2, 2, 3, 3};
+    const int at[6] = {h - 1, h, h - H2X, h, h - H2X - 1, h};
     const T vv[6] = {vw, ve, vs, vn, vsw, vne};
     T acc = zero_of(T{});
 #pragma unroll
-    for (int d = 1; d <= 6; ++d) {
-      const double mm = cf[(7 + d) * H2N + h];
-      acc = acc + mul(cplx{fma(l.re, mm, cf[d * H2N + h]), l.im * mm}, vv[d - 1]);
+    for (int d = 0; d < 6; ++d) {
+      const double kk = cf[pl[d] * H2N + at[d]], mm = cf[(4 + pl[d]) * H2N + at[d]];
+      acc = acc + mul(cplx{fma(l.re, mm, kk), l.im * mm}, vv[d]);
     }
     return acc;
   }
@@ -523,8 +530,8 @@ __device__ __forceinline__ TT<MODE> coff(const double* cf, const TT<MODE>* v, in
 
 template <int MODE, int FAM>
 static constexpr size_t fused_smem(bool down) {
-  return (size_t)CoefPlanes<FAM>::planes * H2N * sizeof(double) +
-         (size_t)3 * H2N * sizeof(TT<MODE>) + (down ? (size_t)QN * sizeof(TT<MODE>) : 0);
+  (void)down;
+  return (size_t)CoefPlanes<FAM>::planes * H2N * sizeof(double) + (size_t)3 * H2N * sizeof(TT<MODE>);
 }
 
 template <int MODE>
@@ -534,7 +541,7 @@ __device__ __forceinline__ cplx lam_of(const Op<MODE>& op, int b) {
 }
 
 template <int MODE, int FAM, int SM>
-__global__ void __launch_bounds__(NT, 3) k_down(Op<MODE> op, Op<MODE> opc, const TT<MODE>* __restrict__ rv,
+__global__ void __launch_bounds__(NT, 4) k_down(Op<MODE> op, Op<MODE> opc, const TT<MODE>* __restrict__ rv,
                                                 TT<MODE>* __restrict__ z2out, TT<MODE>* __restrict__ bc,
                                                 const int* __restrict__ active, double omega, double omega2,
                                                 int nb, int BB) {
@@ -544,7 +551,7 @@ __global__ void __launch_bounds__(NT, 3) k_down(Op<MODE> op, Op<MODE> opc, const
   T* sR = reinterpret_cast<T*>(dsm + (size_t)CoefPlanes<FAM>::planes * H2N * sizeof(double));
   T* sZ = sR + H2N;
   T* sW = sZ + H2N;
-  T* sQ = sW + H2N;
+  T* sQ = sZ;  // residual tile reuses z1's storage (z1 is dead once z2 is formed)
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int x0 = blockIdx.x * TX, y0 = blockIdx.y * TY;
   const int m = op.m, n = op.n;
@@ -635,7 +642,7 @@ __global__ void __launch_bounds__(NT, 3) k_down(Op<MODE> op, Op<MODE> opc, const
 }
 
 template <int MODE, int FAM, int SM>
-__global__ void __launch_bounds__(NT, 3) k_up(Op<MODE> op, const TT<MODE>* __restrict__ rv,
+__global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __restrict__ rv,
                                               const TT<MODE>* __restrict__ z2in,
                                               const TT<MODE>* __restrict__ xc, int mc,
                                               TT<MODE>* __restrict__ zout, const int* __restrict__ active,
@@ -1084,7 +1091,10 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
                                                               bool dot) {
   const int L = (int)ops.size();
   const Op<MODE> op = make_op<MODE>(ops[l], lam);
-  const Geo g = geo_for(ops[l].m, nb, p->num_sms, 8);
+  // coarse levels: few batches per block -- their blocks are latency-bound
+  // chains (stage, two smoothing steps, residual), so more blocks in flight win
+  static const int coarse_bb = std::getenv("TPGPU_COARSE_BB") ? std::atoi(std::getenv("TPGPU_COARSE_BB")) : 4;
+  const Geo g = geo_for(ops[l].m, nb, p->num_sms, l == 0 ? 8 : coarse_bb);
   int* act = active.get();
   cudaStream_t s = p->stream;
   const dim3 blk(TX, TY);
