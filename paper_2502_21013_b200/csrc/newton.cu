@@ -11,6 +11,7 @@
 // norms, in exactly the reference's order and arithmetic.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <string>
 
 #include "mg.cuh"
@@ -63,6 +64,12 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
   mc.max_iter = cfg.inner_max_iter;
+  // Newton Jacobians carry the anisotropic rank-one term (nu'/s) g g^T, so
+  // lambda_max(D^-1 J) can exceed 2: plain damped Jacobi with a safe weight
+  // keeps the V-cycle symmetric positive definite (the Chebyshev pair of the
+  // frequency solver assumes a spectrum in (0, 2]).
+  mc.omega = mc.omega2 = 0.6;
+  if (const char* e = std::getenv("TPGPU_NEWTON_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
   BatchSolver<1> solver;
   solver.init(this, ops, S, mc);
   solver.coarse_inv = inv.get();
