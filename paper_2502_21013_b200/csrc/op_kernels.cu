@@ -196,6 +196,118 @@ __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
     part[((size_t)s * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tot;
 }
 
+// Slice-looped form of k_sweep_fused (the one used by the sweep): a block
+// owns one 32x8 node tile and SB consecutive slices, so everything that
+// does not depend on u -- per-cell material law and nu_hat, per-node mass
+// and source profiles -- is loaded once and reused SB times, u^{s-1} comes
+// from the previous slice's tile, and r^2 is reduced once per block.
+constexpr int SB = 16;
+
+template <bool WANT_G>
+__global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
+    const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
+    int sy0, int rows, double* __restrict__ G, double* __restrict__ part, int m, int c, int N, double inv_tau,
+    const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
+    const double* __restrict__ nu_hat, const double* __restrict__ mass,
+    const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
+  __shared__ double su[TY + 2][TX + 2];
+  __shared__ double cnu0[TY + 1][TX + 1], cdnu[TY + 1][TX + 1], cbs2[TY + 1][TX + 1], chat[TY + 1][TX + 1];
+  __shared__ double red[32];
+  const size_t n = (size_t)m * m;
+  const size_t nl = (size_t)rows * m;
+  const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
+  const int x0 = blockIdx.x * TX, y0 = sy0 + blockIdx.y * TY;
+  const int sbeg = blockIdx.z * SB, send = min(N, sbeg + SB);
+  // per-cell material constants of the tile (+ halo cells)
+  for (int k = tid; k < (TY + 1) * (TX + 1); k += TX * TY) {
+    const int ly = k / (TX + 1), lx = k % (TX + 1);
+    const int i = x0 + lx, j = y0 + ly;
+    double a = 0, b = 0, bs = 1, h = 0;
+    if (i < c && j < c) {
+      const int mt = cell_mat[(size_t)j * c + i];
+      const MaterialDev md = mats[mt];
+      a = md.nu0;
+      b = md.linear ? 0.0 : md.nu_inf - md.nu0;
+      bs = md.bs2;
+      h = WANT_G ? 0.5 * nu_hat[mt] : 0.0;
+    }
+    cnu0[ly][lx] = a;
+    cdnu[ly][lx] = b;
+    cbs2[ly][lx] = bs;
+    chat[ly][lx] = h;
+  }
+  const int x = x0 + tx, y = y0 + ty;
+  const bool own = x < m && y < sy0 + rows;
+  const size_t i = own ? (size_t)y * m + x : 0;           // global
+  const size_t il = own ? (size_t)(y - sy0) * m + x : 0;  // local
+  const double mi = own ? mass[i] : 0.0;
+  double prof[TP_MAX_MATERIALS];
+#pragma unroll
+  for (int r = 0; r < TP_MAX_MATERIALS; ++r) prof[r] = (own && r < nsrc) ? src_prof[r * n + i] : 0.0;
+  double uprev = 0;
+  if (own && mi != 0) uprev = U[(size_t)((sbeg + N - 1) % N) * nl + il];
+  const double c2 = (double)c * (double)c;
+  double r2 = 0;
+  // each thread stages <= 2 tile values; the next slice's are loaded while
+  // the current slice is computed
+  constexpr int TN = (TY + 2) * (TX + 2);
+  const int k0 = tid, k1 = tid + TX * TY;
+  const int l0y = k0 / (TX + 2), l0x = k0 % (TX + 2), l1y = k1 / (TX + 2), l1x = k1 % (TX + 2);
+  auto fetch = [&](int s, double& v0, double& v1) {
+    const StripView sv{halo_lo ? halo_lo + (size_t)s * m : nullptr, halo_hi ? halo_hi + (size_t)s * m : nullptr,
+                       sy0, rows};
+    const double* us = U + (size_t)s * nl;
+    v0 = vertex_u(us, sv, m, x0 + l0x, y0 + l0y);
+    v1 = k1 < TN ? vertex_u(us, sv, m, x0 + l1x, y0 + l1y) : 0.0;
+  };
+  double n0 = 0, n1 = 0;
+  if (sbeg < send) fetch(sbeg, n0, n1);
+  for (int s = sbeg; s < send; ++s) {
+    __syncthreads();  // previous slice's tile fully consumed
+    su[l0y][l0x] = n0;
+    if (k1 < TN) su[l1y][l1x] = n1;
+    __syncthreads();
+    if (s + 1 < send) fetch(s + 1, n0, n1);
+    if (own) {
+      const int lx = tx + 1, ly = ty + 1;
+      const double uC = su[ly][lx], uE = su[ly][lx + 1], uW = su[ly][lx - 1];
+      const double uN = su[ly + 1][lx], uS = su[ly - 1][lx];
+      const double uNE = su[ly + 1][lx + 1], uSW = su[ly - 1][lx - 1];
+      // the six incident triangles: (cell, type, contribution dx*sx + dy*sy, (dx, dy))
+      // T1(X,Y): cell (lx,ly)    d=(uE-uC, uNE-uE)   contrib -(uE-uC)
+      // T2(X,Y): cell (lx,ly)    d=(uNE-uN, uN-uC)   contrib -(uN-uC)
+      // T1(X-1,Y): cell (lx-1,ly) d=(uC-uW, uN-uC)   contrib (uC-uW)-(uN-uC)
+      // T1(X-1,Y-1): cell (lx-1,ly-1) d=(uS-uSW, uC-uS) contrib (uC-uS)
+      // T2(X-1,Y-1): cell (lx-1,ly-1) d=(uC-uW, uW-uSW) contrib (uC-uW)
+      // T2(X,Y-1): cell (lx,ly-1) d=(uE-uC, uC-uS)    contrib -(uE-uC)+(uC-uS)
+      const double dx[6] = {uE - uC, uNE - uN, uC - uW, uS - uSW, uC - uW, uE - uC};
+      const double dy[6] = {uNE - uE, uN - uC, uN - uC, uC - uS, uW - uSW, uC - uS};
+      const double con[6] = {-(uE - uC), -(uN - uC), (uC - uW) - (uN - uC), uC - uS, uC - uW, -(uE - uC) + (uC - uS)};
+      const int cxs[6] = {0, 0, -1, -1, -1, 0}, cys[6] = {0, 0, 0, -1, -1, -1};
+      double ku = 0, kh = 0;
+#pragma unroll
+      for (int t = 0; t < 6; ++t) {
+        const int cx = lx + cxs[t], cy = ly + cys[t];
+        const double s2 = c2 * (dx[t] * dx[t] + dy[t] * dy[t]);
+        const double nu = fma(cdnu[cy][cx], s2 * __drcp_rn(s2 + cbs2[cy][cx]), cnu0[cy][cx]);
+        ku = fma(0.5 * nu, con[t], ku);
+        if (WANT_G) kh = fma(chat[cy][cx], con[t], kh);
+      }
+      double f = 0;
+#pragma unroll
+      for (int r = 0; r < TP_MAX_MATERIALS; ++r)
+        if (r < nsrc) f = fma(src_time[s * nsrc + r], prof[r], f);
+      if (WANT_G) G[(size_t)s * nl + il] = f + kh - ku;
+      const double mdu = mi != 0 ? mi * ((uC - uprev) * inv_tau) : 0.0;
+      const double res = f - mdu - ku;
+      r2 = fma(res, res, r2);
+      uprev = uC;
+    }
+  }
+  const double tot = block_sum(r2, red);
+  if (tid == 0) part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tot;
+}
+
 __global__ void k_reduce_sum(const double* __restrict__ in, int count, double* __restrict__ out) {
   __shared__ double sh[32];
   double v = 0;
@@ -316,21 +428,22 @@ static size_t sweep_partials(int m, int N) {
 double Problem::residual_and_rhs(bool want_rhs) {
   const int rows = sh.y1 - sh.y0;
   if (sharded()) exchange_halo();
-  dim3 grid((m + TX - 1) / TX, (rows + TY - 1) / TY, N);
+  dim3 grid((m + TX - 1) / TX, (rows + TY - 1) / TY, (N + SB - 1) / SB);
   const size_t np = (size_t)grid.x * grid.y * grid.z;
   part.ensure(np);
   const int nsrc = (int)src_mats.size();
+  require(nsrc <= TP_MAX_MATERIALS, "sweep: too many source materials");
   const double* lo = sharded() ? halo_lo.get() : nullptr;
   const double* hi = sharded() ? halo_hi.get() : nullptr;
   if (want_rhs) {
     require(nu_hat_set, "fixed-point sweep: nu_hat not installed");
-    k_sweep_fused<true, false><<<grid, dim3(TX, TY), 0, stream>>>(
-        U.get(), lo, hi, sh.y0, rows, G.get(), nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(),
-        d_mat.get(), d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+    k_sweep_slices<true><<<grid, dim3(TX, TY), 0, stream>>>(
+        U.get(), lo, hi, sh.y0, rows, G.get(), part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   } else {
-    k_sweep_fused<false, false><<<grid, dim3(TX, TY), 0, stream>>>(
-        U.get(), lo, hi, sh.y0, rows, nullptr, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(),
-        d_mat.get(), d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+    k_sweep_slices<false><<<grid, dim3(TX, TY), 0, stream>>>(
+        U.get(), lo, hi, sh.y0, rows, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   }
   TP_LAUNCHED(this);
   return std::sqrt(global_sum(reduce_sum(*this, part.get(), (int)np)));
