@@ -37,6 +37,7 @@ EXPORTS = [
     "tp_m1_begin", "tp_m1_sweep", "tp_problem_stream", "tp_problem_launches",
     "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
     "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
+    "tp_kernel_timer",
 ]
 
 
@@ -98,6 +99,7 @@ def lib():
             getattr(L, f).restype = C.c_int32
         L.tp_problem_create_sharded.argtypes = [D, vp, C.POINTER(vp)]
         L.tp_problem_shard.argtypes = [vp, SP]
+        L.tp_kernel_timer.argtypes = [vp, C.c_int32, C.POINTER(C.c_int64), dp, dp]
         _lib = L
     return _lib
 
@@ -370,6 +372,13 @@ class Problem:
         it = C.c_int32()
         _check(lib().tp_m1_sweep(self._h, C.byref(r), C.byref(it)))
         return r.value, it.value
+
+    def kernel_timer(self, enable: bool):
+        """(launches, ms, algorithmic bytes) of the dominant kernel since the
+        last call; then enable/disable the CUDA-event timer."""
+        n, ms, b = C.c_int64(), C.c_double(), C.c_double()
+        _check(lib().tp_kernel_timer(self._h, 1 if enable else 0, C.byref(n), C.byref(ms), C.byref(b)))
+        return n.value, ms.value, b.value
 
     @property
     def stream(self) -> int:

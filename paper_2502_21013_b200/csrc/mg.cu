@@ -1134,7 +1134,21 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
       } else {
         xcf = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
       }
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (p->ktimer.on) {
+        TP_CUDA(cudaEventCreate(&e0));
+        TP_CUDA(cudaEventCreate(&e1));
+        TP_CUDA(cudaEventRecord(e0, s));
+      }
       launch_fine_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
+      if (p->ktimer.on) {
+        TP_CUDA(cudaEventRecord(e1, s));
+        p->ktimer.pending.emplace_back(e0, e1);
+        // algorithmic bytes: read z2, r and the coarse correction (1/4), write z --
+        // 3.25 complex values per fine node of every active frequency
+        p->ktimer.bytes += 3.25 * 16.0 * (double)ops[l].n * (double)cur_active;
+        ++p->ktimer.launches;
+      }
       return zo;
     }
   }
@@ -1208,6 +1222,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int iters = 0;
   int64_t batch_iters = 0;
   int last_active = h_count[0];
+  cur_active = last_active;
   if (last_active > 0) {
     T* z = vcycle_level(0, nb, r.get(), nullptr, false, true);
     k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
@@ -1244,6 +1259,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       if (it >= 2) {
         TP_CUDA(cudaEventSynchronize(ev[slot ^ 1]));
         last_active = h_count[slot ^ 1];
+        cur_active = last_active;
         if (last_active == 0) {
           iters = it - 1;
           done = true;

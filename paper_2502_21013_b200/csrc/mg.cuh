@@ -68,6 +68,7 @@ struct BatchSolver {
   DevBuf<int> active;
   DevBuf<int> count;
   int* h_count = nullptr;  // pinned [2]
+  int cur_active = 0;      // active batches as last seen by the host (kernel-timer byte accounting)
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   void init(Problem* prob, const std::vector<LevelOp>& levels, int batches, const MGConfig& c);

@@ -224,7 +224,19 @@ Problem::Problem(const tp_problem_desc& d, int dev, const ShardInfo* shard) : de
   TP_CUDA(cudaMemsetAsync(U.get(), 0, U.bytes(), stream));
 }
 
+void Problem::KernelTimer::drain() {
+  for (auto& e : pending) {
+    float t = 0;
+    if (cudaEventSynchronize(e.second) == cudaSuccess && cudaEventElapsedTime(&t, e.first, e.second) == cudaSuccess)
+      ms += t;
+    cudaEventDestroy(e.first);
+    cudaEventDestroy(e.second);
+  }
+  pending.clear();
+}
+
 Problem::~Problem() {
+  ktimer.drain();
   fw.reset();
   if (h_scalars) cudaFreeHost(h_scalars);
   if (stream) cudaStreamDestroy(stream);
@@ -777,6 +789,20 @@ int tp_problem_shard(const tp_problem* p, tp_shard_plan* out) {
     out->slice0 = s.s0;
     out->slice1 = s.s1;
     out->n_local = s.nr;
+  });
+}
+
+int tp_kernel_timer(tp_problem* h, int32_t enable, int64_t* launches, double* ms, double* bytes) {
+  return guarded([&] {
+    Problem& p = P(h);
+    p.ktimer.drain();
+    if (launches) *launches = p.ktimer.launches;
+    if (ms) *ms = p.ktimer.ms;
+    if (bytes) *bytes = p.ktimer.bytes;
+    p.ktimer.launches = 0;
+    p.ktimer.ms = 0;
+    p.ktimer.bytes = 0;
+    p.ktimer.on = enable != 0;
   });
 }
 

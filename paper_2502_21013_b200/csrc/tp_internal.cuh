@@ -209,6 +209,16 @@ class Problem {
   cplx* spec_in() { return sharded() ? Ghat_f.get() : Ghat.get(); }
   cplx* spec_out() { return sharded() ? Uhat_f.get() : Uhat.get(); }
 
+  // live kernel timing for bench.py's roofline (enabled on request): the
+  // dominant kernel (fine-level V-cycle up pass) is bracketed by CUDA events
+  struct KernelTimer {
+    bool on = false;
+    int64_t launches = 0;
+    double bytes = 0, ms = 0;
+    std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+    void drain();
+  } ktimer;
+
   // pinned host scratch
   double* h_scalars = nullptr;  // pinned, 4096 doubles
 
