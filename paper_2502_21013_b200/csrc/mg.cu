@@ -344,11 +344,23 @@ __global__ void __launch_bounds__(NT, 4) k_apply_dot(Op<MODE> op, const TT<MODE>
                                                      TT<MODE>* __restrict__ pout, TT<MODE>* __restrict__ q,
                                                      const TT<MODE>* __restrict__ beta,
                                                      const int* __restrict__ active, int first, int nb,
-                                                     int BB, double* __restrict__ part) {
+                                                     int BB, double* __restrict__ part,
+                                                     TT<MODE>* __restrict__ xs, const TT<MODE>* __restrict__ xa) {
   using T = TT<MODE>;
   __shared__ T s[HY][HX];
   __shared__ StageF st_[FAM == 0 ? 1 : 0 + 1];
   TILE_PROLOGUE
+  // fused solution update of the previous iteration: x += alpha_prev p_prev
+  // (every batch with a pending coefficient, active or just converged)
+  if (xa && in && !first)
+    for (int k = 0; k < BB; ++k) {
+      const int b = blockIdx.z * BB + k;
+      if (b >= nb) break;
+      const T al = xa[b];
+      if (norm2(al) == 0.0) continue;
+      const size_t j = (size_t)b * n + i;
+      xs[j] = xs[j] + mul(al, pin[j]);
+    }
   Ctx<MODE, FAM> cx;
   if constexpr (FAM == 0) cx.st = st_;
   cx.init(op, i, in, tid);
@@ -757,6 +769,23 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
   }
 }
 
+// x += xa p (pending fused solution update after the last iteration)
+template <int MODE>
+__global__ void __launch_bounds__(NT, 4) k_xupdate(Op<MODE> op, TT<MODE>* __restrict__ xs,
+                                                   const TT<MODE>* __restrict__ p, const TT<MODE>* __restrict__ xa,
+                                                   int nb, int BB) {
+  TILE_PROLOGUE
+  if (!in) return;
+  for (int k = 0; k < BB; ++k) {
+    const int b = blockIdx.z * BB + k;
+    if (b >= nb) break;
+    const TT<MODE> al = xa[b];
+    if (norm2(al) == 0.0) continue;
+    const size_t j = (size_t)b * n + i;
+    xs[j] = xs[j] + mul(al, p[j]);
+  }
+}
+
 // partial b^T z
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_dot(Op<MODE> op, const TT<MODE>* __restrict__ a_,
@@ -825,9 +854,11 @@ template <class T>
 __global__ void k_scalars(int stage, const double* __restrict__ part, int per, int nb, double rtol2,
                           T* __restrict__ rho, T* __restrict__ mu, T* __restrict__ alpha,
                           T* __restrict__ beta, double* __restrict__ bn2, double* __restrict__ rn2,
-                          int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask) {
+                          int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask,
+                          T* __restrict__ xa) {
   const int b = blockIdx.x;
   if (b >= nb) return;
+  if (xa && threadIdx.x == 0 && (stage == ST_INIT || (stage == ST_ALPHA && !active[b]))) xa[b] = from2<T>(0.0, 0.0);
   if (stage != ST_INIT && !active[b]) return;
   double s0, s1;
   batch_sum(part, per, b, s0, s1);
@@ -846,6 +877,7 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
       const T m = from2<T>(s0, s1);
       mu[b] = m;
       alpha[b] = cdiv(rho[b], m);
+      if (xa) xa[b] = alpha[b];
       break;
     }
     case ST_RN:
@@ -1049,6 +1081,8 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   }
   const size_t n0 = (size_t)B * levels[0].n;
   r.alloc(n0);
+  if (MODE == 0 && levels[0].fine.we && L > 1) r2.alloc(n0);
+  xa.alloc(B);
   p0.alloc(n0);
   p1.alloc(n0);
   q.alloc(n0);
@@ -1123,9 +1157,35 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   T* zo = lz1[l].get();
   if constexpr (MODE == 0) {
     if (ops[l].fine.we) {
+      fine_down0(nb, bl, nullptr, nullptr);
+      return fine_rest0(nb, bl, dot);
+    }
+  }
+  return vcycle_generic(l, nb, bl, dot);
+}
+
+template <int MODE>
+void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out) {
+  if constexpr (MODE == 0) {
+    FineOp fo = ops[0].fine;
+    fo.lam = lam;
+    launch_fine_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
+                     qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
+  }
+}
+
+template <int MODE>
+typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl, bool dot) {
+  const int l = 0;
+  const int L = (int)ops.size();
+  int* act = active.get();
+  cudaStream_t s = p->stream;
+  T* z2 = lz0[l].get();
+  T* zo = lz1[l].get();
+  if constexpr (MODE == 0) {
+    {
       FineOp fo = ops[l].fine;
       fo.lam = lam;
-      launch_fine_down(*p, fo, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, cfg.omega2, nb);
       T* xcf;
       if (l + 1 == L - 1) {
         k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
@@ -1152,6 +1212,21 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
       return zo;
     }
   }
+  return zo;
+}
+
+template <int MODE>
+typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, const T* bl, bool dot) {
+  const int L = (int)ops.size();
+  const Op<MODE> op = make_op<MODE>(ops[l], lam);
+  static const int coarse_bb = std::getenv("TPGPU_COARSE_BB") ? std::atoi(std::getenv("TPGPU_COARSE_BB")) : 4;
+  const Geo g = geo_for(ops[l].m, nb, p->num_sms, l == 0 ? 8 : coarse_bb);
+  int* act = active.get();
+  cudaStream_t s = p->stream;
+  const dim3 blk(TX, TY);
+  const Op<MODE> opc = make_op<MODE>(ops[l + 1], lam);
+  T* z2 = lz0[l].get();
+  T* zo = lz1[l].get();
   const bool rb = cfg.rb_fine && ops[l].five;
   // down: smoothing from zero, residual, restriction
 #define LAUNCH_DOWN(SMV)                                                                        \
@@ -1188,28 +1263,37 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const Geo g0 = geo_for(ops[0].m, nb, p->num_sms, 8);
   const dim3 blk(TX, TY);
   const bool fine = MODE == 0 && ops[0].fine.we != nullptr;
+  // optional fused Krylov update (fine streaming path): r -= alpha q inside
+  // the fine down pass, x += alpha p inside the next apply.  Off by default:
+  // it removes the update pass (which streams at ~5.4 TB/s) but loads the
+  // latency-bound down pass further -- measured 12.5 vs 12.2 ms per cfg-1 sweep.
+  static const bool want_fuse = std::getenv("TPGPU_FUSED_UPDATE") != nullptr;
+  const bool fused = fine && ops.size() > 1 && want_fuse;
   FineOp fo = ops[0].fine;
   fo.lam = reinterpret_cast<const cplx*>(lam);
   // partials per batch of each producing kernel
   const int per_t = g0.tiles;
-  const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // init, apply
+  const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
+  const int per_d = fine ? fine_partials(ops[0].m, 1) : per_t;   // fused down (||r||^2)
   const int per_u = fine ? fine_partials(ops[0].m, 2) : per_t;   // V-cycle dot (up)
   // the smem-tile apply (FAM 1 reads the stored 5-point stencil) keeps more
   // loads in flight than the streaming one on B200 (measured 102 vs 122 us at cfg 1)
   static const bool use_stream_apply = std::getenv("TPGPU_STREAM_APPLY") != nullptr;
+  const bool sapply = fine && use_stream_apply && !fused;
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
+  T* xa_ptr = fused ? xa.get() : nullptr;
   cudaStream_t s = p->stream;
   const int l = 0;
-  if (fine && warm && use_stream_apply) {
+  if (fine && warm && sapply) {
     if constexpr (MODE == 0) launch_fine_apply(*p, fo, b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
   } else {
     DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
     TP_LAUNCHED(p);
   }
-  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (fine && warm && use_stream_apply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(),
-                                  beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
+  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (fine && warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(),
+                                  mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
   TP_LAUNCHED(p);
   if (warm) {
     k_zero_flagged<MODE><<<g0.grid, blk, 0, s>>>(op0, x, nb, g0.BB, zero);
@@ -1223,32 +1307,37 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int64_t batch_iters = 0;
   int last_active = h_count[0];
   cur_active = last_active;
+  T* rcur = r.get();
+  T* rnext = r2.get();
+  T* pin = p0.get();
+  T* pout = p1.get();
   if (last_active > 0) {
-    T* z = vcycle_level(0, nb, r.get(), nullptr, false, true);
+    T* z = vcycle_level(0, nb, rcur, nullptr, false, true);
     k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
-                                    alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
+                                    alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
     TP_LAUNCHED(p);
-    T* pin = p0.get();
-    T* pout = p1.get();
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
-      if (fine && use_stream_apply) {
+      if (sapply) {
         if constexpr (MODE == 0) launch_fine_apply(*p, fo, z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false);
       } else {
         DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
-                                                                        first, nb, g0.BB, part.get())));
+                                                                        first, nb, g0.BB, part.get(), x, xa_ptr)));
         TP_LAUNCHED(p);
       }
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), (fine && use_stream_apply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
+                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
-      k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, r.get(), pout, q.get(), alpha.get(), act, cfg.omega,
-                                             nullptr, nb, g0.BB,
-                                             part.get());
-      TP_LAUNCHED(p);
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
+      if (fused) {
+        fine_down0(nb, rcur, q.get(), rnext);
+      } else {
+        k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr, nb,
+                                               g0.BB, part.get());
+        TP_LAUNCHED(p);
+      }
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(),
+                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
       const int slot = it & 1;
       k_count_active<<<1, 256, 0, s>>>(act, nb, count.get() + slot);
@@ -1267,15 +1356,26 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         }
       }
       iters = it;
-      z = vcycle_level(0, nb, r.get(), nullptr, false, true);
+      if (fused) {
+        std::swap(rcur, rnext);
+        z = fine_rest0(nb, rcur, true);
+      } else {
+        z = vcycle_level(0, nb, rcur, nullptr, false, true);
+      }
       k_scalars<T><<<nb, 256, 0, s>>>(ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask);
+                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
       std::swap(pin, pout);
     }
     if (!done) {
       TP_CUDA(cudaStreamSynchronize(s));
       last_active = h_count[iters & 1];
+    }
+    if (fused) {
+      // pending x += alpha p of the final iteration (no-op when the loop ended
+      // by convergence: the last apply already consumed every coefficient)
+      k_xupdate<MODE><<<g0.grid, blk, 0, s>>>(op0, x, done ? pout : pin, xa.get(), nb, g0.BB);
+      TP_LAUNCHED(p);
     }
   }
   TP_CUDA(cudaStreamSynchronize(s));

@@ -61,7 +61,8 @@ struct BatchSolver {
   const int* ext_mask = nullptr;  // optional: batches with mask 0 are skipped
   // work
   std::vector<DevBuf<T>> lb, lz0, lz1;  // per level (level 0: b is external)
-  DevBuf<T> r, p0, p1, q;
+  DevBuf<T> r, r2, p0, p1, q;
+  DevBuf<T> xa;  // pending solution-update coefficient per batch (fused update)
   DevBuf<double> part;
   DevBuf<T> rho, mu, alpha, beta;
   DevBuf<double> bn2, rn2;
@@ -81,6 +82,11 @@ struct BatchSolver {
  private:
   void vcycle(int lvl, int nb, T* z_out_level0, bool dot);
   T* vcycle_level(int lvl, int nb, const T* bl, T* z_first, bool first_done, bool dot);
+  T* vcycle_generic(int lvl, int nb, const T* bl, bool dot);
+  // fine streaming level: down pass (optionally fusing r_out = r_in - alpha q)
+  // and the rest of the cycle (coarse levels + up pass)
+  void fine_down0(int nb, const T* r_in, const T* qv, T* r_out);
+  T* fine_rest0(int nb, const T* bl, bool dot);
 };
 
 // Galerkin coarse stencil Ac = P^T Af P for `batches` stencils (stride 7n).
@@ -94,7 +100,8 @@ int fine_partials(int m, int kind);
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init);
 void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                      const int* active, double om1, double om2, int nb);
+                      const int* active, double om1, double om2, int nb, const cplx* q = nullptr,
+                      const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
 void launch_fine_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
                     cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).

@@ -216,10 +216,16 @@ __global__ void __launch_bounds__(WL * WPB, 6) k_fine_apply(FineOp op, const cpl
 }
 
 // ---------------------------------------------------------------- down
-__global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx* __restrict__ rv,
+// With q != nullptr the Krylov residual update is fused in: the right-hand
+// side is r_new = r - alpha q (read r and q, write r_new to rout for the
+// owned block, partial ||r_new||^2 per warp item), replacing the separate
+// x/r update pass (x is updated in the next apply, k_apply_dot).
+__global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx* __restrict__ rv,
                                                            cplx* __restrict__ z2out, cplx* __restrict__ bc,
                                                            int mc, const int* __restrict__ active, double om1,
-                                                           double om2, int nb) {
+                                                           double om2, int nb, const cplx* __restrict__ qv,
+                                                           const cplx* __restrict__ alpha, cplx* __restrict__ rout,
+                                                           double* __restrict__ part) {
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
   const int m = op.m;
   const Item it = item_of(m, OWN, nb, active);
@@ -231,10 +237,23 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
   const int xc = min(max(x, 0), m - 1);
   const size_t o = (size_t)it.b * op.n;
   const RowPtr R{rv + o + xc, m, colok};
+  const RowPtr Q{qv ? qv + o + xc : rv + o + xc, m, colok};
+  cplx* const ro = rout ? rout + o + xc : nullptr;
+  const cplx al = qv ? alpha[it.b] : cplx{0, 0};
   cplx* const zo = z2out + o + xc;
   const cplx l = op.lam[it.b];
   const int ys = it.ys, ye = it.ye;
   const bool cown = own && (x & 1) && (x >> 1) < mc;  // coarse centre column
+  double rn2 = 0;
+  auto rhs = [&](int y) -> cplx {
+    cplx v = R.at(y);
+    if (qv) {
+      const cplx qq = Q.at(y);
+      v.re -= al.re * qq.re - al.im * qq.im;
+      v.im -= al.re * qq.im + al.im * qq.re;
+    }
+    return v;
+  };
   cplx* const bco = bc + (size_t)it.b * mc * mc + (x >> 1);
   // pipeline over input rows yi = ys-2 .. ye+2: z1 at yi, z2 at yi-1,
   // residual at yi-2, restriction centred on yi-3
@@ -243,10 +262,14 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
   cplx b1{0, 0}, b2{0, 0}, b3{0, 0};  // z2 at yi-1, yi-2, yi-3
   cplx q2{0, 0}, q3{0, 0}, q4{0, 0};  // res at yi-2, yi-3, yi-4
   RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
-  cplx rnext = R.at(ys - 2);
+  cplx rnext = rhs(ys - 2);
   for (int yi = ys - 2; yi <= ye + 2; ++yi) {
     const cplx rcur = rnext;
-    rnext = R.at(yi + 1);
+    rnext = rhs(yi + 1);
+    if (qv && own && yi >= ys && yi < ye) {
+      ro[(long)yi * m] = rcur;
+      rn2 += rcur.re * rcur.re + rcur.im * rcur.im;
+    }
     r2 = r1; r1 = r0; r0 = rcur;
     w3 = w2; w2 = w1; w1 = w0;
     w0 = row_w(op, x, yi);
@@ -286,10 +309,20 @@ __global__ void __launch_bounds__(WL * WPB, 5) k_fine_down(FineOp op, const cplx
       }
     }
   }
+  if (qv) {
+    double z = 0;
+    warp_pair(rn2, z);
+    if ((threadIdx.x & 31) == 0) {
+      const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
+      const size_t k = (size_t)it.b * ((size_t)ns * nch) + (size_t)it.chunk * ns + it.strip;
+      part[2 * k] = rn2;
+      part[2 * k + 1] = 0.0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- up
-__global__ void __launch_bounds__(WL * WPB, 5) k_fine_up(FineOp op, const cplx* __restrict__ rv,
+__global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* __restrict__ rv,
                                                          const cplx* __restrict__ z2in, const cplx* __restrict__ xcv,
                                                          int mc, cplx* __restrict__ zout,
                                                          const int* __restrict__ active, double om1, double om2, int nb,
@@ -406,8 +439,10 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
 }
 
 void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                      const int* active, double om1, double om2, int nb) {
-  k_fine_down<<<grid_for(op.m, 26, nb), WL * WPB, 0, p.stream>>>(op, r, z2, bc, mc, active, om1, om2, nb);
+                      const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
+                      cplx* rout, double* part) {
+  k_fine_down<<<grid_for(op.m, 26, nb), WL * WPB, 0, p.stream>>>(op, r, z2, bc, mc, active, om1, om2, nb, q,
+                                                               alpha, rout, part);
   TP_LAUNCHED(&p);
 }
 
