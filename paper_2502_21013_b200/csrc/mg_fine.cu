@@ -263,6 +263,7 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
   cplx q2{0, 0}, q3{0, 0}, q4{0, 0};  // res at yi-2, yi-3, yi-4
   RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
   cplx rnext = rhs(ys - 2);
+  cplx id0{0, 0}, id1{0, 0};  // 1/d of rows yi, yi-1
   for (int yi = ys - 2; yi <= ye + 2; ++yi) {
     const cplx rcur = rnext;
     rnext = rhs(yi + 1);
@@ -275,14 +276,16 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
     w0 = row_w(op, x, yi);
     // z1 = omega r / d at row yi (zero outside the domain: r = 0 there)
     a2 = a1; a1 = a0;
-    a0 = cs(om1, cm(r0, rcp(diag(expand(w0, w1), l))));
+    id1 = id0;
+    id0 = rcp(diag(expand(w0, w1), l));
+    a0 = cs(om1, cm(r0, id0));
     // z2 at row yi-1
     b3 = b2; b2 = b1;
     {
       const cplx aw = shf_up(a1), ae = shf_dn(a1);
       const RowK k1 = expand(w1, w2);
       const cplx Aa = apply_at(k1, l, a1, aw, ae, a2, a0);
-      const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, rcp(diag(k1, l)));
+      const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, id1);
       const int y = yi - 1;
       const bool in = colok && y >= 0 && y < m;
       b1 = in ? cplx{fma(om2, t.re, a1.re), fma(om2, t.im, a1.im)} : cplx{0, 0};
@@ -369,6 +372,7 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* 
   RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
   cplx cnext = zc_at(ys - 2), rnext = R.at(ys - 2);
   double s0 = 0, s1 = 0;
+  cplx jd1{0, 0}, jd2{0, 0};  // 1/d of rows yi-1, yi-2
   for (int yi = ys - 2; yi <= ye + 1; ++yi) {
     const cplx ccur = cnext, rcur = rnext;
     cnext = zc_at(yi + 1);
@@ -383,7 +387,9 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* 
       const cplx cw = shf_up(c1), ce = shf_dn(c1);
       const RowK k1 = expand(w1, w2);
       const cplx Ac = apply_at(k1, l, c1, cw, ce, c2, c0);
-      const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, rcp(diag(k1, l)));
+      jd2 = jd1;
+      jd1 = rcp(diag(k1, l));
+      const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, jd1);
       const int y = yi - 1;
       e1 = (colok && y >= 0 && y < m) ? cplx{fma(om2, t.re, c1.re), fma(om2, t.im, c1.im)} : cplx{0, 0};
     }
@@ -394,7 +400,7 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* 
       const int y = yi - 2;
       if (own && y >= ys && y < ye) {
         const cplx Ae = apply_at(k2, l, e2, ew, ee, e3, e1);
-        const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, rcp(diag(k2, l)));
+        const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, jd2);
         const cplx z4 = {fma(om1, t.re, e2.re), fma(om1, t.im, e2.im)};
         zo[(long)y * m] = z4;
         if (dot) {
