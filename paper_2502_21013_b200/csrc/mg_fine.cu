@@ -262,6 +262,7 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
   cplx b1{0, 0}, b2{0, 0}, b3{0, 0};  // z2 at yi-1, yi-2, yi-3
   cplx q2{0, 0}, q3{0, 0}, q4{0, 0};  // res at yi-2, yi-3, yi-4
   RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
+  RowW wnx = row_w(op, x, ys - 2);                   // row yi+1 in flight
   cplx rnext = rhs(ys - 2);
   cplx id0{0, 0}, id1{0, 0};  // 1/d of rows yi, yi-1
   for (int yi = ys - 2; yi <= ye + 2; ++yi) {
@@ -273,7 +274,8 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
     }
     r2 = r1; r1 = r0; r0 = rcur;
     w3 = w2; w2 = w1; w1 = w0;
-    w0 = row_w(op, x, yi);
+    w0 = wnx;
+    wnx = row_w(op, x, yi + 1);
     // z1 = omega r / d at row yi (zero outside the domain: r = 0 there)
     a2 = a1; a1 = a0;
     id1 = id0;
@@ -370,6 +372,7 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* 
   cplx r0{0, 0}, r1{0, 0}, r2{0, 0};  // r at yi, yi-1, yi-2
   cplx e1{0, 0}, e2{0, 0}, e3{0, 0};  // z3 at yi-1, yi-2, yi-3
   RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
+  RowW wnx = row_w(op, x, ys - 2);                   // row yi+1 in flight
   cplx cnext = zc_at(ys - 2), rnext = R.at(ys - 2);
   double s0 = 0, s1 = 0;
   cplx jd1{0, 0}, jd2{0, 0};  // 1/d of rows yi-1, yi-2
@@ -380,7 +383,8 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* 
     c2 = c1; c1 = c0; c0 = ccur;
     r2 = r1; r1 = r0; r0 = rcur;
     w3 = w2; w2 = w1; w1 = w0;
-    w0 = row_w(op, x, yi);
+    w0 = wnx;
+    wnx = row_w(op, x, yi + 1);
     // z3 at row yi-1
     e3 = e2; e2 = e1;
     {
