@@ -53,9 +53,11 @@ def lib():
     """Load libtpgpu.so (raises if it has not been built -- no fallback)."""
     global _lib
     if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise FileNotFoundError(f"{LIB_PATH} missing: run `python -m paper_2502_21013_b200.build`")
-        L = C.CDLL(LIB_PATH)
+        # TPGPU_LIB: an in-tree experiment build (build.py --variant) instead
+        path = os.path.join(_HERE, os.environ["TPGPU_LIB"]) if os.environ.get("TPGPU_LIB") else LIB_PATH
+        if not os.path.exists(path):
+            raise FileNotFoundError(f"{path} missing: run `python -m paper_2502_21013_b200.build`")
+        L = C.CDLL(path)
         dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
         vp = C.c_void_p
         D, G = C.POINTER(TpProblemDesc), C.POINTER(TpSolverCfg)

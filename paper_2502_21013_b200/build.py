@@ -41,17 +41,24 @@ def _newer(target: str, deps: list[str]) -> bool:
     return any(os.path.getmtime(d) > t for d in deps)
 
 
-def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) -> str:
-    os.makedirs(OBJ, exist_ok=True)
+def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False, defines=None,
+          variant: str = "") -> str:
+    """Compile csrc/*.cu and link libtpgpu.so.  `variant` + `defines` build an
+    experiment copy (libtpgpu_<variant>.so, own object dir) with extra -D
+    flags; api.lib() loads it when TPGPU_LIB names it."""
+    out = OUT if not variant else os.path.join(HERE, f"libtpgpu_{variant}.so")
+    objdir = OBJ if not variant else OBJ + "_" + variant
+    extra = [f"-D{d}" for d in (defines or [])]
+    os.makedirs(objdir, exist_ok=True)
     srcs = sorted(glob.glob(os.path.join(CSRC, "*.cu")))
     hdrs = sorted(glob.glob(os.path.join(CSRC, "*.cuh")) + glob.glob(os.path.join(ROOT, "include", "*.h")))
     objs = []
     jobs = []
     for s in srcs:
-        o = os.path.join(OBJ, os.path.basename(s)[:-3] + ".o")
+        o = os.path.join(objdir, os.path.basename(s)[:-3] + ".o")
         objs.append(o)
         if force or _newer(o, [s] + hdrs):
-            cmd = [nvcc()] + ARCH + FLAGS + (["-Xptxas", "-v"] if ptxas_info else []) + \
+            cmd = [nvcc()] + ARCH + FLAGS + extra + (["-Xptxas", "-v"] if ptxas_info else []) + \
                 ["-I", os.path.join(ROOT, "include"), "-dc", s, "-o", o]
             jobs.append(cmd)
 
@@ -67,13 +74,13 @@ def build(force: bool = False, verbose: bool = False, ptxas_info: bool = False) 
 
     with ThreadPoolExecutor(max_workers=min(8, os.cpu_count() or 1)) as ex:
         list(ex.map(run, jobs))
-    if force or jobs or _newer(OUT, objs):
-        tmp = OUT + ".tmp"
+    if force or jobs or _newer(out, objs):
+        tmp = out + ".tmp"
         cmd = [nvcc()] + ARCH + ["-shared", "-cudart", "static", "-Xcompiler", "-fPIC",
                                  "-o", tmp] + objs + ["-ldl"]
         run(cmd)
-        os.replace(tmp, OUT)
-    return OUT
+        os.replace(tmp, out)
+    return out
 
 
 if __name__ == "__main__":
@@ -81,5 +88,7 @@ if __name__ == "__main__":
     ap.add_argument("--force", action="store_true")
     ap.add_argument("--verbose", action="store_true")
     ap.add_argument("--ptxas", action="store_true")
+    ap.add_argument("--variant", default="")
+    ap.add_argument("-D", dest="defines", action="append", default=[])
     a = ap.parse_args()
-    print(build(a.force, a.verbose, a.ptxas))
+    print(build(a.force, a.verbose, a.ptxas, a.defines, a.variant))

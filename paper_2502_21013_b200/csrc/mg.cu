@@ -1169,7 +1169,7 @@ void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out)
   if constexpr (MODE == 0) {
     FineOp fo = ops[0].fine;
     fo.lam = lam;
-    launch_fine_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
+    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
                      qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
   }
 }
@@ -1200,7 +1200,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
         TP_CUDA(cudaEventCreate(&e1));
         TP_CUDA(cudaEventRecord(e0, s));
       }
-      launch_fine_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
+      launch_stream_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
       if (p->ktimer.on) {
         TP_CUDA(cudaEventRecord(e1, s));
         p->ktimer.pending.emplace_back(e0, e1);
@@ -1228,13 +1228,37 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
   T* z2 = lz0[l].get();
   T* zo = lz1[l].get();
   const bool rb = cfg.rb_fine && ops[l].five;
+  static const bool tile_coarse = std::getenv("TPGPU_TILE_COARSE") != nullptr;
+  static const bool coarse_j1 = std::getenv("TPGPU_COARSE_J1") != nullptr;
+  const bool j1 = coarse_j1 && l > 0;
+  if constexpr (MODE == 0) {
+    // Galerkin levels of the frequency solver: warp-streaming passes
+    if (!ops[l].five && !j1 && !tile_coarse && ops[l].m >= 7) {
+      FineOp so;
+      so.K = ops[l].K;
+      so.M = ops[l].M;
+      so.lam = lam;
+      so.m = ops[l].m;
+      so.n = ops[l].n;
+      launch_stream_down(*p, so, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, cfg.omega2, nb);
+      T* xs;
+      if (l + 1 == L - 1) {
+        k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
+        TP_LAUNCHED(p);
+        xs = lz0[l + 1].get();
+      } else {
+        xs = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
+      }
+      launch_stream_up(*p, so, bl, z2, xs, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0,
+                       part.get());
+      return zo;
+    }
+  }
   // down: smoothing from zero, residual, restriction
 #define LAUNCH_DOWN(SMV)                                                                        \
   DISPATCH_FAM(l, (set_fused_attrs<MODE, FAM, SMV>(),                                          \
                    k_down<MODE, FAM, SMV><<<g.grid, blk, fused_smem<MODE, FAM>(true), s>>>(     \
                        op, opc, bl, z2, lb[l + 1].get(), act, cfg.omega, cfg.omega2, nb, g.BB)))
-  static const bool coarse_j1 = std::getenv("TPGPU_COARSE_J1") != nullptr;
-  const bool j1 = coarse_j1 && l > 0;
   if (rb) { LAUNCH_DOWN(SM_RB); } else if (j1) { LAUNCH_DOWN(SM_J1); } else { LAUNCH_DOWN(SM_JAC); }
   TP_LAUNCHED(p);
   T* xc;

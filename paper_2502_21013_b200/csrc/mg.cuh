@@ -30,12 +30,15 @@ struct MGConfig {
   bool rb_fine = true;      // red-black Gauss-Seidel on the 5-point fine level
 };
 
-// Fine-level operator data for the streaming kernels (mg_fine.cu): K_hat
-// regenerated from cell materials + nu_hat, lumped mass diagonal.
+// Operator data for the streaming kernels (mg_fine.cu).  Fine level: K_hat
+// regenerated from cell materials + nu_hat (edge weights), lumped mass
+// diagonal.  Galerkin levels: the shared 7-point K and M planes (stride n).
 struct FineOp {
   const double* we = nullptr;     // (cells+1)^2 vertex grid: K_hat edge weight (X,Y)-(X+1,Y)
   const double* wn = nullptr;     // (cells+1)^2 vertex grid: K_hat edge weight (X,Y)-(X,Y+1)
   const double* mass = nullptr;   // n
+  const double* K = nullptr;      // Galerkin levels: 7n
+  const double* M = nullptr;      // Galerkin levels: 7n
   const cplx* lam = nullptr;      // per batch symbol
   int m = 0, c = 0, n = 0;
 };
@@ -95,15 +98,16 @@ void launch_rap(Problem& p, const double* Af, int mf, double* Ac, int mc, int ba
 void launch_coarse_inverse_freq(Problem& p, const double* K, const double* M, int m,
                                 const cplx* lam, cplx* inv, int batches);
 void launch_coarse_inverse_slice(Problem& p, const double* J, int m, double* inv, int batches);
-// Fine-level streaming kernels (mg_fine.cu).  kind: 0 apply, 1 down, 2 up.
+// Streaming kernels (mg_fine.cu).  kind: 0 apply, 1 down, 2 up.
 int fine_partials(int m, int kind);
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init);
-void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                      const int* active, double om1, double om2, int nb, const cplx* q = nullptr,
-                      const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
-void launch_fine_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
-                    cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
+// V-cycle down / up passes of one level (fine: op.we set; Galerkin: op.K set)
+void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
+                        const int* active, double om1, double om2, int nb, const cplx* q = nullptr,
+                        const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
+void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
+                      cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).
 void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches);
 

@@ -19,6 +19,8 @@
 //                  b_c = P^T res ; writes z2 and b_c                  (V-cycle down)
 //   k_fine_up      zc = z2 + P x_c ; z3, z4 = two Jacobi steps ;
 //                  writes z4, partial r^T z4                          (V-cycle up)
+#include <cstdlib>
+
 #include "mg.cuh"
 
 namespace tpgpu {
@@ -215,44 +217,252 @@ __global__ void __launch_bounds__(WL * WPB, 6) k_fine_apply(FineOp op, const cpl
   }
 }
 
+// ---------------------------------------------------------------- async row ring
+// The down/up passes walk rows with a long dependent chain per row (two
+// stencil applications, a complex reciprocal, shuffles), so a row load issued
+// one row ahead does not cover HBM latency at the occupancy these register-
+// heavy kernels reach.  Each warp therefore stages its input rows (vectors
+// and coefficient rows) through private shared-memory rings with per-lane
+// cp.async copies issued RA rows ahead: every lane reads back only the slots
+// it wrote itself, so cp.async.wait_group is the only synchronisation (no
+// barriers, no mbarriers).  Out-of-domain entries are zero-filled by the copy
+// (src-size 0).  Vector rows are consumed at once (ring of RA + 2 slots, the
+// overwritten slot was read two rows earlier); coefficient rows stay readable
+// for the three rows below the current one (ring of RA + 4 slots).
+__device__ __forceinline__ void cp16(void* sdst, const void* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void cp8(void* sdst, const void* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_wait() {
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
+}
+
+template <int NV>
+struct VRow {  // NV complex values per lane of one staged row
+  cplx v[NV][WL];
+};
+template <int NW>
+struct WRow {  // NW coefficient doubles per lane of one staged row
+  double w[NW][WL];
+};
+
+// ---- stencil policies.  Src: per-lane cursor staging consecutive
+// coefficient rows (row offsets advance by addition; rows and columns
+// outside the stored grid are zero-filled).  diag / apply: the diagonal and
+// the operator at row y from the staged rows y (sy) and y-1 (sb).
+struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
+  static constexpr int NW = 3;
+  struct Src {
+    const double *we, *wn, *mm;  // lane column bases
+    int woff, moff, wstep, mstep, c, m;
+    bool colw, colm;
+  };
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int y0) {
+    Src s;
+    s.c = op.c;
+    s.m = op.m;
+    s.colw = (unsigned)(x + 1) <= (unsigned)op.c;  // vertex column X = x+1
+    s.colm = x >= 0 && x < op.m;
+    s.we = op.we + (s.colw ? x + 1 : 0);
+    s.wn = op.wn + (s.colw ? x + 1 : 0);
+    s.mm = op.mass + xc;
+    s.wstep = op.c + 1;
+    s.mstep = op.m;
+    s.woff = (y0 + 1) * s.wstep;
+    s.moff = y0 * s.mstep;
+    return s;
+  }
+  // stage row yr (then advance to yr+1)
+  static __device__ __forceinline__ void stage(WRow<NW>& st, Src& s, int lane, int yr) {
+    const bool wv = s.colw && (unsigned)(yr + 1) <= (unsigned)s.c;
+    const bool mv = s.colm && (unsigned)yr < (unsigned)s.m;
+    cp8(&st.w[0][lane], s.we + (wv ? s.woff : 0), wv);
+    cp8(&st.w[1][lane], s.wn + (wv ? s.woff : 0), wv);
+    cp8(&st.w[2][lane], s.mm + (mv ? s.moff : 0), mv);
+    s.woff += s.wstep;
+    s.moff += s.mstep;
+  }
+  // a row's coefficients in registers: own east/north weights, mass, and the
+  // west weight (the west lane's east weight), shuffled once per row
+  static constexpr int RETAIN = 0;  // staged rows are read once, in their own iteration
+  struct Reg {
+    double we, ww, wn, mm;
+  };
+  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane) {
+    Reg k;
+    k.we = st.w[0][lane];
+    k.wn = st.w[1][lane];
+    k.mm = st.w[2][lane];
+    k.ww = __shfl_up_sync(0xffffffffu, k.we, 1);
+    return k;
+  }
+  static __device__ __forceinline__ cplx diag(const Reg& y, const Reg& b, cplx l) {
+    const double kc = (y.we + y.ww) + (y.wn + b.wn);
+    return {fma(l.re, y.mm, kc), l.im * y.mm};
+  }
+  // d v - wE vE - wW vW - wN vN - wS vS (neighbours of Dirichlet vertices are
+  // zero vectors, their edge weights stay on the diagonal)
+  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx l, cplx vs, cplx v, cplx vn) {
+    const cplx vw = shf_up(v), ve = shf_dn(v);
+    cplx acc = cm(diag(y, b, l), v);
+    acc.re -= y.we * ve.re + y.ww * vw.re + y.wn * vn.re + b.wn * vs.re;
+    acc.im -= y.we * ve.im + y.ww * vw.im + y.wn * vn.im + b.wn * vs.im;
+    return acc;
+  }
+};
+
+struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, NE planes)
+  static constexpr int NW = 8;  // K C E N NE, M C E N NE
+  struct Src {
+    const double *K, *M;  // lane column bases
+    size_t n;
+    int off, m;
+    bool col;
+  };
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int y0) {
+    Src s;
+    s.K = op.K + xc;
+    s.M = op.M + xc;
+    s.n = op.n;
+    s.m = op.m;
+    s.off = y0 * op.m;
+    s.col = x >= 0 && x < op.m;
+    return s;
+  }
+  static __device__ __forceinline__ void stage(WRow<NW>& st, Src& s, int lane, int yr) {
+    const bool v = s.col && (unsigned)yr < (unsigned)s.m;
+    const size_t o = v ? s.off : 0;
+    const int dirs[4] = {SC, SE_, SN_, SNE};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      cp8(&st.w[q][lane], s.K + dirs[q] * s.n + o, v);
+      cp8(&st.w[4 + q][lane], s.M + dirs[q] * s.n + o, v);
+    }
+    s.off += s.m;
+  }
+  // rows stay in the ring (8 planes are too many for register windows) and
+  // are read on use: the ring retains the three rows below the current one
+  static constexpr int RETAIN = 3;
+  struct Reg {
+    const WRow<NW>* p;
+    int lane;
+  };
+  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane) { return {&st, lane}; }
+  static __device__ __forceinline__ cplx coef(const Reg& r, int q, cplx l) {
+    const double mm = r.p->w[4 + q][r.lane];
+    return {fma(l.re, mm, r.p->w[q][r.lane]), l.im * mm};
+  }
+  static __device__ __forceinline__ cplx diag(const Reg& y, const Reg&, cplx l) { return coef(y, 0, l); }
+  // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1): products formed by the owner
+  // lane and shuffled one lane up
+  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx l, cplx vs, cplx v, cplx vn) {
+    const cplx cE = coef(y, 1, l), cNEs = coef(b, 3, l);
+    const cplx tw = shf_up(cm(cE, v)), tsw = shf_up(cm(cNEs, vs));
+    const cplx ve = shf_dn(v), vne = shf_dn(vn);
+    cplx acc = cm(coef(y, 0, l), v);
+    acc = acc + cm(cE, ve);
+    acc = acc + tw;
+    acc = acc + cm(coef(y, 2, l), vn);
+    acc = acc + cm(coef(b, 2, l), vs);
+    acc = acc + cm(coef(y, 3, l), vne);
+    acc = acc + tsw;
+    return acc;
+  }
+};
+
+template <class S, int NV, int RA, int WPBK>
+constexpr size_t ring_smem() {
+  return (size_t)WPBK * ((RA + 2) * sizeof(VRow<NV>) + (RA + 2 + S::RETAIN) * sizeof(WRow<S::NW>));
+}
+
+__device__ __forceinline__ int wrap_inc(int s, int n) { return s + 1 == n ? 0 : s + 1; }
+
+// warp work item with a runtime chunk height: ((b * nch) + chunk) * ns + strip
+template <int WPBK>
+__device__ __forceinline__ Item item_rh(int m, int own, int rh, int nb, const int* __restrict__ active) {
+  Item it;
+  const int w = blockIdx.x * WPBK + (threadIdx.x >> 5);
+  const int ns = (m + own - 1) / own, nch = (m + rh - 1) / rh;
+  it.strip = w % ns;
+  it.chunk = (w / ns) % nch;
+  it.b = w / (ns * nch);
+  it.ok = it.b < nb && (!active || active[it.b]);
+  it.ys = it.chunk * rh;
+  it.ye = min(it.ys + rh, m);
+  it.xs = it.strip * own;
+  return it;
+}
+
+#ifndef TPGPU_STREAM_UNROLL
+#define TPGPU_STREAM_UNROLL 3
+#endif
+// resident warps per SM the register allocation is bounded for (0: free)
+#ifndef TPGPU_STREAM_MINW
+#define TPGPU_STREAM_MINW 0
+#endif
+#define TP_MINB(W) (TPGPU_STREAM_MINW > 0 ? TPGPU_STREAM_MINW / (W) : 1)
+#define TP_PRAGMA(x) _Pragma(#x)
+#define TP_UNROLL(n) TP_PRAGMA(unroll n)
+
 // ---------------------------------------------------------------- down
-// With q != nullptr the Krylov residual update is fused in: the right-hand
-// side is r_new = r - alpha q (read r and q, write r_new to rout for the
-// owned block, partial ||r_new||^2 per warp item), replacing the separate
-// x/r update pass (x is updated in the next apply, k_apply_dot).
-__global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx* __restrict__ rv,
+//   z1 = w1 r/d ; z2 = z1 + w2 (r - A z1)/d ; res = r - A z2 ; b_c = P^T res
+// FUSED: the right-hand side is r_new = r - alpha q (read r and q, write
+// r_new to rout for the owned block, partial ||r_new||^2 per warp item),
+// replacing the separate x/r update pass (x is updated in the next apply).
+template <class S, bool FUSED, int RA, int WPBK>
+__global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp op, const cplx* __restrict__ rv,
                                                            cplx* __restrict__ z2out, cplx* __restrict__ bc,
-                                                           int mc, const int* __restrict__ active, double om1,
-                                                           double om2, int nb, const cplx* __restrict__ qv,
+                                                           int mc, int rh, const int* __restrict__ active,
+                                                           double om1, double om2, int nb,
+                                                           const cplx* __restrict__ qv,
                                                            const cplx* __restrict__ alpha, cplx* __restrict__ rout,
                                                            double* __restrict__ part) {
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
+  constexpr int NV = FUSED ? 2 : 1, RV = RA + 2, RC = RA + 2 + S::RETAIN;
+  extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
-  const Item it = item_of(m, OWN, nb, active);
+  const Item it = item_rh<WPBK>(m, OWN, rh, nb, active);
   if (!it.ok) return;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  VRow<NV>* const vring = reinterpret_cast<VRow<NV>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring =
+      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NV>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < H + OWN && colok;
   const int xc = min(max(x, 0), m - 1);
   const size_t o = (size_t)it.b * op.n;
-  const RowPtr R{rv + o + xc, m, colok};
-  const RowPtr Q{qv ? qv + o + xc : rv + o + xc, m, colok};
-  cplx* const ro = rout ? rout + o + xc : nullptr;
-  const cplx al = qv ? alpha[it.b] : cplx{0, 0};
+  const cplx* const rp = rv + o + xc;
+  const cplx* const qp = FUSED ? qv + o + xc : nullptr;
+  cplx* const ro = FUSED ? rout + o + xc : nullptr;
+  const cplx al = FUSED ? alpha[it.b] : cplx{0, 0};
   cplx* const zo = z2out + o + xc;
   const cplx l = op.lam[it.b];
   const int ys = it.ys, ye = it.ye;
+  const int y0 = ys - 3, ylast = ye + 2;  // staged rows
   const bool cown = own && (x & 1) && (x >> 1) < mc;  // coarse centre column
   double rn2 = 0;
-  auto rhs = [&](int y) -> cplx {
-    cplx v = R.at(y);
-    if (qv) {
-      const cplx qq = Q.at(y);
-      v.re -= al.re * qq.re - al.im * qq.im;
-      v.im -= al.re * qq.im + al.im * qq.re;
+  typename S::Src src = S::src(op, x, xc, y0);
+  int voff = y0 * m;       // row offset of the next vector row to stage
+  int vi = 0, wi = 0;      // next ring slots to fill
+  auto issue = [&](int yr) {
+    if (yr <= ylast) {
+      const bool rin = colok && (unsigned)yr < (unsigned)m;
+      const int off = rin ? voff : 0;
+      cp16(&vring[vi].v[0][lane], rp + off, rin);
+      if (FUSED) cp16(&vring[vi].v[1][lane], qp + off, rin);
+      S::stage(wring[wi], src, lane, yr);
+      voff += m;
+      vi = wrap_inc(vi, RV);
+      wi = wrap_inc(wi, RC);
     }
-    return v;
+    cp_commit();
   };
   cplx* const bco = bc + (size_t)it.b * mc * mc + (x >> 1);
   // pipeline over input rows yi = ys-2 .. ye+2: z1 at yi, z2 at yi-1,
@@ -261,52 +471,61 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
   cplx a0{0, 0}, a1{0, 0}, a2{0, 0};  // z1 at yi, yi-1, yi-2
   cplx b1{0, 0}, b2{0, 0}, b3{0, 0};  // z2 at yi-1, yi-2, yi-3
   cplx q2{0, 0}, q3{0, 0}, q4{0, 0};  // res at yi-2, yi-3, yi-4
-  RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
-  RowW wnx = row_w(op, x, ys - 2);                   // row yi+1 in flight
-  cplx rnext = rhs(ys - 2);
+#pragma unroll
+  for (int j = 0; j <= RA; ++j) issue(y0 + j);
+  // coefficient rows yi .. yi-3 (rows before y0 only feed halo values that
+  // are never used: they repeat row y0)
+  int vr = 0, sr = 0;  // ring slots of row yi
+  cp_wait<RA>();
+  typename S::Reg k0 = S::load(wring[0], lane), k1 = k0, k2 = k0, k3 = k0;
   cplx id0{0, 0}, id1{0, 0};  // 1/d of rows yi, yi-1
-  for (int yi = ys - 2; yi <= ye + 2; ++yi) {
-    const cplx rcur = rnext;
-    rnext = rhs(yi + 1);
-    if (qv && own && yi >= ys && yi < ye) {
-      ro[(long)yi * m] = rcur;
-      rn2 += rcur.re * rcur.re + rcur.im * rcur.im;
+  TP_UNROLL(TPGPU_STREAM_UNROLL)
+  for (int yi = ys - 2; yi <= ylast; ++yi) {
+    issue(yi + RA);
+    vr = wrap_inc(vr, RV);
+    sr = wrap_inc(sr, RC);
+    cp_wait<RA>();
+    cplx rcur = vring[vr].v[0][lane];
+    if (FUSED) {
+      const cplx qq = vring[vr].v[1][lane];
+      rcur.re -= al.re * qq.re - al.im * qq.im;
+      rcur.im -= al.re * qq.im + al.im * qq.re;
+      if (own && yi >= ys && yi < ye) {
+        ro[(long)yi * m] = rcur;
+        rn2 += rcur.re * rcur.re + rcur.im * rcur.im;
+      }
     }
     r2 = r1; r1 = r0; r0 = rcur;
-    w3 = w2; w2 = w1; w1 = w0;
-    w0 = wnx;
-    wnx = row_w(op, x, yi + 1);
-    // z1 = omega r / d at row yi (zero outside the domain: r = 0 there)
+    k3 = k2; k2 = k1; k1 = k0;
+    k0 = S::load(wring[sr], lane);
+    // z1 = omega r / d at row yi (off-domain diagonals may vanish: z1 = 0 there)
     a2 = a1; a1 = a0;
     id1 = id0;
-    id0 = rcp(diag(expand(w0, w1), l));
-    a0 = cs(om1, cm(r0, id0));
+    id0 = rcp(S::diag(k0, k1, l));
+    a0 = (colok && (unsigned)yi < (unsigned)m) ? cs(om1, cm(r0, id0)) : cplx{0, 0};
     // z2 at row yi-1
     b3 = b2; b2 = b1;
     {
-      const cplx aw = shf_up(a1), ae = shf_dn(a1);
-      const RowK k1 = expand(w1, w2);
-      const cplx Aa = apply_at(k1, l, a1, aw, ae, a2, a0);
+      const cplx Aa = S::apply(k1, k2, l, a2, a1, a0);
       const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, id1);
       const int y = yi - 1;
-      const bool in = colok && y >= 0 && y < m;
+      const bool in = colok && (unsigned)y < (unsigned)m;
       b1 = in ? cplx{fma(om2, t.re, a1.re), fma(om2, t.im, a1.im)} : cplx{0, 0};
       if (own && y >= ys && y < ye) zo[(long)y * m] = b1;
     }
     // residual at row yi-2
     q4 = q3; q3 = q2;
     {
-      const cplx bw = shf_up(b2), be = shf_dn(b2);
-      const cplx Ab = apply_at(expand(w2, w3), l, b2, bw, be, b3, b1);
+      const cplx Ab = S::apply(k2, k3, l, b3, b2, b1);
       const int y = yi - 2;
-      q2 = (colok && y >= 0 && y < m) ? cplx{r2.re - Ab.re, r2.im - Ab.im} : cplx{0, 0};
+      q2 = (colok && (unsigned)y < (unsigned)m) ? cplx{r2.re - Ab.re, r2.im - Ab.im} : cplx{0, 0};
     }
-    // restriction centred on row yc = yi-3 (odd fine row 2Y+1 of the chunk)
-    {
-      const int yc = yi - 3;
+    // restriction centred on row yc = yi-3 (odd fine rows 2Y+1; warp-uniform branch)
+    const int yc = yi - 3;
+    if ((yc & 1) && yc >= ys && yc < ye) {
       const cplx qw = shf_up(q3), qe = shf_dn(q3);
       const cplx q4w = shf_up(q4), q2e = shf_dn(q2);
-      if (cown && (yc & 1) && yc >= ys && yc < ye && (yc >> 1) < mc) {
+      if (cown && (yc >> 1) < mc) {
         cplx acc = q3;
         acc.re += 0.5 * (qw.re + qe.re + q4.re + q2.re + q4w.re + q2e.re);
         acc.im += 0.5 * (qw.im + qe.im + q4.im + q2.im + q4w.im + q2e.im);
@@ -314,11 +533,12 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
       }
     }
   }
-  if (qv) {
+  cp_wait<0>();
+  if (FUSED) {
     double z = 0;
     warp_pair(rn2, z);
-    if ((threadIdx.x & 31) == 0) {
-      const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
+    if (lane == 0) {
+      const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
       const size_t k = (size_t)it.b * ((size_t)ns * nch) + (size_t)it.chunk * ns + it.strip;
       part[2 * k] = rn2;
       part[2 * k + 1] = 0.0;
@@ -327,116 +547,186 @@ __global__ void __launch_bounds__(WL * WPB, 4) k_fine_down(FineOp op, const cplx
 }
 
 // ---------------------------------------------------------------- up
-__global__ void __launch_bounds__(WL * WPB, 4) k_fine_up(FineOp op, const cplx* __restrict__ rv,
+//   zc = z2 + P x_c ; z3, z4 = two Jacobi steps ; writes z4 (+ partial r^T z4)
+// Staged per row: r, z2 and the (up to two) coarse values P x_c interpolates
+// from at the lane's node, plus the coefficient row.
+template <class S, int RA, int WPBK>
+__global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp op, const cplx* __restrict__ rv,
                                                          const cplx* __restrict__ z2in, const cplx* __restrict__ xcv,
-                                                         int mc, cplx* __restrict__ zout,
-                                                         const int* __restrict__ active, double om1, double om2, int nb,
-                                                         int dot, double* __restrict__ part) {
+                                                         int mc, int rh, cplx* __restrict__ zout,
+                                                         const int* __restrict__ active, double om1, double om2,
+                                                         int nb, int dot, double* __restrict__ part) {
   constexpr int H = 2, OWN = WL - 2 * H;  // 28
+  constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN;
+  extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
-  const Item it = item_of(m, OWN, nb, active);
+  const Item it = item_rh<WPBK>(m, OWN, rh, nb, active);
   if (!it.ok) return;
-  const int lane = threadIdx.x & 31;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  VRow<4>* const vring = reinterpret_cast<VRow<4>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<4>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
   const int xc = min(max(x, 0), m - 1);
   const size_t o = (size_t)it.b * op.n;
-  const RowPtr R{rv + o + xc, m, colok}, Z2{z2in + o + xc, m, colok};
+  const cplx* const rp = rv + o + xc;
+  const cplx* const zp = z2in + o + xc;
   cplx* const zo = zout + o + xc;
   const cplx* xb = xcv + (size_t)it.b * mc * mc;
   const cplx l = op.lam[it.b];
   const int ys = it.ys, ye = it.ye;
-  // P1 prolongation: fine vertex a = x+1 (column parity fixed per lane)
+  const int y0 = ys - 3, ylast = ye + 1;
+  // P1 prolongation: fine vertex a = x+1 (column parity fixed per lane);
+  // coarse columns A1 = ah and A2 (= ah+1 on odd vertex columns)
   const int a = x + 1, ah = a >> 1;
   const bool ao = a & 1;
-  auto coarse = [&](int A, int B) -> cplx {
-    return (A >= 1 && A <= mc && B >= 1 && B <= mc) ? xb[(size_t)(B - 1) * mc + (A - 1)] : cplx{0, 0};
-  };
-  auto zc_at = [&](int y) -> cplx {
-    cplx v = Z2.at(y);
-    if (!colok || y < 0 || y >= m) return v;
-    const int bb = y + 1, bh = bb >> 1;
-    cplx c1, c2{0, 0};
-    double w1 = 0.5;
-    if (!ao && !(bb & 1)) { c1 = coarse(ah, bh); w1 = 1.0; }
-    else if (ao && !(bb & 1)) { c1 = coarse(ah, bh); c2 = coarse(ah + 1, bh); }
-    else if (!ao) { c1 = coarse(ah, bh); c2 = coarse(ah, bh + 1); }
-    else { c1 = coarse(ah, bh); c2 = coarse(ah + 1, bh + 1); }
-    v.re = fma(w1, c1.re, fma(0.5, c2.re, v.re));
-    v.im = fma(w1, c1.im, fma(0.5, c2.im, v.im));
-    return v;
+  const int A2 = ao ? ah + 1 : ah;
+  const bool cA1 = colok && ah >= 1 && ah <= mc, cA2 = colok && A2 >= 1 && A2 <= mc;
+  typename S::Src src = S::src(op, x, xc, y0);
+  int voff = y0 * m;
+  int vi = 0, wi = 0;
+  auto issue = [&](int yr) {
+    if (yr <= ylast) {
+      const bool rin = colok && (unsigned)yr < (unsigned)m;
+      const int off = rin ? voff : 0;
+      VRow<4>& sv = vring[vi];
+      cp16(&sv.v[0][lane], rp + off, rin);
+      cp16(&sv.v[1][lane], zp + off, rin);
+      // coarse vertices of the node's P1 interpolation: (A1, B1) and (A2, B2);
+      // the second is absent at coincident vertices
+      const int bb = yr + 1, bh = bb >> 1;
+      const int B2 = (bb & 1) ? bh + 1 : bh;
+      const bool has2 = ao || (bb & 1);
+      const bool ok1 = rin && cA1 && bh >= 1 && bh <= mc;
+      const bool ok2 = rin && has2 && cA2 && B2 >= 1 && B2 <= mc;
+      cp16(&sv.v[2][lane], xb + (ok1 ? (bh - 1) * mc + (ah - 1) : 0), ok1);
+      cp16(&sv.v[3][lane], xb + (ok2 ? (B2 - 1) * mc + (A2 - 1) : 0), ok2);
+      S::stage(wring[wi], src, lane, yr);
+      voff += m;
+      vi = wrap_inc(vi, RV);
+      wi = wrap_inc(wi, RC);
+    }
+    cp_commit();
   };
   // pipeline over input rows yi = ys-2 .. ye+1: zc at yi, z3 at yi-1, z4 at yi-2
   cplx c0{0, 0}, c1{0, 0}, c2{0, 0};  // zc at yi, yi-1, yi-2
   cplx r0{0, 0}, r1{0, 0}, r2{0, 0};  // r at yi, yi-1, yi-2
   cplx e1{0, 0}, e2{0, 0}, e3{0, 0};  // z3 at yi-1, yi-2, yi-3
-  RowW w0 = row_w(op, x, ys - 3), w1{}, w2{}, w3{};  // rows yi, yi-1, yi-2, yi-3
-  RowW wnx = row_w(op, x, ys - 2);                   // row yi+1 in flight
-  cplx cnext = zc_at(ys - 2), rnext = R.at(ys - 2);
-  double s0 = 0, s1 = 0;
+#pragma unroll
+  for (int j = 0; j <= RA; ++j) issue(y0 + j);
+  int vr = 0, sr = 0;
+  cp_wait<RA>();
+  typename S::Reg k0 = S::load(wring[0], lane), k1 = k0, k2 = k0, k3 = k0;  // rows yi .. yi-3
+  double p0 = 0, p1 = 0;
   cplx jd1{0, 0}, jd2{0, 0};  // 1/d of rows yi-1, yi-2
-  for (int yi = ys - 2; yi <= ye + 1; ++yi) {
-    const cplx ccur = cnext, rcur = rnext;
-    cnext = zc_at(yi + 1);
-    rnext = R.at(yi + 1);
+  TP_UNROLL(TPGPU_STREAM_UNROLL)
+  for (int yi = ys - 2; yi <= ylast; ++yi) {
+    issue(yi + RA);
+    vr = wrap_inc(vr, RV);
+    sr = wrap_inc(sr, RC);
+    cp_wait<RA>();
+    const VRow<4>& sv = vring[vr];
+    const double wc1 = (!ao && !((yi + 1) & 1)) ? 1.0 : 0.5;
+    const cplx zz = sv.v[1][lane], x1 = sv.v[2][lane], x2 = sv.v[3][lane];
+    const cplx ccur = {fma(wc1, x1.re, fma(0.5, x2.re, zz.re)), fma(wc1, x1.im, fma(0.5, x2.im, zz.im))};
     c2 = c1; c1 = c0; c0 = ccur;
-    r2 = r1; r1 = r0; r0 = rcur;
-    w3 = w2; w2 = w1; w1 = w0;
-    w0 = wnx;
-    wnx = row_w(op, x, yi + 1);
+    r2 = r1; r1 = r0; r0 = sv.v[0][lane];
+    k3 = k2; k2 = k1; k1 = k0;
+    k0 = S::load(wring[sr], lane);
     // z3 at row yi-1
     e3 = e2; e2 = e1;
     {
-      const cplx cw = shf_up(c1), ce = shf_dn(c1);
-      const RowK k1 = expand(w1, w2);
-      const cplx Ac = apply_at(k1, l, c1, cw, ce, c2, c0);
+      const cplx Ac = S::apply(k1, k2, l, c2, c1, c0);
       jd2 = jd1;
-      jd1 = rcp(diag(k1, l));
+      jd1 = rcp(S::diag(k1, k2, l));
       const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, jd1);
       const int y = yi - 1;
-      e1 = (colok && y >= 0 && y < m) ? cplx{fma(om2, t.re, c1.re), fma(om2, t.im, c1.im)} : cplx{0, 0};
+      e1 = (colok && (unsigned)y < (unsigned)m) ? cplx{fma(om2, t.re, c1.re), fma(om2, t.im, c1.im)}
+                                                 : cplx{0, 0};
     }
     // z4 at row yi-2
     {
-      const cplx ew = shf_up(e2), ee = shf_dn(e2);
-      const RowK k2 = expand(w2, w3);
+      const cplx Ae = S::apply(k2, k3, l, e3, e2, e1);
       const int y = yi - 2;
       if (own && y >= ys && y < ye) {
-        const cplx Ae = apply_at(k2, l, e2, ew, ee, e3, e1);
         const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, jd2);
         const cplx z4 = {fma(om1, t.re, e2.re), fma(om1, t.im, e2.im)};
         zo[(long)y * m] = z4;
         if (dot) {
           const cplx pr = cm(r2, z4);
-          s0 += pr.re;
-          s1 += pr.im;
+          p0 += pr.re;
+          p1 += pr.im;
         }
       }
     }
   }
+  cp_wait<0>();
   if (dot) {
-    warp_pair(s0, s1);
+    warp_pair(p0, p1);
     if (lane == 0) {
-      const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
+      const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
       const size_t per = (size_t)ns * nch;
       const size_t k = (size_t)it.b * per + (size_t)it.chunk * ns + it.strip;
-      part[2 * k] = s0;
-      part[2 * k + 1] = s1;
+      part[2 * k] = p0;
+      part[2 * k + 1] = p1;
     }
   }
 }
 
-int items_per_batch(int m, int own) { return ((m + own - 1) / own) * ((m + RH - 1) / RH); }
+int items_per_batch(int m, int own, int rh = RH) { return ((m + own - 1) / own) * ((m + rh - 1) / rh); }
 
-dim3 grid_for(int m, int own, int nb) {
-  const long warps = (long)items_per_batch(m, own) * nb;
-  return dim3((unsigned)((warps + WPB - 1) / WPB));
+dim3 grid_for(int m, int own, int nb, int rh = RH, int wpb = WPB) {
+  const long warps = (long)items_per_batch(m, own, rh) * nb;
+  return dim3((unsigned)((warps + wpb - 1) / wpb));
+}
+
+// rows per warp item of the down/up passes: long chunks amortise the 5-6
+// halo rows, short ones give the small grids enough warps
+int rh_for(int m) {
+  static const int env = std::getenv("TPGPU_RH") ? std::atoi(std::getenv("TPGPU_RH")) : 0;
+  if (env > 0 && m >= 200) return env;
+  return m >= 200 ? 64 : m >= 100 ? 32 : m >= 50 ? 16 : 8;
+}
+
+int env_int(const char* name, int dflt) {
+  const char* v = std::getenv(name);
+  return v ? std::atoi(v) : dflt;
+}
+
+template <class S, bool FUSED, int RA, int WPBK>
+void down_t(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc, const int* active, double om1,
+            double om2, int nb, const cplx* q, const cplx* alpha, cplx* rout, double* part) {
+  constexpr size_t sm = ring_smem<S, FUSED ? 2 : 1, RA, WPBK>();
+  static bool attrs = [] {
+    cudaFuncSetAttribute(k_stream_down<S, FUSED, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return true;
+  }();
+  (void)attrs;
+  const int rh = rh_for(op.m);
+  k_stream_down<S, FUSED, RA, WPBK><<<grid_for(op.m, 26, nb, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+      op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
+}
+
+template <class S, int RA, int WPBK>
+void up_t(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc, cplx* z,
+          const int* active, double om1, double om2, int nb, int dot, double* part) {
+  constexpr size_t sm = ring_smem<S, 4, RA, WPBK>();
+  static bool attrs = [] {
+    cudaFuncSetAttribute(k_stream_up<S, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return true;
+  }();
+  (void)attrs;
+  const int rh = rh_for(op.m);
+  k_stream_up<S, RA, WPBK><<<grid_for(op.m, 28, nb, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+      op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
 
 }  // namespace
 
-int fine_partials(int m, int kind) { return items_per_batch(m, kind == 0 ? 30 : kind == 1 ? 26 : 28); }
+int fine_partials(int m, int kind) {
+  return kind == 0 ? items_per_batch(m, 30) : items_per_batch(m, kind == 1 ? 26 : 28, rh_for(m));
+}
 
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init) {
@@ -448,18 +738,50 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
   TP_LAUNCHED(&p);
 }
 
-void launch_fine_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                      const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
-                      cplx* rout, double* part) {
-  k_fine_down<<<grid_for(op.m, 26, nb), WL * WPB, 0, p.stream>>>(op, r, z2, bc, mc, active, om1, om2, nb, q,
-                                                               alpha, rout, part);
+// Down pass of one level: Five on the fine level (op.we set), Seven on the
+// Galerkin levels (op.K / op.M set).  Ring depth RA (rows in flight ahead) and
+// warps per block are tuned per stencil; TPGPU_RA5 / TPGPU_RA7 override RA.
+void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
+                        const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
+                        cplx* rout, double* part) {
+  if (op.we) {
+    static const int ra = env_int("TPGPU_RA5", 6);
+    if (q) {
+      down_t<Five, true, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+    } else if (ra == 4) {
+      down_t<Five, false, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+    } else if (ra == 8) {
+      down_t<Five, false, 8, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+    } else {
+      down_t<Five, false, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+    }
+  } else {
+    static const int ra = env_int("TPGPU_RA7", 4);
+    if (ra == 2)
+      down_t<Seven, false, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb, nullptr, nullptr, nullptr, nullptr);
+    else if (ra == 6)
+      down_t<Seven, false, 6, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb, nullptr, nullptr, nullptr, nullptr);
+    else
+      down_t<Seven, false, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb, nullptr, nullptr, nullptr, nullptr);
+  }
   TP_LAUNCHED(&p);
 }
 
-void launch_fine_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
-                    cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
-  k_fine_up<<<grid_for(op.m, 28, nb), WL * WPB, 0, p.stream>>>(op, r, z2, xc, mc, z, active, om1, om2, nb, dot,
-                                                              part);
+void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
+                      cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
+  if (op.we) {
+    static const int ra = env_int("TPGPU_RA5U", 2);
+    if (ra == 4)
+      up_t<Five, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else
+      up_t<Five, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+  } else {
+    static const int ra = env_int("TPGPU_RA7U", 2);
+    if (ra == 4)
+      up_t<Seven, 4, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else
+      up_t<Seven, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+  }
   TP_LAUNCHED(&p);
 }
 

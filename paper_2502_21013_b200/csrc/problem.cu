@@ -359,7 +359,13 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
     d_wn.alloc(wn.size());
     TP_CUDA(cudaMemcpy(d_we.get(), we.data(), we.size() * sizeof(double), cudaMemcpyHostToDevice));
     TP_CUDA(cudaMemcpy(d_wn.get(), wn.data(), wn.size() * sizeof(double), cudaMemcpyHostToDevice));
-    ops[0].fine = {d_we.get(), d_wn.get(), d_mass.get(), nullptr, m, c, n};
+    FineOp& fo = ops[0].fine;
+    fo.we = d_we.get();
+    fo.wn = d_wn.get();
+    fo.mass = d_mass.get();
+    fo.m = m;
+    fo.c = c;
+    fo.n = n;
   }
   MGConfig mc;
   mc.rtol = cfg.inner_rtol;
