@@ -1079,6 +1079,20 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
     lz0[l].alloc(sz);
     if (l < L - 1 || L == 1) lz1[l].alloc(sz);
   }
+  // frequency mode: the first level from which the rest of the cycle fits
+  // one block's shared memory runs as the fused small-level kernel
+  small_from = -1;
+  if (MODE == 0 && !std::getenv("TPGPU_NO_SMALL")) {
+    for (int l = 1; l + 1 < L; ++l) {
+      if (L - l > kMaxSmall || levels[l].five) continue;
+      int ms[kMaxSmall];
+      for (int j = l; j < L; ++j) ms[j - l] = levels[j].m;
+      if (small_cycle_smem(ms, L - l) <= (size_t)200 * 1024) {
+        small_from = l;
+        break;
+      }
+    }
+  }
   const size_t n0 = (size_t)B * levels[0].n;
   r.alloc(n0);
   if (MODE == 0 && levels[0].fine.we && L > 1) r2.alloc(n0);
@@ -1156,6 +1170,17 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   T* z2 = lz0[l].get();
   T* zo = lz1[l].get();
   if constexpr (MODE == 0) {
+    if (l == small_from) {
+      SmallLevels sl;
+      sl.levels = L - l;
+      for (int j = l; j < L; ++j) {
+        sl.m[j - l] = ops[j].m;
+        sl.K[j - l] = ops[j].K;
+        sl.M[j - l] = ops[j].M;
+      }
+      launch_small_cycle(*p, sl, lam, coarse_inv, bl, zo, act, cfg.omega, cfg.omega2, nb);
+      return zo;
+    }
     if (ops[l].fine.we) {
       fine_down0(nb, bl, nullptr, nullptr);
       return fine_rest0(nb, bl, dot);

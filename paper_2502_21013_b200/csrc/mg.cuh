@@ -43,6 +43,20 @@ struct FineOp {
   int m = 0, c = 0, n = 0;
 };
 
+// The bottom levels of the frequency-mode V-cycle, run as one kernel
+// (mg_small.cu): level 0 of this list is the first level whose work vectors
+// fit in shared memory, the last is the coarsest (dense solve).
+constexpr int kMaxSmall = 6;
+struct SmallLevels {
+  int levels = 0;
+  int m[kMaxSmall] = {};
+  const double* K[kMaxSmall] = {};
+  const double* M[kMaxSmall] = {};
+};
+size_t small_cycle_smem(const int* m, int levels);
+void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, const cplx* inv, const cplx* b,
+                        cplx* z, const int* active, double om1, double om2, int nb);
+
 // Stencils of one level for the whole batch (slice mode) or shared (freq mode).
 struct LevelOp {
   int m = 0, n = 0;
@@ -73,6 +87,8 @@ struct BatchSolver {
   DevBuf<int> count;
   int* h_count = nullptr;  // pinned [2]
   int cur_active = 0;      // active batches as last seen by the host (kernel-timer byte accounting)
+  int small_from = -1;     // frequency mode: first level handled by the fused small-level cycle
+  SmallLevels small;
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   void init(Problem* prob, const std::vector<LevelOp>& levels, int batches, const MGConfig& c);
