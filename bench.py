@@ -243,35 +243,37 @@ def run_b200(args):
                 "inner_iterations_max": int(max(its)) if its else 0}
 
     hbm, src = peaks()
-    # Dominant kernel (k_fine_up: fine-level V-cycle up pass, ~22% of a sweep in
-    # the ncu launch list): algorithmic bytes = 3.25 complex values (read z2, r,
-    # 1/4 coarse correction; write z) x 16 B per fine node per active frequency,
-    # divided by its CUDA-event duration measured over the timed region.
+    # Dominant kernel (k_stream_up<Five>: fine-level V-cycle up pass, ~20% of a
+    # sweep in the ncu launch list): algorithmic bytes = 3.25 complex values
+    # (read z2, r, 1/4 coarse correction; write z) x 16 B per fine node per
+    # active frequency, divided by its CUDA-event duration measured over the
+    # timed region.
     traffic = None
     try:
         with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
-            traffic = json.load(f).get("k_fine_up_dram_bytes_per_launch")
+            traffic = json.load(f).get("dominant_kernel_dram_bytes_per_launch")
     except Exception:
         pass
     k_avg_ms = k_ms / max(k_launches, 1)
     k_bytes_launch = k_bytes / max(k_launches, 1)
     k_ach = k_bytes_launch / (k_avg_ms / 1e3) / 1e9 if k_launches else None
-    roofline = {"bound": "hbm", "kernel": "k_fine_up (fine-level V-cycle up pass)",
+    roofline = {"bound": "hbm", "kernel": "k_stream_up<Five> (fine-level V-cycle up pass)",
                 "achieved": k_ach, "peak": hbm, "unit": "GB/s",
                 "frac": (k_ach / hbm) if k_ach else None, "traffic": traffic, "peak_source": src,
                 "bytes_per_launch": k_bytes_launch, "avg_launch_ms": k_avg_ms, "launches": k_launches}
     # Whole-sweep algorithmic bytes: B = 72 D + 16 n S sum_k it_k
-    # with S = 17.3 complex streams per inner iteration and frequency as
-    # implemented (fine: apply 4, update 6, down 2.25, up 3.25; coarse levels
-    # 5.5 x (1/4 + 1/16 + ...)).
+    # with S = 17.0 complex streams per inner iteration and frequency as
+    # implemented (fine: apply 4, update 6, down 2.25, up 3.25; first Galerkin
+    # level 5.5 / 4; fused small-level cycle: read b, write z at 1/16).
     K = desc.steps // 2 + 1
     n = (desc.cells - 1) ** 2
+    STREAMS = 15.5 + 5.5 / 4 + 2.0 / 16
     mean_inner = float(np.mean(inner)) if inner else 0.0
-    b_alg = 72.0 * D + 16.0 * n * 17.3 * K * mean_inner
+    b_alg = 72.0 * D + 16.0 * n * STREAMS * K * mean_inner
     t_sweep = total_ms / 1e3 / args.steps
     sweep_roofline = {"bound": "hbm", "achieved": b_alg / t_sweep / 1e9, "peak": hbm, "unit": "GB/s",
                       "frac": b_alg / t_sweep / 1e9 / hbm, "bytes_per_sweep": b_alg,
-                      "streams_per_inner_iteration": 17.3, "inner_iterations_mean": mean_inner}
+                      "streams_per_inner_iteration": STREAMS, "inner_iterations_mean": mean_inner}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
