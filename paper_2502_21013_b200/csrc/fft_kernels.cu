@@ -19,6 +19,7 @@
 // energy (Im X_0^2 + Im X_{N/2}^2)/N that the full complex inverse would
 // produce.
 #include <cmath>
+#include <cstdlib>
 #include <numbers>
 
 #include "tp_internal.cuh"
@@ -32,6 +33,16 @@ __device__ __forceinline__ int bitrev(int i, int bits) { return __brev(i) >> (32
 __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
   return {fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
 }
+
+__device__ __forceinline__ void acp8(void* sdst, const void* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+}
+__device__ __forceinline__ void acp16(void* sdst, const void* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0) : "memory");
+}
+__device__ __forceinline__ void acp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
 template <bool INVERSE>
 __device__ void transform(cplx* z, cplx* tmp, const cplx* __restrict__ tw, int N, int P, bool pow2) {
@@ -163,6 +174,224 @@ __global__ void k_rdft_inverse(const cplx* __restrict__ Uhat, double* __restrict
   }
 }
 
+// ------------------------------------------------------------------ Stockham
+// Power-of-two N >= 16: self-sorting Stockham passes of radix 16 (then one
+// pass of radix 2, 4 or 8 for the rest of N), each an in-register R-point DFT
+// between one shared-memory load and one store, instead of log2(N) radix-2
+// passes through shared memory.  Columns are interleaved in shared memory
+// (z[pos * P + p]) so a warp's accesses of one pass hit consecutive 16-byte
+// words.  Every thread holds 16 values per pass (T = P N / 16 threads):
+// load, barrier, twiddle + DFT + store, barrier -- in place.
+// Same transform as the reference's DftPlan (unnormalised forward, 1/N
+// inverse, fft.hpp:61-99) up to rounding.
+__constant__ double kC16[16] = {1.0,
+                                0.92387953251128673848,
+                                0.70710678118654752440,
+                                0.38268343236508977173,
+                                0.0,
+                                -0.38268343236508977173,
+                                -0.70710678118654752440,
+                                -0.92387953251128673848,
+                                -1.0,
+                                -0.92387953251128673848,
+                                -0.70710678118654752440,
+                                -0.38268343236508977173,
+                                0.0,
+                                0.38268343236508977173,
+                                0.70710678118654752440,
+                                0.92387953251128673848};
+
+template <int R>
+__device__ __forceinline__ constexpr int rev_bits(int i) {
+  int r = 0;
+  for (int b = 1; b < R; b <<= 1) {
+    r = (r << 1) | (i & 1);
+    i >>= 1;
+  }
+  return r;
+}
+
+// in-register R-point DFT, natural order in and out (radix-2 DIT)
+template <int R, bool INV>
+__device__ __forceinline__ void dft_reg(cplx (&v)[R]) {
+  cplx t[R];
+#pragma unroll
+  for (int i = 0; i < R; ++i) t[i] = v[rev_bits<R>(i)];
+  constexpr int LOG = R == 2 ? 1 : R == 4 ? 2 : R == 8 ? 3 : 4;
+#pragma unroll
+  for (int st = 0; st < LOG; ++st) {
+    const int len = 2 << st;
+#pragma unroll
+    for (int i = 0; i < R; i += len) {
+#pragma unroll
+      for (int k = 0; k < len / 2; ++k) {
+        const cplx a = t[i + k];
+        cplx b = t[i + k + len / 2];
+        if (k != 0) {
+          // exp(-+2 pi i k / len) = cos - +i sin, from the 16-entry table
+          const int m = k * (16 / len);
+          const double c = kC16[m], sn = kC16[(m + 12) & 15];  // sin(x) = cos(x - pi/2)
+          const cplx w = {c, INV ? sn : -sn};
+          b = cmul(b, w);
+        }
+        t[i + k] = a + b;
+        t[i + k + len / 2] = a - b;
+      }
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < R; ++i) v[i] = t[i];
+}
+
+template <int R, bool INV>
+__device__ __forceinline__ void stockham_pass(cplx* z, const cplx* tw, int N, int P, int Ns, int T) {
+  constexpr int B = 16 / R;  // butterflies per thread
+  cplx v[B][R];
+  const int NR = N / R;
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int t = threadIdx.x + b * T, p = t % P, j = t / P;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = z[(size_t)(j + r * NR) * P + p];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int t = threadIdx.x + b * T, p = t % P, j = t / P;
+    const int k = j % Ns;
+    if (Ns > 1) {
+      const int step = k * (N / (Ns * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cplx w = tw[r * step];
+        if (INV) w.im = -w.im;
+        v[b][r] = cmul(v[b][r], w);
+      }
+    }
+    dft_reg<R, INV>(v[b]);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[(size_t)(base + r * Ns) * P + p] = v[b][r];
+  }
+  __syncthreads();
+}
+
+template <bool INV>
+__device__ void stockham(cplx* z, const cplx* tw, int N, int P) {
+  const int T = blockDim.x;
+  int Ns = 1;
+  while (Ns * 16 <= N) {
+    stockham_pass<16, INV>(z, tw, N, P, Ns, T);
+    Ns *= 16;
+  }
+  const int rest = N / Ns;
+  if (rest == 8) stockham_pass<8, INV>(z, tw, N, P, Ns, T);
+  else if (rest == 4) stockham_pass<4, INV>(z, tw, N, P, Ns, T);
+  else if (rest == 2) stockham_pass<2, INV>(z, tw, N, P, Ns, T);
+}
+
+// shared layout: twiddles W_N^m (N), then the P interleaved columns (P N)
+__global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N, int P,
+                               const cplx* __restrict__ tw) {
+  extern __shared__ cplx smem[];
+  cplx* tws = smem;
+  cplx* z = smem + N;
+  const int C = 2 * P;
+  const size_t j0 = (size_t)blockIdx.x * C;
+  // all loads in flight at once (cp.async, zero-fill past the last column)
+  for (int t = threadIdx.x; t < N; t += blockDim.x) acp16(&tws[t], &tw[t], true);
+  double* zd = reinterpret_cast<double*>(z);
+  for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
+    const int i = t / C, cc = t - i * C;
+    const bool ok = j0 + cc < n;
+    acp8(&zd[(size_t)i * C + cc], G + (ok ? (size_t)i * n + j0 + cc : 0), ok);  // = z[i P + cc/2].{re,im}
+  }
+  acp_wait_all();
+  __syncthreads();
+  stockham<false>(z, tws, N, P);
+  const int K = N / 2 + 1;
+  for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
+    const int k = t / C, cc = t - k * C;
+    if (j0 + cc >= n) continue;
+    const int p = cc >> 1;
+    const cplx Zk = z[(size_t)k * P + p], Zm = conj(z[(size_t)((N - k) % N) * P + p]);
+    cplx X;
+    if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
+    else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
+    Ghat[(size_t)k * n + j0 + cc] = X;
+  }
+}
+
+__global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N, int P,
+                               const cplx* __restrict__ tw, double* __restrict__ part) {
+  extern __shared__ cplx smem[];
+  __shared__ double red[2][32];
+  cplx* tws = smem;
+  cplx* z = smem + N;
+  const int C = 2 * P;
+  const size_t j0 = (size_t)blockIdx.x * C;
+  const int half = N / 2;
+  // stage the K x C half-spectrum block (cp.async, all in flight), then build
+  // the Hermitian extension of the two packed columns in place of the FFT buffer
+  // (N even: self-conjugate bins 0 and N/2)
+  cplx* raw = z + (size_t)N * P;  // K x C
+  const int K = half + 1;
+  for (int t = threadIdx.x; t < N; t += blockDim.x) acp16(&tws[t], &tw[t], true);
+  for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
+    const int k = t / C, cc = t - k * C;
+    const bool ok = j0 + cc < n;
+    acp16(&raw[t], Uhat + (ok ? (size_t)k * n + j0 + cc : 0), ok);
+  }
+  acp_wait_all();
+  __syncthreads();
+  double im2 = 0;
+  for (int t = threadIdx.x; t < N * P; t += blockDim.x) {
+    const int k = t / P, p = t - k * P;
+    const int kk = (k <= half) ? k : N - k;
+    const cplx Xa = raw[kk * C + 2 * p], Xb = raw[kk * C + 2 * p + 1];
+    cplx Z;
+    if (k == 0 || k == half) {
+      Z = {Xa.re, Xb.re};
+      im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
+    } else if (k < half) {
+      Z = {Xa.re - Xb.im, Xa.im + Xb.re};
+    } else {
+      Z = {Xa.re + Xb.im, -Xa.im + Xb.re};
+    }
+    z[(size_t)k * P + p] = Z;
+  }
+  __syncthreads();
+  stockham<true>(z, tws, N, P);
+  const double invN = 1.0 / N;
+  double re2 = 0;
+  const double* zd = reinterpret_cast<const double*>(z);
+  for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
+    const int i = t / C, cc = t - i * C;
+    if (j0 + cc >= n) continue;
+    const double x = zd[(size_t)i * C + cc] * invN;
+    U[(size_t)i * n + j0 + cc] = x;
+    re2 += x * x;
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    re2 += __shfl_down_sync(0xffffffffu, re2, o);
+    im2 += __shfl_down_sync(0xffffffffu, im2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = re2;
+    red[1][threadIdx.x >> 5] = im2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
 __global__ void k_reduce_pairs(const double* __restrict__ part, int count, double* __restrict__ out) {
   __shared__ double sh[2][32];
   double a = 0, b = 0;
@@ -195,6 +424,10 @@ struct FftPlan {
   bool pow2 = false;
   size_t smem = 0;
   DevBuf<cplx> tw;
+  // Stockham path (power-of-two N >= 16): columns pairs per block, threads, shared bytes
+  bool stockham = false;
+  int sP = 0, sT = 0;
+  size_t ssmem = 0;
 };
 
 FftPlan& plan_for(Problem& p) {
@@ -220,6 +453,22 @@ FftPlan& plan_for(Problem& p) {
   TP_CUDA(cudaMemcpy(pl->tw.get(), h.data(), N * sizeof(cplx), cudaMemcpyHostToDevice));
   TP_CUDA(cudaFuncSetAttribute(k_rdft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
   TP_CUDA(cudaFuncSetAttribute(k_rdft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->smem));
+  // Stockham: P N / 16 threads (16 values each per pass), P N ~ 2048 complex
+  // (36 KB of shared memory with the twiddles: six blocks per SM)
+  if (pl->pow2 && N >= 16 && !std::getenv("TPGPU_RADIX2_DFT")) {
+    int sP = std::max(1, 2048 / N);
+    while (sP > 1 && (size_t)(sP + 1) * N * sizeof(cplx) > 100 * 1024) sP >>= 1;
+    const int T = sP * N / 16;
+    if (T <= 1024 && (size_t)((sP + 1) * N + (N / 2 + 1) * 2 * sP) * sizeof(cplx) <= 200 * 1024) {
+      pl->stockham = true;
+      pl->sP = sP;
+      pl->sT = std::max(32, T);
+      // + the inverse's staged half spectrum (N/2+1) x 2P
+      pl->ssmem = (size_t)((sP + 1) * N + (N / 2 + 1) * 2 * sP) * sizeof(cplx);
+      TP_CUDA(cudaFuncSetAttribute(k_sfft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
+      TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
+    }
+  }
   p.fft_plan = pl;
   return *pl;
 }
@@ -229,6 +478,12 @@ FftPlan& plan_for(Problem& p) {
 void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat) {
   FftPlan& pl = plan_for(p);
   const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
+  if (pl.stockham) {
+    const int blocks = (int)((n + 2 * pl.sP - 1) / (2 * pl.sP));
+    k_sfft_forward<<<blocks, pl.sT, pl.ssmem, p.stream>>>(G, Ghat, n, pl.N, pl.sP, pl.tw.get());
+    TP_LAUNCHED(&p);
+    return;
+  }
   const int C = 2 * pl.P;
   const int blocks = (int)((n + C - 1) / C);
   k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2,
@@ -239,12 +494,16 @@ void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat) {
 void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2) {
   FftPlan& pl = plan_for(p);
   const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
-  const int C = 2 * pl.P;
+  const int C = 2 * (pl.stockham ? pl.sP : pl.P);
   const int blocks = (int)((n + C - 1) / C);
   p.part.ensure((size_t)2 * blocks);
   p.red.ensure(16);
-  k_rdft_inverse<<<blocks, 256, pl.smem, p.stream>>>(Uhat, U, n, pl.N, pl.P, pl.bits, pl.pow2,
-                                                     pl.tw.get(), p.part.get());
+  if (pl.stockham) {
+    k_sfft_inverse<<<blocks, pl.sT, pl.ssmem, p.stream>>>(Uhat, U, n, pl.N, pl.sP, pl.tw.get(), p.part.get());
+  } else {
+    k_rdft_inverse<<<blocks, 256, pl.smem, p.stream>>>(Uhat, U, n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
+                                                       p.part.get());
+  }
   TP_LAUNCHED(&p);
   k_reduce_pairs<<<1, 1024, 0, p.stream>>>(p.part.get(), blocks, p.red.get());
   TP_LAUNCHED(&p);
