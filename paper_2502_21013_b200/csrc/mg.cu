@@ -769,23 +769,6 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
   }
 }
 
-// x += xa p (pending fused solution update after the last iteration)
-template <int MODE>
-__global__ void __launch_bounds__(NT, 4) k_xupdate(Op<MODE> op, TT<MODE>* __restrict__ xs,
-                                                   const TT<MODE>* __restrict__ p, const TT<MODE>* __restrict__ xa,
-                                                   int nb, int BB) {
-  TILE_PROLOGUE
-  if (!in) return;
-  for (int k = 0; k < BB; ++k) {
-    const int b = blockIdx.z * BB + k;
-    if (b >= nb) break;
-    const TT<MODE> al = xa[b];
-    if (norm2(al) == 0.0) continue;
-    const size_t j = (size_t)b * n + i;
-    xs[j] = xs[j] + mul(al, p[j]);
-  }
-}
-
 // partial b^T z
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_dot(Op<MODE> op, const TT<MODE>* __restrict__ a_,
@@ -1095,8 +1078,6 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   }
   const size_t n0 = (size_t)B * levels[0].n;
   r.alloc(n0);
-  if (MODE == 0 && levels[0].fine.we && L > 1) r2.alloc(n0);
-  xa.alloc(B);
   p0.alloc(n0);
   p1.alloc(n0);
   q.alloc(n0);
@@ -1182,7 +1163,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
       return zo;
     }
     if (ops[l].fine.we) {
-      fine_down0(nb, bl, nullptr, nullptr);
+      fine_down0(nb, bl);
       return fine_rest0(nb, bl, dot);
     }
   }
@@ -1190,12 +1171,11 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
 }
 
 template <int MODE>
-void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out) {
+void BatchSolver<MODE>::fine_down0(int nb, const T* r_in) {
   if constexpr (MODE == 0) {
     FineOp fo = ops[0].fine;
     fo.lam = lam;
-    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
-                     qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
+    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb);
   }
 }
 
@@ -1312,27 +1292,20 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const Geo g0 = geo_for(ops[0].m, nb, p->num_sms, 8);
   const dim3 blk(TX, TY);
   const bool fine = MODE == 0 && ops[0].fine.we != nullptr;
-  // optional fused Krylov update (fine streaming path): r -= alpha q inside
-  // the fine down pass, x += alpha p inside the next apply.  Off by default:
-  // it removes the update pass (which streams at ~5.4 TB/s) but loads the
-  // latency-bound down pass further -- measured 12.5 vs 12.2 ms per cfg-1 sweep.
-  static const bool want_fuse = std::getenv("TPGPU_FUSED_UPDATE") != nullptr;
-  const bool fused = fine && ops.size() > 1 && want_fuse;
   FineOp fo = ops[0].fine;
   fo.lam = reinterpret_cast<const cplx*>(lam);
   // partials per batch of each producing kernel
   const int per_t = g0.tiles;
   const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
-  const int per_d = fine ? fine_partials(ops[0].m, 1) : per_t;   // fused down (||r||^2)
   const int per_u = fine ? fine_partials(ops[0].m, 2) : per_t;   // V-cycle dot (up)
   // the smem-tile apply (FAM 1 reads the stored 5-point stencil) keeps more
   // loads in flight than the streaming one on B200 (measured 102 vs 122 us at cfg 1)
   static const bool use_stream_apply = std::getenv("TPGPU_STREAM_APPLY") != nullptr;
-  const bool sapply = fine && use_stream_apply && !fused;
+  const bool sapply = fine && use_stream_apply;
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
-  T* xa_ptr = fused ? xa.get() : nullptr;
+  T* const xa_ptr = nullptr;  // (x updates are not deferred: k_update below)
   cudaStream_t s = p->stream;
   const int l = 0;
   if (fine && warm && sapply) {
@@ -1357,7 +1330,6 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int last_active = h_count[0];
   cur_active = last_active;
   T* rcur = r.get();
-  T* rnext = r2.get();
   T* pin = p0.get();
   T* pout = p1.get();
   if (last_active > 0) {
@@ -1378,14 +1350,10 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
-      if (fused) {
-        fine_down0(nb, rcur, q.get(), rnext);
-      } else {
-        k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr, nb,
-                                               g0.BB, part.get());
-        TP_LAUNCHED(p);
-      }
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(),
+      k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr, nb,
+                                             g0.BB, part.get());
+      TP_LAUNCHED(p);
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
       const int slot = it & 1;
@@ -1405,12 +1373,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         }
       }
       iters = it;
-      if (fused) {
-        std::swap(rcur, rnext);
-        z = fine_rest0(nb, rcur, true);
-      } else {
-        z = vcycle_level(0, nb, rcur, nullptr, false, true);
-      }
+      z = vcycle_level(0, nb, rcur, nullptr, false, true);
       k_scalars<T><<<nb, 256, 0, s>>>(ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
@@ -1419,12 +1382,6 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     if (!done) {
       TP_CUDA(cudaStreamSynchronize(s));
       last_active = h_count[iters & 1];
-    }
-    if (fused) {
-      // pending x += alpha p of the final iteration (no-op when the loop ended
-      // by convergence: the last apply already consumed every coefficient)
-      k_xupdate<MODE><<<g0.grid, blk, 0, s>>>(op0, x, done ? pout : pin, xa.get(), nb, g0.BB);
-      TP_LAUNCHED(p);
     }
   }
   TP_CUDA(cudaStreamSynchronize(s));

@@ -78,8 +78,7 @@ struct BatchSolver {
   const int* ext_mask = nullptr;  // optional: batches with mask 0 are skipped
   // work
   std::vector<DevBuf<T>> lb, lz0, lz1;  // per level (level 0: b is external)
-  DevBuf<T> r, r2, p0, p1, q;
-  DevBuf<T> xa;  // pending solution-update coefficient per batch (fused update)
+  DevBuf<T> r, p0, p1, q;
   DevBuf<double> part;
   DevBuf<T> rho, mu, alpha, beta;
   DevBuf<double> bn2, rn2;
@@ -102,9 +101,8 @@ struct BatchSolver {
   void vcycle(int lvl, int nb, T* z_out_level0, bool dot);
   T* vcycle_level(int lvl, int nb, const T* bl, T* z_first, bool first_done, bool dot);
   T* vcycle_generic(int lvl, int nb, const T* bl, bool dot);
-  // fine streaming level: down pass (optionally fusing r_out = r_in - alpha q)
-  // and the rest of the cycle (coarse levels + up pass)
-  void fine_down0(int nb, const T* r_in, const T* qv, T* r_out);
+  // fine streaming level: down pass, and the rest of the cycle (coarse levels + up pass)
+  void fine_down0(int nb, const T* r_in);
   T* fine_rest0(int nb, const T* bl, bool dot);
 };
 
@@ -120,8 +118,7 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init);
 // V-cycle down / up passes of one level (fine: op.we set; Galerkin: op.K set)
 void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                        const int* active, double om1, double om2, int nb, const cplx* q = nullptr,
-                        const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
+                        const int* active, double om1, double om2, int nb);
 void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).

@@ -410,53 +410,87 @@ __device__ __forceinline__ Item item_rh(int m, int own, int rh, int nb, const in
 #define TP_PRAGMA(x) _Pragma(#x)
 #define TP_UNROLL(n) TP_PRAGMA(unroll n)
 
+// warp work item over NB batches: ((g * nch) + chunk) * ns + strip, batches
+// g*NB .. g*NB+NB-1 (inactive or missing ones are computed on a stand-in
+// batch and never stored, so shuffles stay warp-uniform)
+template <int WPBK, int NB>
+struct ItemNB {
+  int b[NB];
+  bool on[NB];
+  int strip, chunk, ys, ye, xs;
+  bool ok;
+};
+template <int WPBK, int NB>
+__device__ __forceinline__ ItemNB<WPBK, NB> item_nb(int m, int own, int rh, int nb, const int* __restrict__ active) {
+  ItemNB<WPBK, NB> it;
+  const int w = blockIdx.x * WPBK + (threadIdx.x >> 5);
+  const int ns = (m + own - 1) / own, nch = (m + rh - 1) / rh;
+  it.strip = w % ns;
+  it.chunk = (w / ns) % nch;
+  const int g = w / (ns * nch);
+  int first = -1;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const int b = g * NB + j;
+    it.on[j] = b < nb && (!active || active[b]);
+    if (it.on[j] && first < 0) first = b;
+  }
+  it.ok = first >= 0;
+#pragma unroll
+  for (int j = 0; j < NB; ++j) it.b[j] = it.on[j] ? g * NB + j : first;
+  it.ys = it.chunk * rh;
+  it.ye = min(it.ys + rh, m);
+  it.xs = it.strip * own;
+  return it;
+}
+
 // ---------------------------------------------------------------- down
 //   z1 = w1 r/d ; z2 = z1 + w2 (r - A z1)/d ; res = r - A z2 ; b_c = P^T res
-// FUSED: the right-hand side is r_new = r - alpha q (read r and q, write
-// r_new to rout for the owned block, partial ||r_new||^2 per warp item),
-// replacing the separate x/r update pass (x is updated in the next apply).
-template <class S, bool FUSED, int RA, int WPBK>
+// NB frequencies per warp share the coefficient rows, the addressing and the
+// ring bookkeeping; their arithmetic chains are independent (ILP).
+template <class S, int NB, int RA, int WPBK>
 __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp op, const cplx* __restrict__ rv,
-                                                           cplx* __restrict__ z2out, cplx* __restrict__ bc,
-                                                           int mc, int rh, const int* __restrict__ active,
-                                                           double om1, double om2, int nb,
-                                                           const cplx* __restrict__ qv,
-                                                           const cplx* __restrict__ alpha, cplx* __restrict__ rout,
-                                                           double* __restrict__ part) {
+                                                                         cplx* __restrict__ z2out,
+                                                                         cplx* __restrict__ bc, int mc, int rh,
+                                                                         const int* __restrict__ active, double om1,
+                                                                         double om2, int nb) {
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
-  constexpr int NV = FUSED ? 2 : 1, RV = RA + 2, RC = RA + 2 + S::RETAIN;
+  constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
-  const Item it = item_rh<WPBK>(m, OWN, rh, nb, active);
+  const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<NV>* const vring = reinterpret_cast<VRow<NV>*>(fine_smem) + wib * RV;
-  WRow<S::NW>* const wring =
-      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NV>)) + wib * RC;
+  VRow<NB>* const vring = reinterpret_cast<VRow<NB>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NB>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < H + OWN && colok;
   const int xc = min(max(x, 0), m - 1);
-  const size_t o = (size_t)it.b * op.n;
-  const cplx* const rp = rv + o + xc;
-  const cplx* const qp = FUSED ? qv + o + xc : nullptr;
-  cplx* const ro = FUSED ? rout + o + xc : nullptr;
-  const cplx al = FUSED ? alpha[it.b] : cplx{0, 0};
-  cplx* const zo = z2out + o + xc;
-  const cplx l = op.lam[it.b];
+  const cplx* rp[NB];
+  cplx* zo[NB];
+  cplx* bco[NB];
+  cplx l[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const size_t o = (size_t)it.b[j] * op.n;
+    rp[j] = rv + o + xc;
+    zo[j] = z2out + o + xc;
+    bco[j] = bc + (size_t)it.b[j] * mc * mc + (x >> 1);
+    l[j] = op.lam[it.b[j]];
+  }
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 3, ylast = ye + 2;  // staged rows
   const bool cown = own && (x & 1) && (x >> 1) < mc;  // coarse centre column
-  double rn2 = 0;
   typename S::Src src = S::src(op, x, xc, y0);
-  int voff = y0 * m;       // row offset of the next vector row to stage
-  int vi = 0, wi = 0;      // next ring slots to fill
+  int voff = y0 * m;  // row offset of the next vector row to stage
+  int vi = 0, wi = 0; // next ring slots to fill
   auto issue = [&](int yr) {
     if (yr <= ylast) {
       const bool rin = colok && (unsigned)yr < (unsigned)m;
       const int off = rin ? voff : 0;
-      cp16(&vring[vi].v[0][lane], rp + off, rin);
-      if (FUSED) cp16(&vring[vi].v[1][lane], qp + off, rin);
+#pragma unroll
+      for (int j = 0; j < NB; ++j) cp16(&vring[vi].v[j][lane], rp[j] + off, rin);
       S::stage(wring[wi], src, lane, yr);
       voff += m;
       vi = wrap_inc(vi, RV);
@@ -464,13 +498,18 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
     }
     cp_commit();
   };
-  cplx* const bco = bc + (size_t)it.b * mc * mc + (x >> 1);
   // pipeline over input rows yi = ys-2 .. ye+2: z1 at yi, z2 at yi-1,
   // residual at yi-2, restriction centred on yi-3
-  cplx r0{0, 0}, r1{0, 0}, r2{0, 0};  // r at yi, yi-1, yi-2
-  cplx a0{0, 0}, a1{0, 0}, a2{0, 0};  // z1 at yi, yi-1, yi-2
-  cplx b1{0, 0}, b2{0, 0}, b3{0, 0};  // z2 at yi-1, yi-2, yi-3
-  cplx q2{0, 0}, q3{0, 0}, q4{0, 0};  // res at yi-2, yi-3, yi-4
+  cplx r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
+  cplx a0[NB], a1[NB], a2[NB];  // z1 at yi, yi-1, yi-2
+  cplx b1[NB], b2[NB], b3[NB];  // z2 at yi-1, yi-2, yi-3
+  cplx q2[NB], q3[NB], q4[NB];  // res at yi-2, yi-3, yi-4
+  cplx id0[NB], id1[NB];        // 1/d of rows yi, yi-1
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    r0[j] = r1[j] = r2[j] = a0[j] = a1[j] = a2[j] = cplx{0, 0};
+    b1[j] = b2[j] = b3[j] = q2[j] = q3[j] = q4[j] = id0[j] = id1[j] = cplx{0, 0};
+  }
 #pragma unroll
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
   // coefficient rows yi .. yi-3 (rows before y0 only feed halo values that
@@ -478,103 +517,100 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   int vr = 0, sr = 0;  // ring slots of row yi
   cp_wait<RA>();
   typename S::Reg k0 = S::load(wring[0], lane), k1 = k0, k2 = k0, k3 = k0;
-  cplx id0{0, 0}, id1{0, 0};  // 1/d of rows yi, yi-1
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 2; yi <= ylast; ++yi) {
     issue(yi + RA);
     vr = wrap_inc(vr, RV);
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
-    cplx rcur = vring[vr].v[0][lane];
-    if (FUSED) {
-      const cplx qq = vring[vr].v[1][lane];
-      rcur.re -= al.re * qq.re - al.im * qq.im;
-      rcur.im -= al.re * qq.im + al.im * qq.re;
-      if (own && yi >= ys && yi < ye) {
-        ro[(long)yi * m] = rcur;
-        rn2 += rcur.re * rcur.re + rcur.im * rcur.im;
-      }
-    }
-    r2 = r1; r1 = r0; r0 = rcur;
     k3 = k2; k2 = k1; k1 = k0;
     k0 = S::load(wring[sr], lane);
-    // z1 = omega r / d at row yi (off-domain diagonals may vanish: z1 = 0 there)
-    a2 = a1; a1 = a0;
-    id1 = id0;
-    id0 = rcp(S::diag(k0, k1, l));
-    a0 = (colok && (unsigned)yi < (unsigned)m) ? cs(om1, cm(r0, id0)) : cplx{0, 0};
-    // z2 at row yi-1
-    b3 = b2; b2 = b1;
-    {
-      const cplx Aa = S::apply(k1, k2, l, a2, a1, a0);
-      const cplx t = cm({r1.re - Aa.re, r1.im - Aa.im}, id1);
-      const int y = yi - 1;
-      const bool in = colok && (unsigned)y < (unsigned)m;
-      b1 = in ? cplx{fma(om2, t.re, a1.re), fma(om2, t.im, a1.im)} : cplx{0, 0};
-      if (own && y >= ys && y < ye) zo[(long)y * m] = b1;
-    }
-    // residual at row yi-2
-    q4 = q3; q3 = q2;
-    {
-      const cplx Ab = S::apply(k2, k3, l, b3, b2, b1);
-      const int y = yi - 2;
-      q2 = (colok && (unsigned)y < (unsigned)m) ? cplx{r2.re - Ab.re, r2.im - Ab.im} : cplx{0, 0};
+    const bool in0 = colok && (unsigned)yi < (unsigned)m;
+    const bool in1 = colok && (unsigned)(yi - 1) < (unsigned)m;
+    const bool in2 = colok && (unsigned)(yi - 2) < (unsigned)m;
+    const bool st1 = own && yi - 1 >= ys && yi - 1 < ye;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = vring[vr].v[j][lane];
+      // z1 = omega r / d at row yi (off-domain diagonals may vanish: z1 = 0 there)
+      a2[j] = a1[j]; a1[j] = a0[j];
+      id1[j] = id0[j];
+      id0[j] = rcp(S::diag(k0, k1, l[j]));
+      a0[j] = in0 ? cs(om1, cm(r0[j], id0[j])) : cplx{0, 0};
+      // z2 at row yi-1
+      b3[j] = b2[j]; b2[j] = b1[j];
+      {
+        const cplx Aa = S::apply(k1, k2, l[j], a2[j], a1[j], a0[j]);
+        const cplx t = cm({r1[j].re - Aa.re, r1[j].im - Aa.im}, id1[j]);
+        b1[j] = in1 ? cplx{fma(om2, t.re, a1[j].re), fma(om2, t.im, a1[j].im)} : cplx{0, 0};
+        if (st1 && it.on[j]) zo[j][(long)(yi - 1) * m] = b1[j];
+      }
+      // residual at row yi-2
+      q4[j] = q3[j]; q3[j] = q2[j];
+      {
+        const cplx Ab = S::apply(k2, k3, l[j], b3[j], b2[j], b1[j]);
+        q2[j] = in2 ? cplx{r2[j].re - Ab.re, r2[j].im - Ab.im} : cplx{0, 0};
+      }
     }
     // restriction centred on row yc = yi-3 (odd fine rows 2Y+1; warp-uniform branch)
     const int yc = yi - 3;
     if ((yc & 1) && yc >= ys && yc < ye) {
-      const cplx qw = shf_up(q3), qe = shf_dn(q3);
-      const cplx q4w = shf_up(q4), q2e = shf_dn(q2);
-      if (cown && (yc >> 1) < mc) {
-        cplx acc = q3;
-        acc.re += 0.5 * (qw.re + qe.re + q4.re + q2.re + q4w.re + q2e.re);
-        acc.im += 0.5 * (qw.im + qe.im + q4.im + q2.im + q4w.im + q2e.im);
-        bco[(size_t)(yc >> 1) * mc] = acc;
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        const cplx qw = shf_up(q3[j]), qe = shf_dn(q3[j]);
+        const cplx q4w = shf_up(q4[j]), q2e = shf_dn(q2[j]);
+        if (cown && it.on[j] && (yc >> 1) < mc) {
+          cplx acc = q3[j];
+          acc.re += 0.5 * (qw.re + qe.re + q4[j].re + q2[j].re + q4w.re + q2e.re);
+          acc.im += 0.5 * (qw.im + qe.im + q4[j].im + q2[j].im + q4w.im + q2e.im);
+          bco[j][(size_t)(yc >> 1) * mc] = acc;
+        }
       }
     }
   }
   cp_wait<0>();
-  if (FUSED) {
-    double z = 0;
-    warp_pair(rn2, z);
-    if (lane == 0) {
-      const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
-      const size_t k = (size_t)it.b * ((size_t)ns * nch) + (size_t)it.chunk * ns + it.strip;
-      part[2 * k] = rn2;
-      part[2 * k + 1] = 0.0;
-    }
-  }
 }
 
 // ---------------------------------------------------------------- up
 //   zc = z2 + P x_c ; z3, z4 = two Jacobi steps ; writes z4 (+ partial r^T z4)
-// Staged per row: r, z2 and the (up to two) coarse values P x_c interpolates
-// from at the lane's node, plus the coefficient row.
-template <class S, int RA, int WPBK>
+// Staged per row and frequency: r, z2 and the (up to two) coarse values P x_c
+// interpolates from at the lane's node; the coefficient row once.
+template <class S, int NB, int RA, int WPBK>
 __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp op, const cplx* __restrict__ rv,
-                                                         const cplx* __restrict__ z2in, const cplx* __restrict__ xcv,
-                                                         int mc, int rh, cplx* __restrict__ zout,
-                                                         const int* __restrict__ active, double om1, double om2,
-                                                         int nb, int dot, double* __restrict__ part) {
+                                                                       const cplx* __restrict__ z2in,
+                                                                       const cplx* __restrict__ xcv, int mc, int rh,
+                                                                       cplx* __restrict__ zout,
+                                                                       const int* __restrict__ active, double om1,
+                                                                       double om2, int nb, int dot,
+                                                                       double* __restrict__ part) {
   constexpr int H = 2, OWN = WL - 2 * H;  // 28
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
-  const Item it = item_rh<WPBK>(m, OWN, rh, nb, active);
+  const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<4>* const vring = reinterpret_cast<VRow<4>*>(fine_smem) + wib * RV;
-  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<4>)) + wib * RC;
+  VRow<4 * NB>* const vring = reinterpret_cast<VRow<4 * NB>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring =
+      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<4 * NB>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
   const int xc = min(max(x, 0), m - 1);
-  const size_t o = (size_t)it.b * op.n;
-  const cplx* const rp = rv + o + xc;
-  const cplx* const zp = z2in + o + xc;
-  cplx* const zo = zout + o + xc;
-  const cplx* xb = xcv + (size_t)it.b * mc * mc;
-  const cplx l = op.lam[it.b];
+  const cplx* rp[NB];
+  const cplx* zp[NB];
+  const cplx* xb[NB];
+  cplx* zo[NB];
+  cplx l[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    const size_t o = (size_t)it.b[j] * op.n;
+    rp[j] = rv + o + xc;
+    zp[j] = z2in + o + xc;
+    zo[j] = zout + o + xc;
+    xb[j] = xcv + (size_t)it.b[j] * mc * mc;
+    l[j] = op.lam[it.b[j]];
+  }
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 3, ylast = ye + 1;
   // P1 prolongation: fine vertex a = x+1 (column parity fixed per lane);
@@ -590,9 +626,6 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
     if (yr <= ylast) {
       const bool rin = colok && (unsigned)yr < (unsigned)m;
       const int off = rin ? voff : 0;
-      VRow<4>& sv = vring[vi];
-      cp16(&sv.v[0][lane], rp + off, rin);
-      cp16(&sv.v[1][lane], zp + off, rin);
       // coarse vertices of the node's P1 interpolation: (A1, B1) and (A2, B2);
       // the second is absent at coincident vertices
       const int bb = yr + 1, bh = bb >> 1;
@@ -600,8 +633,15 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
       const bool has2 = ao || (bb & 1);
       const bool ok1 = rin && cA1 && bh >= 1 && bh <= mc;
       const bool ok2 = rin && has2 && cA2 && B2 >= 1 && B2 <= mc;
-      cp16(&sv.v[2][lane], xb + (ok1 ? (bh - 1) * mc + (ah - 1) : 0), ok1);
-      cp16(&sv.v[3][lane], xb + (ok2 ? (B2 - 1) * mc + (A2 - 1) : 0), ok2);
+      const int c1 = ok1 ? (bh - 1) * mc + (ah - 1) : 0, c2 = ok2 ? (B2 - 1) * mc + (A2 - 1) : 0;
+      VRow<4 * NB>& sv = vring[vi];
+#pragma unroll
+      for (int j = 0; j < NB; ++j) {
+        cp16(&sv.v[4 * j][lane], rp[j] + off, rin);
+        cp16(&sv.v[4 * j + 1][lane], zp[j] + off, rin);
+        cp16(&sv.v[4 * j + 2][lane], xb[j] + c1, ok1);
+        cp16(&sv.v[4 * j + 3][lane], xb[j] + c2, ok2);
+      }
       S::stage(wring[wi], src, lane, yr);
       voff += m;
       vi = wrap_inc(vi, RV);
@@ -610,66 +650,77 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
     cp_commit();
   };
   // pipeline over input rows yi = ys-2 .. ye+1: zc at yi, z3 at yi-1, z4 at yi-2
-  cplx c0{0, 0}, c1{0, 0}, c2{0, 0};  // zc at yi, yi-1, yi-2
-  cplx r0{0, 0}, r1{0, 0}, r2{0, 0};  // r at yi, yi-1, yi-2
-  cplx e1{0, 0}, e2{0, 0}, e3{0, 0};  // z3 at yi-1, yi-2, yi-3
+  cplx c0[NB], c1[NB], c2[NB];  // zc at yi, yi-1, yi-2
+  cplx r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
+  cplx e1[NB], e2[NB], e3[NB];  // z3 at yi-1, yi-2, yi-3
+  cplx jd1[NB], jd2[NB];        // 1/d of rows yi-1, yi-2
+  double p0[NB], p1[NB];
+#pragma unroll
+  for (int j = 0; j < NB; ++j) {
+    c0[j] = c1[j] = c2[j] = r0[j] = r1[j] = r2[j] = cplx{0, 0};
+    e1[j] = e2[j] = e3[j] = jd1[j] = jd2[j] = cplx{0, 0};
+    p0[j] = p1[j] = 0;
+  }
 #pragma unroll
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
   int vr = 0, sr = 0;
   cp_wait<RA>();
   typename S::Reg k0 = S::load(wring[0], lane), k1 = k0, k2 = k0, k3 = k0;  // rows yi .. yi-3
-  double p0 = 0, p1 = 0;
-  cplx jd1{0, 0}, jd2{0, 0};  // 1/d of rows yi-1, yi-2
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 2; yi <= ylast; ++yi) {
     issue(yi + RA);
     vr = wrap_inc(vr, RV);
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
-    const VRow<4>& sv = vring[vr];
+    const VRow<4 * NB>& sv = vring[vr];
     const double wc1 = (!ao && !((yi + 1) & 1)) ? 1.0 : 0.5;
-    const cplx zz = sv.v[1][lane], x1 = sv.v[2][lane], x2 = sv.v[3][lane];
-    const cplx ccur = {fma(wc1, x1.re, fma(0.5, x2.re, zz.re)), fma(wc1, x1.im, fma(0.5, x2.im, zz.im))};
-    c2 = c1; c1 = c0; c0 = ccur;
-    r2 = r1; r1 = r0; r0 = sv.v[0][lane];
     k3 = k2; k2 = k1; k1 = k0;
     k0 = S::load(wring[sr], lane);
-    // z3 at row yi-1
-    e3 = e2; e2 = e1;
-    {
-      const cplx Ac = S::apply(k1, k2, l, c2, c1, c0);
-      jd2 = jd1;
-      jd1 = rcp(S::diag(k1, k2, l));
-      const cplx t = cm({r1.re - Ac.re, r1.im - Ac.im}, jd1);
-      const int y = yi - 1;
-      e1 = (colok && (unsigned)y < (unsigned)m) ? cplx{fma(om2, t.re, c1.re), fma(om2, t.im, c1.im)}
-                                                 : cplx{0, 0};
-    }
-    // z4 at row yi-2
-    {
-      const cplx Ae = S::apply(k2, k3, l, e3, e2, e1);
-      const int y = yi - 2;
-      if (own && y >= ys && y < ye) {
-        const cplx t = cm({r2.re - Ae.re, r2.im - Ae.im}, jd2);
-        const cplx z4 = {fma(om1, t.re, e2.re), fma(om1, t.im, e2.im)};
-        zo[(long)y * m] = z4;
-        if (dot) {
-          const cplx pr = cm(r2, z4);
-          p0 += pr.re;
-          p1 += pr.im;
+    const bool in1 = colok && (unsigned)(yi - 1) < (unsigned)m;
+    const bool st2 = own && yi - 2 >= ys && yi - 2 < ye;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      const cplx zz = sv.v[4 * j + 1][lane], x1 = sv.v[4 * j + 2][lane], x2 = sv.v[4 * j + 3][lane];
+      const cplx ccur = {fma(wc1, x1.re, fma(0.5, x2.re, zz.re)), fma(wc1, x1.im, fma(0.5, x2.im, zz.im))};
+      c2[j] = c1[j]; c1[j] = c0[j]; c0[j] = ccur;
+      r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = sv.v[4 * j][lane];
+      // z3 at row yi-1
+      e3[j] = e2[j]; e2[j] = e1[j];
+      {
+        const cplx Ac = S::apply(k1, k2, l[j], c2[j], c1[j], c0[j]);
+        jd2[j] = jd1[j];
+        jd1[j] = rcp(S::diag(k1, k2, l[j]));
+        const cplx t = cm({r1[j].re - Ac.re, r1[j].im - Ac.im}, jd1[j]);
+        e1[j] = in1 ? cplx{fma(om2, t.re, c1[j].re), fma(om2, t.im, c1[j].im)} : cplx{0, 0};
+      }
+      // z4 at row yi-2
+      {
+        const cplx Ae = S::apply(k2, k3, l[j], e3[j], e2[j], e1[j]);
+        if (st2 && it.on[j]) {
+          const cplx t = cm({r2[j].re - Ae.re, r2[j].im - Ae.im}, jd2[j]);
+          const cplx z4 = {fma(om1, t.re, e2[j].re), fma(om1, t.im, e2[j].im)};
+          zo[j][(long)(yi - 2) * m] = z4;
+          if (dot) {
+            const cplx pr = cm(r2[j], z4);
+            p0[j] += pr.re;
+            p1[j] += pr.im;
+          }
         }
       }
     }
   }
   cp_wait<0>();
   if (dot) {
-    warp_pair(p0, p1);
-    if (lane == 0) {
-      const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
-      const size_t per = (size_t)ns * nch;
-      const size_t k = (size_t)it.b * per + (size_t)it.chunk * ns + it.strip;
-      part[2 * k] = p0;
-      part[2 * k + 1] = p1;
+    const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
+    const size_t per = (size_t)ns * nch;
+#pragma unroll
+    for (int j = 0; j < NB; ++j) {
+      warp_pair(p0[j], p1[j]);
+      if (lane == 0 && it.on[j]) {
+        const size_t k = (size_t)it.b[j] * per + (size_t)it.chunk * ns + it.strip;
+        part[2 * k] = p0[j];
+        part[2 * k + 1] = p1[j];
+      }
     }
   }
 }
@@ -694,31 +745,31 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <class S, bool FUSED, int RA, int WPBK>
+template <class S, int NB, int RA, int WPBK>
 void down_t(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc, const int* active, double om1,
-            double om2, int nb, const cplx* q, const cplx* alpha, cplx* rout, double* part) {
-  constexpr size_t sm = ring_smem<S, FUSED ? 2 : 1, RA, WPBK>();
+            double om2, int nb) {
+  constexpr size_t sm = ring_smem<S, NB, RA, WPBK>();
   static bool attrs = [] {
-    cudaFuncSetAttribute(k_stream_down<S, FUSED, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_down<S, NB, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     return true;
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  k_stream_down<S, FUSED, RA, WPBK><<<grid_for(op.m, 26, nb, rh, WPBK), WL * WPBK, sm, p.stream>>>(
-      op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
+  k_stream_down<S, NB, RA, WPBK><<<grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+      op, r, z2, bc, mc, rh, active, om1, om2, nb);
 }
 
-template <class S, int RA, int WPBK>
+template <class S, int NB, int RA, int WPBK>
 void up_t(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc, cplx* z,
           const int* active, double om1, double om2, int nb, int dot, double* part) {
-  constexpr size_t sm = ring_smem<S, 4, RA, WPBK>();
+  constexpr size_t sm = ring_smem<S, 4 * NB, RA, WPBK>();
   static bool attrs = [] {
-    cudaFuncSetAttribute(k_stream_up<S, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_up<S, NB, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     return true;
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  k_stream_up<S, RA, WPBK><<<grid_for(op.m, 28, nb, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+  k_stream_up<S, NB, RA, WPBK><<<grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.stream>>>(
       op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
 
@@ -738,31 +789,20 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
   TP_LAUNCHED(&p);
 }
 
-// Down pass of one level: Five on the fine level (op.we set), Seven on the
-// Galerkin levels (op.K / op.M set).  Ring depth RA (rows in flight ahead) and
-// warps per block are tuned per stencil; TPGPU_RA5 / TPGPU_RA7 override RA.
+// Down / up pass of one level: Five on the fine level (op.we set), Seven on
+// the Galerkin levels (op.K / op.M set).  Frequencies per warp (NB), ring
+// depth (RA rows in flight ahead) and warps per block are tuned per stencil
+// (two frequencies per warp measured slower on B200: 10.1 vs 9.2 ms per cfg-1
+// sweep -- 224 registers halve the resident warps); TPGPU_RA5 / TPGPU_RA5U
+// override the ring depths for experiments.
 void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                        const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
-                        cplx* rout, double* part) {
+                        const int* active, double om1, double om2, int nb) {
   if (op.we) {
     static const int ra = env_int("TPGPU_RA5", 6);
-    if (q) {
-      down_t<Five, true, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
-    } else if (ra == 4) {
-      down_t<Five, false, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
-    } else if (ra == 8) {
-      down_t<Five, false, 8, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
-    } else {
-      down_t<Five, false, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
-    }
+    if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    else down_t<Five, 1, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   } else {
-    static const int ra = env_int("TPGPU_RA7", 4);
-    if (ra == 2)
-      down_t<Seven, false, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb, nullptr, nullptr, nullptr, nullptr);
-    else if (ra == 6)
-      down_t<Seven, false, 6, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb, nullptr, nullptr, nullptr, nullptr);
-    else
-      down_t<Seven, false, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb, nullptr, nullptr, nullptr, nullptr);
+    down_t<Seven, 1, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   }
   TP_LAUNCHED(&p);
 }
@@ -771,16 +811,10 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
   if (op.we) {
     static const int ra = env_int("TPGPU_RA5U", 2);
-    if (ra == 4)
-      up_t<Five, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
-    else
-      up_t<Five, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    if (ra == 4) up_t<Five, 1, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else up_t<Five, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   } else {
-    static const int ra = env_int("TPGPU_RA7U", 2);
-    if (ra == 4)
-      up_t<Seven, 4, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
-    else
-      up_t<Seven, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    up_t<Seven, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   }
   TP_LAUNCHED(&p);
 }
