@@ -308,9 +308,10 @@ struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
   }
   // d v - wE vE - wW vW - wN vN - wS vS (neighbours of Dirichlet vertices are
   // zero vectors, their edge weights stay on the diagonal)
-  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx l, cplx vs, cplx v, cplx vn) {
+  // (l unused: the diagonal d from diag() carries the shift)
+  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx, cplx d, cplx vs, cplx v, cplx vn) {
     const cplx vw = shf_up(v), ve = shf_dn(v);
-    cplx acc = cm(diag(y, b, l), v);
+    cplx acc = cm(d, v);
     acc.re -= y.we * ve.re + y.ww * vw.re + y.wn * vn.re + b.wn * vs.re;
     acc.im -= y.we * ve.im + y.ww * vw.im + y.wn * vn.im + b.wn * vs.im;
     return acc;
@@ -361,11 +362,13 @@ struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, 
   static __device__ __forceinline__ cplx diag(const Reg& y, const Reg&, cplx l) { return coef(y, 0, l); }
   // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1): products formed by the owner
   // lane and shuffled one lane up
-  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx l, cplx vs, cplx v, cplx vn) {
+  // (l: the frequency's shift; d: the diagonal at this row, from diag())
+  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx l, cplx d, cplx vs, cplx v,
+                                               cplx vn) {
     const cplx cE = coef(y, 1, l), cNEs = coef(b, 3, l);
     const cplx tw = shf_up(cm(cE, v)), tsw = shf_up(cm(cNEs, vs));
     const cplx ve = shf_dn(v), vne = shf_dn(vn);
-    cplx acc = cm(coef(y, 0, l), v);
+    cplx acc = cm(d, v);
     acc = acc + cm(cE, ve);
     acc = acc + tw;
     acc = acc + cm(coef(y, 2, l), vn);
@@ -405,6 +408,11 @@ __device__ __forceinline__ Item item_rh(int m, int own, int rh, int nb, const in
 // resident warps per SM the register allocation is bounded for (0: free)
 #ifndef TPGPU_STREAM_MINW
 #define TPGPU_STREAM_MINW 0
+#endif
+// stage rows past the chunk too (no branch in the row loop; the extra rows are
+// loaded and never read)
+#ifndef TPGPU_ISSUE_ALWAYS
+#define TPGPU_ISSUE_ALWAYS 0
 #endif
 #define TP_MINB(W) (TPGPU_STREAM_MINW > 0 ? TPGPU_STREAM_MINW / (W) : 1)
 #define TP_PRAGMA(x) _Pragma(#x)
@@ -486,7 +494,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   int voff = y0 * m;  // row offset of the next vector row to stage
   int vi = 0, wi = 0; // next ring slots to fill
   auto issue = [&](int yr) {
-    if (yr <= ylast) {
+    if (TPGPU_ISSUE_ALWAYS || yr <= ylast) {
       const bool rin = colok && (unsigned)yr < (unsigned)m;
       const int off = rin ? voff : 0;
 #pragma unroll
@@ -505,10 +513,12 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   cplx b1[NB], b2[NB], b3[NB];  // z2 at yi-1, yi-2, yi-3
   cplx q2[NB], q3[NB], q4[NB];  // res at yi-2, yi-3, yi-4
   cplx id0[NB], id1[NB];        // 1/d of rows yi, yi-1
+  cplx d0[NB], d1[NB], d2[NB];  // d of rows yi, yi-1, yi-2
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     r0[j] = r1[j] = r2[j] = a0[j] = a1[j] = a2[j] = cplx{0, 0};
     b1[j] = b2[j] = b3[j] = q2[j] = q3[j] = q4[j] = id0[j] = id1[j] = cplx{0, 0};
+    d0[j] = d1[j] = d2[j] = cplx{0, 0};
   }
 #pragma unroll
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
@@ -535,12 +545,14 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
       // z1 = omega r / d at row yi (off-domain diagonals may vanish: z1 = 0 there)
       a2[j] = a1[j]; a1[j] = a0[j];
       id1[j] = id0[j];
-      id0[j] = rcp(S::diag(k0, k1, l[j]));
+      d2[j] = d1[j]; d1[j] = d0[j];
+      d0[j] = S::diag(k0, k1, l[j]);
+      id0[j] = rcp(d0[j]);
       a0[j] = in0 ? cs(om1, cm(r0[j], id0[j])) : cplx{0, 0};
       // z2 at row yi-1
       b3[j] = b2[j]; b2[j] = b1[j];
       {
-        const cplx Aa = S::apply(k1, k2, l[j], a2[j], a1[j], a0[j]);
+        const cplx Aa = S::apply(k1, k2, l[j], d1[j], a2[j], a1[j], a0[j]);
         const cplx t = cm({r1[j].re - Aa.re, r1[j].im - Aa.im}, id1[j]);
         b1[j] = in1 ? cplx{fma(om2, t.re, a1[j].re), fma(om2, t.im, a1[j].im)} : cplx{0, 0};
         if (st1 && it.on[j]) zo[j][(long)(yi - 1) * m] = b1[j];
@@ -548,7 +560,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
       // residual at row yi-2
       q4[j] = q3[j]; q3[j] = q2[j];
       {
-        const cplx Ab = S::apply(k2, k3, l[j], b3[j], b2[j], b1[j]);
+        const cplx Ab = S::apply(k2, k3, l[j], d2[j], b3[j], b2[j], b1[j]);
         q2[j] = in2 ? cplx{r2[j].re - Ab.re, r2[j].im - Ab.im} : cplx{0, 0};
       }
     }
@@ -623,7 +635,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   int voff = y0 * m;
   int vi = 0, wi = 0;
   auto issue = [&](int yr) {
-    if (yr <= ylast) {
+    if (TPGPU_ISSUE_ALWAYS || yr <= ylast) {
       const bool rin = colok && (unsigned)yr < (unsigned)m;
       const int off = rin ? voff : 0;
       // coarse vertices of the node's P1 interpolation: (A1, B1) and (A2, B2);
@@ -654,11 +666,12 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   cplx r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
   cplx e1[NB], e2[NB], e3[NB];  // z3 at yi-1, yi-2, yi-3
   cplx jd1[NB], jd2[NB];        // 1/d of rows yi-1, yi-2
+  cplx dd1[NB], dd2[NB];        // d of rows yi-1, yi-2
   double p0[NB], p1[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
     c0[j] = c1[j] = c2[j] = r0[j] = r1[j] = r2[j] = cplx{0, 0};
-    e1[j] = e2[j] = e3[j] = jd1[j] = jd2[j] = cplx{0, 0};
+    e1[j] = e2[j] = e3[j] = jd1[j] = jd2[j] = dd1[j] = dd2[j] = cplx{0, 0};
     p0[j] = p1[j] = 0;
   }
 #pragma unroll
@@ -687,15 +700,17 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
       // z3 at row yi-1
       e3[j] = e2[j]; e2[j] = e1[j];
       {
-        const cplx Ac = S::apply(k1, k2, l[j], c2[j], c1[j], c0[j]);
+        dd2[j] = dd1[j];
+        dd1[j] = S::diag(k1, k2, l[j]);
+        const cplx Ac = S::apply(k1, k2, l[j], dd1[j], c2[j], c1[j], c0[j]);
         jd2[j] = jd1[j];
-        jd1[j] = rcp(S::diag(k1, k2, l[j]));
+        jd1[j] = rcp(dd1[j]);
         const cplx t = cm({r1[j].re - Ac.re, r1[j].im - Ac.im}, jd1[j]);
         e1[j] = in1 ? cplx{fma(om2, t.re, c1[j].re), fma(om2, t.im, c1[j].im)} : cplx{0, 0};
       }
       // z4 at row yi-2
       {
-        const cplx Ae = S::apply(k2, k3, l[j], e3[j], e2[j], e1[j]);
+        const cplx Ae = S::apply(k2, k3, l[j], dd2[j], e3[j], e2[j], e1[j]);
         if (st2 && it.on[j]) {
           const cplx t = cm({r2[j].re - Ae.re, r2[j].im - Ae.im}, jd2[j]);
           const cplx z4 = {fma(om1, t.re, e2[j].re), fma(om1, t.im, e2[j].im)};
