@@ -838,9 +838,12 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
                           T* __restrict__ rho, T* __restrict__ mu, T* __restrict__ alpha,
                           T* __restrict__ beta, double* __restrict__ bn2, double* __restrict__ rn2,
                           int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask,
-                          T* __restrict__ xa) {
+                          T* __restrict__ xa, int* __restrict__ count = nullptr) {
   const int b = blockIdx.x;
   if (b >= nb) return;
+  // active-batch counter of this iteration: cleared by ST_ALPHA, summed by ST_RN
+  // (integer atomics: the count is exact whatever the block order)
+  if (count && stage == ST_ALPHA && b == 0 && threadIdx.x == 0) *count = 0;
   if (xa && threadIdx.x == 0 && (stage == ST_INIT || (stage == ST_ALPHA && !active[b]))) xa[b] = from2<T>(0.0, 0.0);
   if (stage != ST_INIT && !active[b]) return;
   double s0, s1;
@@ -866,6 +869,7 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
     case ST_RN:
       rn2[b] = s0;
       active[b] = s0 > rtol2 * bn2[b];
+      if (count && active[b]) atomicAdd(count, 1);
       break;
     case ST_BETA: {
       const T rn = from2<T>(s0, s1);
@@ -1347,17 +1351,17 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
                                                                         first, nb, g0.BB, part.get(), x, xa_ptr)));
         TP_LAUNCHED(p);
       }
+      const int slot = it & 1;
       k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
+                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
+                                      count.get() + slot);
       TP_LAUNCHED(p);
       k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr, nb,
                                              g0.BB, part.get());
       TP_LAUNCHED(p);
       k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
-      TP_LAUNCHED(p);
-      const int slot = it & 1;
-      k_count_active<<<1, 256, 0, s>>>(act, nb, count.get() + slot);
+                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
+                                      count.get() + slot);
       TP_LAUNCHED(p);
       TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
       TP_CUDA(cudaEventRecord(ev[slot], s));
