@@ -93,8 +93,25 @@ __device__ __forceinline__ cplx diag(const RowK& k, cplx l) {
   const double kc = (k.we + k.ww) + (k.wn + k.ws);
   return {fma(l.re, k.mm, kc), l.im * k.mm};
 }
+// 1/a for the smoothers' D^-1.  TPGPU_FAST_RCP: hardware reciprocal estimate
+// + one Newton step (~46 bits, no special-case path); the V-cycle stays one
+// fixed symmetric operator (every pass uses this same function), only D^-1 is
+// perturbed at the 1e-14 level.
+#ifndef TPGPU_FAST_RCP
+#define TPGPU_FAST_RCP 1
+#endif
+__device__ __forceinline__ double drcp(double x) {
+#if TPGPU_FAST_RCP
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double e = fma(-x, r, 1.0);
+  return fma(r, e, r);
+#else
+  return __drcp_rn(x);
+#endif
+}
 __device__ __forceinline__ cplx rcp(cplx a) {
-  const double d = __drcp_rn(fma(a.re, a.re, a.im * a.im));
+  const double d = drcp(fma(a.re, a.re, a.im * a.im));
   return {a.re * d, -a.im * d};
 }
 
@@ -259,61 +276,63 @@ struct WRow {  // NW coefficient doubles per lane of one staged row
 struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
   static constexpr int NW = 3;
   struct Src {
-    const double *we, *wn, *mm;  // lane column bases
-    int woff, moff, wstep, mstep, c, m;
+    const double *we, *wn, *mm;  // lane column bases (vertex column x+1 clamped to [0, c])
+    int c, m;
     bool colw, colm;
   };
-  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int y0) {
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int) {
     Src s;
     s.c = op.c;
     s.m = op.m;
     s.colw = (unsigned)(x + 1) <= (unsigned)op.c;  // vertex column X = x+1
     s.colm = x >= 0 && x < op.m;
-    s.we = op.we + (s.colw ? x + 1 : 0);
-    s.wn = op.wn + (s.colw ? x + 1 : 0);
+    const int X = min(max(x + 1, 0), op.c);
+    s.we = op.we + X;
+    s.wn = op.wn + X;
     s.mm = op.mass + xc;
-    s.wstep = op.c + 1;
-    s.mstep = op.m;
-    s.woff = (y0 + 1) * s.wstep;
-    s.moff = y0 * s.mstep;
     return s;
   }
-  // stage row yr (then advance to yr+1)
-  static __device__ __forceinline__ void stage(WRow<NW>& st, Src& s, int lane, int yr) {
+  // stage row yr; moff = (row yr clamped to [0, m)) * m, shared with the vectors
+  static __device__ __forceinline__ void stage(WRow<NW>& st, const Src& s, int lane, int yr, unsigned moff,
+                                               bool rowok) {
     const bool wv = s.colw && (unsigned)(yr + 1) <= (unsigned)s.c;
-    const bool mv = s.colm && (unsigned)yr < (unsigned)s.m;
-    cp8(&st.w[0][lane], s.we + (wv ? s.woff : 0), wv);
-    cp8(&st.w[1][lane], s.wn + (wv ? s.woff : 0), wv);
-    cp8(&st.w[2][lane], s.mm + (mv ? s.moff : 0), mv);
-    s.woff += s.wstep;
-    s.moff += s.mstep;
+    const unsigned woff = (unsigned)min(max(yr + 1, 0), s.c) * (unsigned)(s.c + 1);
+    cp8(&st.w[0][lane], s.we + woff, wv);
+    cp8(&st.w[1][lane], s.wn + woff, wv);
+    cp8(&st.w[2][lane], s.mm + moff, s.colm && rowok);
   }
-  // a row's coefficients in registers: own east/north weights, mass, and the
-  // west weight (the west lane's east weight), shuffled once per row
+  // a row's coefficients in registers: own east/north weights, mass, the west
+  // weight (the west lane's east weight, shuffled once per row) and the south
+  // weight (the north weight of the row below)
   static constexpr int RETAIN = 0;  // staged rows are read once, in their own iteration
   struct Reg {
-    double we, ww, wn, mm;
+    double we, ww, wn, ws, mm;
   };
-  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane) {
+  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane, const Reg& below) {
     Reg k;
     k.we = st.w[0][lane];
     k.wn = st.w[1][lane];
     k.mm = st.w[2][lane];
     k.ww = __shfl_up_sync(0xffffffffu, k.we, 1);
+    k.ws = below.wn;
     return k;
   }
-  static __device__ __forceinline__ cplx diag(const Reg& y, const Reg& b, cplx l) {
-    const double kc = (y.we + y.ww) + (y.wn + b.wn);
+  static __device__ __forceinline__ Reg first(const WRow<NW>& st, int lane) {
+    Reg z{0, 0, 0, 0, 0};
+    return load(st, lane, z);
+  }
+  static __device__ __forceinline__ cplx diag(const Reg& y, cplx l) {
+    const double kc = (y.we + y.ww) + (y.wn + y.ws);
     return {fma(l.re, y.mm, kc), l.im * y.mm};
   }
   // d v - wE vE - wW vW - wN vN - wS vS (neighbours of Dirichlet vertices are
   // zero vectors, their edge weights stay on the diagonal)
   // (l unused: the diagonal d from diag() carries the shift)
-  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx, cplx d, cplx vs, cplx v, cplx vn) {
+  static __device__ __forceinline__ cplx apply(const Reg& y, cplx, cplx d, cplx vs, cplx v, cplx vn) {
     const cplx vw = shf_up(v), ve = shf_dn(v);
     cplx acc = cm(d, v);
-    acc.re -= y.we * ve.re + y.ww * vw.re + y.wn * vn.re + b.wn * vs.re;
-    acc.im -= y.we * ve.im + y.ww * vw.im + y.wn * vn.im + b.wn * vs.im;
+    acc.re -= y.we * ve.re + y.ww * vw.re + y.wn * vn.re + y.ws * vs.re;
+    acc.im -= y.we * ve.im + y.ww * vw.im + y.wn * vn.im + y.ws * vs.im;
     return acc;
   }
 };
@@ -322,58 +341,58 @@ struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, 
   static constexpr int NW = 8;  // K C E N NE, M C E N NE
   struct Src {
     const double *K, *M;  // lane column bases
-    size_t n;
-    int off, m;
+    unsigned n;
     bool col;
   };
-  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int y0) {
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int) {
     Src s;
     s.K = op.K + xc;
     s.M = op.M + xc;
-    s.n = op.n;
-    s.m = op.m;
-    s.off = y0 * op.m;
+    s.n = (unsigned)op.n;
     s.col = x >= 0 && x < op.m;
     return s;
   }
-  static __device__ __forceinline__ void stage(WRow<NW>& st, Src& s, int lane, int yr) {
-    const bool v = s.col && (unsigned)yr < (unsigned)s.m;
-    const size_t o = v ? s.off : 0;
+  static __device__ __forceinline__ void stage(WRow<NW>& st, const Src& s, int lane, int, unsigned moff,
+                                               bool rowok) {
+    const bool v = s.col && rowok;
     const int dirs[4] = {SC, SE_, SN_, SNE};
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
-      cp8(&st.w[q][lane], s.K + dirs[q] * s.n + o, v);
-      cp8(&st.w[4 + q][lane], s.M + dirs[q] * s.n + o, v);
+      cp8(&st.w[q][lane], s.K + (dirs[q] * s.n + moff), v);
+      cp8(&st.w[4 + q][lane], s.M + (dirs[q] * s.n + moff), v);
     }
-    s.off += s.m;
   }
   // rows stay in the ring (8 planes are too many for register windows) and
   // are read on use: the ring retains the three rows below the current one
   static constexpr int RETAIN = 3;
   struct Reg {
-    const WRow<NW>* p;
+    const WRow<NW>* p;   // this row
+    const WRow<NW>* pb;  // the row below
     int lane;
   };
-  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane) { return {&st, lane}; }
-  static __device__ __forceinline__ cplx coef(const Reg& r, int q, cplx l) {
-    const double mm = r.p->w[4 + q][r.lane];
-    return {fma(l.re, mm, r.p->w[q][r.lane]), l.im * mm};
+  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane, const Reg& below) {
+    return {&st, below.p, lane};
   }
-  static __device__ __forceinline__ cplx diag(const Reg& y, const Reg&, cplx l) { return coef(y, 0, l); }
+  static __device__ __forceinline__ Reg first(const WRow<NW>& st, int lane) { return {&st, &st, lane}; }
+  static __device__ __forceinline__ cplx coef(const WRow<NW>* r, int q, int lane, cplx l) {
+    const double mm = r->w[4 + q][lane];
+    return {fma(l.re, mm, r->w[q][lane]), l.im * mm};
+  }
+  static __device__ __forceinline__ cplx diag(const Reg& y, cplx l) { return coef(y.p, 0, y.lane, l); }
   // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1): products formed by the owner
   // lane and shuffled one lane up
   // (l: the frequency's shift; d: the diagonal at this row, from diag())
-  static __device__ __forceinline__ cplx apply(const Reg& y, const Reg& b, cplx l, cplx d, cplx vs, cplx v,
-                                               cplx vn) {
-    const cplx cE = coef(y, 1, l), cNEs = coef(b, 3, l);
+  static __device__ __forceinline__ cplx apply(const Reg& y, cplx l, cplx d, cplx vs, cplx v, cplx vn) {
+    const int ln = y.lane;
+    const cplx cE = coef(y.p, 1, ln, l), cNEs = coef(y.pb, 3, ln, l);
     const cplx tw = shf_up(cm(cE, v)), tsw = shf_up(cm(cNEs, vs));
     const cplx ve = shf_dn(v), vne = shf_dn(vn);
     cplx acc = cm(d, v);
     acc = acc + cm(cE, ve);
     acc = acc + tw;
-    acc = acc + cm(coef(y, 2, l), vn);
-    acc = acc + cm(coef(b, 2, l), vs);
-    acc = acc + cm(coef(y, 3, l), vne);
+    acc = acc + cm(coef(y.p, 2, ln, l), vn);
+    acc = acc + cm(coef(y.pb, 2, ln, l), vs);
+    acc = acc + cm(coef(y.p, 3, ln, l), vne);
     acc = acc + tsw;
     return acc;
   }
@@ -413,6 +432,10 @@ __device__ __forceinline__ Item item_rh(int m, int own, int rh, int nb, const in
 // loaded and never read)
 #ifndef TPGPU_ISSUE_ALWAYS
 #define TPGPU_ISSUE_ALWAYS 0
+#endif
+// restriction shuffles on every row (no divergent-shuffle fallback paths)
+#ifndef TPGPU_RESTRICT_SHFL_ALWAYS
+#define TPGPU_RESTRICT_SHFL_ALWAYS 0
 #endif
 #define TP_MINB(W) (TPGPU_STREAM_MINW > 0 ? TPGPU_STREAM_MINW / (W) : 1)
 #define TP_PRAGMA(x) _Pragma(#x)
@@ -490,17 +513,16 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 3, ylast = ye + 2;  // staged rows
   const bool cown = own && (x & 1) && (x >> 1) < mc;  // coarse centre column
-  typename S::Src src = S::src(op, x, xc, y0);
-  int voff = y0 * m;  // row offset of the next vector row to stage
+  const typename S::Src src = S::src(op, x, xc, y0);
   int vi = 0, wi = 0; // next ring slots to fill
+  // stage row yr (rows outside [0, m) read row 0 / m-1 addresses and are zero-filled)
   auto issue = [&](int yr) {
     if (TPGPU_ISSUE_ALWAYS || yr <= ylast) {
-      const bool rin = colok && (unsigned)yr < (unsigned)m;
-      const int off = rin ? voff : 0;
+      const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
+      const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
 #pragma unroll
       for (int j = 0; j < NB; ++j) cp16(&vring[vi].v[j][lane], rp[j] + off, rin);
-      S::stage(wring[wi], src, lane, yr);
-      voff += m;
+      S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
     }
@@ -526,15 +548,15 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   // are never used: they repeat row y0)
   int vr = 0, sr = 0;  // ring slots of row yi
   cp_wait<RA>();
-  typename S::Reg k0 = S::load(wring[0], lane), k1 = k0, k2 = k0, k3 = k0;
+  typename S::Reg k0 = S::first(wring[0], lane), k1 = k0, k2 = k0;  // rows yi, yi-1, yi-2
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 2; yi <= ylast; ++yi) {
     issue(yi + RA);
     vr = wrap_inc(vr, RV);
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
-    k3 = k2; k2 = k1; k1 = k0;
-    k0 = S::load(wring[sr], lane);
+    k2 = k1; k1 = k0;
+    k0 = S::load(wring[sr], lane, k1);
     const bool in0 = colok && (unsigned)yi < (unsigned)m;
     const bool in1 = colok && (unsigned)(yi - 1) < (unsigned)m;
     const bool in2 = colok && (unsigned)(yi - 2) < (unsigned)m;
@@ -546,13 +568,13 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
       a2[j] = a1[j]; a1[j] = a0[j];
       id1[j] = id0[j];
       d2[j] = d1[j]; d1[j] = d0[j];
-      d0[j] = S::diag(k0, k1, l[j]);
+      d0[j] = S::diag(k0, l[j]);
       id0[j] = rcp(d0[j]);
       a0[j] = in0 ? cs(om1, cm(r0[j], id0[j])) : cplx{0, 0};
       // z2 at row yi-1
       b3[j] = b2[j]; b2[j] = b1[j];
       {
-        const cplx Aa = S::apply(k1, k2, l[j], d1[j], a2[j], a1[j], a0[j]);
+        const cplx Aa = S::apply(k1, l[j], d1[j], a2[j], a1[j], a0[j]);
         const cplx t = cm({r1[j].re - Aa.re, r1[j].im - Aa.im}, id1[j]);
         b1[j] = in1 ? cplx{fma(om2, t.re, a1[j].re), fma(om2, t.im, a1[j].im)} : cplx{0, 0};
         if (st1 && it.on[j]) zo[j][(long)(yi - 1) * m] = b1[j];
@@ -560,18 +582,22 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
       // residual at row yi-2
       q4[j] = q3[j]; q3[j] = q2[j];
       {
-        const cplx Ab = S::apply(k2, k3, l[j], d2[j], b3[j], b2[j], b1[j]);
+        const cplx Ab = S::apply(k2, l[j], d2[j], b3[j], b2[j], b1[j]);
         q2[j] = in2 ? cplx{r2[j].re - Ab.re, r2[j].im - Ab.im} : cplx{0, 0};
       }
     }
     // restriction centred on row yc = yi-3 (odd fine rows 2Y+1; warp-uniform branch)
     const int yc = yi - 3;
+#if TPGPU_RESTRICT_SHFL_ALWAYS
+    {
+#else
     if ((yc & 1) && yc >= ys && yc < ye) {
+#endif
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
         const cplx qw = shf_up(q3[j]), qe = shf_dn(q3[j]);
         const cplx q4w = shf_up(q4[j]), q2e = shf_dn(q2[j]);
-        if (cown && it.on[j] && (yc >> 1) < mc) {
+        if ((yc & 1) && yc >= ys && yc < ye && cown && it.on[j] && (yc >> 1) < mc) {
           cplx acc = q3[j];
           acc.re += 0.5 * (qw.re + qe.re + q4[j].re + q2[j].re + q4w.re + q2e.re);
           acc.im += 0.5 * (qw.im + qe.im + q4[j].im + q2[j].im + q4w.im + q2e.im);
@@ -631,13 +657,12 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   const bool ao = a & 1;
   const int A2 = ao ? ah + 1 : ah;
   const bool cA1 = colok && ah >= 1 && ah <= mc, cA2 = colok && A2 >= 1 && A2 <= mc;
-  typename S::Src src = S::src(op, x, xc, y0);
-  int voff = y0 * m;
+  const typename S::Src src = S::src(op, x, xc, y0);
   int vi = 0, wi = 0;
   auto issue = [&](int yr) {
     if (TPGPU_ISSUE_ALWAYS || yr <= ylast) {
-      const bool rin = colok && (unsigned)yr < (unsigned)m;
-      const int off = rin ? voff : 0;
+      const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
+      const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
       // coarse vertices of the node's P1 interpolation: (A1, B1) and (A2, B2);
       // the second is absent at coincident vertices
       const int bb = yr + 1, bh = bb >> 1;
@@ -645,7 +670,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
       const bool has2 = ao || (bb & 1);
       const bool ok1 = rin && cA1 && bh >= 1 && bh <= mc;
       const bool ok2 = rin && has2 && cA2 && B2 >= 1 && B2 <= mc;
-      const int c1 = ok1 ? (bh - 1) * mc + (ah - 1) : 0, c2 = ok2 ? (B2 - 1) * mc + (A2 - 1) : 0;
+      const unsigned c1 = ok1 ? (bh - 1) * mc + (ah - 1) : 0, c2 = ok2 ? (B2 - 1) * mc + (A2 - 1) : 0;
       VRow<4 * NB>& sv = vring[vi];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
@@ -654,8 +679,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
         cp16(&sv.v[4 * j + 2][lane], xb[j] + c1, ok1);
         cp16(&sv.v[4 * j + 3][lane], xb[j] + c2, ok2);
       }
-      S::stage(wring[wi], src, lane, yr);
-      voff += m;
+      S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
     }
@@ -678,7 +702,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
   int vr = 0, sr = 0;
   cp_wait<RA>();
-  typename S::Reg k0 = S::load(wring[0], lane), k1 = k0, k2 = k0, k3 = k0;  // rows yi .. yi-3
+  typename S::Reg k0 = S::first(wring[0], lane), k1 = k0, k2 = k0;  // rows yi, yi-1, yi-2
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 2; yi <= ylast; ++yi) {
     issue(yi + RA);
@@ -687,8 +711,8 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
     cp_wait<RA>();
     const VRow<4 * NB>& sv = vring[vr];
     const double wc1 = (!ao && !((yi + 1) & 1)) ? 1.0 : 0.5;
-    k3 = k2; k2 = k1; k1 = k0;
-    k0 = S::load(wring[sr], lane);
+    k2 = k1; k1 = k0;
+    k0 = S::load(wring[sr], lane, k1);
     const bool in1 = colok && (unsigned)(yi - 1) < (unsigned)m;
     const bool st2 = own && yi - 2 >= ys && yi - 2 < ye;
 #pragma unroll
@@ -701,8 +725,8 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
       e3[j] = e2[j]; e2[j] = e1[j];
       {
         dd2[j] = dd1[j];
-        dd1[j] = S::diag(k1, k2, l[j]);
-        const cplx Ac = S::apply(k1, k2, l[j], dd1[j], c2[j], c1[j], c0[j]);
+        dd1[j] = S::diag(k1, l[j]);
+        const cplx Ac = S::apply(k1, l[j], dd1[j], c2[j], c1[j], c0[j]);
         jd2[j] = jd1[j];
         jd1[j] = rcp(dd1[j]);
         const cplx t = cm({r1[j].re - Ac.re, r1[j].im - Ac.im}, jd1[j]);
@@ -710,7 +734,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
       }
       // z4 at row yi-2
       {
-        const cplx Ae = S::apply(k2, k3, l[j], dd2[j], e3[j], e2[j], e1[j]);
+        const cplx Ae = S::apply(k2, l[j], dd2[j], e3[j], e2[j], e1[j]);
         if (st2 && it.on[j]) {
           const cplx t = cm({r2[j].re - Ae.re, r2[j].im - Ae.im}, jd2[j]);
           const cplx z4 = {fma(om1, t.re, e2[j].re), fma(om1, t.im, e2[j].im)};

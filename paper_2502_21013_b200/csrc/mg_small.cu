@@ -27,8 +27,13 @@ constexpr int SNT = 1024;  // threads per block (one block per frequency)
 __device__ __forceinline__ cplx cmul(cplx a, cplx b) {
   return {fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
 }
+// 1/a from the hardware reciprocal estimate + one Newton step (as mg_fine.cu's
+// smoothers: the V-cycle only needs a fixed D^-1, not a correctly rounded one)
 __device__ __forceinline__ cplx crcp(cplx a) {
-  const double d = 1.0 / fma(a.re, a.re, a.im * a.im);
+  const double x = fma(a.re, a.re, a.im * a.im);
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  const double d = fma(r, fma(-x, r, 1.0), r);
   return {a.re * d, -a.im * d};
 }
 
