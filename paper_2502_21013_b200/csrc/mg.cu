@@ -54,6 +54,18 @@ __device__ __forceinline__ cplx inv_of(cplx a) {
   return {a.re * d, -a.im * d};
 }
 __device__ __forceinline__ double inv_of(double a) { return 1.0 / a; }
+// smoother D^-1: hardware reciprocal estimate + one Newton step (~46 bits, no
+// special-case path; the V-cycle only needs a fixed diagonal scaling)
+__device__ __forceinline__ double fast_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  return fma(r, fma(-x, r, 1.0), r);
+}
+__device__ __forceinline__ cplx sinv(cplx a) {
+  const double d = fast_rcp(fma(a.re, a.re, a.im * a.im));
+  return {a.re * d, -a.im * d};
+}
+__device__ __forceinline__ double sinv(double a) { return fast_rcp(a); }
 __device__ __forceinline__ cplx axpy_r(double k, cplx v, cplx acc) { return {fma(k, v.re, acc.re), fma(k, v.im, acc.im)}; }
 
 // Level operator.  MODE 0: lambda_b M + K with shared stencils; MODE 1:
@@ -417,7 +429,7 @@ __global__ void __launch_bounds__(NT, 4) k_update(Op<MODE> op, TT<MODE>* __restr
       const T rj = r[j] - mul(al, q[j]);
       r[j] = rj;
       v0 = norm2(rj);
-      if (z) z[j] = omega * mul(rj, inv_of(diag_global<MODE>(op, b, i)));
+      if (z) z[j] = omega * mul(rj, sinv(diag_global<MODE>(op, b, i)));
     }
     block_pair(v0, 0.0, part, b);
     __syncthreads();
@@ -605,9 +617,9 @@ __global__ void __launch_bounds__(NT, 4) k_down(Op<MODE> op, Op<MODE> opc, const
       T v;
       if constexpr (SM == SM_RB) {
         const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
-        v = red ? mul(sR[k], inv_of(d)) : zero_of(T{});
+        v = red ? mul(sR[k], sinv(d)) : zero_of(T{});
       } else {
-        v = omega * mul(sR[k], inv_of(d));
+        v = omega * mul(sR[k], sinv(d));
       }
       sZ[k] = v;
     }
@@ -621,13 +633,13 @@ __global__ void __launch_bounds__(NT, 4) k_down(Op<MODE> op, Op<MODE> opc, const
       T v;
       if constexpr (SM == SM_RB) {
         const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
-        v = red ? sZ[h] : mul(sR[h] - off, inv_of(d));
+        v = red ? sZ[h] : mul(sR[h] - off, sinv(d));
       } else if constexpr (SM == SM_J1) {
         (void)d;
         (void)off;
         v = sZ[h];
       } else {
-        v = sZ[h] + omega2 * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
+        v = sZ[h] + omega2 * mul(sR[h] - off - mul(d, sZ[h]), sinv(d));
       }
       sW[h] = v;
     }
@@ -733,13 +745,13 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
       T v;
       if constexpr (SM == SM_RB) {
         const int red = ((x0 - 2 + lx + y0 - 2 + ly) & 1) == 0;
-        v = red ? sZ[h] : mul(sR[h] - off, inv_of(d));
+        v = red ? sZ[h] : mul(sR[h] - off, sinv(d));
       } else if constexpr (SM == SM_J1) {
         (void)d;
         (void)off;
         v = sZ[h];
       } else {
-        v = sZ[h] + omega2 * mul(sR[h] - off - mul(d, sZ[h]), inv_of(d));
+        v = sZ[h] + omega2 * mul(sR[h] - off - mul(d, sZ[h]), sinv(d));
       }
       sW[h] = v;
     }
@@ -755,9 +767,9 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
         T v;
         if constexpr (SM == SM_RB) {
           const int red = ((gx + gy) & 1) == 0;
-          v = red ? mul(sR[h] - off, inv_of(d)) : sW[h];
+          v = red ? mul(sR[h] - off, sinv(d)) : sW[h];
         } else {
-          v = sW[h] + omega * mul(sR[h] - off - mul(d, sW[h]), inv_of(d));
+          v = sW[h] + omega * mul(sR[h] - off - mul(d, sW[h]), sinv(d));
         }
         zout[(size_t)b * n + gy * m + gx] = v;
         if (dot) add_dot(vd, sR[h], v);

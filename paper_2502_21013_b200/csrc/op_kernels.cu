@@ -15,6 +15,16 @@
 
 namespace tpgpu {
 
+// 1/x to full double precision without the special-case path of the correctly
+// rounded reciprocal: hardware estimate + two Newton steps (x > 0 normal here:
+// s^2 + Bs^2 with Bs > 0)
+__device__ __forceinline__ double acc_rcp(double x) {
+  double r;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(x));
+  r = fma(r, fma(-x, r, 1.0), r);
+  return fma(r, fma(-x, r, 1.0), r);
+}
+
 namespace {
 
 constexpr int TX = 32, TY = 8;
@@ -23,7 +33,7 @@ __device__ __forceinline__ double nu_of(const MaterialDev& mt, double s2) {
   if (mt.linear) return mt.nu0;
   // s2/(s2+Bs^2) with a correctly rounded reciprocal (one more rounding than
   // the reference's division: ~1 ulp, far below the 1e-13 K(u) parity bar)
-  return fma(mt.nu_inf - mt.nu0, s2 * __drcp_rn(s2 + mt.bs2), mt.nu0);
+  return fma(mt.nu_inf - mt.nu0, s2 * acc_rcp(s2 + mt.bs2), mt.nu0);
 }
 
 // Shared-memory tile: vertices [x0, x0+TX+1] x [y0, y0+TY+1] (vertex coords),
@@ -289,7 +299,7 @@ __global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
       for (int t = 0; t < 6; ++t) {
         const int cx = lx + cxs[t], cy = ly + cys[t];
         const double s2 = c2 * (dx[t] * dx[t] + dy[t] * dy[t]);
-        const double nu = fma(cdnu[cy][cx], s2 * __drcp_rn(s2 + cbs2[cy][cx]), cnu0[cy][cx]);
+        const double nu = fma(cdnu[cy][cx], s2 * acc_rcp(s2 + cbs2[cy][cx]), cnu0[cy][cx]);
         ku = fma(0.5 * nu, con[t], ku);
         if (WANT_G) kh = fma(chat[cy][cx], con[t], kh);
       }
