@@ -305,6 +305,7 @@ struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
   // weight (the west lane's east weight, shuffled once per row) and the south
   // weight (the north weight of the row below)
   static constexpr int RETAIN = 0;  // staged rows are read once, in their own iteration
+  static constexpr bool XLANE = false;
   struct Reg {
     double we, ww, wn, ws, mm;
   };
@@ -379,22 +380,29 @@ struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, 
     return {fma(l.re, mm, r->w[q][lane]), l.im * mm};
   }
   static __device__ __forceinline__ cplx diag(const Reg& y, cplx l) { return coef(y.p, 0, y.lane, l); }
-  // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1): products formed by the owner
-  // lane and shuffled one lane up
-  // (l: the frequency's shift; d: the diagonal at this row, from diag())
+  // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1).  Split form
+  //   sum_d (K_d + l M_d) v_d = sum_d K_d v_d + l sum_d M_d v_d
+  // (real x complex products, one complex multiply by l at the end); the
+  // west lane's E / NE coefficients are read from its ring slot (XLANE: the
+  // kernels __syncwarp after each ring wait, so every lane's copies are visible).
+  static constexpr bool XLANE = true;
   static __device__ __forceinline__ cplx apply(const Reg& y, cplx l, cplx d, cplx vs, cplx v, cplx vn) {
-    const int ln = y.lane;
-    const cplx cE = coef(y.p, 1, ln, l), cNEs = coef(y.pb, 3, ln, l);
-    const cplx tw = shf_up(cm(cE, v)), tsw = shf_up(cm(cNEs, vs));
-    const cplx ve = shf_dn(v), vne = shf_dn(vn);
-    cplx acc = cm(d, v);
-    acc = acc + cm(cE, ve);
-    acc = acc + tw;
-    acc = acc + cm(coef(y.p, 2, ln, l), vn);
-    acc = acc + cm(coef(y.pb, 2, ln, l), vs);
-    acc = acc + cm(coef(y.p, 3, ln, l), vne);
-    acc = acc + tsw;
-    return acc;
+    const int ln = y.lane, lw = ln > 0 ? ln - 1 : 0;
+    const cplx vw = shf_up(v), ve = shf_dn(v), vne = shf_dn(vn), vsw = shf_up(vs);
+    const WRow<NW>& a = *y.p;
+    const WRow<NW>& b = *y.pb;
+    // K and M coefficients of E, W, N, S, NE, SW
+    const double kE = a.w[1][ln], kW = a.w[1][lw], kN = a.w[2][ln], kS = b.w[2][ln], kNE = a.w[3][ln],
+                 kSW = b.w[3][lw];
+    const double mE = a.w[5][ln], mW = a.w[5][lw], mN = a.w[6][ln], mS = b.w[6][ln], mNE = a.w[7][ln],
+                 mSW = b.w[7][lw];
+    cplx sk, sm;
+    sk.re = kE * ve.re + kW * vw.re + kN * vn.re + kS * vs.re + kNE * vne.re + kSW * vsw.re;
+    sk.im = kE * ve.im + kW * vw.im + kN * vn.im + kS * vs.im + kNE * vne.im + kSW * vsw.im;
+    sm.re = mE * ve.re + mW * vw.re + mN * vn.re + mS * vs.re + mNE * vne.re + mSW * vsw.re;
+    sm.im = mE * ve.im + mW * vw.im + mN * vn.im + mS * vs.im + mNE * vne.im + mSW * vsw.im;
+    const cplx dv = cm(d, v), lm = cm(l, sm);
+    return {dv.re + sk.re + lm.re, dv.im + sk.im + lm.im};
   }
 };
 
@@ -548,6 +556,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   // are never used: they repeat row y0)
   int vr = 0, sr = 0;  // ring slots of row yi
   cp_wait<RA>();
+  if (S::XLANE) __syncwarp();
   typename S::Reg k0 = S::first(wring[0], lane), k1 = k0, k2 = k0;  // rows yi, yi-1, yi-2
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 2; yi <= ylast; ++yi) {
@@ -555,6 +564,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
     vr = wrap_inc(vr, RV);
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
+    if (S::XLANE) __syncwarp();
     k2 = k1; k1 = k0;
     k0 = S::load(wring[sr], lane, k1);
     const bool in0 = colok && (unsigned)yi < (unsigned)m;
@@ -702,6 +712,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
   int vr = 0, sr = 0;
   cp_wait<RA>();
+  if (S::XLANE) __syncwarp();
   typename S::Reg k0 = S::first(wring[0], lane), k1 = k0, k2 = k0;  // rows yi, yi-1, yi-2
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 2; yi <= ylast; ++yi) {
@@ -709,6 +720,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
     vr = wrap_inc(vr, RV);
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
+    if (S::XLANE) __syncwarp();
     const VRow<4 * NB>& sv = vring[vr];
     const double wc1 = (!ao && !((yi + 1) & 1)) ? 1.0 : 0.5;
     k2 = k1; k1 = k0;
@@ -775,7 +787,9 @@ dim3 grid_for(int m, int own, int nb, int rh = RH, int wpb = WPB) {
 // halo rows, short ones give the small grids enough warps
 int rh_for(int m) {
   static const int env = std::getenv("TPGPU_RH") ? std::atoi(std::getenv("TPGPU_RH")) : 0;
+  static const int env1 = std::getenv("TPGPU_RH1") ? std::atoi(std::getenv("TPGPU_RH1")) : 0;
   if (env > 0 && m >= 200) return env;
+  if (env1 > 0 && m >= 100 && m < 200) return env1;
   return m >= 200 ? 64 : m >= 100 ? 32 : m >= 50 ? 16 : 8;
 }
 
@@ -841,7 +855,11 @@ void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, c
     if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
     else down_t<Five, 1, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   } else {
-    down_t<Seven, 1, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    static const int ra = env_int("TPGPU_RA7", 2), w = env_int("TPGPU_WPB7", 2);
+    if (ra == 4) down_t<Seven, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    else if (w == 4) down_t<Seven, 1, 2, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    else if (w == 1) down_t<Seven, 1, 2, 1>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    else down_t<Seven, 1, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   }
   TP_LAUNCHED(&p);
 }
@@ -853,7 +871,11 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
     if (ra == 4) up_t<Five, 1, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else up_t<Five, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   } else {
-    up_t<Seven, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    static const int ra = env_int("TPGPU_RA7U", 2), w = env_int("TPGPU_WPB7", 2);
+    if (ra == 4) up_t<Seven, 1, 4, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else if (w == 4) up_t<Seven, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else if (w == 1) up_t<Seven, 1, 2, 1>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else up_t<Seven, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   }
   TP_LAUNCHED(&p);
 }

@@ -48,18 +48,26 @@ __device__ __forceinline__ cplx coefc(const Lvl& L, int dir, int i, cplx l) {
   return {fma(l.re, mm, k), l.im * mm};
 }
 
-// diagonal and off-diagonal part of (lambda M + K) v at node (x, y); v in shared memory
+// diagonal and off-diagonal part of (lambda M + K) v at node (x, y); v in
+// shared memory.  Off-diagonal part in split form sum K_d v_d + l sum M_d v_d.
 __device__ __forceinline__ void stencil(const Lvl& L, int x, int y, cplx l, const cplx* v, cplx& d, cplx& off) {
   const int m = L.m, i = y * m + x;
   d = coefc(L, SC, i, l);
-  cplx acc{0, 0};
-  if (x + 1 < m) acc = acc + cmul(coefc(L, SE_, i, l), v[i + 1]);
-  if (x > 0) acc = acc + cmul(coefc(L, SE_, i - 1, l), v[i - 1]);
-  if (y + 1 < m) acc = acc + cmul(coefc(L, SN_, i, l), v[i + m]);
-  if (y > 0) acc = acc + cmul(coefc(L, SN_, i - m, l), v[i - m]);
-  if (x + 1 < m && y + 1 < m) acc = acc + cmul(coefc(L, SNE, i, l), v[i + m + 1]);
-  if (x > 0 && y > 0) acc = acc + cmul(coefc(L, SNE, i - m - 1, l), v[i - m - 1]);
-  off = acc;
+  cplx sk{0, 0}, sm{0, 0};
+  auto add = [&](int dir, int at, cplx vv) {
+    const double k = __ldg(L.K + (size_t)dir * L.n + at), mm = __ldg(L.M + (size_t)dir * L.n + at);
+    sk.re = fma(k, vv.re, sk.re);
+    sk.im = fma(k, vv.im, sk.im);
+    sm.re = fma(mm, vv.re, sm.re);
+    sm.im = fma(mm, vv.im, sm.im);
+  };
+  if (x + 1 < m) add(SE_, i, v[i + 1]);
+  if (x > 0) add(SE_, i - 1, v[i - 1]);
+  if (y + 1 < m) add(SN_, i, v[i + m]);
+  if (y > 0) add(SN_, i - m, v[i - m]);
+  if (x + 1 < m && y + 1 < m) add(SNE, i, v[i + m + 1]);
+  if (x > 0 && y > 0) add(SNE, i - m - 1, v[i - m - 1]);
+  off = sk + cmul(l, sm);
 }
 
 // z_out = z_in + w (b - A z_in) / d  (z_in == nullptr: z_out = w b / d)
