@@ -1314,9 +1314,9 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const int per_t = g0.tiles;
   const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
   const int per_u = fine ? fine_partials(ops[0].m, 2) : per_t;   // V-cycle dot (up)
-  // the smem-tile apply (FAM 1 reads the stored 5-point stencil) keeps more
-  // loads in flight than the streaming one on B200 (measured 102 vs 122 us at cfg 1)
-  static const bool use_stream_apply = std::getenv("TPGPU_STREAM_APPLY") != nullptr;
+  // fine level: the ring-staged streaming apply (mg_fine.cu) -- measured 8.08
+  // vs 8.39 ms per cfg-1 sweep against the smem-tile apply (TPGPU_TILE_APPLY)
+  static const bool use_stream_apply = std::getenv("TPGPU_TILE_APPLY") == nullptr;
   const bool sapply = fine && use_stream_apply;
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();

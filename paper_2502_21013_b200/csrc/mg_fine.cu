@@ -162,78 +162,6 @@ struct RowPtr {
   }
 };
 
-// ---------------------------------------------------------------- apply
-// INIT = 0: p = first ? z : z + beta p_in -> p_out ; q = A p ; part += p^T q
-// INIT = 1: r = b - A x (b in z, x in pin, r to q) ; part += (|b|^2, |r|^2)
-template <int INIT>
-__global__ void __launch_bounds__(WL * WPB, 6) k_fine_apply(FineOp op, const cplx* __restrict__ z,
-                                                            const cplx* __restrict__ pin, cplx* __restrict__ pout,
-                                                            cplx* __restrict__ q, const cplx* __restrict__ beta,
-                                                            const int* __restrict__ active, int first, int nb,
-                                                            double* __restrict__ part) {
-  constexpr int H = 1, OWN = WL - 2 * H;
-  const int m = op.m;
-  const Item it = item_of(m, OWN, nb, INIT ? nullptr : active);
-  if (!it.ok) return;
-  const int lane = threadIdx.x & 31;
-  const int x = it.xs - H + lane;
-  const bool colok = x >= 0 && x < m;
-  const bool own = lane >= H && lane < WL - H && colok;
-  const int xc = min(max(x, 0), m - 1);
-  const size_t o = (size_t)it.b * op.n;
-  const RowPtr Z{z + o + xc, m, colok}, P{pin + o + xc, m, colok};
-  cplx* const po = pout + o + xc;
-  cplx* const qo = q + o + xc;
-  const cplx l = op.lam[it.b];
-  const cplx bt = (INIT || first) ? cplx{0, 0} : beta[it.b];
-  auto pval = [&](int y) -> cplx {
-    if (INIT) return P.at(y);  // x (solution) for the residual
-    cplx v = Z.at(y);
-    if (!first) {
-      const cplx pp = P.at(y);
-      v = {fma(bt.re, pp.re, fma(-bt.im, pp.im, v.re)), fma(bt.re, pp.im, fma(bt.im, pp.re, v.im))};
-    }
-    return v;
-  };
-  double wnp = wn_of(op, x, it.ys - 1);
-  cplx pm = pval(it.ys - 1), p0 = pval(it.ys), pn = pval(it.ys + 1);
-  double s0 = 0, s1 = 0;
-  for (int y = it.ys; y < it.ye; ++y) {
-    const cplx pnn = pval(y + 2);  // next row in flight during this row's math
-    const RowK k = row_k(op, x, y, wnp);
-    wnp = k.wn;
-    const cplx pw = shf_up(p0), pe = shf_dn(p0);
-    const cplx Ap = apply_at(k, l, p0, pw, pe, pm, pn);
-    if (own) {
-      const long i = (long)y * m;
-      if (INIT) {
-        const cplx bi = Z.p[i];
-        const cplx r = {bi.re - Ap.re, bi.im - Ap.im};
-        qo[i] = r;
-        s0 += bi.re * bi.re + bi.im * bi.im;
-        s1 += r.re * r.re + r.im * r.im;
-      } else {
-        po[i] = p0;
-        qo[i] = Ap;
-        const cplx t = cm(p0, Ap);
-        s0 += t.re;
-        s1 += t.im;
-      }
-    }
-    pm = p0;
-    p0 = pn;
-    pn = pnn;
-  }
-  warp_pair(s0, s1);
-  if (lane == 0) {
-    const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
-    const size_t per = (size_t)ns * nch;
-    const size_t k = (size_t)it.b * per + (size_t)it.chunk * ns + it.strip;
-    part[2 * k] = s0;
-    part[2 * k + 1] = s1;
-  }
-}
-
 // ---------------------------------------------------------------- async row ring
 // The down/up passes walk rows with a long dependent chain per row (two
 // stencil applications, a complex reciprocal, shuffles), so a row load issued
@@ -776,6 +704,112 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   }
 }
 
+// ---------------------------------------------------------------- apply
+// INIT = 0: p = first ? z : z + beta p_in -> p_out ; q = A p ; part += p^T q
+// INIT = 1: r = b - A x (b in z, x in pin, r to q) ; part += (|b|^2, |r|^2)
+// One fine-level stencil per node: rows of z and p_in staged through the
+// ring, p formed at row yi, q (and the stored p) at row yi-1.
+template <int INIT, int RA, int WPBK>
+__global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cplx* __restrict__ z,
+                                                            const cplx* __restrict__ pin, cplx* __restrict__ pout,
+                                                            cplx* __restrict__ q, const cplx* __restrict__ beta,
+                                                            const int* __restrict__ active, int first, int nb,
+                                                            double* __restrict__ part) {
+  using S = Five;
+  constexpr int H = 1, OWN = WL - 2 * H;  // 30
+  constexpr int RV = RA + 2, RC = RA + 2;
+  extern __shared__ __align__(16) unsigned char fine_smem[];
+  const int m = op.m;
+  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RH, nb, INIT ? nullptr : active);
+  if (!it.ok) return;
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
+  VRow<2>* const vring = reinterpret_cast<VRow<2>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<2>)) + wib * RC;
+  const int x = it.xs - H + lane;
+  const bool colok = x >= 0 && x < m;
+  const bool own = lane >= H && lane < WL - H && colok;
+  const int xc = min(max(x, 0), m - 1);
+  const int b = it.b[0];
+  const size_t o = (size_t)b * op.n;
+  const cplx* const zp = z + o + xc;
+  const cplx* const pp = pin + o + xc;
+  cplx* const po = pout + o + xc;
+  cplx* const qo = q + o + xc;
+  const cplx l = op.lam[b];
+  const bool usep = INIT || !first;  // p_in is read
+  const cplx bt = (INIT || first) ? cplx{0, 0} : beta[b];
+  const int ys = it.ys, ye = it.ye;
+  const int y0 = ys - 2, ylast = ye;  // staged rows
+  const S::Src src = S::src(op, x, xc, y0);
+  int vi = 0, wi = 0;
+  auto issue = [&](int yr) {
+    if (yr <= ylast) {
+      const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
+      const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
+      cp16(&vring[vi].v[0][lane], zp + off, rin);
+      cp16(&vring[vi].v[1][lane], pp + off, rin && usep);
+      S::stage(wring[wi], src, lane, yr, off, rowok);
+      vi = wrap_inc(vi, RV);
+      wi = wrap_inc(wi, RC);
+    }
+    cp_commit();
+  };
+#pragma unroll
+  for (int j = 0; j <= RA; ++j) issue(y0 + j);
+  int vr = 0, sr = 0;
+  cp_wait<RA>();
+  S::Reg k0 = S::first(wring[0], lane), k1 = k0;  // rows yi, yi-1
+  // p at rows yi, yi-1, yi-2; b (INIT) at rows yi, yi-1
+  cplx p0 = (INIT) ? vring[0].v[1][lane] : cplx{0, 0}, p1{0, 0}, p2{0, 0};
+  if (!INIT) {
+    const cplx zz = vring[0].v[0][lane], pv = vring[0].v[1][lane];
+    p0 = {fma(bt.re, pv.re, fma(-bt.im, pv.im, zz.re)), fma(bt.re, pv.im, fma(bt.im, pv.re, zz.im))};
+  }
+  cplx b0 = vring[0].v[0][lane], b1{0, 0};
+  double s0 = 0, s1 = 0;
+  TP_UNROLL(TPGPU_STREAM_UNROLL)
+  for (int yi = ys - 1; yi <= ylast; ++yi) {
+    issue(yi + RA);
+    vr = wrap_inc(vr, RV);
+    sr = wrap_inc(sr, RC);
+    cp_wait<RA>();
+    k1 = k0;
+    k0 = S::load(wring[sr], lane, k1);
+    const cplx zz = vring[vr].v[0][lane], pv = vring[vr].v[1][lane];
+    p2 = p1; p1 = p0;
+    b1 = b0; b0 = zz;
+    p0 = INIT ? pv
+              : cplx{fma(bt.re, pv.re, fma(-bt.im, pv.im, zz.re)), fma(bt.re, pv.im, fma(bt.im, pv.re, zz.im))};
+    // q at row yi-1
+    const cplx Ap = S::apply(k1, l, S::diag(k1, l), p2, p1, p0);
+    const int y = yi - 1;
+    if (own && y >= ys && y < ye) {
+      const long i = (long)y * m;
+      if (INIT) {
+        const cplx r = {b1.re - Ap.re, b1.im - Ap.im};
+        qo[i] = r;
+        s0 += b1.re * b1.re + b1.im * b1.im;
+        s1 += r.re * r.re + r.im * r.im;
+      } else {
+        po[i] = p1;
+        qo[i] = Ap;
+        const cplx t = cm(p1, Ap);
+        s0 += t.re;
+        s1 += t.im;
+      }
+    }
+  }
+  cp_wait<0>();
+  warp_pair(s0, s1);
+  if (lane == 0) {
+    const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
+    const size_t per = (size_t)ns * nch;
+    const size_t k = (size_t)b * per + (size_t)it.chunk * ns + it.strip;
+    part[2 * k] = s0;
+    part[2 * k + 1] = s1;
+  }
+}
+
 int items_per_batch(int m, int own, int rh = RH) { return ((m + own - 1) / own) * ((m + rh - 1) / rh); }
 
 dim3 grid_for(int m, int own, int nb, int rh = RH, int wpb = WPB) {
@@ -834,11 +868,19 @@ int fine_partials(int m, int kind) {
 
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init) {
-  const dim3 g = grid_for(op.m, 30, nb);
+  constexpr int RA = 4, W = 4;
+  constexpr size_t sm = (size_t)W * ((RA + 2) * sizeof(VRow<2>) + (RA + 2) * sizeof(WRow<Five::NW>));
+  static bool attrs = [] {
+    cudaFuncSetAttribute(k_stream_apply<0, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_apply<1, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    return true;
+  }();
+  (void)attrs;
+  const dim3 g = grid_for(op.m, 30, nb, RH, W);
   if (init)
-    k_fine_apply<1><<<g, WL * WPB, 0, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+    k_stream_apply<1, RA, W><<<g, WL * W, sm, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
   else
-    k_fine_apply<0><<<g, WL * WPB, 0, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+    k_stream_apply<0, RA, W><<<g, WL * W, sm, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
   TP_LAUNCHED(&p);
 }
 
