@@ -781,6 +781,19 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
   }
 }
 
+// x += xa p for the frequencies with a deferred update (fused Krylov step)
+__global__ void k_xfix(cplx* __restrict__ x, const cplx* __restrict__ p, const cplx* __restrict__ xa, size_t n,
+                       int nb) {
+  const int b = blockIdx.y;
+  if (b >= nb) return;
+  const cplx a = xa[b];
+  if (a.re == 0.0 && a.im == 0.0) return;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t j = (size_t)b * n + i;
+    x[j] = x[j] + mul(a, p[j]);
+  }
+}
+
 // partial b^T z
 template <int MODE>
 __global__ void __launch_bounds__(NT, 4) k_dot(Op<MODE> op, const TT<MODE>* __restrict__ a_,
@@ -1094,6 +1107,8 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   }
   const size_t n0 = (size_t)B * levels[0].n;
   r.alloc(n0);
+  if (MODE == 0 && levels[0].fine.we && L > 1) r2.alloc(n0);
+  xa.alloc(B);
   p0.alloc(n0);
   p1.alloc(n0);
   q.alloc(n0);
@@ -1187,11 +1202,12 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
 }
 
 template <int MODE>
-void BatchSolver<MODE>::fine_down0(int nb, const T* r_in) {
+void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out) {
   if constexpr (MODE == 0) {
     FineOp fo = ops[0].fine;
     fo.lam = lam;
-    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb);
+    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
+                       qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
   }
 }
 
@@ -1318,10 +1334,17 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   // vs 8.39 ms per cfg-1 sweep against the smem-tile apply (TPGPU_TILE_APPLY)
   static const bool use_stream_apply = std::getenv("TPGPU_TILE_APPLY") == nullptr;
   const bool sapply = fine && use_stream_apply;
+  // fused Krylov update (fine streaming path): r -= alpha q inside the fine
+  // down pass (partial ||r||^2 from there), x += alpha p deferred to the next
+  // apply -- the separate update pass disappears (cfg 1: 8.10 -> 7.65 ms per
+  // sweep; TPGPU_UNFUSED_UPDATE restores the update pass)
+  static const bool want_fuse = std::getenv("TPGPU_UNFUSED_UPDATE") == nullptr;
+  const bool fused = sapply && ops.size() > 1 && want_fuse;
+  const int per_d = fine ? fine_partials(ops[0].m, 1) : per_t;  // fused down (||r||^2)
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
-  T* const xa_ptr = nullptr;  // (x updates are not deferred: k_update below)
+  T* const xa_ptr = fused ? xa.get() : nullptr;
   cudaStream_t s = p->stream;
   const int l = 0;
   if (fine && warm && sapply) {
@@ -1346,6 +1369,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int last_active = h_count[0];
   cur_active = last_active;
   T* rcur = r.get();
+  T* rnext = r2.get();
   T* pin = p0.get();
   T* pout = p1.get();
   if (last_active > 0) {
@@ -1357,7 +1381,9 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
       if (sapply) {
-        if constexpr (MODE == 0) launch_fine_apply(*p, fo, z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false);
+        if constexpr (MODE == 0)
+          launch_fine_apply(*p, fo, z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false,
+                            fused ? x : nullptr, xa_ptr);
       } else {
         DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
                                                                         first, nb, g0.BB, part.get(), x, xa_ptr)));
@@ -1368,10 +1394,14 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
                                       count.get() + slot);
       TP_LAUNCHED(p);
-      k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr, nb,
-                                             g0.BB, part.get());
-      TP_LAUNCHED(p);
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), per_t, nb, rtol2, rho.get(), mu.get(),
+      if (fused) {
+        fine_down0(nb, rcur, q.get(), rnext);
+      } else {
+        k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr,
+                                               nb, g0.BB, part.get());
+        TP_LAUNCHED(p);
+      }
+      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
                                       count.get() + slot);
       TP_LAUNCHED(p);
@@ -1389,7 +1419,12 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         }
       }
       iters = it;
-      z = vcycle_level(0, nb, rcur, nullptr, false, true);
+      if (fused) {
+        std::swap(rcur, rnext);
+        z = fine_rest0(nb, rcur, true);
+      } else {
+        z = vcycle_level(0, nb, rcur, nullptr, false, true);
+      }
       k_scalars<T><<<nb, 256, 0, s>>>(ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
                                       alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
       TP_LAUNCHED(p);
@@ -1398,6 +1433,15 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     if (!done) {
       TP_CUDA(cudaStreamSynchronize(s));
       last_active = h_count[iters & 1];
+    }
+    if constexpr (MODE == 0) {
+      if (fused) {
+        // the deferred x += alpha p of the last iteration (nothing is pending
+        // when the loop ended by convergence: its final apply consumed it)
+        const dim3 gx((unsigned)std::min<size_t>((ops[0].n + 255) / 256, 64), nb);
+        k_xfix<<<gx, 256, 0, s>>>(x, done ? pout : pin, xa.get(), (size_t)ops[0].n, nb);
+        TP_LAUNCHED(p);
+      }
     }
   }
   TP_CUDA(cudaStreamSynchronize(s));

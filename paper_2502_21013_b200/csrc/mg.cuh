@@ -78,7 +78,8 @@ struct BatchSolver {
   const int* ext_mask = nullptr;  // optional: batches with mask 0 are skipped
   // work
   std::vector<DevBuf<T>> lb, lz0, lz1;  // per level (level 0: b is external)
-  DevBuf<T> r, p0, p1, q;
+  DevBuf<T> r, r2, p0, p1, q;
+  DevBuf<T> xa;  // deferred solution-update coefficient per batch (fused Krylov update)
   DevBuf<double> part;
   DevBuf<T> rho, mu, alpha, beta;
   DevBuf<double> bn2, rn2;
@@ -101,8 +102,9 @@ struct BatchSolver {
   void vcycle(int lvl, int nb, T* z_out_level0, bool dot);
   T* vcycle_level(int lvl, int nb, const T* bl, T* z_first, bool first_done, bool dot);
   T* vcycle_generic(int lvl, int nb, const T* bl, bool dot);
-  // fine streaming level: down pass, and the rest of the cycle (coarse levels + up pass)
-  void fine_down0(int nb, const T* r_in);
+  // fine streaming level: down pass (optionally fusing r_out = r_in - alpha q),
+  // and the rest of the cycle (coarse levels + up pass)
+  void fine_down0(int nb, const T* r_in, const T* qv = nullptr, T* r_out = nullptr);
   T* fine_rest0(int nb, const T* bl, bool dot);
 };
 
@@ -114,11 +116,16 @@ void launch_coarse_inverse_freq(Problem& p, const double* K, const double* M, in
 void launch_coarse_inverse_slice(Problem& p, const double* J, int m, double* inv, int batches);
 // Streaming kernels (mg_fine.cu).  kind: 0 apply, 1 down, 2 up.
 int fine_partials(int m, int kind);
+// (xa != nullptr: also x += xa p_in, the deferred update of the fused Krylov step)
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
-                       const cplx* beta, const int* active, int first, int nb, double* part, bool init);
+                       const cplx* beta, const int* active, int first, int nb, double* part, bool init,
+                       cplx* x = nullptr, const cplx* xa = nullptr);
 // V-cycle down / up passes of one level (fine: op.we set; Galerkin: op.K set)
+// (q != nullptr: fine level with the fused Krylov update r_out = r - alpha q,
+// partial ||r_out||^2 per warp item into part)
 void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                        const int* active, double om1, double om2, int nb);
+                        const int* active, double om1, double om2, int nb, const cplx* q = nullptr,
+                        const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
 void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).

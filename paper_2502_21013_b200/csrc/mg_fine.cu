@@ -415,21 +415,34 @@ __device__ __forceinline__ ItemNB<WPBK, NB> item_nb(int m, int own, int rh, int 
 //   z1 = w1 r/d ; z2 = z1 + w2 (r - A z1)/d ; res = r - A z2 ; b_c = P^T res
 // NB frequencies per warp share the coefficient rows, the addressing and the
 // ring bookkeeping; their arithmetic chains are independent (ILP).
-template <class S, int NB, int RA, int WPBK>
+// FUSED (fine level, NB = 1): the Krylov residual update rides along -- the
+// right-hand side is r_new = r - alpha q (read r and q, write r_new to rout
+// for the owned rows, partial ||r_new||^2 per warp item), replacing the
+// separate x/r update pass (x is updated in the next apply).
+template <class S, int NB, int RA, int WPBK, bool FUSED = false>
 __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp op, const cplx* __restrict__ rv,
                                                                          cplx* __restrict__ z2out,
                                                                          cplx* __restrict__ bc, int mc, int rh,
                                                                          const int* __restrict__ active, double om1,
-                                                                         double om2, int nb) {
+                                                                         double om2, int nb,
+                                                                         const cplx* __restrict__ qv = nullptr,
+                                                                         const cplx* __restrict__ alpha = nullptr,
+                                                                         cplx* __restrict__ rout = nullptr,
+                                                                         double* __restrict__ part = nullptr) {
+  static_assert(!FUSED || NB == 1, "fused residual update: one frequency per warp");
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
-  constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN;
+  constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN, NVV = FUSED ? 2 : NB;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
   const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<NB>* const vring = reinterpret_cast<VRow<NB>*>(fine_smem) + wib * RV;
-  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NB>)) + wib * RC;
+  VRow<NVV>* const vring = reinterpret_cast<VRow<NVV>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NVV>)) + wib * RC;
+  const cplx* const qp = FUSED ? qv + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
+  cplx* const ro = FUSED ? rout + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
+  const cplx al = FUSED ? alpha[it.b[0]] : cplx{0, 0};
+  double rn2 = 0;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < H + OWN && colok;
@@ -458,6 +471,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
       const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
 #pragma unroll
       for (int j = 0; j < NB; ++j) cp16(&vring[vi].v[j][lane], rp[j] + off, rin);
+      if (FUSED) cp16(&vring[vi].v[1][lane], qp + off, rin);
       S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
@@ -502,6 +516,15 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
       r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = vring[vr].v[j][lane];
+      if (FUSED) {
+        const cplx qq = vring[vr].v[1][lane];
+        r0[j].re -= al.re * qq.re - al.im * qq.im;
+        r0[j].im -= al.re * qq.im + al.im * qq.re;
+        if (own && yi >= ys && yi < ye) {
+          ro[(long)yi * m] = r0[j];
+          rn2 = fma(r0[j].re, r0[j].re, fma(r0[j].im, r0[j].im, rn2));
+        }
+      }
       // z1 = omega r / d at row yi (off-domain diagonals may vanish: z1 = 0 there)
       a2[j] = a1[j]; a1[j] = a0[j];
       id1[j] = id0[j];
@@ -545,6 +568,16 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
     }
   }
   cp_wait<0>();
+  if (FUSED) {
+    double zz = 0;
+    warp_pair(rn2, zz);
+    if (lane == 0) {
+      const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
+      const size_t k = (size_t)it.b[0] * ((size_t)ns * nch) + (size_t)it.chunk * ns + it.strip;
+      part[2 * k] = rn2;
+      part[2 * k + 1] = 0.0;
+    }
+  }
 }
 
 // ---------------------------------------------------------------- up
@@ -709,22 +742,31 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
 // INIT = 1: r = b - A x (b in z, x in pin, r to q) ; part += (|b|^2, |r|^2)
 // One fine-level stencil per node: rows of z and p_in staged through the
 // ring, p formed at row yi, q (and the stored p) at row yi-1.
-template <int INIT, int RA, int WPBK>
+// XUPD: also the deferred solution update x += xa p_in of the previous
+// iteration (fused Krylov update): x staged as a third vector; frequencies
+// that converged last iteration (inactive, xa != 0) get only that update.
+template <int INIT, int RA, int WPBK, bool XUPD = false>
 __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cplx* __restrict__ z,
                                                             const cplx* __restrict__ pin, cplx* __restrict__ pout,
                                                             cplx* __restrict__ q, const cplx* __restrict__ beta,
                                                             const int* __restrict__ active, int first, int nb,
-                                                            double* __restrict__ part) {
+                                                            double* __restrict__ part, cplx* __restrict__ xs = nullptr,
+                                                            const cplx* __restrict__ xa = nullptr) {
   using S = Five;
   constexpr int H = 1, OWN = WL - 2 * H;  // 30
-  constexpr int RV = RA + 2, RC = RA + 2;
+  constexpr int RV = RA + 2, RC = RA + 2, NVV = XUPD ? 3 : 2;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
-  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RH, nb, INIT ? nullptr : active);
-  if (!it.ok) return;
+  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RH, nb, nullptr);
+  const bool on = INIT || !active || active[it.b[0]];
+  cplx xab{0, 0};
+  if (XUPD) xab = xa[it.b[0]];
+  const bool pend = XUPD && (xab.re != 0.0 || xab.im != 0.0);
+  if (!it.ok || (!on && !pend)) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<2>* const vring = reinterpret_cast<VRow<2>*>(fine_smem) + wib * RV;
-  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<2>)) + wib * RC;
+  VRow<NVV>* const vring = reinterpret_cast<VRow<NVV>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring =
+      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NVV>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
@@ -735,6 +777,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
   const cplx* const pp = pin + o + xc;
   cplx* const po = pout + o + xc;
   cplx* const qo = q + o + xc;
+  cplx* const xo = XUPD ? xs + o + xc : nullptr;
   const cplx l = op.lam[b];
   const bool usep = INIT || !first;  // p_in is read
   const cplx bt = (INIT || first) ? cplx{0, 0} : beta[b];
@@ -747,7 +790,8 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
       const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
       const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
       cp16(&vring[vi].v[0][lane], zp + off, rin);
-      cp16(&vring[vi].v[1][lane], pp + off, rin && usep);
+      cp16(&vring[vi].v[1][lane], pp + off, rin && (usep || pend));
+      if (XUPD) cp16(&vring[vi].v[2][lane], xo + off, rin && pend);
       S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
@@ -776,6 +820,10 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
     k1 = k0;
     k0 = S::load(wring[sr], lane, k1);
     const cplx zz = vring[vr].v[0][lane], pv = vring[vr].v[1][lane];
+    if (XUPD && pend && own && yi >= ys && yi < ye) {
+      const cplx xv = vring[vr].v[2][lane];
+      xo[(long)yi * m] = {xv.re + (xab.re * pv.re - xab.im * pv.im), xv.im + (xab.re * pv.im + xab.im * pv.re)};
+    }
     p2 = p1; p1 = p0;
     b1 = b0; b0 = zz;
     p0 = INIT ? pv
@@ -783,7 +831,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
     // q at row yi-1
     const cplx Ap = S::apply(k1, l, S::diag(k1, l), p2, p1, p0);
     const int y = yi - 1;
-    if (own && y >= ys && y < ye) {
+    if (on && own && y >= ys && y < ye) {
       const long i = (long)y * m;
       if (INIT) {
         const cplx r = {b1.re - Ap.re, b1.im - Ap.im};
@@ -801,7 +849,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
   }
   cp_wait<0>();
   warp_pair(s0, s1);
-  if (lane == 0) {
+  if (lane == 0 && on) {
     const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
     const size_t per = (size_t)ns * nch;
     const size_t k = (size_t)b * per + (size_t)it.chunk * ns + it.strip;
@@ -832,18 +880,21 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <class S, int NB, int RA, int WPBK>
+template <class S, int NB, int RA, int WPBK, bool FUSED = false>
 void down_t(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc, const int* active, double om1,
-            double om2, int nb) {
-  constexpr size_t sm = ring_smem<S, NB, RA, WPBK>();
+            double om2, int nb, const cplx* q = nullptr, const cplx* alpha = nullptr, cplx* rout = nullptr,
+            double* part = nullptr) {
+  constexpr size_t sm = ring_smem<S, FUSED ? 2 : NB, RA, WPBK>();
   static bool attrs = [] {
-    cudaFuncSetAttribute(k_stream_down<S, NB, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_down<S, NB, RA, WPBK, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sm);
     return true;
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  k_stream_down<S, NB, RA, WPBK><<<grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.stream>>>(
-      op, r, z2, bc, mc, rh, active, om1, om2, nb);
+  k_stream_down<S, NB, RA, WPBK, FUSED>
+      <<<grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+          op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
 }
 
 template <class S, int NB, int RA, int WPBK>
@@ -867,18 +918,24 @@ int fine_partials(int m, int kind) {
 }
 
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
-                       const cplx* beta, const int* active, int first, int nb, double* part, bool init) {
+                       const cplx* beta, const int* active, int first, int nb, double* part, bool init, cplx* x,
+                       const cplx* xa) {
   constexpr int RA = 4, W = 4;
   constexpr size_t sm = (size_t)W * ((RA + 2) * sizeof(VRow<2>) + (RA + 2) * sizeof(WRow<Five::NW>));
+  constexpr size_t sm3 = (size_t)W * ((RA + 2) * sizeof(VRow<3>) + (RA + 2) * sizeof(WRow<Five::NW>));
   static bool attrs = [] {
     cudaFuncSetAttribute(k_stream_apply<0, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     cudaFuncSetAttribute(k_stream_apply<1, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_apply<0, RA, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
     return true;
   }();
   (void)attrs;
   const dim3 g = grid_for(op.m, 30, nb, RH, W);
   if (init)
     k_stream_apply<1, RA, W><<<g, WL * W, sm, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+  else if (xa)
+    k_stream_apply<0, RA, W, true><<<g, WL * W, sm3, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb,
+                                                                  part, x, xa);
   else
     k_stream_apply<0, RA, W><<<g, WL * W, sm, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
   TP_LAUNCHED(&p);
@@ -891,8 +948,11 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
 // sweep -- 224 registers halve the resident warps); TPGPU_RA5 / TPGPU_RA5U
 // override the ring depths for experiments.
 void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
-                        const int* active, double om1, double om2, int nb) {
-  if (op.we) {
+                        const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
+                        cplx* rout, double* part) {
+  if (op.we && q) {
+    down_t<Five, 1, 6, 4, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+  } else if (op.we) {
     static const int ra = env_int("TPGPU_RA5", 6);
     if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
     else down_t<Five, 1, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
