@@ -262,12 +262,14 @@ def run_b200(args):
                 "frac": (k_ach / hbm) if k_ach else None, "traffic": traffic, "peak_source": src,
                 "bytes_per_launch": k_bytes_launch, "avg_launch_ms": k_avg_ms, "launches": k_launches}
     # Whole-sweep algorithmic bytes: B = 72 D + 16 n S sum_k it_k
-    # with S = 17.0 complex streams per inner iteration and frequency as
-    # implemented (fine: apply 4, update 6, down 2.25, up 3.25; first Galerkin
-    # level 5.5 / 4; fused small-level cycle: read b, write z at 1/16).
+    # with S = 15.0 complex streams per inner iteration and frequency as
+    # implemented (fine: apply 6 = read z, p, x, write p, q, x; down with the
+    # fused residual update 4.25 = read r, q, write r, z2, 1/4 coarse rhs;
+    # up 3.25; first Galerkin level 5.5 / 4; fused small-level cycle: read b,
+    # write z at 1/16).
     K = desc.steps // 2 + 1
     n = (desc.cells - 1) ** 2
-    STREAMS = 15.5 + 5.5 / 4 + 2.0 / 16
+    STREAMS = 13.5 + 5.5 / 4 + 2.0 / 16
     mean_inner = float(np.mean(inner)) if inner else 0.0
     b_alg = 72.0 * D + 16.0 * n * STREAMS * K * mean_inner
     t_sweep = total_ms / 1e3 / args.steps
