@@ -373,7 +373,15 @@ __device__ __forceinline__ Item item_rh(int m, int own, int rh, int nb, const in
 #ifndef TPGPU_RESTRICT_SHFL_ALWAYS
 #define TPGPU_RESTRICT_SHFL_ALWAYS 0
 #endif
+#ifndef TPGPU_SEVEN_MINW
+#define TPGPU_SEVEN_MINW 0
+#endif
 #define TP_MINB(W) (TPGPU_STREAM_MINW > 0 ? TPGPU_STREAM_MINW / (W) : 1)
+// per stencil: resident warps per SM the registers are bounded for
+#define TP_MINB_S(S, W) ((S::NW == 8 && TPGPU_SEVEN_MINW > 0) ? TPGPU_SEVEN_MINW / (W) : TP_MINB(W))
+#ifndef TPGPU_SEVEN_UNROLL
+#define TPGPU_SEVEN_UNROLL TPGPU_STREAM_UNROLL
+#endif
 #define TP_PRAGMA(x) _Pragma(#x)
 #define TP_UNROLL(n) TP_PRAGMA(unroll n)
 
@@ -420,7 +428,7 @@ __device__ __forceinline__ ItemNB<WPBK, NB> item_nb(int m, int own, int rh, int 
 // for the owned rows, partial ||r_new||^2 per warp item), replacing the
 // separate x/r update pass (x is updated in the next apply).
 template <class S, int NB, int RA, int WPBK, bool FUSED = false>
-__global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp op, const cplx* __restrict__ rv,
+__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(FineOp op, const cplx* __restrict__ rv,
                                                                          cplx* __restrict__ z2out,
                                                                          cplx* __restrict__ bc, int mc, int rh,
                                                                          const int* __restrict__ active, double om1,
@@ -500,7 +508,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
   cp_wait<RA>();
   if (S::XLANE) __syncwarp();
   typename S::Reg k0 = S::first(wring[0], lane), k1 = k0, k2 = k0;  // rows yi, yi-1, yi-2
-  TP_UNROLL(TPGPU_STREAM_UNROLL)
+  TP_UNROLL((S::NW == 8 ? TPGPU_SEVEN_UNROLL : TPGPU_STREAM_UNROLL))
   for (int yi = ys - 2; yi <= ylast; ++yi) {
     issue(yi + RA);
     vr = wrap_inc(vr, RV);
@@ -585,7 +593,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_down(FineOp
 // Staged per row and frequency: r, z2 and the (up to two) coarse values P x_c
 // interpolates from at the lane's node; the coefficient row once.
 template <class S, int NB, int RA, int WPBK>
-__global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp op, const cplx* __restrict__ rv,
+__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(FineOp op, const cplx* __restrict__ rv,
                                                                        const cplx* __restrict__ z2in,
                                                                        const cplx* __restrict__ xcv, int mc, int rh,
                                                                        cplx* __restrict__ zout,
@@ -675,7 +683,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB(WPBK)) k_stream_up(FineOp o
   cp_wait<RA>();
   if (S::XLANE) __syncwarp();
   typename S::Reg k0 = S::first(wring[0], lane), k1 = k0, k2 = k0;  // rows yi, yi-1, yi-2
-  TP_UNROLL(TPGPU_STREAM_UNROLL)
+  TP_UNROLL((S::NW == 8 ? TPGPU_SEVEN_UNROLL : TPGPU_STREAM_UNROLL))
   for (int yi = ys - 2; yi <= ylast; ++yi) {
     issue(yi + RA);
     vr = wrap_inc(vr, RV);
