@@ -471,8 +471,8 @@ struct CoefPlanes<0> {  // coarse frequency mode, symmetric: K and M at C, E, N,
   static constexpr int planes = 8;
 };
 template <>
-struct CoefPlanes<2> {  // slice mode: 7 J (per batch)
-  static constexpr int planes = 7;
+struct CoefPlanes<2> {  // slice mode, symmetric J (per batch): C, E, N, NE
+  static constexpr int planes = 4;
 };
 
 template <int MODE, int FAM>
@@ -500,9 +500,13 @@ __device__ __forceinline__ void stage_coefs(const Op<MODE>& op, double* cf, int 
         cf[(4 + q) * H2N + k] = in ? __ldg(o.M + dirs[q] * n + i) : 0.0;
       }
     } else {
+      // the element-assembled Jacobian is symmetric: W(i) = E(i-1), S(i) = N(i-m),
+      // SW(i) = NE(i-m-1) -- the smoothers read four planes (the PCG operator
+      // itself, k_apply_dot, still applies all seven)
       const Op<1>& o = op;
       const double* J = o.J + (size_t)b * 7 * n;
-      for (int d = 0; d < 7; ++d) cf[d * H2N + k] = in ? __ldg(J + d * n + i) : (d == 0 ? 1.0 : 0.0);
+      const int dirs[4] = {SC, SE_, SN_, SNE};
+      for (int q = 0; q < 4; ++q) cf[q * H2N + k] = in ? __ldg(J + dirs[q] * n + i) : (q == 0 ? 1.0 : 0.0);
     }
   }
 }
@@ -533,8 +537,8 @@ __device__ __forceinline__ TT<MODE> coff(const double* cf, const TT<MODE>* v, in
     return acc;
   } else if constexpr (FAM == 2) {
     const T vsw = v[h - H2X - 1], vne = v[h + H2X + 1];
-    return cf[1 * H2N + h] * vw + cf[2 * H2N + h] * ve + cf[3 * H2N + h] * vs + cf[4 * H2N + h] * vn +
-           cf[5 * H2N + h] * vsw + cf[6 * H2N + h] * vne;
+    return cf[1 * H2N + h - 1] * vw + cf[1 * H2N + h] * ve + cf[2 * H2N + h - H2X] * vs + cf[2 * H2N + h] * vn +
+           cf[3 * H2N + h - H2X - 1] * vsw + cf[3 * H2N + h] * vne;
   } else {
     const T vsw = v[h - H2X - 1], vne = v[h + H2X + 1];
     // (plane, node) of each neighbour's coefficient: W = E(h-1), E = E(h),
