@@ -1022,7 +1022,7 @@ __global__ void k_dense_inverse(const double* __restrict__ K, const double* __re
 void launch_rap(Problem& p, const double* Af, int mf, double* Ac, int mc, int batches) {
   const size_t nc = (size_t)mc * mc;
   dim3 grid((unsigned)((nc + 127) / 128), batches);
-  k_rap<<<grid, 128, 0, p.stream>>>(Af, mf, Ac, mc);
+  k_rap<<<grid, 128, 0, p.cur_stream()>>>(Af, mf, Ac, mc);
   TP_LAUNCHED(&p);
 }
 
@@ -1033,7 +1033,7 @@ static void launch_dense_inverse(Problem& p, const double* K, const double* M, i
   const size_t smem = (size_t)n * 2 * n * sizeof(TT<MODE>);
   require(smem <= 200 * 1024, "multigrid: coarsest grid too large for the dense solve");
   TP_CUDA(cudaFuncSetAttribute(k_dense_inverse<MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  k_dense_inverse<MODE><<<batches, 256, smem, p.stream>>>(K, M, lam, m, inv, strideK);
+  k_dense_inverse<MODE><<<batches, 256, smem, p.cur_stream()>>>(K, M, lam, m, inv, strideK);
   TP_LAUNCHED(&p);
 }
 
@@ -1160,7 +1160,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   static const int coarse_bb = std::getenv("TPGPU_COARSE_BB") ? std::atoi(std::getenv("TPGPU_COARSE_BB")) : 4;
   const Geo g = geo_for(ops[l].m, nb, p->num_sms, l == 0 ? 8 : coarse_bb);
   int* act = active.get();
-  cudaStream_t s = p->stream;
+  cudaStream_t s = p->cur_stream();
   const dim3 blk(TX, TY);
 #define DISPATCH_FAM(lv, CALL)          \
   if constexpr (MODE == 1) {            \
@@ -1220,7 +1220,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
   const int l = 0;
   const int L = (int)ops.size();
   int* act = active.get();
-  cudaStream_t s = p->stream;
+  cudaStream_t s = p->cur_stream();
   T* z2 = lz0[l].get();
   T* zo = lz1[l].get();
   if constexpr (MODE == 0) {
@@ -1244,6 +1244,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
       launch_stream_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
       if (p->ktimer.on) {
         TP_CUDA(cudaEventRecord(e1, s));
+        std::lock_guard<std::mutex> lk(p->ktimer.mu);
         p->ktimer.pending.emplace_back(e0, e1);
         // algorithmic bytes: read z2, r and the coarse correction (1/4), write z --
         // 3.25 complex values per fine node of every active frequency
@@ -1263,7 +1264,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
   static const int coarse_bb = std::getenv("TPGPU_COARSE_BB") ? std::atoi(std::getenv("TPGPU_COARSE_BB")) : 4;
   const Geo g = geo_for(ops[l].m, nb, p->num_sms, l == 0 ? 8 : coarse_bb);
   int* act = active.get();
-  cudaStream_t s = p->stream;
+  cudaStream_t s = p->cur_stream();
   const dim3 blk(TX, TY);
   const Op<MODE> opc = make_op<MODE>(ops[l + 1], lam);
   T* z2 = lz0[l].get();
@@ -1349,7 +1350,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int* act = active.get();
   int* zero = active.get() + B;
   T* const xa_ptr = fused ? xa.get() : nullptr;
-  cudaStream_t s = p->stream;
+  cudaStream_t s = p->cur_stream();
   const int l = 0;
   if (fine && warm && sapply) {
     if constexpr (MODE == 0) launch_fine_apply(*p, fo, b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
@@ -1450,8 +1451,9 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   }
   TP_CUDA(cudaStreamSynchronize(s));
   std::vector<double> hb(nb), hr(nb);
-  TP_CUDA(cudaMemcpy(hb.data(), bn2.get(), nb * sizeof(double), cudaMemcpyDeviceToHost));
-  TP_CUDA(cudaMemcpy(hr.data(), rn2.get(), nb * sizeof(double), cudaMemcpyDeviceToHost));
+  TP_CUDA(cudaMemcpyAsync(hb.data(), bn2.get(), nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TP_CUDA(cudaMemcpyAsync(hr.data(), rn2.get(), nb * sizeof(double), cudaMemcpyDeviceToHost, s));
+  TP_CUDA(cudaStreamSynchronize(s));
   double worst = 0;
   for (int k = 0; k < nb; ++k)
     if (hb[k] > 0) worst = std::max(worst, std::sqrt(hr[k] / hb[k]));

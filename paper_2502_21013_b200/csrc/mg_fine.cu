@@ -901,7 +901,7 @@ void down_t(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int
   (void)attrs;
   const int rh = rh_for(op.m);
   k_stream_down<S, NB, RA, WPBK, FUSED>
-      <<<grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+      <<<grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.cur_stream()>>>(
           op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
 }
 
@@ -915,7 +915,7 @@ void up_t(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cpl
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  k_stream_up<S, NB, RA, WPBK><<<grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.stream>>>(
+  k_stream_up<S, NB, RA, WPBK><<<grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.cur_stream()>>>(
       op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
 
@@ -940,12 +940,12 @@ void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* 
   (void)attrs;
   const dim3 g = grid_for(op.m, 30, nb, RH, W);
   if (init)
-    k_stream_apply<1, RA, W><<<g, WL * W, sm, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+    k_stream_apply<1, RA, W><<<g, WL * W, sm, p.cur_stream()>>>(op, z, pin, pout, q, beta, active, first, nb, part);
   else if (xa)
-    k_stream_apply<0, RA, W, true><<<g, WL * W, sm3, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb,
+    k_stream_apply<0, RA, W, true><<<g, WL * W, sm3, p.cur_stream()>>>(op, z, pin, pout, q, beta, active, first, nb,
                                                                   part, x, xa);
   else
-    k_stream_apply<0, RA, W><<<g, WL * W, sm, p.stream>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+    k_stream_apply<0, RA, W><<<g, WL * W, sm, p.cur_stream()>>>(op, z, pin, pout, q, beta, active, first, nb, part);
   TP_LAUNCHED(&p);
 }
 

@@ -220,12 +220,12 @@ size_t small_cycle_smem(const int* m, int levels) {
 void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, const cplx* inv, const cplx* b,
                         cplx* z, const int* active, double om1, double om2, int nb) {
   const size_t sm = small_cycle_smem(sl.m, sl.levels);
-  static size_t set = 0;
-  if (sm > set) {
-    TP_CUDA(cudaFuncSetAttribute(k_small_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm));
-    set = sm;
-  }
-  k_small_cycle<<<nb, SNT, sm, p.stream>>>(sl, lam, inv, b, z, active, om1, om2);
+  static const bool attr = [] {  // (thread-safe one-time init: the largest opt-in size)
+    return cudaFuncSetAttribute(k_small_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
+           cudaSuccess;
+  }();
+  require(attr && sm <= 227 * 1024, "small-level cycle: shared memory");
+  k_small_cycle<<<nb, SNT, sm, p.cur_stream()>>>(sl, lam, inv, b, z, active, om1, om2);
   TP_LAUNCHED(&p);
 }
 

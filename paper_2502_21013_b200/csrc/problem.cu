@@ -13,6 +13,7 @@
 #include <cstring>
 #include <limits>
 #include <numbers>
+#include <thread>
 #include <string>
 
 #include "../../include/tpgpu_baseline.h"
@@ -94,13 +95,32 @@ void flux_bounds(const tp_material& m, double lo, double hi, int samples, double
 
 }  // namespace
 
+// Frequency-solver workspace.  With parts > 1, a chunk's frequencies are
+// split into `parts` groups solved by independent batch solvers on their own
+// streams, each driven by its own host thread: the latency-bound coarse part
+// of one group's V-cycle overlaps the bandwidth-bound fine passes of another.
 struct Problem::FreqWork {
   DevBuf<cplx> lam;       // K symbols
   DevBuf<cplx> inv;       // K * nL^2 coarsest inverses
-  BatchSolver<0> solver;
-  int chunk = 0;
+  BatchSolver<0> solver;  // group 0 (and the only one when parts == 1)
+  std::vector<std::unique_ptr<BatchSolver<0>>> extra;  // groups 1 .. parts-1
+  int parts = 1;
+  std::vector<cudaStream_t> hs;
+  cudaEvent_t ev_in = nullptr;
+  std::vector<cudaEvent_t> ev_out;
+  int chunk = 0;  // frequencies per group
   int nL = 0;
+  BatchSolver<0>& group(int g) { return g == 0 ? solver : *extra[g - 1]; }
+  ~FreqWork() {
+    for (auto& e : ev_out)
+      if (e) cudaEventDestroy(e);
+    if (ev_in) cudaEventDestroy(ev_in);
+    for (auto& h : hs)
+      if (h) cudaStreamDestroy(h);
+  }
 };
+
+thread_local cudaStream_t Problem::tl_stream = nullptr;
 
 Problem::Problem(const tp_problem_desc& d, int dev, const ShardInfo* shard) : desc(d), device(dev) {
   validate_desc(d);
@@ -285,8 +305,10 @@ void Problem::install_nu_hat(const double* nu, double q) {
 void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   require(nu_hat_set, "periodic solver: nu_hat not installed");
   if (freq_ready && fw && (cfg.freq_chunk <= 0 || cfg.freq_chunk == fw->chunk)) {
-    fw->solver.cfg.rtol = cfg.inner_rtol;
-    fw->solver.cfg.max_iter = cfg.inner_max_iter;
+    for (int g = 0; g < fw->parts; ++g) {
+      fw->group(g).cfg.rtol = cfg.inner_rtol;
+      fw->group(g).cfg.max_iter = cfg.inner_max_iter;
+    }
     return;
   }
   fw.reset();
@@ -374,7 +396,24 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   if (const char* e = std::getenv("TPGPU_RB_FINE")) mc.rb_fine = std::atoi(e) != 0;
   if (const char* e = std::getenv("TPGPU_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
   if (const char* e = std::getenv("TPGPU_OMEGA2")) mc.omega2 = std::atof(e);
-  fw->solver.init(this, ops, chunk, mc);
+  // concurrent frequency groups (TPGPU_FREQ_GROUPS overrides; 1 = one solver on the problem stream)
+  int parts = std::getenv("TPGPU_FREQ_GROUPS") ? std::atoi(std::getenv("TPGPU_FREQ_GROUPS")) : 3;
+  parts = std::max(1, std::min(parts, chunk));
+  fw->parts = parts;
+  const int per_group = (chunk + parts - 1) / parts;
+  fw->chunk = per_group;
+  fw->solver.init(this, ops, per_group, mc);
+  for (int g = 1; g < parts; ++g) {
+    fw->extra.push_back(std::make_unique<BatchSolver<0>>());
+    fw->extra.back()->init(this, ops, per_group, mc);
+  }
+  if (parts > 1) {
+    fw->hs.assign(parts, nullptr);
+    fw->ev_out.assign(parts, nullptr);
+    for (auto& h : fw->hs) TP_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
+    TP_CUDA(cudaEventCreateWithFlags(&fw->ev_in, cudaEventDisableTiming));
+    for (auto& e : fw->ev_out) TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+  }
   TP_CUDA(cudaStreamSynchronize(stream));
   freq_ready = true;
   uhat_valid = false;
@@ -387,12 +426,55 @@ void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
   const bool warm = cfg.warm_start && uhat_valid;
   const int Kr = sh.k1 - sh.k0;
   int iters = 0;
-  for (int k0 = 0; k0 < Kr; k0 += fw->chunk) {
-    const int nb = std::min(fw->chunk, Kr - k0);
-    fw->solver.lam = fw->lam.get() + k0;
-    fw->solver.coarse_inv = fw->inv.get() + (size_t)k0 * fw->nL * fw->nL;
-    iters = std::max(iters, fw->solver.solve(spec_in() + (size_t)k0 * n, spec_out() + (size_t)k0 * n, nb,
-                                             warm, st));
+  auto run = [&](BatchSolver<0>& sv, int k0, int nb, SolveStats* sst) {
+    sv.lam = fw->lam.get() + k0;
+    sv.coarse_inv = fw->inv.get() + (size_t)k0 * fw->nL * fw->nL;
+    return sv.solve(spec_in() + (size_t)k0 * n, spec_out() + (size_t)k0 * n, nb, warm, sst);
+  };
+  if (fw->parts == 1) {
+    for (int k0 = 0; k0 < Kr; k0 += fw->chunk)
+      iters = std::max(iters, run(fw->solver, k0, std::min(fw->chunk, Kr - k0), st));
+  } else {
+    // groups of `parts` chunks: group 0 on hs[0] (this thread), the others on
+    // hs[g] driven by helper threads
+    const int P = fw->parts;
+    for (int k0 = 0; k0 < Kr; k0 += P * fw->chunk) {
+      TP_CUDA(cudaEventRecord(fw->ev_in, stream));
+      for (auto h : fw->hs) TP_CUDA(cudaStreamWaitEvent(h, fw->ev_in, 0));
+      std::vector<SolveStats> gst(P);
+      std::vector<int> git(P, 0);
+      std::vector<std::exception_ptr> gerr(P);
+      auto body = [&](int g) {
+        const int kg = k0 + g * fw->chunk, nbg = std::min(fw->chunk, Kr - kg);
+        if (nbg <= 0) return;
+        try {
+          if (g > 0) TP_CUDA(cudaSetDevice(device));
+          tl_stream = fw->hs[g];
+          git[g] = run(fw->group(g), kg, nbg, &gst[g]);
+        } catch (...) {
+          gerr[g] = std::current_exception();
+        }
+        tl_stream = nullptr;
+      };
+      std::vector<std::thread> helpers;
+      for (int g = 1; g < P; ++g) helpers.emplace_back(body, g);
+      body(0);
+      for (auto& t : helpers) t.join();
+      for (int g = 0; g < P; ++g) {
+        TP_CUDA(cudaEventRecord(fw->ev_out[g], fw->hs[g]));
+        TP_CUDA(cudaStreamWaitEvent(stream, fw->ev_out[g], 0));
+      }
+      for (auto& e : gerr)
+        if (e) std::rethrow_exception(e);
+      for (int g = 0; g < P; ++g) {
+        iters = std::max(iters, git[g]);
+        if (st) {
+          st->iterations = std::max(st->iterations, gst[g].iterations);
+          st->batch_iterations += gst[g].batch_iterations;
+          st->max_rel_residual = std::max(st->max_rel_residual, gst[g].max_rel_residual);
+        }
+      }
+    }
   }
   last_inner = iters;
   if (sharded()) alltoall_from_freq();
@@ -814,6 +896,6 @@ int tp_kernel_timer(tp_problem* h, int32_t enable, int64_t* launches, double* ms
 
 void* tp_problem_stream(tp_problem* p) { return (p && p->impl) ? (void*)p->impl->stream : nullptr; }
 
-int64_t tp_problem_launches(const tp_problem* p) { return (p && p->impl) ? p->impl->launches : 0; }
+int64_t tp_problem_launches(const tp_problem* p) { return (p && p->impl) ? p->impl->launches.load() : 0; }
 
 }  // extern "C"

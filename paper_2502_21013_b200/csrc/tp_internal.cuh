@@ -4,8 +4,10 @@
 
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdint>
 #include <memory>
+#include <mutex>
 #include <stdexcept>
 #include <string>
 #include <vector>
@@ -166,7 +168,11 @@ class Problem {
 
   // device constants
   cudaStream_t stream = nullptr;
-  int64_t launches = 0;
+  // stream the calling host thread launches on: the problem's stream, or the
+  // per-thread override of a concurrently driven frequency half (problem.cu)
+  static thread_local cudaStream_t tl_stream;
+  cudaStream_t cur_stream() const { return tl_stream ? tl_stream : stream; }
+  std::atomic<int64_t> launches{0};
   int num_sms = 148;
   DevBuf<uint8_t> d_cell_mat;
   DevBuf<double> d_mass;
@@ -212,6 +218,7 @@ class Problem {
   // live kernel timing for bench.py's roofline (enabled on request): the
   // dominant kernel (fine-level V-cycle up pass) is bracketed by CUDA events
   struct KernelTimer {
+    std::mutex mu;
     bool on = false;
     int64_t launches = 0;
     double bytes = 0, ms = 0;
