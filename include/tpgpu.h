@@ -112,6 +112,9 @@ typedef struct tp_solver_cfg {
   int32_t warm_start;         /* start frequency solves from the previous sweep (default 1) */
   int32_t freq_chunk;         /* frequencies per batched solve (0 = automatic) */
   int32_t slice_chunk;        /* slices per batched Newton solve (0 = automatic) */
+  int32_t freq_groups;        /* frequency groups solved concurrently on their own
+                                 streams (0 = automatic: 3) */
+  int32_t reserved_;          /* keeps the struct size a multiple of 8 */
 } tp_solver_cfg;
 
 /* Mirrors SolveReport (solvers.hpp:88-96); residual/contraction histories are

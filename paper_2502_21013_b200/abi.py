@@ -43,7 +43,8 @@ class TpSolverCfg(C.Structure):
                 ("static_tol", C.c_double), ("static_max_newton", C.c_int32),
                 ("threads", C.c_int32), ("inner_rtol", C.c_double),
                 ("inner_max_iter", C.c_int32), ("warm_start", C.c_int32),
-                ("freq_chunk", C.c_int32), ("slice_chunk", C.c_int32)]
+                ("freq_chunk", C.c_int32), ("slice_chunk", C.c_int32),
+                ("freq_groups", C.c_int32), ("reserved_", C.c_int32)]
 
 
 class TpShardPlan(C.Structure):
@@ -81,6 +82,8 @@ def default_cfg(**overrides) -> TpSolverCfg:
     c.warm_start = 1
     c.freq_chunk = 0
     c.slice_chunk = 0
+    c.freq_groups = 0
+    c.reserved_ = 0
     for k, v in overrides.items():
         setattr(c, k, v)
     return c

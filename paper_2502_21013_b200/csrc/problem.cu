@@ -110,6 +110,7 @@ struct Problem::FreqWork {
   std::vector<cudaEvent_t> ev_out;
   int chunk = 0;  // frequencies per group
   int nL = 0;
+  int req_chunk = 0, req_groups = 0;  // the configuration it was built for
   BatchSolver<0>& group(int g) { return g == 0 ? solver : *extra[g - 1]; }
   ~FreqWork() {
     for (auto& e : ev_out)
@@ -304,7 +305,10 @@ void Problem::install_nu_hat(const double* nu, double q) {
 // for (lambda_k M + K_hat), all frequencies sharing the real stencils.
 void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   require(nu_hat_set, "periodic solver: nu_hat not installed");
-  if (freq_ready && fw && (cfg.freq_chunk <= 0 || cfg.freq_chunk == fw->chunk)) {
+  static const int env_groups = std::getenv("TPGPU_FREQ_GROUPS") ? std::atoi(std::getenv("TPGPU_FREQ_GROUPS")) : 3;
+  const int want_groups = cfg.freq_groups > 0 ? cfg.freq_groups : env_groups;
+  if (freq_ready && fw && (cfg.freq_chunk <= 0 || cfg.freq_chunk == fw->req_chunk) &&
+      (want_groups == fw->req_groups)) {
     for (int g = 0; g < fw->parts; ++g) {
       fw->group(g).cfg.rtol = cfg.inner_rtol;
       fw->group(g).cfg.max_iter = cfg.inner_max_iter;
@@ -397,8 +401,9 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   if (const char* e = std::getenv("TPGPU_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
   if (const char* e = std::getenv("TPGPU_OMEGA2")) mc.omega2 = std::atof(e);
   // concurrent frequency groups (TPGPU_FREQ_GROUPS overrides; 1 = one solver on the problem stream)
-  int parts = std::getenv("TPGPU_FREQ_GROUPS") ? std::atoi(std::getenv("TPGPU_FREQ_GROUPS")) : 3;
-  parts = std::max(1, std::min(parts, chunk));
+  fw->req_chunk = cfg.freq_chunk;
+  fw->req_groups = want_groups;
+  int parts = std::max(1, std::min(want_groups, chunk));
   fw->parts = parts;
   const int per_group = (chunk + parts - 1) / parts;
   fw->chunk = per_group;
@@ -764,6 +769,7 @@ int tp_m1_begin(tp_problem* h, const tp_solver_cfg* c, double* residual0) {
     tpgpu::validate_cfg(cfg);
     tpgpu::require(p.state_valid, "m1: no state (static_init or set_state first)");
     p.build_frequency_solver(cfg);
+    p.sweep_cfg = cfg;
     p.uhat_valid = false;
     const double r0 = p.residual_and_rhs(true);
     if (residual0) *residual0 = r0;
@@ -774,10 +780,7 @@ int tp_m1_sweep(tp_problem* h, double* residual, int32_t* inner) {
   return guarded([&] {
     Problem& p = P(h);
     tpgpu::require(p.freq_ready, "m1 sweep: call tp_m1_begin first");
-    tp_solver_cfg cfg;
-    tp_solver_cfg_default(&cfg);
-    cfg.inner_rtol = p.fw->solver.cfg.rtol;
-    cfg.inner_max_iter = p.fw->solver.cfg.max_iter;
+    const tp_solver_cfg cfg = p.sweep_cfg;
     tpgpu::SolveStats st;
     p.periodic_solve_dev(cfg, &st);
     const double r = p.residual_and_rhs(true);

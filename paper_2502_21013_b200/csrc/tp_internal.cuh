@@ -173,6 +173,7 @@ class Problem {
   static thread_local cudaStream_t tl_stream;
   cudaStream_t cur_stream() const { return tl_stream ? tl_stream : stream; }
   std::atomic<int64_t> launches{0};
+  tp_solver_cfg sweep_cfg{};  // the configuration tp_m1_begin set up the sweeps with
   int num_sms = 148;
   DevBuf<uint8_t> d_cell_mat;
   DevBuf<double> d_mass;
