@@ -424,6 +424,15 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   uhat_valid = false;
 }
 
+// U_{k+1} = IDFT(U_hat) stays close to U_k near the fixed point, so DFT(U) is
+// a far better first guess for the frequency solves than zero; the solves
+// still converge to the same tolerance (only their iteration count changes).
+void Problem::seed_spectrum() {
+  launch_rdft_forward(*this, U.get(), Uhat.get());
+  if (sharded()) alltoall_to_freq(Uhat.get(), Uhat_f.get());
+  uhat_valid = true;
+}
+
 void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
   build_frequency_solver(cfg);
   launch_rdft_forward(*this, G.get(), Ghat.get());
@@ -772,6 +781,7 @@ int tp_m1_begin(tp_problem* h, const tp_solver_cfg* c, double* residual0) {
     p.sweep_cfg = cfg;
     p.uhat_valid = false;
     const double r0 = p.residual_and_rhs(true);
+    if (cfg.warm_start) p.seed_spectrum();
     if (residual0) *residual0 = r0;
   });
 }
@@ -824,6 +834,7 @@ int tp_solve_m1(tp_problem* h, const tp_solver_cfg* c, const double* U0, double*
       const auto ts = std::chrono::steady_clock::now();
       p.build_frequency_solver(cfg);
       p.uhat_valid = false;
+      if (cfg.warm_start) p.seed_spectrum();
       setup = seconds_since(ts);
       for (int k = 1; k <= cfg.m1_max_outer; ++k) {
         const auto tk = std::chrono::steady_clock::now();

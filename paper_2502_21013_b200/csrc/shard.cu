@@ -179,7 +179,9 @@ void Problem::global_minmax(double* lo, double* hi, int count) {
 // To rank q: rows [ks[q], ks[q+1]) of my Ghat -- contiguous.  From rank q:
 // its strip of my frequencies, (k1-k0) x n_q, received into staging and
 // scattered into the columns [ys[q]*m, ys[q+1]*m) of Ghat_f.
-void Problem::alltoall_to_freq() {
+void Problem::alltoall_to_freq(const cplx* src, cplx* dst) {
+  if (!src) src = Ghat.get();
+  if (!dst) dst = Ghat_f.get();
   const int Kr = sh.k1 - sh.k0;
   ncclComm_t c = comm_of(*this);
   size_t off = 0;
@@ -193,13 +195,13 @@ void Problem::alltoall_to_freq() {
   for (int q = 0; q < sh.P; ++q) {
     const size_t cnt_send = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * 2;  // doubles
     const size_t cnt_recv = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * 2;
-    TP_NCCL(ncclSend(Ghat.get() + (size_t)sh.ks[q] * sh.nr, cnt_send, ncclDouble, q, c, stream));
+    TP_NCCL(ncclSend(src + (size_t)sh.ks[q] * sh.nr, cnt_send, ncclDouble, q, c, stream));
     TP_NCCL(ncclRecv(xstage.get() + soff[q], cnt_recv, ncclDouble, q, c, stream));
   }
   TP_NCCL(ncclGroupEnd());
   for (int q = 0; q < sh.P; ++q) {
     const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
-    TP_CUDA(cudaMemcpy2DAsync(Ghat_f.get() + (size_t)sh.ys[q] * m, (size_t)n * sizeof(cplx), xstage.get() + soff[q],
+    TP_CUDA(cudaMemcpy2DAsync(dst + (size_t)sh.ys[q] * m, (size_t)n * sizeof(cplx), xstage.get() + soff[q],
                               nq * sizeof(cplx), nq * sizeof(cplx), Kr, cudaMemcpyDeviceToDevice, stream));
   }
 }

@@ -210,7 +210,10 @@ class Problem {
   void exchange_halo();
   double global_sum(double local);
   void global_minmax(double* lo, double* hi, int count);
-  void alltoall_to_freq();    // Ghat (K x nr) -> Ghat_f ((k1-k0) x n)
+  void alltoall_to_freq(const cplx* src = nullptr, cplx* dst = nullptr);  // Ghat (K x nr) -> Ghat_f ((k1-k0) x n)
+  // warm start of the first sweep's frequency solves: the spectrum of the
+  // current state U (its frequency blocks) as the initial guess
+  void seed_spectrum();
   void alltoall_from_freq();  // Uhat_f -> Uhat (K x nr)
   void slices_to_strips(const double* Us);  // static-init slices (full grid) -> U strips
   cplx* spec_in() { return sharded() ? Ghat_f.get() : Ghat.get(); }
