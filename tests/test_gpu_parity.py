@@ -228,3 +228,24 @@ def test_sharded_path_single_rank_matches():
     assert reps.iterations == rep.iterations
     assert np.allclose(reps.residual_history, rep.residual_history, rtol=1e-14, atol=0)
     assert rel(Us, U) <= 1e-14
+
+
+@pytest.mark.gpu
+def test_run_cli_writes_reference_formats(tmp_path):
+    """python -m paper_2502_21013_b200.run: report.json / residuals.csv in the
+    reference runner's formats, histories equal to the solve's report."""
+    import csv
+    import json
+    from paper_2502_21013_b200 import run
+    out = tmp_path / "cfg0"
+    rc = run.main(["--config", "0", "--out", str(out), "--tol", "1e-8"])
+    assert rc == 0
+    j = json.loads((out / "report.json").read_text())
+    m1 = j["methods"]["m1"]
+    assert m1["status"] == "converged" and m1["method"] == "m1"
+    assert j["problem"] == "grid" and j["steps"] == 64 and j["n_dof"] == 961
+    assert len(j["frequency_symbol_abs"]) == 33
+    rows = list(csv.reader((out / "residuals.csv").open()))
+    assert rows[0] == ["method", "iteration", "residual", "contraction"]
+    assert len(rows) - 1 == len(m1["residual_history"]) == m1["iterations"] + 1
+    assert rows[1][3] == "" and all(float(r[2]) == h for r, h in zip(rows[1:], m1["residual_history"]))
