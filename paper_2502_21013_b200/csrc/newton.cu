@@ -12,7 +12,9 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdlib>
+#include <memory>
 #include <string>
+#include <thread>
 
 #include "mg.cuh"
 
@@ -20,7 +22,7 @@ namespace tpgpu {
 
 void newton_residual(Problem& p, const double* Ub, const double* Db, const double* d_alpha, double* Ut,
                      double* Rt, const int* d_slice_of, const int* d_active, int batches,
-                     double* norms2_host);
+                     double* norms2_host, DevBuf<double>& part, DevBuf<double>& red);
 
 namespace {
 __global__ void k_accept(double* __restrict__ Ub, double* __restrict__ Rb, const double* __restrict__ Ut,
@@ -33,6 +35,17 @@ __global__ void k_accept(double* __restrict__ Ub, double* __restrict__ Rb, const
   }
 }
 }  // namespace
+
+// One group of slices [g0, g1): its own buffers, batch solver and (when the
+// slices are split into concurrent groups) its own stream / host thread.
+struct NewtonGroup {
+  int S = 0;  // slices per batch
+  DevBuf<double> Ub, Rb, Db, Ut, Rt, inv, part, red;
+  std::vector<DevBuf<double>> J;
+  DevBuf<int> d_slice, d_active, d_acc;
+  DevBuf<double> d_alpha;
+  BatchSolver<1> solver;
+};
 
 void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) {
   // geometry of the hierarchy
@@ -52,15 +65,14 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   const int Nr = sh.s1 - sh.s0;
   int S = cfg.slice_chunk > 0 ? cfg.slice_chunk : (int)std::min<size_t>(Nr, (size_t)(0.5 * free_b) / per_slice);
   S = std::max(1, std::min(S, Nr));
+  // optional concurrent slice groups (TPGPU_SLICE_GROUPS, as the frequency
+  // groups of the periodic solve).  Off by default: the Newton loop is a chain
+  // of short launches and host decisions, and concurrent host threads measured
+  // slower at cfg 1 (0.31-0.96 s vs 0.20 s) and no faster at cfg 2.
+  const int want = std::getenv("TPGPU_SLICE_GROUPS") ? std::atoi(std::getenv("TPGPU_SLICE_GROUPS")) : 1;
+  const int G = std::max(1, std::min(want, S));
+  const int Sg = (S + G - 1) / G;
 
-  DevBuf<double> Ub((size_t)S * n), Rb((size_t)S * n), Db((size_t)S * n), Ut((size_t)S * n), Rt((size_t)S * n);
-  std::vector<DevBuf<double>> J(nl);
-  for (int l = 0; l < nl; ++l) J[l].alloc((size_t)S * 7 * ms[l] * ms[l]);
-  DevBuf<double> inv((size_t)S * nL * nL);
-  DevBuf<int> d_slice(S), d_active(S), d_acc(S);
-  DevBuf<double> d_alpha(S);
-  std::vector<LevelOp> ops(nl);
-  for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], J[l].get(), nullptr, false, {}};
   MGConfig mc;
   // Newton steps are solved to the reference SparseSolver's own residual
   // contract (1e-10, solve.hpp:79-89) -- tighter buys nothing: Newton counts
@@ -74,101 +86,159 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   // frequency solver assumes a spectrum in (0, 2]).
   mc.omega = mc.omega2 = 0.6;
   if (const char* e = std::getenv("TPGPU_NEWTON_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
-  BatchSolver<1> solver;
-  solver.init(this, ops, S, mc);
-  solver.coarse_inv = inv.get();
 
-  std::vector<int> h_slice(S), h_active(S), h_acc(S), counts(N, 0);
-  std::vector<double> h_alpha(S), rnorm(S), scale(S), nrm2(S);
+  std::vector<std::unique_ptr<NewtonGroup>> groups(G);
+  for (auto& gp : groups) {
+    gp = std::make_unique<NewtonGroup>();
+    NewtonGroup& g = *gp;
+    g.S = Sg;
+    for (auto* b : {&g.Ub, &g.Rb, &g.Db, &g.Ut, &g.Rt}) b->alloc((size_t)Sg * n);
+    g.J.resize(nl);
+    for (int l = 0; l < nl; ++l) g.J[l].alloc((size_t)Sg * 7 * ms[l] * ms[l]);
+    g.inv.alloc((size_t)Sg * nL * nL);
+    g.d_slice.alloc(Sg);
+    g.d_active.alloc(Sg);
+    g.d_acc.alloc(Sg);
+    g.d_alpha.alloc(Sg);
+    std::vector<LevelOp> ops(nl);
+    for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], g.J[l].get(), nullptr, false, {}};
+    g.solver.init(this, ops, Sg, mc);
+    g.solver.coarse_inv = g.inv.get();
+  }
+  std::vector<int> counts(N, 0);
   // slices of this rank (all of them on a single GPU); sharded problems
   // solve their slice block on the full grid and redistribute to strips
   DevBuf<double> Us;
   if (sharded()) Us.alloc((size_t)(sh.s1 - sh.s0) * n);
-  for (int s0 = sh.s0; s0 < sh.s1; s0 += S) {
-    const int nb = std::min(S, sh.s1 - s0);
-    for (int b = 0; b < S; ++b) {
-      h_slice[b] = std::min(s0 + b, N - 1);
-      h_active[b] = b < nb;
-    }
-    TP_CUDA(cudaMemcpyAsync(d_slice.get(), h_slice.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
-    TP_CUDA(cudaMemcpyAsync(d_active.get(), h_active.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
-    TP_CUDA(cudaMemsetAsync(Ub.get(), 0, Ub.bytes(), stream));
-    // r = f - K(0) = f ; scale = max(||f||, ||r||)  (solvers.hpp:148-152)
-    newton_residual(*this, Ub.get(), nullptr, nullptr, nullptr, Rb.get(), d_slice.get(), d_active.get(), S,
-                    nrm2.data());
-    for (int b = 0; b < nb; ++b) {
-      rnorm[b] = std::sqrt(nrm2[b]);
-      scale[b] = std::max(rnorm[b], rnorm[b]);
-      if (scale[b] == 0 || rnorm[b] <= cfg.static_tol * scale[b]) h_active[b] = 0;
-    }
-    for (int step = 1; step <= cfg.static_max_newton; ++step) {
-      int n_active = 0;
-      for (int b = 0; b < nb; ++b) n_active += h_active[b];
-      if (n_active == 0) break;
-      TP_CUDA(cudaMemcpyAsync(d_active.get(), h_active.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
-      // J(u) for the batch, Galerkin hierarchy, coarsest inverses
-      launch_element_stencil(*this, true, Ub.get(), J[0].get(), nb);
-      for (int l = 1; l < nl; ++l) launch_rap(*this, J[l - 1].get(), ms[l - 1], J[l].get(), ms[l], nb);
-      launch_coarse_inverse_slice(*this, J[nl - 1].get(), ms[nl - 1], inv.get(), nb);
-      // delta = J^{-1} r  (masked to the active slices)
-      solver.ext_mask = d_active.get();
-      SolveStats st;
-      solver.solve(Rb.get(), Db.get(), nb, false, &st);
-      solver.ext_mask = nullptr;
-      // Armijo backtracking (solvers.hpp:158-177)
-      for (int b = 0; b < S; ++b) {
-        h_alpha[b] = 1.0;
-        h_acc[b] = 0;
+
+  // damped Newton over the slices [r0, r1) of this rank, batches of g.S
+  auto run_group = [&](NewtonGroup& g, int r0, int r1) {
+    const int Sb = g.S;
+    cudaStream_t s = cur_stream();
+    std::vector<int> h_slice(Sb), h_active(Sb), h_acc(Sb);
+    std::vector<double> h_alpha(Sb), rnorm(Sb), scale(Sb), nrm2(Sb);
+    for (int s0 = r0; s0 < r1; s0 += Sb) {
+      const int nb = std::min(Sb, r1 - s0);
+      for (int b = 0; b < Sb; ++b) {
+        h_slice[b] = std::min(s0 + b, N - 1);
+        h_active[b] = b < nb;
       }
-      std::vector<int> searching(h_active.begin(), h_active.end());
-      for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
-        int any = 0;
-        for (int b = 0; b < nb; ++b) any += searching[b];
-        if (!any) break;
-        TP_CUDA(cudaMemcpyAsync(d_alpha.get(), h_alpha.data(), S * sizeof(double), cudaMemcpyHostToDevice, stream));
-        TP_CUDA(cudaMemcpyAsync(d_acc.get(), searching.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
-        newton_residual(*this, Ub.get(), Db.get(), d_alpha.get(), Ut.get(), Rt.get(), d_slice.get(),
-                        d_acc.get(), S, nrm2.data());
-        std::vector<int> accept(S, 0);
+      TP_CUDA(cudaMemcpyAsync(g.d_slice.get(), h_slice.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+      TP_CUDA(cudaMemcpyAsync(g.d_active.get(), h_active.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+      TP_CUDA(cudaMemsetAsync(g.Ub.get(), 0, g.Ub.bytes(), s));
+      // r = f - K(0) = f ; scale = max(||f||, ||r||)  (solvers.hpp:148-152)
+      newton_residual(*this, g.Ub.get(), nullptr, nullptr, nullptr, g.Rb.get(), g.d_slice.get(), g.d_active.get(),
+                      Sb, nrm2.data(), g.part, g.red);
+      for (int b = 0; b < nb; ++b) {
+        rnorm[b] = std::sqrt(nrm2[b]);
+        scale[b] = std::max(rnorm[b], rnorm[b]);
+        if (scale[b] == 0 || rnorm[b] <= cfg.static_tol * scale[b]) h_active[b] = 0;
+      }
+      for (int step = 1; step <= cfg.static_max_newton; ++step) {
+        int n_active = 0;
+        for (int b = 0; b < nb; ++b) n_active += h_active[b];
+        if (n_active == 0) break;
+        TP_CUDA(cudaMemcpyAsync(g.d_active.get(), h_active.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+        // J(u) for the batch, Galerkin hierarchy, coarsest inverses
+        launch_element_stencil(*this, true, g.Ub.get(), g.J[0].get(), nb);
+        for (int l = 1; l < nl; ++l) launch_rap(*this, g.J[l - 1].get(), ms[l - 1], g.J[l].get(), ms[l], nb);
+        launch_coarse_inverse_slice(*this, g.J[nl - 1].get(), ms[nl - 1], g.inv.get(), nb);
+        // delta = J^{-1} r  (masked to the active slices)
+        g.solver.ext_mask = g.d_active.get();
+        SolveStats st;
+        g.solver.solve(g.Rb.get(), g.Db.get(), nb, false, &st);
+        g.solver.ext_mask = nullptr;
+        // Armijo backtracking (solvers.hpp:158-177)
+        for (int b = 0; b < Sb; ++b) {
+          h_alpha[b] = 1.0;
+          h_acc[b] = 0;
+        }
+        std::vector<int> searching(h_active.begin(), h_active.end());
+        for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
+          int any = 0;
+          for (int b = 0; b < nb; ++b) any += searching[b];
+          if (!any) break;
+          TP_CUDA(cudaMemcpyAsync(g.d_alpha.get(), h_alpha.data(), Sb * sizeof(double), cudaMemcpyHostToDevice, s));
+          TP_CUDA(cudaMemcpyAsync(g.d_acc.get(), searching.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+          newton_residual(*this, g.Ub.get(), g.Db.get(), g.d_alpha.get(), g.Ut.get(), g.Rt.get(), g.d_slice.get(),
+                          g.d_acc.get(), Sb, nrm2.data(), g.part, g.red);
+          std::vector<int> accept(Sb, 0);
+          for (int b = 0; b < nb; ++b) {
+            if (!searching[b]) continue;
+            const double tnorm = std::sqrt(nrm2[b]);
+            if (tnorm <= (1.0 - cfg.armijo_slope * h_alpha[b]) * rnorm[b]) {
+              accept[b] = 1;
+              rnorm[b] = tnorm;
+              h_acc[b] = 1;
+              searching[b] = 0;
+            } else {
+              h_alpha[b] *= cfg.armijo_backtrack;
+            }
+          }
+          TP_CUDA(cudaMemcpyAsync(g.d_acc.get(), accept.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+          dim3 gr((unsigned)std::min<size_t>((n + 255) / 256, 1024), Sb);
+          k_accept<<<gr, 256, 0, s>>>(g.Ub.get(), g.Rb.get(), g.Ut.get(), g.Rt.get(), g.d_acc.get(), n);
+          TP_LAUNCHED(this);
+          TP_CUDA(cudaStreamSynchronize(s));
+        }
         for (int b = 0; b < nb; ++b) {
-          if (!searching[b]) continue;
-          const double tnorm = std::sqrt(nrm2[b]);
-          if (tnorm <= (1.0 - cfg.armijo_slope * h_alpha[b]) * rnorm[b]) {
-            accept[b] = 1;
-            rnorm[b] = tnorm;
-            h_acc[b] = 1;
-            searching[b] = 0;
-          } else {
-            h_alpha[b] *= cfg.armijo_backtrack;
+          if (!h_active[b]) continue;
+          if (!h_acc[b])
+            throw Error(TP_ESOLVE,
+                        "static init, step " + std::to_string(s0 + b + 1) +
+                            ": newton: line search exhausted at residual " + std::to_string(rnorm[b]),
+                        rnorm[b] / scale[b]);
+          if (rnorm[b] <= cfg.static_tol * scale[b]) {
+            counts[s0 + b] = step;
+            h_active[b] = 0;
           }
         }
-        TP_CUDA(cudaMemcpyAsync(d_acc.get(), accept.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
-        dim3 g((unsigned)std::min<size_t>((n + 255) / 256, 1024), S);
-        k_accept<<<g, 256, 0, stream>>>(Ub.get(), Rb.get(), Ut.get(), Rt.get(), d_acc.get(), n);
-        TP_LAUNCHED(this);
-        TP_CUDA(cudaStreamSynchronize(stream));
       }
-      for (int b = 0; b < nb; ++b) {
-        if (!h_active[b]) continue;
-        if (!h_acc[b])
+      for (int b = 0; b < nb; ++b)
+        if (h_active[b])
           throw Error(TP_ESOLVE,
-                      "static init, step " + std::to_string(s0 + b + 1) +
-                          ": newton: line search exhausted at residual " + std::to_string(rnorm[b]),
+                      "static init, step " + std::to_string(s0 + b + 1) + ": newton: no convergence within " +
+                          std::to_string(cfg.static_max_newton) + " steps",
                       rnorm[b] / scale[b]);
-        if (rnorm[b] <= cfg.static_tol * scale[b]) {
-          counts[s0 + b] = step;
-          h_active[b] = 0;
-        }
-      }
+      double* dst = sharded() ? Us.get() + (size_t)(s0 - sh.s0) * n : U.get() + (size_t)s0 * n;
+      TP_CUDA(cudaMemcpyAsync(dst, g.Ub.get(), (size_t)nb * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
-    for (int b = 0; b < nb; ++b)
-      if (h_active[b])
-        throw Error(TP_ESOLVE,
-                    "static init, step " + std::to_string(s0 + b + 1) + ": newton: no convergence within " +
-                        std::to_string(cfg.static_max_newton) + " steps",
-                    rnorm[b] / scale[b]);
-    double* dst = sharded() ? Us.get() + (size_t)(s0 - sh.s0) * n : U.get() + (size_t)s0 * n;
-    TP_CUDA(cudaMemcpyAsync(dst, Ub.get(), (size_t)nb * n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    TP_CUDA(cudaStreamSynchronize(s));
+  };
+
+  if (G == 1) {
+    run_group(*groups[0], sh.s0, sh.s1);
+  } else {
+    // contiguous slice ranges per group, each on its own stream and host thread
+    std::vector<cudaStream_t> hs(G, nullptr);
+    for (auto& h : hs) TP_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
+    cudaEvent_t ev = nullptr;
+    TP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+    TP_CUDA(cudaEventRecord(ev, stream));
+    for (auto h : hs) TP_CUDA(cudaStreamWaitEvent(h, ev, 0));
+    std::vector<std::exception_ptr> err(G);
+    auto body = [&](int gi) {
+      const int r0 = sh.s0 + (int)((long)Nr * gi / G), r1 = sh.s0 + (int)((long)Nr * (gi + 1) / G);
+      try {
+        if (gi > 0) TP_CUDA(cudaSetDevice(device));
+        tl_stream = hs[gi];
+        run_group(*groups[gi], r0, r1);
+      } catch (...) {
+        err[gi] = std::current_exception();
+      }
+      tl_stream = nullptr;
+    };
+    std::vector<std::thread> th;
+    for (int gi = 1; gi < G; ++gi) th.emplace_back(body, gi);
+    body(0);
+    for (auto& t : th) t.join();
+    for (auto h : hs) {
+      TP_CUDA(cudaStreamSynchronize(h));
+      cudaStreamDestroy(h);
+    }
+    cudaEventDestroy(ev);
+    for (auto& e : err)
+      if (e) std::rethrow_exception(e);
   }
   TP_CUDA(cudaStreamSynchronize(stream));
   if (sharded()) slices_to_strips(Us.get());

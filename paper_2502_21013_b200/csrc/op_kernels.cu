@@ -473,10 +473,10 @@ void Problem::residual_dev(const double* u, double* r, int count_slices) {
 void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches) {
   dim3 grid((p.n + 255) / 256, 1, batches);
   if (jacobian)
-    k_element_stencil<true><<<grid, 256, 0, p.stream>>>(U, st, p.m, p.c, p.d_cell_mat.get(),
+    k_element_stencil<true><<<grid, 256, 0, p.cur_stream()>>>(U, st, p.m, p.c, p.d_cell_mat.get(),
                                                          p.d_mat.get(), nullptr);
   else
-    k_element_stencil<false><<<grid, 256, 0, p.stream>>>(nullptr, st, p.m, p.c, p.d_cell_mat.get(),
+    k_element_stencil<false><<<grid, 256, 0, p.cur_stream()>>>(nullptr, st, p.m, p.c, p.d_cell_mat.get(),
                                                           p.d_mat.get(), p.d_nu_hat.get());
   TP_LAUNCHED(&p);
 }
@@ -545,20 +545,20 @@ __global__ void k_reduce_batches(const double* __restrict__ part, int per, doubl
 // host `norms2` (synchronising).
 void newton_residual(Problem& p, const double* Ub, const double* Db, const double* d_alpha,
                      double* Ut, double* Rt, const int* d_slice_of, const int* d_active, int batches,
-                     double* norms2_host) {
+                     double* norms2_host, DevBuf<double>& part, DevBuf<double>& red) {
   dim3 grid((p.m + TX - 1) / TX, (p.m + TY - 1) / TY, batches);
   const int per = grid.x * grid.y;
-  p.part.ensure((size_t)per * batches);
-  p.red.ensure(batches + 16);
-  k_newton_residual<<<grid, dim3(TX, TY), 0, p.stream>>>(
-      Ub, Db, d_alpha, Ut, Rt, p.part.get(), d_slice_of, d_active, p.m, p.c, p.d_cell_mat.get(),
+  part.ensure((size_t)per * batches);
+  red.ensure(batches + 16);
+  cudaStream_t s = p.cur_stream();
+  k_newton_residual<<<grid, dim3(TX, TY), 0, s>>>(
+      Ub, Db, d_alpha, Ut, Rt, part.get(), d_slice_of, d_active, p.m, p.c, p.d_cell_mat.get(),
       p.d_mat.get(), p.d_src_prof.get(), p.d_src_time.get(), (int)p.src_mats.size());
   TP_LAUNCHED(&p);
-  k_reduce_batches<<<batches, 256, 0, p.stream>>>(p.part.get(), per, p.red.get());
+  k_reduce_batches<<<batches, 256, 0, s>>>(part.get(), per, red.get());
   TP_LAUNCHED(&p);
-  TP_CUDA(cudaMemcpyAsync(norms2_host, p.red.get(), sizeof(double) * batches, cudaMemcpyDeviceToHost,
-                          p.stream));
-  TP_CUDA(cudaStreamSynchronize(p.stream));
+  TP_CUDA(cudaMemcpyAsync(norms2_host, red.get(), sizeof(double) * batches, cudaMemcpyDeviceToHost, s));
+  TP_CUDA(cudaStreamSynchronize(s));
 }
 
 // per-material min/max of |grad u| over all slices of the device state
