@@ -1150,6 +1150,18 @@ static void set_fused_attrs() {
   done = true;
 }
 
+// slice mode: levels with at least 15 nodes per side run the streaming passes
+// (TPGPU_TILE_SLICE: the 32x8-tile kernels everywhere)
+template <int MODE>
+bool BatchSolver<MODE>::stream_level(int l) const {
+  if constexpr (MODE == 1) {
+    static const bool tile = std::getenv("TPGPU_TILE_SLICE") != nullptr;
+    return !tile && l + 1 < (int)ops.size() && ops[l].m >= 15;
+  } else {
+    return false;
+  }
+}
+
 template <int MODE>
 typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, const T* bl, T*, bool,
                                                               bool dot) {
@@ -1273,6 +1285,28 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
   static const bool tile_coarse = std::getenv("TPGPU_TILE_COARSE") != nullptr;
   static const bool coarse_j1 = std::getenv("TPGPU_COARSE_J1") != nullptr;
   const bool j1 = coarse_j1 && l > 0;
+  if constexpr (MODE == 1) {
+    // slice mode: warp-streaming passes over the per-slice Jacobian stencils
+    if (stream_level(l)) {
+      FineOp so;
+      so.K = ops[l].K;
+      so.kstride = (size_t)7 * ops[l].n;
+      so.m = ops[l].m;
+      so.n = ops[l].n;
+      launch_stream_down(*p, so, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, cfg.omega2, nb);
+      T* xs;
+      if (l + 1 == L - 1) {
+        k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
+        TP_LAUNCHED(p);
+        xs = lz0[l + 1].get();
+      } else {
+        xs = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
+      }
+      launch_stream_up(*p, so, bl, z2, xs, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0,
+                       part.get());
+      return zo;
+    }
+  }
   if constexpr (MODE == 0) {
     // Galerkin levels of the frequency solver: warp-streaming passes
     if (!ops[l].five && !j1 && !tile_coarse && ops[l].m >= 7) {
@@ -1334,7 +1368,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   // partials per batch of each producing kernel
   const int per_t = g0.tiles;
   const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
-  const int per_u = fine ? fine_partials(ops[0].m, 2) : per_t;   // V-cycle dot (up)
+  const int per_u = (fine || stream_level(0)) ? fine_partials(ops[0].m, 2) : per_t;  // V-cycle dot (up)
   // fine level: the ring-staged streaming apply (mg_fine.cu) -- measured 8.08
   // vs 8.39 ms per cfg-1 sweep against the smem-tile apply (TPGPU_TILE_APPLY)
   static const bool use_stream_apply = std::getenv("TPGPU_TILE_APPLY") == nullptr;

@@ -37,8 +37,9 @@ struct FineOp {
   const double* we = nullptr;     // (cells+1)^2 vertex grid: K_hat edge weight (X,Y)-(X+1,Y)
   const double* wn = nullptr;     // (cells+1)^2 vertex grid: K_hat edge weight (X,Y)-(X,Y+1)
   const double* mass = nullptr;   // n
-  const double* K = nullptr;      // Galerkin levels: 7n
+  const double* K = nullptr;      // Galerkin levels: 7n (slice mode: per-slice Jacobians, stride kstride)
   const double* M = nullptr;      // Galerkin levels: 7n
+  size_t kstride = 0;             // slice mode: coefficients per batch (7n)
   const cplx* lam = nullptr;      // per batch symbol
   int m = 0, c = 0, n = 0;
 };
@@ -102,6 +103,7 @@ struct BatchSolver {
   void vcycle(int lvl, int nb, T* z_out_level0, bool dot);
   T* vcycle_level(int lvl, int nb, const T* bl, T* z_first, bool first_done, bool dot);
   T* vcycle_generic(int lvl, int nb, const T* bl, bool dot);
+  bool stream_level(int l) const;  // slice mode: this level's passes run streamed
   // fine streaming level: down pass (optionally fusing r_out = r_in - alpha q),
   // and the rest of the cycle (coarse levels + up pass)
   void fine_down0(int nb, const T* r_in, const T* qv = nullptr, T* r_out = nullptr);
@@ -128,6 +130,11 @@ void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, c
                         const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
 void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
+// slice mode: real vectors, per-slice Jacobian stencils
+void launch_stream_down(Problem& p, const FineOp& op, const double* r, double* z2, double* bc, int mc,
+                        const int* active, double om1, double om2, int nb);
+void launch_stream_up(Problem& p, const FineOp& op, const double* r, const double* z2, const double* xc, int mc,
+                      double* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).
 void launch_element_stencil(Problem& p, bool jacobian, const double* U, double* st, int batches);
 

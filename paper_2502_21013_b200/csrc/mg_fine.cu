@@ -42,57 +42,6 @@ __device__ __forceinline__ cplx shf_dn(cplx v) {
   return {__shfl_down_sync(0xffffffffu, v.re, 1), __shfl_down_sync(0xffffffffu, v.im, 1)};
 }
 
-// Per-row coefficients of the lane's node: K_hat edge weights to E/W/N/S
-// (the diagonal is their sum) and the lumped mass.  op.we / op.wn are
-// (c+1)^2 vertex grids: we[Y][X] = weight of the edge (X,Y)-(X+1,Y),
-// wn[Y][X] = weight of the edge (X,Y)-(X,Y+1); node (x,y) is vertex (x+1,y+1).
-struct RowK {
-  double we, ww, wn, ws, mm;
-};
-
-// Load the lane's row-y coefficients; ws comes from the previous row's wn,
-// ww from the west lane's we (warp shuffle, all lanes participate).
-__device__ __forceinline__ RowK row_k(const FineOp& op, int x, int y, double wn_prev) {
-  const int c = op.c, m = op.m;
-  const int X = min(max(x + 1, 0), c), Y = min(max(y + 1, 0), c);
-  const size_t v = (size_t)Y * (c + 1) + X;
-  RowK k;
-  k.we = __ldg(op.we + v);
-  k.wn = __ldg(op.wn + v);
-  k.ww = __shfl_up_sync(0xffffffffu, k.we, 1);
-  k.ws = wn_prev;
-  k.mm = (x >= 0 && x < m && y >= 0 && y < m) ? __ldg(op.mass + (size_t)y * m + x) : 0.0;
-  return k;
-}
-// Compact per-row window entry: the lane's own we, wn and mass.
-struct RowW {
-  double we, wn, mm;
-};
-__device__ __forceinline__ RowW row_w(const FineOp& op, int x, int y) {
-  const int c = op.c, m = op.m;
-  const int X = min(max(x + 1, 0), c), Y = min(max(y + 1, 0), c);
-  const size_t v = (size_t)Y * (c + 1) + X;
-  RowW w;
-  w.we = __ldg(op.we + v);
-  w.wn = __ldg(op.wn + v);
-  w.mm = (x >= 0 && x < m && y >= 0 && y < m) ? __ldg(op.mass + (size_t)y * m + x) : 0.0;
-  return w;
-}
-// full coefficients of a row from its window entry and the row below (all lanes call)
-__device__ __forceinline__ RowK expand(const RowW& w, const RowW& below) {
-  return {w.we, __shfl_up_sync(0xffffffffu, w.we, 1), w.wn, below.wn, w.mm};
-}
-// wn of row y-1 for the first row of a chunk
-__device__ __forceinline__ double wn_of(const FineOp& op, int x, int y) {
-  const int c = op.c;
-  const int X = min(max(x + 1, 0), c), Y = min(max(y + 1, 0), c);
-  return __ldg(op.wn + (size_t)Y * (c + 1) + X);
-}
-
-__device__ __forceinline__ cplx diag(const RowK& k, cplx l) {
-  const double kc = (k.we + k.ww) + (k.wn + k.ws);
-  return {fma(l.re, k.mm, kc), l.im * k.mm};
-}
 // 1/a for the smoothers' D^-1.  TPGPU_FAST_RCP: hardware reciprocal estimate
 // + one Newton step (~46 bits, no special-case path); the V-cycle stays one
 // fixed symmetric operator (every pass uses this same function), only D^-1 is
@@ -115,14 +64,24 @@ __device__ __forceinline__ cplx rcp(cplx a) {
   return {a.re * d, -a.im * d};
 }
 
-// (A v) at a node: d v - wE vE - wW vW - wN vN - wS vS (neighbours of
-// Dirichlet vertices are zero vectors, their edge weights stay on the diagonal)
-__device__ __forceinline__ cplx apply_at(const RowK& k, cplx l, cplx v, cplx vw, cplx ve, cplx vs, cplx vn) {
-  cplx acc = cm(diag(k, l), v);
-  acc.re -= k.we * ve.re + k.ww * vw.re + k.wn * vn.re + k.ws * vs.re;
-  acc.im -= k.we * ve.im + k.ww * vw.im + k.wn * vn.im + k.ws * vs.im;
-  return acc;
+// ---- the same operations on real values (slice mode: Newton Jacobians)
+__device__ __forceinline__ double cm(double a, double b) { return a * b; }
+__device__ __forceinline__ double cs(double s, double a) { return s * a; }
+__device__ __forceinline__ double shf_up(double v) { return __shfl_up_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double shf_dn(double v) { return __shfl_down_sync(0xffffffffu, v, 1); }
+__device__ __forceinline__ double rcp(double a) { return drcp(a); }
+// a x + y, componentwise fma
+__device__ __forceinline__ cplx fmav(double a, cplx x, cplx y) { return {fma(a, x.re, y.re), fma(a, x.im, y.im)}; }
+__device__ __forceinline__ double fmav(double a, double x, double y) { return fma(a, x, y); }
+// bilinear partial sums x^T y (the COCG dot: (re, im); real: (value, 0))
+__device__ __forceinline__ void dot_acc(cplx x, cplx y, double& s0, double& s1) {
+  const cplx t = cm(x, y);
+  s0 += t.re;
+  s1 += t.im;
 }
+__device__ __forceinline__ void dot_acc(double x, double y, double& s0, double&) { s0 += x * y; }
+__device__ __forceinline__ double sq_acc(cplx v, double s) { return fma(v.re, v.re, fma(v.im, v.im, s)); }
+__device__ __forceinline__ double sq_acc(double v, double s) { return fma(v, v, s); }
 
 __device__ __forceinline__ void warp_pair(double& a, double& b) {
   for (int o = 16; o > 0; o >>= 1) {
@@ -134,32 +93,6 @@ __device__ __forceinline__ void warp_pair(double& a, double& b) {
 struct Item {
   int b, strip, chunk, ys, ye, xs;
   bool ok;
-};
-
-// warp work item: ((b * nch) + chunk) * ns + strip
-__device__ __forceinline__ Item item_of(int m, int own, int nb, const int* __restrict__ active) {
-  Item it;
-  const int w = blockIdx.x * WPB + (threadIdx.x >> 5);
-  const int ns = (m + own - 1) / own, nch = (m + RH - 1) / RH;
-  it.strip = w % ns;
-  it.chunk = (w / ns) % nch;
-  it.b = w / (ns * nch);
-  it.ok = it.b < nb && (!active || active[it.b]);
-  it.ys = it.chunk * RH;
-  it.ye = min(it.ys + RH, m);
-  it.xs = it.strip * own;
-  return it;
-}
-
-
-// Row-streamed vector access: pointer to (row y, lane column), zero outside.
-struct RowPtr {
-  const cplx* p;  // element (y, x) of the current row (clamped column)
-  int m;
-  bool colok;
-  __device__ __forceinline__ cplx at(int y) const {
-    return (colok && y >= 0 && y < m) ? p[(long)y * m] : cplx{0, 0};
-  }
 };
 
 // ---------------------------------------------------------------- async row ring
@@ -188,10 +121,15 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
-template <int NV>
-struct VRow {  // NV complex values per lane of one staged row
-  cplx v[NV][WL];
+template <class T, int NV>
+struct VRowT {  // NV values per lane of one staged row
+  T v[NV][WL];
 };
+template <int NV>
+using VRow = VRowT<cplx, NV>;
+// stage one vector element per lane (16 B complex, 8 B real)
+__device__ __forceinline__ void cpv(cplx* sdst, const cplx* g, bool ok) { cp16(sdst, g, ok); }
+__device__ __forceinline__ void cpv(double* sdst, const double* g, bool ok) { cp8(sdst, g, ok); }
 template <int NW>
 struct WRow {  // NW coefficient doubles per lane of one staged row
   double w[NW][WL];
@@ -202,13 +140,14 @@ struct WRow {  // NW coefficient doubles per lane of one staged row
 // outside the stored grid are zero-filled).  diag / apply: the diagonal and
 // the operator at row y from the staged rows y (sy) and y-1 (sb).
 struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
+  using T = cplx;
   static constexpr int NW = 3;
   struct Src {
     const double *we, *wn, *mm;  // lane column bases (vertex column x+1 clamped to [0, c])
     int c, m;
     bool colw, colm;
   };
-  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int) {
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int, int) {
     Src s;
     s.c = op.c;
     s.m = op.m;
@@ -267,13 +206,14 @@ struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
 };
 
 struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, NE planes)
+  using T = cplx;
   static constexpr int NW = 8;  // K C E N NE, M C E N NE
   struct Src {
     const double *K, *M;  // lane column bases
     unsigned n;
     bool col;
   };
-  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int) {
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int, int) {
     Src s;
     s.K = op.K + xc;
     s.M = op.M + xc;
@@ -334,9 +274,58 @@ struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, 
   }
 };
 
+// slice mode (static_init Newton): per-slice symmetric 7-point Jacobians J_b
+// (planes C, E, N, NE of the 7n-per-slice stencil), real vectors
+struct SevenJ {
+  using T = double;
+  static constexpr int NW = 4;  // J C E N NE
+  struct Src {
+    const double* J;  // lane column base of this slice's stencil
+    unsigned n;
+    bool col;
+  };
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int, int b) {
+    Src s;
+    s.J = op.K + (size_t)b * op.kstride + xc;
+    s.n = (unsigned)op.n;
+    s.col = x >= 0 && x < op.m;
+    return s;
+  }
+  static __device__ __forceinline__ void stage(WRow<NW>& st, const Src& s, int lane, int, unsigned moff,
+                                               bool rowok) {
+    const bool v = s.col && rowok;
+    const int dirs[4] = {SC, SE_, SN_, SNE};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cp8(&st.w[q][lane], s.J + (dirs[q] * s.n + moff), v);
+  }
+  static constexpr int RETAIN = 3;
+  static constexpr bool XLANE = true;
+  struct Reg {
+    const WRow<NW>* p;   // this row
+    const WRow<NW>* pb;  // the row below
+    int lane;
+  };
+  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane, const Reg& below) {
+    return {&st, below.p, lane};
+  }
+  static __device__ __forceinline__ Reg first(const WRow<NW>& st, int lane) { return {&st, &st, lane}; }
+  static __device__ __forceinline__ double diag(const Reg& y, cplx) { return y.p->w[0][y.lane]; }
+  // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1) (west lane's slots, XLANE)
+  static __device__ __forceinline__ double apply(const Reg& y, cplx, double d, double vs, double v, double vn) {
+    const int ln = y.lane, lw = ln > 0 ? ln - 1 : 0;
+    const double vw = shf_up(v), ve = shf_dn(v), vne = shf_dn(vn), vsw = shf_up(vs);
+    const WRow<NW>& a = *y.p;
+    const WRow<NW>& b = *y.pb;
+    const double off = a.w[1][ln] * ve + a.w[1][lw] * vw + a.w[2][ln] * vn + b.w[2][ln] * vs + a.w[3][ln] * vne +
+                       b.w[3][lw] * vsw;
+    return fma(d, v, off);
+  }
+};
+
 template <class S, int NV, int RA, int WPBK>
 constexpr size_t ring_smem() {
-  return (size_t)WPBK * ((RA + 2) * sizeof(VRow<NV>) + (RA + 2 + S::RETAIN) * sizeof(WRow<S::NW>));
+  return (size_t)WPBK *
+         ((RA + 2) * sizeof(VRowT<typename S::T, NV>) + (RA + 2 + S::RETAIN) * sizeof(WRow<S::NW>));
 }
 
 __device__ __forceinline__ int wrap_inc(int s, int n) { return s + 1 == n ? 0 : s + 1; }
@@ -428,15 +417,16 @@ __device__ __forceinline__ ItemNB<WPBK, NB> item_nb(int m, int own, int rh, int 
 // for the owned rows, partial ||r_new||^2 per warp item), replacing the
 // separate x/r update pass (x is updated in the next apply).
 template <class S, int NB, int RA, int WPBK, bool FUSED = false>
-__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(FineOp op, const cplx* __restrict__ rv,
-                                                                         cplx* __restrict__ z2out,
-                                                                         cplx* __restrict__ bc, int mc, int rh,
-                                                                         const int* __restrict__ active, double om1,
-                                                                         double om2, int nb,
-                                                                         const cplx* __restrict__ qv = nullptr,
-                                                                         const cplx* __restrict__ alpha = nullptr,
-                                                                         cplx* __restrict__ rout = nullptr,
+__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(FineOp op, const typename S::T* __restrict__ rv,
+                                                                         typename S::T* __restrict__ z2out,
+                                                                         typename S::T* __restrict__ bc, int mc,
+                                                                         int rh, const int* __restrict__ active,
+                                                                         double om1, double om2, int nb,
+                                                                         const typename S::T* __restrict__ qv = nullptr,
+                                                                         const typename S::T* __restrict__ alpha = nullptr,
+                                                                         typename S::T* __restrict__ rout = nullptr,
                                                                          double* __restrict__ part = nullptr) {
+  using T = typename S::T;
   static_assert(!FUSED || NB == 1, "fused residual update: one frequency per warp");
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN, NVV = FUSED ? 2 : NB;
@@ -445,19 +435,20 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
   const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<NVV>* const vring = reinterpret_cast<VRow<NVV>*>(fine_smem) + wib * RV;
-  WRow<S::NW>* const wring = reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NVV>)) + wib * RC;
-  const cplx* const qp = FUSED ? qv + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
-  cplx* const ro = FUSED ? rout + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
-  const cplx al = FUSED ? alpha[it.b[0]] : cplx{0, 0};
+  VRowT<T, NVV>* const vring = reinterpret_cast<VRowT<T, NVV>*>(fine_smem) + wib * RV;
+  WRow<S::NW>* const wring =
+      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRowT<T, NVV>)) + wib * RC;
+  const T* const qp = FUSED ? qv + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
+  T* const ro = FUSED ? rout + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
+  const T al = FUSED ? alpha[it.b[0]] : T{};
   double rn2 = 0;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < H + OWN && colok;
   const int xc = min(max(x, 0), m - 1);
-  const cplx* rp[NB];
-  cplx* zo[NB];
-  cplx* bco[NB];
+  const T* rp[NB];
+  T* zo[NB];
+  T* bco[NB];
   cplx l[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
@@ -465,12 +456,12 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
     rp[j] = rv + o + xc;
     zo[j] = z2out + o + xc;
     bco[j] = bc + (size_t)it.b[j] * mc * mc + (x >> 1);
-    l[j] = op.lam[it.b[j]];
+    l[j] = op.lam ? op.lam[it.b[j]] : cplx{0, 0};
   }
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 3, ylast = ye + 2;  // staged rows
   const bool cown = own && (x & 1) && (x >> 1) < mc;  // coarse centre column
-  const typename S::Src src = S::src(op, x, xc, y0);
+  const typename S::Src src = S::src(op, x, xc, y0, it.b[0]);
   int vi = 0, wi = 0; // next ring slots to fill
   // stage row yr (rows outside [0, m) read row 0 / m-1 addresses and are zero-filled)
   auto issue = [&](int yr) {
@@ -478,8 +469,8 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
       const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
       const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
 #pragma unroll
-      for (int j = 0; j < NB; ++j) cp16(&vring[vi].v[j][lane], rp[j] + off, rin);
-      if (FUSED) cp16(&vring[vi].v[1][lane], qp + off, rin);
+      for (int j = 0; j < NB; ++j) cpv(&vring[vi].v[j][lane], rp[j] + off, rin);
+      if (FUSED) cpv(&vring[vi].v[1][lane], qp + off, rin);
       S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
@@ -488,17 +479,17 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
   };
   // pipeline over input rows yi = ys-2 .. ye+2: z1 at yi, z2 at yi-1,
   // residual at yi-2, restriction centred on yi-3
-  cplx r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
-  cplx a0[NB], a1[NB], a2[NB];  // z1 at yi, yi-1, yi-2
-  cplx b1[NB], b2[NB], b3[NB];  // z2 at yi-1, yi-2, yi-3
-  cplx q2[NB], q3[NB], q4[NB];  // res at yi-2, yi-3, yi-4
-  cplx id0[NB], id1[NB];        // 1/d of rows yi, yi-1
-  cplx d0[NB], d1[NB], d2[NB];  // d of rows yi, yi-1, yi-2
+  T r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
+  T a0[NB], a1[NB], a2[NB];  // z1 at yi, yi-1, yi-2
+  T b1[NB], b2[NB], b3[NB];  // z2 at yi-1, yi-2, yi-3
+  T q2[NB], q3[NB], q4[NB];  // res at yi-2, yi-3, yi-4
+  T id0[NB], id1[NB];        // 1/d of rows yi, yi-1
+  T d0[NB], d1[NB], d2[NB];  // d of rows yi, yi-1, yi-2
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
-    r0[j] = r1[j] = r2[j] = a0[j] = a1[j] = a2[j] = cplx{0, 0};
-    b1[j] = b2[j] = b3[j] = q2[j] = q3[j] = q4[j] = id0[j] = id1[j] = cplx{0, 0};
-    d0[j] = d1[j] = d2[j] = cplx{0, 0};
+    r0[j] = r1[j] = r2[j] = a0[j] = a1[j] = a2[j] = T{};
+    b1[j] = b2[j] = b3[j] = q2[j] = q3[j] = q4[j] = id0[j] = id1[j] = T{};
+    d0[j] = d1[j] = d2[j] = T{};
   }
 #pragma unroll
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
@@ -525,12 +516,11 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
     for (int j = 0; j < NB; ++j) {
       r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = vring[vr].v[j][lane];
       if (FUSED) {
-        const cplx qq = vring[vr].v[1][lane];
-        r0[j].re -= al.re * qq.re - al.im * qq.im;
-        r0[j].im -= al.re * qq.im + al.im * qq.re;
+        const T qq = vring[vr].v[1][lane];
+        r0[j] = r0[j] - cm(al, qq);
         if (own && yi >= ys && yi < ye) {
           ro[(long)yi * m] = r0[j];
-          rn2 = fma(r0[j].re, r0[j].re, fma(r0[j].im, r0[j].im, rn2));
+          rn2 = sq_acc(r0[j], rn2);
         }
       }
       // z1 = omega r / d at row yi (off-domain diagonals may vanish: z1 = 0 there)
@@ -539,20 +529,20 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
       d2[j] = d1[j]; d1[j] = d0[j];
       d0[j] = S::diag(k0, l[j]);
       id0[j] = rcp(d0[j]);
-      a0[j] = in0 ? cs(om1, cm(r0[j], id0[j])) : cplx{0, 0};
+      a0[j] = in0 ? cs(om1, cm(r0[j], id0[j])) : T{};
       // z2 at row yi-1
       b3[j] = b2[j]; b2[j] = b1[j];
       {
-        const cplx Aa = S::apply(k1, l[j], d1[j], a2[j], a1[j], a0[j]);
-        const cplx t = cm({r1[j].re - Aa.re, r1[j].im - Aa.im}, id1[j]);
-        b1[j] = in1 ? cplx{fma(om2, t.re, a1[j].re), fma(om2, t.im, a1[j].im)} : cplx{0, 0};
+        const T Aa = S::apply(k1, l[j], d1[j], a2[j], a1[j], a0[j]);
+        const T t = cm(r1[j] - Aa, id1[j]);
+        b1[j] = in1 ? fmav(om2, t, a1[j]) : T{};
         if (st1 && it.on[j]) zo[j][(long)(yi - 1) * m] = b1[j];
       }
       // residual at row yi-2
       q4[j] = q3[j]; q3[j] = q2[j];
       {
-        const cplx Ab = S::apply(k2, l[j], d2[j], b3[j], b2[j], b1[j]);
-        q2[j] = in2 ? cplx{r2[j].re - Ab.re, r2[j].im - Ab.im} : cplx{0, 0};
+        const T Ab = S::apply(k2, l[j], d2[j], b3[j], b2[j], b1[j]);
+        q2[j] = in2 ? r2[j] - Ab : T{};
       }
     }
     // restriction centred on row yc = yi-3 (odd fine rows 2Y+1; warp-uniform branch)
@@ -564,14 +554,10 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
 #endif
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        const cplx qw = shf_up(q3[j]), qe = shf_dn(q3[j]);
-        const cplx q4w = shf_up(q4[j]), q2e = shf_dn(q2[j]);
-        if ((yc & 1) && yc >= ys && yc < ye && cown && it.on[j] && (yc >> 1) < mc) {
-          cplx acc = q3[j];
-          acc.re += 0.5 * (qw.re + qe.re + q4[j].re + q2[j].re + q4w.re + q2e.re);
-          acc.im += 0.5 * (qw.im + qe.im + q4[j].im + q2[j].im + q4w.im + q2e.im);
-          bco[j][(size_t)(yc >> 1) * mc] = acc;
-        }
+        const T qw = shf_up(q3[j]), qe = shf_dn(q3[j]);
+        const T q4w = shf_up(q4[j]), q2e = shf_dn(q2[j]);
+        if ((yc & 1) && yc >= ys && yc < ye && cown && it.on[j] && (yc >> 1) < mc)
+          bco[j][(size_t)(yc >> 1) * mc] = q3[j] + 0.5 * (qw + qe + q4[j] + q2[j] + q4w + q2e);
       }
     }
   }
@@ -593,13 +579,14 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
 // Staged per row and frequency: r, z2 and the (up to two) coarse values P x_c
 // interpolates from at the lane's node; the coefficient row once.
 template <class S, int NB, int RA, int WPBK>
-__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(FineOp op, const cplx* __restrict__ rv,
-                                                                       const cplx* __restrict__ z2in,
-                                                                       const cplx* __restrict__ xcv, int mc, int rh,
-                                                                       cplx* __restrict__ zout,
+__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(FineOp op, const typename S::T* __restrict__ rv,
+                                                                       const typename S::T* __restrict__ z2in,
+                                                                       const typename S::T* __restrict__ xcv, int mc,
+                                                                       int rh, typename S::T* __restrict__ zout,
                                                                        const int* __restrict__ active, double om1,
                                                                        double om2, int nb, int dot,
                                                                        double* __restrict__ part) {
+  using T = typename S::T;
   constexpr int H = 2, OWN = WL - 2 * H;  // 28
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN;
   extern __shared__ __align__(16) unsigned char fine_smem[];
@@ -607,17 +594,17 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
   const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<4 * NB>* const vring = reinterpret_cast<VRow<4 * NB>*>(fine_smem) + wib * RV;
+  VRowT<T, 4 * NB>* const vring = reinterpret_cast<VRowT<T, 4 * NB>*>(fine_smem) + wib * RV;
   WRow<S::NW>* const wring =
-      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<4 * NB>)) + wib * RC;
+      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRowT<T, 4 * NB>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
   const int xc = min(max(x, 0), m - 1);
-  const cplx* rp[NB];
-  const cplx* zp[NB];
-  const cplx* xb[NB];
-  cplx* zo[NB];
+  const T* rp[NB];
+  const T* zp[NB];
+  const T* xb[NB];
+  T* zo[NB];
   cplx l[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
@@ -626,7 +613,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
     zp[j] = z2in + o + xc;
     zo[j] = zout + o + xc;
     xb[j] = xcv + (size_t)it.b[j] * mc * mc;
-    l[j] = op.lam[it.b[j]];
+    l[j] = op.lam ? op.lam[it.b[j]] : cplx{0, 0};
   }
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 3, ylast = ye + 1;
@@ -636,7 +623,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
   const bool ao = a & 1;
   const int A2 = ao ? ah + 1 : ah;
   const bool cA1 = colok && ah >= 1 && ah <= mc, cA2 = colok && A2 >= 1 && A2 <= mc;
-  const typename S::Src src = S::src(op, x, xc, y0);
+  const typename S::Src src = S::src(op, x, xc, y0, it.b[0]);
   int vi = 0, wi = 0;
   auto issue = [&](int yr) {
     if (TPGPU_ISSUE_ALWAYS || yr <= ylast) {
@@ -650,13 +637,13 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
       const bool ok1 = rin && cA1 && bh >= 1 && bh <= mc;
       const bool ok2 = rin && has2 && cA2 && B2 >= 1 && B2 <= mc;
       const unsigned c1 = ok1 ? (bh - 1) * mc + (ah - 1) : 0, c2 = ok2 ? (B2 - 1) * mc + (A2 - 1) : 0;
-      VRow<4 * NB>& sv = vring[vi];
+      VRowT<T, 4 * NB>& sv = vring[vi];
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        cp16(&sv.v[4 * j][lane], rp[j] + off, rin);
-        cp16(&sv.v[4 * j + 1][lane], zp[j] + off, rin);
-        cp16(&sv.v[4 * j + 2][lane], xb[j] + c1, ok1);
-        cp16(&sv.v[4 * j + 3][lane], xb[j] + c2, ok2);
+        cpv(&sv.v[4 * j][lane], rp[j] + off, rin);
+        cpv(&sv.v[4 * j + 1][lane], zp[j] + off, rin);
+        cpv(&sv.v[4 * j + 2][lane], xb[j] + c1, ok1);
+        cpv(&sv.v[4 * j + 3][lane], xb[j] + c2, ok2);
       }
       S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
@@ -665,16 +652,16 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
     cp_commit();
   };
   // pipeline over input rows yi = ys-2 .. ye+1: zc at yi, z3 at yi-1, z4 at yi-2
-  cplx c0[NB], c1[NB], c2[NB];  // zc at yi, yi-1, yi-2
-  cplx r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
-  cplx e1[NB], e2[NB], e3[NB];  // z3 at yi-1, yi-2, yi-3
-  cplx jd1[NB], jd2[NB];        // 1/d of rows yi-1, yi-2
-  cplx dd1[NB], dd2[NB];        // d of rows yi-1, yi-2
+  T c0[NB], c1[NB], c2[NB];  // zc at yi, yi-1, yi-2
+  T r0[NB], r1[NB], r2[NB];  // r at yi, yi-1, yi-2
+  T e1[NB], e2[NB], e3[NB];  // z3 at yi-1, yi-2, yi-3
+  T jd1[NB], jd2[NB];        // 1/d of rows yi-1, yi-2
+  T dd1[NB], dd2[NB];        // d of rows yi-1, yi-2
   double p0[NB], p1[NB];
 #pragma unroll
   for (int j = 0; j < NB; ++j) {
-    c0[j] = c1[j] = c2[j] = r0[j] = r1[j] = r2[j] = cplx{0, 0};
-    e1[j] = e2[j] = e3[j] = jd1[j] = jd2[j] = dd1[j] = dd2[j] = cplx{0, 0};
+    c0[j] = c1[j] = c2[j] = r0[j] = r1[j] = r2[j] = T{};
+    e1[j] = e2[j] = e3[j] = jd1[j] = jd2[j] = dd1[j] = dd2[j] = T{};
     p0[j] = p1[j] = 0;
   }
 #pragma unroll
@@ -690,7 +677,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
     if (S::XLANE) __syncwarp();
-    const VRow<4 * NB>& sv = vring[vr];
+    const VRowT<T, 4 * NB>& sv = vring[vr];
     const double wc1 = (!ao && !((yi + 1) & 1)) ? 1.0 : 0.5;
     k2 = k1; k1 = k0;
     k0 = S::load(wring[sr], lane, k1);
@@ -698,8 +685,8 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
     const bool st2 = own && yi - 2 >= ys && yi - 2 < ye;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      const cplx zz = sv.v[4 * j + 1][lane], x1 = sv.v[4 * j + 2][lane], x2 = sv.v[4 * j + 3][lane];
-      const cplx ccur = {fma(wc1, x1.re, fma(0.5, x2.re, zz.re)), fma(wc1, x1.im, fma(0.5, x2.im, zz.im))};
+      const T zz = sv.v[4 * j + 1][lane], x1 = sv.v[4 * j + 2][lane], x2 = sv.v[4 * j + 3][lane];
+      const T ccur = fmav(wc1, x1, fmav(0.5, x2, zz));
       c2[j] = c1[j]; c1[j] = c0[j]; c0[j] = ccur;
       r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = sv.v[4 * j][lane];
       // z3 at row yi-1
@@ -707,24 +694,20 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
       {
         dd2[j] = dd1[j];
         dd1[j] = S::diag(k1, l[j]);
-        const cplx Ac = S::apply(k1, l[j], dd1[j], c2[j], c1[j], c0[j]);
+        const T Ac = S::apply(k1, l[j], dd1[j], c2[j], c1[j], c0[j]);
         jd2[j] = jd1[j];
         jd1[j] = rcp(dd1[j]);
-        const cplx t = cm({r1[j].re - Ac.re, r1[j].im - Ac.im}, jd1[j]);
-        e1[j] = in1 ? cplx{fma(om2, t.re, c1[j].re), fma(om2, t.im, c1[j].im)} : cplx{0, 0};
+        const T t = cm(r1[j] - Ac, jd1[j]);
+        e1[j] = in1 ? fmav(om2, t, c1[j]) : T{};
       }
       // z4 at row yi-2
       {
-        const cplx Ae = S::apply(k2, l[j], dd2[j], e3[j], e2[j], e1[j]);
+        const T Ae = S::apply(k2, l[j], dd2[j], e3[j], e2[j], e1[j]);
         if (st2 && it.on[j]) {
-          const cplx t = cm({r2[j].re - Ae.re, r2[j].im - Ae.im}, jd2[j]);
-          const cplx z4 = {fma(om1, t.re, e2[j].re), fma(om1, t.im, e2[j].im)};
+          const T t = cm(r2[j] - Ae, jd2[j]);
+          const T z4 = fmav(om1, t, e2[j]);
           zo[j][(long)(yi - 2) * m] = z4;
-          if (dot) {
-            const cplx pr = cm(r2[j], z4);
-            p0[j] += pr.re;
-            p1[j] += pr.im;
-          }
+          if (dot) dot_acc(r2[j], z4, p0[j], p1[j]);
         }
       }
     }
@@ -791,7 +774,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
   const cplx bt = (INIT || first) ? cplx{0, 0} : beta[b];
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 2, ylast = ye;  // staged rows
-  const S::Src src = S::src(op, x, xc, y0);
+  const S::Src src = S::src(op, x, xc, y0, b);
   int vi = 0, wi = 0;
   auto issue = [&](int yr) {
     if (yr <= ylast) {
@@ -888,9 +871,9 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <class S, int NB, int RA, int WPBK, bool FUSED = false>
-void down_t(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc, const int* active, double om1,
-            double om2, int nb, const cplx* q = nullptr, const cplx* alpha = nullptr, cplx* rout = nullptr,
+template <class S, int NB, int RA, int WPBK, bool FUSED = false, class T = typename S::T>
+void down_t(Problem& p, const FineOp& op, const T* r, T* z2, T* bc, int mc, const int* active, double om1,
+            double om2, int nb, const T* q = nullptr, const T* alpha = nullptr, T* rout = nullptr,
             double* part = nullptr) {
   constexpr size_t sm = ring_smem<S, FUSED ? 2 : NB, RA, WPBK>();
   static bool attrs = [] {
@@ -905,9 +888,9 @@ void down_t(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int
           op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
 }
 
-template <class S, int NB, int RA, int WPBK>
-void up_t(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc, cplx* z,
-          const int* active, double om1, double om2, int nb, int dot, double* part) {
+template <class S, int NB, int RA, int WPBK, class T = typename S::T>
+void up_t(Problem& p, const FineOp& op, const T* r, const T* z2, const T* xc, int mc, T* z, const int* active,
+          double om1, double om2, int nb, int dot, double* part) {
   constexpr size_t sm = ring_smem<S, 4 * NB, RA, WPBK>();
   static bool attrs = [] {
     cudaFuncSetAttribute(k_stream_up<S, NB, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
@@ -987,6 +970,20 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
     else if (w == 1) up_t<Seven, 1, 2, 1>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else up_t<Seven, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   }
+  TP_LAUNCHED(&p);
+}
+
+// Slice mode (static_init Newton solves): the same passes on real vectors with
+// per-slice symmetric Jacobian stencils (op.K = J of level l, op.kstride = 7n)
+void launch_stream_down(Problem& p, const FineOp& op, const double* r, double* z2, double* bc, int mc,
+                        const int* active, double om1, double om2, int nb) {
+  down_t<SevenJ, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+  TP_LAUNCHED(&p);
+}
+
+void launch_stream_up(Problem& p, const FineOp& op, const double* r, const double* z2, const double* xc, int mc,
+                      double* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
+  up_t<SevenJ, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   TP_LAUNCHED(&p);
 }
 
