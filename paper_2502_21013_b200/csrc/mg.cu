@@ -113,8 +113,10 @@ struct CoefFine {
 
 struct CoefSlice {  // FAM 2
   const double* J;
-  int n, i;
+  int n, i, m;
   __device__ __forceinline__ double c(int d) const { return __ldg(J + (size_t)d * n + i); }
+  // plane d at node j (clamped into the grid: off-grid neighbours multiply zero halo values)
+  __device__ __forceinline__ double c_at(int d, int j) const { return __ldg(J + (size_t)d * n + max(j, 0)); }
   __device__ __forceinline__ double diag() const { return c(0); }
 };
 
@@ -138,15 +140,18 @@ __device__ __forceinline__ cplx apply_tile(const CoefFine& a, const cplx (*s)[W]
   acc = axpy_r(a.r.kn, s[ly + 1][lx], acc);
   return acc;
 }
+// The element-assembled Jacobian is symmetric: W(i) = E(i-1), S(i) = N(i-m),
+// SW(i) = NE(i-m-1), so four of its seven planes are read (32 instead of 56
+// bytes per node and slice; neighbouring threads share the sectors)
 template <class T, int W>
 __device__ __forceinline__ T apply_tile(const CoefSlice& a, const T (*s)[W], int lx, int ly) {
-  T acc = a.c(0) * s[ly][lx];
-  acc = acc + a.c(1) * s[ly][lx - 1];
-  acc = acc + a.c(2) * s[ly][lx + 1];
-  acc = acc + a.c(3) * s[ly - 1][lx];
-  acc = acc + a.c(4) * s[ly + 1][lx];
-  acc = acc + a.c(5) * s[ly - 1][lx - 1];
-  acc = acc + a.c(6) * s[ly + 1][lx + 1];
+  T acc = a.c(SC) * s[ly][lx];
+  acc = acc + a.c_at(SE_, a.i - 1) * s[ly][lx - 1];
+  acc = acc + a.c(SE_) * s[ly][lx + 1];
+  acc = acc + a.c_at(SN_, a.i - a.m) * s[ly - 1][lx];
+  acc = acc + a.c(SN_) * s[ly + 1][lx];
+  acc = acc + a.c_at(SNE, a.i - a.m - 1) * s[ly - 1][lx - 1];
+  acc = acc + a.c(SNE) * s[ly + 1][lx + 1];
   return acc;
 }
 
@@ -183,7 +188,7 @@ template <>
 struct Ctx<1, 2> {
   __device__ void init(const Op<1>&, int, bool, int) {}
   __device__ CoefSlice at(const Op<1>& op, int b, int i, int) const {
-    return {op.J + (size_t)b * 7 * op.n, op.n, i};
+    return {op.J + (size_t)b * 7 * op.n, op.n, i, op.m};
   }
 };
 
