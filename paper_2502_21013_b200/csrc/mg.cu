@@ -930,6 +930,24 @@ __global__ void k_count_active(const int* __restrict__ active, int nb, int* __re
 
 // ---- hierarchy construction kernels
 
+// Galerkin product P^T A P for one coarse node per thread.  The coarse
+// centre (X, Y) is fine node (2X+1, 2Y+1); its P^T row gathers the 7 fine
+// nodes fx = 2X+1+ox_s (weights 1, 1/2 x 6), each fine stencil entry d
+// reaches fine node g = f + dir_d, and P interpolates g from its one or two
+// coarse parents -- all offsets relative to (X, Y) are compile-time constants
+// (fully unrolled), only the grid-boundary tests are run time.
+__device__ __forceinline__ constexpr int floordiv2(int v) { return v >= 0 ? v / 2 : -((1 - v) / 2); }
+__device__ __forceinline__ constexpr int dir_of(int ex, int ey) {
+  return (ex == 0 && ey == 0) ? SC
+         : (ex == -1 && ey == 0) ? SW_
+         : (ex == 1 && ey == 0) ? SE_
+         : (ex == 0 && ey == -1) ? SS_
+         : (ex == 0 && ey == 1) ? SN_
+         : (ex == -1 && ey == -1) ? SSW
+         : (ex == 1 && ey == 1) ? SNE
+                                : -1;
+}
+
 __global__ void k_rap(const double* __restrict__ Af, int mf, double* __restrict__ Ac, int mc) {
   const size_t nf = (size_t)mf * mf, nc = (size_t)mc * mc;
   const int b = blockIdx.y;
@@ -937,31 +955,40 @@ __global__ void k_rap(const double* __restrict__ Af, int mf, double* __restrict_
   if (ic >= nc) return;
   const double* A = Af + (size_t)b * 7 * nf;
   const int X = (int)(ic % mc), Y = (int)(ic / mc);
-  const int sox[7] = {0, -1, 1, 0, 0, -1, 1}, soy[7] = {0, 0, 0, -1, 1, -1, 1};
-  const double sw[7] = {1.0, 0.5, 0.5, 0.5, 0.5, 0.5, 0.5};
+  constexpr int sox[7] = {0, -1, 1, 0, 0, -1, 1}, soy[7] = {0, 0, 0, -1, 1, -1, 1};
   double out[7] = {0, 0, 0, 0, 0, 0, 0};
+#pragma unroll
   for (int s = 0; s < 7; ++s) {
+    const double sw = s == 0 ? 1.0 : 0.5;
     const int fx = 2 * X + 1 + sox[s], fy = 2 * Y + 1 + soy[s];
     if (fx < 0 || fx >= mf || fy < 0 || fy >= mf) continue;
     const size_t fi = (size_t)fy * mf + fx;
+#pragma unroll
     for (int d = 0; d < 7; ++d) {
-      const double a = A[d * nf + fi];
-      if (a == 0.0) continue;
+      // fine neighbour g = f + dir_d, vertex (a, b) = g + 1 = 2 (X+1, Y+1) + (ox, oy)
+      const int ox = sox[s] + dir_dx(d), oy = soy[s] + dir_dy(d);
       const int gx = fx + dir_dx(d), gy = fy + dir_dy(d);
       if (gx < 0 || gx >= mf || gy < 0 || gy >= mf) continue;
-      int cx[2], cy[2];
-      double w[2];
-      const int np = parents(gx, gy, mc, cx, cy, w);
-      for (int t = 0; t < np; ++t) {
-        const int ex = cx[t] - X, ey = cy[t] - Y;
-        int e = -1;
-        for (int dd = 0; dd < 7; ++dd)
-          if (dir_dx(dd) == ex && dir_dy(dd) == ey) e = dd;
-        if (e >= 0) out[e] += sw[s] * a * w[t];
+      const double a = __ldg(A + d * nf + fi) * sw;
+      // parents relative to (X, Y): first (fx2, fy2); second +1 in x and/or y
+      const int px = floordiv2(ox), py = floordiv2(oy);
+      const bool aodd = (ox & 1) != 0, bodd = (oy & 1) != 0;
+      const double w1 = (aodd || bodd) ? 0.5 : 1.0;
+      {
+        const int e = dir_of(px, py);
+        const int CX = X + px, CY = Y + py;
+        if (e >= 0 && CX >= 0 && CX < mc && CY >= 0 && CY < mc) out[e] += a * w1;
+      }
+      if (aodd || bodd) {
+        const int qx = px + (aodd ? 1 : 0), qy = py + (bodd ? 1 : 0);
+        const int e = dir_of(qx, qy);
+        const int CX = X + qx, CY = Y + qy;
+        if (e >= 0 && CX >= 0 && CX < mc && CY >= 0 && CY < mc) out[e] += a * 0.5;
       }
     }
   }
   double* C = Ac + (size_t)b * 7 * nc;
+#pragma unroll
   for (int d = 0; d < 7; ++d) C[d * nc + ic] = out[d];
 }
 
