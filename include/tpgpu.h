@@ -114,7 +114,11 @@ typedef struct tp_solver_cfg {
   int32_t slice_chunk;        /* slices per batched Newton solve (0 = automatic) */
   int32_t freq_groups;        /* frequency groups solved concurrently on their own
                                  streams (0 = automatic: 3) */
-  int32_t reserved_;          /* keeps the struct size a multiple of 8 */
+  /* M2 all-at-once Newton (SolverConfig m2_*, solvers.hpp:52,63-65) */
+  int32_t m2_max_outer;       /* default 50 */
+  double m2_inner_tol;        /* FGMRES relative tolerance, default 1e-8 */
+  int32_t m2_inner_max;       /* FGMRES iteration cap, default 300 */
+  int32_t m2_restart;         /* FGMRES restart length, default 60 */
 } tp_solver_cfg;
 
 /* Mirrors SolveReport (solvers.hpp:88-96); residual/contraction histories are
@@ -182,6 +186,13 @@ int tp_periodic_solve(tp_problem* p, const tp_solver_cfg* cfg, const double* G, 
 int tp_solve_m1(tp_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out,
                 tp_report* report, double* history, double* contraction, int32_t cap,
                 tp_iterate_cb cb, void* user);
+
+/* M2 all-at-once Newton: FGMRES right-preconditioned by the periodic solver on
+ * the time-averaged Jacobian, Armijo line search (solve_m2_newton,
+ * solvers.hpp:375-484).  Single-GPU problems.  Same outputs as tp_solve_m1
+ * (q_estimate is NaN; inner_iterations = total FGMRES iterations). */
+int tp_solve_m2(tp_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out, tp_report* rep,
+                double* history, double* contraction, int32_t cap);
 
 /* ---- device-resident sweep (benchmark / driver building blocks) -------- */
 /* Builds the frequency solver (PeriodicSolver ctor, periodic.hpp:128-139) and

@@ -6,6 +6,7 @@
 // Every entry point drives reference code unchanged:
 //   tpref_static_init   -> tpfem::static_init            (solvers.hpp:276-296)
 //   tpref_solve_m1      -> tpfem::solve_m1_fixed_point   (solvers.hpp:301-369)
+//   tpref_solve_m2      -> tpfem::solve_m2_newton        (solvers.hpp:375-484)
 //   tpref_periodic_solve-> tpfem::PeriodicSolver::solve  (periodic.hpp:154-198)
 //   tpref_residual      -> tpfem::residual + block_l2    (periodic.hpp:35-67)
 // with tporacle::GridProblem (grid_problem.hpp) supplying the BASELINE physics.
@@ -57,6 +58,10 @@ tpfem::SolverConfig to_ref(const tp_solver_cfg* c) {
   s.imag_tol = c->imag_tol;
   s.static_tol = c->static_tol;
   s.static_max_newton = c->static_max_newton;
+  if (c->m2_max_outer > 0) s.m2_max_outer = c->m2_max_outer;
+  if (c->m2_inner_tol > 0) s.m2_inner_tol = c->m2_inner_tol;
+  if (c->m2_inner_max > 0) s.m2_inner_max = c->m2_inner_max;
+  if (c->m2_restart > 0) s.m2_restart = c->m2_restart;
   s.threads = c->threads > 0 ? c->threads
                              : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   return s;
@@ -234,6 +239,25 @@ int tpref_solve_m1(const tp_problem_desc* d, const tp_solver_cfg* c, const doubl
       for (std::size_t k = 0; k < log.size() && static_cast<int>(k) < cap; ++k)
         std::memcpy(iterates + k * sz, log[k].data.data(), sz * sizeof(double));
     }
+  });
+}
+
+// tpfem::solve_m2_newton (solvers.hpp:375-484) on the grid problem
+int tpref_solve_m2(const tp_problem_desc* d, const tp_solver_cfg* c, const double* U0, double* U_out,
+                   double* history, int32_t cap, int32_t* iterations, int32_t* status, double* wall) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const tpfem::BlockRhs F = p.loads();
+    const tpfem::PeriodicState U0s = state_from(p, U0);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [U, rep] = tpfem::solve_m2_newton(p, F, U0s, cfg);
+    if (wall) *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
+    for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)
+      history[k] = rep.residual_history[k];
+    if (iterations) *iterations = rep.iterations;
+    if (status) *status = static_cast<int32_t>(rep.status);
   });
 }
 

@@ -44,7 +44,8 @@ class TpSolverCfg(C.Structure):
                 ("threads", C.c_int32), ("inner_rtol", C.c_double),
                 ("inner_max_iter", C.c_int32), ("warm_start", C.c_int32),
                 ("freq_chunk", C.c_int32), ("slice_chunk", C.c_int32),
-                ("freq_groups", C.c_int32), ("reserved_", C.c_int32)]
+                ("freq_groups", C.c_int32), ("m2_max_outer", C.c_int32),
+                ("m2_inner_tol", C.c_double), ("m2_inner_max", C.c_int32), ("m2_restart", C.c_int32)]
 
 
 class TpShardPlan(C.Structure):
@@ -83,7 +84,10 @@ def default_cfg(**overrides) -> TpSolverCfg:
     c.freq_chunk = 0
     c.slice_chunk = 0
     c.freq_groups = 0
-    c.reserved_ = 0
+    c.m2_max_outer = 50
+    c.m2_inner_tol = 1e-8
+    c.m2_inner_max = 300
+    c.m2_restart = 60
     for k, v in overrides.items():
         setattr(c, k, v)
     return c

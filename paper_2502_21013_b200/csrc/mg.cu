@@ -1400,7 +1400,12 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   // partials per batch of each producing kernel
   const int per_t = g0.tiles;
   const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
-  const int per_u = (fine || stream_level(0)) ? fine_partials(ops[0].m, 2) : per_t;  // V-cycle dot (up)
+  // V-cycle dot (up pass of level 0): streaming layout when that pass is streamed
+  static const bool tile_coarse0 = std::getenv("TPGPU_TILE_COARSE") != nullptr;
+  const bool up0_streamed = fine || stream_level(0) ||
+                            (MODE == 0 && ops.size() > 1 && !ops[0].five && !tile_coarse0 && ops[0].m >= 7 &&
+                             small_from != 0);
+  const int per_u = up0_streamed ? fine_partials(ops[0].m, 2) : per_t;
   // fine level: the ring-staged streaming apply (mg_fine.cu) -- measured 8.08
   // vs 8.39 ms per cfg-1 sweep against the smem-tile apply (TPGPU_TILE_APPLY)
   static const bool use_stream_apply = std::getenv("TPGPU_TILE_APPLY") == nullptr;

@@ -459,6 +459,12 @@ double Problem::residual_and_rhs(bool want_rhs) {
   return std::sqrt(global_sum(reduce_sum(*this, part.get(), (int)np)));
 }
 
+// block residual of a device state u into r and its norm (block_l2)
+double residual_norm_dev(Problem& p, const double* u, double* r) {
+  p.residual_dev(u, r, p.N);
+  return std::sqrt(reduce_sum(p, p.part.get(), (int)sweep_partials(p.m, p.N)));
+}
+
 void Problem::residual_dev(const double* u, double* r, int count_slices) {
   require(count_slices == N, "residual: needs all slices");
   require(!sharded(), "residual of a host state: single-rank problems only");

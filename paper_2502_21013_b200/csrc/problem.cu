@@ -316,31 +316,48 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
     return;
   }
   fw.reset();
-  levels.clear();
+  build_freq_work(levels, fw, nullptr, cfg, want_groups);
+  freq_ready = true;
+  uhat_valid = false;
+}
+
+// Multigrid hierarchy and batched frequency solvers for lambda_k M + K0 into
+// (lv, out).  K0 == nullptr: K_hat from nu_hat (the M1 operator; the fine
+// level runs the Five streaming passes from edge weights).  Otherwise K0 is a
+// fine-grid 7-point stencil on the device (7n, e.g. M2's time-averaged
+// Jacobian): the fine level runs the Galerkin-style 7-point passes.
+void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>& out, const double* K0,
+                              const tp_solver_cfg& cfg, int want_groups) {
+  lv.clear();
   int cl = c;
   while (true) {
     Level L;
     L.m = cl - 1;
     L.n = L.m * L.m;
-    levels.push_back(std::move(L));
+    lv.push_back(std::move(L));
     if (cl <= 8) break;
     require(cl % 2 == 0, "multigrid: cells per side must be 2^k * q with q <= 8");
     cl /= 2;
   }
-  const int nl = (int)levels.size();
-  // fine level: K_hat element stencil, lumped M on the diagonal
-  levels[0].K.alloc((size_t)7 * n);
-  levels[0].M.alloc((size_t)7 * n);
-  launch_element_stencil(*this, false, nullptr, levels[0].K.get(), 1);
-  TP_CUDA(cudaMemsetAsync(levels[0].M.get(), 0, levels[0].M.bytes(), stream));
-  TP_CUDA(cudaMemcpyAsync(levels[0].M.get(), d_mass.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
-  for (int l = 1; l < nl; ++l) {
-    levels[l].K.alloc((size_t)7 * levels[l].n);
-    levels[l].M.alloc((size_t)7 * levels[l].n);
-    launch_rap(*this, levels[l - 1].K.get(), levels[l - 1].m, levels[l].K.get(), levels[l].m, 1);
-    launch_rap(*this, levels[l - 1].M.get(), levels[l - 1].m, levels[l].M.get(), levels[l].m, 1);
+  const int nl = (int)lv.size();
+  // fine level: K (K_hat element stencil or the given K0), lumped M on the diagonal
+  lv[0].K.alloc((size_t)7 * n);
+  lv[0].M.alloc((size_t)7 * n);
+  if (K0) {
+    TP_CUDA(cudaMemcpyAsync(lv[0].K.get(), K0, lv[0].K.bytes(), cudaMemcpyDeviceToDevice, stream));
+  } else {
+    launch_element_stencil(*this, false, nullptr, lv[0].K.get(), 1);
   }
-  fw = std::make_unique<FreqWork>();
+  TP_CUDA(cudaMemsetAsync(lv[0].M.get(), 0, lv[0].M.bytes(), stream));
+  TP_CUDA(cudaMemcpyAsync(lv[0].M.get(), d_mass.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  for (int l = 1; l < nl; ++l) {
+    lv[l].K.alloc((size_t)7 * lv[l].n);
+    lv[l].M.alloc((size_t)7 * lv[l].n);
+    launch_rap(*this, lv[l - 1].K.get(), lv[l - 1].m, lv[l].K.get(), lv[l].m, 1);
+    launch_rap(*this, lv[l - 1].M.get(), lv[l - 1].m, lv[l].M.get(), lv[l].m, 1);
+  }
+  out = std::make_unique<FreqWork>();
+  FreqWork* w = out.get();
   // symbols lambda_k (periodic.hpp:146-152) of this rank's frequencies
   const int Kr = sh.k1 - sh.k0;
   std::vector<cplx> lam(Kr);
@@ -355,22 +372,22 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
       lk = {(1.0 - rr) / tau, (0.0 - ri) / tau};
     }
   }
-  fw->lam.alloc(Kr);
-  TP_CUDA(cudaMemcpy(fw->lam.get(), lam.data(), Kr * sizeof(cplx), cudaMemcpyHostToDevice));
-  const Level& LC = levels.back();
-  fw->nL = LC.n;
-  fw->inv.alloc((size_t)Kr * LC.n * LC.n);
-  launch_coarse_inverse_freq(*this, LC.K.get(), LC.M.get(), LC.m, fw->lam.get(), fw->inv.get(), Kr);
+  w->lam.alloc(Kr);
+  TP_CUDA(cudaMemcpy(w->lam.get(), lam.data(), Kr * sizeof(cplx), cudaMemcpyHostToDevice));
+  const Level& LC = lv.back();
+  w->nL = LC.n;
+  w->inv.alloc((size_t)Kr * LC.n * LC.n);
+  launch_coarse_inverse_freq(*this, LC.K.get(), LC.M.get(), LC.m, w->lam.get(), w->inv.get(), Kr);
   // chunk: work ~ 7 complex vectors per frequency on the fine level (+1/3 coarse)
   size_t free_b = 0, total_b = 0;
   TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
   const double per = 16.0 * 8.5 * n;
   int chunk = cfg.freq_chunk > 0 ? cfg.freq_chunk : (int)std::min<double>(Kr, 0.6 * free_b / per);
   chunk = std::max(1, std::min(chunk, Kr));
-  fw->chunk = chunk;
+  w->chunk = chunk;
   std::vector<LevelOp> ops(nl);
-  for (int l = 0; l < nl; ++l) ops[l] = {levels[l].m, levels[l].n, levels[l].K.get(), levels[l].M.get(), l == 0, {}};
-  if (!std::getenv("TPGPU_NO_STREAM_FINE")) {
+  for (int l = 0; l < nl; ++l) ops[l] = {lv[l].m, lv[l].n, lv[l].K.get(), lv[l].M.get(), l == 0 && !K0, {}};
+  if (!K0 && !std::getenv("TPGPU_NO_STREAM_FINE")) {
     // K_hat edge weights: we[Y][X] = (nu_hat(cell(X,Y)) + nu_hat(cell(X,Y-1)))/2,
     // wn[Y][X] = (nu_hat(cell(X,Y)) + nu_hat(cell(X-1,Y)))/2 (the two triangles
     // sharing the edge, assemble_stiffness_frozen on the right-triangle grid)
@@ -401,27 +418,44 @@ void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   if (const char* e = std::getenv("TPGPU_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
   if (const char* e = std::getenv("TPGPU_OMEGA2")) mc.omega2 = std::atof(e);
   // concurrent frequency groups (TPGPU_FREQ_GROUPS overrides; 1 = one solver on the problem stream)
-  fw->req_chunk = cfg.freq_chunk;
-  fw->req_groups = want_groups;
+  w->req_chunk = cfg.freq_chunk;
+  w->req_groups = want_groups;
   int parts = std::max(1, std::min(want_groups, chunk));
-  fw->parts = parts;
+  w->parts = parts;
   const int per_group = (chunk + parts - 1) / parts;
-  fw->chunk = per_group;
-  fw->solver.init(this, ops, per_group, mc);
+  w->chunk = per_group;
+  w->solver.init(this, ops, per_group, mc);
   for (int g = 1; g < parts; ++g) {
-    fw->extra.push_back(std::make_unique<BatchSolver<0>>());
-    fw->extra.back()->init(this, ops, per_group, mc);
+    w->extra.push_back(std::make_unique<BatchSolver<0>>());
+    w->extra.back()->init(this, ops, per_group, mc);
   }
   if (parts > 1) {
-    fw->hs.assign(parts, nullptr);
-    fw->ev_out.assign(parts, nullptr);
-    for (auto& h : fw->hs) TP_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
-    TP_CUDA(cudaEventCreateWithFlags(&fw->ev_in, cudaEventDisableTiming));
-    for (auto& e : fw->ev_out) TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    w->hs.assign(parts, nullptr);
+    w->ev_out.assign(parts, nullptr);
+    for (auto& h : w->hs) TP_CUDA(cudaStreamCreateWithFlags(&h, cudaStreamNonBlocking));
+    TP_CUDA(cudaEventCreateWithFlags(&w->ev_in, cudaEventDisableTiming));
+    for (auto& e : w->ev_out) TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
   TP_CUDA(cudaStreamSynchronize(stream));
-  freq_ready = true;
-  uhat_valid = false;
+}
+
+namespace {
+struct PrecondHolder {
+  std::vector<Level> lv;
+  std::unique_ptr<Problem::FreqWork> fw;
+};
+}  // namespace
+
+std::shared_ptr<void> Problem::make_periodic_precond(const double* K0, const tp_solver_cfg& cfg) {
+  auto h = std::make_shared<PrecondHolder>();
+  build_freq_work(h->lv, h->fw, K0, cfg, cfg.freq_groups > 0 ? cfg.freq_groups : 3);
+  return h;
+}
+
+void Problem::precond_solve(void* handle, const double* in, double* out, const tp_solver_cfg& cfg) {
+  auto* h = static_cast<PrecondHolder*>(handle);
+  SolveStats st;
+  periodic_solve_with(*h->fw, in, out, false, cfg, &st);
 }
 
 // U_{k+1} = IDFT(U_hat) stays close to U_k near the fixed point, so DFT(U) is
@@ -435,36 +469,46 @@ void Problem::seed_spectrum() {
 
 void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
   build_frequency_solver(cfg);
-  launch_rdft_forward(*this, G.get(), Ghat.get());
-  if (sharded()) alltoall_to_freq();
   const bool warm = cfg.warm_start && uhat_valid;
+  periodic_solve_with(*fw, G.get(), U.get(), warm, cfg, st);
+  uhat_valid = true;
+}
+
+// PeriodicSolver::solve (periodic.hpp:154-198) of `in` (N x n, this rank's
+// strip layout) into `out` with the frequency solvers of `w`: forward time
+// DFT, [all-to-all to frequency blocks], batched block solves (warm: from the
+// current spectrum), [all-to-all back], inverse DFT and the imaginary guard.
+void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bool warm, const tp_solver_cfg& cfg,
+                                  SolveStats* st) {
+  launch_rdft_forward(*this, in, Ghat.get());
+  if (sharded()) alltoall_to_freq();
   const int Kr = sh.k1 - sh.k0;
   int iters = 0;
   auto run = [&](BatchSolver<0>& sv, int k0, int nb, SolveStats* sst) {
-    sv.lam = fw->lam.get() + k0;
-    sv.coarse_inv = fw->inv.get() + (size_t)k0 * fw->nL * fw->nL;
+    sv.lam = w.lam.get() + k0;
+    sv.coarse_inv = w.inv.get() + (size_t)k0 * w.nL * w.nL;
     return sv.solve(spec_in() + (size_t)k0 * n, spec_out() + (size_t)k0 * n, nb, warm, sst);
   };
-  if (fw->parts == 1) {
-    for (int k0 = 0; k0 < Kr; k0 += fw->chunk)
-      iters = std::max(iters, run(fw->solver, k0, std::min(fw->chunk, Kr - k0), st));
+  if (w.parts == 1) {
+    for (int k0 = 0; k0 < Kr; k0 += w.chunk)
+      iters = std::max(iters, run(w.solver, k0, std::min(w.chunk, Kr - k0), st));
   } else {
     // groups of `parts` chunks: group 0 on hs[0] (this thread), the others on
     // hs[g] driven by helper threads
-    const int P = fw->parts;
-    for (int k0 = 0; k0 < Kr; k0 += P * fw->chunk) {
-      TP_CUDA(cudaEventRecord(fw->ev_in, stream));
-      for (auto h : fw->hs) TP_CUDA(cudaStreamWaitEvent(h, fw->ev_in, 0));
+    const int P = w.parts;
+    for (int k0 = 0; k0 < Kr; k0 += P * w.chunk) {
+      TP_CUDA(cudaEventRecord(w.ev_in, stream));
+      for (auto h : w.hs) TP_CUDA(cudaStreamWaitEvent(h, w.ev_in, 0));
       std::vector<SolveStats> gst(P);
       std::vector<int> git(P, 0);
       std::vector<std::exception_ptr> gerr(P);
       auto body = [&](int g) {
-        const int kg = k0 + g * fw->chunk, nbg = std::min(fw->chunk, Kr - kg);
+        const int kg = k0 + g * w.chunk, nbg = std::min(w.chunk, Kr - kg);
         if (nbg <= 0) return;
         try {
           if (g > 0) TP_CUDA(cudaSetDevice(device));
-          tl_stream = fw->hs[g];
-          git[g] = run(fw->group(g), kg, nbg, &gst[g]);
+          tl_stream = w.hs[g];
+          git[g] = run(w.group(g), kg, nbg, &gst[g]);
         } catch (...) {
           gerr[g] = std::current_exception();
         }
@@ -475,8 +519,8 @@ void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
       body(0);
       for (auto& t : helpers) t.join();
       for (int g = 0; g < P; ++g) {
-        TP_CUDA(cudaEventRecord(fw->ev_out[g], fw->hs[g]));
-        TP_CUDA(cudaStreamWaitEvent(stream, fw->ev_out[g], 0));
+        TP_CUDA(cudaEventRecord(w.ev_out[g], w.hs[g]));
+        TP_CUDA(cudaStreamWaitEvent(stream, w.ev_out[g], 0));
       }
       for (auto& e : gerr)
         if (e) std::rethrow_exception(e);
@@ -493,10 +537,9 @@ void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
   last_inner = iters;
   if (sharded()) alltoall_from_freq();
   double re2 = 0, im2 = 0;
-  launch_rdft_inverse(*this, Uhat.get(), U.get(), &re2, &im2);
+  launch_rdft_inverse(*this, Uhat.get(), out, &re2, &im2);
   re2 = global_sum(re2);
   im2 = global_sum(im2);
-  uhat_valid = true;
   // imaginary-residue guard, periodic.hpp:186-196
   const double re_norm = std::sqrt(re2), im_norm = std::sqrt(im2);
   if (im_norm > cfg.imag_tol * std::max(re_norm, 1e-300))
@@ -594,6 +637,10 @@ void tp_solver_cfg_default(tp_solver_cfg* c) {
   c->inner_rtol = 1e-12;
   c->inner_max_iter = 200;
   c->warm_start = 1;
+  c->m2_max_outer = 50;
+  c->m2_inner_tol = 1e-8;
+  c->m2_inner_max = 300;
+  c->m2_restart = 60;
 }
 
 int tp_problem_desc_baseline(int32_t config, tp_problem_desc* desc) {
@@ -905,6 +952,42 @@ int tp_kernel_timer(tp_problem* h, int32_t enable, int64_t* launches, double* ms
     p.ktimer.ms = 0;
     p.ktimer.bytes = 0;
     p.ktimer.on = enable != 0;
+  });
+}
+
+// solve_m2_newton, solvers.hpp:375-484 (single GPU)
+int tp_solve_m2(tp_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
+                double* history, double* contraction, int32_t cap) {
+  return guarded([&] {
+    Problem& p = P(h);
+    const tp_solver_cfg cfg = cfg_or_default(c);
+    tpgpu::validate_cfg(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    if (U0) {
+      TP_CUDA(cudaMemcpyAsync(p.U.get(), U0, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+      p.state_valid = true;
+      p.uhat_valid = false;
+    }
+    Problem::M2Result res;
+    p.solve_m2_dev(cfg, res);
+    tp_report r{};
+    r.iterations = res.iterations;
+    r.status = res.status;
+    r.q_estimate = std::numeric_limits<double>::quiet_NaN();
+    r.inner_iterations = (int32_t)res.inner_total;
+    const auto& hist = res.history;
+    r.history_len = (int32_t)std::min<size_t>(hist.size(), cap > 0 ? cap : 0);
+    if (history)
+      for (int k = 0; k < r.history_len; ++k) history[k] = hist[k];
+    if (contraction)
+      for (size_t k = 0; k + 1 < hist.size() && (int)k < cap; ++k)
+        contraction[k] = hist[k] > 0 ? hist[k + 1] / hist[k] : 0.0;
+    if (U_out) {
+      TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      TP_CUDA(cudaStreamSynchronize(p.stream));
+    }
+    r.wall_time = seconds_since(t0);
+    if (rep) *rep = r;
   });
 }
 

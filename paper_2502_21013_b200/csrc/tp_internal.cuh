@@ -237,6 +237,14 @@ class Problem {
   void upload_constants();
   void install_nu_hat(const double* nu, double q);
   void build_frequency_solver(const tp_solver_cfg& cfg);
+  void build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>& out, const double* K0,
+                       const tp_solver_cfg& cfg, int want_groups);
+  void periodic_solve_with(FreqWork& w, const double* in, double* out, bool warm, const tp_solver_cfg& cfg,
+                           SolveStats* st);
+  // a periodic solver for lambda_k M + K0 (K0: fine 7-point stencil, device)
+  // as an opaque handle, and its application in -> out (cold start)
+  std::shared_ptr<void> make_periodic_precond(const double* K0, const tp_solver_cfg& cfg);
+  void precond_solve(void* handle, const double* in, double* out, const tp_solver_cfg& cfg);
   // K(u) for `count` slices of `u` into `out` (device pointers)
   void apply_k_dev(const double* u, double* out, int count);
   // fused residual + next RHS over the device state: returns ||R||
@@ -246,6 +254,13 @@ class Problem {
   // periodic linear solve of the device G into the device U
   void periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st);
   void static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts);
+  // M2 all-at-once Newton (m2.cu) from the device state U
+  struct M2Result {
+    int iterations = 0, status = 0;
+    int64_t inner_total = 0;
+    std::vector<double> history;
+  };
+  void solve_m2_dev(const tp_solver_cfg& cfg, M2Result& res);
   void field_ranges(double* lo, double* hi, int* any);
   int last_inner = 0;
 };

@@ -249,3 +249,25 @@ def test_run_cli_writes_reference_formats(tmp_path):
     assert rows[0] == ["method", "iteration", "residual", "contraction"]
     assert len(rows) - 1 == len(m1["residual_history"]) == m1["iterations"] + 1
     assert rows[1][3] == "" and all(float(r[2]) == h for r, h in zip(rows[1:], m1["residual_history"]))
+
+
+@pytest.mark.gpu
+def test_m2_newton_matches_reference(ref, cfg0_ref):
+    """M2 all-at-once Newton against the reference's
+    solve_m2_newton from the same U0: Newton step count equal, the
+    quadratically converging residual history and the final iterate close
+    (the inner FGMRES is inexact on both sides at m2_inner_tol = 1e-8)."""
+    r = cfg0_ref
+    cfg = default_cfg(tol=1e-8)
+    Ur, hr, kr, str_, _ = ref.solve_m2(r["desc"], r["U0"], cfg)
+    with Problem(r["desc"]) as p:
+        p.set_nu_hat(r["nu"], r["q"])
+        U, rep = p.solve_m2_newton(r["U0"], cfg)
+    assert rep.method == "m2" and rep.status == "converged" and str_ == 0
+    assert rep.iterations == kr
+    h = np.array(rep.residual_history)
+    assert h.shape == hr.shape
+    assert abs(h[0] - hr[0]) <= 1e-12 * hr[0]
+    np.testing.assert_allclose(h[1:3], hr[1:3], rtol=1e-6)
+    assert h[-1] <= cfg.tol * h[0]
+    assert rel(U, Ur) <= 1e-9
