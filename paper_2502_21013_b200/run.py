@@ -31,6 +31,7 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=0, help="override N")
     ap.add_argument("--u0", choices=["static_init", "zero"], default="static_init")
     ap.add_argument("--device", type=int, default=0)
+    ap.add_argument("--methods", default="m1", help="comma list of m1, m2 (run from the same U0)")
     a = ap.parse_args(argv)
 
     desc = baseline_desc(a.config)
@@ -50,17 +51,25 @@ def main(argv=None) -> int:
             p.set_state(U0)
         nu, q = p.choose_nu_hat(cfg)
         init_s = time.perf_counter() - t0
-        U, rep = p.solve_m1_fixed_point(U0, cfg)
         print(f"grid: {p.shape[1]} unknowns, {desc.steps} steps, initialization {R.format_double(init_s)} s")
-        print(f"m1: {rep.status} after {rep.iterations} iterations ({R.format_double(rep.wall_time)} s), "
-              f"residual {R.format_double(rep.residual_history[-1])}")
+        reports = []
+        for meth in [x.strip() for x in a.methods.split(",") if x.strip()]:
+            if meth == "m1":
+                _, rep = p.solve_m1_fixed_point(U0, cfg)
+            elif meth == "m2":
+                _, rep = p.solve_m2_newton(U0, cfg)
+            else:
+                raise SystemExit(f"unknown method {meth!r} (m1, m2)")
+            print(f"{meth}: {rep.status} after {rep.iterations} iterations ({R.format_double(rep.wall_time)} s), "
+                  f"residual {R.format_double(rep.residual_history[-1])}")
+            reports.append((meth, rep))
         tau = desc.period / desc.steps
         j = R.run_report(desc, desc.steps, p.shape[1], tau, cfg.threads, nu, q, init_s, newton_max,
-                         R.symbol_abs(desc.steps, tau), {"m1": R.report_to_dict(rep, "m1")})
+                         R.symbol_abs(desc.steps, tau), {mm: R.report_to_dict(r, mm) for mm, r in reports})
     R.ensure_dir(a.out)
     R.write_json(os.path.join(a.out, "report.json"), j)
-    R.write_residuals_csv(os.path.join(a.out, "residuals.csv"), [("m1", rep)])
-    return R.exit_code([rep.status])
+    R.write_residuals_csv(os.path.join(a.out, "residuals.csv"), reports)
+    return R.exit_code([r.status for _, r in reports])
 
 
 if __name__ == "__main__":

@@ -238,17 +238,21 @@ def test_run_cli_writes_reference_formats(tmp_path):
     import json
     from paper_2502_21013_b200 import run
     out = tmp_path / "cfg0"
-    rc = run.main(["--config", "0", "--out", str(out), "--tol", "1e-8"])
+    rc = run.main(["--config", "0", "--out", str(out), "--tol", "1e-8", "--methods", "m1,m2"])
     assert rc == 0
     j = json.loads((out / "report.json").read_text())
     m1 = j["methods"]["m1"]
+    m2 = j["methods"]["m2"]
+    assert m2["status"] == "converged" and m2["iterations"] == 4 and "q_estimate" not in m2
     assert m1["status"] == "converged" and m1["method"] == "m1"
     assert j["problem"] == "grid" and j["steps"] == 64 and j["n_dof"] == 961
     assert len(j["frequency_symbol_abs"]) == 33
     rows = list(csv.reader((out / "residuals.csv").open()))
     assert rows[0] == ["method", "iteration", "residual", "contraction"]
-    assert len(rows) - 1 == len(m1["residual_history"]) == m1["iterations"] + 1
-    assert rows[1][3] == "" and all(float(r[2]) == h for r, h in zip(rows[1:], m1["residual_history"]))
+    assert len(rows) - 1 == len(m1["residual_history"]) + len(m2["residual_history"])
+    rows = [r for r in rows if r[0] == "m1"]
+    assert len(rows) + 1 - 1 == m1["iterations"] + 1
+    assert rows[0][3] == "" and all(float(r[2]) == h for r, h in zip(rows, m1["residual_history"]))
 
 
 @pytest.mark.gpu
