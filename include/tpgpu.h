@@ -119,6 +119,8 @@ typedef struct tp_solver_cfg {
   double m2_inner_tol;        /* FGMRES relative tolerance, default 1e-8 */
   int32_t m2_inner_max;       /* FGMRES iteration cap, default 300 */
   int32_t m2_restart;         /* FGMRES restart length, default 60 */
+  int32_t m3_max_cycles;      /* M3 time-stepping periods (SolverConfig::m3_max_cycles), default 10 */
+  int32_t reserved_;          /* keeps the struct size a multiple of 8 */
 } tp_solver_cfg;
 
 /* Mirrors SolveReport (solvers.hpp:88-96); residual/contraction histories are
@@ -192,6 +194,13 @@ int tp_solve_m1(tp_problem* p, const tp_solver_cfg* cfg, const double* U0, doubl
  * solvers.hpp:375-484).  Single-GPU problems.  Same outputs as tp_solve_m1
  * (q_estimate is NaN; inner_iterations = total FGMRES iterations). */
 int tp_solve_m2(tp_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out, tp_report* rep,
+                double* history, double* contraction, int32_t cap);
+
+/* M3 sequential time stepping toward the limit cycle: implicit Euler period
+ * after period from U0, per-step damped Newton (solve_m3_timestepping,
+ * solvers.hpp:489-542; newton_elliptic with mass_scale 1/tau).  Single GPU.
+ * iterations = completed periods. */
+int tp_solve_m3(tp_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out, tp_report* rep,
                 double* history, double* contraction, int32_t cap);
 
 /* ---- device-resident sweep (benchmark / driver building blocks) -------- */

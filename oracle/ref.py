@@ -56,6 +56,7 @@ def lib():
         L.tpref_solve_m1.argtypes = [D, G, dp, C.c_double, dp, dp, dp, dp, C.c_int32, ip, ip, dp,
                                      C.c_int32, dp]
         L.tpref_solve_m2.argtypes = [D, G, dp, dp, dp, C.c_int32, ip, ip, dp]
+        L.tpref_solve_m3.argtypes = [D, G, dp, dp, dp, C.c_int32, ip, ip, dp]
         _lib = L
     return _lib
 
@@ -211,6 +212,23 @@ def solve_m2(desc, U0, cfg: TpSolverCfg | None = None):
     wall = np.zeros(1)
     U = np.zeros_like(U0)
     _check(lib().tpref_solve_m2(C.byref(desc), C.byref(cfg), _ptr(U0), _ptr(U), _ptr(hist), cap, C.byref(it),
+                                C.byref(st), _ptr(wall)))
+    k = it.value
+    return U, hist[:k + 1].copy(), k, st.value, float(wall[0])
+
+
+def solve_m3(desc, U0, cfg: TpSolverCfg | None = None):
+    """tpfem::solve_m3_timestepping on the grid problem (solvers.hpp:489-542).
+    Returns (U, history, iterations, status, wall seconds)."""
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    cap = cfg.m3_max_cycles + 1
+    hist = np.zeros(cap)
+    it = C.c_int32()
+    st = C.c_int32()
+    wall = np.zeros(1)
+    U = np.zeros_like(U0)
+    _check(lib().tpref_solve_m3(C.byref(desc), C.byref(cfg), _ptr(U0), _ptr(U), _ptr(hist), cap, C.byref(it),
                                 C.byref(st), _ptr(wall)))
     k = it.value
     return U, hist[:k + 1].copy(), k, st.value, float(wall[0])

@@ -7,6 +7,7 @@
 //   tpref_static_init   -> tpfem::static_init            (solvers.hpp:276-296)
 //   tpref_solve_m1      -> tpfem::solve_m1_fixed_point   (solvers.hpp:301-369)
 //   tpref_solve_m2      -> tpfem::solve_m2_newton        (solvers.hpp:375-484)
+//   tpref_solve_m3      -> tpfem::solve_m3_timestepping  (solvers.hpp:489-542)
 //   tpref_periodic_solve-> tpfem::PeriodicSolver::solve  (periodic.hpp:154-198)
 //   tpref_residual      -> tpfem::residual + block_l2    (periodic.hpp:35-67)
 // with tporacle::GridProblem (grid_problem.hpp) supplying the BASELINE physics.
@@ -62,6 +63,7 @@ tpfem::SolverConfig to_ref(const tp_solver_cfg* c) {
   if (c->m2_inner_tol > 0) s.m2_inner_tol = c->m2_inner_tol;
   if (c->m2_inner_max > 0) s.m2_inner_max = c->m2_inner_max;
   if (c->m2_restart > 0) s.m2_restart = c->m2_restart;
+  if (c->m3_max_cycles > 0) s.m3_max_cycles = c->m3_max_cycles;
   s.threads = c->threads > 0 ? c->threads
                              : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   return s;
@@ -252,6 +254,25 @@ int tpref_solve_m2(const tp_problem_desc* d, const tp_solver_cfg* c, const doubl
     const tpfem::PeriodicState U0s = state_from(p, U0);
     const auto t0 = std::chrono::steady_clock::now();
     auto [U, rep] = tpfem::solve_m2_newton(p, F, U0s, cfg);
+    if (wall) *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
+    for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)
+      history[k] = rep.residual_history[k];
+    if (iterations) *iterations = rep.iterations;
+    if (status) *status = static_cast<int32_t>(rep.status);
+  });
+}
+
+// tpfem::solve_m3_timestepping (solvers.hpp:489-542) on the grid problem
+int tpref_solve_m3(const tp_problem_desc* d, const tp_solver_cfg* c, const double* U0, double* U_out,
+                   double* history, int32_t cap, int32_t* iterations, int32_t* status, double* wall) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const tpfem::BlockRhs F = p.loads();
+    const tpfem::PeriodicState U0s = state_from(p, U0);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [U, rep] = tpfem::solve_m3_timestepping(p, F, U0s, cfg);
     if (wall) *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
     for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)

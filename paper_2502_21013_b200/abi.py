@@ -45,7 +45,8 @@ class TpSolverCfg(C.Structure):
                 ("inner_max_iter", C.c_int32), ("warm_start", C.c_int32),
                 ("freq_chunk", C.c_int32), ("slice_chunk", C.c_int32),
                 ("freq_groups", C.c_int32), ("m2_max_outer", C.c_int32),
-                ("m2_inner_tol", C.c_double), ("m2_inner_max", C.c_int32), ("m2_restart", C.c_int32)]
+                ("m2_inner_tol", C.c_double), ("m2_inner_max", C.c_int32), ("m2_restart", C.c_int32),
+                ("m3_max_cycles", C.c_int32), ("reserved_", C.c_int32)]
 
 
 class TpShardPlan(C.Structure):
@@ -88,6 +89,8 @@ def default_cfg(**overrides) -> TpSolverCfg:
     c.m2_inner_tol = 1e-8
     c.m2_inner_max = 300
     c.m2_restart = 60
+    c.m3_max_cycles = 10
+    c.reserved_ = 0
     for k, v in overrides.items():
         setattr(c, k, v)
     return c

@@ -33,7 +33,7 @@ EXPORTS = [
     "tp_version", "tp_last_error", "tp_solver_cfg_default", "tp_problem_desc_baseline",
     "tp_problem_create", "tp_problem_destroy", "tp_problem_sizes", "tp_problem_loads",
     "tp_problem_mass", "tp_apply_k", "tp_residual", "tp_static_init", "tp_set_state",
-    "tp_get_state", "tp_choose_nu_hat", "tp_set_nu_hat", "tp_periodic_solve", "tp_solve_m1", "tp_solve_m2",
+    "tp_get_state", "tp_choose_nu_hat", "tp_set_nu_hat", "tp_periodic_solve", "tp_solve_m1", "tp_solve_m2", "tp_solve_m3",
     "tp_m1_begin", "tp_m1_sweep", "tp_problem_stream", "tp_problem_launches",
     "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
     "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
@@ -81,6 +81,7 @@ def lib():
         L.tp_set_nu_hat.argtypes = [vp, dp, C.c_double]
         L.tp_periodic_solve.argtypes = [vp, G, dp, dp]
         L.tp_solve_m2.argtypes = [vp, G, dp, dp, C.POINTER(TpReport), dp, dp, C.c_int32]
+        L.tp_solve_m3.argtypes = [vp, G, dp, dp, C.POINTER(TpReport), dp, dp, C.c_int32]
         L.tp_solve_m1.argtypes = [vp, G, dp, dp, C.POINTER(TpReport), dp, dp, C.c_int32,
                                   TP_ITERATE_CB, vp]
         L.tp_m1_begin.argtypes = [vp, G, dp]
@@ -363,24 +364,33 @@ class Problem:
                              sweep_time=rep.sweep_time, inner_iterations=rep.inner_iterations)
         return U, report
 
+    def _solve_m23(self, fn, method, cap, U0, cfg, out):
+        U0a = None if U0 is None else self._state(U0)
+        hist = np.zeros(cap)
+        contr = np.zeros(cap)
+        U = out if out is not None else np.zeros(self.shape)
+        rep = TpReport()
+        _check(fn(self._h, C.byref(cfg), _dp(U0a), _dp(U), C.byref(rep), _dp(hist), _dp(contr), cap))
+        k = rep.history_len
+        report = SolveReport(method=method, iterations=rep.iterations, residual_history=hist[:k].tolist(),
+                             contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
+                             wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
+                             inner_iterations=rep.inner_iterations)
+        return U, report
+
     def solve_m2_newton(self, U0=None, cfg: TpSolverCfg | None = None, out=None):
         """M2 all-at-once Newton (solve_m2_newton, solvers.hpp:375-484):
         FGMRES right-preconditioned by the periodic solver on the time-averaged
         Jacobian, Armijo line search.  Returns (U, SolveReport(method="m2"))."""
         cfg = cfg or default_cfg()
-        U0a = None if U0 is None else self._state(U0)
-        cap = cfg.m2_max_outer + 1
-        hist = np.zeros(cap)
-        contr = np.zeros(cap)
-        U = out if out is not None else np.zeros(self.shape)
-        rep = TpReport()
-        _check(lib().tp_solve_m2(self._h, C.byref(cfg), _dp(U0a), _dp(U), C.byref(rep), _dp(hist), _dp(contr), cap))
-        k = rep.history_len
-        report = SolveReport(method="m2", iterations=rep.iterations, residual_history=hist[:k].tolist(),
-                             contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
-                             wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
-                             inner_iterations=rep.inner_iterations)
-        return U, report
+        return self._solve_m23(lib().tp_solve_m2, "m2", cfg.m2_max_outer + 1, U0, cfg, out)
+
+    def solve_m3_timestepping(self, U0=None, cfg: TpSolverCfg | None = None, out=None):
+        """M3 sequential time stepping toward the limit cycle
+        (solve_m3_timestepping, solvers.hpp:489-542).  Returns
+        (U, SolveReport(method="m3")); iterations = completed periods."""
+        cfg = cfg or default_cfg()
+        return self._solve_m23(lib().tp_solve_m3, "m3", cfg.m3_max_cycles + 1, U0, cfg, out)
 
     # ---- device-resident sweeps
     def m1_begin(self, cfg: TpSolverCfg | None = None) -> float:

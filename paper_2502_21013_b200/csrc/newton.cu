@@ -22,7 +22,8 @@ namespace tpgpu {
 
 void newton_residual(Problem& p, const double* Ub, const double* Db, const double* d_alpha, double* Ut,
                      double* Rt, const int* d_slice_of, const int* d_active, int batches,
-                     double* norms2_host, DevBuf<double>& part, DevBuf<double>& red);
+                     double* norms2_host, DevBuf<double>& part, DevBuf<double>& red,
+                     const double* rhs = nullptr, double ms = 0.0);
 
 namespace {
 __global__ void k_accept(double* __restrict__ Ub, double* __restrict__ Rb, const double* __restrict__ Ut,

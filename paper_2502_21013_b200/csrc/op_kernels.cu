@@ -498,7 +498,8 @@ __global__ void __launch_bounds__(TX * TY) k_newton_residual(
     double* __restrict__ Ut, double* __restrict__ Rt, double* __restrict__ part,
     const int* __restrict__ slice_of, const int* __restrict__ active, int m, int c,
     const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
-    const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
+    const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc,
+    const double* __restrict__ rhs, double ms, const double* __restrict__ mass) {
   __shared__ Tile t;
   __shared__ double red[32];
   const size_t n = (size_t)m * m;
@@ -518,9 +519,16 @@ __global__ void __launch_bounds__(TX * TY) k_newton_residual(
   double r2 = 0;
   if (x < m && y < m) {
     const size_t i = (size_t)y * m + x;
-    double f = 0;
-    for (int r = 0; r < nsrc; ++r) f += src_time[s * nsrc + r] * src_prof[r * n + i];
-    const double res = f - gather<0>(t, threadIdx.x, threadIdx.y);
+    double res;
+    if (rhs) {
+      // time step (newton_elliptic with mass_scale, solvers.hpp:139-146): rhs - ms M u - K(u)
+      res = rhs[b * n + i] - ms * (mass[i] * t.u[threadIdx.y + 1][threadIdx.x + 1]) -
+            gather<0>(t, threadIdx.x, threadIdx.y);
+    } else {
+      double f = 0;
+      for (int r = 0; r < nsrc; ++r) f += src_time[s * nsrc + r] * src_prof[r * n + i];
+      res = f - gather<0>(t, threadIdx.x, threadIdx.y);
+    }
     Rt[b * n + i] = res;
     if (Ut) Ut[b * n + i] = t.u[threadIdx.y + 1][threadIdx.x + 1];
     r2 = res * res;
@@ -551,7 +559,8 @@ __global__ void k_reduce_batches(const double* __restrict__ part, int per, doubl
 // host `norms2` (synchronising).
 void newton_residual(Problem& p, const double* Ub, const double* Db, const double* d_alpha,
                      double* Ut, double* Rt, const int* d_slice_of, const int* d_active, int batches,
-                     double* norms2_host, DevBuf<double>& part, DevBuf<double>& red) {
+                     double* norms2_host, DevBuf<double>& part, DevBuf<double>& red, const double* rhs,
+                     double ms) {
   dim3 grid((p.m + TX - 1) / TX, (p.m + TY - 1) / TY, batches);
   const int per = grid.x * grid.y;
   part.ensure((size_t)per * batches);
@@ -559,7 +568,7 @@ void newton_residual(Problem& p, const double* Ub, const double* Db, const doubl
   cudaStream_t s = p.cur_stream();
   k_newton_residual<<<grid, dim3(TX, TY), 0, s>>>(
       Ub, Db, d_alpha, Ut, Rt, part.get(), d_slice_of, d_active, p.m, p.c, p.d_cell_mat.get(),
-      p.d_mat.get(), p.d_src_prof.get(), p.d_src_time.get(), (int)p.src_mats.size());
+      p.d_mat.get(), p.d_src_prof.get(), p.d_src_time.get(), (int)p.src_mats.size(), rhs, ms, p.d_mass.get());
   TP_LAUNCHED(&p);
   k_reduce_batches<<<batches, 256, 0, s>>>(part.get(), per, red.get());
   TP_LAUNCHED(&p);

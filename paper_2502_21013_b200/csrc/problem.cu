@@ -641,6 +641,7 @@ void tp_solver_cfg_default(tp_solver_cfg* c) {
   c->m2_inner_tol = 1e-8;
   c->m2_inner_max = 300;
   c->m2_restart = 60;
+  c->m3_max_cycles = 10;
 }
 
 int tp_problem_desc_baseline(int32_t config, tp_problem_desc* desc) {
@@ -955,9 +956,22 @@ int tp_kernel_timer(tp_problem* h, int32_t enable, int64_t* launches, double* ms
   });
 }
 
-// solve_m2_newton, solvers.hpp:375-484 (single GPU)
+// solve_m2_newton, solvers.hpp:375-484 / solve_m3_timestepping, solvers.hpp:489-542 (single GPU)
+static int solve_m23(tp_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
+                     double* history, double* contraction, int32_t cap, int method);
+
 int tp_solve_m2(tp_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
                 double* history, double* contraction, int32_t cap) {
+  return solve_m23(h, c, U0, U_out, rep, history, contraction, cap, 2);
+}
+
+int tp_solve_m3(tp_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
+                double* history, double* contraction, int32_t cap) {
+  return solve_m23(h, c, U0, U_out, rep, history, contraction, cap, 3);
+}
+
+static int solve_m23(tp_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
+                     double* history, double* contraction, int32_t cap, int method) {
   return guarded([&] {
     Problem& p = P(h);
     const tp_solver_cfg cfg = cfg_or_default(c);
@@ -969,7 +983,8 @@ int tp_solve_m2(tp_problem* h, const tp_solver_cfg* c, const double* U0, double*
       p.uhat_valid = false;
     }
     Problem::M2Result res;
-    p.solve_m2_dev(cfg, res);
+    if (method == 2) p.solve_m2_dev(cfg, res);
+    else p.solve_m3_dev(cfg, res);
     tp_report r{};
     r.iterations = res.iterations;
     r.status = res.status;

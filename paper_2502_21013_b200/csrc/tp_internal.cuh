@@ -261,6 +261,7 @@ class Problem {
     std::vector<double> history;
   };
   void solve_m2_dev(const tp_solver_cfg& cfg, M2Result& res);
+  void solve_m3_dev(const tp_solver_cfg& cfg, M2Result& res);  // M3 time stepping (m3.cu)
   void field_ranges(double* lo, double* hi, int* any);
   int last_inner = 0;
 };

@@ -31,7 +31,7 @@ def main(argv=None) -> int:
     ap.add_argument("--steps", type=int, default=0, help="override N")
     ap.add_argument("--u0", choices=["static_init", "zero"], default="static_init")
     ap.add_argument("--device", type=int, default=0)
-    ap.add_argument("--methods", default="m1", help="comma list of m1, m2 (run from the same U0)")
+    ap.add_argument("--methods", default="m1", help="comma list of m1, m2, m3 (run from the same U0)")
     a = ap.parse_args(argv)
 
     desc = baseline_desc(a.config)
@@ -58,9 +58,12 @@ def main(argv=None) -> int:
                 _, rep = p.solve_m1_fixed_point(U0, cfg)
             elif meth == "m2":
                 _, rep = p.solve_m2_newton(U0, cfg)
+            elif meth == "m3":
+                _, rep = p.solve_m3_timestepping(U0, cfg)
             else:
-                raise SystemExit(f"unknown method {meth!r} (m1, m2)")
-            print(f"{meth}: {rep.status} after {rep.iterations} iterations ({R.format_double(rep.wall_time)} s), "
+                raise SystemExit(f"unknown method {meth!r} (m1, m2, m3)")
+            unit = "cycles" if meth == "m3" else "iterations"
+            print(f"{meth}: {rep.status} after {rep.iterations} {unit} ({R.format_double(rep.wall_time)} s), "
                   f"residual {R.format_double(rep.residual_history[-1])}")
             reports.append((meth, rep))
         tau = desc.period / desc.steps

@@ -275,3 +275,24 @@ def test_m2_newton_matches_reference(ref, cfg0_ref):
     np.testing.assert_allclose(h[1:3], hr[1:3], rtol=1e-6)
     assert h[-1] <= cfg.tol * h[0]
     assert rel(U, Ur) <= 1e-9
+
+
+@pytest.mark.gpu
+def test_m3_timestepping_matches_reference(ref, cfg0_ref):
+    """M3 sequential time stepping against the
+    reference's solve_m3_timestepping from the same U0: same number of
+    periods and status, residual history (the per-step Newton solves stop at
+    static_tol, so the limit-cycle plateau agrees to that level)."""
+    r = cfg0_ref
+    cfg = default_cfg(tol=1e-8)
+    Ur, hr, kr, str_, _ = ref.solve_m3(r["desc"], r["U0"], cfg)
+    with Problem(r["desc"]) as p:
+        U, rep = p.solve_m3_timestepping(r["U0"], cfg)
+    assert rep.method == "m3" and rep.iterations == kr
+    assert rep.status == {0: "converged", 1: "max_iter", 2: "stalled"}[str_]
+    h = np.array(rep.residual_history)
+    assert h.shape == hr.shape
+    assert abs(h[0] - hr[0]) <= 1e-12 * hr[0]
+    np.testing.assert_allclose(h[1], hr[1], rtol=1e-8)
+    np.testing.assert_allclose(h[2:], hr[2:], rtol=1e-2)
+    assert rel(U, Ur) <= 1e-8
