@@ -791,12 +791,12 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
 }
 
 // x += xa p for the frequencies with a deferred update (fused Krylov step)
-__global__ void k_xfix(cplx* __restrict__ x, const cplx* __restrict__ p, const cplx* __restrict__ xa, size_t n,
-                       int nb) {
+template <class T>
+__global__ void k_xfix(T* __restrict__ x, const T* __restrict__ p, const T* __restrict__ xa, size_t n, int nb) {
   const int b = blockIdx.y;
   if (b >= nb) return;
-  const cplx a = xa[b];
-  if (a.re == 0.0 && a.im == 0.0) return;
+  const T a = xa[b];
+  if (norm2(a) == 0.0) return;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
     const size_t j = (size_t)b * n + i;
     x[j] = x[j] + mul(a, p[j]);
@@ -1143,7 +1143,7 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   }
   const size_t n0 = (size_t)B * levels[0].n;
   r.alloc(n0);
-  if (MODE == 0 && levels[0].fine.we && L > 1) r2.alloc(n0);
+  if (L > 1 && ((MODE == 0 && levels[0].fine.we) || MODE == 1)) r2.alloc(n0);
   xa.alloc(B);
   p0.alloc(n0);
   p1.alloc(n0);
@@ -1249,14 +1249,28 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   return vcycle_generic(l, nb, bl, dot);
 }
 
+// the streaming-kernel view of level l: the fine K_hat edge weights (frequency
+// mode) or the per-slice Jacobian stencils (slice mode)
+template <int MODE>
+FineOp BatchSolver<MODE>::stream_op(int l) const {
+  FineOp so;
+  if constexpr (MODE == 0) {
+    so = ops[l].fine;
+    so.lam = lam;
+  } else {
+    so.K = ops[l].K;
+    so.kstride = (size_t)7 * ops[l].n;
+    so.m = ops[l].m;
+    so.n = ops[l].n;
+  }
+  return so;
+}
+
 template <int MODE>
 void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out) {
-  if constexpr (MODE == 0) {
-    FineOp fo = ops[0].fine;
-    fo.lam = lam;
-    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
-                       qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
-  }
+  const FineOp fo = stream_op(0);
+  launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb, qv,
+                     qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
 }
 
 template <int MODE>
@@ -1267,10 +1281,9 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
   cudaStream_t s = p->cur_stream();
   T* z2 = lz0[l].get();
   T* zo = lz1[l].get();
-  if constexpr (MODE == 0) {
+  {
     {
-      FineOp fo = ops[l].fine;
-      fo.lam = lam;
+      const FineOp fo = stream_op(l);
       T* xcf;
       if (l + 1 == L - 1) {
         k_coarse_solve<T><<<nb, 64, 0, s>>>(coarse_inv, lb[l + 1].get(), lz0[l + 1].get(), ops[l + 1].n, act);
@@ -1291,8 +1304,8 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
         std::lock_guard<std::mutex> lk(p->ktimer.mu);
         p->ktimer.pending.emplace_back(e0, e1);
         // algorithmic bytes: read z2, r and the coarse correction (1/4), write z --
-        // 3.25 complex values per fine node of every active frequency
-        p->ktimer.bytes += 3.25 * 16.0 * (double)ops[l].n * (double)cur_active;
+        // 3.25 values per fine node of every active frequency
+        p->ktimer.bytes += 3.25 * (double)sizeof(T) * (double)ops[l].n * (double)cur_active;
         ++p->ktimer.launches;
       }
       return zo;
@@ -1395,11 +1408,12 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const Geo g0 = geo_for(ops[0].m, nb, p->num_sms, 8);
   const dim3 blk(TX, TY);
   const bool fine = MODE == 0 && ops[0].fine.we != nullptr;
-  FineOp fo = ops[0].fine;
-  fo.lam = reinterpret_cast<const cplx*>(lam);
+  // level 0 streamed (frequency mode: K_hat edge weights; slice mode: the
+  // per-slice Jacobian stencils) -- the streaming apply / fused update apply
+  const bool stream0 = fine || (MODE == 1 && stream_level(0));
   // partials per batch of each producing kernel
   const int per_t = g0.tiles;
-  const int per_a = fine ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
+  const int per_a = stream0 ? fine_partials(ops[0].m, 0) : per_t;   // streaming init / apply
   // V-cycle dot (up pass of level 0): streaming layout when that pass is streamed
   static const bool tile_coarse0 = std::getenv("TPGPU_TILE_COARSE") != nullptr;
   const bool up0_streamed = fine || stream_level(0) ||
@@ -1409,27 +1423,31 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   // fine level: the ring-staged streaming apply (mg_fine.cu) -- measured 8.08
   // vs 8.39 ms per cfg-1 sweep against the smem-tile apply (TPGPU_TILE_APPLY)
   static const bool use_stream_apply = std::getenv("TPGPU_TILE_APPLY") == nullptr;
-  const bool sapply = fine && use_stream_apply;
+  // slice mode: the tile apply (reading the symmetric Jacobian's four planes)
+  // and the separate update pass measured faster than the streaming apply with
+  // the fused update (cfg 1 init, ncu: 97 vs 99 ms); TPGPU_SLICE_STREAM_APPLY opts in
+  static const bool slice_sapply = std::getenv("TPGPU_SLICE_STREAM_APPLY") != nullptr;
+  const bool sapply = stream0 && use_stream_apply && (MODE == 0 || slice_sapply);
   // fused Krylov update (fine streaming path): r -= alpha q inside the fine
   // down pass (partial ||r||^2 from there), x += alpha p deferred to the next
   // apply -- the separate update pass disappears (cfg 1: 8.10 -> 7.65 ms per
   // sweep; TPGPU_UNFUSED_UPDATE restores the update pass)
   static const bool want_fuse = std::getenv("TPGPU_UNFUSED_UPDATE") == nullptr;
   const bool fused = sapply && ops.size() > 1 && want_fuse;
-  const int per_d = fine ? fine_partials(ops[0].m, 1) : per_t;  // fused down (||r||^2)
+  const int per_d = stream0 ? fine_partials(ops[0].m, 1) : per_t;  // fused down (||r||^2)
   const double rtol2 = cfg.rtol * cfg.rtol;
   int* act = active.get();
   int* zero = active.get() + B;
   T* const xa_ptr = fused ? xa.get() : nullptr;
   cudaStream_t s = p->cur_stream();
   const int l = 0;
-  if (fine && warm && sapply) {
-    if constexpr (MODE == 0) launch_fine_apply(*p, fo, b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
+  if (warm && sapply) {
+    launch_fine_apply(*p, stream_op(0), b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
   } else {
     DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
     TP_LAUNCHED(p);
   }
-  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (fine && warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(),
+  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(),
                                   mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
   TP_LAUNCHED(p);
   if (warm) {
@@ -1457,9 +1475,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
       if (sapply) {
-        if constexpr (MODE == 0)
-          launch_fine_apply(*p, fo, z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false,
-                            fused ? x : nullptr, xa_ptr);
+        launch_fine_apply(*p, stream_op(0), z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false,
+                          fused ? x : nullptr, xa_ptr);
       } else {
         DISPATCH_FAM(l, (k_apply_dot<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, z, pin, pout, q.get(), beta.get(), act,
                                                                         first, nb, g0.BB, part.get(), x, xa_ptr)));
@@ -1510,14 +1527,12 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       TP_CUDA(cudaStreamSynchronize(s));
       last_active = h_count[iters & 1];
     }
-    if constexpr (MODE == 0) {
-      if (fused) {
-        // the deferred x += alpha p of the last iteration (nothing is pending
-        // when the loop ended by convergence: its final apply consumed it)
-        const dim3 gx((unsigned)std::min<size_t>((ops[0].n + 255) / 256, 64), nb);
-        k_xfix<<<gx, 256, 0, s>>>(x, done ? pout : pin, xa.get(), (size_t)ops[0].n, nb);
-        TP_LAUNCHED(p);
-      }
+    if (fused) {
+      // the deferred x += alpha p of the last iteration (nothing is pending
+      // when the loop ended by convergence: its final apply consumed it)
+      const dim3 gx((unsigned)std::min<size_t>((ops[0].n + 255) / 256, 64), nb);
+      k_xfix<T><<<gx, 256, 0, s>>>(x, done ? pout : pin, xa.get(), (size_t)ops[0].n, nb);
+      TP_LAUNCHED(p);
     }
   }
   TP_CUDA(cudaStreamSynchronize(s));

@@ -104,6 +104,7 @@ struct BatchSolver {
   T* vcycle_level(int lvl, int nb, const T* bl, T* z_first, bool first_done, bool dot);
   T* vcycle_generic(int lvl, int nb, const T* bl, bool dot);
   bool stream_level(int l) const;  // slice mode: this level's passes run streamed
+  FineOp stream_op(int l) const;   // the streaming kernels' view of level l
   // fine streaming level: down pass (optionally fusing r_out = r_in - alpha q),
   // and the rest of the cycle (coarse levels + up pass)
   void fine_down0(int nb, const T* r_in, const T* qv = nullptr, T* r_out = nullptr);
@@ -132,7 +133,11 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // slice mode: real vectors, per-slice Jacobian stencils
 void launch_stream_down(Problem& p, const FineOp& op, const double* r, double* z2, double* bc, int mc,
-                        const int* active, double om1, double om2, int nb);
+                        const int* active, double om1, double om2, int nb, const double* q = nullptr,
+                        const double* alpha = nullptr, double* rout = nullptr, double* part = nullptr);
+void launch_fine_apply(Problem& p, const FineOp& op, const double* z, const double* pin, double* pout, double* q,
+                       const double* beta, const int* active, int first, int nb, double* part, bool init,
+                       double* x = nullptr, const double* xa = nullptr);
 void launch_stream_up(Problem& p, const FineOp& op, const double* r, const double* z2, const double* xc, int mc,
                       double* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // Build fine-grid element stencils (K_hat or Jacobians at U, per batch).

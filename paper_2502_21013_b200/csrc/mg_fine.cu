@@ -736,53 +736,69 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
 // XUPD: also the deferred solution update x += xa p_in of the previous
 // iteration (fused Krylov update): x staged as a third vector; frequencies
 // that converged last iteration (inactive, xa != 0) get only that update.
-template <int INIT, int RA, int WPBK, bool XUPD = false>
-__global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cplx* __restrict__ z,
-                                                            const cplx* __restrict__ pin, cplx* __restrict__ pout,
-                                                            cplx* __restrict__ q, const cplx* __restrict__ beta,
+// p = z + beta p_in with the exact fma pattern of the complex recurrence
+__device__ __forceinline__ cplx zpb(cplx bt, cplx pv, cplx zz) {
+  return {fma(bt.re, pv.re, fma(-bt.im, pv.im, zz.re)), fma(bt.re, pv.im, fma(bt.im, pv.re, zz.im))};
+}
+__device__ __forceinline__ double zpb(double bt, double pv, double zz) { return fma(bt, pv, zz); }
+__device__ __forceinline__ bool nonzero(cplx a) { return a.re != 0.0 || a.im != 0.0; }
+__device__ __forceinline__ bool nonzero(double a) { return a != 0.0; }
+// x + a p (the deferred solution update; complex: the same product order as before)
+__device__ __forceinline__ cplx xpa(cplx xv, cplx a, cplx pv) {
+  return {xv.re + (a.re * pv.re - a.im * pv.im), xv.im + (a.re * pv.im + a.im * pv.re)};
+}
+__device__ __forceinline__ double xpa(double xv, double a, double pv) { return xv + a * pv; }
+
+template <class S, int INIT, int RA, int WPBK, bool XUPD = false>
+__global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typename S::T* __restrict__ z,
+                                                            const typename S::T* __restrict__ pin,
+                                                            typename S::T* __restrict__ pout,
+                                                            typename S::T* __restrict__ q,
+                                                            const typename S::T* __restrict__ beta,
                                                             const int* __restrict__ active, int first, int nb,
-                                                            double* __restrict__ part, cplx* __restrict__ xs = nullptr,
-                                                            const cplx* __restrict__ xa = nullptr) {
-  using S = Five;
+                                                            double* __restrict__ part,
+                                                            typename S::T* __restrict__ xs = nullptr,
+                                                            const typename S::T* __restrict__ xa = nullptr) {
+  using T = typename S::T;
   constexpr int H = 1, OWN = WL - 2 * H;  // 30
-  constexpr int RV = RA + 2, RC = RA + 2, NVV = XUPD ? 3 : 2;
+  constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN, NVV = XUPD ? 3 : 2;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
   const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RH, nb, nullptr);
   const bool on = INIT || !active || active[it.b[0]];
-  cplx xab{0, 0};
+  T xab{};
   if (XUPD) xab = xa[it.b[0]];
-  const bool pend = XUPD && (xab.re != 0.0 || xab.im != 0.0);
+  const bool pend = XUPD && nonzero(xab);
   if (!it.ok || (!on && !pend)) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
-  VRow<NVV>* const vring = reinterpret_cast<VRow<NVV>*>(fine_smem) + wib * RV;
+  VRowT<T, NVV>* const vring = reinterpret_cast<VRowT<T, NVV>*>(fine_smem) + wib * RV;
   WRow<S::NW>* const wring =
-      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRow<NVV>)) + wib * RC;
+      reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRowT<T, NVV>)) + wib * RC;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
   const int xc = min(max(x, 0), m - 1);
   const int b = it.b[0];
   const size_t o = (size_t)b * op.n;
-  const cplx* const zp = z + o + xc;
-  const cplx* const pp = pin + o + xc;
-  cplx* const po = pout + o + xc;
-  cplx* const qo = q + o + xc;
-  cplx* const xo = XUPD ? xs + o + xc : nullptr;
-  const cplx l = op.lam[b];
+  const T* const zp = z + o + xc;
+  const T* const pp = pin + o + xc;
+  T* const po = pout + o + xc;
+  T* const qo = q + o + xc;
+  T* const xo = XUPD ? xs + o + xc : nullptr;
+  const cplx l = op.lam ? op.lam[b] : cplx{0, 0};
   const bool usep = INIT || !first;  // p_in is read
-  const cplx bt = (INIT || first) ? cplx{0, 0} : beta[b];
+  const T bt = (INIT || first) ? T{} : beta[b];
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 2, ylast = ye;  // staged rows
-  const S::Src src = S::src(op, x, xc, y0, b);
+  const typename S::Src src = S::src(op, x, xc, y0, b);
   int vi = 0, wi = 0;
   auto issue = [&](int yr) {
     if (yr <= ylast) {
       const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
       const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
-      cp16(&vring[vi].v[0][lane], zp + off, rin);
-      cp16(&vring[vi].v[1][lane], pp + off, rin && (usep || pend));
-      if (XUPD) cp16(&vring[vi].v[2][lane], xo + off, rin && pend);
+      cpv(&vring[vi].v[0][lane], zp + off, rin);
+      cpv(&vring[vi].v[1][lane], pp + off, rin && (usep || pend));
+      if (XUPD) cpv(&vring[vi].v[2][lane], xo + off, rin && pend);
       S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
@@ -793,14 +809,11 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
   for (int j = 0; j <= RA; ++j) issue(y0 + j);
   int vr = 0, sr = 0;
   cp_wait<RA>();
-  S::Reg k0 = S::first(wring[0], lane), k1 = k0;  // rows yi, yi-1
+  if (S::XLANE) __syncwarp();
+  typename S::Reg k0 = S::first(wring[0], lane), k1 = k0;  // rows yi, yi-1
   // p at rows yi, yi-1, yi-2; b (INIT) at rows yi, yi-1
-  cplx p0 = (INIT) ? vring[0].v[1][lane] : cplx{0, 0}, p1{0, 0}, p2{0, 0};
-  if (!INIT) {
-    const cplx zz = vring[0].v[0][lane], pv = vring[0].v[1][lane];
-    p0 = {fma(bt.re, pv.re, fma(-bt.im, pv.im, zz.re)), fma(bt.re, pv.im, fma(bt.im, pv.re, zz.im))};
-  }
-  cplx b0 = vring[0].v[0][lane], b1{0, 0};
+  T p0 = INIT ? vring[0].v[1][lane] : zpb(bt, vring[0].v[1][lane], vring[0].v[0][lane]), p1{}, p2{};
+  T b0 = vring[0].v[0][lane], b1{};
   double s0 = 0, s1 = 0;
   TP_UNROLL(TPGPU_STREAM_UNROLL)
   for (int yi = ys - 1; yi <= ylast; ++yi) {
@@ -808,33 +821,28 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const cpl
     vr = wrap_inc(vr, RV);
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
+    if (S::XLANE) __syncwarp();
     k1 = k0;
     k0 = S::load(wring[sr], lane, k1);
-    const cplx zz = vring[vr].v[0][lane], pv = vring[vr].v[1][lane];
-    if (XUPD && pend && own && yi >= ys && yi < ye) {
-      const cplx xv = vring[vr].v[2][lane];
-      xo[(long)yi * m] = {xv.re + (xab.re * pv.re - xab.im * pv.im), xv.im + (xab.re * pv.im + xab.im * pv.re)};
-    }
+    const T zz = vring[vr].v[0][lane], pv = vring[vr].v[1][lane];
+    if (XUPD && pend && own && yi >= ys && yi < ye) xo[(long)yi * m] = xpa(vring[vr].v[2][lane], xab, pv);
     p2 = p1; p1 = p0;
     b1 = b0; b0 = zz;
-    p0 = INIT ? pv
-              : cplx{fma(bt.re, pv.re, fma(-bt.im, pv.im, zz.re)), fma(bt.re, pv.im, fma(bt.im, pv.re, zz.im))};
+    p0 = INIT ? pv : zpb(bt, pv, zz);
     // q at row yi-1
-    const cplx Ap = S::apply(k1, l, S::diag(k1, l), p2, p1, p0);
+    const T Ap = S::apply(k1, l, S::diag(k1, l), p2, p1, p0);
     const int y = yi - 1;
     if (on && own && y >= ys && y < ye) {
       const long i = (long)y * m;
       if (INIT) {
-        const cplx r = {b1.re - Ap.re, b1.im - Ap.im};
+        const T r = b1 - Ap;
         qo[i] = r;
-        s0 += b1.re * b1.re + b1.im * b1.im;
-        s1 += r.re * r.re + r.im * r.im;
+        s0 = sq_acc(b1, s0);
+        s1 = sq_acc(r, s1);
       } else {
         po[i] = p1;
         qo[i] = Ap;
-        const cplx t = cm(p1, Ap);
-        s0 += t.re;
-        s1 += t.im;
+        dot_acc(p1, Ap, s0, s1);
       }
     }
   }
@@ -902,6 +910,30 @@ void up_t(Problem& p, const FineOp& op, const T* r, const T* z2, const T* xc, in
       op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
 
+template <class S, int RA, int W, class T = typename S::T>
+void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T* q, const T* beta, const int* active,
+             int first, int nb, double* part, bool init, T* x, const T* xa) {
+  constexpr size_t sm = ring_smem<S, 2, RA, W>();
+  constexpr size_t sm3 = ring_smem<S, 3, RA, W>();
+  static bool attrs = [] {
+    cudaFuncSetAttribute(k_stream_apply<S, 0, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_apply<S, 1, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_apply<S, 0, RA, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
+    return true;
+  }();
+  (void)attrs;
+  const dim3 g = grid_for(op.m, 30, nb, RH, W);
+  cudaStream_t s = p.cur_stream();
+  if (init)
+    k_stream_apply<S, 1, RA, W><<<g, WL * W, sm, s>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+  else if (xa)
+    k_stream_apply<S, 0, RA, W, true><<<g, WL * W, sm3, s>>>(op, z, pin, pout, q, beta, active, first, nb, part, x,
+                                                             xa);
+  else
+    k_stream_apply<S, 0, RA, W><<<g, WL * W, sm, s>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+  TP_LAUNCHED(&p);
+}
+
 }  // namespace
 
 int fine_partials(int m, int kind) {
@@ -911,25 +943,15 @@ int fine_partials(int m, int kind) {
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init, cplx* x,
                        const cplx* xa) {
-  constexpr int RA = 4, W = 4;
-  constexpr size_t sm = (size_t)W * ((RA + 2) * sizeof(VRow<2>) + (RA + 2) * sizeof(WRow<Five::NW>));
-  constexpr size_t sm3 = (size_t)W * ((RA + 2) * sizeof(VRow<3>) + (RA + 2) * sizeof(WRow<Five::NW>));
-  static bool attrs = [] {
-    cudaFuncSetAttribute(k_stream_apply<0, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_stream_apply<1, RA, W>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    cudaFuncSetAttribute(k_stream_apply<0, RA, W, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm3);
-    return true;
-  }();
-  (void)attrs;
-  const dim3 g = grid_for(op.m, 30, nb, RH, W);
-  if (init)
-    k_stream_apply<1, RA, W><<<g, WL * W, sm, p.cur_stream()>>>(op, z, pin, pout, q, beta, active, first, nb, part);
-  else if (xa)
-    k_stream_apply<0, RA, W, true><<<g, WL * W, sm3, p.cur_stream()>>>(op, z, pin, pout, q, beta, active, first, nb,
-                                                                  part, x, xa);
-  else
-    k_stream_apply<0, RA, W><<<g, WL * W, sm, p.cur_stream()>>>(op, z, pin, pout, q, beta, active, first, nb, part);
-  TP_LAUNCHED(&p);
+  apply_t<Five, 4, 4>(p, op, z, pin, pout, q, beta, active, first, nb, part, init, x, xa);
+}
+
+// slice mode: the fine-level Jacobian apply (p = z + beta p, q = J p, p^T q;
+// or the initial residual; with xa: the deferred x update)
+void launch_fine_apply(Problem& p, const FineOp& op, const double* z, const double* pin, double* pout, double* q,
+                       const double* beta, const int* active, int first, int nb, double* part, bool init, double* x,
+                       const double* xa) {
+  apply_t<SevenJ, 4, 2>(p, op, z, pin, pout, q, beta, active, first, nb, part, init, x, xa);
 }
 
 // Down / up pass of one level: Five on the fine level (op.we set), Seven on
@@ -976,8 +998,12 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
 // Slice mode (static_init Newton solves): the same passes on real vectors with
 // per-slice symmetric Jacobian stencils (op.K = J of level l, op.kstride = 7n)
 void launch_stream_down(Problem& p, const FineOp& op, const double* r, double* z2, double* bc, int mc,
-                        const int* active, double om1, double om2, int nb) {
-  down_t<SevenJ, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+                        const int* active, double om1, double om2, int nb, const double* q, const double* alpha,
+                        double* rout, double* part) {
+  if (q)
+    down_t<SevenJ, 1, 4, 2, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+  else
+    down_t<SevenJ, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   TP_LAUNCHED(&p);
 }
 
