@@ -1135,7 +1135,8 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
       if (L - l > kMaxSmall || levels[l].five) continue;
       int ms[kMaxSmall];
       for (int j = l; j < L; ++j) ms[j - l] = levels[j].m;
-      if (small_cycle_smem(ms, L - l) <= (size_t)200 * 1024) {
+      static const size_t cap_kb = std::getenv("TPGPU_SMALL_KB") ? std::atoi(std::getenv("TPGPU_SMALL_KB")) : 200;
+      if (small_cycle_smem(ms, L - l) <= cap_kb * 1024) {
         small_from = l;
         break;
       }
