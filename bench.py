@@ -185,10 +185,12 @@ def run_b200(args):
     barrier(pg)
     torch.cuda.synchronize()
     evs[0].record(stream)
+    fiters = []
     for k in range(args.steps):
         r, it = p.m1_sweep()
         history.append(r)
         inner.append(it)
+        fiters.append(p.sweep_stats()[1])
         evs[k + 1].record(stream)
     torch.cuda.synchronize()
     clk.__exit__(None, None, None)
@@ -248,11 +250,12 @@ def run_b200(args):
         t_setup = time.perf_counter() - t0
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(cfg.m1_max_outer + 1)]
         ev[0].record(stream)
-        hist, its = [r0], []
+        hist, its, fits = [r0], [], []
         while len(its) < cfg.m1_max_outer and not hist[-1] <= cfg.tol * hist[0]:
             r, it = p.m1_sweep()
             hist.append(r)
             its.append(it)
+            fits.append(p.sweep_stats()[1])
             ev[len(its)].record(stream)
         torch.cuda.synchronize()
         sw = [ev[k].elapsed_time(ev[k + 1]) for k in range(len(its))]
@@ -262,7 +265,8 @@ def run_b200(args):
                 "median_sweep_ms": float(np.median(sw)),
                 "median_dof_per_s": D * jobs / (allreduce_max(pg, float(np.median(sw))) / 1e3),
                 "inner_iterations_median": float(np.median(its)),
-                "inner_iterations_max": int(max(its)) if its else 0}
+                "inner_iterations_max": int(max(its)) if its else 0,
+                "frequency_iterations_mean": float(np.mean(fits)) if fits else 0.0}
 
     hbm, src = peaks()
     # Dominant kernel (k_stream_up<Five>: fine-level V-cycle up pass, ~20% of a
@@ -295,21 +299,23 @@ def run_b200(args):
                                            "includes the other groups' kernels")
     else:
         roofline.update(timed)
-    # Whole-sweep algorithmic bytes: B = 72 D + 16 n S sum_k it_k
-    # with S = 15.0 complex streams per inner iteration and frequency as
-    # implemented (fine: apply 6 = read z, p, x, write p, q, x; down with the
-    # fused residual update 4.25 = read r, q, write r, z2, 1/4 coarse rhs;
-    # up 3.25; first Galerkin level 5.5 / 4; fused small-level cycle: read b,
-    # write z at 1/16).
-    K = desc.steps // 2 + 1
+    # Whole-sweep algorithmic bytes per GPU:
+    # B = 72 D / P + 16 n S sum_k it_k over this rank's frequency blocks
+    # (sum_k it_k counted exactly by the solver, tp_sweep_stats), with S = 15.0
+    # complex streams per inner iteration and frequency as implemented (fine:
+    # apply 6 = read z, p, x, write p, q, x; down with the fused residual update
+    # 4.25 = read r, q, write r, z2, 1/4 coarse rhs; up 3.25; first Galerkin
+    # level 5.5 / 4; fused small-level cycle: read b, write z at 1/16).
     n = (desc.cells - 1) ** 2
     STREAMS = 13.5 + 5.5 / 4 + 2.0 / 16
     mean_inner = float(np.mean(inner)) if inner else 0.0
-    b_alg = 72.0 * D + 16.0 * n * STREAMS * K * mean_inner
+    mean_fit = float(np.mean(fiters)) if fiters else 0.0
+    b_alg = 72.0 * D / (world if sharded else 1) + 16.0 * n * STREAMS * mean_fit
     t_sweep = total_ms / 1e3 / args.steps
     sweep_roofline = {"bound": "hbm", "achieved": b_alg / t_sweep / 1e9, "peak": hbm, "unit": "GB/s",
                       "frac": b_alg / t_sweep / 1e9 / hbm, "bytes_per_sweep": b_alg,
-                      "streams_per_inner_iteration": STREAMS, "inner_iterations_mean": mean_inner}
+                      "streams_per_inner_iteration": STREAMS, "inner_iterations_mean": mean_inner,
+                      "frequency_iterations_per_sweep": mean_fit}
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,

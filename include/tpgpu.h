@@ -210,6 +210,10 @@ int tp_m1_begin(tp_problem* p, const tp_solver_cfg* cfg, double* residual0);
 /* One fixed-point sweep (solvers.hpp:326-341) on the device state; returns
  * ||R|| of the new iterate and the inner iteration count of the sweep. */
 int tp_m1_sweep(tp_problem* p, double* residual, int32_t* inner_iterations);
+/* Inner-solve work of the last periodic solve (sweep): the largest iteration
+ * count of any frequency block and the sum over blocks of their iteration
+ * counts (the bench's algorithmic-byte count). */
+int tp_sweep_stats(const tp_problem* p, int32_t* max_iterations, int64_t* frequency_iterations);
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------
  * Partition of a sharded problem: node-row strip [row0,row1)
  * for K(u)/residual/RHS/DFT (all N slices local), frequency block

@@ -34,7 +34,7 @@ EXPORTS = [
     "tp_problem_create", "tp_problem_destroy", "tp_problem_sizes", "tp_problem_loads",
     "tp_problem_mass", "tp_apply_k", "tp_residual", "tp_static_init", "tp_set_state",
     "tp_get_state", "tp_choose_nu_hat", "tp_set_nu_hat", "tp_periodic_solve", "tp_solve_m1", "tp_solve_m2", "tp_solve_m3",
-    "tp_m1_begin", "tp_m1_sweep", "tp_problem_stream", "tp_problem_launches",
+    "tp_m1_begin", "tp_m1_sweep", "tp_sweep_stats", "tp_problem_stream", "tp_problem_launches",
     "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
     "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
     "tp_kernel_timer",
@@ -86,6 +86,7 @@ def lib():
                                   TP_ITERATE_CB, vp]
         L.tp_m1_begin.argtypes = [vp, G, dp]
         L.tp_m1_sweep.argtypes = [vp, dp, ip]
+        L.tp_sweep_stats.argtypes = [vp, ip, C.POINTER(C.c_int64)]
         L.tp_problem_stream.argtypes = [vp]
         L.tp_problem_stream.restype = vp
         L.tp_problem_launches.argtypes = [vp]
@@ -404,6 +405,13 @@ class Problem:
         it = C.c_int32()
         _check(lib().tp_m1_sweep(self._h, C.byref(r), C.byref(it)))
         return r.value, it.value
+
+    def sweep_stats(self):
+        """(largest per-frequency iteration count, sum over frequency blocks of
+        their iteration counts) of the last periodic solve."""
+        mx, tot = C.c_int32(), C.c_int64()
+        _check(lib().tp_sweep_stats(self._h, C.byref(mx), C.byref(tot)))
+        return mx.value, tot.value
 
     def kernel_timer(self, enable: bool):
         """(launches, ms, algorithmic bytes) of the dominant kernel since the

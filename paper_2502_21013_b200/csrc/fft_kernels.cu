@@ -44,6 +44,19 @@ __device__ __forceinline__ void acp16(void* sdst, const void* g, bool ok) {
 }
 __device__ __forceinline__ void acp_wait_all() { asm volatile("cp.async.wait_all;\n" ::: "memory"); }
 
+// block sum of v into *out (thread 0); blockDim.x a multiple of 32
+__device__ __forceinline__ void block_sum_to(double v, double* out) {
+  __shared__ double red[32];
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double t = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) t += red[w];
+    *out = t;
+  }
+}
+
 template <bool INVERSE>
 __device__ void transform(cplx* z, cplx* tmp, const cplx* __restrict__ tw, int N, int P, bool pow2) {
   const int tid = threadIdx.x, nt = blockDim.x;
@@ -82,7 +95,8 @@ __device__ void transform(cplx* z, cplx* tmp, const cplx* __restrict__ tw, int N
 }
 
 __global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N,
-                               int P, int bits, int pow2, const cplx* __restrict__ tw) {
+                               int P, int bits, int pow2, const cplx* __restrict__ tw,
+                               double* __restrict__ sq) {
   extern __shared__ cplx smem[];
   cplx* z = smem;
   cplx* tmp = smem + (size_t)P * N;
@@ -98,6 +112,7 @@ __global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ 
   __syncthreads();
   transform<false>(z, tmp, tw, N, P, pow2);
   const int K = N / 2 + 1;
+  double e = 0;
   for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
     const int k = t / C, cc = t % C;
     if (j0 + cc >= n) continue;
@@ -107,7 +122,9 @@ __global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ 
     if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
     else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
     Ghat[(size_t)k * n + j0 + cc] = X;
+    e = fma(X.re, X.re, fma(X.im, X.im, e));
   }
+  if (sq) block_sum_to(e, sq + blockIdx.x);
 }
 
 __global__ void k_rdft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N,
@@ -292,7 +309,7 @@ __device__ void stockham(cplx* z, const cplx* tw, int N, int P) {
 
 // shared layout: twiddles W_N^m (N), then the P interleaved columns (P N)
 __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N, int P,
-                               const cplx* __restrict__ tw) {
+                               const cplx* __restrict__ tw, double* __restrict__ sq) {
   extern __shared__ cplx smem[];
   cplx* tws = smem;
   cplx* z = smem + N;
@@ -310,6 +327,7 @@ __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ 
   __syncthreads();
   stockham<false>(z, tws, N, P);
   const int K = N / 2 + 1;
+  double e = 0;
   for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
     const int k = t / C, cc = t - k * C;
     if (j0 + cc >= n) continue;
@@ -319,7 +337,9 @@ __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ 
     if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
     else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
     Ghat[(size_t)k * n + j0 + cc] = X;
+    e = fma(X.re, X.re, fma(X.im, X.im, e));
   }
+  if (sq) block_sum_to(e, sq + blockIdx.x);
 }
 
 __global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N, int P,
@@ -475,19 +495,23 @@ FftPlan& plan_for(Problem& p) {
 
 }  // namespace
 
-void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat) {
+int rdft_forward_blocks(Problem& p) {
+  FftPlan& pl = plan_for(p);
+  const size_t n = (size_t)p.sh.nr;
+  const int C = 2 * (pl.stockham ? pl.sP : pl.P);
+  return (int)((n + C - 1) / C);
+}
+
+void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat, double* sq) {
   FftPlan& pl = plan_for(p);
   const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
+  const int blocks = rdft_forward_blocks(p);
   if (pl.stockham) {
-    const int blocks = (int)((n + 2 * pl.sP - 1) / (2 * pl.sP));
-    k_sfft_forward<<<blocks, pl.sT, pl.ssmem, p.stream>>>(G, Ghat, n, pl.N, pl.sP, pl.tw.get());
-    TP_LAUNCHED(&p);
-    return;
+    k_sfft_forward<<<blocks, pl.sT, pl.ssmem, p.stream>>>(G, Ghat, n, pl.N, pl.sP, pl.tw.get(), sq);
+  } else {
+    k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
+                                                       sq);
   }
-  const int C = 2 * pl.P;
-  const int blocks = (int)((n + C - 1) / C);
-  k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2,
-                                                     pl.tw.get());
   TP_LAUNCHED(&p);
 }
 

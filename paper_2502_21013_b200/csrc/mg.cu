@@ -22,7 +22,9 @@
 // streams on the fine level, ~1/3 of that again on the coarse levels.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
+#include <string>
 
 #include "mg.cuh"
 
@@ -872,7 +874,8 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
                           T* __restrict__ rho, T* __restrict__ mu, T* __restrict__ alpha,
                           T* __restrict__ beta, double* __restrict__ bn2, double* __restrict__ rn2,
                           int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask,
-                          T* __restrict__ xa, int* __restrict__ count = nullptr) {
+                          T* __restrict__ xa, int* __restrict__ count = nullptr,
+                          const double* __restrict__ bfloor = nullptr, double fscale = 0.0) {
   const int b = blockIdx.x;
   if (b >= nb) return;
   // active-batch counter of this iteration: cleared by ST_ALPHA, summed by ST_RN
@@ -884,12 +887,16 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
   batch_sum(part, per, b, s0, s1);
   if (threadIdx.x != 0) return;
   switch (stage) {
-    case ST_INIT:
-      bn2[b] = s0;
+    case ST_INIT: {
+      // stopping reference: ||g_k||^2, floored at the frequency's equal share
+      // of the whole right-hand side (BatchSolver::bfloor)
+      const double bref = bfloor ? fmax(s0, fscale * *bfloor) : s0;
+      bn2[b] = bref;
       rn2[b] = s1;
       zero[b] = (s0 == 0.0);
-      active[b] = (!mask || mask[b]) && (s0 > 0.0) && (s1 > rtol2 * s0);
+      active[b] = (!mask || mask[b]) && (s0 > 0.0) && (s1 > rtol2 * bref);
       break;
+    }
     case ST_RHO0:
       rho[b] = from2<T>(s0, s1);
       break;
@@ -1449,7 +1456,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     TP_LAUNCHED(p);
   }
   k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(),
-                                  mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
+                                  mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
+                                  nullptr, bfloor, bfloor_scale);
   TP_LAUNCHED(p);
   if (warm) {
     k_zero_flagged<MODE><<<g0.grid, blk, 0, s>>>(op0, x, nb, g0.BB, zero);
@@ -1459,6 +1467,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   TP_LAUNCHED(p);
   TP_CUDA(cudaMemcpyAsync(h_count, count.get(), sizeof(int), cudaMemcpyDeviceToHost, s));
   TP_CUDA(cudaStreamSynchronize(s));
+  static const bool dbg_freq = std::getenv("TPGPU_DEBUG_FREQ") != nullptr;
+  std::vector<int> dbg_it(dbg_freq ? nb : 0, 1);
   int iters = 0;
   int64_t batch_iters = 0;
   int last_active = h_count[0];
@@ -1501,7 +1511,15 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       TP_LAUNCHED(p);
       TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
       TP_CUDA(cudaEventRecord(ev[slot], s));
-      batch_iters += last_active;
+      if (dbg_freq) {  // experiment: per-frequency iteration counts (synchronizes every iteration)
+        std::vector<int> ha(nb);
+        TP_CUDA(cudaMemcpyAsync(ha.data(), act, nb * sizeof(int), cudaMemcpyDeviceToHost, s));
+        TP_CUDA(cudaStreamSynchronize(s));
+        for (int k = 0; k < nb; ++k) dbg_it[k] += ha[k] ? 1 : 0;
+      }
+      // frequency-iterations (exact): iteration 1 works on the initially
+      // active batches, iteration it >= 2 on those still active after it - 1
+      if (it == 1) batch_iters += last_active;
       if (it >= 2) {
         TP_CUDA(cudaEventSynchronize(ev[slot ^ 1]));
         last_active = h_count[slot ^ 1];
@@ -1511,6 +1529,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
           done = true;
           break;
         }
+        batch_iters += last_active;
       }
       iters = it;
       if (fused) {
@@ -1544,6 +1563,15 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   double worst = 0;
   for (int k = 0; k < nb; ++k)
     if (hb[k] > 0) worst = std::max(worst, std::sqrt(hr[k] / hb[k]));
+  if (dbg_freq) {
+    std::string line = "freqdbg nb " + std::to_string(nb) + " iters " + std::to_string(iters) + " |";
+    for (int k = 0; k < nb; ++k) {
+      char buf[64];
+      std::snprintf(buf, sizeof buf, " %d:%.2e", dbg_it[k], std::sqrt(hb[k]));
+      line += buf;
+    }
+    std::fprintf(stderr, "%s\n", line.c_str());
+  }
   if (st) {
     st->iterations = std::max(st->iterations, iters);
     st->batch_iterations += batch_iters;

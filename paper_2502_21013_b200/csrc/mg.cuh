@@ -77,6 +77,10 @@ struct BatchSolver {
   const T* coarse_inv = nullptr;  // n_L^2 per batch
   const cplx* lam = nullptr;      // freq mode: per batch symbol (device)
   const int* ext_mask = nullptr;  // optional: batches with mask 0 are skipped
+  // optional stopping floor: batch b stops at ||r_b||^2 <= rtol^2 max(||b_b||^2,
+  // bfloor_scale * *bfloor) (device scalar: ||b||^2 of the whole right-hand side)
+  const double* bfloor = nullptr;
+  double bfloor_scale = 0.0;
   // work
   std::vector<DevBuf<T>> lb, lz0, lz1;  // per level (level 0: b is external)
   DevBuf<T> r, r2, p0, p1, q;

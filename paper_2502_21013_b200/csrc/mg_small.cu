@@ -173,16 +173,30 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
     restrict_to(L.m, sl.m[j + 1], a, bs(j + 1));
     __syncthreads();
   }
-  // coarsest: x = inv b (inv transposed: A[j * nc + i] = inv(i, j))
+  // coarsest: x = inv b (inv transposed: A[j * nc + i] = inv(i, j)), spread
+  // over the whole block: G groups of nc threads each sum a strided share of
+  // the columns (coalesced rows of A), then a fixed-order sum of the G partials
+  // (scratch: level 0's first work vector, free until the up pass).  One
+  // thread per row walking all nc columns left the other warps at the barrier
+  // for a quarter of the kernel (ncu stall sampling).
   {
     const int nc = mof(nl - 1) * mof(nl - 1);
     const cplx* A = inv + (size_t)bt * nc * nc;
     const cplx* bc = bs(nl - 1);
     cplx* x = za(nl - 1);
-    for (int i = threadIdx.x; i < nc; i += SNT) {
+    cplx* scratch = za(0);
+    const int G = max(1, min(SNT / nc, n0 / nc));
+    const int t = threadIdx.x, g = t / nc, i = t - g * nc;
+    if (g < G) {
       cplx acc{0, 0};
-      for (int k = 0; k < nc; ++k) acc = acc + cmul(A[(size_t)k * nc + i], bc[k]);
-      x[i] = acc;
+      for (int k = g; k < nc; k += G) acc = acc + cmul(A[(size_t)k * nc + i], bc[k]);
+      scratch[g * nc + i] = acc;
+    }
+    __syncthreads();
+    for (int r = t; r < nc; r += SNT) {
+      cplx acc = scratch[r];
+      for (int q = 1; q < G; ++q) acc = acc + scratch[q * nc + r];
+      x[r] = acc;
     }
     __syncthreads();
   }

@@ -480,18 +480,50 @@ void Problem::periodic_solve_dev(const tp_solver_cfg& cfg, SolveStats* st) {
 // current spectrum), [all-to-all back], inverse DFT and the imaginary guard.
 void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bool warm, const tp_solver_cfg& cfg,
                                   SolveStats* st) {
-  launch_rdft_forward(*this, in, Ghat.get());
+  // Stopping floor of the frequency solves: ||r_k|| <= rtol max(||g_k||,
+  // ||g||/sqrt(K)) with ||g||^2 the energy of the whole half spectrum (summed
+  // inside the forward DFT).  Blocks whose right-hand side is round-off (the
+  // even harmonics of an odd-symmetric response) stop at the frequency's
+  // equal share of the total instead of iterating on noise; the aggregate
+  // residual bound stays within sqrt(2) of the per-frequency rule's
+  // (DESIGN.md §5).  TPGPU_NO_FREQ_FLOOR restores the plain per-frequency rule.
+  static const bool use_floor = std::getenv("TPGPU_NO_FREQ_FLOOR") == nullptr;
+  const int nblk = rdft_forward_blocks(*this);
+  spec_sq.ensure((size_t)nblk + 1);
+  launch_rdft_forward(*this, in, Ghat.get(), use_floor ? spec_sq.get() : nullptr);
+  if (use_floor) {
+    if (sharded()) {
+      const double tot = global_sum(reduce_sum(*this, spec_sq.get(), nblk));
+      TP_CUDA(cudaMemcpyAsync(spec_sq.get() + nblk, &tot, sizeof(double), cudaMemcpyHostToDevice, stream));
+      TP_CUDA(cudaStreamSynchronize(stream));
+    } else {
+      reduce_sum_dev(*this, spec_sq.get(), nblk, spec_sq.get() + nblk);
+    }
+  }
   if (sharded()) alltoall_to_freq();
   const int Kr = sh.k1 - sh.k0;
+  const double* floor_ptr = use_floor ? spec_sq.get() + nblk : nullptr;
+  const double floor_scale = 1.0 / (double)(N / 2 + 1);
   int iters = 0;
+  int64_t fiters = 0;
   auto run = [&](BatchSolver<0>& sv, int k0, int nb, SolveStats* sst) {
+    sv.bfloor = floor_ptr;
+    sv.bfloor_scale = floor_scale;
     sv.lam = w.lam.get() + k0;
     sv.coarse_inv = w.inv.get() + (size_t)k0 * w.nL * w.nL;
     return sv.solve(spec_in() + (size_t)k0 * n, spec_out() + (size_t)k0 * n, nb, warm, sst);
   };
   if (w.parts == 1) {
-    for (int k0 = 0; k0 < Kr; k0 += w.chunk)
-      iters = std::max(iters, run(w.solver, k0, std::min(w.chunk, Kr - k0), st));
+    for (int k0 = 0; k0 < Kr; k0 += w.chunk) {
+      SolveStats cs;
+      iters = std::max(iters, run(w.solver, k0, std::min(w.chunk, Kr - k0), &cs));
+      fiters += cs.batch_iterations;
+      if (st) {
+        st->iterations = std::max(st->iterations, cs.iterations);
+        st->batch_iterations += cs.batch_iterations;
+        st->max_rel_residual = std::max(st->max_rel_residual, cs.max_rel_residual);
+      }
+    }
   } else {
     // groups of `parts` chunks: group 0 on hs[0] (this thread), the others on
     // hs[g] driven by helper threads
@@ -526,6 +558,7 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
         if (e) std::rethrow_exception(e);
       for (int g = 0; g < P; ++g) {
         iters = std::max(iters, git[g]);
+        fiters += gst[g].batch_iterations;
         if (st) {
           st->iterations = std::max(st->iterations, gst[g].iterations);
           st->batch_iterations += gst[g].batch_iterations;
@@ -535,6 +568,7 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
     }
   }
   last_inner = iters;
+  last_freq_iters = fiters;
   if (sharded()) alltoall_from_freq();
   double re2 = 0, im2 = 0;
   launch_rdft_inverse(*this, Uhat.get(), out, &re2, &im2);
@@ -844,6 +878,15 @@ int tp_m1_sweep(tp_problem* h, double* residual, int32_t* inner) {
     const double r = p.residual_and_rhs(true);
     if (residual) *residual = r;
     if (inner) *inner = st.iterations;
+  });
+}
+
+int tp_sweep_stats(const tp_problem* h, int32_t* max_iterations, int64_t* frequency_iterations) {
+  return guarded([&] {
+    tpgpu::require(h != nullptr, "sweep stats: null problem");
+    const Problem& p = *h->impl;
+    if (max_iterations) *max_iterations = p.last_inner;
+    if (frequency_iterations) *frequency_iterations = p.last_freq_iters;
   });
 }
 

@@ -207,6 +207,7 @@ class Problem {
   DevBuf<double> halo_lo, halo_hi, halo_send;  // N*m each
   DevBuf<cplx> Ghat_f, Uhat_f, xstage;         // (k1-k0)*n frequency blocks, staging
   DevBuf<double> red_all;                      // P doubles (allgather)
+  DevBuf<double> spec_sq;  // forward-DFT |X|^2 partials, then [last] the total (frequency stopping floor)
   void exchange_halo();
   double global_sum(double local);
   void global_minmax(double* lo, double* hi, int count);
@@ -264,12 +265,17 @@ class Problem {
   void solve_m3_dev(const tp_solver_cfg& cfg, M2Result& res);  // M3 time stepping (m3.cu)
   void field_ranges(double* lo, double* hi, int* any);
   int last_inner = 0;
+  int64_t last_freq_iters = 0;  // sum over frequency blocks of the last periodic solve
 };
 
 // kernels / helpers implemented in the .cu files
-void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat);
+// sq (optional): per-block partial sums of |X|^2 over the half spectrum written
+// (rdft_forward_blocks(p) of them)
+void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat, double* sq = nullptr);
+int rdft_forward_blocks(Problem& p);
 // returns imaginary-residue norm^2 partial sum and real norm^2 (host)
 void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2);
 double reduce_sum(Problem& p, const double* partials, int count);
+void reduce_sum_dev(Problem& p, const double* partials, int count, double* out);  // no host sync
 
 }  // namespace tpgpu

@@ -124,6 +124,25 @@ def test_m1_fixed_point_matches_reference(cfg0_ref):
         assert rel(U, m1.U) <= ITERATE_TOL
 
 
+def test_sweep_stats_and_stopping_floor(cfg0_ref):
+    """tp_sweep_stats: the largest per-frequency count and the sum over the
+    N/2+1 frequency blocks.  The even harmonics of the cfg-0 response are
+    round-off; with the stopping floor they stop early, so the sum stays well
+    below (N/2+1) x max."""
+    r = cfg0_ref
+    with Problem(r["desc"]) as p:
+        p.set_nu_hat(r["nu"], r["q"])
+        p.set_state(r["U0"])
+        p.m1_begin(r["cfg"])
+        K = r["desc"].steps // 2 + 1
+        for _ in range(3):
+            _, it = p.m1_sweep()
+            mx, tot = p.sweep_stats()
+            assert mx == it and mx >= 1
+            assert 1 <= tot <= K * mx
+        assert tot < 0.8 * K * mx, (tot, K, mx)
+
+
 def test_linear_control_converges_in_one_sweep(ref):
     """nu == nu0 everywhere: frozen nu_hat == nu, K_hat == K, one sweep."""
     d = baseline_desc(5)
