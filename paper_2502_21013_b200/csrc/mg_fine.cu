@@ -871,7 +871,7 @@ int rh_for(int m) {
   static const int env1 = std::getenv("TPGPU_RH1") ? std::atoi(std::getenv("TPGPU_RH1")) : 0;
   if (env > 0 && m >= 200) return env;
   if (env1 > 0 && m >= 100 && m < 200) return env1;
-  return m >= 200 ? 64 : m >= 100 ? 32 : m >= 50 ? 16 : 8;
+  return m >= 200 ? 32 : m >= 100 ? 16 : m >= 50 ? 16 : 8;
 }
 
 int env_int(const char* name, int dflt) {

@@ -14,6 +14,8 @@ from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg  # noqa: E
 g = np.load(os.path.join(os.path.dirname(__file__), "..", "tests", "golden", "cfg0_reference.npz"))
 for rtol in [float(x) for x in sys.argv[1:]] or [1e-13]:
     cfg = default_cfg(tol=1e-8, inner_rtol=rtol)
+    if os.environ.get("FG"):
+        cfg.freq_groups = int(os.environ["FG"])
     with Problem(baseline_desc(0)) as p:
         p.set_nu_hat(g["nu_hat"], float(g["q"]))
         log = []
