@@ -795,6 +795,7 @@ __global__ void __launch_bounds__(NT, 4) k_up(Op<MODE> op, const TT<MODE>* __res
 // x += xa p for the frequencies with a deferred update (fused Krylov step)
 template <class T>
 __global__ void k_xfix(T* __restrict__ x, const T* __restrict__ p, const T* __restrict__ xa, size_t n, int nb) {
+  TP_PDL_ENTRY();
   const int b = blockIdx.y;
   if (b >= nb) return;
   const T a = xa[b];
@@ -876,6 +877,7 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
                           int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask,
                           T* __restrict__ xa, int* __restrict__ count = nullptr,
                           const double* __restrict__ bfloor = nullptr, double fscale = 0.0) {
+  TP_PDL_ENTRY();
   const int b = blockIdx.x;
   if (b >= nb) return;
   // active-batch counter of this iteration: cleared by ST_ALPHA, summed by ST_RN
@@ -1455,9 +1457,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
     TP_LAUNCHED(p);
   }
-  k_scalars<T><<<nb, 256, 0, s>>>(ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(),
-                                  mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
-                                  nullptr, bfloor, bfloor_scale);
+  launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, nullptr, bfloor, bfloor_scale);
   TP_LAUNCHED(p);
   if (warm) {
     k_zero_flagged<MODE><<<g0.grid, blk, 0, s>>>(op0, x, nb, g0.BB, zero);
@@ -1479,8 +1479,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   T* pout = p1.get();
   if (last_active > 0) {
     T* z = vcycle_level(0, nb, rcur, nullptr, false, true);
-    k_scalars<T><<<nb, 256, 0, s>>>(ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
-                                    alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
+    launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0);
     TP_LAUNCHED(p);
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
@@ -1494,9 +1493,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         TP_LAUNCHED(p);
       }
       const int slot = it & 1;
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
-                                      count.get() + slot);
+      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0);
       TP_LAUNCHED(p);
       if (fused) {
         fine_down0(nb, rcur, q.get(), rnext);
@@ -1505,9 +1502,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
                                                nb, g0.BB, part.get());
         TP_LAUNCHED(p);
       }
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_RN, part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr,
-                                      count.get() + slot);
+      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RN, part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0);
       TP_LAUNCHED(p);
       TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
       TP_CUDA(cudaEventRecord(ev[slot], s));
@@ -1538,8 +1533,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       } else {
         z = vcycle_level(0, nb, rcur, nullptr, false, true);
       }
-      k_scalars<T><<<nb, 256, 0, s>>>(ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(),
-                                      alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr);
+      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0);
       TP_LAUNCHED(p);
       std::swap(pin, pout);
     }
@@ -1551,7 +1545,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       // the deferred x += alpha p of the last iteration (nothing is pending
       // when the loop ended by convergence: its final apply consumed it)
       const dim3 gx((unsigned)std::min<size_t>((ops[0].n + 255) / 256, 64), nb);
-      k_xfix<T><<<gx, 256, 0, s>>>(x, done ? pout : pin, xa.get(), (size_t)ops[0].n, nb);
+      launch_pdl(k_xfix<T>, gx, dim3(256), 0, s, x, static_cast<const T*>(done ? pout : pin), static_cast<const T*>(xa.get()),
+                 (size_t)ops[0].n, nb);
       TP_LAUNCHED(p);
     }
   }

@@ -432,6 +432,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN, NVV = FUSED ? 2 : NB;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
+  TP_PDL_ENTRY();
   const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -591,6 +592,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
+  TP_PDL_ENTRY();
   const ItemNB<WPBK, NB> it = item_nb<WPBK, NB>(m, OWN, rh, nb, active);
   if (!it.ok) return;
   const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
@@ -764,6 +766,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN, NVV = XUPD ? 3 : 2;
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
+  TP_PDL_ENTRY();
   const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RH, nb, nullptr);
   const bool on = INIT || !active || active[it.b[0]];
   T xab{};
@@ -891,9 +894,8 @@ void down_t(Problem& p, const FineOp& op, const T* r, T* z2, T* bc, int mc, cons
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  k_stream_down<S, NB, RA, WPBK, FUSED>
-      <<<grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.cur_stream()>>>(
-          op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
+  launch_pdl(k_stream_down<S, NB, RA, WPBK, FUSED>, grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK),
+             sm, p.cur_stream(), op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
 }
 
 template <class S, int NB, int RA, int WPBK, class T = typename S::T>
@@ -906,8 +908,8 @@ void up_t(Problem& p, const FineOp& op, const T* r, const T* z2, const T* xc, in
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  k_stream_up<S, NB, RA, WPBK><<<grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), WL * WPBK, sm, p.cur_stream()>>>(
-      op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
+  launch_pdl(k_stream_up<S, NB, RA, WPBK>, grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK), sm,
+             p.cur_stream(), op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
 
 template <class S, int RA, int W, class T = typename S::T>
@@ -924,13 +926,17 @@ void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T*
   (void)attrs;
   const dim3 g = grid_for(op.m, 30, nb, RH, W);
   cudaStream_t s = p.cur_stream();
+  using T0 = T*;
+  using C0 = const T*;
   if (init)
-    k_stream_apply<S, 1, RA, W><<<g, WL * W, sm, s>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+    launch_pdl(k_stream_apply<S, 1, RA, W>, g, dim3(WL * W), sm, s, op, z, pin, pout, q, beta, active, first, nb, part,
+               T0(nullptr), C0(nullptr));
   else if (xa)
-    k_stream_apply<S, 0, RA, W, true><<<g, WL * W, sm3, s>>>(op, z, pin, pout, q, beta, active, first, nb, part, x,
-                                                             xa);
+    launch_pdl(k_stream_apply<S, 0, RA, W, true>, g, dim3(WL * W), sm3, s, op, z, pin, pout, q, beta, active, first,
+               nb, part, x, xa);
   else
-    k_stream_apply<S, 0, RA, W><<<g, WL * W, sm, s>>>(op, z, pin, pout, q, beta, active, first, nb, part);
+    launch_pdl(k_stream_apply<S, 0, RA, W>, g, dim3(WL * W), sm, s, op, z, pin, pout, q, beta, active, first, nb, part,
+               T0(nullptr), C0(nullptr));
   TP_LAUNCHED(&p);
 }
 

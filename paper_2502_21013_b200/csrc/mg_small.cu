@@ -129,6 +129,7 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
                                                         const cplx* __restrict__ inv, const cplx* __restrict__ b0,
                                                         cplx* __restrict__ z0, const int* __restrict__ active,
                                                         double om1, double om2) {
+  TP_PDL_ENTRY();
   const int bt = blockIdx.x;
   if (active && !active[bt]) return;
   extern __shared__ __align__(16) unsigned char small_smem[];
@@ -239,7 +240,7 @@ void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, cons
            cudaSuccess;
   }();
   require(attr && sm <= 227 * 1024, "small-level cycle: shared memory");
-  k_small_cycle<<<nb, SNT, sm, p.cur_stream()>>>(sl, lam, inv, b, z, active, om1, om2);
+  launch_pdl(k_small_cycle, dim3(nb), dim3(SNT), sm, p.cur_stream(), sl, lam, inv, b, z, active, om1, om2);
   TP_LAUNCHED(&p);
 }
 

@@ -210,17 +210,26 @@ __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
 // owns one 32x8 node tile and SB consecutive slices, so everything that
 // does not depend on u -- per-cell material law and nu_hat, per-node mass
 // and source profiles -- is loaded once and reused SB times, u^{s-1} comes
-// from the previous slice's tile, and r^2 is reduced once per block.
+// from the previous slice's tile, and r^2 is reduced once per block.  The
+// u tiles of the next SD-1 slices are in flight (cp.async ring of SD slots,
+// zero-filled off the domain, one barrier per slice): with one slice of
+// look-ahead the kernel was latency-bound at ~1.3 TB/s.
 constexpr int SB = 16;
+constexpr int SD = 6;
+
+__device__ __forceinline__ void cp_async8(void* sdst, const void* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+}
 
 template <bool WANT_G>
-__global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
+__global__ void __launch_bounds__(TX * TY, 4) k_sweep_slices(
     const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
     int sy0, int rows, double* __restrict__ G, double* __restrict__ part, int m, int c, int N, double inv_tau,
     const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
     const double* __restrict__ nu_hat, const double* __restrict__ mass,
     const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
-  __shared__ double su[TY + 2][TX + 2];
+  __shared__ double su[SD][TY + 2][TX + 2];
   __shared__ double cnu0[TY + 1][TX + 1], cdnu[TY + 1][TX + 1], cbs2[TY + 1][TX + 1], chat[TY + 1][TX + 1];
   __shared__ double red[32];
   const size_t n = (size_t)m * m;
@@ -228,6 +237,47 @@ __global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
   const int x0 = blockIdx.x * TX, y0 = sy0 + blockIdx.y * TY;
   const int sbeg = blockIdx.z * SB, send = min(N, sbeg + SB);
+  // staged tile elements of this thread (<= 2): source of vertex (X, Y) =
+  // (x0 + lx, y0 + ly) in slice s = base + s * stride (main strip, or the
+  // neighbours' halo rows), or zero (Dirichlet boundary / outside)
+  constexpr int TN = (TY + 2) * (TX + 2);
+  const int k0 = tid, k1 = tid + TX * TY;
+  const double* sb[2];
+  size_t sstr[2];
+  bool sok[2];
+  int sly[2], slx[2];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int k = e == 0 ? k0 : k1;
+    const int ly = k / (TX + 2), lx = k % (TX + 2);
+    sly[e] = ly;
+    slx[e] = lx;
+    const int x = x0 + lx - 1, y = y0 + ly - 1;  // node of vertex (X, Y)
+    sb[e] = U;
+    sstr[e] = nl;
+    sok[e] = false;
+    if (k < TN && x >= 0 && x < m && y >= 0 && y < m) {
+      const int yl = y - sy0;
+      if (yl < 0) {
+        if (yl == -1 && halo_lo) { sb[e] = halo_lo + x; sstr[e] = m; sok[e] = true; }
+      } else if (yl >= rows) {
+        if (yl == rows && halo_hi) { sb[e] = halo_hi + x; sstr[e] = m; sok[e] = true; }
+      } else {
+        sb[e] = U + (size_t)yl * m + x;
+        sok[e] = true;
+      }
+    }
+  }
+  auto issue = [&](int sl) {
+    if (sl < send) {
+      double(*t)[TX + 2] = su[sl % SD];
+      cp_async8(&t[sly[0]][slx[0]], sok[0] ? sb[0] + (size_t)sl * sstr[0] : U, sok[0]);
+      if (k1 < TN) cp_async8(&t[sly[1]][slx[1]], sok[1] ? sb[1] + (size_t)sl * sstr[1] : U, sok[1]);
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+#pragma unroll
+  for (int j = 0; j < SD - 1; ++j) issue(sbeg + j);
   // per-cell material constants of the tile (+ halo cells)
   for (int k = tid; k < (TY + 1) * (TX + 1); k += TX * TY) {
     const int ly = k / (TX + 1), lx = k % (TX + 1);
@@ -258,31 +308,16 @@ __global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
   if (own && mi != 0) uprev = U[(size_t)((sbeg + N - 1) % N) * nl + il];
   const double c2 = (double)c * (double)c;
   double r2 = 0;
-  // each thread stages <= 2 tile values; the next slice's are loaded while
-  // the current slice is computed
-  constexpr int TN = (TY + 2) * (TX + 2);
-  const int k0 = tid, k1 = tid + TX * TY;
-  const int l0y = k0 / (TX + 2), l0x = k0 % (TX + 2), l1y = k1 / (TX + 2), l1x = k1 % (TX + 2);
-  auto fetch = [&](int s, double& v0, double& v1) {
-    const StripView sv{halo_lo ? halo_lo + (size_t)s * m : nullptr, halo_hi ? halo_hi + (size_t)s * m : nullptr,
-                       sy0, rows};
-    const double* us = U + (size_t)s * nl;
-    v0 = vertex_u(us, sv, m, x0 + l0x, y0 + l0y);
-    v1 = k1 < TN ? vertex_u(us, sv, m, x0 + l1x, y0 + l1y) : 0.0;
-  };
-  double n0 = 0, n1 = 0;
-  if (sbeg < send) fetch(sbeg, n0, n1);
   for (int s = sbeg; s < send; ++s) {
-    __syncthreads();  // previous slice's tile fully consumed
-    su[l0y][l0x] = n0;
-    if (k1 < TN) su[l1y][l1x] = n1;
-    __syncthreads();
-    if (s + 1 < send) fetch(s + 1, n0, n1);
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SD - 2) : "memory");
+    __syncthreads();  // slice s staged by every thread; slice s-1's slot free
+    issue(s + SD - 1);
     if (own) {
+      const double(*t)[TX + 2] = su[s % SD];
       const int lx = tx + 1, ly = ty + 1;
-      const double uC = su[ly][lx], uE = su[ly][lx + 1], uW = su[ly][lx - 1];
-      const double uN = su[ly + 1][lx], uS = su[ly - 1][lx];
-      const double uNE = su[ly + 1][lx + 1], uSW = su[ly - 1][lx - 1];
+      const double uC = t[ly][lx], uE = t[ly][lx + 1], uW = t[ly][lx - 1];
+      const double uN = t[ly + 1][lx], uS = t[ly - 1][lx];
+      const double uNE = t[ly + 1][lx + 1], uSW = t[ly - 1][lx - 1];
       // the six incident triangles: (cell, type, contribution dx*sx + dy*sy, (dx, dy))
       // T1(X,Y): cell (lx,ly)    d=(uE-uC, uNE-uE)   contrib -(uE-uC)
       // T2(X,Y): cell (lx,ly)    d=(uNE-uN, uN-uC)   contrib -(uN-uC)
@@ -296,12 +331,12 @@ __global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
       const int cxs[6] = {0, 0, -1, -1, -1, 0}, cys[6] = {0, 0, 0, -1, -1, -1};
       double ku = 0, kh = 0;
 #pragma unroll
-      for (int t = 0; t < 6; ++t) {
-        const int cx = lx + cxs[t], cy = ly + cys[t];
-        const double s2 = c2 * (dx[t] * dx[t] + dy[t] * dy[t]);
+      for (int t6 = 0; t6 < 6; ++t6) {
+        const int cx = lx + cxs[t6], cy = ly + cys[t6];
+        const double s2 = c2 * (dx[t6] * dx[t6] + dy[t6] * dy[t6]);
         const double nu = fma(cdnu[cy][cx], s2 * acc_rcp(s2 + cbs2[cy][cx]), cnu0[cy][cx]);
-        ku = fma(0.5 * nu, con[t], ku);
-        if (WANT_G) kh = fma(chat[cy][cx], con[t], kh);
+        ku = fma(0.5 * nu, con[t6], ku);
+        if (WANT_G) kh = fma(chat[cy][cx], con[t6], kh);
       }
       double f = 0;
 #pragma unroll
@@ -314,6 +349,7 @@ __global__ void __launch_bounds__(TX * TY, 3) k_sweep_slices(
       uprev = uC;
     }
   }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   const double tot = block_sum(r2, red);
   if (tid == 0) part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tot;
 }

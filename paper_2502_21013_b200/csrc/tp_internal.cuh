@@ -38,6 +38,39 @@ struct Error : std::runtime_error {
 
 void set_last_error(const std::string& msg, double residual);
 
+// ---------------------------------------------------------------- PDL
+// Programmatic dependent launch for the kernel chains of the frequency solves
+// (one stream per frequency group, ~9 dependent kernels per inner iteration):
+// a kernel launched by launch_pdl may be scheduled while its predecessor
+// drains; it waits in TP_PDL_ENTRY (griddepcontrol.wait: every prerequisite
+// grid complete and its memory visible) before touching memory, and at once
+// allows its own dependents to launch.  Every kernel launched through
+// launch_pdl must start with TP_PDL_ENTRY (a no-op under a normal launch).
+// TPGPU_PDL=0 launches normally.
+#ifndef TPGPU_PDL_TRIGGER
+#define TPGPU_PDL_TRIGGER 0
+#endif
+#define TP_PDL_ENTRY()                                               \
+  do {                                                               \
+    asm volatile("griddepcontrol.wait;\n" ::: "memory");            \
+    if (TPGPU_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); \
+  } while (0)
+bool pdl_enabled();
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+  cudaLaunchConfig_t c = {};
+  c.gridDim = grid;
+  c.blockDim = block;
+  c.dynamicSmemBytes = smem;
+  c.stream = s;
+  c.attrs = at;
+  c.numAttrs = 1;
+  TP_CUDA(cudaLaunchKernelEx(&c, kern, static_cast<KArgs>(args)...));
+}
+
 inline void require(bool ok, const std::string& msg) {
   if (!ok) throw Error(TP_EINVAL, msg);
 }

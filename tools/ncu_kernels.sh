@@ -9,5 +9,6 @@ for spec in $1; do
   ncu -i /tmp/p_${TAG}_${k}_$s.ncu-rep --page raw --csv > gpurun_out/raw_${TAG}_${k}_$s.csv
   ncu -i /tmp/p_${TAG}_${k}_$s.ncu-rep --page details --csv > gpurun_out/details_${TAG}_${k}_$s.csv
   ncu -i /tmp/p_${TAG}_${k}_$s.ncu-rep --page source --csv > gpurun_out/source_${TAG}_${k}_$s.csv 2>/dev/null
+  ncu -i /tmp/p_${TAG}_${k}_$s.ncu-rep --page source --csv --print-source cuda > gpurun_out/srccuda_${TAG}_${k}_$s.csv 2>/dev/null
 done
 ls -la gpurun_out | tail -20
