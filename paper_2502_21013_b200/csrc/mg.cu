@@ -1144,12 +1144,23 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
       if (L - l > kMaxSmall || levels[l].five) continue;
       int ms[kMaxSmall];
       for (int j = l; j < L; ++j) ms[j - l] = levels[j].m;
-      static const size_t cap_kb = std::getenv("TPGPU_SMALL_KB") ? std::atoi(std::getenv("TPGPU_SMALL_KB")) : 200;
+      static const size_t cap_kb = std::getenv("TPGPU_SMALL_KB") ? std::atoi(std::getenv("TPGPU_SMALL_KB")) : 224;
       if (small_cycle_smem(ms, L - l) <= cap_kb * 1024) {
         small_from = l;
         break;
       }
     }
+  }
+  if (small_from >= 0) {
+    small = SmallLevels{};
+    small.levels = L - small_from;
+    for (int j = small_from; j < L; ++j) {
+      small.m[j - small_from] = levels[j].m;
+      small.K[j - small_from] = levels[j].K;
+      small.M[j - small_from] = levels[j].M;
+    }
+    small_pack.alloc(small_pack_size(small.m, small.levels));
+    pack_small_levels(*p, small, small_pack.get());
   }
   const size_t n0 = (size_t)B * levels[0].n;
   r.alloc(n0);
@@ -1241,14 +1252,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   T* zo = lz1[l].get();
   if constexpr (MODE == 0) {
     if (l == small_from) {
-      SmallLevels sl;
-      sl.levels = L - l;
-      for (int j = l; j < L; ++j) {
-        sl.m[j - l] = ops[j].m;
-        sl.K[j - l] = ops[j].K;
-        sl.M[j - l] = ops[j].M;
-      }
-      launch_small_cycle(*p, sl, lam, coarse_inv, bl, zo, act, cfg.omega, cfg.omega2, nb);
+      launch_small_cycle(*p, small, lam, coarse_inv, bl, zo, act, cfg.omega, cfg.omega2, nb);
       return zo;
     }
     if (ops[l].fine.we) {

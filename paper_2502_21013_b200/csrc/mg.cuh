@@ -53,8 +53,13 @@ struct SmallLevels {
   int m[kMaxSmall] = {};
   const double* K[kMaxSmall] = {};
   const double* M[kMaxSmall] = {};
+  // packed copies (pack_small_levels): per level 4 planes (C, E, N, NE) of
+  // (m+2)^2 zero-padded {K, M} pairs
+  const double2* KM[kMaxSmall] = {};
 };
 size_t small_cycle_smem(const int* m, int levels);
+size_t small_pack_size(const int* m, int levels);  // doubles
+void pack_small_levels(Problem& p, SmallLevels& sl, double* buf);
 void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, const cplx* inv, const cplx* b,
                         cplx* z, const int* active, double om1, double om2, int nb);
 
@@ -93,7 +98,8 @@ struct BatchSolver {
   int* h_count = nullptr;  // pinned [2]
   int cur_active = 0;      // active batches as last seen by the host (kernel-timer byte accounting)
   int small_from = -1;     // frequency mode: first level handled by the fused small-level cycle
-  SmallLevels small;
+  SmallLevels small;        // its levels (stencils packed into small_pack)
+  DevBuf<double> small_pack;
   cudaEvent_t ev[2] = {nullptr, nullptr};
 
   void init(Problem* prob, const std::vector<LevelOp>& levels, int batches, const MGConfig& c);

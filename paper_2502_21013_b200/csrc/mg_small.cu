@@ -16,6 +16,13 @@
 // with __syncthreads between the half-steps.  The same operator, weights and
 // transfer operators as mg.cu / mg_fine.cu, so the preconditioner (and COCG's
 // iterates) do not depend on which path ran.
+//
+// Layout: every level's vectors are stored zero-padded, (m+2)^2 with the node
+// (x, y) at (y+1)(m+2) + x+1, and the level's stencil is a packed copy
+// (pack_small_levels) of its C, E, N, NE planes as {K, M} pairs on the same
+// padded grid -- so a node's 7-point row is 7 16-byte coefficient loads and
+// 7 neighbour reads with no boundary tests, and threads map to (x, y) by
+// shifts (a power-of-two row pitch) instead of divisions.
 #include "mg.cuh"
 
 namespace tpgpu {
@@ -38,126 +45,146 @@ __device__ __forceinline__ cplx crcp(cplx a) {
 }
 
 struct Lvl {
-  const double* K;
-  const double* M;
-  int m, n;
+  const double2* C;  // 4 planes of np padded {K, M}
+  int m, w, np;      // nodes per side, padded pitch m+2, padded size
+  int sh;            // log2 of the power-of-two thread pitch >= m
 };
 
-__device__ __forceinline__ cplx coefc(const Lvl& L, int dir, int i, cplx l) {
-  const double k = __ldg(L.K + (size_t)dir * L.n + i), mm = __ldg(L.M + (size_t)dir * L.n + i);
-  return {fma(l.re, mm, k), l.im * mm};
-}
+#ifndef TPGPU_SMALL_UNROLL
+#define TPGPU_SMALL_UNROLL 1
+#endif
+#define TP_SMALL_PRAGMA(x) _Pragma(#x)
+#define TP_SMALL_UNROLL_N(n) TP_SMALL_PRAGMA(unroll n)
+#define TP_SMALL_UNROLL TP_SMALL_UNROLL_N(TPGPU_SMALL_UNROLL)
+// threads of the block over the level's nodes: x = tid & (2^sh - 1), rows
+// stepping by SNT >> sh
+#define FOR_NODES(L, ...)                                                     \
+  {                                                                           \
+    const int x_ = threadIdx.x & ((1 << (L).sh) - 1);                         \
+    if (x_ < (L).m)                                                           \
+      TP_SMALL_UNROLL                                                         \
+      for (int y_ = threadIdx.x >> (L).sh; y_ < (L).m; y_ += SNT >> (L).sh) { \
+        const int x = x_, y = y_;                                             \
+        const int P = (y + 1) * (L).w + x + 1;                                \
+        __VA_ARGS__                                                           \
+      }                                                                       \
+  }
 
-// diagonal and off-diagonal part of (lambda M + K) v at node (x, y); v in
-// shared memory.  Off-diagonal part in split form sum K_d v_d + l sum M_d v_d.
-__device__ __forceinline__ void stencil(const Lvl& L, int x, int y, cplx l, const cplx* v, cplx& d, cplx& off) {
-  const int m = L.m, i = y * m + x;
-  d = coefc(L, SC, i, l);
-  cplx sk{0, 0}, sm{0, 0};
-  auto add = [&](int dir, int at, cplx vv) {
-    const double k = __ldg(L.K + (size_t)dir * L.n + at), mm = __ldg(L.M + (size_t)dir * L.n + at);
-    sk.re = fma(k, vv.re, sk.re);
-    sk.im = fma(k, vv.im, sk.im);
-    sm.re = fma(mm, vv.re, sm.re);
-    sm.im = fma(mm, vv.im, sm.im);
-  };
-  if (x + 1 < m) add(SE_, i, v[i + 1]);
-  if (x > 0) add(SE_, i - 1, v[i - 1]);
-  if (y + 1 < m) add(SN_, i, v[i + m]);
-  if (y > 0) add(SN_, i - m, v[i - m]);
-  if (x + 1 < m && y + 1 < m) add(SNE, i, v[i + m + 1]);
-  if (x > 0 && y > 0) add(SNE, i - m - 1, v[i - m - 1]);
+__device__ __forceinline__ cplx diag_of(double2 c, cplx l) { return {fma(l.re, c.y, c.x), l.im * c.y}; }
+
+// diagonal and off-diagonal part of (lambda M + K) v at padded node P; v in
+// shared memory (zero border).  Off-diagonal in split form sum K_d v_d + l sum M_d v_d.
+__device__ __forceinline__ void stencil(const Lvl& L, int P, cplx l, const cplx* v, cplx& d, cplx& off) {
+  const double2* C = L.C;
+  const int w = L.w, np = L.np;
+  const double2 cc = __ldg(C + P);
+  const double2 kE = __ldg(C + np + P), kW = __ldg(C + np + P - 1);
+  const double2 kN = __ldg(C + 2 * np + P), kS = __ldg(C + 2 * np + P - w);
+  const double2 kNE = __ldg(C + 3 * np + P), kSW = __ldg(C + 3 * np + P - w - 1);
+  const cplx vE = v[P + 1], vW = v[P - 1], vN = v[P + w], vS = v[P - w], vNE = v[P + w + 1], vSW = v[P - w - 1];
+  cplx sk, sm;
+  sk.re = kE.x * vE.re + kW.x * vW.re + kN.x * vN.re + kS.x * vS.re + kNE.x * vNE.re + kSW.x * vSW.re;
+  sk.im = kE.x * vE.im + kW.x * vW.im + kN.x * vN.im + kS.x * vS.im + kNE.x * vNE.im + kSW.x * vSW.im;
+  sm.re = kE.y * vE.re + kW.y * vW.re + kN.y * vN.re + kS.y * vS.re + kNE.y * vNE.re + kSW.y * vSW.re;
+  sm.im = kE.y * vE.im + kW.y * vW.im + kN.y * vN.im + kS.y * vS.im + kNE.y * vNE.im + kSW.y * vSW.im;
+  d = diag_of(cc, l);
   off = sk + cmul(l, sm);
 }
 
-// z_out = z_in + w (b - A z_in) / d  (z_in == nullptr: z_out = w b / d)
+// z_out = z_in + w (b - A z_in) / d  (z_in == nullptr: z_out = w b / d);
+// b from global (unpadded, b_g) on the top level, else from shared (padded)
 __device__ __forceinline__ void jacobi(const Lvl& L, cplx l, const cplx* b_g, const cplx* b_s, const cplx* zin,
                                        cplx* zout, double w) {
-  for (int i = threadIdx.x; i < L.n; i += SNT) {
-    const int y = i / L.m, x = i - y * L.m;
-    const cplx bi = b_g ? b_g[i] : b_s[i];
+  FOR_NODES(L, {
+    const cplx bi = b_g ? b_g[y * L.m + x] : b_s[P];
     if (!zin) {
-      const cplx d = coefc(L, SC, i, l);
-      zout[i] = w * cmul(bi, crcp(d));
+      const cplx d = diag_of(__ldg(L.C + P), l);
+      zout[P] = w * cmul(bi, crcp(d));
     } else {
       cplx d, off;
-      stencil(L, x, y, l, zin, d, off);
-      const cplx r = bi - off - cmul(d, zin[i]);
-      zout[i] = zin[i] + w * cmul(r, crcp(d));
+      stencil(L, P, l, zin, d, off);
+      const cplx r = bi - off - cmul(d, zin[P]);
+      zout[P] = zin[P] + w * cmul(r, crcp(d));
     }
-  }
+  })
 }
 
 __device__ __forceinline__ void residual(const Lvl& L, cplx l, const cplx* b_g, const cplx* b_s, const cplx* z,
                                          cplx* res) {
-  for (int i = threadIdx.x; i < L.n; i += SNT) {
-    const int y = i / L.m, x = i - y * L.m;
+  FOR_NODES(L, {
     cplx d, off;
-    stencil(L, x, y, l, z, d, off);
-    res[i] = (b_g ? b_g[i] : b_s[i]) - off - cmul(d, z[i]);
-  }
+    stencil(L, P, l, z, d, off);
+    res[P] = (b_g ? b_g[y * L.m + x] : b_s[P]) - off - cmul(d, z[P]);
+  })
 }
 
 // b_c = P^T res (interior fine centre (2X+1, 2Y+1) and its six neighbours)
-__device__ __forceinline__ void restrict_to(int m, int mc, const cplx* res, cplx* bc) {
-  for (int I = threadIdx.x; I < mc * mc; I += SNT) {
-    const int Y = I / mc, X = I - Y * mc;
-    const int f = (2 * Y + 1) * m + 2 * X + 1;
-    const cplx side = res[f - 1] + res[f + 1] + res[f - m] + res[f + m] + res[f - m - 1] + res[f + m + 1];
-    bc[I] = res[f] + 0.5 * side;
-  }
+__device__ __forceinline__ void restrict_to(const Lvl& F, const Lvl& Cc, const cplx* res, cplx* bc) {
+  const int w = F.w;
+  FOR_NODES(Cc, {
+    const int f = (2 * y + 2) * w + 2 * x + 2;
+    const cplx side = res[f - 1] + res[f + 1] + res[f - w] + res[f + w] + res[f - w - 1] + res[f + w + 1];
+    bc[P] = res[f] + 0.5 * side;
+  })
 }
 
-// z += P x_c (P1 interpolation on the nested triangulation)
-__device__ __forceinline__ void prolong_add(int m, int mc, const cplx* xc, cplx* z) {
-  for (int i = threadIdx.x; i < m * m; i += SNT) {
-    const int y = i / m, x = i - y * m;
+// z += P x_c (P1 interpolation on the nested triangulation); coarse vertex
+// (A, B), A, B in [0, mc+1], sits at padded index B (mc+2) + A (zero border)
+__device__ __forceinline__ void prolong_add(const Lvl& F, const Lvl& Cc, const cplx* xc, cplx* z) {
+  const int wc = Cc.w;
+  FOR_NODES(F, {
     const int a = x + 1, b = y + 1, ah = a >> 1, bh = b >> 1;
-    auto at = [&](int A, int B) -> cplx {
-      return (A >= 1 && A <= mc && B >= 1 && B <= mc) ? xc[(B - 1) * mc + (A - 1)] : cplx{0, 0};
-    };
+    const int c0 = bh * wc + ah;
     cplx v;
-    if (!(a & 1) && !(b & 1)) v = at(ah, bh);
-    else if (a & 1 && !(b & 1)) v = 0.5 * (at(ah, bh) + at(ah + 1, bh));
-    else if (!(a & 1)) v = 0.5 * (at(ah, bh) + at(ah, bh + 1));
-    else v = 0.5 * (at(ah, bh) + at(ah + 1, bh + 1));
-    z[i] = z[i] + v;
-  }
+    if (!(a & 1) && !(b & 1)) v = xc[c0];
+    else if (a & 1 && !(b & 1)) v = 0.5 * (xc[c0] + xc[c0 + 1]);
+    else if (!(a & 1)) v = 0.5 * (xc[c0] + xc[c0 + wc]);
+    else v = 0.5 * (xc[c0] + xc[c0 + wc + 1]);
+    z[P] = z[P] + v;
+  })
 }
+
+__device__ __forceinline__ int pitch_shift(int m) { return m <= 1 ? 0 : 32 - __clz(m - 1); }
 
 __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cplx* __restrict__ lam,
                                                         const cplx* __restrict__ inv, const cplx* __restrict__ b0,
                                                         cplx* __restrict__ z0, const int* __restrict__ active,
-                                                        double om1, double om2) {
+                                                        double om1, double om2, int smem_c16) {
   TP_PDL_ENTRY();
   const int bt = blockIdx.x;
   if (active && !active[bt]) return;
   extern __shared__ __align__(16) unsigned char small_smem[];
   cplx* sm = reinterpret_cast<cplx*>(small_smem);
+  // zero borders: clear the whole work area once
+  for (int k = threadIdx.x; k < smem_c16; k += SNT) sm[k] = cplx{0, 0};
   const int nl = sl.levels;  // levels handled, the last is the coarsest
-  // shared layout: level 0: zA, zB; levels 1..nl-2: b, zA, zB; coarsest: b, x
-  // sl.m[j] for a runtime j without a dynamically indexed parameter array
-  auto mof = [&](int j) -> int {
+  // shared layout (padded): level 0: zA, zB; levels 1..nl-2: b, zA, zB; coarsest: b, x
+  auto mof = [&](int j) -> int {  // sl.m[j] for a runtime j (no dynamically indexed parameter array)
     int v = 0;
 #pragma unroll
     for (int k = 0; k < kMaxSmall; ++k)
       if (k == j) v = sl.m[k];
     return v;
   };
-  auto lvl = [&](int j) -> Lvl { return {sl.K[j], sl.M[j], sl.m[j], sl.m[j] * sl.m[j]}; };
+  auto npad = [&](int j) -> int { return (mof(j) + 2) * (mof(j) + 2); };
+  auto lvl = [&](int j) -> Lvl {
+    const int m = sl.m[j];
+    return {sl.KM[j], m, m + 2, (m + 2) * (m + 2), pitch_shift(m)};
+  };
   auto base = [&](int j) -> cplx* {
     cplx* q = sm;
 #pragma unroll
     for (int k = 0; k < kMaxSmall; ++k)
-      if (k < j) q += (size_t)sl.m[k] * sl.m[k] * ((k == 0 || k == nl - 1) ? 2 : 3);
+      if (k < j) q += (size_t)(sl.m[k] + 2) * (sl.m[k] + 2) * ((k == 0 || k == nl - 1) ? 2 : 3);
     return q;
   };
   auto bs = [&](int j) -> cplx* { return j == 0 ? nullptr : base(j); };
-  auto za = [&](int j) -> cplx* { return base(j) + (j == 0 ? 0 : mof(j) * mof(j)); };
-  auto zb = [&](int j) -> cplx* { return za(j) + mof(j) * mof(j); };
+  auto za = [&](int j) -> cplx* { return base(j) + (j == 0 ? 0 : npad(j)); };
+  auto zb = [&](int j) -> cplx* { return za(j) + npad(j); };
   const cplx l = lam[bt];
   const int n0 = sl.m[0] * sl.m[0];
   const cplx* bg = b0 + (size_t)bt * n0;
+  __syncthreads();
   // down (loops unrolled over the level bound: static indices into sl)
 #pragma unroll
   for (int j = 0; j < kMaxSmall - 1; ++j) {
@@ -171,7 +198,7 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
     __syncthreads();
     residual(L, l, b_g, b, c, a);
     __syncthreads();
-    restrict_to(L.m, sl.m[j + 1], a, bs(j + 1));
+    restrict_to(L, lvl(j + 1), a, bs(j + 1));
     __syncthreads();
   }
   // coarsest: x = inv b (inv transposed: A[j * nc + i] = inv(i, j)), spread
@@ -181,24 +208,32 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
   // thread per row walking all nc columns left the other warps at the barrier
   // for a quarter of the kernel (ncu stall sampling).
   {
-    const int nc = mof(nl - 1) * mof(nl - 1);
+    const int mc = mof(nl - 1), nc = mc * mc, wc = mc + 2;
     const cplx* A = inv + (size_t)bt * nc * nc;
     const cplx* bc = bs(nl - 1);
     cplx* x = za(nl - 1);
     cplx* scratch = za(0);
-    const int G = max(1, min(SNT / nc, n0 / nc));
+    const int G = max(1, min(SNT / nc, npad(0) / nc));
     const int t = threadIdx.x, g = t / nc, i = t - g * nc;
     if (g < G) {
       cplx acc{0, 0};
-      for (int k = g; k < nc; k += G) acc = acc + cmul(A[(size_t)k * nc + i], bc[k]);
+      for (int k = g; k < nc; k += G) {
+        const int ky = k / mc, kx = k - ky * mc;
+        acc = acc + cmul(A[(size_t)k * nc + i], bc[(ky + 1) * wc + kx + 1]);
+      }
       scratch[g * nc + i] = acc;
     }
     __syncthreads();
     for (int r = t; r < nc; r += SNT) {
       cplx acc = scratch[r];
       for (int q = 1; q < G; ++q) acc = acc + scratch[q * nc + r];
-      x[r] = acc;
+      const int ry = r / mc, rx = r - ry * mc;
+      x[(ry + 1) * wc + rx + 1] = acc;
     }
+    __syncthreads();
+    // level 0's first work vector is zero-bordered again before its next use
+    // as a padded vector (the up pass writes its interior only)
+    for (int k = t; k < G * nc; k += SNT) scratch[k] = cplx{0, 0};
     __syncthreads();
   }
   // up
@@ -209,7 +244,7 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
     const cplx* b_g = j == 0 ? bg : nullptr;
     cplx *b = bs(j), *a = za(j), *c = zb(j);
     const cplx* xc = (j == nl - 2) ? za(nl - 1) : zb(j + 1);
-    prolong_add(L.m, sl.m[j + 1], xc, c);  // zc = z2 + P x_c
+    prolong_add(L, lvl(j + 1), xc, c);  // zc = z2 + P x_c
     __syncthreads();
     jacobi(L, l, b_g, b, c, a, om2);  // z3
     __syncthreads();
@@ -218,7 +253,26 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
   }
   cplx* zo = z0 + (size_t)bt * n0;
   const cplx* z4 = zb(0);
-  for (int i = threadIdx.x; i < n0; i += SNT) zo[i] = z4[i];
+  const Lvl L0 = lvl(0);
+  FOR_NODES(L0, { zo[y * L0.m + x] = z4[P]; })
+}
+
+// packed, zero-padded {K, M} planes C, E, N, NE of one level
+__global__ void k_pack_small(const double* __restrict__ K, const double* __restrict__ M, int m,
+                             double2* __restrict__ out) {
+  const int w = m + 2, np = w * w, n = m * m;
+  const int dirs[4] = {SC, SE_, SN_, SNE};
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < 4 * np; k += gridDim.x * blockDim.x) {
+    const int q = k / np, P = k - q * np;
+    const int py = P / w, px = P - py * w;
+    const int x = px - 1, y = py - 1;
+    double2 v{0.0, 0.0};
+    if (x >= 0 && x < m && y >= 0 && y < m) {
+      const size_t i = (size_t)dirs[q] * n + (size_t)y * m + x;
+      v = {K[i], M[i]};
+    }
+    out[k] = v;
+  }
 }
 
 }  // namespace
@@ -226,10 +280,27 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
 size_t small_cycle_smem(const int* m, int levels) {
   size_t c = 0;
   for (int j = 0; j < levels; ++j) {
-    const size_t n = (size_t)m[j] * m[j];
+    const size_t n = (size_t)(m[j] + 2) * (m[j] + 2);
     c += (j == 0 || j == levels - 1) ? 2 * n : 3 * n;
   }
   return c * sizeof(cplx);
+}
+
+size_t small_pack_size(const int* m, int levels) {
+  size_t c = 0;
+  for (int j = 0; j < levels; ++j) c += (size_t)8 * (m[j] + 2) * (m[j] + 2);
+  return c;
+}
+
+void pack_small_levels(Problem& p, SmallLevels& sl, double* buf) {
+  for (int j = 0; j < sl.levels; ++j) {
+    const int m = sl.m[j], np = (m + 2) * (m + 2);
+    double2* out = reinterpret_cast<double2*>(buf);
+    k_pack_small<<<(4 * np + 255) / 256, 256, 0, p.cur_stream()>>>(sl.K[j], sl.M[j], m, out);
+    TP_LAUNCHED(&p);
+    sl.KM[j] = out;
+    buf += (size_t)8 * np;
+  }
 }
 
 void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, const cplx* inv, const cplx* b,
@@ -240,7 +311,9 @@ void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, cons
            cudaSuccess;
   }();
   require(attr && sm <= 227 * 1024, "small-level cycle: shared memory");
-  launch_pdl(k_small_cycle, dim3(nb), dim3(SNT), sm, p.cur_stream(), sl, lam, inv, b, z, active, om1, om2);
+  require(sl.KM[0] != nullptr, "small-level cycle: stencils not packed");
+  launch_pdl(k_small_cycle, dim3(nb), dim3(SNT), sm, p.cur_stream(), sl, lam, inv, b, z, active, om1, om2,
+             (int)(sm / sizeof(cplx)));
   TP_LAUNCHED(&p);
 }
 
