@@ -274,12 +274,17 @@ def run_b200(args):
     # (read z2, r, 1/4 coarse correction; write z) x 16 B per fine node per
     # active frequency, divided by its CUDA-event duration measured over the
     # timed region.
-    traffic = None
+    # ncu DRAM bytes of the dominant kernel per active frequency
+    # (profiles/kernel_traffic.json: one cfg-1 sweep's launch list, total DRAM
+    # bytes of its k_stream_up<Five> launches / the sweep's frequency-
+    # iterations), scaled to this run's launches
+    dram_per_freq = None
     try:
         with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
-            traffic = json.load(f).get("dominant_kernel_dram_bytes_per_launch")
+            dram_per_freq = json.load(f).get("dominant_kernel_dram_bytes_per_frequency")
     except Exception:
         pass
+    alg_per_freq = 3.25 * 16.0 * (desc.cells - 1) ** 2
     def kstats(nl, ms, by):
         avg_ms = ms / max(nl, 1)
         b_launch = by / max(nl, 1)
@@ -289,7 +294,7 @@ def run_b200(args):
 
     timed = kstats(k_launches, k_ms, k_bytes)
     roofline = {"bound": "hbm", "kernel": "k_stream_up<Five> (fine-level V-cycle up pass)", "peak": hbm,
-                "unit": "GB/s", "traffic": traffic, "peak_source": src}
+                "unit": "GB/s", "traffic": None, "peak_source": src}
     if iso is not None and iso[0]:
         roofline.update(kstats(*iso))
         roofline["measured"] = ("live in bench.py: CUDA events around every launch on its stream, over "
@@ -299,6 +304,10 @@ def run_b200(args):
                                            "includes the other groups' kernels")
     else:
         roofline.update(timed)
+    if dram_per_freq and roofline.get("bytes_per_launch"):
+        roofline["traffic"] = dram_per_freq * roofline["bytes_per_launch"] / alg_per_freq
+        roofline["traffic_note"] = ("ncu dram__bytes_read+write per launch, from the per-frequency figure in "
+                                    "profiles/kernel_traffic.json scaled to this launch's active frequencies")
     # Whole-sweep algorithmic bytes per GPU:
     # B = 72 D / P + 16 n S sum_k it_k over this rank's frequency blocks
     # (sum_k it_k counted exactly by the solver, tp_sweep_stats), with S = 15.0

@@ -27,4 +27,4 @@ for _ in range(a.sweeps):
     r, it = p.m1_sweep()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()
-print("residual", r, "inner", it)
+print("residual", r, "inner", it, "frequency_iterations", p.sweep_stats()[1])
