@@ -876,10 +876,17 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
                           T* __restrict__ beta, double* __restrict__ bn2, double* __restrict__ rn2,
                           int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask,
                           T* __restrict__ xa, int* __restrict__ count = nullptr,
-                          const double* __restrict__ bfloor = nullptr, double fscale = 0.0) {
+                          const double* __restrict__ bfloor = nullptr, double fscale = 0.0,
+                          int* __restrict__ count_clear = nullptr) {
   TP_PDL_ENTRY();
   const int b = blockIdx.x;
   if (b >= nb) return;
+  // fused-scalar path (no ST_ALPHA stage): ST_RN clears the other counter slot
+  // for the next iteration and retires the deferred x coefficient of batches
+  // that converged an iteration ago (their last update was applied by this
+  // iteration's apply)
+  if (count_clear && b == 0 && threadIdx.x == 0) *count_clear = 0;
+  if (count_clear && xa && threadIdx.x == 0 && stage == ST_RN && !active[b]) xa[b] = from2<T>(0.0, 0.0);
   // active-batch counter of this iteration: cleared by ST_ALPHA, summed by ST_RN
   // (integer atomics: the count is exact whatever the block order)
   if (count && stage == ST_ALPHA && b == 0 && threadIdx.x == 0) *count = 0;
@@ -933,7 +940,8 @@ __global__ void k_count_active(const int* __restrict__ active, int nb, int* __re
   if (threadIdx.x == 0) {
     int s = 0;
     for (int w = 0; w < (int)(blockDim.x / 32); ++w) s += sh[w];
-    *count = s;
+    count[0] = s;
+    count[1] = 0;  // the first iteration's counter slot
   }
 }
 
@@ -1252,6 +1260,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   T* zo = lz1[l].get();
   if constexpr (MODE == 0) {
     if (l == small_from) {
+      trace_mark("small", p->cur_stream());
       launch_small_cycle(*p, small, lam, coarse_inv, bl, zo, act, cfg.omega, cfg.omega2, nb);
       return zo;
     }
@@ -1281,10 +1290,15 @@ FineOp BatchSolver<MODE>::stream_op(int l) const {
 }
 
 template <int MODE>
-void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out) {
+void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out, const ScalFuse* sf,
+                                   double* part_out) {
   const FineOp fo = stream_op(0);
-  launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb, qv,
-                     qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
+  if constexpr (MODE == 0)
+    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
+                       qv, qv ? alpha.get() : nullptr, r_out, qv ? (part_out ? part_out : part.get()) : nullptr, sf);
+  else
+    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
+                       qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
 }
 
 template <int MODE>
@@ -1312,6 +1326,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
         TP_CUDA(cudaEventCreate(&e1));
         TP_CUDA(cudaEventRecord(e0, s));
       }
+      trace_mark("up", s);
       launch_stream_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
       if (p->ktimer.on) {
         TP_CUDA(cudaEventRecord(e1, s));
@@ -1375,6 +1390,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
       so.lam = lam;
       so.m = ops[l].m;
       so.n = ops[l].n;
+      trace_mark("g-down", s);
       launch_stream_down(*p, so, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, cfg.omega2, nb);
       T* xs;
       if (l + 1 == L - 1) {
@@ -1384,6 +1400,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
       } else {
         xs = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
       }
+      trace_mark("g-up", s);
       launch_stream_up(*p, so, bl, z2, xs, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0,
                        part.get());
       return zo;
@@ -1453,6 +1470,17 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   int* act = active.get();
   int* zero = active.get() + B;
   T* const xa_ptr = fused ? xa.get() : nullptr;
+  // fused scalars (frequency mode, fused fine path): the apply reduces rho and
+  // beta from the up pass's partials, the down pass mu and alpha from the
+  // apply's -- two scalar kernels per iteration fewer on the critical path
+  // (TPGPU_SCALAR_KERNELS=1 keeps them)
+  static const bool want_fscal = std::getenv("TPGPU_SCALAR_KERNELS") == nullptr;
+  const bool fscal = MODE == 0 && fused && want_fscal;
+  if (fscal) {
+    rho2.ensure((size_t)2 * B);
+    partA.ensure((size_t)B * per_a * 2);
+    partD.ensure((size_t)B * per_d * 2);
+  }
   cudaStream_t s = p->cur_stream();
   const int l = 0;
   if (warm && sapply) {
@@ -1461,7 +1489,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
     DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
     TP_LAUNCHED(p);
   }
-  launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, nullptr, bfloor, bfloor_scale);
+  launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, nullptr, bfloor, bfloor_scale, static_cast<int*>(nullptr));
   TP_LAUNCHED(p);
   if (warm) {
     k_zero_flagged<MODE><<<g0.grid, blk, 0, s>>>(op0, x, nb, g0.BB, zero);
@@ -1483,12 +1511,25 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   T* pout = p1.get();
   if (last_active > 0) {
     T* z = vcycle_level(0, nb, rcur, nullptr, false, true);
-    launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0);
+    if (!fscal)
+    launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0, static_cast<int*>(nullptr));
     TP_LAUNCHED(p);
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
-      if (sapply) {
+      trace_mark("apply", s);
+      const int par = it & 1;
+      if (fscal) {
+        if constexpr (MODE == 0) {
+          ScalFuse sf;
+          sf.part = part.get();  // the up pass's r^T z partials
+          sf.per = per_u;
+          sf.rho_r = rho2.get() + (size_t)(par ^ 1) * B;
+          sf.rho_w = rho2.get() + (size_t)par * B;
+          launch_fine_apply(*p, stream_op(0), z, pin, pout, q.get(), beta.get(), act, first, nb, partA.get(), false, x,
+                            xa_ptr, &sf);
+        }
+      } else if (sapply) {
         launch_fine_apply(*p, stream_op(0), z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false,
                           fused ? x : nullptr, xa_ptr);
       } else {
@@ -1497,16 +1538,32 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         TP_LAUNCHED(p);
       }
       const int slot = it & 1;
-      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0);
+      trace_mark("scalars", s);
+      if (!fscal)
+      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0, static_cast<int*>(nullptr));
       TP_LAUNCHED(p);
-      if (fused) {
+      if (fscal) {
+        trace_mark("down", s);
+        if constexpr (MODE == 0) {
+          ScalFuse sf;
+          sf.part = partA.get();  // the apply's p^T q partials
+          sf.per = per_a;
+          sf.rho_r = rho2.get() + (size_t)par * B;
+          sf.alpha = alpha.get();
+          sf.xa = xa.get();
+          sf.mu = mu.get();
+          fine_down0(nb, rcur, q.get(), rnext, &sf, partD.get());
+        }
+      } else if (fused) {
+        trace_mark("down", s);
         fine_down0(nb, rcur, q.get(), rnext);
       } else {
         k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr,
                                                nb, g0.BB, part.get());
         TP_LAUNCHED(p);
       }
-      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RN, part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0);
+      trace_mark("scalars", s);
+      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RN, fscal ? partD.get() : part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0, fscal ? count.get() + (slot ^ 1) : static_cast<int*>(nullptr));
       TP_LAUNCHED(p);
       TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
       TP_CUDA(cudaEventRecord(ev[slot], s));
@@ -1537,7 +1594,9 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       } else {
         z = vcycle_level(0, nb, rcur, nullptr, false, true);
       }
-      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0);
+      trace_mark("scalars", s);
+      if (!fscal)
+      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0, static_cast<int*>(nullptr));
       TP_LAUNCHED(p);
       std::swap(pin, pout);
     }

@@ -44,6 +44,21 @@ struct FineOp {
   int m = 0, c = 0, n = 0;
 };
 
+// Krylov scalars reduced inside the fine passes (frequency mode, fused path):
+// the consumer of a pass's per-warp partial sums sums them itself (every warp
+// of a batch, fixed order) instead of a separate scalar kernel.  apply:
+// rho_it = sum of the up pass's r^T z partials, beta = rho_it / rho_{it-1};
+// down: mu = sum of the apply's p^T q partials, alpha = rho_it / mu.
+struct ScalFuse {
+  const double* part = nullptr;  // producer's partials, per (re, im) pairs per batch; nullptr: off
+  int per = 0;
+  const cplx* rho_r = nullptr;   // apply: rho of the previous iteration; down: this iteration's
+  cplx* rho_w = nullptr;         // apply: this iteration's rho (written by one warp per batch)
+  cplx* alpha = nullptr;         // down: alpha, the deferred x coefficient, mu (one warp per batch)
+  cplx* xa = nullptr;
+  cplx* mu = nullptr;
+};
+
 // The bottom levels of the frequency-mode V-cycle, run as one kernel
 // (mg_small.cu): level 0 of this list is the first level whose work vectors
 // fit in shared memory, the last is the coarsest (dense solve).
@@ -92,6 +107,8 @@ struct BatchSolver {
   DevBuf<T> xa;  // deferred solution-update coefficient per batch (fused Krylov update)
   DevBuf<double> part;
   DevBuf<T> rho, mu, alpha, beta;
+  DevBuf<T> rho2;               // fused scalars: rho of the two most recent iterations (2B)
+  DevBuf<double> partA, partD;  // fused scalars: apply / down partials (kept apart from the up pass's)
   DevBuf<double> bn2, rn2;
   DevBuf<int> active;
   DevBuf<int> count;
@@ -117,7 +134,8 @@ struct BatchSolver {
   FineOp stream_op(int l) const;   // the streaming kernels' view of level l
   // fine streaming level: down pass (optionally fusing r_out = r_in - alpha q),
   // and the rest of the cycle (coarse levels + up pass)
-  void fine_down0(int nb, const T* r_in, const T* qv = nullptr, T* r_out = nullptr);
+  void fine_down0(int nb, const T* r_in, const T* qv = nullptr, T* r_out = nullptr, const ScalFuse* sf = nullptr,
+                  double* part_out = nullptr);
   T* fine_rest0(int nb, const T* bl, bool dot);
 };
 
@@ -132,13 +150,14 @@ int fine_partials(int m, int kind);
 // (xa != nullptr: also x += xa p_in, the deferred update of the fused Krylov step)
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init,
-                       cplx* x = nullptr, const cplx* xa = nullptr);
+                       cplx* x = nullptr, const cplx* xa = nullptr, const ScalFuse* sf = nullptr);
 // V-cycle down / up passes of one level (fine: op.we set; Galerkin: op.K set)
 // (q != nullptr: fine level with the fused Krylov update r_out = r - alpha q,
 // partial ||r_out||^2 per warp item into part)
 void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
                         const int* active, double om1, double om2, int nb, const cplx* q = nullptr,
-                        const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr);
+                        const cplx* alpha = nullptr, cplx* rout = nullptr, double* part = nullptr,
+                        const ScalFuse* sf = nullptr);
 void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z2, const cplx* xc, int mc,
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part);
 // slice mode: real vectors, per-slice Jacobian stencils

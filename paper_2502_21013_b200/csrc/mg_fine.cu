@@ -20,6 +20,7 @@
 //   k_fine_up      zc = z2 + P x_c ; z3, z4 = two Jacobi steps ;
 //                  writes z4, partial r^T z4                          (V-cycle up)
 #include <cstdlib>
+#include <type_traits>
 
 #include "mg.cuh"
 
@@ -88,6 +89,24 @@ __device__ __forceinline__ void warp_pair(double& a, double& b) {
     a += __shfl_down_sync(0xffffffffu, a, o);
     b += __shfl_down_sync(0xffffffffu, b, o);
   }
+}
+
+// sum of batch b's `per` partial pairs, every lane the same fixed-order result
+__device__ __forceinline__ cplx warp_batch_sum(const double* __restrict__ part, int per, int b) {
+  double a = 0, c = 0;
+  for (int k = threadIdx.x & 31; k < per; k += 32) {
+    a += part[((size_t)b * per + k) * 2];
+    c += part[((size_t)b * per + k) * 2 + 1];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  return {a, c};
+}
+__device__ __forceinline__ cplx cdivv(cplx a, cplx b) {
+  const double d = 1.0 / fma(b.re, b.re, b.im * b.im);
+  return {fma(a.re, b.re, a.im * b.im) * d, fma(a.im, b.re, -a.re * b.im) * d};
 }
 
 struct Item {
@@ -425,7 +444,8 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
                                                                          const typename S::T* __restrict__ qv = nullptr,
                                                                          const typename S::T* __restrict__ alpha = nullptr,
                                                                          typename S::T* __restrict__ rout = nullptr,
-                                                                         double* __restrict__ part = nullptr) {
+                                                                         double* __restrict__ part = nullptr,
+                                                                         ScalFuse sf = ScalFuse{}) {
   using T = typename S::T;
   static_assert(!FUSED || NB == 1, "fused residual update: one frequency per warp");
   constexpr int H = 3, OWN = 26;  // lanes 3..28 own fine columns; even strip start
@@ -441,7 +461,26 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
       reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRowT<T, NVV>)) + wib * RC;
   const T* const qp = FUSED ? qv + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
   T* const ro = FUSED ? rout + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
-  const T al = FUSED ? alpha[it.b[0]] : T{};
+  T al{};
+  if constexpr (FUSED) {
+    if constexpr (std::is_same_v<T, cplx>) {
+      if (sf.part) {
+        // alpha = rho / (p^T q), reduced here from the apply's partials
+        const int b0 = it.b[0];
+        const cplx mu = warp_batch_sum(sf.part, sf.per, b0);
+        al = cdivv(sf.rho_r[b0], mu);
+        if (it.chunk == 0 && it.strip == 0 && (threadIdx.x & 31) == 0) {
+          sf.alpha[b0] = al;
+          sf.xa[b0] = al;
+          sf.mu[b0] = mu;
+        }
+      } else {
+        al = alpha[it.b[0]];
+      }
+    } else {
+      al = alpha[it.b[0]];
+    }
+  }
   double rn2 = 0;
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
@@ -760,7 +799,8 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
                                                             const int* __restrict__ active, int first, int nb,
                                                             double* __restrict__ part,
                                                             typename S::T* __restrict__ xs = nullptr,
-                                                            const typename S::T* __restrict__ xa = nullptr) {
+                                                            const typename S::T* __restrict__ xa = nullptr,
+                                                            ScalFuse sf = ScalFuse{}) {
   using T = typename S::T;
   constexpr int H = 1, OWN = WL - 2 * H;  // 30
   constexpr int RV = RA + 2, RC = RA + 2 + S::RETAIN, NVV = XUPD ? 3 : 2;
@@ -790,7 +830,21 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
   T* const xo = XUPD ? xs + o + xc : nullptr;
   const cplx l = op.lam ? op.lam[b] : cplx{0, 0};
   const bool usep = INIT || !first;  // p_in is read
-  const T bt = (INIT || first) ? T{} : beta[b];
+  T bt{};
+  if constexpr (!INIT && std::is_same_v<T, cplx>) {
+    if (sf.part) {
+      // rho = r^T z (the up pass's partials), beta = rho / rho_prev
+      if (on) {
+        const cplx rn = warp_batch_sum(sf.part, sf.per, b);
+        if (!first) bt = cdivv(rn, sf.rho_r[b]);
+        if (it.chunk == 0 && it.strip == 0 && lane == 0) sf.rho_w[b] = rn;
+      }
+    } else if (!first) {
+      bt = beta[b];
+    }
+  } else if (!INIT && !first) {
+    bt = beta[b];
+  }
   const int ys = it.ys, ye = it.ye;
   const int y0 = ys - 2, ylast = ye;  // staged rows
   const typename S::Src src = S::src(op, x, xc, y0, b);
@@ -885,7 +939,7 @@ int env_int(const char* name, int dflt) {
 template <class S, int NB, int RA, int WPBK, bool FUSED = false, class T = typename S::T>
 void down_t(Problem& p, const FineOp& op, const T* r, T* z2, T* bc, int mc, const int* active, double om1,
             double om2, int nb, const T* q = nullptr, const T* alpha = nullptr, T* rout = nullptr,
-            double* part = nullptr) {
+            double* part = nullptr, const ScalFuse* sf = nullptr) {
   constexpr size_t sm = ring_smem<S, FUSED ? 2 : NB, RA, WPBK>();
   static bool attrs = [] {
     cudaFuncSetAttribute(k_stream_down<S, NB, RA, WPBK, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -895,7 +949,8 @@ void down_t(Problem& p, const FineOp& op, const T* r, T* z2, T* bc, int mc, cons
   (void)attrs;
   const int rh = rh_for(op.m);
   launch_pdl(k_stream_down<S, NB, RA, WPBK, FUSED>, grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK),
-             sm, p.cur_stream(), op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part);
+             sm, p.cur_stream(), op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part,
+             sf ? *sf : ScalFuse{});
 }
 
 template <class S, int NB, int RA, int WPBK, class T = typename S::T>
@@ -914,7 +969,8 @@ void up_t(Problem& p, const FineOp& op, const T* r, const T* z2, const T* xc, in
 
 template <class S, int RA, int W, class T = typename S::T>
 void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T* q, const T* beta, const int* active,
-             int first, int nb, double* part, bool init, T* x, const T* xa) {
+             int first, int nb, double* part, bool init, T* x, const T* xa, const ScalFuse* sf = nullptr) {
+  const ScalFuse sfv = sf ? *sf : ScalFuse{};
   constexpr size_t sm = ring_smem<S, 2, RA, W>();
   constexpr size_t sm3 = ring_smem<S, 3, RA, W>();
   static bool attrs = [] {
@@ -930,13 +986,13 @@ void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T*
   using C0 = const T*;
   if (init)
     launch_pdl(k_stream_apply<S, 1, RA, W>, g, dim3(WL * W), sm, s, op, z, pin, pout, q, beta, active, first, nb, part,
-               T0(nullptr), C0(nullptr));
+               T0(nullptr), C0(nullptr), ScalFuse{});
   else if (xa)
     launch_pdl(k_stream_apply<S, 0, RA, W, true>, g, dim3(WL * W), sm3, s, op, z, pin, pout, q, beta, active, first,
-               nb, part, x, xa);
+               nb, part, x, xa, sfv);
   else
     launch_pdl(k_stream_apply<S, 0, RA, W>, g, dim3(WL * W), sm, s, op, z, pin, pout, q, beta, active, first, nb, part,
-               T0(nullptr), C0(nullptr));
+               T0(nullptr), C0(nullptr), sfv);
   TP_LAUNCHED(&p);
 }
 
@@ -948,8 +1004,8 @@ int fine_partials(int m, int kind) {
 
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
                        const cplx* beta, const int* active, int first, int nb, double* part, bool init, cplx* x,
-                       const cplx* xa) {
-  apply_t<Five, 4, 4>(p, op, z, pin, pout, q, beta, active, first, nb, part, init, x, xa);
+                       const cplx* xa, const ScalFuse* sf) {
+  apply_t<Five, 4, 4>(p, op, z, pin, pout, q, beta, active, first, nb, part, init, x, xa, sf);
 }
 
 // slice mode: the fine-level Jacobian apply (p = z + beta p, q = J p, p^T q;
@@ -968,9 +1024,9 @@ void launch_fine_apply(Problem& p, const FineOp& op, const double* z, const doub
 // override the ring depths for experiments.
 void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, cplx* bc, int mc,
                         const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
-                        cplx* rout, double* part) {
+                        cplx* rout, double* part, const ScalFuse* sf) {
   if (op.we && q) {
-    down_t<Five, 1, 6, 4, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+    down_t<Five, 1, 6, 4, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part, sf);
   } else if (op.we) {
     static const int ra = env_int("TPGPU_RA5", 6);
     if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);

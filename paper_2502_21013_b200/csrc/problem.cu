@@ -10,6 +10,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <map>
 #include <cstdlib>
 #include <cstring>
 #include <limits>
@@ -21,6 +22,8 @@
 #include "mg.cuh"
 
 namespace tpgpu {
+
+thread_local StreamTrace* tl_trace = nullptr;
 
 bool pdl_enabled() {
   static const bool on = !std::getenv("TPGPU_PDL") || std::atoi(std::getenv("TPGPU_PDL")) != 0;
@@ -556,10 +559,33 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
       auto body = [&](int g) {
         const int kg = k0 + g * w.chunk, nbg = std::min(w.chunk, Kr - kg);
         if (nbg <= 0) return;
+        static const bool tracing = std::getenv("TPGPU_TRACE") != nullptr;
+        StreamTrace trace;
         try {
           if (g > 0) TP_CUDA(cudaSetDevice(device));
           tl_stream = w.hs[g];
+          if (tracing) {
+            tl_trace = &trace;
+            trace_mark("start", w.hs[g]);
+          }
           git[g] = run(w.group(g), kg, nbg, &gst[g]);
+          if (tracing) {
+            trace_mark("end", w.hs[g]);
+            tl_trace = nullptr;
+            TP_CUDA(cudaStreamSynchronize(w.hs[g]));
+            std::map<std::string, std::pair<int, double>> acc;
+            for (size_t i = 0; i + 1 < trace.ev.size(); ++i) {
+              float ms = 0;
+              TP_CUDA(cudaEventElapsedTime(&ms, trace.ev[i].second, trace.ev[i + 1].second));
+              auto& a = acc[trace.ev[i].first];
+              a.first += 1;
+              a.second += ms;
+            }
+            std::string line = "trace g" + std::to_string(g) + ":";
+            for (auto& [k, v] : acc) line += " " + k + " " + std::to_string(v.first) + "x " + std::to_string(v.second * 1e3).substr(0, 6) + "us";
+            std::fprintf(stderr, "%s\n", line.c_str());
+            for (auto& e : trace.ev) cudaEventDestroy(e.second);
+          }
         } catch (...) {
           gerr[g] = std::current_exception();
         }

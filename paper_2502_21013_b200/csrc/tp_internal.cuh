@@ -56,6 +56,20 @@ void set_last_error(const std::string& msg, double residual);
     if (TPGPU_PDL_TRIGGER) asm volatile("griddepcontrol.launch_dependents;\n" ::: "memory"); \
   } while (0)
 bool pdl_enabled();
+
+// Experiment: stream-event trace of one host thread's launches (TPGPU_TRACE=1;
+// problem.cu prints the live time between consecutive marks per group)
+struct StreamTrace {
+  std::vector<std::pair<const char*, cudaEvent_t>> ev;
+};
+extern thread_local StreamTrace* tl_trace;
+inline void trace_mark(const char* name, cudaStream_t s) {
+  if (!tl_trace) return;
+  cudaEvent_t e;
+  TP_CUDA(cudaEventCreate(&e));
+  TP_CUDA(cudaEventRecord(e, s));
+  tl_trace->ev.emplace_back(name, e);
+}
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s, Args... args) {
   cudaLaunchAttribute at[1];
