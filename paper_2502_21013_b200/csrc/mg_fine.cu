@@ -31,6 +31,11 @@ namespace {
 constexpr int WL = 32;     // lanes per warp
 constexpr int WPB = 4;     // warps per block
 constexpr int RH = 64;     // rows per warp work item
+// rows per warp item of the apply pass
+#ifndef TPGPU_RH_APPLY
+#define TPGPU_RH_APPLY 32
+#endif
+constexpr int RHA = TPGPU_RH_APPLY;
 
 __device__ __forceinline__ cplx cm(cplx a, cplx b) {
   return {fma(a.re, b.re, -a.im * b.im), fma(a.re, b.im, a.im * b.re)};
@@ -807,7 +812,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
   TP_PDL_ENTRY();
-  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RH, nb, nullptr);
+  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RHA, nb, nullptr);
   const bool on = INIT || !active || active[it.b[0]];
   T xab{};
   if (XUPD) xab = xa[it.b[0]];
@@ -906,7 +911,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
   cp_wait<0>();
   warp_pair(s0, s1);
   if (lane == 0 && on) {
-    const int ns = (m + OWN - 1) / OWN, nch = (m + RH - 1) / RH;
+    const int ns = (m + OWN - 1) / OWN, nch = (m + RHA - 1) / RHA;
     const size_t per = (size_t)ns * nch;
     const size_t k = (size_t)b * per + (size_t)it.chunk * ns + it.strip;
     part[2 * k] = s0;
@@ -980,7 +985,7 @@ void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T*
     return true;
   }();
   (void)attrs;
-  const dim3 g = grid_for(op.m, 30, nb, RH, W);
+  const dim3 g = grid_for(op.m, 30, nb, RHA, W);
   cudaStream_t s = p.cur_stream();
   using T0 = T*;
   using C0 = const T*;
@@ -999,7 +1004,7 @@ void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T*
 }  // namespace
 
 int fine_partials(int m, int kind) {
-  return kind == 0 ? items_per_batch(m, 30) : items_per_batch(m, kind == 1 ? 26 : 28, rh_for(m));
+  return kind == 0 ? items_per_batch(m, 30, RHA) : items_per_batch(m, kind == 1 ? 26 : 28, rh_for(m));
 }
 
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,
