@@ -446,8 +446,9 @@ struct FftPlan {
   DevBuf<cplx> tw;
   // Stockham path (power-of-two N >= 16): columns pairs per block, threads, shared bytes
   bool stockham = false;
-  int sP = 0, sT = 0;
-  size_t ssmem = 0;
+  int sP = 0, sT = 0;    // forward: column pairs per block, threads
+  int siP = 0, siT = 0;  // inverse
+  size_t ssmem = 0, fsmem = 0;  // inverse (+ staged half spectrum) / forward
 };
 
 FftPlan& plan_for(Problem& p) {
@@ -483,9 +484,18 @@ FftPlan& plan_for(Problem& p) {
       pl->stockham = true;
       pl->sP = sP;
       pl->sT = std::max(32, T);
-      // + the inverse's staged half spectrum (N/2+1) x 2P
-      pl->ssmem = (size_t)((sP + 1) * N + (N / 2 + 1) * 2 * sP) * sizeof(cplx);
-      TP_CUDA(cudaFuncSetAttribute(k_sfft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
+      // inverse: the same column pairs per block + its staged half spectrum
+      // (N/2+1) x 2P (halving P measured no faster: 132.6 vs 132.6 us at cfg 1;
+      // TPGPU_IFFT_P overrides)
+      static const int ip_env = std::getenv("TPGPU_IFFT_P") ? std::atoi(std::getenv("TPGPU_IFFT_P")) : 0;
+      const int siP = ip_env > 0 ? ip_env : sP;
+      pl->siP = siP;
+      pl->siT = std::max(32, siP * N / 16);
+      pl->ssmem = (size_t)((siP + 1) * N + (N / 2 + 1) * 2 * siP) * sizeof(cplx);
+      // the forward transform needs only the twiddles and the P columns (half
+      // the inverse's footprint: twice the resident blocks)
+      pl->fsmem = (size_t)((sP + 1) * N) * sizeof(cplx);
+      TP_CUDA(cudaFuncSetAttribute(k_sfft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->fsmem));
       TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
     }
   }
@@ -507,7 +517,7 @@ void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat, double* sq) {
   const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
   const int blocks = rdft_forward_blocks(p);
   if (pl.stockham) {
-    k_sfft_forward<<<blocks, pl.sT, pl.ssmem, p.stream>>>(G, Ghat, n, pl.N, pl.sP, pl.tw.get(), sq);
+    k_sfft_forward<<<blocks, pl.sT, pl.fsmem, p.stream>>>(G, Ghat, n, pl.N, pl.sP, pl.tw.get(), sq);
   } else {
     k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
                                                        sq);
@@ -518,12 +528,12 @@ void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat, double* sq) {
 void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2) {
   FftPlan& pl = plan_for(p);
   const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
-  const int C = 2 * (pl.stockham ? pl.sP : pl.P);
+  const int C = 2 * (pl.stockham ? pl.siP : pl.P);
   const int blocks = (int)((n + C - 1) / C);
   p.part.ensure((size_t)2 * blocks);
   p.red.ensure(16);
   if (pl.stockham) {
-    k_sfft_inverse<<<blocks, pl.sT, pl.ssmem, p.stream>>>(Uhat, U, n, pl.N, pl.sP, pl.tw.get(), p.part.get());
+    k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, p.stream>>>(Uhat, U, n, pl.N, pl.siP, pl.tw.get(), p.part.get());
   } else {
     k_rdft_inverse<<<blocks, 256, pl.smem, p.stream>>>(Uhat, U, n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
                                                        p.part.get());
