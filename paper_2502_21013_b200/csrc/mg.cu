@@ -1483,14 +1483,21 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   }
   cudaStream_t s = p->cur_stream();
   const int l = 0;
+  // one k_scalars stage over `per` partials per batch (launch + count)
+  auto scalars = [&](int stage, const double* partials, int per, int* cnt, int* cnt_clear, const double* floor_ptr,
+                     double floor_scale) {
+    launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, stage, partials, per, nb, rtol2, rho.get(), mu.get(),
+               alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, cnt, floor_ptr,
+               floor_scale, cnt_clear);
+    TP_LAUNCHED(p);
+  };
   if (warm && sapply) {
     launch_fine_apply(*p, stream_op(0), b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
   } else {
     DISPATCH_FAM(l, (k_init<MODE, FAM><<<g0.grid, blk, 0, s>>>(op0, b, x, r.get(), nb, g0.BB, warm ? 1 : 0, part.get())));
     TP_LAUNCHED(p);
   }
-  launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, nullptr, bfloor, bfloor_scale, static_cast<int*>(nullptr));
-  TP_LAUNCHED(p);
+  scalars(ST_INIT, part.get(), (warm && sapply) ? per_a : per_t, nullptr, nullptr, bfloor, bfloor_scale);
   if (warm) {
     k_zero_flagged<MODE><<<g0.grid, blk, 0, s>>>(op0, x, nb, g0.BB, zero);
     TP_LAUNCHED(p);
@@ -1511,9 +1518,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   T* pout = p1.get();
   if (last_active > 0) {
     T* z = vcycle_level(0, nb, rcur, nullptr, false, true);
-    if (!fscal)
-    launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0, static_cast<int*>(nullptr));
-    TP_LAUNCHED(p);
+    if (!fscal) scalars(ST_RHO0, part.get(), ops.size() > 1 ? per_u : per_t, nullptr, nullptr, nullptr, 0.0);
     bool done = false;
     for (int it = 1; it <= cfg.max_iter; ++it) {
       const int first = it == 1 ? 1 : 0;
@@ -1539,9 +1544,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       }
       const int slot = it & 1;
       trace_mark("scalars", s);
-      if (!fscal)
-      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_ALPHA, part.get(), sapply ? per_a : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0, static_cast<int*>(nullptr));
-      TP_LAUNCHED(p);
+      if (!fscal) scalars(ST_ALPHA, part.get(), sapply ? per_a : per_t, count.get() + slot, nullptr, nullptr, 0.0);
       if (fscal) {
         trace_mark("down", s);
         if constexpr (MODE == 0) {
@@ -1563,8 +1566,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         TP_LAUNCHED(p);
       }
       trace_mark("scalars", s);
-      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_RN, fscal ? partD.get() : part.get(), fused ? per_d : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, count.get() + slot, static_cast<const double*>(nullptr), 0.0, fscal ? count.get() + (slot ^ 1) : static_cast<int*>(nullptr));
-      TP_LAUNCHED(p);
+      scalars(ST_RN, fscal ? partD.get() : part.get(), fused ? per_d : per_t, count.get() + slot,
+              fscal ? count.get() + (slot ^ 1) : nullptr, nullptr, 0.0);
       TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
       TP_CUDA(cudaEventRecord(ev[slot], s));
       if (dbg_freq) {  // experiment: per-frequency iteration counts (synchronizes every iteration)
@@ -1595,9 +1598,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         z = vcycle_level(0, nb, rcur, nullptr, false, true);
       }
       trace_mark("scalars", s);
-      if (!fscal)
-      launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nb, rtol2, rho.get(), mu.get(), alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, static_cast<int*>(nullptr), static_cast<const double*>(nullptr), 0.0, static_cast<int*>(nullptr));
-      TP_LAUNCHED(p);
+      if (!fscal) scalars(ST_BETA, part.get(), ops.size() > 1 ? per_u : per_t, nullptr, nullptr, nullptr, 0.0);
       std::swap(pin, pout);
     }
     if (!done) {
