@@ -497,7 +497,12 @@ double Problem::residual_and_rhs(bool want_rhs) {
         d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   }
   TP_LAUNCHED(this);
-  return std::sqrt(global_sum(reduce_sum(*this, part.get(), (int)np)));
+  const double r = std::sqrt(global_sum(reduce_sum(*this, part.get(), (int)np)));
+  if (want_rhs) {  // the fixed-point residual history (warm-start extrapolation, problem.cu)
+    resid_prev = resid_last;
+    resid_last = r;
+  }
+  return r;
 }
 
 // block residual of a device state u into r and its norm (block_l2)

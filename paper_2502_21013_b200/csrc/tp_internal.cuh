@@ -254,6 +254,10 @@ class Problem {
   DevBuf<double> halo_lo, halo_hi, halo_send;  // N*m each
   DevBuf<cplx> Ghat_f, Uhat_f, xstage;         // (k1-k0)*n frequency blocks, staging
   DevBuf<double> red_all;                      // P doubles (allgather)
+  DevBuf<cplx> uhat_prev;  // warm-start extrapolation: the spectrum of the sweep before
+  bool uhat_prev_valid = false;
+  double extrap_theta = 0.0;  // > 0: the next periodic_solve_with extrapolates its warm start
+  double resid_prev = -1.0, resid_last = -1.0;  // the last two M1 residual norms
   DevBuf<double> spec_sq;  // forward-DFT |X|^2 partials, then [last] the total (frequency stopping floor)
   void exchange_halo();
   double global_sum(double local);

@@ -27,13 +27,15 @@ for rtol in [float(x) for x in sys.argv[1:]] or [1e-13]:
         p.static_init(cfg, want_state=False)
         p.choose_nu_hat(cfg)
         p.m1_begin(cfg)
-        its = []
+        its, fits = [], []
         torch.cuda.synchronize()
         t = time.perf_counter()
         for _ in range(20):
             its.append(p.m1_sweep()[1])
+            fits.append(p.sweep_stats()[1])
         torch.cuda.synchronize()
         dt = (time.perf_counter() - t) / 20
     print(f"rtol {rtol:.0e} omega {os.environ.get('TPGPU_OMEGA','0.8')} rb {os.environ.get('TPGPU_RB_FINE','1')}: "
           f"cfg0 iters {rep.iterations} (ref {int(g['iterations'])}) err U1 {e1:.1e} U2 {e2:.1e} final {ef:.1e}"
-          f" | cfg1 inner {its[:6]}.. mean {np.mean(its):.1f}, {dt*1e3:.2f} ms/sweep", flush=True)
+          f" | cfg1 inner {its[:6]}.. mean {np.mean(its):.1f}, f-its {np.mean(fits):.0f}, {dt*1e3:.2f} ms/sweep",
+          flush=True)
