@@ -30,7 +30,7 @@ t0 = time.perf_counter()
 r0 = p.m1_begin(cfg)
 torch.cuda.synchronize()
 t_setup = time.perf_counter() - t0
-hist, its, times = [r0], [], []
+hist, its, times, fits = [r0], [], [], []
 while len(its) < a.max_sweeps and not hist[-1] <= a.tol * hist[0]:
     t = time.perf_counter()
     r, it = p.m1_sweep()
@@ -38,11 +38,13 @@ while len(its) < a.max_sweeps and not hist[-1] <= a.tol * hist[0]:
     times.append(time.perf_counter() - t)
     hist.append(r)
     its.append(it)
+    fits.append(p.sweep_stats()[1])
 free, total = torch.cuda.mem_get_info()
 D = p.n_dof * p.steps
 out = dict(config=a.config, cells=d.cells, steps=d.steps, n=p.n_dof, D=D, create_s=t_create, init_s=t_init,
            newton_max=int(counts.max()), nu_hat=list(nu), q=q, setup_s=t_setup, sweeps=len(its),
            converged=bool(hist[-1] <= a.tol * hist[0]), median_sweep_s=sorted(times)[len(times) // 2] if times else None,
-           dof_per_s=D / sorted(times)[len(times) // 2] if times else None, inner=its, history=hist,
+           dof_per_s=D / sorted(times)[len(times) // 2] if times else None, inner=its, frequency_iterations=fits,
+           history=hist,
            time_to_residual_s=t_init + t_setup + sum(times), gpu_mem_used_gb=(total - free) / 1e9)
 print(json.dumps(out))
