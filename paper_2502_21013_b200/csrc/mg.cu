@@ -930,6 +930,13 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
   }
 }
 
+// count -> mapped host memory (read by the host after an event on the stream)
+__global__ void k_publish(const int* __restrict__ count, volatile int* __restrict__ host) {
+  TP_PDL_ENTRY();
+  *host = *count;
+  __threadfence_system();
+}
+
 __global__ void k_count_active(const int* __restrict__ active, int nb, int* __restrict__ count) {
   __shared__ int sh[32];
   int c = 0;
@@ -1188,7 +1195,13 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   rn2.alloc(B);
   active.alloc(2 * B);
   count.alloc(2);
-  if (!h_count) TP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_count), 2 * sizeof(int)));
+  if (!h_count) {
+    // mapped pinned memory: the per-iteration active count is published by a
+    // one-thread kernel (k_publish) instead of a D2H copy, so the solver's
+    // kernel chain is not broken by a copy node every iteration
+    TP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_count), 2 * sizeof(int), cudaHostAllocMapped));
+    TP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_count_dev), h_count, 0));
+  }
   for (auto& e : ev)
     if (!e) TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
 }
@@ -1475,6 +1488,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   // apply's -- two scalar kernels per iteration fewer on the critical path
   // (TPGPU_SCALAR_KERNELS=1 keeps them)
   static const bool want_fscal = std::getenv("TPGPU_SCALAR_KERNELS") == nullptr;
+  static const bool use_publish = std::getenv("TPGPU_COUNT_MEMCPY") == nullptr;
   const bool fscal = MODE == 0 && fused && want_fscal;
   if (fscal) {
     rho2.ensure((size_t)2 * B);
@@ -1568,7 +1582,13 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       trace_mark("scalars", s);
       scalars(ST_RN, fscal ? partD.get() : part.get(), fused ? per_d : per_t, count.get() + slot,
               fscal ? count.get() + (slot ^ 1) : nullptr, nullptr, 0.0);
-      TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
+      if (use_publish) {
+        launch_pdl(k_publish, dim3(1), dim3(1), 0, s, static_cast<const int*>(count.get() + slot),
+                   static_cast<volatile int*>(h_count_dev + slot));
+        TP_LAUNCHED(p);
+      } else {
+        TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
+      }
       TP_CUDA(cudaEventRecord(ev[slot], s));
       if (dbg_freq) {  // experiment: per-frequency iteration counts (synchronizes every iteration)
         std::vector<int> ha(nb);

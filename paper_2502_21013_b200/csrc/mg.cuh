@@ -112,7 +112,8 @@ struct BatchSolver {
   DevBuf<double> bn2, rn2;
   DevBuf<int> active;
   DevBuf<int> count;
-  int* h_count = nullptr;  // pinned [2]
+  int* h_count = nullptr;      // mapped pinned [2]
+  int* h_count_dev = nullptr;  // its device address
   int cur_active = 0;      // active batches as last seen by the host (kernel-timer byte accounting)
   int small_from = -1;     // frequency mode: first level handled by the fused small-level cycle
   SmallLevels small;        // its levels (stencils packed into small_pack)
