@@ -1505,6 +1505,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
                floor_scale, cnt_clear);
     TP_LAUNCHED(p);
   };
+  trace_mark("pcg-init", s);
   if (warm && sapply) {
     launch_fine_apply(*p, stream_op(0), b, x, nullptr, r.get(), nullptr, nullptr, 1, nb, part.get(), true);
   } else {
@@ -1575,6 +1576,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         trace_mark("down", s);
         fine_down0(nb, rcur, q.get(), rnext);
       } else {
+        trace_mark("update", s);
         k_update<MODE><<<g0.grid, blk, 0, s>>>(op0, x, rcur, pout, q.get(), alpha.get(), act, cfg.omega, nullptr,
                                                nb, g0.BB, part.get());
         TP_LAUNCHED(p);
@@ -1615,6 +1617,7 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
         std::swap(rcur, rnext);
         z = fine_rest0(nb, rcur, true);
       } else {
+        trace_mark("vcycle", s);
         z = vcycle_level(0, nb, rcur, nullptr, false, true);
       }
       trace_mark("scalars", s);

@@ -116,6 +116,12 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   auto run_group = [&](NewtonGroup& g, int r0, int r1) {
     const int Sb = g.S;
     cudaStream_t s = cur_stream();
+    static const bool tracing = std::getenv("TPGPU_TRACE") != nullptr;
+    StreamTrace trace;
+    if (tracing) {
+      tl_trace = &trace;
+      trace_mark("start", s);
+    }
     std::vector<int> h_slice(Sb), h_active(Sb), h_acc(Sb);
     std::vector<double> h_alpha(Sb), rnorm(Sb), scale(Sb), nrm2(Sb);
     for (int s0 = r0; s0 < r1; s0 += Sb) {
@@ -141,6 +147,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
         if (n_active == 0) break;
         TP_CUDA(cudaMemcpyAsync(g.d_active.get(), h_active.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
         // J(u) for the batch, Galerkin hierarchy, coarsest inverses
+        trace_mark("jacobian", s);
         launch_element_stencil(*this, true, g.Ub.get(), g.J[0].get(), nb);
         for (int l = 1; l < nl; ++l) launch_rap(*this, g.J[l - 1].get(), ms[l - 1], g.J[l].get(), ms[l], nb);
         launch_coarse_inverse_slice(*this, g.J[nl - 1].get(), ms[nl - 1], g.inv.get(), nb);
@@ -155,6 +162,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
           h_acc[b] = 0;
         }
         std::vector<int> searching(h_active.begin(), h_active.end());
+        trace_mark("linesearch", s);
         for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
           int any = 0;
           for (int b = 0; b < nb; ++b) any += searching[b];
@@ -201,10 +209,16 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
                       "static init, step " + std::to_string(s0 + b + 1) + ": newton: no convergence within " +
                           std::to_string(cfg.static_max_newton) + " steps",
                       rnorm[b] / scale[b]);
+      trace_mark("store", s);
       double* dst = sharded() ? Us.get() + (size_t)(s0 - sh.s0) * n : U.get() + (size_t)s0 * n;
       TP_CUDA(cudaMemcpyAsync(dst, g.Ub.get(), (size_t)nb * n * sizeof(double), cudaMemcpyDeviceToDevice, s));
     }
     TP_CUDA(cudaStreamSynchronize(s));
+    if (tracing) {
+      trace_mark("end", s);
+      tl_trace = nullptr;
+      trace_report(trace, "trace static_init", s);
+    }
   };
 
   if (G == 1) {

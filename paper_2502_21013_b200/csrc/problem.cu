@@ -25,6 +25,24 @@ namespace tpgpu {
 
 thread_local StreamTrace* tl_trace = nullptr;
 
+void trace_report(StreamTrace& trace, const std::string& label, cudaStream_t s) {
+  TP_CUDA(cudaStreamSynchronize(s));
+  std::map<std::string, std::pair<int, double>> acc;
+  for (size_t i = 0; i + 1 < trace.ev.size(); ++i) {
+    float ms = 0;
+    TP_CUDA(cudaEventElapsedTime(&ms, trace.ev[i].second, trace.ev[i + 1].second));
+    auto& a = acc[trace.ev[i].first];
+    a.first += 1;
+    a.second += ms;
+  }
+  std::string line = label + ":";
+  for (auto& [k, v] : acc)
+    line += " " + k + " " + std::to_string(v.first) + "x " + std::to_string(v.second * 1e3).substr(0, 7) + "us";
+  std::fprintf(stderr, "%s\n", line.c_str());
+  for (auto& e : trace.ev) cudaEventDestroy(e.second);
+  trace.ev.clear();
+}
+
 bool pdl_enabled() {
   static const bool on = !std::getenv("TPGPU_PDL") || std::atoi(std::getenv("TPGPU_PDL")) != 0;
   return on;
@@ -627,19 +645,7 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
           if (tracing) {
             trace_mark("end", w.hs[g]);
             tl_trace = nullptr;
-            TP_CUDA(cudaStreamSynchronize(w.hs[g]));
-            std::map<std::string, std::pair<int, double>> acc;
-            for (size_t i = 0; i + 1 < trace.ev.size(); ++i) {
-              float ms = 0;
-              TP_CUDA(cudaEventElapsedTime(&ms, trace.ev[i].second, trace.ev[i + 1].second));
-              auto& a = acc[trace.ev[i].first];
-              a.first += 1;
-              a.second += ms;
-            }
-            std::string line = "trace g" + std::to_string(g) + ":";
-            for (auto& [k, v] : acc) line += " " + k + " " + std::to_string(v.first) + "x " + std::to_string(v.second * 1e3).substr(0, 6) + "us";
-            std::fprintf(stderr, "%s\n", line.c_str());
-            for (auto& e : trace.ev) cudaEventDestroy(e.second);
+            trace_report(trace, "trace g" + std::to_string(g), w.hs[g]);
           }
         } catch (...) {
           gerr[g] = std::current_exception();

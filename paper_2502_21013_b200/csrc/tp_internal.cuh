@@ -63,6 +63,7 @@ struct StreamTrace {
   std::vector<std::pair<const char*, cudaEvent_t>> ev;
 };
 extern thread_local StreamTrace* tl_trace;
+void trace_report(StreamTrace& trace, const std::string& label, cudaStream_t s);
 inline void trace_mark(const char* name, cudaStream_t s) {
   if (!tl_trace) return;
   cudaEvent_t e;
