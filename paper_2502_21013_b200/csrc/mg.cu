@@ -877,10 +877,23 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
                           int* __restrict__ active, int* __restrict__ zero, const int* __restrict__ mask,
                           T* __restrict__ xa, int* __restrict__ count = nullptr,
                           const double* __restrict__ bfloor = nullptr, double fscale = 0.0,
-                          int* __restrict__ count_clear = nullptr) {
+                          int* __restrict__ count_clear = nullptr, volatile int* __restrict__ pub = nullptr,
+                          unsigned* __restrict__ done = nullptr) {
   TP_PDL_ENTRY();
   const int b = blockIdx.x;
   if (b >= nb) return;
+  // ST_RN with pub: the last block to finish publishes the active count to
+  // mapped host memory (the host reads it after an event)
+  auto arrive = [&]() {
+    if (!pub || stage != ST_RN || threadIdx.x != 0) return;
+    __threadfence();
+    if (atomicAdd(done, 1u) == (unsigned)nb - 1u) {
+      __threadfence();
+      *pub = atomicAdd(count, 0);
+      *done = 0u;
+      __threadfence_system();
+    }
+  };
   // fused-scalar path (no ST_ALPHA stage): ST_RN clears the other counter slot
   // for the next iteration and retires the deferred x coefficient of batches
   // that converged an iteration ago (their last update was applied by this
@@ -891,7 +904,10 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
   // (integer atomics: the count is exact whatever the block order)
   if (count && stage == ST_ALPHA && b == 0 && threadIdx.x == 0) *count = 0;
   if (xa && threadIdx.x == 0 && (stage == ST_INIT || (stage == ST_ALPHA && !active[b]))) xa[b] = from2<T>(0.0, 0.0);
-  if (stage != ST_INIT && !active[b]) return;
+  if (stage != ST_INIT && !active[b]) {
+    arrive();
+    return;
+  }
   double s0, s1;
   batch_sum(part, per, b, s0, s1);
   if (threadIdx.x != 0) return;
@@ -920,6 +936,7 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
       rn2[b] = s0;
       active[b] = s0 > rtol2 * bn2[b];
       if (count && active[b]) atomicAdd(count, 1);
+      arrive();
       break;
     case ST_BETA: {
       const T rn = from2<T>(s0, s1);
@@ -928,13 +945,6 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
       break;
     }
   }
-}
-
-// count -> mapped host memory (read by the host after an event on the stream)
-__global__ void k_publish(const int* __restrict__ count, volatile int* __restrict__ host) {
-  TP_PDL_ENTRY();
-  *host = *count;
-  __threadfence_system();
 }
 
 __global__ void k_count_active(const int* __restrict__ active, int nb, int* __restrict__ count) {
@@ -1195,10 +1205,12 @@ void BatchSolver<MODE>::init(Problem* prob, const std::vector<LevelOp>& levels, 
   rn2.alloc(B);
   active.alloc(2 * B);
   count.alloc(2);
+  done_ctr.alloc(1);
+  TP_CUDA(cudaMemset(done_ctr.get(), 0, sizeof(unsigned)));
   if (!h_count) {
-    // mapped pinned memory: the per-iteration active count is published by a
-    // one-thread kernel (k_publish) instead of a D2H copy, so the solver's
-    // kernel chain is not broken by a copy node every iteration
+    // mapped pinned memory: the per-iteration active count is published by
+    // the last block of the stopping-test kernel instead of a D2H copy, so the
+    // solver's kernel chain is not broken by a copy node every iteration
     TP_CUDA(cudaHostAlloc(reinterpret_cast<void**>(&h_count), 2 * sizeof(int), cudaHostAllocMapped));
     TP_CUDA(cudaHostGetDevicePointer(reinterpret_cast<void**>(&h_count_dev), h_count, 0));
   }
@@ -1499,10 +1511,10 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
   const int l = 0;
   // one k_scalars stage over `per` partials per batch (launch + count)
   auto scalars = [&](int stage, const double* partials, int per, int* cnt, int* cnt_clear, const double* floor_ptr,
-                     double floor_scale) {
+                     double floor_scale, volatile int* pub = nullptr) {
     launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, stage, partials, per, nb, rtol2, rho.get(), mu.get(),
                alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, cnt, floor_ptr,
-               floor_scale, cnt_clear);
+               floor_scale, cnt_clear, pub, pub ? done_ctr.get() : static_cast<unsigned*>(nullptr));
     TP_LAUNCHED(p);
   };
   trace_mark("pcg-init", s);
@@ -1583,14 +1595,10 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
       }
       trace_mark("scalars", s);
       scalars(ST_RN, fscal ? partD.get() : part.get(), fused ? per_d : per_t, count.get() + slot,
-              fscal ? count.get() + (slot ^ 1) : nullptr, nullptr, 0.0);
-      if (use_publish) {
-        launch_pdl(k_publish, dim3(1), dim3(1), 0, s, static_cast<const int*>(count.get() + slot),
-                   static_cast<volatile int*>(h_count_dev + slot));
-        TP_LAUNCHED(p);
-      } else {
+              fscal ? count.get() + (slot ^ 1) : nullptr, nullptr, 0.0,
+              use_publish ? static_cast<volatile int*>(h_count_dev + slot) : nullptr);
+      if (!use_publish)
         TP_CUDA(cudaMemcpyAsync(h_count + slot, count.get() + slot, sizeof(int), cudaMemcpyDeviceToHost, s));
-      }
       TP_CUDA(cudaEventRecord(ev[slot], s));
       if (dbg_freq) {  // experiment: per-frequency iteration counts (synchronizes every iteration)
         std::vector<int> ha(nb);

@@ -112,6 +112,7 @@ struct BatchSolver {
   DevBuf<double> bn2, rn2;
   DevBuf<int> active;
   DevBuf<int> count;
+  DevBuf<unsigned> done_ctr;  // blocks of the stopping-test kernel that finished (last one publishes)
   int* h_count = nullptr;      // mapped pinned [2]
   int* h_count_dev = nullptr;  // its device address
   int cur_active = 0;      // active batches as last seen by the host (kernel-timer byte accounting)
