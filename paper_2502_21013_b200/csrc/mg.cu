@@ -1286,7 +1286,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_level(int l, int nb, co
   if constexpr (MODE == 0) {
     if (l == small_from) {
       trace_mark("small", p->cur_stream());
-      launch_small_cycle(*p, small, lam, coarse_inv, bl, zo, act, cfg.omega, cfg.omega2, nb);
+      launch_small_cycle(*p, small, lam, coarse_inv, bl, zo, act, cfg.omega, cfg.omega2, nb, cur_active);
       return zo;
     }
     if (ops[l].fine.we) {

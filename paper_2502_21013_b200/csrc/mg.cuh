@@ -76,7 +76,7 @@ size_t small_cycle_smem(const int* m, int levels);
 size_t small_pack_size(const int* m, int levels);  // doubles
 void pack_small_levels(Problem& p, SmallLevels& sl, double* buf);
 void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, const cplx* inv, const cplx* b,
-                        cplx* z, const int* active, double om1, double om2, int nb);
+                        cplx* z, const int* active, double om1, double om2, int nb, int n_active);
 
 // Stencils of one level for the whole batch (slice mode) or shared (freq mode).
 struct LevelOp {

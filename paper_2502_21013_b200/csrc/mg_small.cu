@@ -23,6 +23,9 @@
 // padded grid -- so a node's 7-point row is 7 16-byte coefficient loads and
 // 7 neighbour reads with no boundary tests, and threads map to (x, y) by
 // shifts (a power-of-two row pitch) instead of divisions.
+#include <cooperative_groups.h>
+#include <cstdlib>
+
 #include "mg.cuh"
 
 namespace tpgpu {
@@ -58,17 +61,18 @@ struct Lvl {
 #define TP_SMALL_UNROLL TP_SMALL_UNROLL_N(TPGPU_SMALL_UNROLL)
 // threads of the block over the level's nodes: x = tid & (2^sh - 1), rows
 // stepping by SNT >> sh
-#define FOR_NODES(L, ...)                                                     \
-  {                                                                           \
-    const int x_ = threadIdx.x & ((1 << (L).sh) - 1);                         \
-    if (x_ < (L).m)                                                           \
-      TP_SMALL_UNROLL                                                         \
-      for (int y_ = threadIdx.x >> (L).sh; y_ < (L).m; y_ += SNT >> (L).sh) { \
-        const int x = x_, y = y_;                                             \
-        const int P = (y + 1) * (L).w + x + 1;                                \
-        __VA_ARGS__                                                           \
-      }                                                                       \
+#define FOR_ROWS(L, YLO, YHI, ...)                                                  \
+  {                                                                                 \
+    const int x_ = threadIdx.x & ((1 << (L).sh) - 1);                               \
+    if (x_ < (L).m)                                                                 \
+      TP_SMALL_UNROLL                                                               \
+      for (int y_ = (YLO) + (threadIdx.x >> (L).sh); y_ < (YHI); y_ += SNT >> (L).sh) { \
+        const int x = x_, y = y_;                                                   \
+        const int P = (y + 1) * (L).w + x + 1;                                      \
+        __VA_ARGS__                                                                 \
+      }                                                                             \
   }
+#define FOR_NODES(L, ...) FOR_ROWS(L, 0, (L).m, __VA_ARGS__)
 
 __device__ __forceinline__ cplx diag_of(double2 c, cplx l) { return {fma(l.re, c.y, c.x), l.im * c.y}; }
 
@@ -94,8 +98,8 @@ __device__ __forceinline__ void stencil(const Lvl& L, int P, cplx l, const cplx*
 // z_out = z_in + w (b - A z_in) / d  (z_in == nullptr: z_out = w b / d);
 // b from global (unpadded, b_g) on the top level, else from shared (padded)
 __device__ __forceinline__ void jacobi(const Lvl& L, cplx l, const cplx* b_g, const cplx* b_s, const cplx* zin,
-                                       cplx* zout, double w) {
-  FOR_NODES(L, {
+                                       cplx* zout, double w, int ylo = 0, int yhi = 1 << 30) {
+  FOR_ROWS(L, ylo, min(yhi, L.m), {
     const cplx bi = b_g ? b_g[y * L.m + x] : b_s[P];
     if (!zin) {
       const cplx d = diag_of(__ldg(L.C + P), l);
@@ -110,8 +114,8 @@ __device__ __forceinline__ void jacobi(const Lvl& L, cplx l, const cplx* b_g, co
 }
 
 __device__ __forceinline__ void residual(const Lvl& L, cplx l, const cplx* b_g, const cplx* b_s, const cplx* z,
-                                         cplx* res) {
-  FOR_NODES(L, {
+                                         cplx* res, int ylo = 0, int yhi = 1 << 30) {
+  FOR_ROWS(L, ylo, min(yhi, L.m), {
     cplx d, off;
     stencil(L, P, l, z, d, off);
     res[P] = (b_g ? b_g[y * L.m + x] : b_s[P]) - off - cmul(d, z[P]);
@@ -119,20 +123,24 @@ __device__ __forceinline__ void residual(const Lvl& L, cplx l, const cplx* b_g, 
 }
 
 // b_c = P^T res (interior fine centre (2X+1, 2Y+1) and its six neighbours)
-__device__ __forceinline__ void restrict_to(const Lvl& F, const Lvl& Cc, const cplx* res, cplx* bc) {
+__device__ __forceinline__ void restrict_to(const Lvl& F, const Lvl& Cc, const cplx* res, cplx* bc, int ylo = 0,
+                                            int yhi = 1 << 30, cplx* bc2 = nullptr) {
   const int w = F.w;
-  FOR_NODES(Cc, {
+  FOR_ROWS(Cc, ylo, min(yhi, Cc.m), {
     const int f = (2 * y + 2) * w + 2 * x + 2;
     const cplx side = res[f - 1] + res[f + 1] + res[f - w] + res[f + w] + res[f - w - 1] + res[f + w + 1];
-    bc[P] = res[f] + 0.5 * side;
+    const cplx v = res[f] + 0.5 * side;
+    bc[P] = v;
+    if (bc2) bc2[P] = v;  // the cluster partner's copy
   })
 }
 
 // z += P x_c (P1 interpolation on the nested triangulation); coarse vertex
 // (A, B), A, B in [0, mc+1], sits at padded index B (mc+2) + A (zero border)
-__device__ __forceinline__ void prolong_add(const Lvl& F, const Lvl& Cc, const cplx* xc, cplx* z) {
+__device__ __forceinline__ void prolong_add(const Lvl& F, const Lvl& Cc, const cplx* xc, cplx* z, int ylo = 0,
+                                            int yhi = 1 << 30) {
   const int wc = Cc.w;
-  FOR_NODES(F, {
+  FOR_ROWS(F, ylo, min(yhi, F.m), {
     const int a = x + 1, b = y + 1, ah = a >> 1, bh = b >> 1;
     const int c0 = bh * wc + ah;
     cplx v;
@@ -146,12 +154,19 @@ __device__ __forceinline__ void prolong_add(const Lvl& F, const Lvl& Cc, const c
 
 __device__ __forceinline__ int pitch_shift(int m) { return m <= 1 ? 0 : 32 - __clz(m - 1); }
 
+// CL = 2: a cluster of two blocks per frequency splits the top small level's
+// rows between them (the level carries ~60 % of the kernel's time): after each
+// half-step a block stores its boundary row into its partner's copy of the
+// vector (distributed shared memory) and the pair meets at a cluster barrier;
+// the restriction's coarse rows go to both blocks, which then run the lower
+// levels and the coarsest solve redundantly (identical arithmetic).
+template <int CL>
 __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cplx* __restrict__ lam,
                                                         const cplx* __restrict__ inv, const cplx* __restrict__ b0,
                                                         cplx* __restrict__ z0, const int* __restrict__ active,
                                                         double om1, double om2, int smem_c16) {
   TP_PDL_ENTRY();
-  const int bt = blockIdx.x;
+  const int bt = blockIdx.x / CL;
   if (active && !active[bt]) return;
   extern __shared__ __align__(16) unsigned char small_smem[];
   cplx* sm = reinterpret_cast<cplx*>(small_smem);
@@ -182,9 +197,37 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
   auto za = [&](int j) -> cplx* { return base(j) + (j == 0 ? 0 : npad(j)); };
   auto zb = [&](int j) -> cplx* { return za(j) + npad(j); };
   const cplx l = lam[bt];
-  const int n0 = sl.m[0] * sl.m[0];
+  const int m0 = sl.m[0], n0 = m0 * m0;
   const cplx* bg = b0 + (size_t)bt * n0;
-  __syncthreads();
+  // top-level rows of this block: [ya, yb); coarse rows of its restriction [Ya, Yb)
+  int rank = 0, ya = 0, yb = m0, Ya = 0, Yb = 1 << 30;
+  const int ymid = (m0 + 1) / 2;
+  if constexpr (CL == 2) {
+    rank = (int)cooperative_groups::this_cluster().block_rank();
+    ya = rank == 0 ? 0 : ymid;
+    yb = rank == 0 ? ymid : m0;
+    Ya = rank == 0 ? 0 : ymid / 2;
+    Yb = rank == 0 ? ymid / 2 : (1 << 30);
+  }
+  // the partner's copy of a vector of this block's shared memory
+  auto remote = [&](cplx* v) -> cplx* {
+    if constexpr (CL == 2) return cooperative_groups::this_cluster().map_shared_rank(v, rank ^ 1);
+    else return nullptr;
+  };
+  // after a top-level half-step: boundary row to the partner, then both meet
+  auto exchange = [&](cplx* v) {
+    if constexpr (CL == 2) {
+      const int row = rank == 0 ? yb - 1 : ya, w = m0 + 2;
+      __syncthreads();  // the row was written by other threads of this block
+      cplx* r = remote(v);
+      for (int x = threadIdx.x; x < m0; x += SNT) r[(row + 1) * w + x + 1] = v[(row + 1) * w + x + 1];
+      cooperative_groups::this_cluster().sync();
+    } else {
+      __syncthreads();
+    }
+  };
+  if constexpr (CL == 2) cooperative_groups::this_cluster().sync();  // both cleared before remote stores
+  else __syncthreads();
   // down (loops unrolled over the level bound: static indices into sl)
 #pragma unroll
   for (int j = 0; j < kMaxSmall - 1; ++j) {
@@ -192,14 +235,25 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
     const Lvl L = lvl(j);
     const cplx* b_g = j == 0 ? bg : nullptr;
     cplx *b = bs(j), *a = za(j), *c = zb(j);
-    jacobi(L, l, b_g, b, nullptr, a, om1);  // z1
-    __syncthreads();
-    jacobi(L, l, b_g, b, a, c, om2);  // z2
-    __syncthreads();
-    residual(L, l, b_g, b, c, a);
-    __syncthreads();
-    restrict_to(L, lvl(j + 1), a, bs(j + 1));
-    __syncthreads();
+    if (j == 0 && CL == 2) {
+      jacobi(L, l, b_g, b, nullptr, a, om1, ya, yb);  // z1
+      exchange(a);
+      jacobi(L, l, b_g, b, a, c, om2, ya, yb);  // z2
+      exchange(c);
+      residual(L, l, b_g, b, c, a, ya, yb);
+      exchange(a);
+      restrict_to(L, lvl(1), a, bs(1), Ya, Yb, remote(bs(1)));
+      if constexpr (CL == 2) cooperative_groups::this_cluster().sync();
+    } else {
+      jacobi(L, l, b_g, b, nullptr, a, om1);  // z1
+      __syncthreads();
+      jacobi(L, l, b_g, b, a, c, om2);  // z2
+      __syncthreads();
+      residual(L, l, b_g, b, c, a);
+      __syncthreads();
+      restrict_to(L, lvl(j + 1), a, bs(j + 1));
+      __syncthreads();
+    }
   }
   // coarsest: x = inv b (inv transposed: A[j * nc + i] = inv(i, j)), spread
   // over the whole block: G groups of nc threads each sum a strided share of
@@ -244,17 +298,29 @@ __global__ void __launch_bounds__(SNT, 1) k_small_cycle(SmallLevels sl, const cp
     const cplx* b_g = j == 0 ? bg : nullptr;
     cplx *b = bs(j), *a = za(j), *c = zb(j);
     const cplx* xc = (j == nl - 2) ? za(nl - 1) : zb(j + 1);
-    prolong_add(L, lvl(j + 1), xc, c);  // zc = z2 + P x_c
-    __syncthreads();
-    jacobi(L, l, b_g, b, c, a, om2);  // z3
-    __syncthreads();
-    jacobi(L, l, b_g, b, a, c, om1);  // z4
-    __syncthreads();
+    if (j == 0 && CL == 2) {
+      prolong_add(L, lvl(1), xc, c, ya, yb);  // zc = z2 + P x_c
+      exchange(c);
+      jacobi(L, l, b_g, b, c, a, om2, ya, yb);  // z3
+      exchange(a);
+      jacobi(L, l, b_g, b, a, c, om1, ya, yb);  // z4
+      __syncthreads();
+    } else {
+      prolong_add(L, lvl(j + 1), xc, c);  // zc = z2 + P x_c
+      __syncthreads();
+      jacobi(L, l, b_g, b, c, a, om2);  // z3
+      __syncthreads();
+      jacobi(L, l, b_g, b, a, c, om1);  // z4
+      __syncthreads();
+    }
   }
   cplx* zo = z0 + (size_t)bt * n0;
   const cplx* z4 = zb(0);
   const Lvl L0 = lvl(0);
-  FOR_NODES(L0, { zo[y * L0.m + x] = z4[P]; })
+  FOR_ROWS(L0, ya, yb, { zo[y * L0.m + x] = z4[P]; })
+  // the partner may still read this block's shared memory (remote stores are
+  // done, but keep both alive until the pair is through)
+  if constexpr (CL == 2) cooperative_groups::this_cluster().sync();
 }
 
 // packed, zero-padded {K, M} planes C, E, N, NE of one level
@@ -304,16 +370,41 @@ void pack_small_levels(Problem& p, SmallLevels& sl, double* buf) {
 }
 
 void launch_small_cycle(Problem& p, const SmallLevels& sl, const cplx* lam, const cplx* inv, const cplx* b,
-                        cplx* z, const int* active, double om1, double om2, int nb) {
+                        cplx* z, const int* active, double om1, double om2, int nb, int n_active) {
   const size_t sm = small_cycle_smem(sl.m, sl.levels);
   static const bool attr = [] {  // (thread-safe one-time init: the largest opt-in size)
-    return cudaFuncSetAttribute(k_small_cycle, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
-           cudaSuccess;
+    return cudaFuncSetAttribute(k_small_cycle<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
+               cudaSuccess &&
+           cudaFuncSetAttribute(k_small_cycle<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024) ==
+               cudaSuccess;
   }();
   require(attr && sm <= 227 * 1024, "small-level cycle: shared memory");
   require(sl.KM[0] != nullptr, "small-level cycle: stencils not packed");
-  launch_pdl(k_small_cycle, dim3(nb), dim3(SNT), sm, p.cur_stream(), sl, lam, inv, b, z, active, om1, om2,
-             (int)(sm / sizeof(cplx)));
+  // two-block clusters when few frequencies are active (the tail of a solve:
+  // half the latency; with many active frequencies the second SM per frequency
+  // costs the concurrent groups more than it saves -- cfg 1 3.38 vs 3.33 ms
+  // always-on).  TPGPU_SMALL_CLUSTER = the largest active count that uses them.
+  static const int cl_max = std::getenv("TPGPU_SMALL_CLUSTER") ? std::atoi(std::getenv("TPGPU_SMALL_CLUSTER")) : 0;
+  if (n_active <= cl_max && sl.levels >= 2 && sl.m[0] >= 15) {
+    cudaLaunchAttribute at[2];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cudaLaunchConfig_t c = {};
+    c.gridDim = dim3(2 * nb);
+    c.blockDim = dim3(SNT);
+    c.dynamicSmemBytes = sm;
+    c.stream = p.cur_stream();
+    c.attrs = at;
+    c.numAttrs = 2;
+    TP_CUDA(cudaLaunchKernelEx(&c, k_small_cycle<2>, sl, lam, inv, b, z, active, om1, om2, (int)(sm / sizeof(cplx))));
+  } else {
+    launch_pdl(k_small_cycle<1>, dim3(nb), dim3(SNT), sm, p.cur_stream(), sl, lam, inv, b, z, active, om1, om2,
+               (int)(sm / sizeof(cplx)));
+  }
   TP_LAUNCHED(&p);
 }
 
