@@ -12,6 +12,7 @@
 // is here for completeness of the reference's method set, not for speed.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <memory>
 #include <string>
 #include <vector>
@@ -96,6 +97,10 @@ void Problem::solve_m3_dev(const tp_solver_cfg& cfg, M2Result& res) {
   mc.rtol = std::max(cfg.inner_rtol, 1e-10);  // the reference SparseSolver's contract (solve.hpp:79-89)
   mc.max_iter = cfg.inner_max_iter;
   mc.omega = mc.omega2 = 0.6;
+  if (TPGPU_SLICE_L1 && !std::getenv("TPGPU_TILE_SLICE")) {  // l1-Jacobi + Chebyshev (mg.cuh)
+    mc.omega = kL1Omega1;
+    mc.omega2 = kL1Omega2;
+  }
   BatchSolver<1> solver;
   solver.init(this, ops, 1, mc);
   solver.coarse_inv = inv.get();

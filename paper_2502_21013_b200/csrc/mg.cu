@@ -1241,8 +1241,10 @@ static void set_fused_attrs() {
 template <int MODE>
 bool BatchSolver<MODE>::stream_level(int l) const {
   if constexpr (MODE == 1) {
+    // (the l1-Jacobi smoother exists in the streaming passes only: with it every
+    // non-coarsest level streams)
     static const bool tile = std::getenv("TPGPU_TILE_SLICE") != nullptr;
-    return !tile && l + 1 < (int)ops.size() && ops[l].m >= 15;
+    return !tile && l + 1 < (int)ops.size() && (TPGPU_SLICE_L1 || ops[l].m >= 15);
   } else {
     return false;
   }

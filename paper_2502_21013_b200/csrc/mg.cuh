@@ -19,6 +19,14 @@
 
 namespace tpgpu {
 
+// Slice-mode (Newton Jacobian) smoother: l1-Jacobi diagonal sum_j |J_ij| with
+// the degree-2 Chebyshev weights for D_l1^-1 J on [1/6, 1] (1: on; 0: plain
+// damped Jacobi, omega = 0.6 on the true diagonal)
+#ifndef TPGPU_SLICE_L1
+#define TPGPU_SLICE_L1 1
+#endif
+constexpr double kL1Omega1 = 1.1387, kL1Omega2 = 3.4641;
+
 struct MGConfig {
   int pre = 2, post = 2;    // smoothing sweeps
   // Damped-Jacobi steps with a degree-2 Chebyshev pair of weights for D^-1 A

@@ -217,6 +217,8 @@ struct Five {  // fine level: K_hat from edge weights (we, wn), lumped mass
     const double kc = (y.we + y.ww) + (y.wn + y.ws);
     return {fma(l.re, y.mm, kc), l.im * y.mm};
   }
+  // the smoother's diagonal: the operator's own
+  static __device__ __forceinline__ cplx sdiag(const Reg&, cplx d) { return d; }
   // d v - wE vE - wW vW - wN vN - wS vS (neighbours of Dirichlet vertices are
   // zero vectors, their edge weights stay on the diagonal)
   // (l unused: the diagonal d from diag() carries the shift)
@@ -272,6 +274,7 @@ struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, 
     return {fma(l.re, mm, r->w[q][lane]), l.im * mm};
   }
   static __device__ __forceinline__ cplx diag(const Reg& y, cplx l) { return coef(y.p, 0, y.lane, l); }
+  static __device__ __forceinline__ cplx sdiag(const Reg&, cplx d) { return d; }
   // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1).  Split form
   //   sum_d (K_d + l M_d) v_d = sum_d K_d v_d + l sum_d M_d v_d
   // (real x complex products, one complex multiply by l at the end); the
@@ -334,6 +337,20 @@ struct SevenJ {
   }
   static __device__ __forceinline__ Reg first(const WRow<NW>& st, int lane) { return {&st, &st, lane}; }
   static __device__ __forceinline__ double diag(const Reg& y, cplx) { return y.p->w[0][y.lane]; }
+  // the smoother's diagonal: the l1 row sum sum_j |J_ij| (TPGPU_SLICE_L1, mg.cuh)
+  // -- D_l1^-1 J has its spectrum in (0, 1] for any SPD J, so the Chebyshev
+  // pair of weights is safe despite the anisotropic rank-one Jacobian term
+  static __device__ __forceinline__ double sdiag(const Reg& y, double d) {
+#if TPGPU_SLICE_L1
+    const int ln = y.lane, lw = ln > 0 ? ln - 1 : 0;
+    const WRow<NW>& a = *y.p;
+    const WRow<NW>& b = *y.pb;
+    return fabs(d) + fabs(a.w[1][ln]) + fabs(a.w[1][lw]) + fabs(a.w[2][ln]) + fabs(b.w[2][ln]) + fabs(a.w[3][ln]) +
+           fabs(b.w[3][lw]);
+#else
+    return d;
+#endif
+  }
   // W = E(x-1), S = N(y-1), SW = NE(x-1, y-1) (west lane's slots, XLANE)
   static __device__ __forceinline__ double apply(const Reg& y, cplx, double d, double vs, double v, double vn) {
     const int ln = y.lane, lw = ln > 0 ? ln - 1 : 0;
@@ -573,7 +590,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
       id1[j] = id0[j];
       d2[j] = d1[j]; d1[j] = d0[j];
       d0[j] = S::diag(k0, l[j]);
-      id0[j] = rcp(d0[j]);
+      id0[j] = rcp(S::sdiag(k0, d0[j]));
       a0[j] = in0 ? cs(om1, cm(r0[j], id0[j])) : T{};
       // z2 at row yi-1
       b3[j] = b2[j]; b2[j] = b1[j];
@@ -742,7 +759,7 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
         dd1[j] = S::diag(k1, l[j]);
         const T Ac = S::apply(k1, l[j], dd1[j], c2[j], c1[j], c0[j]);
         jd2[j] = jd1[j];
-        jd1[j] = rcp(dd1[j]);
+        jd1[j] = rcp(S::sdiag(k1, dd1[j]));
         const T t = cm(r1[j] - Ac, jd1[j]);
         e1[j] = in1 ? fmav(om2, t, c1[j]) : T{};
       }

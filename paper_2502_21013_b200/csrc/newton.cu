@@ -86,7 +86,12 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   // keeps the V-cycle symmetric positive definite (the Chebyshev pair of the
   // frequency solver assumes a spectrum in (0, 2]).
   mc.omega = mc.omega2 = 0.6;
+  if (TPGPU_SLICE_L1 && !std::getenv("TPGPU_TILE_SLICE")) {  // l1-Jacobi + Chebyshev (mg.cuh)
+    mc.omega = kL1Omega1;
+    mc.omega2 = kL1Omega2;
+  }
   if (const char* e = std::getenv("TPGPU_NEWTON_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
+  if (const char* e = std::getenv("TPGPU_NEWTON_OMEGA2")) mc.omega2 = std::atof(e);
 
   std::vector<std::unique_ptr<NewtonGroup>> groups(G);
   for (auto& gp : groups) {
