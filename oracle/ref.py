@@ -232,3 +232,120 @@ def solve_m3(desc, U0, cfg: TpSolverCfg | None = None):
                                 C.byref(st), _ptr(wall)))
     k = it.value
     return U, hist[:k + 1].copy(), k, st.value, float(wall[0])
+
+
+# ---------------------------------------------------------------- transformer (reference physics)
+class TrCfg(C.Structure):
+    """tpref_mesh_cfg: configs/transformer.json fields (RunConfig, config.hpp:39-53)."""
+    _fields_ = [("nx", C.c_int32), ("ny", C.c_int32), ("refinements", C.c_int32), ("steps", C.c_int32),
+                ("period", C.c_double), ("s_max", C.c_double), ("flux_samples", C.c_int32),
+                ("pad_", C.c_int32), ("j_amp", C.c_double)]
+
+
+def tr_cfg(nx=40, ny=40, refinements=0, steps=64, period=0.02, s_max=3.0, flux_samples=10001,
+           j_amp=0.0) -> TrCfg:
+    """j_amp: winding amplitude override (0: MaterialTable::transformer's 1.9e4;
+    configs/transformer_saturated.json uses 9.5e5)."""
+    return TrCfg(nx, ny, refinements, steps, period, s_max, flux_samples, 0, j_amp)
+
+
+def _trlib():
+    L = lib()
+    if not getattr(L, "_tr_ready", False):
+        dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+        T, G = C.POINTER(TrCfg), C.POINTER(TpSolverCfg)
+        L.tpref_tr_mesh.argtypes = [C.c_int32, C.c_int32, C.c_int32, ip, ip, ip, dp, ip, ip]
+        L.tpref_tr_loads.argtypes = [T, dp]
+        L.tpref_tr_mass.argtypes = [T, ip, ip, ip, ip, dp]
+        L.tpref_tr_apply_k.argtypes = [T, dp, dp, C.c_int32]
+        L.tpref_tr_residual.argtypes = [T, dp, dp, dp]
+        L.tpref_tr_static_init.argtypes = [T, G, dp, ip]
+        L.tpref_tr_choose_nu_hat.argtypes = [T, G, dp, dp, dp]
+        L.tpref_tr_periodic_solve.argtypes = [T, G, dp, dp, dp]
+        L.tpref_tr_solve_m1.argtypes = [T, G, dp, C.c_double, dp, dp, dp, C.c_int32, ip, ip, dp, dp]
+        L._tr_ready = True
+    return L
+
+
+def tr_mesh(nx, ny, refinements=0):
+    """build_rectilinear_mesh(transformer_regions()) + refine_uniform (mesh.hpp:139-246):
+    (vertices (nv, 2), triangles (nt, 3), region (nt,), n_dof)."""
+    L = _trlib()
+    nv, nt, nd = C.c_int32(), C.c_int32(), C.c_int32()
+    _check(L.tpref_tr_mesh(nx, ny, refinements, C.byref(nv), C.byref(nt), C.byref(nd), None, None, None))
+    V = np.zeros((nv.value, 2))
+    Tr = np.zeros((nt.value, 3), dtype=np.int32)
+    R = np.zeros(nt.value, dtype=np.int32)
+    _check(L.tpref_tr_mesh(nx, ny, refinements, None, None, None, _ptr(V), _ptr(Tr), _ptr(R)))
+    return V, Tr, R, nd.value
+
+
+def tr_sizes(c: TrCfg):
+    return tr_mesh(c.nx, c.ny, c.refinements)[3], c.steps
+
+
+def tr_loads(c: TrCfg):
+    n, N = tr_sizes(c)
+    F = np.zeros((N, n))
+    _check(_trlib().tpref_tr_loads(C.byref(c), _ptr(F)))
+    return F
+
+
+def tr_apply_k(c: TrCfg, U):
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    out = np.zeros_like(U)
+    _check(_trlib().tpref_tr_apply_k(C.byref(c), _ptr(U), _ptr(out), 1 if U.ndim == 1 else U.shape[0]))
+    return out
+
+
+def tr_residual(c: TrCfg, U):
+    U = np.ascontiguousarray(U, dtype=np.float64)
+    R = np.zeros_like(U)
+    nrm = C.c_double()
+    _check(_trlib().tpref_tr_residual(C.byref(c), _ptr(U), _ptr(R), C.byref(nrm)))
+    return R, nrm.value
+
+
+def tr_static_init(c: TrCfg, cfg: TpSolverCfg | None = None):
+    cfg = cfg or default_cfg()
+    n, N = tr_sizes(c)
+    U0 = np.zeros((N, n))
+    counts = np.zeros(N, dtype=np.int32)
+    _check(_trlib().tpref_tr_static_init(C.byref(c), C.byref(cfg), _ptr(U0), _ptr(counts)))
+    return U0, counts
+
+
+def tr_choose_nu_hat(c: TrCfg, U0, cfg: TpSolverCfg | None = None):
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    nu = np.zeros(5)
+    q = C.c_double()
+    _check(_trlib().tpref_tr_choose_nu_hat(C.byref(c), C.byref(cfg), _ptr(U0), _ptr(nu), C.byref(q)))
+    return nu, q.value
+
+
+def tr_periodic_solve(c: TrCfg, nu_hat, G, cfg: TpSolverCfg | None = None):
+    cfg = cfg or default_cfg()
+    G = np.ascontiguousarray(G, dtype=np.float64)
+    U = np.zeros_like(G)
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(_trlib().tpref_tr_periodic_solve(C.byref(c), C.byref(cfg), _ptr(nu), _ptr(G), _ptr(U)))
+    return U
+
+
+def tr_solve_m1(c: TrCfg, nu_hat, q, U0, cfg: TpSolverCfg | None = None, keep_iterates=False) -> RefM1Result:
+    """solve_m1_fixed_point on the reference's own transformer problem."""
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    cap = cfg.m1_max_outer + 1
+    hist = np.zeros(cap)
+    it, st = C.c_int32(), C.c_int32()
+    U = np.zeros_like(U0)
+    its = np.zeros((cap,) + U0.shape) if keep_iterates else None
+    wall = np.zeros(1)
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(_trlib().tpref_tr_solve_m1(C.byref(c), C.byref(cfg), _ptr(nu), q, _ptr(U0), _ptr(U), _ptr(hist), cap,
+                                      C.byref(it), C.byref(st), _ptr(its), _ptr(wall)))
+    k = it.value
+    return RefM1Result(U=U, history=hist[:k + 1].copy(), contraction=np.zeros(0), iterations=k, status=st.value,
+                       iterates=None if its is None else its[:k + 1].copy(), wall_time=float(wall[0]))

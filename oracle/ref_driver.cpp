@@ -10,16 +10,23 @@
 //   tpref_solve_m3      -> tpfem::solve_m3_timestepping  (solvers.hpp:489-542)
 //   tpref_periodic_solve-> tpfem::PeriodicSolver::solve  (periodic.hpp:154-198)
 //   tpref_residual      -> tpfem::residual + block_l2    (periodic.hpp:35-67)
-// with tporacle::GridProblem (grid_problem.hpp) supplying the BASELINE physics.
+// with tporacle::GridProblem (grid_problem.hpp) supplying the BASELINE physics,
+// and (tpref_tr_*) the reference's own transformer problem end to end
+// (build_rectilinear_mesh + refine_uniform, MaterialTable::transformer,
+// NonlinearOperator, assemble_mass / assemble_loads, FemProblem: the
+// setup_transformer pipeline, runner.hpp:27-73) for the general-mesh path.
 #include <chrono>
 #include <cstring>
 #include <string>
 #include <thread>
 
 #include "grid_problem.hpp"
+#include "tpfem/assembly.hpp"
+#include "tpfem/mesh.hpp"
 #include "tpfem/periodic.hpp"
 #include "tpfem/solvers.hpp"
 #include "../include/tpgpu_baseline.h"
+#include "../include/tpgpu_mesh.h"
 
 namespace {
 
@@ -279,6 +286,202 @@ int tpref_solve_m3(const tp_problem_desc* d, const tp_solver_cfg* c, const doubl
       history[k] = rep.residual_history[k];
     if (iterations) *iterations = rep.iterations;
     if (status) *status = static_cast<int32_t>(rep.status);
+  });
+}
+
+}  // extern "C"
+
+// ---------------------------------------------------------------- transformer (reference physics)
+extern "C" {
+// configs/transformer.json fields (RunConfig, config.hpp:39-53)
+typedef struct tpref_mesh_cfg {
+  int32_t nx, ny, refinements, steps;
+  double period, s_max;
+  int32_t flux_samples, pad_;
+  double j_amp;  // winding current amplitude override (configs/transformer_saturated.json); 0: table value
+} tpref_mesh_cfg;
+}
+
+namespace {
+
+// runner.hpp:27-31 + 46-73 (up to static_init), on the reference's own types
+struct TrSetup {
+  std::shared_ptr<const tpfem::Mesh> mesh;
+  tpfem::MaterialTable mat = tpfem::MaterialTable::transformer();
+  std::unique_ptr<tpfem::NonlinearOperator> op;
+  tpfem::SparseMatrix<double> M;
+  tpfem::BlockRhs F;
+  double tau = 0;
+  int N = 0;
+  explicit TrSetup(const tpref_mesh_cfg& c) {
+    if (c.j_amp != 0) {  // parse_materials override (config.hpp:146-170)
+      auto wp = mat.at(tpfem::Region::winding_plus), wm = mat.at(tpfem::Region::winding_minus);
+      wp.j_amp = c.j_amp;
+      wm.j_amp = -c.j_amp;
+      mat.set(tpfem::Region::winding_plus, wp);
+      mat.set(tpfem::Region::winding_minus, wm);
+    }
+    tpfem::Mesh m = tpfem::build_rectilinear_mesh(tpfem::transformer_regions(), c.nx, c.ny);
+    for (int r = 0; r < c.refinements; ++r) m = tpfem::refine_uniform(m);
+    mesh = std::make_shared<const tpfem::Mesh>(std::move(m));
+    op = std::make_unique<tpfem::NonlinearOperator>(mesh, mat);
+    N = c.steps;
+    tau = c.period / c.steps;
+    F = tpfem::assemble_loads(*mesh, mat, c.steps, c.period);
+    M = tpfem::assemble_mass(*mesh, mat);
+  }
+  tpfem::FemProblem problem() const { return tpfem::FemProblem{&M, op.get()}; }
+  tpfem::PeriodicState state(const double* U) const {
+    tpfem::PeriodicState s(N, op->n_dof(), tau);
+    std::memcpy(s.data.data(), U, s.data.size() * sizeof(double));
+    return s;
+  }
+};
+
+}  // namespace
+
+extern "C" {
+
+int tpref_tr_mesh(int32_t nx, int32_t ny, int32_t refinements, int32_t* nv, int32_t* nt, int32_t* ndof,
+                  double* verts, int32_t* tris, int32_t* region) {
+  return guarded([&] {
+    tpfem::Mesh m = tpfem::build_rectilinear_mesh(tpfem::transformer_regions(), nx, ny);
+    for (int r = 0; r < refinements; ++r) m = tpfem::refine_uniform(m);
+    if (nv) *nv = m.n_vertices();
+    if (nt) *nt = m.n_triangles();
+    if (ndof) *ndof = m.n_dof();
+    if (verts)
+      for (int v = 0; v < m.n_vertices(); ++v) {
+        verts[2 * v] = m.vertices[v][0];
+        verts[2 * v + 1] = m.vertices[v][1];
+      }
+    if (tris)
+      for (int t = 0; t < m.n_triangles(); ++t)
+        for (int k = 0; k < 3; ++k) tris[3 * t + k] = m.triangles[t][k];
+    if (region)
+      for (int t = 0; t < m.n_triangles(); ++t) region[t] = static_cast<int32_t>(m.region[t]);
+  });
+}
+
+int tpref_tr_material(tp_exp_material* out) {
+  return guarded([&] {
+    const auto t = tpfem::MaterialTable::transformer();
+    for (int r = 0; r < tpfem::kNumRegions; ++r) {
+      const auto& m = t.at(static_cast<tpfem::Region>(r));
+      out[r] = tp_exp_material{m.sigma, m.a, m.b, m.c, m.d, m.j_amp};
+    }
+  });
+}
+
+int tpref_tr_loads(const tpref_mesh_cfg* c, double* F) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    std::memcpy(F, s.F.data.data(), s.F.data.size() * sizeof(double));
+  });
+}
+
+// consistent mass as CSR (rowptr n+1, col nnz, val nnz); call with NULL
+// arrays first for n / nnz
+int tpref_tr_mass(const tpref_mesh_cfg* c, int32_t* n, int32_t* nnz, int32_t* rowptr, int32_t* col,
+                  double* val) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const auto& M = s.M;
+    if (n) *n = static_cast<int32_t>(M.rows());
+    if (nnz) *nnz = static_cast<int32_t>(M.nnz());
+    if (rowptr)
+      for (std::size_t i = 0; i <= static_cast<std::size_t>(M.rows()); ++i) rowptr[i] = M.row_offsets()[i];
+    if (col)
+      for (std::size_t k = 0; k < static_cast<std::size_t>(M.nnz()); ++k) col[k] = M.col_indices()[k];
+    if (val)
+      for (std::size_t k = 0; k < static_cast<std::size_t>(M.nnz()); ++k) val[k] = M.values()[k];
+  });
+}
+
+int tpref_tr_apply_k(const tpref_mesh_cfg* c, const double* U, double* out, int32_t count) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const std::size_t n = static_cast<std::size_t>(s.op->n_dof());
+    for (int i = 0; i < count; ++i) s.op->apply(U + i * n, out + i * n);
+  });
+}
+
+int tpref_tr_residual(const tpref_mesh_cfg* c, const double* U, double* R, double* norm) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const tpfem::BlockRhs Rb = tpfem::residual(s.problem(), s.state(U), s.F, 1);
+    if (R) std::memcpy(R, Rb.data.data(), Rb.data.size() * sizeof(double));
+    if (norm) *norm = tpfem::block_l2(Rb);
+  });
+}
+
+int tpref_tr_static_init(const tpref_mesh_cfg* c, const tp_solver_cfg* sc, double* U0, int32_t* counts) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    std::vector<int> nc;
+    const tpfem::PeriodicState U = tpfem::static_init(s.problem(), s.F, s.tau, to_ref(sc), &nc);
+    std::memcpy(U0, U.data.data(), U.data.size() * sizeof(double));
+    if (counts)
+      for (std::size_t i = 0; i < nc.size(); ++i) counts[i] = nc[i];
+  });
+}
+
+// runner.hpp:62-66: ranges over every slice of U0, flux_bounds(s_max,
+// flux_samples), choose_nu_hat(mode, bounds, table, &ranges, samples)
+int tpref_tr_choose_nu_hat(const tpref_mesh_cfg* c, const tp_solver_cfg* sc, const double* U0, double* nu_hat,
+                           double* q) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const tpfem::SolverConfig cfg = to_ref(sc);
+    const tpfem::FluxBounds bounds = tpfem::flux_bounds(s.mat, c->s_max, c->flux_samples);
+    tpfem::RegionFieldRanges ranges;
+    const std::size_t n = static_cast<std::size_t>(s.op->n_dof());
+    for (int i = 0; i < s.N; ++i) tpfem::absorb_field_ranges(*s.op, U0 + i * n, ranges);
+    const int samples = sc && sc->nu_hat_samples > 0 ? sc->nu_hat_samples : 2000;
+    const tpfem::NuHatChoice ch = tpfem::choose_nu_hat(cfg.nu_hat_mode, bounds, s.mat, &ranges, samples);
+    for (int r = 0; r < tpfem::kNumRegions; ++r) nu_hat[r] = ch.nu_hat[static_cast<std::size_t>(r)];
+    if (q) *q = ch.q;
+  });
+}
+
+int tpref_tr_periodic_solve(const tpref_mesh_cfg* c, const tp_solver_cfg* sc, const double* nu_hat,
+                            const double* G, double* U) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const tpfem::SolverConfig cfg = to_ref(sc);
+    const auto K = tpfem::assemble_stiffness_frozen(*s.mesh, nu_array(nu_hat));
+    const tpfem::PeriodicSolver ps(s.M, K, s.tau, s.N, tpfem::make_periodic_options(cfg));
+    tpfem::BlockRhs Gb(s.N, s.op->n_dof());
+    std::memcpy(Gb.data.data(), G, Gb.data.size() * sizeof(double));
+    const tpfem::PeriodicState X = ps.solve(Gb);
+    std::memcpy(U, X.data.data(), X.data.size() * sizeof(double));
+  });
+}
+
+// solve_m1_fixed_point(FemSystem, op, F, U0, cfg) as run_transformer_method
+// (runner.hpp:84) calls it; iterates (may be NULL): (cap) x N x n
+int tpref_tr_solve_m1(const tpref_mesh_cfg* c, const tp_solver_cfg* sc, const double* nu_hat, double q,
+                      const double* U0, double* U_out, double* history, int32_t cap, int32_t* iterations,
+                      int32_t* status, double* iterates, double* wall) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const tpfem::SolverConfig cfg = to_ref(sc);
+    const auto K = tpfem::assemble_stiffness_frozen(*s.mesh, nu_array(nu_hat));
+    std::vector<tpfem::PeriodicState> log;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [U, rep] = tpfem::solve_m1_fixed_point(s.problem(), K, s.F, s.state(U0), cfg, q,
+                                                iterates ? &log : nullptr);
+    if (wall) *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
+    for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)
+      history[k] = rep.residual_history[k];
+    if (iterations) *iterations = rep.iterations;
+    if (status) *status = static_cast<int32_t>(rep.status);
+    if (iterates) {
+      const std::size_t sz = U.data.size();
+      for (std::size_t k = 0; k < log.size() && static_cast<int>(k) < cap; ++k)
+        std::memcpy(iterates + k * sz, log[k].data.data(), sz * sizeof(double));
+    }
   });
 }
 

@@ -451,10 +451,9 @@ struct FftPlan {
   size_t ssmem = 0, fsmem = 0;  // inverse (+ staged half spectrum) / forward
 };
 
-FftPlan& plan_for(Problem& p) {
-  if (p.fft_plan) return *static_cast<FftPlan*>(p.fft_plan.get());
+FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
+  if (slot) return *static_cast<FftPlan*>(slot.get());
   auto pl = std::make_shared<FftPlan>();
-  const int N = p.N;
   pl->N = N;
   pl->pow2 = (N & (N - 1)) == 0;
   while ((1 << pl->bits) < N) ++pl->bits;
@@ -499,54 +498,75 @@ FftPlan& plan_for(Problem& p) {
       TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
     }
   }
-  p.fft_plan = pl;
+  slot = pl;
   return *pl;
+}
+
+void launched(const DftCtx& c) {
+  if (c.launches) ++*c.launches;
+  const cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) throw_cuda(e, "kernel launch", __FILE__, __LINE__);
 }
 
 }  // namespace
 
-int rdft_forward_blocks(Problem& p) {
-  FftPlan& pl = plan_for(p);
-  const size_t n = (size_t)p.sh.nr;
+int dft_forward_blocks(const DftCtx& c) {
+  FftPlan& pl = plan_for(*c.plan, c.N);
   const int C = 2 * (pl.stockham ? pl.sP : pl.P);
-  return (int)((n + C - 1) / C);
+  return (int)((c.n + C - 1) / C);
 }
 
-void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat, double* sq) {
-  FftPlan& pl = plan_for(p);
-  const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
-  const int blocks = rdft_forward_blocks(p);
+void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
+  FftPlan& pl = plan_for(*c.plan, c.N);
+  const int blocks = dft_forward_blocks(c);
   if (pl.stockham) {
-    k_sfft_forward<<<blocks, pl.sT, pl.fsmem, p.stream>>>(G, Ghat, n, pl.N, pl.sP, pl.tw.get(), sq);
+    k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq);
   } else {
-    k_rdft_forward<<<blocks, 256, pl.smem, p.stream>>>(G, Ghat, n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
+    k_rdft_forward<<<blocks, 256, pl.smem, c.stream>>>(G, Ghat, c.n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
                                                        sq);
   }
-  TP_LAUNCHED(&p);
+  launched(c);
+}
+
+void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, double* im2) {
+  FftPlan& pl = plan_for(*c.plan, c.N);
+  const int C = 2 * (pl.stockham ? pl.siP : pl.P);
+  const int blocks = (int)((c.n + C - 1) / C);
+  c.part->ensure((size_t)2 * blocks);
+  c.red->ensure(16);
+  if (pl.stockham) {
+    k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.N, pl.siP, pl.tw.get(),
+                                                            c.part->get());
+  } else {
+    k_rdft_inverse<<<blocks, 256, pl.smem, c.stream>>>(Uhat, U, c.n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
+                                                       c.part->get());
+  }
+  launched(c);
+  k_reduce_pairs<<<1, 1024, 0, c.stream>>>(c.part->get(), blocks, c.red->get());
+  launched(c);
+  if (re2 || im2) {
+    TP_CUDA(cudaMemcpyAsync(c.h_scalars, c.red->get(), 2 * sizeof(double), cudaMemcpyDeviceToHost, c.stream));
+    TP_CUDA(cudaStreamSynchronize(c.stream));
+    if (re2) *re2 = c.h_scalars[0];
+    if (im2) *im2 = c.h_scalars[1];
+  }
+}
+
+namespace {
+DftCtx ctx_of(Problem& p) {
+  // columns of this rank's strip
+  return DftCtx{p.N, (size_t)p.sh.nr, p.stream, &p.fft_plan, &p.part, &p.red, p.h_scalars, &p.launches};
+}
+}  // namespace
+
+int rdft_forward_blocks(Problem& p) { return dft_forward_blocks(ctx_of(p)); }
+
+void launch_rdft_forward(Problem& p, const double* G, cplx* Ghat, double* sq) {
+  dft_forward(ctx_of(p), G, Ghat, sq);
 }
 
 void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2) {
-  FftPlan& pl = plan_for(p);
-  const size_t n = (size_t)p.sh.nr;  // columns of this rank's strip
-  const int C = 2 * (pl.stockham ? pl.siP : pl.P);
-  const int blocks = (int)((n + C - 1) / C);
-  p.part.ensure((size_t)2 * blocks);
-  p.red.ensure(16);
-  if (pl.stockham) {
-    k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, p.stream>>>(Uhat, U, n, pl.N, pl.siP, pl.tw.get(), p.part.get());
-  } else {
-    k_rdft_inverse<<<blocks, 256, pl.smem, p.stream>>>(Uhat, U, n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
-                                                       p.part.get());
-  }
-  TP_LAUNCHED(&p);
-  k_reduce_pairs<<<1, 1024, 0, p.stream>>>(p.part.get(), blocks, p.red.get());
-  TP_LAUNCHED(&p);
-  if (re2 || im2) {
-    TP_CUDA(cudaMemcpyAsync(p.h_scalars, p.red.get(), 2 * sizeof(double), cudaMemcpyDeviceToHost, p.stream));
-    TP_CUDA(cudaStreamSynchronize(p.stream));
-    if (re2) *re2 = p.h_scalars[0];
-    if (im2) *im2 = p.h_scalars[1];
-  }
+  dft_inverse(ctx_of(p), Uhat, U, re2, im2);
 }
 
 }  // namespace tpgpu

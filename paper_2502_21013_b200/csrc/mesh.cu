@@ -1,0 +1,1513 @@
+// General-mesh path: the reference's own P1 meshes and
+// transformer physics through the same fixed-point sweep.  C ABI in
+// include/tpgpu_mesh.h.
+//
+// Reference pieces restated here (file:line in /root/reference/proj/include/tpfem):
+//   mesher          build_rectilinear_mesh, grid_lines, refine_uniform,
+//                   finalize_mesh, transformer_regions   mesh.hpp:86-246
+//   materials       nu, nu_prime, capped_exp, transformer(),
+//                   flux_jacobian_bounds, flux_bounds     materials.hpp:42-155
+//   element data    compute_element_data                  assembly.hpp:28-46
+//   assembly        assemble_mass / _stiffness_frozen /
+//                   _loads (triplets summed in (row, col,
+//                   value-bit) order, sparse.hpp:49-82)   assembly.hpp:48-106
+//   operator        NonlinearOperator::apply / jacobian   assembly.hpp:126-177
+//   nu_hat          absorb_field_ranges, choose_nu_hat    assembly.hpp:236-303
+//   methods         residual, static_init/newton_elliptic,
+//                   PeriodicSolver::solve, solve_m1       periodic.hpp:35-198,
+//                                                         solvers.hpp:131-182,276-369
+//
+// Device layout: U, G, F slice-major N x n (the reference's PeriodicState);
+// half spectrum frequency-major (N/2+1) x n complex; per-element data SoA;
+// the operators on one CSR pattern (all dof pairs sharing a triangle).  The
+// linear blocks -- lambda_k M + K_hat per frequency, the Newton Jacobians
+// per slice -- are factorised once by a banded LDL^T (complex symmetric: no
+// conjugation, like the reference's block factorisations, periodic.hpp:124)
+// in a reverse-Cuthill-McKee order and solved directly, one warp per block.
+#include <algorithm>
+#include <array>
+#include <chrono>
+#include <cmath>
+#include <cstdint>
+#include <cstring>
+#include <deque>
+#include <limits>
+#include <numbers>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "../../include/tpgpu_mesh.h"
+#include "tp_internal.cuh"
+
+namespace tpgpu {
+
+namespace {
+
+constexpr int kRegions = TP_MAX_MATERIALS;
+
+// ================================================================= host mesher
+struct HostMesh {
+  std::vector<double> xy;  // 2 per vertex
+  std::vector<int> tri;    // 3 per triangle
+  std::vector<int> reg;    // per triangle
+  double x0 = 0, x1 = 0, y0 = 0, y1 = 0;
+};
+
+struct Rect {
+  double x0, y0, x1, y1;
+  int label;
+};
+
+// transformer_regions (mesh.hpp:231-244): painter's order, first entry last
+const Rect kTransformer[] = {
+    {0.000, 0.000, 0.355, 0.466, 0}, {0.010, 0.010, 0.345, 0.456, 2}, {0.060, 0.028, 0.295, 0.438, 1},
+    {0.140, 0.108, 0.215, 0.358, 2}, {0.028, 0.123, 0.041, 0.343, 4}, {0.159, 0.123, 0.172, 0.343, 3},
+    {0.183, 0.123, 0.196, 0.343, 4}, {0.314, 0.123, 0.327, 0.343, 3},
+};
+
+// grid_lines (mesh.hpp:105-131): every rectangle edge is a line; gaps are cut
+// into equal pieces no longer than (hi - lo) / target
+std::vector<double> snapped_lines(double lo, double hi, std::vector<double> edges, int target) {
+  edges.push_back(lo);
+  edges.push_back(hi);
+  std::sort(edges.begin(), edges.end());
+  const double tol = 1e-12 * (hi - lo);
+  std::vector<double> br;
+  for (const double e : edges) {
+    require(e >= lo - tol && e <= hi + tol, "mesh: region rectangle outside the domain");
+    if (br.empty() || e - br.back() > tol) br.push_back(e);
+  }
+  br.front() = lo;
+  br.back() = hi;
+  const double h = (hi - lo) / target;
+  std::vector<double> out{lo};
+  for (size_t g = 0; g + 1 < br.size(); ++g) {
+    const double a = br[g], b = br[g + 1];
+    const int pieces = std::max(1, (int)std::ceil((b - a) / h - 1e-9));
+    for (int q = 1; q < pieces; ++q) out.push_back(a + (b - a) * q / pieces);
+    out.push_back(b);
+  }
+  return out;
+}
+
+// build_rectilinear_mesh (mesh.hpp:139-190)
+HostMesh rectilinear(const Rect* rects, int nr, int nx, int ny) {
+  require(nr > 0, "mesh: no regions given");
+  require(nx >= 1 && ny >= 1, "mesh: cell counts must be positive");
+  HostMesh m;
+  m.x0 = m.x1 = rects[0].x0;
+  m.y0 = m.y1 = rects[0].y0;
+  std::vector<double> ex, ey;
+  for (int r = 0; r < nr; ++r) {
+    const Rect& q = rects[r];
+    require(q.x0 < q.x1 && q.y0 < q.y1, "mesh: degenerate region rectangle");
+    m.x0 = std::min(m.x0, q.x0);
+    m.x1 = std::max(m.x1, q.x1);
+    m.y0 = std::min(m.y0, q.y0);
+    m.y1 = std::max(m.y1, q.y1);
+    ex.insert(ex.end(), {q.x0, q.x1});
+    ey.insert(ey.end(), {q.y0, q.y1});
+  }
+  const std::vector<double> gx = snapped_lines(m.x0, m.x1, ex, nx);
+  const std::vector<double> gy = snapped_lines(m.y0, m.y1, ey, ny);
+  const int cols = (int)gx.size();
+  for (const double y : gy)
+    for (const double x : gx) m.xy.insert(m.xy.end(), {x, y});
+  for (size_t j = 0; j + 1 < gy.size(); ++j)
+    for (size_t i = 0; i + 1 < gx.size(); ++i) {
+      const double cx = 0.5 * (gx[i] + gx[i + 1]), cy = 0.5 * (gy[j] + gy[j + 1]);
+      int label = -1;
+      for (int r = 0; r < nr; ++r)
+        if (cx >= rects[r].x0 && cx <= rects[r].x1 && cy >= rects[r].y0 && cy <= rects[r].y1) label = rects[r].label;
+      require(label >= 0, "mesh: cell centroid (" + std::to_string(cx) + ", " + std::to_string(cy) +
+                              ") not covered by any region");
+      const int a = (int)j * cols + (int)i, b = a + 1, d = a + cols, c = d + 1;
+      m.tri.insert(m.tri.end(), {a, b, c, a, c, d});
+      m.reg.insert(m.reg.end(), {label, label});
+    }
+  return m;
+}
+
+// refine_uniform (mesh.hpp:192-228): four children per triangle, midpoints
+// numbered in order of first use
+HostMesh refine(const HostMesh& m) {
+  HostMesh f;
+  f.x0 = m.x0;
+  f.x1 = m.x1;
+  f.y0 = m.y0;
+  f.y1 = m.y1;
+  f.xy = m.xy;
+  std::unordered_map<uint64_t, int> mids;
+  mids.reserve(m.tri.size());
+  auto mid = [&](int a, int b) {
+    const uint64_t key = ((uint64_t)std::min(a, b) << 32) | (uint64_t)std::max(a, b);
+    const auto it = mids.find(key);
+    if (it != mids.end()) return it->second;
+    const int v = (int)(f.xy.size() / 2);
+    f.xy.push_back(0.5 * (m.xy[2 * a] + m.xy[2 * b]));
+    f.xy.push_back(0.5 * (m.xy[2 * a + 1] + m.xy[2 * b + 1]));
+    mids.emplace(key, v);
+    return v;
+  };
+  const size_t nt = m.reg.size();
+  for (size_t t = 0; t < nt; ++t) {
+    const int p0 = m.tri[3 * t], p1 = m.tri[3 * t + 1], p2 = m.tri[3 * t + 2];
+    const int a = mid(p0, p1), b = mid(p1, p2), c = mid(p2, p0);
+    f.tri.insert(f.tri.end(), {p0, a, c, a, p1, b, c, b, p2, a, b, c});
+    f.reg.insert(f.reg.end(), 4, m.reg[t]);
+  }
+  return f;
+}
+
+// ================================================================= materials
+// nu(s) = a min{exp(b s^2), c} + d (materials.hpp:42-57); logc = std::log(c)
+// computed once on the host
+struct MatExp {
+  double a, b, c, d, logc, sigma, j_amp;
+  int konst;  // a == 0
+};
+
+__host__ __device__ inline double capped_exp(const MatExp& m, double s) {
+  const double e = m.b * s * s;
+  return e >= m.logc ? m.c : exp(e);
+}
+__host__ __device__ inline double nu_of(const MatExp& m, double s) { return m.konst ? m.d : m.a * capped_exp(m, s) + m.d; }
+__host__ __device__ inline double nu_prime_of(const MatExp& m, double s) {
+  if (m.konst) return 0.0;
+  const double e = capped_exp(m, s);
+  if (e >= m.c) return 0.0;
+  return 2.0 * m.a * m.b * s * e;
+}
+
+// flux_jacobian_bounds (materials.hpp:103-120): sampled eigenvalue range of
+// nu(s) I + (nu'(s)/s) g g^T on [lo, hi]
+void flux_range(const MatExp& m, double lo, double hi, int samples, double* lam, double* Lam) {
+  require(lo >= 0 && hi >= lo, "flux bounds: need 0 <= s_lo <= s_hi");
+  require(samples >= 2, "flux bounds: need at least 2 samples");
+  double l = std::numeric_limits<double>::infinity(), L = 0;
+  for (int j = 0; j < samples; ++j) {
+    const double s = lo + (hi - lo) * j / (samples - 1);
+    const double nu = nu_of(m, s);
+    const double gp = nu + nu_prime_of(m, s) * s;
+    l = std::min({l, nu, gp});
+    L = std::max({L, nu, gp});
+  }
+  *lam = l;
+  *Lam = L;
+}
+
+// ================================================================= kernels
+__device__ __forceinline__ double dm(double a, double b) { return __dmul_rn(a, b); }
+__device__ __forceinline__ double da(double a, double b) { return __dadd_rn(a, b); }
+
+struct ElemDev {
+  const int* dof;  // 3 per triangle, -1 on the boundary
+  const double *gx, *gy, *area;
+  const int* reg;
+  int nt;
+};
+
+// per (slice, triangle): grad u, |grad u|, nu, nu'/|grad u| (the reference's
+// gradient loop and hypot, assembly.hpp:130-137, 158-166; unfused products so
+// the element values match the host arithmetic)
+__global__ void k_elem_eval(ElemDev e, const MatExp* __restrict__ mat, const double* __restrict__ U, size_t n,
+                            const int* __restrict__ slices, double4* __restrict__ out, double* __restrict__ smag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= e.nt) return;
+  const int sl = slices ? slices[blockIdx.y] : (int)blockIdx.y;
+  const double* u = U + (size_t)sl * n;
+  double gx = 0, gy = 0;
+#pragma unroll
+  for (int k = 0; k < 3; ++k) {
+    const int d = e.dof[3 * t + k];
+    if (d < 0) continue;
+    const double v = u[d];
+    gx = da(gx, dm(v, e.gx[3 * t + k]));
+    gy = da(gy, dm(v, e.gy[3 * t + k]));
+  }
+  const double s = hypot(gx, gy);
+  const MatExp m = mat[e.reg[t]];
+  const double nu = nu_of(m, s);
+  const double r1 = s > 0 ? nu_prime_of(m, s) / s : 0.0;
+  out[(size_t)blockIdx.y * e.nt + t] = make_double4(nu, r1, gx, gy);
+  if (smag) smag[(size_t)blockIdx.y * e.nt + t] = s;
+}
+
+// K(u) at dof j from its incident triangles in ascending order (the reference
+// scatters in element order: the same sums, assembly.hpp:138-139)
+__device__ __forceinline__ double k_at(const ElemDev& e, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                                       const int* __restrict__ inc, int j) {
+  double acc = 0;
+  for (int q = iptr[j]; q < iptr[j + 1]; ++q) {
+    const int t = inc[q] >> 2, k = inc[q] & 3;
+    const double4 v = ev[t];
+    const double dot = da(dm(v.z, e.gx[3 * t + k]), dm(v.w, e.gy[3 * t + k]));
+    acc = da(acc, dm(dm(v.x, e.area[t]), dot));
+  }
+  return acc;
+}
+
+struct Csr {
+  const int *ptr, *col;
+  const double *m, *k;  // mass, K_hat on the same pattern
+};
+
+// R = F - M(u^i - u^{i-1})/tau - K(u^i), G = F + K_hat u^i - K(u^i)
+// (residual, periodic.hpp:43-57; M1 RHS, solvers.hpp:326-336), per-block r^2
+__global__ void k_resid_rhs(ElemDev e, Csr A, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                            const int* __restrict__ inc, const double* __restrict__ U, const double* __restrict__ F,
+                            double* __restrict__ R, double* __restrict__ G, double* __restrict__ part, int n, int N,
+                            double tau) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  double r2 = 0;
+  if (j < n) {
+    const double* u = U + (size_t)i * n;
+    const double* up = U + (size_t)((i + N - 1) % N) * n;
+    const double ku = k_at(e, ev + (size_t)i * e.nt, iptr, inc, j);
+    double mdu = 0, khu = 0;
+    for (int q = A.ptr[j]; q < A.ptr[j + 1]; ++q) {
+      const int c = A.col[q];
+      mdu = da(mdu, dm(A.m[q], (u[c] - up[c]) / tau));
+      if (G) khu = da(khu, dm(A.k[q], u[c]));
+    }
+    const double f = F[(size_t)i * n + j];
+    const double r = f - mdu - ku;
+    if (R) R[(size_t)i * n + j] = r;
+    if (G) G[(size_t)i * n + j] = f + khu - ku;
+    r2 = r * r;
+  }
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
+    part[(size_t)blockIdx.y * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// out = K(u) per slice
+__global__ void k_apply(ElemDev e, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                        const int* __restrict__ inc, double* __restrict__ out, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  out[(size_t)blockIdx.y * n + j] = k_at(e, ev + (size_t)blockIdx.y * e.nt, iptr, inc, j);
+}
+
+// Newton residual r = rhs - K(v) per batch slot b (newton_elliptic's
+// residual_at with mass_scale 0, solvers.hpp:141-148), per-block r^2
+__global__ void k_newton_res(ElemDev e, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                             const int* __restrict__ inc, const double* __restrict__ F,
+                             const int* __restrict__ slices, double* __restrict__ R, double* __restrict__ part,
+                             int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  double r2 = 0;
+  if (j < n) {
+    const double r = F[(size_t)slices[b] * n + j] - k_at(e, ev + (size_t)b * e.nt, iptr, inc, j);
+    R[(size_t)b * n + j] = r;
+    r2 = r * r;
+  }
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
+    part[(size_t)b * gridDim.x + blockIdx.x] = s;
+  }
+}
+
+// fixed-order sums of `per` partials per row (one warp per row)
+__global__ void k_sum_rows(const double* __restrict__ part, int per, int rows, double* __restrict__ out) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  double s = 0;
+  for (int q = threadIdx.x & 31; q < per; q += 32) s += part[(size_t)r * per + q];
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if ((threadIdx.x & 31) == 0) out[r] = s;
+}
+
+// trial = u + alpha_b delta (active slots only)
+__global__ void k_axpy_slots(const double* __restrict__ u, const double* __restrict__ dlt,
+                             const double* __restrict__ alpha, const int* __restrict__ on, double* __restrict__ trial,
+                             int n) {
+  const int b = blockIdx.y;
+  if (!on[b]) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) trial[(size_t)b * n + j] = u[(size_t)b * n + j] + alpha[b] * dlt[(size_t)b * n + j];
+}
+
+// accepted slots: u <- trial, r <- rtrial
+__global__ void k_accept_slots(double* __restrict__ u, double* __restrict__ r, const double* __restrict__ t,
+                               const double* __restrict__ rt, const int* __restrict__ acc, int n) {
+  const int b = blockIdx.y;
+  if (!acc[b]) return;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) {
+    u[(size_t)b * n + j] = t[(size_t)b * n + j];
+    r[(size_t)b * n + j] = rt[(size_t)b * n + j];
+  }
+}
+
+// per-block, per-region min / max of |grad u| (absorb_field_ranges, assembly.hpp:236-245)
+__global__ void k_field_ranges(const double* __restrict__ smag, const int* __restrict__ reg, int nt, size_t total,
+                               double* __restrict__ part) {
+  double lo[kRegions], hi[kRegions];
+  for (int r = 0; r < kRegions; ++r) {
+    lo[r] = INFINITY;
+    hi[r] = -1.0;
+  }
+  for (size_t q = (size_t)blockIdx.x * blockDim.x + threadIdx.x; q < total; q += (size_t)gridDim.x * blockDim.x) {
+    const int r = reg[q % nt];
+    const double s = smag[q];
+    lo[r] = fmin(lo[r], s);
+    hi[r] = fmax(hi[r], s);
+  }
+  __shared__ double sl[kRegions][32], sh[kRegions][32];
+  for (int r = 0; r < kRegions; ++r) {
+    double a = lo[r], b = hi[r];
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmin(a, __shfl_xor_sync(0xffffffffu, a, o));
+      b = fmax(b, __shfl_xor_sync(0xffffffffu, b, o));
+    }
+    if ((threadIdx.x & 31) == 0) {
+      sl[r][threadIdx.x >> 5] = a;
+      sh[r][threadIdx.x >> 5] = b;
+    }
+  }
+  __syncthreads();
+  if (threadIdx.x < kRegions) {
+    const int r = threadIdx.x;
+    double a = INFINITY, b = -1.0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      a = fmin(a, sl[r][w]);
+      b = fmax(b, sh[r][w]);
+    }
+    part[(size_t)blockIdx.x * 2 * kRegions + r] = a;
+    part[(size_t)blockIdx.x * 2 * kRegions + kRegions + r] = b;
+  }
+}
+
+// ---- banded LDL^T.  Band row p holds columns p-bw .. p (diagonal at offset bw).
+template <class T>
+__device__ __forceinline__ T tz() { return T{}; }
+__device__ __forceinline__ double mulv(double a, double b) { return a * b; }
+__device__ __forceinline__ cplx mulv(cplx a, cplx b) { return a * b; }
+__device__ __forceinline__ double divv(double a, double b) { return a / b; }
+__device__ __forceinline__ cplx divv(cplx a, cplx b) { return cdiv(a, b); }
+__device__ __forceinline__ bool is_zero(double a) { return a == 0.0; }
+__device__ __forceinline__ bool is_zero(cplx a) { return a.re == 0.0 && a.im == 0.0; }
+__device__ __forceinline__ double shx(double v, int o) { return __shfl_xor_sync(0xffffffffu, v, o); }
+__device__ __forceinline__ cplx shx(cplx v, int o) { return {shx(v.re, o), shx(v.im, o)}; }
+
+// frequency blocks lambda_k M + K_hat in band form (periodic.hpp:203-209 /
+// add_scaled, sparse.hpp:162-181), lower triangle of the RCM-ordered matrix
+__global__ void k_band_freq(Csr A, const int* __restrict__ perm, const int* __restrict__ iperm,
+                            const cplx* __restrict__ lam, cplx* __restrict__ band, int n, int bw) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  const int k = blockIdx.y;
+  cplx* row = band + ((size_t)k * n + p) * (bw + 1);
+  for (int q = 0; q <= bw; ++q) row[q] = cplx{0, 0};
+  const int j = perm[p];
+  const cplx l = lam[k];
+  for (int q = A.ptr[j]; q < A.ptr[j + 1]; ++q) {
+    const int pc = iperm[A.col[q]];
+    if (pc > p) continue;
+    const cplx v = cplx{l.re * A.m[q], l.im * A.m[q]} + cplx{A.k[q], 0.0};
+    row[pc - p + bw] = v;
+  }
+}
+
+// Newton Jacobians J(u) per slot in band form: element blocks
+// area (nu I + (nu'/s) g g^T) (assembly.hpp:153-177), gathered row by row
+// from the incident triangles in ascending order
+__global__ void k_band_jac(ElemDev e, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                           const int* __restrict__ inc, const int* __restrict__ perm, const int* __restrict__ iperm,
+                           const int* __restrict__ on, double* __restrict__ band, int n, int bw) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (p >= n || !on[b]) return;
+  double* row = band + ((size_t)b * n + p) * (bw + 1);
+  for (int q = 0; q <= bw; ++q) row[q] = 0.0;
+  const int j = perm[p];
+  const double4* evb = ev + (size_t)b * e.nt;
+  for (int q = iptr[j]; q < iptr[j + 1]; ++q) {
+    const int t = inc[q] >> 2, i = inc[q] & 3;
+    const double4 v = evb[t];
+    const double gxi = e.gx[3 * t + i], gyi = e.gy[3 * t + i];
+    const double di = v.z * gxi + v.w * gyi;
+    for (int c = 0; c < 3; ++c) {
+      const int dc = e.dof[3 * t + c];
+      if (dc < 0) continue;
+      const int pc = iperm[dc];
+      if (pc > p) continue;
+      const double gxc = e.gx[3 * t + c], gyc = e.gy[3 * t + c];
+      const double iso = v.x * (gxi * gxc + gyi * gyc);
+      const double dir = v.y * di * (v.z * gxc + v.w * gyc);
+      row[pc - p + bw] += e.area[t] * (iso + dir);
+    }
+  }
+}
+
+// right-looking band LDL^T of one block per CTA: column c's multipliers
+// l_i = a_ic / d_c, then the trailing triangle a_ik -= l_i a_kc (c < k <= i <= c+bw);
+// a zero pivot sets *fail
+template <class T>
+__global__ void __launch_bounds__(512) k_band_factor(T* __restrict__ band, int n, int bw, const int* __restrict__ on,
+                                                     int* __restrict__ fail) {
+  const int b = blockIdx.x;
+  if (on && !on[b]) return;
+  T* A = band + (size_t)b * n * (bw + 1);
+  extern __shared__ __align__(16) unsigned char bsm[];
+  T* col = reinterpret_cast<T*>(bsm);  // bw entries: a_{c+1..c+bw, c}
+  __shared__ int bad;
+  if (threadIdx.x == 0) bad = 0;
+  __syncthreads();
+  const int W = bw + 1;
+  for (int c = 0; c < n; ++c) {
+    const T d = A[(size_t)c * W + bw];
+    const int len = min(bw, n - 1 - c);
+    for (int a = threadIdx.x; a < len; a += blockDim.x) col[a] = A[(size_t)(c + 1 + a) * W + bw - 1 - a];
+    if (threadIdx.x == 0 && is_zero(d)) bad = 1;
+    __syncthreads();
+    if (bad) break;
+    // trailing update: row i = c+1+a, column k = c+1+q, q <= a
+    for (int idx = threadIdx.x; idx < len * len; idx += blockDim.x) {
+      const int a = idx / len, q = idx - a * len;
+      if (q > a) continue;
+      const T li = divv(col[a], d);
+      T& x = A[(size_t)(c + 1 + a) * W + bw - (a - q)];
+      x = x - mulv(li, col[q]);
+    }
+    __syncthreads();
+    for (int a = threadIdx.x; a < len; a += blockDim.x) A[(size_t)(c + 1 + a) * W + bw - 1 - a] = divv(col[a], d);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0 && bad) atomicExch(fail, 1);
+}
+
+// x = (L D L^T)^-1 b for one block per warp.  gather: b from src[perm[p]]
+// (frequency-major spectrum or slot vector), scatter x to dst[perm[p]].
+// Forward rows are dot products over the contiguous band row; the backward
+// pass is column-oriented (row p of L updates the bw unknowns above it).
+template <class T>
+__global__ void k_band_solve(const T* __restrict__ band, const T* __restrict__ src, T* __restrict__ dst,
+                             const int* __restrict__ perm, int n, int bw, const int* __restrict__ on,
+                             T* __restrict__ gscratch) {
+  const int b = blockIdx.x;
+  if (on && !on[b]) return;
+  extern __shared__ __align__(16) unsigned char ssm[];
+  T* y = gscratch ? gscratch + (size_t)b * n : reinterpret_cast<T*>(ssm);
+  const T* A = band + (size_t)b * n * (bw + 1);
+  const T* s = src + (size_t)b * n;
+  const int lane = threadIdx.x;
+  const int W = bw + 1;
+  for (int p = lane; p < n; p += 32) y[p] = s[perm[p]];
+  __syncwarp();
+  // forward: y_p -= sum_{c < p} L_pc y_c
+  for (int p = 1; p < n; ++p) {
+    const int c0 = max(0, p - bw);
+    T acc = tz<T>();
+    for (int c = c0 + lane; c < p; c += 32) acc = acc + mulv(A[(size_t)p * W + bw - (p - c)], y[c]);
+    for (int o = 16; o > 0; o >>= 1) acc = acc + shx(acc, o);
+    if (lane == 0) y[p] = y[p] - acc;
+    __syncwarp();
+  }
+  // diagonal
+  for (int p = lane; p < n; p += 32) y[p] = divv(y[p], A[(size_t)p * W + bw]);
+  __syncwarp();
+  // backward: x_p final once every row below has been applied
+  for (int p = n - 1; p > 0; --p) {
+    const T xp = y[p];
+    const int c0 = max(0, p - bw);
+    for (int c = c0 + lane; c < p; c += 32) y[c] = y[c] - mulv(A[(size_t)p * W + bw - (p - c)], xp);
+    __syncwarp();
+  }
+  T* d = dst + (size_t)b * n;
+  for (int p = lane; p < n; p += 32) d[perm[p]] = y[p];
+}
+
+// per-frequency residual check of the block solves (SparseSolver::solve's
+// re-multiplication, solve.hpp:79-89): |b - (lambda M + K_hat) x|^2 and |b|^2
+__global__ void k_freq_check(Csr A, const cplx* __restrict__ lam, const cplx* __restrict__ X,
+                             const cplx* __restrict__ B, double* __restrict__ part, int n) {
+  const int k = blockIdx.y;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double r2 = 0, b2 = 0;
+  if (j < n) {
+    const cplx* x = X + (size_t)k * n;
+    const cplx l = lam[k];
+    cplx acc{0, 0};
+    for (int q = A.ptr[j]; q < A.ptr[j + 1]; ++q) {
+      const cplx v = cplx{l.re * A.m[q] + A.k[q], l.im * A.m[q]};
+      acc = acc + v * x[A.col[q]];
+    }
+    const cplx bb = B[(size_t)k * n + j];
+    const cplx r = bb - acc;
+    r2 = norm2(r);
+    b2 = norm2(bb);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    r2 += __shfl_down_sync(0xffffffffu, r2, o);
+    b2 += __shfl_down_sync(0xffffffffu, b2, o);
+  }
+  __shared__ double w1[32], w2[32];
+  if ((threadIdx.x & 31) == 0) {
+    w1[threadIdx.x >> 5] = r2;
+    w2[threadIdx.x >> 5] = b2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s1 = 0, s2 = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) {
+      s1 += w1[w];
+      s2 += w2[w];
+    }
+    part[((size_t)k * gridDim.x + blockIdx.x) * 2] = s1;
+    part[((size_t)k * gridDim.x + blockIdx.x) * 2 + 1] = s2;
+  }
+}
+
+// sums of (r^2, b^2) pairs per frequency
+__global__ void k_sum_pairs_rows(const double* __restrict__ part, int per, int rows, double* __restrict__ out) {
+  const int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (r >= rows) return;
+  double a = 0, c = 0;
+  for (int q = threadIdx.x & 31; q < per; q += 32) {
+    a += part[((size_t)r * per + q) * 2];
+    c += part[((size_t)r * per + q) * 2 + 1];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, o);
+    c += __shfl_xor_sync(0xffffffffu, c, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    out[2 * r] = a;
+    out[2 * r + 1] = c;
+  }
+}
+
+// triplets summed like SparseMatrix::from_triplets (sparse.hpp:49-82): sorted
+// by (row, col, value bits), duplicates added in that order
+struct Trip {
+  int r, c;
+  double v;
+};
+void sum_triplets(std::vector<Trip>& t, const std::vector<int>& ptr, const std::vector<int>& col,
+                  std::vector<double>& out) {
+  std::sort(t.begin(), t.end(), [](const Trip& a, const Trip& b) {
+    if (a.r != b.r) return a.r < b.r;
+    if (a.c != b.c) return a.c < b.c;
+    uint64_t x, y;
+    std::memcpy(&x, &a.v, 8);
+    std::memcpy(&y, &b.v, 8);
+    return x < y;
+  });
+  out.assign(col.size(), 0.0);
+  size_t i = 0;
+  while (i < t.size()) {
+    double s = 0;
+    size_t j = i;
+    while (j < t.size() && t[j].r == t[i].r && t[j].c == t[i].c) s += t[j++].v;
+    const int r = t[i].r;
+    const auto it = std::lower_bound(col.begin() + ptr[r], col.begin() + ptr[r + 1], t[i].c);
+    out[(size_t)(it - col.begin())] = s;
+    i = j;
+  }
+}
+
+}  // namespace
+
+// ================================================================= problem
+class MeshProblem {
+ public:
+  MeshProblem(const tp_mesh_desc& d, int dev);
+  ~MeshProblem();
+
+  int device = 0, n = 0, N = 0, K = 0, nt = 0, nv = 0, bw = 0;
+  double tau = 0, T = 0, s_max = 3.0;
+  int flux_samples = 10001;
+  MatExp mat[kRegions];
+  std::vector<int> edof, ereg, iptr, inc, rptr, rcol, perm, iperm;
+  std::vector<double> egx, egy, earea, mval;
+  bool region_present[kRegions] = {};
+  double nu_hat[kRegions] = {};
+  double q_estimate = 0;
+  bool nu_hat_set = false, state_valid = false, factored = false;
+
+  cudaStream_t stream = nullptr;
+  std::atomic<int64_t> launches{0};
+  std::shared_ptr<void> fft_plan;
+  double* h_scalars = nullptr;
+  DevBuf<double> part, red, part2, red2;
+  DevBuf<int> d_edof, d_ereg, d_iptr, d_inc, d_rptr, d_rcol, d_perm, d_iperm, d_fail;
+  DevBuf<double> d_egx, d_egy, d_earea, d_mval, d_kval, F, U, G, R;
+  DevBuf<MatExp> d_mat;
+  DevBuf<double4> ev;
+  DevBuf<cplx> Ghat, Uhat, band, lam;
+
+  ElemDev elem() const { return {d_edof.get(), d_egx.get(), d_egy.get(), d_earea.get(), d_ereg.get(), nt}; }
+  Csr csr() const { return {d_rptr.get(), d_rcol.get(), d_mval.get(), d_kval.get()}; }
+  DftCtx dft() { return DftCtx{N, (size_t)n, stream, &fft_plan, &part2, &red2, h_scalars, &launches}; }
+  void launched() {
+    ++launches;
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) throw_cuda(e, "kernel launch", __FILE__, __LINE__);
+  }
+  void sync() { TP_CUDA(cudaStreamSynchronize(stream)); }
+
+  void eval_elements(const double* Ubase, int count, const int* slices, double* smag = nullptr);
+  double residual_and_rhs(bool want_rhs, bool want_r = false);
+  void apply_k(const double* Ud, double* out, int count);
+  void install_nu_hat(const double* nu, double q);
+  void choose_nu_hat(const tp_solver_cfg& cfg, double* nu, double* q);
+  void static_init(const tp_solver_cfg& cfg, int32_t* counts);
+  void factor_blocks();
+  void periodic_solve(const tp_solver_cfg& cfg);
+};
+
+MeshProblem::MeshProblem(const tp_mesh_desc& d, int dev) : device(dev) {
+  require(d.vertices && d.triangles && d.region, "mesh problem: null mesh arrays");
+  require(d.n_vertices >= 3 && d.n_triangles >= 1, "mesh problem: empty mesh");
+  require(d.steps >= 1, "loads: need at least one time step");
+  require(d.period > 0, "loads: period must be positive");
+  nv = d.n_vertices;
+  nt = d.n_triangles;
+  N = d.steps;
+  K = N / 2 + 1;
+  T = d.period;
+  tau = T / N;
+  if (d.s_max > 0) s_max = d.s_max;
+  if (d.flux_samples > 0) flux_samples = d.flux_samples;
+  for (int r = 0; r < kRegions; ++r) {
+    const tp_exp_material& m = d.material[r];
+    // MaterialTable::set (materials.hpp:30-37)
+    require(m.sigma >= 0, "material table: sigma must be >= 0");
+    require(m.d > 0, "material table: d must be > 0");
+    require(m.a >= 0, "material table: a must be >= 0");
+    require(m.b >= 0, "material table: b must be >= 0");
+    require(m.c > 0, "material table: c must be > 0");
+    mat[r] = MatExp{m.a, m.b, m.c, m.d, std::log(m.c), m.sigma, m.j_amp, m.a == 0 ? 1 : 0};
+  }
+  // finalize_mesh (mesh.hpp:86-103): vertices on the bounding box are Dirichlet
+  double x0 = d.vertices[0], x1 = x0, y0 = d.vertices[1], y1 = y0;
+  for (int v = 0; v < nv; ++v) {
+    x0 = std::min(x0, d.vertices[2 * v]);
+    x1 = std::max(x1, d.vertices[2 * v]);
+    y0 = std::min(y0, d.vertices[2 * v + 1]);
+    y1 = std::max(y1, d.vertices[2 * v + 1]);
+  }
+  const double tol = 1e-12 * std::max(x1 - x0, y1 - y0);
+  std::vector<int> dof_of(nv, -1);
+  for (int v = 0; v < nv; ++v) {
+    const double x = d.vertices[2 * v], y = d.vertices[2 * v + 1];
+    const bool edge = std::abs(x - x0) <= tol || std::abs(x - x1) <= tol || std::abs(y - y0) <= tol ||
+                      std::abs(y - y1) <= tol;
+    if (!edge) dof_of[v] = n++;
+  }
+  require(n > 0, "mesh problem: no free dofs");
+  // compute_element_data (assembly.hpp:28-46)
+  edof.resize(3 * nt);
+  egx.resize(3 * nt);
+  egy.resize(3 * nt);
+  earea.resize(nt);
+  ereg.resize(nt);
+  for (int t = 0; t < nt; ++t) {
+    const int* tv = d.triangles + 3 * t;
+    for (int k = 0; k < 3; ++k) require(tv[k] >= 0 && tv[k] < nv, "mesh problem: triangle vertex out of range");
+    const int rg = d.region[t];
+    require(rg >= 0 && rg < kRegions, "material table: invalid region code " + std::to_string(rg));
+    ereg[t] = rg;
+    region_present[rg] = true;
+    const double* a = d.vertices + 2 * tv[0];
+    const double* b = d.vertices + 2 * tv[1];
+    const double* c = d.vertices + 2 * tv[2];
+    const double area = 0.5 * ((b[0] - a[0]) * (c[1] - a[1]) - (c[0] - a[0]) * (b[1] - a[1]));
+    require(area > 0, "mesh: non-positive triangle area");
+    earea[t] = area;
+    const double inv2A = 1.0 / (2.0 * area);
+    egx[3 * t] = (b[1] - c[1]) * inv2A;
+    egx[3 * t + 1] = (c[1] - a[1]) * inv2A;
+    egx[3 * t + 2] = (a[1] - b[1]) * inv2A;
+    egy[3 * t] = (c[0] - b[0]) * inv2A;
+    egy[3 * t + 1] = (a[0] - c[0]) * inv2A;
+    egy[3 * t + 2] = (b[0] - a[0]) * inv2A;
+    for (int k = 0; k < 3; ++k) edof[3 * t + k] = dof_of[tv[k]];
+  }
+  // incidence lists (dof -> (triangle, corner), ascending triangle) and the
+  // CSR pattern of all dof pairs sharing a triangle
+  iptr.assign(n + 1, 0);
+  for (int t = 0; t < nt; ++t)
+    for (int k = 0; k < 3; ++k)
+      if (edof[3 * t + k] >= 0) ++iptr[edof[3 * t + k] + 1];
+  for (int j = 0; j < n; ++j) iptr[j + 1] += iptr[j];
+  inc.resize(iptr[n]);
+  {
+    std::vector<int> fill(iptr.begin(), iptr.end() - 1);
+    for (int t = 0; t < nt; ++t)
+      for (int k = 0; k < 3; ++k)
+        if (edof[3 * t + k] >= 0) inc[fill[edof[3 * t + k]]++] = t * 4 + k;
+  }
+  std::vector<std::vector<int>> adj(n);
+  for (int t = 0; t < nt; ++t)
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        const int i = edof[3 * t + a], j = edof[3 * t + b];
+        if (i >= 0 && j >= 0) adj[i].push_back(j);
+      }
+  rptr.assign(n + 1, 0);
+  for (int i = 0; i < n; ++i) {
+    std::sort(adj[i].begin(), adj[i].end());
+    adj[i].erase(std::unique(adj[i].begin(), adj[i].end()), adj[i].end());
+    rptr[i + 1] = rptr[i] + (int)adj[i].size();
+  }
+  rcol.reserve(rptr[n]);
+  for (int i = 0; i < n; ++i) rcol.insert(rcol.end(), adj[i].begin(), adj[i].end());
+  // consistent sigma-mass (assemble_mass, assembly.hpp:48-65)
+  {
+    std::vector<Trip> tr;
+    for (int t = 0; t < nt; ++t) {
+      const double sg = mat[ereg[t]].sigma;
+      if (sg == 0) continue;
+      const double sc = sg * earea[t] / 12.0;
+      for (int a = 0; a < 3; ++a)
+        for (int b = 0; b < 3; ++b) {
+          const int i = edof[3 * t + a], j = edof[3 * t + b];
+          if (i >= 0 && j >= 0) tr.push_back({i, j, sc * (a == b ? 2.0 : 1.0)});
+        }
+    }
+    sum_triplets(tr, rptr, rcol, mval);
+  }
+  // reverse Cuthill-McKee from a pseudo-peripheral start (George-Liu), or
+  // the natural order when its bandwidth is no larger
+  {
+    auto band_of = [&](const std::vector<int>& ip) {
+      int w = 0;
+      for (int i = 0; i < n; ++i)
+        for (const int j : adj[i]) w = std::max(w, std::abs(ip[i] - ip[j]));
+      return w;
+    };
+    std::vector<int> deg(n);
+    for (int i = 0; i < n; ++i) deg[i] = (int)adj[i].size();
+    std::vector<int> order;
+    order.reserve(n);
+    std::vector<char> seen(n, 0);
+    std::vector<int> level(n);
+    auto bfs_levels = [&](int s, int& last, int& ecc) {
+      std::fill(level.begin(), level.end(), -1);
+      std::deque<int> qu{s};
+      level[s] = 0;
+      last = s;
+      ecc = 0;
+      while (!qu.empty()) {
+        const int v = qu.front();
+        qu.pop_front();
+        if (level[v] > ecc || (level[v] == ecc && deg[v] < deg[last])) {
+          ecc = level[v];
+          last = v;
+        }
+        for (const int w : adj[v])
+          if (level[w] < 0) {
+            level[w] = level[v] + 1;
+            qu.push_back(w);
+          }
+      }
+    };
+    for (int root = 0; root < n; ++root) {
+      if (seen[root]) continue;
+      // component's min-degree vertex, then peripheral refinement
+      int s = root, last = root, ecc = 0;
+      for (int it = 0; it < 8; ++it) {
+        int l2, e2;
+        bfs_levels(s, l2, e2);
+        if (it > 0 && e2 <= ecc) break;
+        ecc = e2;
+        s = l2;
+      }
+      const size_t first = order.size();
+      order.push_back(s);
+      seen[s] = 1;
+      for (size_t h = first; h < order.size(); ++h) {
+        const int v = order[h];
+        std::vector<int> nb;
+        for (const int w : adj[v])
+          if (!seen[w]) {
+            seen[w] = 1;
+            nb.push_back(w);
+          }
+        std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
+        order.insert(order.end(), nb.begin(), nb.end());
+      }
+      (void)last;
+    }
+    std::reverse(order.begin(), order.end());
+    std::vector<int> ip(n), nat(n);
+    for (int p = 0; p < n; ++p) ip[order[p]] = p;
+    for (int i = 0; i < n; ++i) nat[i] = i;
+    const int brcm = band_of(ip), bnat = band_of(nat);
+    if (bnat <= brcm) {
+      perm = nat;
+      iperm = nat;
+      bw = bnat;
+    } else {
+      perm = order;
+      iperm = ip;
+      bw = brcm;
+    }
+  }
+  // loads (assemble_loads, assembly.hpp:86-106): element order, t^n = (n+1) T / N
+  std::vector<double> hF((size_t)N * n, 0.0);
+  for (int s = 0; s < N; ++s) {
+    const double t = (s + 1) * T / N;
+    double* fs = hF.data() + (size_t)s * n;
+    double jr[kRegions];
+    for (int r = 0; r < kRegions; ++r)
+      jr[r] = mat[r].j_amp == 0 ? 0.0 : mat[r].j_amp * std::cos(2.0 * std::numbers::pi * t / T);
+    for (int e = 0; e < nt; ++e) {
+      const double j = jr[ereg[e]];
+      if (j == 0) continue;
+      const double contrib = j * earea[e] / 3.0;
+      for (int k = 0; k < 3; ++k)
+        if (edof[3 * e + k] >= 0) fs[edof[3 * e + k]] += contrib;
+    }
+  }
+  // device
+  TP_CUDA(cudaSetDevice(device));
+  TP_CUDA(cudaStreamCreateWithFlags(&stream, cudaStreamNonBlocking));
+  TP_CUDA(cudaMallocHost(reinterpret_cast<void**>(&h_scalars), 4096 * sizeof(double)));
+  auto up_i = [&](DevBuf<int>& b, const std::vector<int>& h) {
+    b.alloc(std::max<size_t>(1, h.size()));
+    TP_CUDA(cudaMemcpy(b.get(), h.data(), h.size() * sizeof(int), cudaMemcpyHostToDevice));
+  };
+  auto up_d = [&](DevBuf<double>& b, const std::vector<double>& h) {
+    b.alloc(std::max<size_t>(1, h.size()));
+    TP_CUDA(cudaMemcpy(b.get(), h.data(), h.size() * sizeof(double), cudaMemcpyHostToDevice));
+  };
+  up_i(d_edof, edof);
+  up_i(d_ereg, ereg);
+  up_i(d_iptr, iptr);
+  up_i(d_inc, inc);
+  up_i(d_rptr, rptr);
+  up_i(d_rcol, rcol);
+  up_i(d_perm, perm);
+  up_i(d_iperm, iperm);
+  up_d(d_egx, egx);
+  up_d(d_egy, egy);
+  up_d(d_earea, earea);
+  up_d(d_mval, mval);
+  up_d(F, hF);
+  d_kval.alloc(rcol.size());
+  TP_CUDA(cudaMemset(d_kval.get(), 0, d_kval.bytes()));
+  d_mat.alloc(kRegions);
+  TP_CUDA(cudaMemcpy(d_mat.get(), mat, sizeof(mat), cudaMemcpyHostToDevice));
+  d_fail.alloc(1);
+  U.alloc((size_t)N * n);
+  G.alloc((size_t)N * n);
+  TP_CUDA(cudaMemset(U.get(), 0, U.bytes()));
+}
+
+MeshProblem::~MeshProblem() {
+  cudaSetDevice(device);
+  if (stream) cudaStreamSynchronize(stream);
+  if (h_scalars) cudaFreeHost(h_scalars);
+  if (stream) cudaStreamDestroy(stream);
+}
+
+void MeshProblem::eval_elements(const double* Ubase, int count, const int* slices, double* smag) {
+  ev.ensure((size_t)count * nt);
+  dim3 g((nt + 127) / 128, count);
+  k_elem_eval<<<g, 128, 0, stream>>>(elem(), d_mat.get(), Ubase, (size_t)n, slices, ev.get(), smag);
+  launched();
+}
+
+// ||R|| of the device state U (and G = F + K_hat U - K(U) when asked; R kept
+// in this->R when want_r)
+double MeshProblem::residual_and_rhs(bool want_rhs, bool want_r) {
+  eval_elements(U.get(), N, nullptr);
+  const int nb = (n + 255) / 256;
+  part.ensure((size_t)N * nb);
+  red.ensure(N);
+  if (want_r) R.ensure((size_t)N * n);
+  k_resid_rhs<<<dim3(nb, N), 256, 0, stream>>>(elem(), csr(), ev.get(), d_iptr.get(), d_inc.get(), U.get(), F.get(),
+                                               want_r ? R.get() : nullptr, want_rhs ? G.get() : nullptr, part.get(),
+                                               n, N, tau);
+  launched();
+  k_sum_rows<<<1, 32, 0, stream>>>(part.get(), N * nb, 1, red.get());
+  launched();
+  TP_CUDA(cudaMemcpyAsync(h_scalars, red.get(), sizeof(double), cudaMemcpyDeviceToHost, stream));
+  sync();
+  return std::sqrt(h_scalars[0]);
+}
+
+void MeshProblem::apply_k(const double* Ud, double* out, int count) {
+  eval_elements(Ud, count, nullptr);
+  k_apply<<<dim3((n + 255) / 256, count), 256, 0, stream>>>(elem(), ev.get(), d_iptr.get(), d_inc.get(), out, n);
+  launched();
+}
+
+// assemble_stiffness_frozen (assembly.hpp:67-84) on the CSR pattern
+void MeshProblem::install_nu_hat(const double* nu, double q) {
+  for (int r = 0; r < kRegions; ++r) require(nu[r] > 0, "frozen stiffness: nu_hat must be positive");
+  std::vector<Trip> tr;
+  tr.reserve((size_t)9 * nt);
+  for (int t = 0; t < nt; ++t) {
+    const double co = nu[ereg[t]] * earea[t];
+    for (int a = 0; a < 3; ++a)
+      for (int b = 0; b < 3; ++b) {
+        const int i = edof[3 * t + a], j = edof[3 * t + b];
+        if (i >= 0 && j >= 0)
+          tr.push_back({i, j, co * (egx[3 * t + a] * egx[3 * t + b] + egy[3 * t + a] * egy[3 * t + b])});
+      }
+  }
+  std::vector<double> kv;
+  sum_triplets(tr, rptr, rcol, kv);
+  TP_CUDA(cudaMemcpy(d_kval.get(), kv.data(), kv.size() * sizeof(double), cudaMemcpyHostToDevice));
+  for (int r = 0; r < kRegions; ++r) nu_hat[r] = nu[r];
+  q_estimate = q;
+  nu_hat_set = true;
+  factored = false;
+}
+
+// choose_nu_hat (assembly.hpp:236-303) with flux_bounds (materials.hpp:140-150)
+void MeshProblem::choose_nu_hat(const tp_solver_cfg& cfg, double* nu, double* q) {
+  require(state_valid, "choose_nu_hat: frozen-field mode needs u_init");
+  double out[kRegions];
+  double qq = 0;
+  double flam[kRegions], fLam[kRegions];
+  for (int r = 0; r < kRegions; ++r) flux_range(mat[r], 0.0, s_max, flux_samples, &flam[r], &fLam[r]);
+  if (cfg.nu_hat_mode == TP_NU_HAT_THEORY) {
+    for (int r = 0; r < kRegions; ++r) {
+      out[r] = 0.5 * (flam[r] + fLam[r]);
+      qq = std::max(qq, (fLam[r] - flam[r]) / (fLam[r] + flam[r]));
+    }
+  } else {
+    // per-region |grad u| over every slice of the state
+    DevBuf<double> smag((size_t)N * nt);
+    eval_elements(U.get(), N, nullptr, smag.get());
+    const int blocks = 148;
+    DevBuf<double> rp((size_t)blocks * 2 * kRegions);
+    k_field_ranges<<<blocks, 256, 0, stream>>>(smag.get(), d_ereg.get(), nt, (size_t)N * nt, rp.get());
+    launched();
+    std::vector<double> h((size_t)blocks * 2 * kRegions);
+    TP_CUDA(cudaMemcpyAsync(h.data(), rp.get(), h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    sync();
+    const int samples = cfg.nu_hat_samples > 0 ? cfg.nu_hat_samples : 2000;
+    for (int r = 0; r < kRegions; ++r) {
+      double lo = INFINITY, hi = -1.0;
+      for (int b = 0; b < blocks; ++b) {
+        lo = std::min(lo, h[(size_t)b * 2 * kRegions + r]);
+        hi = std::max(hi, h[(size_t)b * 2 * kRegions + kRegions + r]);
+      }
+      if (!region_present[r] || hi < 0) {  // no observation: theory value, no say on q
+        out[r] = 0.5 * (flam[r] + fLam[r]);
+        continue;
+      }
+      const double margin = 0.2 * (hi - lo) + 1e-3;
+      double l, L;
+      flux_range(mat[r], std::max(0.0, lo - margin), hi + margin, samples, &l, &L);
+      out[r] = 0.5 * (l + L);
+      qq = std::max(qq, (L - l) / (L + l));
+    }
+  }
+  install_nu_hat(out, qq);
+  if (nu)
+    for (int r = 0; r < kRegions; ++r) nu[r] = out[r];
+  if (q) *q = qq;
+}
+
+// static_init (solvers.hpp:276-296): all slices' damped Newton steps batched;
+// the accept / stop decisions on the host in the reference's order
+void MeshProblem::static_init(const tp_solver_cfg& cfg, int32_t* counts) {
+  const size_t bandb = (size_t)n * (bw + 1) * sizeof(double);
+  size_t fb = 0, tb = 0;
+  TP_CUDA(cudaMemGetInfo(&fb, &tb));
+  const size_t per = bandb + (size_t)6 * n * sizeof(double) + (size_t)nt * sizeof(double4);
+  const int S = (int)std::max<size_t>(1, std::min<size_t>((size_t)N, (size_t)(0.5 * fb) / per));
+  const bool ysm = (size_t)n * sizeof(double) <= 200 * 1024;
+  DevBuf<double> Ub((size_t)S * n), Rb((size_t)S * n), Db((size_t)S * n), Ut((size_t)S * n), Rt((size_t)S * n),
+      Jb((size_t)S * n * (bw + 1)), ysc(ysm ? 0 : (size_t)S * n);
+  DevBuf<int> d_sl(S), d_on(S), d_acc(S);
+  DevBuf<double> d_alpha(S), nrm(S);
+  const int nb = (n + 255) / 256;
+  DevBuf<double> pp((size_t)S * nb);
+  std::vector<int> cnt(N, 0);
+  if (!ysm) TP_CUDA(cudaFuncSetAttribute(k_band_solve<double>, cudaFuncAttributeMaxDynamicSharedMemorySize, 0));
+  else
+    TP_CUDA(cudaFuncSetAttribute(k_band_solve<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)(n * sizeof(double))));
+  TP_CUDA(cudaFuncSetAttribute(k_band_factor<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(std::max(1, bw) * sizeof(double))));
+  std::vector<int> hs(S), hon(S), hacc(S);
+  std::vector<double> ha(S), rn(S), sc(S), tn(S);
+  auto norms = [&](const double* base, const int* slots_on) {
+    // r = F - K(v) for every slot, norms to the host
+    eval_elements(base, S, nullptr);
+    k_newton_res<<<dim3(nb, S), 256, 0, stream>>>(elem(), ev.get(), d_iptr.get(), d_inc.get(), F.get(), d_sl.get(),
+                                                  base == Ub.get() ? Rb.get() : Rt.get(), pp.get(), n);
+    launched();
+    k_sum_rows<<<(S + 3) / 4, 128, 0, stream>>>(pp.get(), nb, S, nrm.get());
+    launched();
+    TP_CUDA(cudaMemcpyAsync(tn.data(), nrm.get(), S * sizeof(double), cudaMemcpyDeviceToHost, stream));
+    sync();
+    for (int b = 0; b < S; ++b) tn[b] = std::sqrt(tn[b]);
+    (void)slots_on;
+  };
+  for (int s0 = 0; s0 < N; s0 += S) {
+    const int cb = std::min(S, N - s0);
+    for (int b = 0; b < S; ++b) hs[b] = std::min(s0 + b, N - 1);
+    TP_CUDA(cudaMemcpyAsync(d_sl.get(), hs.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+    TP_CUDA(cudaMemsetAsync(Ub.get(), 0, Ub.bytes(), stream));
+    // ||rhs|| and the initial residual (u = 0: r = rhs - K(0))
+    norms(Ub.get(), nullptr);
+    for (int b = 0; b < S; ++b) {
+      rn[b] = tn[b];
+      sc[b] = rn[b];  // max(|rhs|, r0) with r0 = |rhs - K(0)| = |rhs|
+      hon[b] = b < cb && !(sc[b] == 0 || rn[b] <= cfg.static_tol * sc[b]);
+    }
+    for (int step = 1; step <= cfg.static_max_newton; ++step) {
+      bool any = false;
+      for (int b = 0; b < S; ++b) any |= hon[b] != 0;
+      if (!any) break;
+      TP_CUDA(cudaMemcpyAsync(d_on.get(), hon.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+      // J(u), LDL^T, delta = J^-1 r
+      eval_elements(Ub.get(), S, nullptr);
+      k_band_jac<<<dim3((n + 127) / 128, S), 128, 0, stream>>>(elem(), ev.get(), d_iptr.get(), d_inc.get(),
+                                                               d_perm.get(), d_iperm.get(), d_on.get(), Jb.get(), n,
+                                                               bw);
+      launched();
+      TP_CUDA(cudaMemsetAsync(d_fail.get(), 0, sizeof(int), stream));
+      k_band_factor<double><<<S, 512, std::max(1, bw) * sizeof(double), stream>>>(Jb.get(), n, bw, d_on.get(),
+                                                                                   d_fail.get());
+      launched();
+      k_band_solve<double><<<S, 32, ysm ? n * sizeof(double) : 0, stream>>>(
+          Jb.get(), Rb.get(), Db.get(), d_perm.get(), n, bw, d_on.get(), ysm ? nullptr : ysc.get());
+      launched();
+      int fail = 0;
+      TP_CUDA(cudaMemcpyAsync(&h_scalars[0], d_fail.get(), sizeof(int), cudaMemcpyDeviceToHost, stream));
+      sync();
+      std::memcpy(&fail, &h_scalars[0], sizeof(int));
+      if (fail) throw Error(TP_ESOLVE, "static init: singular Newton Jacobian (zero pivot)");
+      // Armijo backtracking (solvers.hpp:154-177)
+      std::vector<int> searching = hon;
+      for (int b = 0; b < S; ++b) ha[b] = 1.0;
+      for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
+        bool more = false;
+        for (int b = 0; b < S; ++b) more |= searching[b] != 0;
+        if (!more) break;
+        TP_CUDA(cudaMemcpyAsync(d_alpha.get(), ha.data(), S * sizeof(double), cudaMemcpyHostToDevice, stream));
+        TP_CUDA(cudaMemcpyAsync(d_acc.get(), searching.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+        k_axpy_slots<<<dim3(nb, S), 256, 0, stream>>>(Ub.get(), Db.get(), d_alpha.get(), d_acc.get(), Ut.get(), n);
+        launched();
+        norms(Ut.get(), nullptr);
+        for (int b = 0; b < S; ++b) {
+          hacc[b] = 0;
+          if (!searching[b]) continue;
+          if (tn[b] <= (1.0 - cfg.armijo_slope * ha[b]) * rn[b]) {
+            hacc[b] = 1;
+            rn[b] = tn[b];
+            searching[b] = 0;
+          } else {
+            ha[b] *= cfg.armijo_backtrack;
+          }
+        }
+        TP_CUDA(cudaMemcpyAsync(d_acc.get(), hacc.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
+        k_accept_slots<<<dim3(nb, S), 256, 0, stream>>>(Ub.get(), Rb.get(), Ut.get(), Rt.get(), d_acc.get(), n);
+        launched();
+      }
+      for (int b = 0; b < S; ++b) {
+        if (!hon[b]) continue;
+        if (searching[b])
+          throw Error(TP_ESOLVE,
+                      "static init, step " + std::to_string(hs[b] + 1) + ": newton: line search exhausted at residual " +
+                          std::to_string(rn[b]),
+                      rn[b] / sc[b]);
+        if (rn[b] <= cfg.static_tol * sc[b]) {
+          cnt[hs[b]] = step;
+          hon[b] = 0;
+        }
+      }
+      if (step == cfg.static_max_newton)
+        for (int b = 0; b < S; ++b)
+          if (hon[b])
+            throw Error(TP_ESOLVE,
+                        "static init, step " + std::to_string(hs[b] + 1) + ": newton: no convergence within " +
+                            std::to_string(cfg.static_max_newton) + " steps",
+                        rn[b] / sc[b]);
+    }
+    TP_CUDA(cudaMemcpyAsync(U.get() + (size_t)s0 * n, Ub.get(), (size_t)cb * n * sizeof(double),
+                            cudaMemcpyDeviceToDevice, stream));
+  }
+  sync();
+  state_valid = true;
+  if (counts)
+    for (int i = 0; i < N; ++i) counts[i] = cnt[i];
+}
+
+// PeriodicSolver ctor (periodic.hpp:128-139, 211-248 with every block
+// cached): symbols and one factorisation per frequency
+void MeshProblem::factor_blocks() {
+  require(nu_hat_set, "periodic solver: K_hat not installed (tp_mesh_choose_nu_hat / tp_mesh_set_nu_hat)");
+  std::vector<cplx> hl(K);
+  for (int k = 0; k < K; ++k) {  // symbol, periodic.hpp:146-152
+    if (k == 0) hl[k] = {0.0, 0.0};
+    else if (2 * k == N) hl[k] = {2.0 / tau, 0.0};
+    else {
+      const double a = -2.0 * std::numbers::pi * k / N;
+      hl[k] = {(1.0 - std::cos(a)) / tau, (0.0 - std::sin(a)) / tau};
+    }
+  }
+  lam.alloc(K);
+  TP_CUDA(cudaMemcpy(lam.get(), hl.data(), K * sizeof(cplx), cudaMemcpyHostToDevice));
+  band.alloc((size_t)K * n * (bw + 1));
+  k_band_freq<<<dim3((n + 127) / 128, K), 128, 0, stream>>>(csr(), d_perm.get(), d_iperm.get(), lam.get(),
+                                                           band.get(), n, bw);
+  launched();
+  TP_CUDA(cudaFuncSetAttribute(k_band_factor<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               (int)(std::max(1, bw) * sizeof(cplx))));
+  TP_CUDA(cudaMemsetAsync(d_fail.get(), 0, sizeof(int), stream));
+  k_band_factor<cplx><<<K, 512, std::max(1, bw) * sizeof(cplx), stream>>>(band.get(), n, bw, nullptr, d_fail.get());
+  launched();
+  TP_CUDA(cudaMemcpyAsync(h_scalars, d_fail.get(), sizeof(int), cudaMemcpyDeviceToHost, stream));
+  sync();
+  int fail = 0;
+  std::memcpy(&fail, h_scalars, sizeof(int));
+  if (fail) throw Error(TP_ESOLVE, "periodic solver: singular frequency block (zero pivot)", -1.0);
+  Ghat.alloc((size_t)K * n);
+  Uhat.alloc((size_t)K * n);
+  factored = true;
+}
+
+// PeriodicSolver::solve (periodic.hpp:154-198) of the device G into U
+void MeshProblem::periodic_solve(const tp_solver_cfg& cfg) {
+  if (!factored) factor_blocks();
+  const DftCtx c = dft();
+  dft_forward(c, G.get(), Ghat.get());
+  const bool ysm = (size_t)n * sizeof(cplx) <= 200 * 1024;
+  DevBuf<cplx> ysc(ysm ? 0 : (size_t)K * n);
+  TP_CUDA(cudaFuncSetAttribute(k_band_solve<cplx>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               ysm ? (int)(n * sizeof(cplx)) : 0));
+  k_band_solve<cplx><<<K, 32, ysm ? n * sizeof(cplx) : 0, stream>>>(band.get(), Ghat.get(), Uhat.get(),
+                                                                   d_perm.get(), n, bw, nullptr,
+                                                                   ysm ? nullptr : ysc.get());
+  launched();
+  // the reference's per-solve residual contract (solve.hpp:79-89)
+  const int nb = (n + 255) / 256;
+  part.ensure((size_t)K * nb * 2);
+  red.ensure((size_t)2 * K);
+  k_freq_check<<<dim3(nb, K), 256, 0, stream>>>(csr(), lam.get(), Uhat.get(), Ghat.get(), part.get(), n);
+  launched();
+  k_sum_pairs_rows<<<(K + 3) / 4, 128, 0, stream>>>(part.get(), nb, K, red.get());
+  launched();
+  std::vector<double> chk((size_t)2 * K);
+  TP_CUDA(cudaMemcpyAsync(chk.data(), red.get(), chk.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  double re2 = 0, im2 = 0;
+  dft_inverse(c, Uhat.get(), U.get(), &re2, &im2);  // synchronises the stream
+  for (int k = 0; k < K; ++k) {
+    const double rel = chk[2 * k + 1] > 0 ? std::sqrt(chk[2 * k] / chk[2 * k + 1]) : std::sqrt(chk[2 * k]);
+    if (!(rel <= 1e-10))
+      throw Error(TP_ESOLVE, "sparse solve: relative residual " + std::to_string(rel) + " exceeds 1e-10", rel);
+  }
+  const double rn = std::sqrt(re2), in = std::sqrt(im2);
+  if (in > cfg.imag_tol * std::max(rn, 1e-300))
+    throw Error(TP_ESOLVE,
+                "periodic solver: imaginary residue " + std::to_string(in) + " exceeds " +
+                    std::to_string(cfg.imag_tol) + " x " + std::to_string(rn),
+                in / std::max(rn, 1e-300));
+  state_valid = true;
+}
+
+}  // namespace tpgpu
+
+// ================================================================= C ABI
+struct tp_mesh_problem {
+  std::unique_ptr<tpgpu::MeshProblem> impl;
+};
+
+namespace {
+template <class F>
+int mguard(F&& f) {
+  try {
+    f();
+    return TP_OK;
+  } catch (const tpgpu::Error& e) {
+    tpgpu::set_last_error(e.what(), e.residual);
+    return e.code;
+  } catch (const std::bad_alloc& e) {
+    tpgpu::set_last_error(std::string("allocation failed: ") + e.what(), -1);
+    return TP_ECUDA;
+  } catch (const std::exception& e) {
+    tpgpu::set_last_error(e.what(), -1);
+    return TP_EINVAL;
+  }
+}
+
+tpgpu::MeshProblem& MP(tp_mesh_problem* p) {
+  tpgpu::require(p && p->impl, "null problem handle");
+  TP_CUDA(cudaSetDevice(p->impl->device));
+  return *p->impl;
+}
+
+tp_solver_cfg mcfg(const tp_solver_cfg* c) {
+  tp_solver_cfg d;
+  tp_solver_cfg_default(&d);
+  return c ? *c : d;
+}
+
+double secs(std::chrono::steady_clock::time_point t0) {
+  return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+}
+}  // namespace
+
+extern "C" {
+
+void tp_material_table_transformer(tp_exp_material out[TP_MAX_MATERIALS]) {
+  // materials.hpp:67-79: steel, iron, air, winding_plus, winding_minus
+  const double nu_air = 1e7 / (4.0 * std::numbers::pi);
+  out[0] = {1e7, 130.171, 1.102, 6112.97, 43.742, 0.0};
+  out[1] = {0.0, 5.85, 2.196, 136026.0, 23.15, 0.0};
+  out[2] = {0.0, 0.0, 0.0, 1.0, nu_air, 0.0};
+  out[3] = {0.0, 0.0, 0.0, 1.0, nu_air, 1.9e4};
+  out[4] = {0.0, 0.0, 0.0, 1.0, nu_air, -1.9e4};
+}
+
+int tp_transformer_mesh(int32_t nx, int32_t ny, int32_t refinements, int32_t* nv, int32_t* nt, int32_t* n_dof,
+                        double* vertices, int32_t* triangles, int32_t* region) {
+  return mguard([&] {
+    tpgpu::require(refinements >= 0, "mesh: refinements must be >= 0");
+    tpgpu::HostMesh m = tpgpu::rectilinear(tpgpu::kTransformer, 8, nx, ny);
+    for (int r = 0; r < refinements; ++r) m = tpgpu::refine(m);
+    const int V = (int)(m.xy.size() / 2), Tn = (int)m.reg.size();
+    if (nv) *nv = V;
+    if (nt) *nt = Tn;
+    if (n_dof) {
+      const double tol = 1e-12 * std::max(m.x1 - m.x0, m.y1 - m.y0);
+      int c = 0;
+      for (int v = 0; v < V; ++v) {
+        const double x = m.xy[2 * v], y = m.xy[2 * v + 1];
+        c += !(std::abs(x - m.x0) <= tol || std::abs(x - m.x1) <= tol || std::abs(y - m.y0) <= tol ||
+               std::abs(y - m.y1) <= tol);
+      }
+      *n_dof = c;
+    }
+    if (vertices) std::memcpy(vertices, m.xy.data(), m.xy.size() * sizeof(double));
+    if (triangles) std::memcpy(triangles, m.tri.data(), m.tri.size() * sizeof(int32_t));
+    if (region) std::memcpy(region, m.reg.data(), m.reg.size() * sizeof(int32_t));
+  });
+}
+
+int tp_mesh_problem_create(const tp_mesh_desc* desc, int32_t device, tp_mesh_problem** out) {
+  return mguard([&] {
+    tpgpu::require(desc && out, "null argument");
+    int count = 0;
+    TP_CUDA(cudaGetDeviceCount(&count));
+    tpgpu::require(device >= 0 && device < count, "invalid device");
+    auto h = std::make_unique<tp_mesh_problem>();
+    h->impl = std::make_unique<tpgpu::MeshProblem>(*desc, device);
+    *out = h.release();
+  });
+}
+
+void tp_mesh_problem_destroy(tp_mesh_problem* p) { delete p; }
+
+int tp_mesh_problem_sizes(const tp_mesh_problem* p, int32_t* n_dof, int32_t* steps, double* tau, int32_t* bandwidth) {
+  return mguard([&] {
+    tpgpu::require(p && p->impl, "null problem handle");
+    if (n_dof) *n_dof = p->impl->n;
+    if (steps) *steps = p->impl->N;
+    if (tau) *tau = p->impl->tau;
+    if (bandwidth) *bandwidth = p->impl->bw;
+  });
+}
+
+int tp_mesh_loads(tp_mesh_problem* h, double* F) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(F != nullptr, "null argument");
+    TP_CUDA(cudaMemcpy(F, p.F.get(), p.F.bytes(), cudaMemcpyDeviceToHost));
+  });
+}
+
+int tp_mesh_apply_k(tp_mesh_problem* h, const double* U, double* KU, int32_t count) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(U && KU && count >= 0 && count <= p.N, "apply_k: bad arguments");
+    if (count == 0) return;
+    tpgpu::DevBuf<double> u((size_t)count * p.n), o((size_t)count * p.n);
+    TP_CUDA(cudaMemcpyAsync(u.get(), U, u.bytes(), cudaMemcpyHostToDevice, p.stream));
+    p.apply_k(u.get(), o.get(), count);
+    TP_CUDA(cudaMemcpyAsync(KU, o.get(), o.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    p.sync();
+  });
+}
+
+int tp_mesh_residual(tp_mesh_problem* h, const double* U, double* R, double* norm) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(U != nullptr, "null argument");
+    tpgpu::DevBuf<double> keep((size_t)p.N * p.n);
+    TP_CUDA(cudaMemcpyAsync(keep.get(), p.U.get(), p.U.bytes(), cudaMemcpyDeviceToDevice, p.stream));
+    TP_CUDA(cudaMemcpyAsync(p.U.get(), U, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+    const double r = p.residual_and_rhs(false, R != nullptr);
+    if (R) TP_CUDA(cudaMemcpyAsync(R, p.R.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    TP_CUDA(cudaMemcpyAsync(p.U.get(), keep.get(), p.U.bytes(), cudaMemcpyDeviceToDevice, p.stream));
+    p.sync();
+    if (norm) *norm = r;
+  });
+}
+
+int tp_mesh_static_init(tp_mesh_problem* h, const tp_solver_cfg* c, double* U0, int32_t* newton_counts) {
+  return mguard([&] {
+    auto& p = MP(h);
+    const tp_solver_cfg cfg = mcfg(c);
+    tpgpu::validate_cfg(cfg);
+    p.static_init(cfg, newton_counts);
+    if (U0) {
+      TP_CUDA(cudaMemcpyAsync(U0, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      p.sync();
+    }
+  });
+}
+
+int tp_mesh_set_state(tp_mesh_problem* h, const double* U) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(U != nullptr, "null argument");
+    TP_CUDA(cudaMemcpyAsync(p.U.get(), U, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+    p.sync();
+    p.state_valid = true;
+  });
+}
+
+int tp_mesh_get_state(tp_mesh_problem* h, double* U) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(U != nullptr, "null argument");
+    TP_CUDA(cudaMemcpyAsync(U, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    p.sync();
+  });
+}
+
+int tp_mesh_choose_nu_hat(tp_mesh_problem* h, const tp_solver_cfg* c, double* nu_hat, double* q) {
+  return mguard([&] {
+    auto& p = MP(h);
+    p.choose_nu_hat(mcfg(c), nu_hat, q);
+  });
+}
+
+int tp_mesh_set_nu_hat(tp_mesh_problem* h, const double* nu_hat, double q) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(nu_hat != nullptr, "null argument");
+    p.install_nu_hat(nu_hat, q);
+  });
+}
+
+int tp_mesh_periodic_solve(tp_mesh_problem* h, const tp_solver_cfg* c, const double* G, double* U) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tpgpu::require(G && U, "null argument");
+    const tp_solver_cfg cfg = mcfg(c);
+    tpgpu::DevBuf<double> keep((size_t)p.N * p.n);
+    TP_CUDA(cudaMemcpyAsync(keep.get(), p.U.get(), p.U.bytes(), cudaMemcpyDeviceToDevice, p.stream));
+    TP_CUDA(cudaMemcpyAsync(p.G.get(), G, p.G.bytes(), cudaMemcpyHostToDevice, p.stream));
+    const bool had = p.state_valid;
+    p.periodic_solve(cfg);
+    TP_CUDA(cudaMemcpyAsync(U, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+    TP_CUDA(cudaMemcpyAsync(p.U.get(), keep.get(), p.U.bytes(), cudaMemcpyDeviceToDevice, p.stream));
+    p.sync();
+    p.state_valid = had;
+  });
+}
+
+int tp_mesh_solve_m1(tp_mesh_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
+                     double* history, double* contraction, int32_t cap, tp_iterate_cb cb, void* user) {
+  return mguard([&] {
+    auto& p = MP(h);
+    const tp_solver_cfg cfg = mcfg(c);
+    tpgpu::validate_cfg(cfg);
+    tpgpu::require(p.nu_hat_set, "m1: nu_hat not installed (tp_mesh_choose_nu_hat / tp_mesh_set_nu_hat)");
+    const auto t0 = std::chrono::steady_clock::now();
+    if (U0) {
+      TP_CUDA(cudaMemcpyAsync(p.U.get(), U0, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+      p.state_valid = true;
+    }
+    tpgpu::require(p.state_valid, "m1: no initial state");
+    std::vector<double> hist, host_u;
+    auto callback = [&](int k, double res) {
+      if (!cb) return;
+      host_u.resize((size_t)p.N * p.n);
+      TP_CUDA(cudaMemcpyAsync(host_u.data(), p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      p.sync();
+      if (cb(k, host_u.data(), res, user) != 0) throw tpgpu::Error(TP_EINVAL, "m1: aborted by iterate callback");
+    };
+    auto stop = [&]() { return hist.back() <= cfg.tol * hist.front(); };  // solvers.hpp:100-103
+    hist.push_back(p.residual_and_rhs(true));
+    callback(0, hist.back());
+    tp_report r{};
+    r.q_estimate = p.q_estimate;
+    double setup = 0, sweeps = 0;
+    if (!stop()) {
+      const auto ts = std::chrono::steady_clock::now();
+      if (!p.factored) p.factor_blocks();
+      setup = secs(ts);
+      for (int k = 1; k <= cfg.m1_max_outer; ++k) {
+        const auto tk = std::chrono::steady_clock::now();
+        p.periodic_solve(cfg);
+        r.iterations = k;
+        hist.push_back(p.residual_and_rhs(true));
+        sweeps += secs(tk);
+        callback(k, hist.back());
+        if (stop()) break;
+      }
+    }
+    r.status = stop() ? TP_CONVERGED : TP_MAX_ITER;
+    r.history_len = (int32_t)std::min<size_t>(hist.size(), cap > 0 ? cap : 0);
+    if (history)
+      for (int k = 0; k < r.history_len; ++k) history[k] = hist[k];
+    if (contraction)
+      for (size_t k = 0; k + 1 < hist.size() && (int)k < cap; ++k)
+        contraction[k] = hist[k] > 0 ? hist[k + 1] / hist[k] : 0.0;
+    if (U_out) {
+      TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      p.sync();
+    }
+    r.setup_time = setup;
+    r.sweep_time = sweeps;
+    r.wall_time = secs(t0);
+    if (rep) *rep = r;
+  });
+}
+
+int tp_mesh_m1_begin(tp_mesh_problem* h, const tp_solver_cfg* c, double* residual0) {
+  return mguard([&] {
+    auto& p = MP(h);
+    (void)c;
+    tpgpu::require(p.nu_hat_set && p.state_valid, "m1_begin: needs nu_hat and a state");
+    if (!p.factored) p.factor_blocks();
+    const double r = p.residual_and_rhs(true);
+    if (residual0) *residual0 = r;
+  });
+}
+
+int tp_mesh_m1_sweep(tp_mesh_problem* h, double* residual) {
+  return mguard([&] {
+    auto& p = MP(h);
+    tp_solver_cfg cfg;
+    tp_solver_cfg_default(&cfg);
+    p.periodic_solve(cfg);
+    const double r = p.residual_and_rhs(true);
+    if (residual) *residual = r;
+  });
+}
+
+void* tp_mesh_problem_stream(tp_mesh_problem* h) { return h && h->impl ? (void*)h->impl->stream : nullptr; }
+
+int64_t tp_mesh_problem_launches(const tp_mesh_problem* h) { return h && h->impl ? h->impl->launches.load() : 0; }
+
+}  // extern "C"

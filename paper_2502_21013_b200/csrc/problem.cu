@@ -81,6 +81,8 @@ void validate_desc(const tp_problem_desc& d) {
   }
 }
 
+}  // namespace
+
 void validate_cfg(const tp_solver_cfg& c) {
   // validate(), solvers.hpp:71-86 (fields on this path)
   require(c.tol > 0 && c.tol < 1, "solver config: tol must lie in (0,1)");
@@ -93,6 +95,8 @@ void validate_cfg(const tp_solver_cfg& c) {
   require(c.inner_rtol > 0 && c.inner_rtol < 1e-6, "solver config: inner_rtol must lie in (0,1e-6)");
   require(c.inner_max_iter >= 1, "solver config: inner_max_iter must be positive");
 }
+
+namespace {
 
 // nu(s) and nu'(s) on the host, for the flux-bound sampling (materials.hpp:42-57 law swapped).
 double h_nu(const tp_material& m, double s) {

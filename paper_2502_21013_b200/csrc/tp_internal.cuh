@@ -37,6 +37,7 @@ struct Error : std::runtime_error {
   } while (0)
 
 void set_last_error(const std::string& msg, double residual);
+void validate_cfg(const tp_solver_cfg& c);  // validate(), solvers.hpp:71-86
 
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch for the kernel chains of the frequency solves
@@ -328,6 +329,21 @@ int rdft_forward_blocks(Problem& p);
 // returns imaginary-residue norm^2 partial sum and real norm^2 (host)
 void launch_rdft_inverse(Problem& p, const cplx* Uhat, double* U, double* re2, double* im2);
 double reduce_sum(Problem& p, const double* partials, int count);
+// The same real time-DFTs over any slice-major N x n array (general-mesh
+// problems, mesh.cu): plan slot, reduction scratch and pinned scalars of the owner
+struct DftCtx {
+  int N;
+  size_t n;
+  cudaStream_t stream;
+  std::shared_ptr<void>* plan;
+  DevBuf<double>* part;
+  DevBuf<double>* red;
+  double* h_scalars;
+  std::atomic<int64_t>* launches;
+};
+int dft_forward_blocks(const DftCtx& c);
+void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq = nullptr);
+void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, double* im2);
 void reduce_sum_dev(Problem& p, const double* partials, int count, double* out);  // no host sync
 
 }  // namespace tpgpu
