@@ -31,9 +31,9 @@ template <int BYTES>
 __device__ __forceinline__ void cpa(void* sdst, const void* g, bool ok) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
   if constexpr (BYTES == 16)
-    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0) : "memory");
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 16 : 0));
   else
-    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0));
 }
 __device__ __forceinline__ void cpa_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
@@ -123,28 +123,30 @@ __global__ void __launch_bounds__(32) k_solve(const T* __restrict__ bandp, const
   const T* A = bandp + (size_t)b * n * W;
   const T* s_ = src + (size_t)b * n;
   const int nch = (n + 31) >> 5;
-  // forward stage of chunk m: entry (ro, u) = L[c0+ro][c0+u], 0 < ro-u <= bw
-  // (rows padded to 33 entries: the compute loop reads a column across lanes)
+  // forward stage of chunk base c: entry (ro, u) = L[c+ro][c+u] at
+  // A + c W + bw + u + ro bw, valid for 0 < ro-u <= bw and c+ro < n (rows
+  // padded to 33 entries: the compute loop reads a column across lanes)
+  auto fwd_copy = [&](T* st, int c, int ro) {
+    const int hi = min(lane + bw, n - 1 - c);
+    const bool ok = ro > lane && ro <= hi;
+    cpa<sizeof(T)>(&st[ro * 33 + lane], ok ? A + (size_t)c * W + bw + lane + (size_t)ro * bw : A, ok);
+  };
   auto stage_fwd = [&](int m, T* st) {
-    const int c0 = m << 5;
 #pragma unroll 4
-    for (int ro = 0; ro < 32 * S; ++ro) {
-      const int d = ro - lane;
-      const bool ok = d > 0 && d <= bw && c0 + ro < n;
-      cpa<sizeof(T)>(&st[ro * 33 + lane], ok ? &A[(size_t)(c0 + ro) * W + bw - d] : A, ok);
-    }
+    for (int ro = 0; ro < 32 * S; ++ro) fwd_copy(st, m << 5, ro);
     cpa_commit();
   };
-  // backward stage: entry (u, s, l) = L[c0+u][c0-32s+l], 0 < u+32s-l <= bw
+  // backward stage of chunk base c: entry (u, s, l) = L[c+u][c-32s+l] at
+  // A + c W + bw + l + u bw - 32 s, valid for 0 < u+32s-l <= bw, c+u < n, c-32s+l >= 0
+  auto bwd_copy = [&](T* st, int c, int u, int s) {
+    const int d = u + 32 * s - lane;
+    const bool ok = d > 0 && d <= bw && c + u < n && c - 32 * s + lane >= 0;
+    cpa<sizeof(T)>(&st[(u * S + s) * 32 + lane],
+                   ok ? A + (size_t)c * W + bw + lane + (size_t)u * bw - 32 * s : A, ok);
+  };
   auto stage_bwd = [&](int m, T* st) {
-    const int c0 = m << 5;
 #pragma unroll 4
-    for (int us = 0; us < 32 * S; ++us) {
-      const int u = us / S, s = us - u * S;
-      const int d = u + 32 * s - lane;
-      const bool ok = d > 0 && d <= bw && c0 + u < n && c0 - 32 * s + lane >= 0;
-      cpa<sizeof(T)>(&st[us * 32 + lane], ok ? &A[(size_t)(c0 + u) * W + bw - d] : A, ok);
-    }
+    for (int us = 0; us < 32 * S; ++us) bwd_copy(st, m << 5, us / S, us % S);
     cpa_commit();
   };
   T win[S];
@@ -153,29 +155,48 @@ __global__ void __launch_bounds__(32) k_solve(const T* __restrict__ bandp, const
     const int r = 32 * s + lane;
     win[s] = r < n ? s_[perm[r]] : T{};
   }
-  // ---- forward: L y = b, then y / D
+  // ---- forward: L y = b, then y / D.  The next chunk's coefficients are
+  // staged while this chunk computes: its cp.async copies are issued inside
+  // the u loop (S per step), filling the shuffle latency of the chain; the
+  // values needed at the chunk end (D, the next right-hand-side rows) are
+  // loaded at the chunk start.
   stage_fwd(0, stage);
-  if (NB > 1 && nch > 1) stage_fwd(1, stage + CH);
+  int pn = 32 * S + lane < n ? perm[32 * S + lane] : 0;  // perm of the row entering after chunk 0
   for (int m = 0; m < nch; ++m) {
     T* st = stage + (NB > 1 ? (m & 1) * CH : 0);
-    if (NB > 1 && m + 1 < nch) cpa_wait<1>();
-    else cpa_wait<0>();
+    T* nx = stage + (NB > 1 ? ((m + 1) & 1) * CH : 0);
+    const int c0 = m << 5, r = c0 + lane, rn = c0 + 32 * S + lane;
+    const T dg = r < n ? A[(size_t)r * W + bw] : T{};
+    const T bn = rn < n ? s_[pn] : T{};
+    pn = rn + 32 < n ? perm[rn + 32] : 0;
+    cpa_wait<0>();
     __syncwarp();
+    const bool pre = NB > 1 && m + 1 < nch;
+    const int c1 = c0 + 32;
+    if (pre) {
 #pragma unroll
-    for (int u = 0; u < 32; ++u) {
-      const T yc = shfl(win[0], u);
+      for (int u = 0; u < 32; ++u) {
+        const T yc = shfl(win[0], u);
 #pragma unroll
-      for (int s = 0; s < S; ++s) win[s] = fnma(st[(32 * s + lane) * 33 + u], yc, win[s]);
+        for (int s = 0; s < S; ++s) win[s] = fnma(st[(32 * s + lane) * 33 + u], yc, win[s]);
+#pragma unroll
+        for (int s = 0; s < S; ++s) fwd_copy(nx, c1, 32 * s + u);
+      }
+      cpa_commit();
+    } else {
+#pragma unroll
+      for (int u = 0; u < 32; ++u) {
+        const T yc = shfl(win[0], u);
+#pragma unroll
+        for (int s = 0; s < S; ++s) win[s] = fnma(st[(32 * s + lane) * 33 + u], yc, win[s]);
+      }
     }
-    const int c0 = m << 5, r = c0 + lane;
-    if (r < n) y[r] = divv(win[0], A[(size_t)r * W + bw]);
+    if (r < n) y[r] = divv(win[0], dg);
 #pragma unroll
     for (int s = 0; s + 1 < S; ++s) win[s] = win[s + 1];
-    const int rn = c0 + 32 * S + lane;
-    win[S - 1] = rn < n ? s_[perm[rn]] : T{};
+    win[S - 1] = bn;
     __syncwarp();
-    if (m + NB < nch) stage_fwd(m + NB, st);
-    else if (NB == 1 && m + 1 < nch) stage_fwd(m + 1, st);
+    if (NB == 1 && m + 1 < nch) stage_fwd(m + 1, st);
   }
   __syncwarp();
   // ---- backward: L^T x = y / D, chunks from the last down
@@ -188,28 +209,41 @@ __global__ void __launch_bounds__(32) k_solve(const T* __restrict__ bandp, const
   cpa_wait<0>();
   __syncwarp();
   stage_bwd(mt, stage);
-  if (NB > 1 && mt > 0) stage_bwd(mt - 1, stage + CH);
   T* d_ = dst + (size_t)b * n;
   for (int m = mt, i = 0; m >= 0; --m, ++i) {
     T* st = stage + (NB > 1 ? (i & 1) * CH : 0);
-    if (NB > 1 && m > 0) cpa_wait<1>();
-    else cpa_wait<0>();
+    T* nx = stage + (NB > 1 ? ((i + 1) & 1) * CH : 0);
+    const int c0 = m << 5, r = c0 + lane, rn = c0 - 32 * S + lane;
+    const int pr = r < n ? perm[r] : 0;
+    const T yn = rn >= 0 ? y[rn] : T{};
+    cpa_wait<0>();
     __syncwarp();
+    const bool pre = NB > 1 && m > 0;
+    const int c1 = c0 - 32;
+    if (pre) {
 #pragma unroll
-    for (int u = 31; u >= 0; --u) {
-      const T xc = shfl(win[0], u);
+      for (int u = 31; u >= 0; --u) {
+        const T xc = shfl(win[0], u);
 #pragma unroll
-      for (int s = 0; s < S; ++s) win[s] = fnma(st[(u * S + s) * 32 + lane], xc, win[s]);
+        for (int s = 0; s < S; ++s) win[s] = fnma(st[(u * S + s) * 32 + lane], xc, win[s]);
+#pragma unroll
+        for (int s = 0; s < S; ++s) bwd_copy(nx, c1, u, s);
+      }
+      cpa_commit();
+    } else {
+#pragma unroll
+      for (int u = 31; u >= 0; --u) {
+        const T xc = shfl(win[0], u);
+#pragma unroll
+        for (int s = 0; s < S; ++s) win[s] = fnma(st[(u * S + s) * 32 + lane], xc, win[s]);
+      }
     }
-    const int c0 = m << 5, r = c0 + lane;
-    if (r < n) d_[perm[r]] = win[0];
+    if (r < n) d_[pr] = win[0];
 #pragma unroll
     for (int s = 0; s + 1 < S; ++s) win[s] = win[s + 1];
-    const int rn = c0 - 32 * S + lane;
-    win[S - 1] = rn >= 0 ? y[rn] : T{};
+    win[S - 1] = yn;
     __syncwarp();
-    if (m - NB >= 0) stage_bwd(m - NB, st);
-    else if (NB == 1 && m - 1 >= 0) stage_bwd(m - 1, st);
+    if (NB == 1 && m - 1 >= 0) stage_bwd(m - 1, st);
   }
 }
 
