@@ -5,6 +5,11 @@
 //   tpfem::PeriodicState U0 = tpgpu::static_init(prob, cfg);          // solvers.hpp:276-278
 //   auto [U, rep] = tpgpu::solve_m1_fixed_point(prob, U0, cfg);       // solvers.hpp:301-306
 //
+// prob is a GpuProblem (BASELINE uniform grids, tpgpu.h) or a GpuMeshProblem
+// built from the reference's own tpfem::Mesh + tpfem::MaterialTable
+// (tpgpu_mesh.h: build_transformer_mesh / refine_uniform meshes, the
+// reference's transformer physics).
+//
 // Requires the tpfem headers (tpfem/solvers.hpp) on the include path and
 // libtpgpu.so at link time.  Header-only; the mapping of types is:
 //   tpfem::SolverConfig   -> tp_solver_cfg      (solvers.hpp:49-69)
@@ -19,8 +24,11 @@
 #include <utility>
 #include <vector>
 
+#include "tpfem/assembly.hpp"
+#include "tpfem/mesh.hpp"
 #include "tpfem/solvers.hpp"
 #include "tpgpu.h"
+#include "tpgpu_mesh.h"
 
 namespace tpgpu {
 
@@ -75,23 +83,97 @@ class GpuProblem {
   double tau_ = 0;
 };
 
-inline tpfem::PeriodicState static_init(GpuProblem& p, const tpfem::SolverConfig& cfg,
+/// Owning handle of a device-resident problem on a reference mesh: the
+/// setup_transformer pipeline (runner.hpp:46-73) up to static_init, from the
+/// reference's own Mesh and MaterialTable (vertices, triangles, labels and
+/// coefficients are passed through unchanged; dofs are numbered by the same
+/// finalize_mesh rule, so states are interchangeable with tpfem's).
+class GpuMeshProblem {
+ public:
+  GpuMeshProblem(const tpfem::Mesh& mesh, const tpfem::MaterialTable& mat, int steps, double period,
+                 double s_max = 3.0, int flux_samples = 10001, int device = 0) {
+    std::vector<double> xy;
+    std::vector<int32_t> tri, reg;
+    for (const auto& v : mesh.vertices) xy.insert(xy.end(), {v[0], v[1]});
+    for (const auto& t : mesh.triangles) tri.insert(tri.end(), {(int32_t)t[0], (int32_t)t[1], (int32_t)t[2]});
+    for (const auto r : mesh.region) reg.push_back(static_cast<int32_t>(r));
+    tp_mesh_desc d{};
+    d.n_vertices = static_cast<int32_t>(mesh.vertices.size());
+    d.n_triangles = static_cast<int32_t>(mesh.triangles.size());
+    d.vertices = xy.data();
+    d.triangles = tri.data();
+    d.region = reg.data();
+    for (int r = 0; r < tpfem::kNumRegions; ++r) {
+      const auto& m = mat.at(static_cast<tpfem::Region>(r));
+      d.material[r] = tp_exp_material{m.sigma, m.a, m.b, m.c, m.d, m.j_amp};
+    }
+    d.steps = steps;
+    d.period = period;
+    d.s_max = s_max;
+    d.flux_samples = flux_samples;
+    tp_mesh_problem* p = nullptr;
+    check(tp_mesh_problem_create(&d, device, &p));
+    h_.reset(p);
+    check(tp_mesh_problem_sizes(p, &n_, &steps_, &tau_, &bw_));
+  }
+  tpfem::Index n_dof() const { return n_; }
+  int steps() const { return steps_; }
+  double tau() const { return tau_; }
+  tp_mesh_problem* get() const { return h_.get(); }
+  void apply_k(const double* u, double* out) const { check(tp_mesh_apply_k(h_.get(), u, out, 1)); }
+
+ private:
+  struct Del {
+    void operator()(tp_mesh_problem* p) const { tp_mesh_problem_destroy(p); }
+  };
+  std::unique_ptr<tp_mesh_problem, Del> h_;
+  int32_t n_ = 0, steps_ = 0, bw_ = 0;
+  double tau_ = 0;
+};
+
+namespace detail {
+// the C entry points of each problem kind
+inline int c_static_init(GpuProblem& p, const tp_solver_cfg* c, double* U, int32_t* n) {
+  return tp_static_init(p.get(), c, U, n);
+}
+inline int c_static_init(GpuMeshProblem& p, const tp_solver_cfg* c, double* U, int32_t* n) {
+  return tp_mesh_static_init(p.get(), c, U, n);
+}
+inline int c_choose(GpuProblem& p, const tp_solver_cfg* c, double* nu, double* q) {
+  return tp_choose_nu_hat(p.get(), c, nu, q);
+}
+inline int c_choose(GpuMeshProblem& p, const tp_solver_cfg* c, double* nu, double* q) {
+  return tp_mesh_choose_nu_hat(p.get(), c, nu, q);
+}
+inline int c_m1(GpuProblem& p, const tp_solver_cfg* c, const double* U0, double* U, tp_report* r, double* h,
+                double* ct, int32_t cap, tp_iterate_cb cb, void* u) {
+  return tp_solve_m1(p.get(), c, U0, U, r, h, ct, cap, cb, u);
+}
+inline int c_m1(GpuMeshProblem& p, const tp_solver_cfg* c, const double* U0, double* U, tp_report* r, double* h,
+                double* ct, int32_t cap, tp_iterate_cb cb, void* u) {
+  return tp_mesh_solve_m1(p.get(), c, U0, U, r, h, ct, cap, cb, u);
+}
+}  // namespace detail
+
+template <class P>
+inline tpfem::PeriodicState static_init(P& p, const tpfem::SolverConfig& cfg,
                                         std::vector<int>* newton_counts = nullptr) {
   tpfem::validate(cfg);
   tpfem::PeriodicState U(p.steps(), p.n_dof(), p.tau());
   std::vector<int32_t> counts(static_cast<std::size_t>(p.steps()));
   const tp_solver_cfg c = to_c(cfg);
-  check(tp_static_init(p.get(), &c, U.data.data(), counts.data()));
+  check(detail::c_static_init(p, &c, U.data.data(), counts.data()));
   if (newton_counts) newton_counts->assign(counts.begin(), counts.end());
   return U;
 }
 
 /// choose_nu_hat (assembly.hpp:254-303) from the device state; returns q.
-inline double choose_nu_hat(GpuProblem& p, const tpfem::SolverConfig& cfg,
+template <class P>
+inline double choose_nu_hat(P& p, const tpfem::SolverConfig& cfg,
                             std::array<double, tpfem::kNumRegions>* nu_hat = nullptr) {
   const tp_solver_cfg c = to_c(cfg);
   double nu[TP_MAX_MATERIALS], q = 0;
-  check(tp_choose_nu_hat(p.get(), &c, nu, &q));
+  check(detail::c_choose(p, &c, nu, &q));
   if (nu_hat)
     for (int r = 0; r < tpfem::kNumRegions; ++r) (*nu_hat)[static_cast<std::size_t>(r)] = nu[r];
   return q;
@@ -99,8 +181,9 @@ inline double choose_nu_hat(GpuProblem& p, const tpfem::SolverConfig& cfg,
 
 /// solve_m1_fixed_point (solvers.hpp:301-369) with K_hat = the installed
 /// frozen stiffness; iterate_log as in the reference.
+template <class P>
 inline std::pair<tpfem::PeriodicState, tpfem::SolveReport> solve_m1_fixed_point(
-    GpuProblem& p, const tpfem::PeriodicState& U0, const tpfem::SolverConfig& cfg,
+    P& p, const tpfem::PeriodicState& U0, const tpfem::SolverConfig& cfg,
     std::vector<tpfem::PeriodicState>* iterate_log = nullptr) {
   tpfem::validate(cfg);
   const tp_solver_cfg c = to_c(cfg);
@@ -119,7 +202,7 @@ inline std::pair<tpfem::PeriodicState, tpfem::SolveReport> solve_m1_fixed_point(
     c2->log->push_back(std::move(s));
     return 0;
   };
-  check(tp_solve_m1(p.get(), &c, U0.data.data(), U.data.data(), &rep, hist.data(), contr.data(), cap,
+  check(detail::c_m1(p, &c, U0.data.data(), U.data.data(), &rep, hist.data(), contr.data(), cap,
                     iterate_log ? +cb : nullptr, &ctx));
   tpfem::SolveReport r;
   r.method = tpfem::Method::m1;

@@ -99,6 +99,10 @@ def test_tpfem_adapter_compiles_against_reference_headers(tmp_path):
                    "int f(){ tp_problem_desc d; tp_problem_desc_baseline(0,&d);"
                    " tpgpu::GpuProblem p(d); tpfem::SolverConfig c; c.tol=1e-8;"
                    " auto U0 = tpgpu::static_init(p, c); tpgpu::choose_nu_hat(p, c);"
-                   " auto r = tpgpu::solve_m1_fixed_point(p, U0, c); return r.second.iterations; }\n")
+                   " auto r = tpgpu::solve_m1_fixed_point(p, U0, c); return r.second.iterations; }\n"
+                   "int g(){ auto m = tpfem::build_rectilinear_mesh(tpfem::transformer_regions(), 40, 40);"
+                   " tpgpu::GpuMeshProblem p(m, tpfem::MaterialTable::transformer(), 64, 0.02);"
+                   " tpfem::SolverConfig c; auto U0 = tpgpu::static_init(p, c); tpgpu::choose_nu_hat(p, c);"
+                   " return tpgpu::solve_m1_fixed_point(p, U0, c).second.iterations; }\n")
     subprocess.run(["g++", "-std=c++20", "-fsyntax-only", "-I", os.path.join(ROOT, "oracle", "shim"),
                     "-I", ref_inc, "-I", os.path.join(ROOT, "include"), str(src)], check=True)

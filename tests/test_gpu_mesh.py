@@ -152,3 +152,20 @@ def test_general_mesh_arrays_and_errors():
         with MeshProblem(V, T, R, mats, 8, 0.02) as p:
             p.solve_m1_fixed_point(np.zeros(p.shape), default_cfg())  # no nu_hat installed
     _ = SolveError
+
+
+def test_reference_side_adapter_drop_in():
+    """INTEGRATION.md's reference-side change, compiled against the reference
+    headers (oracle/_ref/adapter_demo): runner.hpp's transformer pipeline with
+    M1 through tpgpu_tpfem.hpp's GpuMeshProblem vs tpfem on the CPU."""
+    import json
+    import os
+    import subprocess
+    exe = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "oracle", "_ref", "adapter_demo")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/adapter_demo not built")
+    out = subprocess.run([exe, "40", "40", "0", "64", "9.5e5", "1e-8"], capture_output=True, text=True, timeout=300)
+    r = json.loads(out.stdout.strip().splitlines()[-1])
+    assert out.returncode == 0, r
+    assert r["newton_equal"] and r["cpu_iterations"] == r["gpu_iterations"] == 45
+    assert r["final_rel"] <= ITERATE_TOL and r["nu_hat_rel"] <= 1e-12
