@@ -338,11 +338,63 @@ def run_b200(args):
            "residual_last": history[-1], "residual_first": history[0]}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(desc, U0, nu, q)
+    if rank == 0 and world == 1 and args.mesh:
+        out["reference_mesh"] = mesh_leg(args)
     if rank == 0:
         print(json.dumps(out), flush=True)
     p.close()
     if comm is not None:
         comm.close()
+
+
+def mesh_leg(args):
+    """General-mesh path on the reference's own config
+    configs/transformer_saturated.json (40x40 snapped transformer mesh, 2142
+    dofs, N=64, windings +-9.5e5 A/m^2) at tol 1e-8: device sweeps timed with
+    CUDA events on the problem's stream; M1 to 1e-8 through the C ABI (host
+    U0 in, U out) beside the reference's solve_m1_fixed_point on the same U0
+    (oracle/_ref, all host threads)."""
+    from paper_2502_21013_b200.mesh import MeshProblem
+    from paper_2502_21013_b200 import default_cfg
+    cfg = default_cfg(tol=1e-8)
+    with MeshProblem.transformer(j_amp=9.5e5) as mp:
+        U0, _ = mp.static_init(cfg)
+        mp.choose_nu_hat(cfg)
+        _, rep = mp.solve_m1_fixed_point(U0, cfg)          # warm
+        t0 = time.perf_counter()
+        U, rep = mp.solve_m1_fixed_point(U0, cfg)
+        t_solve = time.perf_counter() - t0
+        mp.set_state(U0)
+        mp.m1_begin(cfg)
+        for _ in range(3):
+            mp.m1_sweep()
+        import torch
+        stream = torch.cuda.ExternalStream(mp.stream, device=0)
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        K = 20
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for _ in range(K):
+            mp.m1_sweep()
+        ev[1].record(stream)
+        ev[1].synchronize()
+        sweep_ms = ev[0].elapsed_time(ev[1]) / K
+        D = mp.n_dof * mp.steps
+        leg = {"workload": "reference configs/transformer_saturated.json: 40x40 snapped transformer mesh "
+                           f"({mp.n_dof} dofs, band {mp.bandwidth}) x N={mp.steps}, tol 1e-8",
+               "sweep_ms": sweep_ms, "dof_per_s": D / (sweep_ms / 1e3), "m1_sweeps": rep.iterations,
+               "m1_wall_s": t_solve}
+    try:
+        from oracle import ref
+        if ref.available():
+            c = ref.tr_cfg(j_amp=9.5e5)
+            r = ref.tr_solve_m1(c, *ref.tr_choose_nu_hat(c, U0, cfg), U0, cfg)
+            leg["reference_m1_wall_s"] = r.wall_time
+            leg["reference_m1_sweeps"] = r.iterations
+            leg["reference_threads"] = ref.hardware_threads()
+    except Exception as e:  # the checker is optional on the box
+        leg["reference_error"] = str(e)
+    return leg
 
 
 def cpu_baseline(desc, U0, nu, q):
@@ -418,6 +470,8 @@ def main():
     ap.add_argument("--calib-sweeps", type=int, default=3,
                     help="isolated dominant-kernel calibration sweeps after the timed region (0: off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-mesh", dest="mesh", action="store_false",
+                    help="skip the general-mesh leg (reference transformer config)")
     ap.add_argument("--no-full-solve", dest="full_solve", action="store_false")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent copies instead of sharding")
     ap.add_argument("--ref-u0", default=None, help="reference arm: precomputed U0 (.npy)")
