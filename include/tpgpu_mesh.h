@@ -14,6 +14,7 @@
  *     materials.hpp:17-24, 42-65);
  *   - the consistent sigma-mass (assemble_mass, assembly.hpp:48-65) and the
  *     element-wise loads F (assemble_loads, assembly.hpp:86-106);
+ *   - M1, M2 and M3 (configs/transformer.json's "method": "all");
  *   - every frequency block (and every static-init Newton Jacobian) is
  *     factorised once with a banded complex-symmetric LDL^T in a
  *     reverse-Cuthill-McKee order and solved directly, as the reference's
@@ -92,6 +93,12 @@ int tp_mesh_periodic_solve(tp_mesh_problem* p, const tp_solver_cfg* cfg, const d
 int tp_mesh_solve_m1(tp_mesh_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out,
                      tp_report* report, double* history, double* contraction, int32_t cap,
                      tp_iterate_cb cb, void* user);
+/* solve_m2_newton (solvers.hpp:375-484) and solve_m3_timestepping
+ * (solvers.hpp:489-542) on the mesh problem; outputs as tp_solve_m2 / _m3. */
+int tp_mesh_solve_m2(tp_mesh_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out,
+                     tp_report* report, double* history, double* contraction, int32_t cap);
+int tp_mesh_solve_m3(tp_mesh_problem* p, const tp_solver_cfg* cfg, const double* U0, double* U_out,
+                     tp_report* report, double* history, double* contraction, int32_t cap);
 /* device-resident sweeps (benchmarks): factorise the blocks + initial
  * residual; one sweep returning ||R||. */
 int tp_mesh_m1_begin(tp_mesh_problem* p, const tp_solver_cfg* cfg, double* residual0);

@@ -263,6 +263,7 @@ def _trlib():
         L.tpref_tr_choose_nu_hat.argtypes = [T, G, dp, dp, dp]
         L.tpref_tr_periodic_solve.argtypes = [T, G, dp, dp, dp]
         L.tpref_tr_solve_m1.argtypes = [T, G, dp, C.c_double, dp, dp, dp, C.c_int32, ip, ip, dp, dp]
+        L.tpref_tr_solve_m23.argtypes = [T, G, C.c_int32, dp, dp, dp, C.c_int32, ip, ip, dp]
         L._tr_ready = True
     return L
 
@@ -349,3 +350,19 @@ def tr_solve_m1(c: TrCfg, nu_hat, q, U0, cfg: TpSolverCfg | None = None, keep_it
     k = it.value
     return RefM1Result(U=U, history=hist[:k + 1].copy(), contraction=np.zeros(0), iterations=k, status=st.value,
                        iterates=None if its is None else its[:k + 1].copy(), wall_time=float(wall[0]))
+
+
+def tr_solve_m23(c: TrCfg, method: int, U0, cfg: TpSolverCfg | None = None):
+    """solve_m2_newton (method 2) / solve_m3_timestepping (3) on the reference
+    transformer: (U, history, iterations, status, wall seconds)."""
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    cap = (cfg.m2_max_outer if method == 2 else cfg.m3_max_cycles) + 1
+    hist = np.zeros(cap)
+    it, st = C.c_int32(), C.c_int32()
+    wall = np.zeros(1)
+    U = np.zeros_like(U0)
+    _check(_trlib().tpref_tr_solve_m23(C.byref(c), C.byref(cfg), method, _ptr(U0), _ptr(U), _ptr(hist), cap,
+                                       C.byref(it), C.byref(st), _ptr(wall)))
+    k = it.value
+    return U, hist[:k + 1].copy(), k, st.value, float(wall[0])

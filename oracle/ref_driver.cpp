@@ -486,3 +486,23 @@ int tpref_tr_solve_m1(const tpref_mesh_cfg* c, const tp_solver_cfg* sc, const do
 }
 
 }  // extern "C"
+
+// solve_m2_newton / solve_m3_timestepping on the reference transformer
+// problem (run_transformer_method, runner.hpp:85-86)
+extern "C" int tpref_tr_solve_m23(const tpref_mesh_cfg* c, const tp_solver_cfg* sc, int32_t method, const double* U0,
+                                  double* U_out, double* history, int32_t cap, int32_t* iterations, int32_t* status,
+                                  double* wall) {
+  return guarded([&] {
+    const TrSetup s(*c);
+    const tpfem::SolverConfig cfg = to_ref(sc);
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [U, rep] = method == 2 ? tpfem::solve_m2_newton(s.problem(), s.F, s.state(U0), cfg)
+                                : tpfem::solve_m3_timestepping(s.problem(), s.F, s.state(U0), cfg);
+    if (wall) *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
+    for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)
+      history[k] = rep.residual_history[k];
+    if (iterations) *iterations = rep.iterations;
+    if (status) *status = static_cast<int32_t>(rep.status);
+  });
+}

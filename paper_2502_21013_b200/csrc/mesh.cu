@@ -541,6 +541,133 @@ __global__ void k_sum_pairs_rows(const double* __restrict__ part, int per, int r
   }
 }
 
+// ---- M2 / M3 kernels
+// J(u) (+ ms M) values on the CSR pattern, per slot b: row j gathers its
+// incident element blocks area (nu I + (nu'/s) g g^T) in ascending triangle
+// order (assembly.hpp:153-177); incpos maps (incidence, corner) -> CSR entry
+__global__ void k_csr_jac(ElemDev e, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                          const int* __restrict__ inc, const int* __restrict__ incpos, const int* __restrict__ rptr,
+                          const double* __restrict__ mval, double ms, double* __restrict__ vals, int n, int nnz) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.y;
+  if (j >= n) return;
+  double* v = vals + (size_t)b * nnz;
+  for (int q = rptr[j]; q < rptr[j + 1]; ++q) v[q] = ms * mval[q];  // add_scaled(ms, M, 1, J): ms*M first
+  const double4* evb = ev + (size_t)b * e.nt;
+  for (int q = iptr[j]; q < iptr[j + 1]; ++q) {
+    const int t = inc[q] >> 2, i = inc[q] & 3;
+    const double4 x = evb[t];
+    const double gxi = e.gx[3 * t + i], gyi = e.gy[3 * t + i];
+    const double di = x.z * gxi + x.w * gyi;
+    for (int c = 0; c < 3; ++c) {
+      const int pos = incpos[3 * q + c];
+      if (pos < 0) continue;
+      const double gxc = e.gx[3 * t + c], gyc = e.gy[3 * t + c];
+      const double iso = x.x * (gxi * gxc + gyi * gyc);
+      const double dir = x.y * di * (x.z * gxc + x.w * gyc);
+      v[pos] += e.area[t] * (iso + dir);
+    }
+  }
+}
+
+// one real block in band form from CSR values (lower triangle, RCM order)
+__global__ void k_band_csr(const int* __restrict__ rptr, const int* __restrict__ rcol, const double* __restrict__ vals,
+                           const int* __restrict__ perm, const int* __restrict__ iperm, double* __restrict__ band,
+                           int n, int bw) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= n) return;
+  double* row = band + (size_t)p * (bw + 1);
+  for (int q = 0; q <= bw; ++q) row[q] = 0.0;
+  const int j = perm[p];
+  for (int q = rptr[j]; q < rptr[j + 1]; ++q) {
+    const int pc = iperm[rcol[q]];
+    if (pc <= p) row[pc - p + bw] = vals[q];
+  }
+}
+
+// time average of the slice Jacobians, slice order then / N (solvers.hpp:410-415)
+__global__ void k_average_rows(const double* __restrict__ J, size_t per, int N, double* __restrict__ out) {
+  const size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x;
+  if (i >= per) return;
+  double s = J[i];
+  for (int k = 1; k < N; ++k) s += J[(size_t)k * per + i];
+  out[i] = s / N;
+}
+
+// out_i = M ((v_i - v_{i-1}) / tau) + J_i v_i (solvers.hpp:426-440)
+__global__ void k_m2_apply_csr(Csr A, const double* __restrict__ J, int nnz, const double* __restrict__ v,
+                               double* __restrict__ out, int n, int N, double tau) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int i = blockIdx.y;
+  if (j >= n) return;
+  const double* vi = v + (size_t)i * n;
+  const double* vp = v + (size_t)((i + N - 1) % N) * n;
+  const double* Ji = J + (size_t)i * nnz;
+  double jv = 0, mdv = 0;
+  for (int q = A.ptr[j]; q < A.ptr[j + 1]; ++q) {
+    const int c = A.col[q];
+    jv += Ji[q] * vi[c];
+    mdv += A.m[q] * ((vi[c] - vp[c]) / tau);
+  }
+  out[(size_t)i * n + j] = mdv + jv;
+}
+
+// M3 step right-hand side rhs = f_i + (1/tau) M u_prev (solvers.hpp:512-514)
+__global__ void k_step_rhs(Csr A, const double* __restrict__ f, const double* __restrict__ up, double inv_tau,
+                           double* __restrict__ rhs, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double mu = 0;
+  for (int q = A.ptr[j]; q < A.ptr[j + 1]; ++q) mu += A.m[q] * up[A.col[q]];
+  rhs[j] = f[j] + inv_tau * mu;
+}
+
+// newton_elliptic's residual r = rhs - ms M v - K(v) (solvers.hpp:141-148), r^2 partials
+__global__ void k_step_res(ElemDev e, Csr A, const double4* __restrict__ ev, const int* __restrict__ iptr,
+                           const int* __restrict__ inc, const double* __restrict__ rhs, const double* __restrict__ v,
+                           double ms, double* __restrict__ r, double* __restrict__ part, int n) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  double r2 = 0;
+  if (j < n) {
+    double mv = 0;
+    for (int q = A.ptr[j]; q < A.ptr[j + 1]; ++q) mv += A.m[q] * v[A.col[q]];
+    const double x = rhs[j] - ms * mv - k_at(e, ev, iptr, inc, j);
+    r[j] = x;
+    r2 = x * x;
+  }
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_down_sync(0xffffffffu, r2, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_dot_parts(const double* __restrict__ a, const double* __restrict__ b, size_t len,
+                            double* __restrict__ part) {
+  double v = 0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+    v = fma(a[i], b[i], v);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  __shared__ double ws[32];
+  if ((threadIdx.x & 31) == 0) ws[threadIdx.x >> 5] = v;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+    for (int w = 0; w < (int)(blockDim.x >> 5); ++w) s += ws[w];
+    part[blockIdx.x] = s;
+  }
+}
+
+__global__ void k_axpy_flat(double a, const double* __restrict__ x, double* __restrict__ y, size_t len,
+                            int overwrite) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < len; i += (size_t)gridDim.x * blockDim.x)
+    y[i] = overwrite ? a * x[i] : fma(a, x[i], y[i]);
+}
+
 // triplets summed like SparseMatrix::from_triplets (sparse.hpp:49-82): sorted
 // by (row, col, value bits), duplicates added in that order
 struct Trip {
@@ -594,7 +721,7 @@ class MeshProblem {
   std::shared_ptr<void> fft_plan;
   double* h_scalars = nullptr;
   DevBuf<double> part, red, part2, red2;
-  DevBuf<int> d_edof, d_ereg, d_iptr, d_inc, d_rptr, d_rcol, d_perm, d_iperm, d_fail;
+  DevBuf<int> d_edof, d_ereg, d_iptr, d_inc, d_rptr, d_rcol, d_perm, d_iperm, d_fail, d_incpos;
   DevBuf<double> d_egx, d_egy, d_earea, d_mval, d_kval, F, U, G, R;
   DevBuf<MatExp> d_mat;
   DevBuf<double4> ev;
@@ -603,6 +730,7 @@ class MeshProblem {
 
   ElemDev elem() const { return {d_edof.get(), d_egx.get(), d_egy.get(), d_earea.get(), d_ereg.get(), nt}; }
   Csr csr() const { return {d_rptr.get(), d_rcol.get(), d_mval.get(), d_kval.get()}; }
+  Csr csr_with(const double* kv) const { return {d_rptr.get(), d_rcol.get(), d_mval.get(), kv}; }
   DftCtx dft() { return DftCtx{N, (size_t)n, stream, &fft_plan, &part2, &red2, h_scalars, &launches}; }
   void launched() {
     ++launches;
@@ -618,7 +746,22 @@ class MeshProblem {
   void choose_nu_hat(const tp_solver_cfg& cfg, double* nu, double* q);
   void static_init(const tp_solver_cfg& cfg, int32_t* counts);
   void factor_blocks();
+  void build_blocks(const double* kvals, DevBuf<cplx>& bandbuf);
+  void periodic_apply(const double* in, double* out, DevBuf<cplx>& bandbuf, const double* kvals,
+                      const tp_solver_cfg& cfg);
   void periodic_solve(const tp_solver_cfg& cfg);
+  // M2 / M3 (solvers.hpp:375-542)
+  struct MethodResult {
+    int iterations = 0, status = 0;
+    int64_t inner_total = 0;
+    std::vector<double> history;
+  };
+  double residual_of(const double* V, double* Rout);
+  double dot(const double* a, const double* b, size_t len);
+  void axpy(double a, const double* x, double* y, size_t len, bool overwrite);
+  void jacobians_csr(const double* Ubase, int count, double ms, double* vals);
+  void solve_m2(const tp_solver_cfg& cfg, MethodResult& res);
+  void solve_m3(const tp_solver_cfg& cfg, MethodResult& res);
 };
 
 
@@ -776,6 +919,18 @@ MeshProblem::MeshProblem(const tp_mesh_desc& d, int dev) : device(dev) {
   }
   rcol.reserve(rptr[n]);
   for (int i = 0; i < n; ++i) rcol.insert(rcol.end(), adj[i].begin(), adj[i].end());
+  // (incidence, corner) -> CSR entry of (its dof, the corner's dof), -1 on the boundary
+  std::vector<int> incpos((size_t)3 * inc.size(), -1);
+  for (int j = 0; j < n; ++j)
+    for (int q = iptr[j]; q < iptr[j + 1]; ++q) {
+      const int t = inc[q] >> 2;
+      for (int c = 0; c < 3; ++c) {
+        const int dc = edof[3 * t + c];
+        if (dc < 0) continue;
+        const auto it = std::lower_bound(rcol.begin() + rptr[j], rcol.begin() + rptr[j + 1], dc);
+        incpos[(size_t)3 * q + c] = (int)(it - rcol.begin());
+      }
+    }
   // consistent sigma-mass (assemble_mass, assembly.hpp:48-65)
   {
     std::vector<Trip> tr;
@@ -904,6 +1059,7 @@ MeshProblem::MeshProblem(const tp_mesh_desc& d, int dev) : device(dev) {
   up_i(d_rcol, rcol);
   up_i(d_perm, perm);
   up_i(d_iperm, iperm);
+  up_i(d_incpos, incpos);
   up_d(d_egx, egx);
   up_d(d_egy, egy);
   up_d(d_earea, earea);
@@ -1145,9 +1301,8 @@ void MeshProblem::static_init(const tp_solver_cfg& cfg, int32_t* counts) {
 }
 
 // PeriodicSolver ctor (periodic.hpp:128-139, 211-248 with every block
-// cached): symbols and one factorisation per frequency
-void MeshProblem::factor_blocks() {
-  require(nu_hat_set, "periodic solver: K_hat not installed (tp_mesh_choose_nu_hat / tp_mesh_set_nu_hat)");
+// cached) for lambda_k M + Kv: symbols and one factorisation per frequency
+void MeshProblem::build_blocks(const double* kvals, DevBuf<cplx>& bandbuf) {
   std::vector<cplx> hl(K);
   for (int k = 0; k < K; ++k) {  // symbol, periodic.hpp:146-152
     if (k == 0) hl[k] = {0.0, 0.0};
@@ -1157,29 +1312,36 @@ void MeshProblem::factor_blocks() {
       hl[k] = {(1.0 - std::cos(a)) / tau, (0.0 - std::sin(a)) / tau};
     }
   }
-  lam.alloc(K);
+  lam.ensure(K);
   TP_CUDA(cudaMemcpy(lam.get(), hl.data(), K * sizeof(cplx), cudaMemcpyHostToDevice));
-  band.alloc((size_t)K * n * (bw + 1));
-  k_band_freq<<<dim3((n + 127) / 128, K), 128, 0, stream>>>(csr(), d_perm.get(), d_iperm.get(), lam.get(),
-                                                           band.get(), n, bw);
+  bandbuf.ensure((size_t)K * n * (bw + 1));
+  k_band_freq<<<dim3((n + 127) / 128, K), 128, 0, stream>>>(csr_with(kvals), d_perm.get(), d_iperm.get(),
+                                                           lam.get(), bandbuf.get(), n, bw);
   launched();
-  band_factor<cplx>(*this, band.get(), K, nullptr);
+  band_factor<cplx>(*this, bandbuf.get(), K, nullptr);
   TP_CUDA(cudaMemcpyAsync(h_scalars, d_fail.get(), sizeof(int), cudaMemcpyDeviceToHost, stream));
   sync();
   int fail = 0;
   std::memcpy(&fail, h_scalars, sizeof(int));
   if (fail) throw Error(TP_ESOLVE, "periodic solver: singular frequency block (zero pivot)", -1.0);
-  Ghat.alloc((size_t)K * n);
-  Uhat.alloc((size_t)K * n);
+  Ghat.ensure((size_t)K * n);
+  Uhat.ensure((size_t)K * n);
+}
+
+void MeshProblem::factor_blocks() {
+  require(nu_hat_set, "periodic solver: K_hat not installed (tp_mesh_choose_nu_hat / tp_mesh_set_nu_hat)");
+  build_blocks(d_kval.get(), band);
   factored = true;
 }
 
-// PeriodicSolver::solve (periodic.hpp:154-198) of the device G into U
-void MeshProblem::periodic_solve(const tp_solver_cfg& cfg) {
-  if (!factored) factor_blocks();
+// PeriodicSolver::solve (periodic.hpp:154-198): in -> out (device, N x n)
+// through the factorised blocks of lambda_k M + Kv
+void MeshProblem::periodic_apply(const double* in, double* out, DevBuf<cplx>& bandbuf, const double* kvals,
+                                 const tp_solver_cfg& cfg) {
   const DftCtx c = dft();
-  dft_forward(c, G.get(), Ghat.get());
-  band_solve<cplx>(*this, band.get(), Ghat.get(), Uhat.get(), K, nullptr, ysc);
+  const Csr A = csr_with(kvals);
+  dft_forward(c, in, Ghat.get());
+  band_solve<cplx>(*this, bandbuf.get(), Ghat.get(), Uhat.get(), K, nullptr, ysc);
   // the per-solve residual contract (solve.hpp:79-89): |b - A x| <= 1e-10 |b|,
   // with up to three steps of iterative refinement (kept while they reduce the
   // residual) for blocks above kRefine = 1e-11 -- as the checker's SparseSolver does
@@ -1192,7 +1354,7 @@ void MeshProblem::periodic_solve(const tp_solver_cfg& cfg) {
   red.ensure((size_t)2 * K);
   std::vector<double> chk((size_t)2 * K);
   auto check = [&](const cplx* X, cplx* Rout, const int* on) {
-    k_freq_check<<<dim3(nb, K), 256, 0, stream>>>(csr(), lam.get(), X, Ghat.get(), part.get(), n, Rout, on);
+    k_freq_check<<<dim3(nb, K), 256, 0, stream>>>(A, lam.get(), X, Ghat.get(), part.get(), n, Rout, on);
     launched();
     k_sum_pairs_rows<<<(K + 3) / 4, 128, 0, stream>>>(part.get(), nb, K, red.get());
     launched();
@@ -1219,7 +1381,7 @@ void MeshProblem::periodic_solve(const tp_solver_cfg& cfg) {
     d_on.ensure(K);
     for (int it = 0; it < 3 && any; ++it) {
       TP_CUDA(cudaMemcpyAsync(d_on.get(), on.data(), K * sizeof(int), cudaMemcpyHostToDevice, stream));
-      band_solve<cplx>(*this, band.get(), Rf.get(), DXf.get(), K, d_on.get(), ysc);
+      band_solve<cplx>(*this, bandbuf.get(), Rf.get(), DXf.get(), K, d_on.get(), ysc);
       k_freq_add<<<dim3(nb, K), 256, 0, stream>>>(Uhat.get(), DXf.get(), X2f.get(), d_on.get(), n);
       launched();
       check(X2f.get(), R2f.get(), d_on.get());
@@ -1243,18 +1405,301 @@ void MeshProblem::periodic_solve(const tp_solver_cfg& cfg) {
     }
   }
   double re2 = 0, im2 = 0;
-  dft_inverse(c, Uhat.get(), U.get(), &re2, &im2);  // synchronises the stream
+  dft_inverse(c, Uhat.get(), out, &re2, &im2);  // synchronises the stream
   for (int k = 0; k < K; ++k)
     if (!(rel[k] <= 1e-10))
       throw Error(TP_ESOLVE, "sparse solve: relative residual " + std::to_string(rel[k]) + " exceeds tolerance",
                   rel[k]);
-  const double rn = std::sqrt(re2), in = std::sqrt(im2);
-  if (in > cfg.imag_tol * std::max(rn, 1e-300))
+  const double rn = std::sqrt(re2), in2 = std::sqrt(im2);
+  if (in2 > cfg.imag_tol * std::max(rn, 1e-300))
     throw Error(TP_ESOLVE,
-                "periodic solver: imaginary residue " + std::to_string(in) + " exceeds " +
+                "periodic solver: imaginary residue " + std::to_string(in2) + " exceeds " +
                     std::to_string(cfg.imag_tol) + " x " + std::to_string(rn),
-                in / std::max(rn, 1e-300));
+                in2 / std::max(rn, 1e-300));
+}
+
+void MeshProblem::periodic_solve(const tp_solver_cfg& cfg) {
+  if (!factored) factor_blocks();
+  periodic_apply(G.get(), U.get(), band, d_kval.get(), cfg);
   state_valid = true;
+}
+
+// ---------------------------------------------------------------- M2 / M3 on meshes
+// ||F - A(V)|| of any device state V (residual, periodic.hpp:35-58), R kept in Rout
+double MeshProblem::residual_of(const double* V, double* Rout) {
+  eval_elements(V, N, nullptr);
+  const int nb = (n + 255) / 256;
+  part.ensure((size_t)N * nb);
+  red.ensure(N);
+  k_resid_rhs<<<dim3(nb, N), 256, 0, stream>>>(elem(), csr(), ev.get(), d_iptr.get(), d_inc.get(), V, F.get(), Rout,
+                                               nullptr, part.get(), n, N, tau);
+  launched();
+  k_sum_rows<<<1, 32, 0, stream>>>(part.get(), N * nb, 1, red.get());
+  launched();
+  TP_CUDA(cudaMemcpyAsync(h_scalars, red.get(), sizeof(double), cudaMemcpyDeviceToHost, stream));
+  sync();
+  return std::sqrt(h_scalars[0]);
+}
+
+double MeshProblem::dot(const double* a, const double* b, size_t len) {
+  const int blocks = (int)std::min<size_t>(4 * 148, (len + 255) / 256);
+  part.ensure(blocks);
+  red.ensure(1);
+  k_dot_parts<<<blocks, 256, 0, stream>>>(a, b, len, part.get());
+  launched();
+  k_sum_rows<<<1, 32, 0, stream>>>(part.get(), blocks, 1, red.get());
+  launched();
+  TP_CUDA(cudaMemcpyAsync(h_scalars, red.get(), sizeof(double), cudaMemcpyDeviceToHost, stream));
+  sync();
+  return h_scalars[0];
+}
+
+void MeshProblem::axpy(double a, const double* x, double* y, size_t len, bool overwrite) {
+  const int blocks = (int)std::min<size_t>(4 * 148, (len + 255) / 256);
+  k_axpy_flat<<<blocks, 256, 0, stream>>>(a, x, y, len, overwrite ? 1 : 0);
+  launched();
+}
+
+// Jacobians J_b(u_b) (+ ms M) on the CSR pattern for `count` slices of Ubase
+void MeshProblem::jacobians_csr(const double* Ubase, int count, double ms, double* vals) {
+  eval_elements(Ubase, count, nullptr);
+  k_csr_jac<<<dim3((n + 127) / 128, count), 128, 0, stream>>>(elem(), ev.get(), d_iptr.get(), d_inc.get(),
+                                                               d_incpos.get(), d_rptr.get(), d_mval.get(), ms, vals,
+                                                               n, (int)rcol.size());
+  launched();
+}
+
+// solve_m3_timestepping (solvers.hpp:489-542): periods of implicit Euler from
+// U0, per step newton_elliptic with mass_scale 1/tau (solvers.hpp:131-182)
+// on J = M/tau + J_K(u) in band form (one block)
+void MeshProblem::solve_m3(const tp_solver_cfg& cfg, MethodResult& res) {
+  require(state_valid, "m3: no initial state");
+  require(cfg.m3_max_cycles >= 1, "m3: iteration caps must be positive");
+  const double inv_tau = 1.0 / tau;
+  const int nnz = (int)rcol.size(), nb = (n + 255) / 256;
+  DevBuf<double> ub(n), rb(n), db(n), ut(n), rt(n), rhs(n), jv(nnz), jb((size_t)n * (bw + 1)), R((size_t)N * n), gs;
+  DevBuf<int> one(1);
+  const int h1 = 1;
+  TP_CUDA(cudaMemcpyAsync(one.get(), &h1, sizeof(int), cudaMemcpyHostToDevice, stream));
+  part.ensure(nb);
+  red.ensure(1);
+  // r = rhs - ms M v - K(v) and its norm (newton_elliptic's residual_at)
+  auto residual_at = [&](const double* v, double* r) {
+    eval_elements(v, 1, nullptr);
+    k_step_res<<<nb, 256, 0, stream>>>(elem(), csr(), ev.get(), d_iptr.get(), d_inc.get(), rhs.get(), v, inv_tau, r,
+                                       part.get(), n);
+    launched();
+    k_sum_rows<<<1, 32, 0, stream>>>(part.get(), nb, 1, red.get());
+    launched();
+    TP_CUDA(cudaMemcpyAsync(h_scalars, red.get(), sizeof(double), cudaMemcpyDeviceToHost, stream));
+    sync();
+    return std::sqrt(h_scalars[0]);
+  };
+  auto newton = [&](int cycle, int step_i) {
+    const auto fail = [&](const std::string& what, double resid) {
+      throw Error(TP_ESOLVE,
+                  "time stepping, cycle " + std::to_string(cycle) + ", step " + std::to_string(step_i + 1) + ": " +
+                      what,
+                  resid);
+    };
+    double rnorm = residual_at(ub.get(), rb.get());
+    const double scale = std::max(std::sqrt(dot(rhs.get(), rhs.get(), n)), rnorm);
+    if (scale == 0 || rnorm <= cfg.static_tol * scale) return;
+    for (int step = 1; step <= cfg.static_max_newton; ++step) {
+      jacobians_csr(ub.get(), 1, inv_tau, jv.get());
+      k_band_csr<<<(n + 127) / 128, 128, 0, stream>>>(d_rptr.get(), d_rcol.get(), jv.get(), d_perm.get(),
+                                                      d_iperm.get(), jb.get(), n, bw);
+      launched();
+      band_factor<double>(*this, jb.get(), 1, nullptr);
+      band_solve<double>(*this, jb.get(), rb.get(), db.get(), 1, nullptr, gs);
+      double alpha = 1.0;
+      bool accepted = false;
+      for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
+        TP_CUDA(cudaMemcpyAsync(ut.get(), ub.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        axpy(alpha, db.get(), ut.get(), n, false);
+        const double tnorm = residual_at(ut.get(), rt.get());
+        if (tnorm <= (1.0 - cfg.armijo_slope * alpha) * rnorm) {
+          TP_CUDA(cudaMemcpyAsync(ub.get(), ut.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+          TP_CUDA(cudaMemcpyAsync(rb.get(), rt.get(), n * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+          rnorm = tnorm;
+          accepted = true;
+          break;
+        }
+        alpha *= cfg.armijo_backtrack;
+      }
+      if (!accepted) fail("newton: line search exhausted at residual " + std::to_string(rnorm), rnorm / scale);
+      if (rnorm <= cfg.static_tol * scale) return;
+    }
+    fail("newton: no convergence within " + std::to_string(cfg.static_max_newton) + " steps", rnorm / scale);
+  };
+  res.history.assign(1, residual_of(U.get(), R.get()));
+  res.status = TP_CONVERGED;
+  res.iterations = 0;
+  auto stop = [&] { return res.history.back() <= cfg.tol * res.history.front(); };
+  TP_CUDA(cudaMemcpyAsync(ub.get(), U.get() + (size_t)(N - 1) * n, n * sizeof(double), cudaMemcpyDeviceToDevice,
+                          stream));
+  while (!stop()) {
+    if (res.iterations >= cfg.m3_max_cycles) {
+      res.status = TP_MAX_ITER;
+      break;
+    }
+    for (int i = 0; i < N; ++i) {
+      // rhs = f_i + (1/tau) M u_prev (solvers.hpp:512-514)
+      k_step_rhs<<<nb, 256, 0, stream>>>(csr(), F.get() + (size_t)i * n, ub.get(), inv_tau, rhs.get(), n);
+      launched();
+      newton(res.iterations + 1, i);
+      TP_CUDA(cudaMemcpyAsync(U.get() + (size_t)i * n, ub.get(), n * sizeof(double), cudaMemcpyDeviceToDevice,
+                              stream));
+    }
+    res.iterations += 1;
+    res.history.push_back(residual_of(U.get(), R.get()));
+    if (stop()) break;
+  }
+  if (stop()) res.status = TP_CONVERGED;
+  sync();
+}
+
+// solve_m2_newton (solvers.hpp:375-484): per outer step the slice Jacobians,
+// their time average as the periodic preconditioner's stiffness (blocks
+// lambda_k M + J_avg factorised as for M1), restarted FGMRES (detail::fgmres,
+// solvers.hpp:187-270; Arnoldi scalars on the host from deterministic device
+// dots, in the reference's order), Armijo on the block residual
+void MeshProblem::solve_m2(const tp_solver_cfg& cfg, MethodResult& res) {
+  require(state_valid, "m2: no initial state");
+  const int restart = cfg.m2_restart, max_total = cfg.m2_inner_max;
+  require(restart >= 1 && max_total >= 1 && cfg.m2_max_outer >= 1, "m2: iteration caps must be positive");
+  require(cfg.m2_inner_tol > 0 && cfg.m2_inner_tol < 1, "m2: inner tolerance must lie in (0,1)");
+  const size_t flat = (size_t)N * n;
+  const int nnz = (int)rcol.size();
+  DevBuf<double> Rv(flat), Rt(flat), trial(flat), delta(flat), w(flat), Jall((size_t)N * nnz), Javg(nnz);
+  DevBuf<cplx> pband;
+  std::vector<DevBuf<double>> V(restart + 1), Z(restart);
+  for (auto& v : V) v.alloc(flat);
+  for (auto& z : Z) z.alloc(flat);
+  double rnorm = residual_of(U.get(), Rv.get());
+  res.history.assign(1, rnorm);
+  res.status = TP_CONVERGED;
+  res.iterations = 0;
+  res.inner_total = 0;
+  auto stop = [&] { return res.history.back() <= cfg.tol * res.history.front(); };
+  auto norm2 = [&](const double* a) { return std::sqrt(dot(a, a, flat)); };
+  while (!stop()) {
+    if (res.iterations >= cfg.m2_max_outer) {
+      res.status = TP_MAX_ITER;
+      break;
+    }
+    jacobians_csr(U.get(), N, 0.0, Jall.get());
+    k_average_rows<<<(nnz + 255) / 256, 256, 0, stream>>>(Jall.get(), (size_t)nnz, N, Javg.get());
+    launched();
+    build_blocks(Javg.get(), pband);
+    auto apply_a = [&](const double* v, double* out) {
+      k_m2_apply_csr<<<dim3((n + 255) / 256, N), 256, 0, stream>>>(csr(), Jall.get(), nnz, v, out, n, N, tau);
+      launched();
+    };
+    auto apply_p = [&](const double* v, double* out) { periodic_apply(v, out, pband, Javg.get(), cfg); };
+    const double bnorm = rnorm;
+    TP_CUDA(cudaMemsetAsync(delta.get(), 0, delta.bytes(), stream));
+    int total = 0;
+    bool inner_ok = bnorm == 0;
+    if (!inner_ok) {
+      const double target = cfg.m2_inner_tol * bnorm;
+      TP_CUDA(cudaMemcpyAsync(w.get(), Rv.get(), flat * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+      while (true) {
+        const double beta = norm2(w.get());
+        if (beta <= target) {
+          inner_ok = true;
+          break;
+        }
+        const int mm = restart;
+        axpy(1.0 / beta, w.get(), V[0].get(), flat, true);
+        std::vector<double> H((size_t)(mm + 1) * mm, 0.0), cs(mm), sn(mm), g(mm + 1, 0.0);
+        auto h = [&](int i, int j) -> double& { return H[(size_t)i * mm + j]; };
+        g[0] = beta;
+        int cols = 0;
+        for (int j = 0; j < mm && total < max_total; ++j, ++total) {
+          apply_p(V[j].get(), Z[j].get());
+          apply_a(Z[j].get(), w.get());
+          for (int i = 0; i <= j; ++i) {
+            const double d = dot(w.get(), V[i].get(), flat);
+            h(i, j) = d;
+            axpy(-d, V[i].get(), w.get(), flat, false);
+          }
+          const double wnorm = norm2(w.get());
+          h(j + 1, j) = wnorm;
+          for (int i = 0; i < j; ++i) {
+            const double t = cs[i] * h(i, j) + sn[i] * h(i + 1, j);
+            h(i + 1, j) = -sn[i] * h(i, j) + cs[i] * h(i + 1, j);
+            h(i, j) = t;
+          }
+          const double denom = std::hypot(h(j, j), h(j + 1, j));
+          if (denom == 0) {
+            cols = j;
+            ++total;
+            break;
+          }
+          cs[j] = h(j, j) / denom;
+          sn[j] = h(j + 1, j) / denom;
+          h(j, j) = denom;
+          h(j + 1, j) = 0;
+          g[j + 1] = -sn[j] * g[j];
+          g[j] = cs[j] * g[j];
+          cols = j + 1;
+          if (wnorm == 0 || std::abs(g[j + 1]) <= target) {
+            ++total;
+            break;
+          }
+          if (j + 1 < mm) axpy(1.0 / wnorm, w.get(), V[j + 1].get(), flat, true);
+        }
+        std::vector<double> y(cols, 0.0);
+        for (int i = cols - 1; i >= 0; --i) {
+          double acc = g[i];
+          for (int j = i + 1; j < cols; ++j) acc -= h(i, j) * y[j];
+          y[i] = acc / h(i, i);
+        }
+        for (int j = 0; j < cols; ++j) axpy(y[j], Z[j].get(), delta.get(), flat, false);
+        apply_a(delta.get(), w.get());   // w = A delta
+        axpy(-1.0, Rv.get(), w.get(), flat, false);  // w = A delta - b
+        axpy(-1.0, w.get(), w.get(), flat, true);    // w = b - A delta
+        if (norm2(w.get()) <= target) {
+          inner_ok = true;
+          break;
+        }
+        if (total >= max_total) break;
+      }
+    }
+    res.inner_total += total;
+    if (!inner_ok)
+      throw Error(TP_ESOLVE, "newton solver: inner linear solve missed its tolerance within " +
+                                 std::to_string(max_total) + " iterations",
+                  -1.0);
+    double alpha = 1.0;
+    bool accepted = false;
+    for (int hv = 0; hv <= cfg.armijo_max_halvings; ++hv) {
+      TP_CUDA(cudaMemcpyAsync(trial.get(), U.get(), flat * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+      axpy(alpha, delta.get(), trial.get(), flat, false);
+      const double tnorm = residual_of(trial.get(), Rt.get());
+      if (tnorm < rnorm && tnorm <= (1.0 - cfg.armijo_slope * alpha) * rnorm) {
+        TP_CUDA(cudaMemcpyAsync(U.get(), trial.get(), flat * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        TP_CUDA(cudaMemcpyAsync(Rv.get(), Rt.get(), flat * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+        rnorm = tnorm;
+        accepted = true;
+        break;
+      }
+      alpha *= cfg.armijo_backtrack;
+    }
+    if (!accepted) {
+      res.status = TP_STALLED;
+      break;
+    }
+    res.iterations += 1;
+    res.history.push_back(rnorm);
+    if (stop()) {
+      res.status = TP_CONVERGED;
+      break;
+    }
+  }
+  if (stop()) res.status = TP_CONVERGED;
+  sync();
 }
 
 }  // namespace tpgpu
@@ -1544,5 +1989,55 @@ int tp_mesh_m1_sweep(tp_mesh_problem* h, double* residual) {
 void* tp_mesh_problem_stream(tp_mesh_problem* h) { return h && h->impl ? (void*)h->impl->stream : nullptr; }
 
 int64_t tp_mesh_problem_launches(const tp_mesh_problem* h) { return h && h->impl ? h->impl->launches.load() : 0; }
+
+}  // extern "C"
+
+namespace {
+int mesh_m23(tp_mesh_problem* h, const tp_solver_cfg* c, const double* U0, double* U_out, tp_report* rep,
+             double* history, double* contraction, int32_t cap, bool m2) {
+  return mguard([&] {
+    auto& p = MP(h);
+    const tp_solver_cfg cfg = mcfg(c);
+    tpgpu::validate_cfg(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    if (U0) {
+      TP_CUDA(cudaMemcpyAsync(p.U.get(), U0, p.U.bytes(), cudaMemcpyHostToDevice, p.stream));
+      p.state_valid = true;
+    }
+    tpgpu::MeshProblem::MethodResult res;
+    if (m2) p.solve_m2(cfg, res);
+    else p.solve_m3(cfg, res);
+    tp_report r{};
+    r.iterations = res.iterations;
+    r.status = res.status;
+    r.inner_iterations = (int32_t)res.inner_total;
+    r.q_estimate = std::numeric_limits<double>::quiet_NaN();
+    r.history_len = (int32_t)std::min<size_t>(res.history.size(), cap > 0 ? cap : 0);
+    if (history)
+      for (int k = 0; k < r.history_len; ++k) history[k] = res.history[k];
+    if (contraction)
+      for (size_t k = 0; k + 1 < res.history.size() && (int)k < cap; ++k)
+        contraction[k] = res.history[k] > 0 ? res.history[k + 1] / res.history[k] : 0.0;
+    if (U_out) {
+      TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      p.sync();
+    }
+    r.wall_time = secs(t0);
+    if (rep) *rep = r;
+  });
+}
+}  // namespace
+
+extern "C" {
+
+int tp_mesh_solve_m2(tp_mesh_problem* h, const tp_solver_cfg* cfg, const double* U0, double* U_out, tp_report* rep,
+                     double* history, double* contraction, int32_t cap) {
+  return mesh_m23(h, cfg, U0, U_out, rep, history, contraction, cap, true);
+}
+
+int tp_mesh_solve_m3(tp_mesh_problem* h, const tp_solver_cfg* cfg, const double* U0, double* U_out, tp_report* rep,
+                     double* history, double* contraction, int32_t cap) {
+  return mesh_m23(h, cfg, U0, U_out, rep, history, contraction, cap, false);
+}
 
 }  // extern "C"

@@ -10,6 +10,8 @@ Names follow tpfem (/root/reference/proj/include/tpfem):
   MeshProblem.choose_nu_hat   choose_nu_hat + flux_bounds  assembly.hpp:236-303
   MeshProblem.solve_m1_fixed_point  solve_m1_fixed_point  solvers.hpp:301-369
   MeshProblem.periodic_solve  PeriodicSolver::solve     periodic.hpp:154-198
+  MeshProblem.solve_m2_newton solve_m2_newton           solvers.hpp:375-484
+  MeshProblem.solve_m3_timestepping solve_m3_timestepping solvers.hpp:489-542
   MeshProblem.residual        residual + block_l2       periodic.hpp:35-67
   MeshProblem.apply_k         NonlinearOperator::apply  assembly.hpp:126-140
 Errors as in api.py (ValueError / SolveError / RuntimeError); no CPU fallback.
@@ -30,7 +32,7 @@ MESH_EXPORTS = [
     "tp_mesh_problem_sizes", "tp_mesh_loads", "tp_mesh_apply_k", "tp_mesh_residual", "tp_mesh_static_init",
     "tp_mesh_set_state", "tp_mesh_get_state", "tp_mesh_choose_nu_hat", "tp_mesh_set_nu_hat",
     "tp_mesh_periodic_solve", "tp_mesh_solve_m1", "tp_mesh_m1_begin", "tp_mesh_m1_sweep", "tp_mesh_problem_stream",
-    "tp_mesh_problem_launches",
+    "tp_mesh_problem_launches", "tp_mesh_solve_m2", "tp_mesh_solve_m3",
 ]
 
 
@@ -70,6 +72,8 @@ def _mlib():
         L.tp_mesh_set_nu_hat.argtypes = [vp, dp, C.c_double]
         L.tp_mesh_periodic_solve.argtypes = [vp, G, dp, dp]
         L.tp_mesh_solve_m1.argtypes = [vp, G, dp, dp, C.POINTER(TpReport), dp, dp, C.c_int32, TP_ITERATE_CB, vp]
+        for fn in ("tp_mesh_solve_m2", "tp_mesh_solve_m3"):
+            getattr(L, fn).argtypes = [vp, G, dp, dp, C.POINTER(TpReport), dp, dp, C.c_int32]
         L.tp_mesh_m1_begin.argtypes = [vp, G, dp]
         L.tp_mesh_m1_sweep.argtypes = [vp, dp]
         L.tp_mesh_problem_stream.argtypes = [vp]
@@ -231,6 +235,29 @@ class MeshProblem:
                               contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
                               wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
                               setup_time=rep.setup_time, sweep_time=rep.sweep_time)
+
+    def _m23(self, fn, method, cap, U0, cfg):
+        U0a = None if U0 is None else self._state(U0)
+        hist, contr = np.zeros(cap), np.zeros(cap)
+        U = np.zeros(self.shape)
+        rep = TpReport()
+        _check(getattr(_mlib(), fn)(self._h, C.byref(cfg), _dp(U0a), _dp(U), C.byref(rep), _dp(hist), _dp(contr),
+                                    cap))
+        k = rep.history_len
+        return U, SolveReport(method=method, iterations=rep.iterations, residual_history=hist[:k].tolist(),
+                              contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
+                              wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
+                              inner_iterations=rep.inner_iterations)
+
+    def solve_m2_newton(self, U0=None, cfg: TpSolverCfg | None = None):
+        """solve_m2_newton (solvers.hpp:375-484) -> (U, SolveReport)."""
+        cfg = cfg or default_cfg()
+        return self._m23("tp_mesh_solve_m2", "m2", cfg.m2_max_outer + 1, U0, cfg)
+
+    def solve_m3_timestepping(self, U0=None, cfg: TpSolverCfg | None = None):
+        """solve_m3_timestepping (solvers.hpp:489-542) -> (U, SolveReport)."""
+        cfg = cfg or default_cfg()
+        return self._m23("tp_mesh_solve_m3", "m3", cfg.m3_max_cycles + 1, U0, cfg)
 
     def m1_begin(self, cfg: TpSolverCfg | None = None) -> float:
         cfg = cfg or default_cfg()

@@ -169,3 +169,31 @@ def test_reference_side_adapter_drop_in():
     assert out.returncode == 0, r
     assert r["newton_equal"] and r["cpu_iterations"] == r["gpu_iterations"] == 45
     assert r["final_rel"] <= ITERATE_TOL and r["nu_hat_rel"] <= 1e-12
+
+
+@pytest.mark.parametrize("j_amp,tol", [(0.0, 1e-4), (9.5e5, 1e-8)])
+def test_m2_newton_on_reference_mesh(ref, j_amp, tol):
+    """transformer.json's "method": "all" -- M2 (solve_m2_newton): same Newton
+    step count and status, final state within 1e-10."""
+    c = ref.tr_cfg(j_amp=j_amp)
+    cfg = default_cfg(tol=tol)
+    U0, _ = ref.tr_static_init(c, cfg)
+    Ur, hr, kr, sr, _ = ref.tr_solve_m23(c, 2, U0, cfg)
+    with MeshProblem.transformer(j_amp=j_amp or None) as p:
+        U, rep = p.solve_m2_newton(U0, cfg)
+    assert rep.iterations == kr and {"converged": 0, "max_iter": 1, "stalled": 2}[rep.status] == sr
+    assert rel(U, Ur) <= ITERATE_TOL
+    assert np.allclose(rep.residual_history[:2], hr[:2], rtol=1e-10)
+
+
+def test_m3_timestepping_on_reference_mesh(ref):
+    """M3 (solve_m3_timestepping), two periods of the saturated transformer."""
+    c = ref.tr_cfg(j_amp=9.5e5)
+    cfg = default_cfg(tol=1e-8, m3_max_cycles=2)
+    U0, _ = ref.tr_static_init(c, cfg)
+    Ur, hr, kr, sr, _ = ref.tr_solve_m23(c, 3, U0, cfg)
+    with MeshProblem.transformer(j_amp=9.5e5) as p:
+        U, rep = p.solve_m3_timestepping(U0, cfg)
+    assert rep.iterations == kr == 2 and rep.status == "max_iter" and sr == 1
+    assert rel(U, Ur) <= ITERATE_TOL
+    assert np.allclose(rep.residual_history, hr, rtol=1e-8)
