@@ -2,6 +2,13 @@
 runner's output files (report.json, residuals.csv; runner.hpp:174-223).
 
     python -m paper_2502_21013_b200.run --config 1 --out out/cfg1 [--tol 1e-8]
+    python -m paper_2502_21013_b200.run --ref-config configs/transformer.json [--out dir]
+
+The second form reads the reference's own run configs (problem "transformer":
+parse_run_config, config.hpp:176-230 -- method m1/m2/m3/all, nx, ny,
+refinements, steps, period, solver, flux, materials) and runs them on the
+general-mesh path (mesh.py): setup_transformer + run_transformer_method
+(runner.hpp:46-89); VTK fields/mesh are not written.
 
 static_init (U0) -> frozen-field nu_hat -> M1 fixed-point iteration on the
 device, then report.json / residuals.csv in the reference's formats
@@ -18,13 +25,86 @@ import time
 import numpy as np
 
 
+SOLVER_KEYS = {"tol": "tol", "max_outer_m1": "m1_max_outer", "max_outer_m2": "m2_max_outer",
+               "m3_max_cycles": "m3_max_cycles", "static_tol": "static_tol", "static_max_newton": "static_max_newton",
+               "m2_inner_tol": "m2_inner_tol", "m2_inner_max": "m2_inner_max", "m2_restart": "m2_restart",
+               "imag_tol": "imag_tol"}
+
+
+def run_ref_config(path: str, out: str | None, device: int) -> int:
+    """A reference run config (configs/*.json, problem "transformer") on the device."""
+    import json
+
+    from . import default_cfg
+    from . import report as R
+    from .abi import TP_NU_HAT_THEORY
+    from .mesh import REGIONS, MeshProblem, transformer_materials, transformer_mesh
+
+    j = json.load(open(path))
+    if j.get("problem", "transformer") != "transformer":
+        raise SystemExit("only problem \"transformer\" runs on the device (the toy problem is out of scope)")
+    if "sweep" in j:
+        raise SystemExit("sweep configs (tpfem table) are not supported here")
+    method = j.get("method", "m1")
+    methods = ["m1", "m2", "m3"] if method == "all" else [method]
+    nx, ny, refinements = j.get("nx", 40), j.get("ny", 40), j.get("refinements", 0)
+    steps, period = j.get("steps", 64), j.get("period", 0.02)
+    cfg = default_cfg()
+    sv = j.get("solver", {})
+    for k, v in sv.items():
+        if k in SOLVER_KEYS:
+            setattr(cfg, SOLVER_KEYS[k], v)
+        elif k == "nu_hat_mode":
+            cfg.nu_hat_mode = TP_NU_HAT_THEORY if v == "theory" else 1
+        elif k == "armijo":
+            cfg.armijo_slope = v.get("slope", cfg.armijo_slope)
+            cfg.armijo_backtrack = v.get("backtrack", cfg.armijo_backtrack)
+            cfg.armijo_max_halvings = v.get("max_halvings", cfg.armijo_max_halvings)
+    cfg.threads = j.get("threads", cfg.threads)
+    flux = j.get("flux", {})
+    mats = transformer_materials()
+    for name, entry in j.get("materials", {}).items():  # parse_materials (config.hpp:146-170)
+        r = REGIONS.index(name)
+        for fld, v in entry.items():
+            setattr(mats[r], fld, v)
+    V, T, Rg, _ = transformer_mesh(nx, ny, refinements)
+    out = out or j.get("output_dir", ".")
+    with MeshProblem(V, T, Rg, mats, steps, period, flux.get("s_max", 3.0), flux.get("samples", 10001),
+                     device=device) as p:
+        t0 = time.perf_counter()
+        U0, counts = p.static_init(cfg)
+        nu, q = p.choose_nu_hat(cfg)
+        init_s = time.perf_counter() - t0
+        print(f"transformer: {p.n_dof} unknowns, {steps} steps, initialization {R.format_double(init_s)} s")
+        reports = []
+        for meth in methods:
+            fn = {"m1": p.solve_m1_fixed_point, "m2": p.solve_m2_newton, "m3": p.solve_m3_timestepping}[meth]
+            _, rep = fn(U0, cfg)
+            unit = "cycles" if meth == "m3" else "iterations"
+            print(f"{meth}: {rep.status} after {rep.iterations} {unit} ({R.format_double(rep.wall_time)} s), "
+                  f"residual {R.format_double(rep.residual_history[-1])}")
+            reports.append((meth, rep))
+        tau = period / steps
+        rj = {"problem": "transformer", "steps": int(steps), "n_dof": int(p.n_dof), "refinements": int(refinements),
+              "period": float(period), "tau": float(tau), "threads": int(cfg.threads),
+              "nu_hat": {REGIONS[r]: float(nu[r]) for r in range(5)}, "q_estimate": float(q),
+              "init": {"seconds": float(init_s), "max_newton_steps": int(max(counts) if len(counts) else 0)},
+              "frequency_symbol_abs": [float(x) for x in R.symbol_abs(steps, tau)],
+              "methods": {mm: R.report_to_dict(r, mm) for mm, r in reports}}
+    R.ensure_dir(out)
+    R.write_json(os.path.join(out, "report.json"), rj)
+    R.write_residuals_csv(os.path.join(out, "residuals.csv"), reports)
+    return R.exit_code([r.status for _, r in reports])
+
+
 def main(argv=None) -> int:
     from . import Problem, baseline_desc, default_cfg
     from . import report as R
 
     ap = argparse.ArgumentParser(prog="python -m paper_2502_21013_b200.run")
     ap.add_argument("--config", type=int, default=0, help="BASELINE config 0..5")
-    ap.add_argument("--out", required=True, help="output directory")
+    ap.add_argument("--ref-config", default=None, help="a reference run config (configs/*.json, transformer)")
+    ap.add_argument("--out", default=None, help="output directory")
     ap.add_argument("--tol", type=float, default=1e-8)
     ap.add_argument("--max-outer", type=int, default=200)
     ap.add_argument("--cells", type=int, default=0, help="override the grid (cells per side)")
@@ -33,6 +113,10 @@ def main(argv=None) -> int:
     ap.add_argument("--device", type=int, default=0)
     ap.add_argument("--methods", default="m1", help="comma list of m1, m2, m3 (run from the same U0)")
     a = ap.parse_args(argv)
+    if a.ref_config:
+        return run_ref_config(a.ref_config, a.out, a.device)
+    if not a.out:
+        ap.error("--out is required")
 
     desc = baseline_desc(a.config)
     if a.cells:

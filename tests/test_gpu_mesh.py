@@ -197,3 +197,33 @@ def test_m3_timestepping_on_reference_mesh(ref):
     assert rep.iterations == kr == 2 and rep.status == "max_iter" and sr == 1
     assert rel(U, Ur) <= ITERATE_TOL
     assert np.allclose(rep.residual_history, hr, rtol=1e-8)
+
+
+def test_reference_run_config_cli(ref, tmp_path):
+    """python -m paper_2502_21013_b200.run --ref-config: a run config in the
+    reference's format (the fields of configs/transformer_saturated.json with
+    method "all"; parse_run_config, config.hpp:176-230) -> report.json /
+    residuals.csv in the runner's formats, iteration counts as the reference's."""
+    import json
+    from paper_2502_21013_b200 import run
+    conf = {"problem": "transformer", "method": "all", "nx": 40, "ny": 40, "refinements": 0, "steps": 64,
+            "period": 0.02, "threads": 1, "output_dir": str(tmp_path / "out"),
+            "materials": {"winding_plus": {"j_amp": 950000.0}, "winding_minus": {"j_amp": -950000.0}},
+            "solver": {"tol": 1e-4, "nu_hat_mode": "frozen_field", "m3_max_cycles": 2}}
+    path = tmp_path / "run.json"
+    path.write_text(json.dumps(conf))
+    code = run.main(["--ref-config", str(path)])
+    rj = json.loads((tmp_path / "out" / "report.json").read_text())
+    assert rj["problem"] == "transformer" and rj["n_dof"] == 2142 and len(rj["frequency_symbol_abs"]) == 33
+    c = ref.tr_cfg(j_amp=9.5e5)
+    cfg = default_cfg(tol=1e-4, m3_max_cycles=2)
+    U0, counts = ref.tr_static_init(c, cfg)
+    nu, q = ref.tr_choose_nu_hat(c, U0, cfg)
+    m1 = ref.tr_solve_m1(c, nu, q, U0, cfg)
+    _, _, k2, s2, _ = ref.tr_solve_m23(c, 2, U0, cfg)
+    _, _, k3, s3, _ = ref.tr_solve_m23(c, 3, U0, cfg)
+    assert rj["init"]["max_newton_steps"] == int(counts.max())
+    assert abs(rj["q_estimate"] - q) <= 1e-12
+    assert [rj["methods"][m]["iterations"] for m in ("m1", "m2", "m3")] == [m1.iterations, k2, k3]
+    assert code == (0 if (m1.status, s2, s3) == (0, 0, 0) else 2)
+    assert (tmp_path / "out" / "residuals.csv").read_text().startswith("method,")
