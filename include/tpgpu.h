@@ -113,7 +113,7 @@ typedef struct tp_solver_cfg {
   int32_t freq_chunk;         /* frequencies per batched solve (0 = automatic) */
   int32_t slice_chunk;        /* slices per batched Newton solve (0 = automatic) */
   int32_t freq_groups;        /* frequency groups solved concurrently on their own
-                                 streams (0 = automatic: 3) */
+                                 streams (0 = automatic: 5) */
   /* M2 all-at-once Newton (SolverConfig m2_*, solvers.hpp:52,63-65) */
   int32_t m2_max_outer;       /* default 50 */
   double m2_inner_tol;        /* FGMRES relative tolerance, default 1e-8 */

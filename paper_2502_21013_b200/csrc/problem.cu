@@ -336,7 +336,7 @@ void Problem::install_nu_hat(const double* nu, double q) {
 // for (lambda_k M + K_hat), all frequencies sharing the real stencils.
 void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
   require(nu_hat_set, "periodic solver: nu_hat not installed");
-  static const int env_groups = std::getenv("TPGPU_FREQ_GROUPS") ? std::atoi(std::getenv("TPGPU_FREQ_GROUPS")) : 3;
+  static const int env_groups = std::getenv("TPGPU_FREQ_GROUPS") ? std::atoi(std::getenv("TPGPU_FREQ_GROUPS")) : 5;
   const int want_groups = cfg.freq_groups > 0 ? cfg.freq_groups : env_groups;
   if (freq_ready && fw && (cfg.freq_chunk <= 0 || cfg.freq_chunk == fw->req_chunk) &&
       (want_groups == fw->req_groups)) {
@@ -467,11 +467,13 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
     // iterations, the sweep's critical path) highest, group 1 next, the rest
     // default -- the other groups fill the gaps of its latency-bound chain
     // (cfg 1: 3.85 -> 3.76 ms per sweep).  TPGPU_GROUP_PRIO=0: all default.
-    static const bool prio = !std::getenv("TPGPU_GROUP_PRIO") || std::atoi(std::getenv("TPGPU_GROUP_PRIO")) != 0;
+    // TPGPU_GROUP_PRIO=2: priorities graded over the whole range, group 0 highest
+    static const int prio = std::getenv("TPGPU_GROUP_PRIO") ? std::atoi(std::getenv("TPGPU_GROUP_PRIO")) : 1;
     int lo = 0, hi = 0;
     TP_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));  // hi: numerically smallest = highest
     for (int g = 0; g < parts; ++g) {
-      const int pr = !prio ? lo : g == 0 ? hi : g == 1 ? std::max(hi, lo - 1) : lo;
+      const int graded = parts > 1 ? hi + (int)std::lround((double)(lo - hi) * g / (parts - 1)) : hi;
+      const int pr = prio == 0 ? lo : prio == 2 ? graded : g == 0 ? hi : g == 1 ? std::max(hi, lo - 1) : lo;
       TP_CUDA(cudaStreamCreateWithPriority(&w->hs[g], cudaStreamNonBlocking, pr));
     }
     TP_CUDA(cudaEventCreateWithFlags(&w->ev_in, cudaEventDisableTiming));
