@@ -227,3 +227,26 @@ def test_reference_run_config_cli(ref, tmp_path):
     assert [rj["methods"][m]["iterations"] for m in ("m1", "m2", "m3")] == [m1.iterations, k2, k3]
     assert code == (0 if (m1.status, s2, s3) == (0, 0, 0) else 2)
     assert (tmp_path / "out" / "residuals.csv").read_text().startswith("method,")
+
+
+@pytest.mark.parametrize("steps", [1, 2, 3])
+def test_tiny_step_counts(ref, steps):
+    """N = 1 (the block is K_hat alone, test_periodic.cpp:96-107), N = 2, odd N = 3:
+    periodic solve and a few M1 sweeps against the reference."""
+    c = ref.tr_cfg(nx=12, ny=10, j_amp=9.5e5, steps=steps)
+    cfg = default_cfg(tol=1e-8, m1_max_outer=4)
+    U0, counts = ref.tr_static_init(c, cfg)
+    nu, q = ref.tr_choose_nu_hat(c, U0, cfg)
+    G = ref.tr_loads(c) + np.random.default_rng(steps).standard_normal(U0.shape)
+    Ur = ref.tr_periodic_solve(c, nu, G, cfg)
+    r = ref.tr_solve_m1(c, nu, q, U0, cfg, keep_iterates=True)
+    V, T, R, _ = transformer_mesh(12, 10, 0)
+    with MeshProblem(V, T, R, transformer_materials(9.5e5), steps, 0.02) as p:
+        U0g, cg = p.static_init(cfg)
+        assert np.array_equal(cg, counts)
+        p.set_nu_hat(nu, q)
+        assert rel(p.periodic_solve(G, cfg), Ur) <= 1e-10
+        log = []
+        U, rep = p.solve_m1_fixed_point(U0, cfg, iterate_log=log)
+    assert rep.iterations == r.iterations
+    assert max(rel(a, b) for a, b in zip(log, r.iterates)) <= ITERATE_TOL
