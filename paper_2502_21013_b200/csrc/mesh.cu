@@ -984,7 +984,7 @@ MeshProblem::MeshProblem(const tp_mesh_desc& d, int dev) : device(dev) {
     for (int root = 0; root < n; ++root) {
       if (seen[root]) continue;
       // component's min-degree vertex, then peripheral refinement
-      int s = root, last = root, ecc = 0;
+      int s = root, ecc = 0;
       for (int it = 0; it < 8; ++it) {
         int l2, e2;
         bfs_levels(s, l2, e2);
@@ -1006,7 +1006,6 @@ MeshProblem::MeshProblem(const tp_mesh_desc& d, int dev) : device(dev) {
         std::stable_sort(nb.begin(), nb.end(), [&](int a, int b) { return deg[a] < deg[b]; });
         order.insert(order.end(), nb.begin(), nb.end());
       }
-      (void)last;
     }
     std::reverse(order.begin(), order.end());
     std::vector<int> ip(n), nat(n);
@@ -1201,7 +1200,7 @@ void MeshProblem::static_init(const tp_solver_cfg& cfg, int32_t* counts) {
   std::vector<int> cnt(N, 0);
   std::vector<int> hs(S), hon(S), hacc(S);
   std::vector<double> ha(S), rn(S), sc(S), tn(S);
-  auto norms = [&](const double* base, const int* slots_on) {
+  auto norms = [&](const double* base) {
     // r = F - K(v) for every slot, norms to the host
     eval_elements(base, S, nullptr);
     k_newton_res<<<dim3(nb, S), 256, 0, stream>>>(elem(), ev.get(), d_iptr.get(), d_inc.get(), F.get(), d_sl.get(),
@@ -1212,7 +1211,6 @@ void MeshProblem::static_init(const tp_solver_cfg& cfg, int32_t* counts) {
     TP_CUDA(cudaMemcpyAsync(tn.data(), nrm.get(), S * sizeof(double), cudaMemcpyDeviceToHost, stream));
     sync();
     for (int b = 0; b < S; ++b) tn[b] = std::sqrt(tn[b]);
-    (void)slots_on;
   };
   for (int s0 = 0; s0 < N; s0 += S) {
     const int cb = std::min(S, N - s0);
@@ -1220,7 +1218,7 @@ void MeshProblem::static_init(const tp_solver_cfg& cfg, int32_t* counts) {
     TP_CUDA(cudaMemcpyAsync(d_sl.get(), hs.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
     TP_CUDA(cudaMemsetAsync(Ub.get(), 0, Ub.bytes(), stream));
     // ||rhs|| and the initial residual (u = 0: r = rhs - K(0))
-    norms(Ub.get(), nullptr);
+    norms(Ub.get());
     for (int b = 0; b < S; ++b) {
       rn[b] = tn[b];
       sc[b] = rn[b];  // max(|rhs|, r0) with r0 = |rhs - K(0)| = |rhs|
@@ -1255,7 +1253,7 @@ void MeshProblem::static_init(const tp_solver_cfg& cfg, int32_t* counts) {
         TP_CUDA(cudaMemcpyAsync(d_acc.get(), searching.data(), S * sizeof(int), cudaMemcpyHostToDevice, stream));
         k_axpy_slots<<<dim3(nb, S), 256, 0, stream>>>(Ub.get(), Db.get(), d_alpha.get(), d_acc.get(), Ut.get(), n);
         launched();
-        norms(Ut.get(), nullptr);
+        norms(Ut.get());
         for (int b = 0; b < S; ++b) {
           hacc[b] = 0;
           if (!searching[b]) continue;
