@@ -300,7 +300,7 @@ def run_b200(args):
         roofline["measured"] = ("live in bench.py: CUDA events around every launch on its stream, over "
                                 f"{args.calib_sweeps} sweeps run right after the timed region with the frequency "
                                 "groups serialized (freq_groups=1), so launches do not overlap other kernels")
-        roofline["in_timed_region"] = dict(timed, note="3 concurrent frequency groups: a launch's event span "
+        roofline["in_timed_region"] = dict(timed, note="concurrent frequency groups (5 by default): a launch's event span "
                                            "includes the other groups' kernels")
     else:
         roofline.update(timed)
