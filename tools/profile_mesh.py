@@ -5,7 +5,6 @@ timed sweeps are captured.
     python tools/profile_mesh.py [--refinements 0] [--steps 64] [--sweeps 10]
 """
 import argparse
-import ctypes as C
 import os
 import sys
 import time
@@ -23,7 +22,6 @@ ap.add_argument("--steps", type=int, default=64)
 ap.add_argument("--sweeps", type=int, default=10)
 ap.add_argument("--j-amp", type=float, default=9.5e5)
 a = ap.parse_args()
-cudart = C.CDLL("libcudart.so") if False else None
 cfg = default_cfg(tol=1e-8)
 p = MeshProblem.transformer(a.nx, a.nx, a.refinements, a.steps, 0.02, j_amp=a.j_amp)
 t = time.perf_counter()
