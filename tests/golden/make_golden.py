@@ -64,10 +64,35 @@ def cfg1(sweeps=2):
     print("cfg1:", time.time() - t, "s; history", r.history)
 
 
+def transformer():
+    """The reference's own transformer problem (mesh.hpp / materials.hpp
+    physics, transformer_saturated.json windings) through tpfem's setup and
+    solve_m1_fixed_point: full vectors on a 12 x 10 mesh (N = 8), counts,
+    histories, checksums and samples on the 40 x 40 mesh (N = 64)."""
+    cfg = default_cfg(tol=1e-8)
+    out = {}
+    for tag, c in (("small", ref.tr_cfg(nx=12, ny=10, steps=8, j_amp=9.5e5)), ("sat", ref.tr_cfg(j_amp=9.5e5))):
+        U0, counts = ref.tr_static_init(c, cfg)
+        nu, q = ref.tr_choose_nu_hat(c, U0, cfg)
+        r = ref.tr_solve_m1(c, nu, q, U0, cfg)
+        out.update({f"{tag}_newton_counts": counts, f"{tag}_nu_hat": nu, f"{tag}_q": q,
+                    f"{tag}_history": r.history, f"{tag}_iterations": r.iterations,
+                    f"{tag}_U_checksum": checksum(r.U), f"{tag}_U0_checksum": checksum(U0),
+                    f"{tag}_U_sample": r.U.reshape(-1)[::97], f"{tag}_U0_sample": U0.reshape(-1)[::97]})
+        if tag == "small":
+            out.update({"small_U0": U0, "small_U": r.U})
+        print("transformer", tag, "iterations", r.iterations)
+    np.savez_compressed(os.path.join(OUT, "transformer_reference.npz"), **out)
+
+
 if __name__ == "__main__":
     ap = argparse.ArgumentParser()
     ap.add_argument("--cfg1", action="store_true")
+    ap.add_argument("--transformer", action="store_true")
     a = ap.parse_args()
+    if a.transformer:
+        transformer()
+        sys.exit(0)
     cfg0()
     if a.cfg1:
         cfg1()

@@ -250,3 +250,23 @@ def test_tiny_step_counts(ref, steps):
         U, rep = p.solve_m1_fixed_point(U0, cfg, iterate_log=log)
     assert rep.iterations == r.iterations
     assert max(rel(a, b) for a, b in zip(log, r.iterates)) <= ITERATE_TOL
+
+
+def test_transformer_golden_fixture():
+    """Against tests/golden/transformer_reference.npz (written by the reference
+    itself, tests/golden/make_golden.py --transformer): runs without oracle/_ref."""
+    import os
+    g = np.load(os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden", "transformer_reference.npz"))
+    cfg = default_cfg(tol=1e-8)
+    for tag, args in (("small", (12, 10, 0, 8)), ("sat", (40, 40, 0, 64))):
+        with MeshProblem.transformer(*args, 0.02, j_amp=9.5e5) as p:
+            U0, counts = p.static_init(cfg)
+            nu, q = p.choose_nu_hat(cfg)
+            U, rep = p.solve_m1_fixed_point(None, cfg)
+        assert np.array_equal(counts, g[f"{tag}_newton_counts"])
+        assert rel(nu, g[f"{tag}_nu_hat"]) <= 1e-12 and abs(q - float(g[f"{tag}_q"])) <= 1e-12
+        assert rep.iterations == int(g[f"{tag}_iterations"])
+        assert rel(U.reshape(-1)[::97], g[f"{tag}_U_sample"]) <= ITERATE_TOL
+        assert rel(U0.reshape(-1)[::97], g[f"{tag}_U0_sample"]) <= ITERATE_TOL
+        if tag == "small":
+            assert rel(U, g["small_U"]) <= ITERATE_TOL and rel(U0, g["small_U0"]) <= ITERATE_TOL
