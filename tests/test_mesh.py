@@ -112,3 +112,17 @@ def test_mesh_problem_without_gpu_fails_loudly():
         pass
     with pytest.raises(RuntimeError):
         mesh.MeshProblem.transformer()
+
+
+def test_oracle_transformer_matches_golden(ref):
+    """The checker (the reference's own transformer pipeline in oracle/_ref)
+    reproduces the committed fixture bit for bit (same host arithmetic)."""
+    from paper_2502_21013_b200.abi import default_cfg
+    g = np.load(os.path.join(ROOT, "tests", "golden", "transformer_reference.npz"))
+    c = ref.tr_cfg(nx=12, ny=10, steps=8, j_amp=9.5e5)
+    cfg = default_cfg(tol=1e-8)
+    U0, counts = ref.tr_static_init(c, cfg)
+    nu, q = ref.tr_choose_nu_hat(c, U0, cfg)
+    r = ref.tr_solve_m1(c, nu, q, U0, cfg)
+    assert np.array_equal(counts, g["small_newton_counts"]) and r.iterations == int(g["small_iterations"])
+    assert np.array_equal(U0, g["small_U0"]) and np.array_equal(r.U, g["small_U"])
