@@ -476,7 +476,8 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
   // Stockham: P N / 16 threads (16 values each per pass), P N ~ 2048 complex
   // (36 KB of shared memory with the twiddles: six blocks per SM)
   if (pl->pow2 && N >= 16 && !std::getenv("TPGPU_RADIX2_DFT")) {
-    int sP = std::max(1, 2048 / N);
+    static const int fp_env = std::getenv("TPGPU_FFT_P") ? std::atoi(std::getenv("TPGPU_FFT_P")) : 0;
+    int sP = fp_env > 0 ? fp_env : std::max(1, 2048 / N);
     while (sP > 1 && (size_t)(sP + 1) * N * sizeof(cplx) > 100 * 1024) sP >>= 1;
     const int T = sP * N / 16;
     if (T <= 1024 && (size_t)((sP + 1) * N + (N / 2 + 1) * 2 * sP) * sizeof(cplx) <= 200 * 1024) {
