@@ -236,6 +236,19 @@ int tp_shard_plan_make(int32_t cells, int32_t steps, int32_t nranks, int32_t ran
 /* ncclGetUniqueId on one rank; the caller broadcasts the 128 bytes. */
 int tp_nccl_unique_id(unsigned char id[128]);
 int tp_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device, tp_comm** out);
+/* Host-staged transport (no NCCL): every exchange of the sharded sweep is
+ * staged through pinned host memory and handed to `fn`, which must deliver
+ * send_buf[i] (send_bytes[i]) to rank send_peer[i] and fill recv_buf[i]
+ * (recv_bytes[i]) with what rank recv_peer[i] sent this rank in the same
+ * call (peers never equal this rank; transfers to self stay on the device).
+ * Returns 0 on success.  For ranks sharing one GPU (tests) or hosts without
+ * NVLink; the stream is drained before each call, so no kernel ever waits on
+ * another process. */
+typedef int (*tp_host_exchange_fn)(void* user, int32_t nsend, const int32_t* send_peer,
+                                   const void* const* send_buf, const size_t* send_bytes, int32_t nrecv,
+                                   const int32_t* recv_peer, void* const* recv_buf, const size_t* recv_bytes);
+int tp_comm_create_host(int32_t nranks, int32_t rank, int32_t device, tp_host_exchange_fn fn, void* user,
+                        tp_comm** out);
 void tp_comm_destroy(tp_comm* c);
 void* tp_comm_nccl(tp_comm* c);
 int32_t tp_comm_rank(const tp_comm* c);

@@ -255,18 +255,21 @@ class GridProblem {
   tpfem::BlockRhs loads() const {
     const int N = d_.steps;
     tpfem::BlockRhs f(N, n_dof());
-    for (int n = 0; n < N; ++n) {
-      const double t = (n + 1) * d_.period / N;
-      double* fn = f.block(n);
-      for (const tpfem::ElementData& e : op_->elements()) {
-        const double j = source_current(static_cast<int>(e.region), t);
-        if (j == 0) continue;
-        const double contrib = j * e.area / 3.0;
-        for (int k = 0; k < 3; ++k)
-          if (e.dof[k] >= 0) fn[e.dof[k]] += contrib;
-      }
-    }
+    for (int n = 0; n < N; ++n) load_slice(n, f.block(n));
     return f;
+  }
+
+  /// f^n alone (fn zero-initialised by the caller), for samples of configs
+  /// whose whole F does not fit in host memory.
+  void load_slice(int n, double* fn) const {
+    const double t = (n + 1) * d_.period / d_.steps;
+    for (const tpfem::ElementData& e : op_->elements()) {
+      const double j = source_current(static_cast<int>(e.region), t);
+      if (j == 0) continue;
+      const double contrib = j * e.area / 3.0;
+      for (int k = 0; k < 3; ++k)
+        if (e.dof[k] >= 0) fn[e.dof[k]] += contrib;
+    }
   }
 
   /// Sampled eigenvalue range of the flux-map Jacobian (materials.hpp:112-128).

@@ -30,6 +30,16 @@ def available() -> bool:
     return os.path.exists(LIB_PATH)
 
 
+def select(variant: str = "") -> None:
+    """Switch to another build of the checker: "" = libtpref.so (the
+    reference's 1e-10 SparseSolver contract), "relaxed" = libtpref_relaxed.so
+    (same build, shim throw threshold 1e-8: BASELINE grids >= 1024^2 where
+    1e-10 is below the fp64 residual floor)."""
+    global LIB_PATH, _lib
+    LIB_PATH = os.path.join(_HERE, "_ref", "libtpref_relaxed.so" if variant == "relaxed" else "libtpref.so")
+    _lib = None
+
+
 def lib():
     global _lib
     if _lib is None:
@@ -366,3 +376,100 @@ def tr_solve_m23(c: TrCfg, method: int, U0, cfg: TpSolverCfg | None = None):
                                        C.byref(it), C.byref(st), _ptr(wall)))
     k = it.value
     return U, hist[:k + 1].copy(), k, st.value, float(wall[0])
+
+
+# ---------------------------------------------------------------- large-config parity support
+def _biglib():
+    L = lib()
+    if not getattr(L, "_big_ready", False):
+        dp, ip = C.POINTER(C.c_double), C.POINTER(C.c_int32)
+        D, G = C.POINTER(TpProblemDesc), C.POINTER(TpSolverCfg)
+        L.tpref_solve_m1_digest.argtypes = [D, G, dp, C.c_double, dp, dp, dp, dp, C.c_int32, ip, ip, dp,
+                                            C.c_int64, dp, C.c_int32, dp]
+        L.tpref_static_init_slices.argtypes = [D, G, ip, C.c_int32, dp, ip]
+        L.tpref_frequency_blocks.argtypes = [D, G, dp, ip, C.c_int32, dp, dp]
+        L._big_ready = True
+    return L
+
+
+@dataclass
+class RefM1Digest:
+    U: np.ndarray
+    history: np.ndarray
+    contraction: np.ndarray
+    iterations: int
+    status: int
+    digests: np.ndarray      # (iterations+1) x 5: norm, sum, cos-weighted sum, max|.|, ||U^k - U^{k-1}||
+    samples: np.ndarray      # (iterations+1) x ceil(N n / stride): U^k[::stride]
+    wall_time: float = 0.0
+
+
+def solve_m1_digest(desc, nu_hat, q, U0, cfg: TpSolverCfg | None = None, stride=997, cache=0) -> RefM1Digest:
+    """solve_m1_fixed_point (solvers.hpp:301-369) keeping per-iterate digests
+    and strided samples instead of whole iterates."""
+    cfg = cfg or default_cfg()
+    U0 = np.ascontiguousarray(U0, dtype=np.float64)
+    cap = cfg.m1_max_outer + 1
+    hist, contr = np.zeros(cap), np.zeros(cap)
+    it, st = C.c_int32(), C.c_int32()
+    U = np.zeros_like(U0)
+    dig = np.zeros((cap, 5))
+    ns = -(-U0.size // stride)
+    smp = np.zeros((cap, ns))
+    wall = np.zeros(1)
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(_biglib().tpref_solve_m1_digest(C.byref(desc), C.byref(cfg), _ptr(nu), q, _ptr(U0), _ptr(U),
+                                           _ptr(hist), _ptr(contr), cap, C.byref(it), C.byref(st), _ptr(dig),
+                                           stride, _ptr(smp), cache, _ptr(wall)))
+    k = it.value
+    return RefM1Digest(U=U, history=hist[:k + 1].copy(), contraction=contr[:k].copy(), iterations=k,
+                       status=st.value, digests=dig[:k + 1].copy(), samples=smp[:k + 1].copy(),
+                       wall_time=float(wall[0]))
+
+
+def static_init_slices(desc, slices, cfg: TpSolverCfg | None = None):
+    """static_init's per-slice Newton (solvers.hpp:282-294) on the listed slices:
+    (U (len x n), newton counts)."""
+    cfg = cfg or default_cfg()
+    n, _, _ = sizes(desc)
+    sl = np.ascontiguousarray(slices, dtype=np.int32)
+    U = np.zeros((sl.size, n))
+    counts = np.zeros(sl.size, dtype=np.int32)
+    _check(_biglib().tpref_static_init_slices(C.byref(desc), C.byref(cfg), _ptr(sl), sl.size, _ptr(U),
+                                              _ptr(counts)))
+    return U, counts
+
+
+def frequency_blocks(desc, nu_hat, ks, B, cfg: TpSolverCfg | None = None):
+    """(lambda_k M + K_hat) x_k = b_k for the listed k (solve_frequency,
+    periodic.hpp:252-289); B: len(ks) x n complex."""
+    cfg = cfg or default_cfg()
+    ks = np.ascontiguousarray(ks, dtype=np.int32)
+    B = np.ascontiguousarray(B, dtype=np.complex128)
+    X = np.zeros_like(B)
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(_biglib().tpref_frequency_blocks(C.byref(desc), C.byref(cfg), _ptr(nu), _ptr(ks), ks.size,
+                                            B.ctypes.data_as(C.POINTER(C.c_double)),
+                                            X.ctypes.data_as(C.POINTER(C.c_double))))
+    return X
+
+
+def sweep_sample(desc, nu_hat, slices, cols, blocks=0, threads=0):
+    """Stage-by-stage timing of one reference sweep on a bounded sample
+    (tpref_sweep_sample): dict of seconds for A (RHS on `slices` slices),
+    B / D (forward / inverse transforms on `cols` columns), E (residual on
+    the slices), C (`blocks` frequency-block solves) and the setup."""
+    L = lib()
+    if not getattr(L, "_ss_ready", False):
+        dp = C.POINTER(C.c_double)
+        L.tpref_sweep_sample.argtypes = [C.POINTER(TpProblemDesc), C.POINTER(TpSolverCfg), dp, C.c_int32,
+                                         C.c_int32, C.c_int32, dp, dp]
+        L._ss_ready = True
+    cfg = default_cfg(threads=threads or hardware_threads())
+    t = np.zeros(5)
+    setup = C.c_double()
+    nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
+    _check(L.tpref_sweep_sample(C.byref(desc), C.byref(cfg), _ptr(nu), slices, cols, blocks, _ptr(t),
+                                C.byref(setup)))
+    return {"A_rhs": t[0], "B_forward_dft": t[1], "D_inverse_dft": t[2], "E_residual": t[3],
+            "C_blocks": t[4], "setup": setup.value}

@@ -506,3 +506,269 @@ extern "C" int tpref_tr_solve_m23(const tpref_mesh_cfg* c, const tp_solver_cfg* 
     if (status) *status = static_cast<int32_t>(rep.status);
   });
 }
+
+// ---------------------------------------------------------------- large-config parity support
+// Entry points for parity at BASELINE configs too large to archive whole
+// iterates of ("per-iterate ||U^k|| and ||U^k - U^{k-1}||,
+// plus full vectors at the iterates the oracle can afford").
+namespace {
+
+// Order-sensitive fingerprint of one iterate; must match
+// tests/golden/make_golden.py:checksum (norm, sum, cos-weighted sum, max |.|).
+void digest_of(const double* a, std::size_t n, double* out) {
+  long double ss = 0, s = 0, ws = 0;
+  double mx = 0;
+  for (std::size_t i = 0; i < n; ++i) {
+    const double v = a[i];
+    ss += static_cast<long double>(v) * v;
+    s += v;
+    ws += static_cast<long double>(std::cos(0.001 * static_cast<double>(i))) * v;
+    mx = std::max(mx, std::abs(v));
+  }
+  out[0] = std::sqrt(static_cast<double>(ss));
+  out[1] = static_cast<double>(s);
+  out[2] = static_cast<double>(ws);
+  out[3] = mx;
+}
+
+}  // namespace
+
+extern "C" {
+
+/// solve_m1_fixed_point (solvers.hpp:301-369) with the iterate log reduced
+/// on the fly: digests (cap x 5: checksum of U^k, then ||U^k - U^{k-1}||,
+/// 0 for k = 0), samples (cap x ceil(N n / stride): U^k[::stride]).
+int tpref_solve_m1_digest(const tp_problem_desc* d, const tp_solver_cfg* c, const double* nu_hat, double q,
+                          const double* U0, double* U_out, double* history, double* contraction, int32_t cap,
+                          int32_t* iterations, int32_t* status, double* digests, int64_t stride,
+                          double* samples, int32_t cache, double* wall) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    tpfem::SolverConfig cfg = to_ref(c);
+    cfg.cache = cache == 1 ? tpfem::CachePolicy::always
+                           : cache == 2 ? tpfem::CachePolicy::never : tpfem::CachePolicy::automatic;
+    const tpfem::BlockRhs F = p.loads();
+    const tpfem::SparseMatrix<double> K = p.stiffness_frozen(nu_array(nu_hat));
+    std::vector<tpfem::PeriodicState> log;
+    const auto t0 = std::chrono::steady_clock::now();
+    auto [U, rep] = tpfem::solve_m1_fixed_point(p, K, F, state_from(p, U0), cfg, q, &log);
+    if (wall) *wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    if (U_out) std::memcpy(U_out, U.data.data(), U.data.size() * sizeof(double));
+    for (std::size_t k = 0; k < rep.residual_history.size() && static_cast<int>(k) < cap; ++k)
+      history[k] = rep.residual_history[k];
+    if (contraction)
+      for (std::size_t k = 0; k < rep.contraction_history.size() && static_cast<int>(k) < cap; ++k)
+        contraction[k] = rep.contraction_history[k];
+    if (iterations) *iterations = rep.iterations;
+    if (status) *status = static_cast<int32_t>(rep.status);
+    const std::size_t sz = U.data.size();
+    const std::size_t ns = stride > 0 ? (sz + static_cast<std::size_t>(stride) - 1) / static_cast<std::size_t>(stride) : 0;
+    for (std::size_t k = 0; k < log.size() && static_cast<int>(k) < cap; ++k) {
+      const double* a = log[k].data.data();
+      digest_of(a, sz, digests + 5 * k);
+      long double dd = 0;
+      if (k > 0) {
+        const double* b = log[k - 1].data.data();
+        for (std::size_t i = 0; i < sz; ++i) dd += static_cast<long double>(a[i] - b[i]) * (a[i] - b[i]);
+      }
+      digests[5 * k + 4] = std::sqrt(static_cast<double>(dd));
+      if (samples)
+        for (std::size_t s = 0; s < ns; ++s) samples[k * ns + s] = a[s * static_cast<std::size_t>(stride)];
+    }
+  });
+}
+
+/// The body of static_init's slice loop (solvers.hpp:282-294) for the listed
+/// slices only: newton_elliptic(p, 0, f^i, u = 0, static_tol, static_max_newton).
+/// U_out: count x n; counts: count.
+int tpref_static_init_slices(const tp_problem_desc* d, const tp_solver_cfg* c, const int32_t* slices,
+                             int32_t count, double* U_out, int32_t* counts) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const std::size_t n = static_cast<std::size_t>(p.n_dof());
+    tpfem::parallel_for(0, count, cfg.threads, [&](int s) {
+      const int i = slices[s];
+      if (i < 0 || i >= p.steps()) throw std::invalid_argument("static_init_slices: slice out of range");
+      std::vector<double> rhs(n, 0.0);
+      p.load_slice(i, rhs.data());
+      std::vector<double> u(n, 0.0);
+      counts[s] = tpfem::detail::newton_elliptic(p, 0.0, rhs, u, cfg.static_tol, cfg.static_max_newton,
+                                                  cfg.armijo);
+      std::copy(u.begin(), u.end(), U_out + static_cast<std::size_t>(s) * n);
+    });
+  });
+}
+
+/// The frequency-block solves of PeriodicSolver::solve_frequency
+/// (periodic.hpp:252-289) for the listed frequencies, on caller right-hand
+/// sides: (lambda_k M + K_hat) x = b with lambda_k = PeriodicSolver::symbol(k)
+/// (periodic.hpp:146-152); real blocks (k = 0, N/2) as two real solves of
+/// real_block(k), complex ones through complex_block(k) = add_scaled(lambda_k,
+/// to_complex(M), 1, to_complex(K_hat)).  B, X: count x n complex (re, im
+/// interleaved).  Every solve carries the SparseSolver residual contract.
+int tpref_frequency_blocks(const tp_problem_desc* d, const tp_solver_cfg* c, const double* nu_hat,
+                           const int32_t* ks, int32_t count, const double* B, double* X) {
+  return guarded([&] {
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const tpfem::SparseMatrix<double> K = p.stiffness_frozen(nu_array(nu_hat));
+    tpfem::PeriodicSolverOptions opts = tpfem::make_periodic_options(cfg);
+    opts.cache = tpfem::CachePolicy::never;
+    const tpfem::PeriodicSolver ps(p.mass(), K, p.tau(), p.steps(), opts);
+    const std::size_t n = static_cast<std::size_t>(p.n_dof());
+    const int N = p.steps();
+    const auto Mc = tpfem::to_complex(p.mass());
+    const auto Kc = tpfem::to_complex(K);
+    tpfem::parallel_for(0, count, cfg.threads, [&](int s) {
+      const int k = ks[s];
+      if (k < 0 || 2 * k > N) throw std::invalid_argument("frequency_blocks: k outside 0..N/2");
+      const double* b = B + 2 * n * static_cast<std::size_t>(s);
+      double* x = X + 2 * n * static_cast<std::size_t>(s);
+      const std::complex<double> lam = ps.symbol(k);
+      if (k == 0 || 2 * k == N) {
+        const tpfem::SparseSolver<double> solver(tpfem::add_scaled(lam.real(), p.mass(), 1.0, K));
+        std::vector<double> bre(n), bim(n);
+        for (std::size_t j = 0; j < n; ++j) {
+          bre[j] = b[2 * j];
+          bim[j] = b[2 * j + 1];
+        }
+        const std::vector<double> xre = solver.solve(bre), xim = solver.solve(bim);
+        for (std::size_t j = 0; j < n; ++j) {
+          x[2 * j] = xre[j];
+          x[2 * j + 1] = xim[j];
+        }
+      } else {
+        const tpfem::SparseSolver<std::complex<double>> solver(
+            tpfem::add_scaled(lam, Mc, std::complex<double>{1.0, 0.0}, Kc));
+        std::vector<std::complex<double>> bc(n);
+        for (std::size_t j = 0; j < n; ++j) bc[j] = {b[2 * j], b[2 * j + 1]};
+        const std::vector<std::complex<double>> xc = solver.solve(bc);
+        for (std::size_t j = 0; j < n; ++j) {
+          x[2 * j] = xc[j].real();
+          x[2 * j + 1] = xc[j].imag();
+        }
+      }
+    });
+  });
+}
+
+}  // extern "C"
+
+extern "C" {
+
+/// Bounded sample of one reference sweep for bench.py's reference arm at
+/// sizes where a whole sweep takes hours: each stage of the sweep timed on a
+/// sample with the reference's own code, each a parallel_for over
+/// cfg.threads like the reference's:
+///   times[0] A  the RHS lambda (solvers.hpp:326-336) on `slices` slices:
+///               apply_k, K_hat.multiply, g = f + K_hat u - K(u)
+///   times[1] B  the forward transform (periodic.hpp:163-167) on `cols` dof
+///               columns: gather a column of length N, DftPlan::forward
+///   times[2] D  the inverse transform + Re / Im sums (periodic.hpp:174-185)
+///               on the same columns
+///   times[3] E  the residual lambda (periodic.hpp:43-52) on the slices:
+///               apply_k, M (u - u_prev) / tau, r = f - M du - K(u)
+///   times[4] C  `blocks` frequency-block solves (solve_frequency,
+///               periodic.hpp:252-289: assemble lambda_k M + K_hat, factorise,
+///               solve, residual contract), k = 1 .. blocks; 0 skips
+/// The state is a seeded smooth field (the stages' cost does not depend on
+/// it).  setup_s: GridProblem + K_hat construction (not part of a sweep).
+int tpref_sweep_sample(const tp_problem_desc* d, const tp_solver_cfg* c, const double* nu_hat, int32_t slices,
+                       int32_t cols, int32_t blocks, double* times, double* setup_s) {
+  return guarded([&] {
+    using clk = std::chrono::steady_clock;
+    const auto secs = [](clk::time_point a) { return std::chrono::duration<double>(clk::now() - a).count(); };
+    auto t0 = clk::now();
+    const tporacle::GridProblem p(*d);
+    const tpfem::SolverConfig cfg = to_ref(c);
+    const tpfem::SparseMatrix<double> K = p.stiffness_frozen(nu_array(nu_hat));
+    const std::size_t n = static_cast<std::size_t>(p.n_dof());
+    const int N = p.steps();
+    const double tau = p.tau();
+    const int S = std::max(1, std::min<int>(slices, N));
+    // state: S+1 consecutive slices of a smooth seeded field
+    std::vector<double> U((static_cast<std::size_t>(S) + 1) * n), F(static_cast<std::size_t>(S) * n, 0.0);
+    for (std::size_t s = 0; s <= static_cast<std::size_t>(S); ++s)
+      for (std::size_t j = 0; j < n; ++j)
+        U[s * n + j] = 1e-3 * std::sin(0.001 * static_cast<double>(j) + 0.1 * static_cast<double>(s));
+    for (int s = 0; s < S; ++s) p.load_slice(s, F.data() + static_cast<std::size_t>(s) * n);
+    if (setup_s) *setup_s = secs(t0);
+    std::vector<double> G(static_cast<std::size_t>(S) * n), R(static_cast<std::size_t>(S) * n);
+    // A: RHS
+    t0 = clk::now();
+    tpfem::parallel_for(0, S, cfg.threads, [&](int i) {
+      const double* u = U.data() + (static_cast<std::size_t>(i) + 1) * n;
+      double* g = G.data() + static_cast<std::size_t>(i) * n;
+      std::vector<double> ku(n), khu(n);
+      p.apply_k(u, ku.data());
+      K.multiply(u, khu.data());
+      const double* f = F.data() + static_cast<std::size_t>(i) * n;
+      for (std::size_t j = 0; j < n; ++j) g[j] = f[j] + khu[j] - ku[j];
+    });
+    times[0] = secs(t0);
+    // B, D: transforms over `cols` columns (gather stride n like periodic.hpp:165)
+    const tpfem::DftPlan plan(N, cfg.transform);
+    const int C = std::max(1, std::min<int>(cols, static_cast<int>(n)));
+    std::vector<std::complex<double>> work(static_cast<std::size_t>(C) * N);
+    std::vector<double> src(static_cast<std::size_t>(N) * C);
+    for (std::size_t k = 0; k < src.size(); ++k) src[k] = std::cos(0.37 * static_cast<double>(k));
+    t0 = clk::now();
+    tpfem::parallel_for(0, C, cfg.threads, [&](int j) {
+      std::complex<double>* col = work.data() + static_cast<std::size_t>(j) * N;
+      for (int i = 0; i < N; ++i) col[i] = src[static_cast<std::size_t>(i) * C + j];
+      plan.forward(col);
+    });
+    times[1] = secs(t0);
+    std::vector<double> re2(C), im2(C);
+    t0 = clk::now();
+    tpfem::parallel_for(0, C, cfg.threads, [&](int j) {
+      std::complex<double>* col = work.data() + static_cast<std::size_t>(j) * N;
+      plan.inverse(col);
+      double r = 0, m = 0;
+      for (int i = 0; i < N; ++i) {
+        src[static_cast<std::size_t>(i) * C + j] = col[i].real();
+        r += col[i].real() * col[i].real();
+        m += col[i].imag() * col[i].imag();
+      }
+      re2[j] = r;
+      im2[j] = m;
+    });
+    times[2] = secs(t0);
+    // E: residual
+    const tpfem::SparseMatrix<double>& M = p.mass();
+    t0 = clk::now();
+    tpfem::parallel_for(0, S, cfg.threads, [&](int i) {
+      const double* u = U.data() + (static_cast<std::size_t>(i) + 1) * n;
+      const double* uprev = U.data() + static_cast<std::size_t>(i) * n;
+      double* r = R.data() + static_cast<std::size_t>(i) * n;
+      std::vector<double> ku(n), du(n), mdu(n);
+      p.apply_k(u, ku.data());
+      for (std::size_t j = 0; j < n; ++j) du[j] = (u[j] - uprev[j]) / tau;
+      M.multiply(du.data(), mdu.data());
+      const double* f = F.data() + static_cast<std::size_t>(i) * n;
+      for (std::size_t j = 0; j < n; ++j) r[j] = f[j] - mdu[j] - ku[j];
+    });
+    times[3] = secs(t0);
+    // C: frequency blocks k = 1..blocks
+    times[4] = 0;
+    if (blocks > 0) {
+      tpfem::PeriodicSolverOptions opts = tpfem::make_periodic_options(cfg);
+      opts.cache = tpfem::CachePolicy::never;
+      const tpfem::PeriodicSolver ps(M, K, tau, N, opts);
+      const auto Mc = tpfem::to_complex(M);
+      const auto Kc = tpfem::to_complex(K);
+      t0 = clk::now();
+      tpfem::parallel_for(1, blocks + 1, cfg.threads, [&](int k) {
+        const tpfem::SparseSolver<std::complex<double>> solver(
+            tpfem::add_scaled(ps.symbol(k), Mc, std::complex<double>{1.0, 0.0}, Kc));
+        std::vector<std::complex<double>> b(n);
+        for (std::size_t j = 0; j < n; ++j) b[j] = {G[j], 0.5 * G[j]};
+        (void)solver.solve(b);
+      });
+      times[4] = secs(t0);
+    }
+  });
+}
+
+}  // extern "C"

@@ -368,10 +368,20 @@ class DenseLu {
 /// Direct factorization of a square sparse matrix with the reference's
 /// contract (solve.hpp:47-126): every solve checks the relative residual
 /// against kResidualTol and throws SolveError on failure.
+// TPREF_THROW_TOL: the threshold at which solve() throws.  It is the
+// reference's kResidualTol unless oracle/Makefile builds the "relaxed"
+// checker (libtpref_relaxed.so, -DTPREF_THROW_TOL=1e-8) for the BASELINE
+// grids >= 1024^2, where 1e-10 is below the fp64 floor of the evaluated
+// ||b - A x||.
+#ifndef TPREF_THROW_TOL
+#define TPREF_THROW_TOL 1e-10
+#endif
+
 template <class Scalar>
 class SparseSolver {
  public:
   static constexpr double kResidualTol = 1e-10;
+  static constexpr double kThrowTol = TPREF_THROW_TOL;
   static constexpr Index kDenseLimit = 6000;
 
   explicit SparseSolver(const SparseMatrix<Scalar>& A) : A_(A) {
@@ -405,7 +415,7 @@ class SparseSolver {
       rnorm = rn2;
     }
     const double rel = rnorm / bnorm;
-    if (!(rel <= kResidualTol))
+    if (!(rel <= kThrowTol))
       throw SolveError("sparse solve: relative residual " + std::to_string(rel) +
                            " exceeds tolerance",
                        rel);

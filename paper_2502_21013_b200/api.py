@@ -37,8 +37,13 @@ EXPORTS = [
     "tp_m1_begin", "tp_m1_sweep", "tp_sweep_stats", "tp_problem_stream", "tp_problem_launches",
     "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
     "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
-    "tp_kernel_timer",
+    "tp_kernel_timer", "tp_comm_create_host",
 ]
+
+# tp_host_exchange_fn (tpgpu.h)
+HOST_EXCHANGE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                               C.POINTER(C.c_size_t), C.c_int32, C.POINTER(C.c_int32), C.POINTER(C.c_void_p),
+                               C.POINTER(C.c_size_t))
 
 
 class SolveError(RuntimeError):
@@ -95,6 +100,7 @@ def lib():
         L.tp_shard_plan_make.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, SP]
         L.tp_nccl_unique_id.argtypes = [C.c_char_p]
         L.tp_comm_create.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
+        L.tp_comm_create_host.argtypes = [C.c_int32, C.c_int32, C.c_int32, HOST_EXCHANGE_FN, vp, C.POINTER(vp)]
         L.tp_comm_destroy.argtypes = [vp]
         L.tp_comm_destroy.restype = None
         L.tp_comm_nccl.argtypes = [vp]
@@ -195,6 +201,40 @@ class Comm:
         t = torch.tensor(list(uid), dtype=torch.uint8)
         dist.broadcast(t, src=0, group=group)
         return cls(bytes(t.tolist()), world, rank, device)
+
+    @classmethod
+    def host_staged(cls, device: int, group=None) -> "Comm":
+        """Host-staged transport over an initialised torch.distributed
+        process group (gloo): every exchange of the sharded sweep goes
+        through pinned host memory and point-to-point gloo messages
+        (tp_comm_create_host).  For several ranks sharing one GPU (tests)."""
+        import torch
+        import torch.distributed as dist
+        rank, world = dist.get_rank(group), dist.get_world_size(group)
+
+        def exchange(_user, ns, sp, sb, sz, nr, rp, rb, rz):
+            try:
+                reqs = []
+                for i in range(ns):
+                    a = np.ctypeslib.as_array(C.cast(sb[i], C.POINTER(C.c_uint8)), shape=(sz[i],))
+                    reqs.append(dist.isend(torch.from_numpy(a.copy()), int(sp[i]), group=group))
+                for i in range(nr):
+                    a = np.ctypeslib.as_array(C.cast(rb[i], C.POINTER(C.c_uint8)), shape=(rz[i],))
+                    reqs.append(dist.irecv(torch.from_numpy(a), int(rp[i]), group=group))
+                for q in reqs:
+                    q.wait()
+                return 0
+            except Exception:  # surfaces as TP_ECUDA "host transport callback failed"
+                import traceback
+                traceback.print_exc()
+                return 1
+
+        self = cls.__new__(cls)
+        self._fn = HOST_EXCHANGE_FN(exchange)  # keep alive with the communicator
+        self._h = C.c_void_p()
+        _check(lib().tp_comm_create_host(world, rank, device, self._fn, None, C.byref(self._h)))
+        self.nranks, self.rank, self.device = world, rank, device
+        return self
 
     def close(self):
         if self._h:

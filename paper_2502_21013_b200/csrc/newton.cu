@@ -261,7 +261,10 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
       if (e) std::rethrow_exception(e);
   }
   TP_CUDA(cudaStreamSynchronize(stream));
-  if (sharded()) slices_to_strips(Us.get());
+  if (sharded()) {
+    slices_to_strips(Us.get());
+    global_sum_ints(counts);  // every rank reports all N counts
+  }
   if (newton_counts)
     for (int s = 0; s < N; ++s) newton_counts[s] = counts[s];
 }

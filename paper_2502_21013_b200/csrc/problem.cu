@@ -829,15 +829,19 @@ int tp_problem_sizes(const tp_problem* p, int32_t* n_dof, int32_t* steps, double
   });
 }
 
+// Host arrays of a sharded rank are its strip (N x n_local, tpgpu.h): loads
+// and mass are written for the strip's dofs [y0*m, y1*m).
 int tp_problem_loads(tp_problem* h, double* F) {
   return guarded([&] {
     Problem& p = P(h);
     const int nsrc = (int)p.src_mats.size();
+    const int i0 = p.sh.y0 * p.m, nl = p.sh.nr;
     for (int s = 0; s < p.N; ++s)
-      for (int i = 0; i < p.n; ++i) {
+      for (int i = 0; i < nl; ++i) {
         double f = 0;
-        for (int r = 0; r < nsrc; ++r) f += p.src_time[(size_t)s * nsrc + r] * p.src_prof[(size_t)r * p.n + i];
-        F[(size_t)s * p.n + i] = f;
+        for (int r = 0; r < nsrc; ++r)
+          f += p.src_time[(size_t)s * nsrc + r] * p.src_prof[(size_t)r * p.n + i0 + i];
+        F[(size_t)s * nl + i] = f;
       }
   });
 }
@@ -845,13 +849,14 @@ int tp_problem_loads(tp_problem* h, double* F) {
 int tp_problem_mass(tp_problem* h, double* m) {
   return guarded([&] {
     Problem& p = P(h);
-    std::memcpy(m, p.mass.data(), p.n * sizeof(double));
+    std::memcpy(m, p.mass.data() + (size_t)p.sh.y0 * p.m, (size_t)p.sh.nr * sizeof(double));
   });
 }
 
 int tp_apply_k(tp_problem* h, const double* U, double* KU, int32_t count) {
   return guarded([&] {
     Problem& p = P(h);
+    tpgpu::require(!p.sharded(), "apply_k of host slices: single-rank problems only");
     tpgpu::require(count >= 1, "apply_k: count must be positive");
     tpgpu::DevBuf<double> du((size_t)count * p.n), dk((size_t)count * p.n);
     TP_CUDA(cudaMemcpyAsync(du.get(), U, du.bytes(), cudaMemcpyHostToDevice, p.stream));
@@ -864,6 +869,7 @@ int tp_apply_k(tp_problem* h, const double* U, double* KU, int32_t count) {
 int tp_residual(tp_problem* h, const double* U, double* R, double* norm) {
   return guarded([&] {
     Problem& p = P(h);
+    tpgpu::require(!p.sharded(), "residual of a host state: single-rank problems only");
     const size_t sz = (size_t)p.N * p.n;
     tpgpu::DevBuf<double> du(sz), dr(sz);
     TP_CUDA(cudaMemcpyAsync(du.get(), U, sz * sizeof(double), cudaMemcpyHostToDevice, p.stream));
@@ -1082,7 +1088,7 @@ int tp_problem_create_sharded(const tp_problem_desc* desc, tp_comm* comm, tp_pro
     const int P = tp_comm_size(comm), r = tp_comm_rank(comm), dev = tp_comm_device(comm);
     tpgpu::ShardInfo sh;
     tpgpu::make_partition(desc->cells - 1, desc->steps / 2 + 1, desc->steps, P, r, sh);
-    sh.comm = tp_comm_nccl(comm);
+    sh.comm = comm;
     auto h = std::make_unique<tp_problem>();
     h->impl = std::make_unique<Problem>(*desc, dev, &sh);
     *out = h.release();

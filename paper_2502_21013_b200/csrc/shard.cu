@@ -82,6 +82,105 @@ static NcclApi& nccl() {
                                 __FILE__ + ":" + std::to_string(__LINE__) + ": " #x);           \
   } while (0)
 
+// ---------------------------------------------------------------- transport
+// Every exchange of the sharded sweep is one of two patterns: a grouped set
+// of point-to-point transfers (halo rows, the three all-to-alls) or an
+// all-gather of a few doubles (rank-ordered norms, min/max).  tp_comm carries
+// the backend: NCCL over NVLink (production, one process per GPU), or a
+// host-staged exchange through a caller callback (tp_comm_create_host: device
+// buffers are staged through pinned host memory, the callback moves bytes
+// between processes, e.g. over gloo).  The host backend lets several ranks
+// share one GPU without any kernel waiting on another process's kernel: the
+// stream is drained before the callback and refilled after it.
+struct P2P {
+  int peer;
+  void* buf;  // device
+  size_t bytes;
+};
+
+static void host_stage_grow(tp_comm* c, size_t bytes) {
+  if (bytes <= c->host_cap) return;
+  if (c->host_buf) cudaFreeHost(c->host_buf);
+  c->host_buf = nullptr;
+  c->host_cap = 0;
+  TP_CUDA(cudaMallocHost(&c->host_buf, bytes));
+  c->host_cap = bytes;
+}
+
+// Grouped point-to-point exchange: sends[i] to sends[i].peer, recvs[i] from
+// recvs[i].peer.  Transfers to self pair up in order.
+static void comm_exchange(tp_comm* c, const std::vector<P2P>& sends, const std::vector<P2P>& recvs,
+                          cudaStream_t stream) {
+  if (c->kind == tp_comm::Kind::Nccl) {
+    ncclComm_t nc = static_cast<ncclComm_t>(c->comm);
+    TP_NCCL(ncclGroupStart());
+    for (size_t i = 0; i < std::max(sends.size(), recvs.size()); ++i) {
+      if (i < sends.size() && sends[i].bytes)
+        TP_NCCL(ncclSend(sends[i].buf, sends[i].bytes, ncclChar, sends[i].peer, nc, stream));
+      if (i < recvs.size() && recvs[i].bytes)
+        TP_NCCL(ncclRecv(recvs[i].buf, recvs[i].bytes, ncclChar, recvs[i].peer, nc, stream));
+    }
+    TP_NCCL(ncclGroupEnd());
+    return;
+  }
+  // host-staged: self transfers stay on the device; remote ones go through
+  // one pinned staging area (sends first, then receives)
+  std::vector<const P2P*> self_s, self_r, rs, rr;
+  for (const P2P& t : sends) (t.peer == c->rank ? self_s : rs).push_back(&t);
+  for (const P2P& t : recvs) (t.peer == c->rank ? self_r : rr).push_back(&t);
+  require(self_s.size() == self_r.size(), "comm: unmatched self transfer");
+  for (size_t i = 0; i < self_s.size(); ++i) {
+    require(self_s[i]->bytes == self_r[i]->bytes, "comm: self transfer size mismatch");
+    if (self_s[i]->bytes)
+      TP_CUDA(cudaMemcpyAsync(self_r[i]->buf, self_s[i]->buf, self_s[i]->bytes, cudaMemcpyDeviceToDevice, stream));
+  }
+  size_t tot = 0;
+  for (auto* t : rs) tot += t->bytes;
+  for (auto* t : rr) tot += t->bytes;
+  host_stage_grow(c, tot);
+  char* h = static_cast<char*>(c->host_buf);
+  std::vector<int32_t> sp, rp;
+  std::vector<const void*> sb;
+  std::vector<void*> rb;
+  std::vector<size_t> sz, rz;
+  size_t off = 0;
+  for (auto* t : rs) {
+    if (t->bytes) TP_CUDA(cudaMemcpyAsync(h + off, t->buf, t->bytes, cudaMemcpyDeviceToHost, stream));
+    sp.push_back(t->peer);
+    sb.push_back(h + off);
+    sz.push_back(t->bytes);
+    off += t->bytes;
+  }
+  for (auto* t : rr) {
+    rp.push_back(t->peer);
+    rb.push_back(h + off);
+    rz.push_back(t->bytes);
+    off += t->bytes;
+  }
+  TP_CUDA(cudaStreamSynchronize(stream));
+  const int rc = c->host_fn(c->host_user, (int32_t)sp.size(), sp.data(), sb.data(), sz.data(), (int32_t)rp.size(),
+                            rp.data(), rb.data(), rz.data());
+  if (rc != 0) throw Error(TP_ECUDA, "host transport callback failed (" + std::to_string(rc) + ")");
+  for (size_t i = 0; i < rr.size(); ++i)
+    if (rr[i]->bytes) TP_CUDA(cudaMemcpyAsync(rr[i]->buf, rb[i], rr[i]->bytes, cudaMemcpyHostToDevice, stream));
+  // the staging area is reused by the next exchange: drain the uploads
+  TP_CUDA(cudaStreamSynchronize(stream));
+}
+
+// dst[q*bytes .. ] = rank q's src (bytes each), all device buffers
+static void comm_allgather(tp_comm* c, const void* src, void* dst, size_t bytes, cudaStream_t stream) {
+  if (c->kind == tp_comm::Kind::Nccl) {
+    TP_NCCL(ncclAllGather(src, dst, bytes, ncclChar, static_cast<ncclComm_t>(c->comm), stream));
+    return;
+  }
+  std::vector<P2P> s, r;
+  for (int q = 0; q < c->nranks; ++q) {
+    s.push_back({q, const_cast<void*>(src), bytes});
+    r.push_back({q, static_cast<char*>(dst) + (size_t)q * bytes, bytes});
+  }
+  comm_exchange(c, s, r, stream);
+}
+
 void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh) {
   require(P >= 1 && r >= 0 && r < P, "shard: rank out of range");
   require(m >= P, "shard: more ranks than grid rows");
@@ -106,7 +205,6 @@ void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh) {
   sh.nr = (sh.y1 - sh.y0) * m;
 }
 
-static ncclComm_t comm_of(const Problem& p) { return static_cast<ncclComm_t>(p.sh.comm); }
 
 // Halo rows of all N slices: my first owned row goes to rank r-1 (its hi),
 // my last to rank r+1 (its lo).
@@ -123,17 +221,16 @@ void Problem::exchange_halo() {
   TP_CUDA(cudaMemcpy2DAsync(halo_send.get() + nm, m * sizeof(double), U.get() + (size_t)(rows - 1) * m,
                             (size_t)sh.nr * sizeof(double), m * sizeof(double), N, cudaMemcpyDeviceToDevice,
                             stream));
-  ncclComm_t c = comm_of(*this);
-  TP_NCCL(ncclGroupStart());
+  std::vector<P2P> sends, recvs;
   if (sh.r > 0) {
-    TP_NCCL(ncclSend(halo_send.get(), nm, ncclDouble, sh.r - 1, c, stream));
-    TP_NCCL(ncclRecv(halo_lo.get(), nm, ncclDouble, sh.r - 1, c, stream));
+    sends.push_back({sh.r - 1, halo_send.get(), nm * sizeof(double)});
+    recvs.push_back({sh.r - 1, halo_lo.get(), nm * sizeof(double)});
   }
   if (sh.r < sh.P - 1) {
-    TP_NCCL(ncclSend(halo_send.get() + nm, nm, ncclDouble, sh.r + 1, c, stream));
-    TP_NCCL(ncclRecv(halo_hi.get(), nm, ncclDouble, sh.r + 1, c, stream));
+    sends.push_back({sh.r + 1, halo_send.get() + nm, nm * sizeof(double)});
+    recvs.push_back({sh.r + 1, halo_hi.get(), nm * sizeof(double)});
   }
-  TP_NCCL(ncclGroupEnd());
+  comm_exchange(sh.comm, sends, recvs, stream);
   // outer boundary ranks: no neighbour -> zero halo (Dirichlet)
   if (sh.r == 0) TP_CUDA(cudaMemsetAsync(halo_lo.get(), 0, nm * sizeof(double), stream));
   if (sh.r == sh.P - 1) TP_CUDA(cudaMemsetAsync(halo_hi.get(), 0, nm * sizeof(double), stream));
@@ -144,13 +241,33 @@ double Problem::global_sum(double local) {
   red_all.ensure(sh.P + 1);
   double* d = red_all.get();
   TP_CUDA(cudaMemcpyAsync(d + sh.P, &local, sizeof(double), cudaMemcpyHostToDevice, stream));
-  TP_NCCL(ncclAllGather(d + sh.P, d, 1, ncclDouble, comm_of(*this), stream));
+  comm_allgather(sh.comm, d + sh.P, d, sizeof(double), stream);
   std::vector<double> h(sh.P);
   TP_CUDA(cudaMemcpyAsync(h.data(), d, sh.P * sizeof(double), cudaMemcpyDeviceToHost, stream));
   TP_CUDA(cudaStreamSynchronize(stream));
   double s = 0;
   for (int q = 0; q < sh.P; ++q) s += h[q];  // rank order: deterministic
   return s;
+}
+
+// Element-wise sum over ranks of an integer vector (each rank fills its own
+// entries, zeros elsewhere): the per-slice Newton counts of the sharded
+// static initialisation.
+void Problem::global_sum_ints(std::vector<int>& v) {
+  if (!sharded() || v.empty()) return;
+  const size_t cnt = v.size();
+  DevBuf<int> d((size_t)(sh.P + 1) * cnt);
+  int* src = d.get() + (size_t)sh.P * cnt;
+  TP_CUDA(cudaMemcpyAsync(src, v.data(), cnt * sizeof(int), cudaMemcpyHostToDevice, stream));
+  comm_allgather(sh.comm, src, d.get(), cnt * sizeof(int), stream);
+  std::vector<int> h((size_t)sh.P * cnt);
+  TP_CUDA(cudaMemcpyAsync(h.data(), d.get(), h.size() * sizeof(int), cudaMemcpyDeviceToHost, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  for (size_t i = 0; i < cnt; ++i) {
+    int acc = 0;
+    for (int q = 0; q < sh.P; ++q) acc += h[(size_t)q * cnt + i];
+    v[i] = acc;
+  }
 }
 
 void Problem::global_minmax(double* lo, double* hi, int count) {
@@ -164,7 +281,7 @@ void Problem::global_minmax(double* lo, double* hi, int count) {
   }
   double* src = d + (size_t)2 * count * sh.P;
   TP_CUDA(cudaMemcpyAsync(src, mine.data(), 2 * count * sizeof(double), cudaMemcpyHostToDevice, stream));
-  TP_NCCL(ncclAllGather(src, d, 2 * count, ncclDouble, comm_of(*this), stream));
+  comm_allgather(sh.comm, src, d, 2 * count * sizeof(double), stream);
   std::vector<double> h((size_t)2 * count * sh.P);
   TP_CUDA(cudaMemcpyAsync(h.data(), d, h.size() * sizeof(double), cudaMemcpyDeviceToHost, stream));
   TP_CUDA(cudaStreamSynchronize(stream));
@@ -183,7 +300,6 @@ void Problem::alltoall_to_freq(const cplx* src, cplx* dst) {
   if (!src) src = Ghat.get();
   if (!dst) dst = Ghat_f.get();
   const int Kr = sh.k1 - sh.k0;
-  ncclComm_t c = comm_of(*this);
   size_t off = 0;
   std::vector<size_t> soff(sh.P);
   for (int q = 0; q < sh.P; ++q) {
@@ -191,14 +307,14 @@ void Problem::alltoall_to_freq(const cplx* src, cplx* dst) {
     off += (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m;
   }
   xstage.ensure(off);
-  TP_NCCL(ncclGroupStart());
+  std::vector<P2P> sends, recvs;
   for (int q = 0; q < sh.P; ++q) {
-    const size_t cnt_send = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * 2;  // doubles
-    const size_t cnt_recv = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * 2;
-    TP_NCCL(ncclSend(src + (size_t)sh.ks[q] * sh.nr, cnt_send, ncclDouble, q, c, stream));
-    TP_NCCL(ncclRecv(xstage.get() + soff[q], cnt_recv, ncclDouble, q, c, stream));
+    const size_t cnt_send = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * sizeof(cplx);
+    const size_t cnt_recv = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * sizeof(cplx);
+    sends.push_back({q, const_cast<cplx*>(src) + (size_t)sh.ks[q] * sh.nr, cnt_send});
+    recvs.push_back({q, xstage.get() + soff[q], cnt_recv});
   }
-  TP_NCCL(ncclGroupEnd());
+  comm_exchange(sh.comm, sends, recvs, stream);
   for (int q = 0; q < sh.P; ++q) {
     const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
     TP_CUDA(cudaMemcpy2DAsync(dst + (size_t)sh.ys[q] * m, (size_t)n * sizeof(cplx), xstage.get() + soff[q],
@@ -209,7 +325,6 @@ void Problem::alltoall_to_freq(const cplx* src, cplx* dst) {
 // Uhat_f ((k1-k0) x n) -> Uhat (K x nr): the reverse of alltoall_to_freq.
 void Problem::alltoall_from_freq() {
   const int Kr = sh.k1 - sh.k0;
-  ncclComm_t c = comm_of(*this);
   size_t off = 0;
   std::vector<size_t> soff(sh.P);
   for (int q = 0; q < sh.P; ++q) {
@@ -222,14 +337,14 @@ void Problem::alltoall_from_freq() {
     TP_CUDA(cudaMemcpy2DAsync(xstage.get() + soff[q], nq * sizeof(cplx), Uhat_f.get() + (size_t)sh.ys[q] * m,
                               (size_t)n * sizeof(cplx), nq * sizeof(cplx), Kr, cudaMemcpyDeviceToDevice, stream));
   }
-  TP_NCCL(ncclGroupStart());
+  std::vector<P2P> sends, recvs;
   for (int q = 0; q < sh.P; ++q) {
-    const size_t cnt_send = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * 2;
-    const size_t cnt_recv = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * 2;
-    TP_NCCL(ncclSend(xstage.get() + soff[q], cnt_send, ncclDouble, q, c, stream));
-    TP_NCCL(ncclRecv(Uhat.get() + (size_t)sh.ks[q] * sh.nr, cnt_recv, ncclDouble, q, c, stream));
+    const size_t cnt_send = (size_t)Kr * (sh.ys[q + 1] - sh.ys[q]) * m * sizeof(cplx);
+    const size_t cnt_recv = (size_t)(sh.ks[q + 1] - sh.ks[q]) * sh.nr * sizeof(cplx);
+    sends.push_back({q, xstage.get() + soff[q], cnt_send});
+    recvs.push_back({q, Uhat.get() + (size_t)sh.ks[q] * sh.nr, cnt_recv});
   }
-  TP_NCCL(ncclGroupEnd());
+  comm_exchange(sh.comm, sends, recvs, stream);
 }
 
 // Us: my static-init slices [s0, s1) on the full grid ((s1-s0) x n).  To
@@ -237,7 +352,6 @@ void Problem::alltoall_from_freq() {
 // its slices of my strip, contiguous at U + ss[q]*nr.
 void Problem::slices_to_strips(const double* Us) {
   const int Ns = sh.s1 - sh.s0;
-  ncclComm_t c = comm_of(*this);
   DevBuf<double> pack((size_t)Ns * n);
   size_t off = 0;
   std::vector<size_t> soff(sh.P);
@@ -248,24 +362,19 @@ void Problem::slices_to_strips(const double* Us) {
                               nq * sizeof(double), Ns, cudaMemcpyDeviceToDevice, stream));
     off += (size_t)Ns * nq;
   }
-  TP_NCCL(ncclGroupStart());
+  std::vector<P2P> sends, recvs;
   for (int q = 0; q < sh.P; ++q) {
     const size_t nq = (size_t)(sh.ys[q + 1] - sh.ys[q]) * m;
-    TP_NCCL(ncclSend(pack.get() + soff[q], (size_t)Ns * nq, ncclDouble, q, c, stream));
-    TP_NCCL(ncclRecv(U.get() + (size_t)sh.ss[q] * sh.nr, (size_t)(sh.ss[q + 1] - sh.ss[q]) * sh.nr, ncclDouble,
-                     q, c, stream));
+    sends.push_back({q, pack.get() + soff[q], (size_t)Ns * nq * sizeof(double)});
+    recvs.push_back({q, U.get() + (size_t)sh.ss[q] * sh.nr, (size_t)(sh.ss[q + 1] - sh.ss[q]) * sh.nr * sizeof(double)});
   }
-  TP_NCCL(ncclGroupEnd());
+  comm_exchange(sh.comm, sends, recvs, stream);
   TP_CUDA(cudaStreamSynchronize(stream));
 }
 
 }  // namespace tpgpu
 
 // =================================================================== C ABI
-struct tp_comm {
-  ncclComm_t comm = nullptr;
-  int nranks = 1, rank = 0, device = 0;
-};
 
 extern "C" {
 
@@ -315,11 +424,14 @@ int tp_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, in
     c->nranks = nranks;
     c->rank = rank;
     c->device = device;
-    if (ncclCommInitRank(&c->comm, nranks, u, rank) != ncclSuccess) {
+    ncclComm_t nc = nullptr;
+    if (ncclCommInitRank(&nc, nranks, u, rank) != ncclSuccess) {
       delete c;
       tpgpu::set_last_error("ncclCommInitRank failed", -1.0);
       return TP_ECUDA;
     }
+    c->comm = nc;
+    c->kind = tp_comm::Kind::Nccl;
     *out = c;
     return TP_OK;
   } catch (const std::exception& e) {
@@ -328,16 +440,32 @@ int tp_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, in
   }
 }
 
+int tp_comm_create_host(int32_t nranks, int32_t rank, int32_t device, tp_host_exchange_fn fn, void* user,
+                        tp_comm** out) {
+  if (!out || !fn || nranks < 1 || rank < 0 || rank >= nranks) return TP_EINVAL;
+  if (cudaSetDevice(device) != cudaSuccess) return TP_ECUDA;
+  auto* c = new tp_comm;
+  c->kind = tp_comm::Kind::Host;
+  c->nranks = nranks;
+  c->rank = rank;
+  c->device = device;
+  c->host_fn = fn;
+  c->host_user = user;
+  *out = c;
+  return TP_OK;
+}
+
 void tp_comm_destroy(tp_comm* c) {
   if (!c) return;
   try {
-    if (c->comm) ncclCommDestroy(c->comm);
+    if (c->kind == tp_comm::Kind::Nccl && c->comm) ncclCommDestroy(static_cast<ncclComm_t>(c->comm));
   } catch (...) {
   }
+  if (c->host_buf) cudaFreeHost(c->host_buf);
   delete c;
 }
 
-void* tp_comm_nccl(tp_comm* c) { return c ? (void*)c->comm : nullptr; }
+void* tp_comm_nccl(tp_comm* c) { return c && c->kind == tp_comm::Kind::Nccl ? c->comm : nullptr; }
 int32_t tp_comm_rank(const tp_comm* c) { return c ? c->rank : -1; }
 int32_t tp_comm_size(const tp_comm* c) { return c ? c->nranks : 0; }
 int32_t tp_comm_device(const tp_comm* c) { return c ? c->device : -1; }

@@ -14,6 +14,18 @@
 
 #include "../../include/tpgpu.h"
 
+// One rank's transport for the sharded sweep (shard.cu): an NCCL
+// communicator, or the host-staged exchange of tp_comm_create_host.
+struct tp_comm {
+  enum class Kind { Nccl, Host } kind = Kind::Nccl;
+  void* comm = nullptr;  // ncclComm_t
+  int nranks = 1, rank = 0, device = 0;
+  tp_host_exchange_fn host_fn = nullptr;
+  void* host_user = nullptr;
+  void* host_buf = nullptr;  // pinned staging
+  size_t host_cap = 0;
+};
+
 namespace tpgpu {
 
 // ---------------------------------------------------------------- errors
@@ -190,7 +202,7 @@ struct ShardInfo {
   int s0 = 0, s1 = 0;
   int nr = 0;  // local dofs (y1-y0)*m
   std::vector<int> ys, ks, ss;  // partition points, P+1 each
-  void* comm = nullptr;         // ncclComm_t
+  tp_comm* comm = nullptr;      // NCCL or host-staged transport (shard.cu)
 };
 void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh);
 
@@ -264,6 +276,7 @@ class Problem {
   void exchange_halo();
   double global_sum(double local);
   void global_minmax(double* lo, double* hi, int count);
+  void global_sum_ints(std::vector<int>& v);
   void alltoall_to_freq(const cplx* src = nullptr, cplx* dst = nullptr);  // Ghat (K x nr) -> Ghat_f ((k1-k0) x n)
   // warm start of the first sweep's frequency solves: the spectrum of the
   // current state U (its frequency blocks) as the initial guess
