@@ -2,18 +2,26 @@
 """Benchmark: space-time DoF/s per fixed-point sweep (BASELINE.json metric).
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl b200|reference]
-                    [--config 1] [--no-cpu-baseline]
+                    [--config 3] [--no-cpu-baseline] [--no-cfg1-leg] [--no-mesh]
 
 One step = one fixed-point sweep over all N time slices of the workload
 (solvers.hpp:326-342: RHS f + K_hat u - K(u), DFT along time, the N/2+1
 frequency-block solves, inverse DFT, residual + norm).  Default workload:
-BASELINE.json configs[1] (256x256 cells, 65,025 dofs, N = 256, fp64).
+BASELINE.json configs[3], the largest configuration that fits one GPU
+(2048x2048 cells, 4,190,209 dofs, N = 1024: 4.29e9 space-time DoF, fp64,
+~169 GB of HBM in use).
 
 Timing: W untimed warm-up sweeps, then exactly K sweeps bracketed by a
 barrier + cudaDeviceSynchronize and CUDA events on the library's stream,
-max over ranks.  Every sweep streams U, G, Ghat, Uhat (133 MB each, > L2).
+max over ranks.  Every sweep streams U, G, Ghat, Uhat (34 GB each, >> L2).
 `e2e` goes through the C ABI with pinned HOST buffers: each step uploads U,
 runs one sweep (tp_solve_m1 with m1_max_outer = 1) and downloads U.
+`full_solve` is the time-to-residual leg: static_init + nu_hat + solver
+setup + sweeps until the residual reaches 1e-8 of the first, or stops
+improving (the fp64 floor of the fixed point on configs 2 / 3),
+with the time to every decade reached.  `cfg1_leg` repeats the sweep and
+the full solve on configs[1] (the configuration the CPU reference can solve
+to 1e-8), beside one reference sweep on the host.
 
 Multi-GPU (torchrun, one process per GPU): the workload is SHARDED across
 the ranks (strong scaling): node-row strips for K(u) /
@@ -130,18 +138,94 @@ def cudart():
     return torch
 
 
-def workload_config(desc, world, replicas=False):
+WORKLOAD_NAMES = {
+    0: "BASELINE configs[0]: small 2D model problem",
+    1: "BASELINE configs[1]: unit square, seeded sigma noise",
+    2: "BASELINE configs[2]: transformer-like cross-section",
+    3: "BASELINE configs[3]: scaling config (configs[2] geometry)",
+    4: "BASELINE configs[4]: harmonic-rich strongly saturating",
+    5: "BASELINE configs[4] linear control (nu == nu0)",
+}
+
+
+def workload_config(desc, config, world, replicas=False):
     n = (desc.cells - 1) ** 2
     D = n * desc.steps
     par = "single GPU" if world == 1 else (f"replicas x{world}" if replicas else
                                            f"sharded x{world}: row strips + frequency blocks, NCCL all-to-all")
+    vec = 8.0 * D
     return D, {
-        "workload": f"BASELINE configs[1]: {desc.cells}x{desc.cells} cells ({n} dofs) x N={desc.steps} "
-                    "slices, fp64, U0 = static_init, frozen-field nu_hat",
-        "cells": desc.cells, "steps": desc.steps, "space_time_dof": D,
-        "l2": "inputs larger than L2 (U, G, Ghat, Uhat 133 MB each, streamed every sweep)",
+        "workload": f"{WORKLOAD_NAMES.get(config, f'config {config}')}: {desc.cells}x{desc.cells} cells "
+                    f"({n} dofs) x N={desc.steps} slices, fp64, U0 = static_init, frozen-field nu_hat",
+        "baseline_config": config, "cells": desc.cells, "steps": desc.steps, "space_time_dof": D,
+        "l2": f"inputs larger than L2 (U, G, Ghat, Uhat {vec / 1e9:.3g} GB each, streamed every sweep)",
         "parallelism": par,
     }
+
+
+def warm_modules(device):
+    """Pay CUDA module loading / first-launch costs on a tiny problem so the
+    init timing of the workload is a warm process's (one untimed call)."""
+    from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg
+    cfg = default_cfg(tol=1e-8, m1_max_outer=2)
+    with Problem(baseline_desc(0), device=device) as w:
+        w.static_init(cfg, want_state=False)
+        w.choose_nu_hat(cfg)
+        w.m1_begin(cfg)
+        w.m1_sweep()
+
+
+def pinned(shape, torch):
+    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+
+
+def full_solve_leg(p, U0, cfg, init_s, D, jobs, pg, torch, stream, stall_window=20):
+    """Time to residual: sweeps from U0 until history[-1] <= tol * history[0]
+    (stopping_check, solvers.hpp:100-103), m1_max_outer, or no 5 % gain on
+    the best residual for `stall_window` sweeps (the fp64 floor of the fixed
+    point on configs 2 / 3: rounding of G = f + K_hat u - K(u) amplified by
+    1 / (1 - q), q ~ 0.97 -- DESIGN.md §8).  Reports the time to every decade."""
+    p.set_state(U0)
+    t0 = time.perf_counter()
+    r0 = p.m1_begin(cfg)
+    t_setup = time.perf_counter() - t0
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(cfg.m1_max_outer + 1)]
+    ev[0].record(stream)
+    hist, its, fits = [r0], [], []
+    best, since = r0, 0
+    while len(its) < cfg.m1_max_outer and not hist[-1] <= cfg.tol * hist[0]:
+        r, it = p.m1_sweep()
+        hist.append(r)
+        its.append(it)
+        fits.append(p.sweep_stats()[1])
+        ev[len(its)].record(stream)
+        if r < 0.95 * best:
+            best, since = r, 0
+        else:
+            since += 1
+            if since >= stall_window:
+                break
+    torch.cuda.synchronize()
+    sw = [ev[k].elapsed_time(ev[k + 1]) for k in range(len(its))]
+    cum = np.cumsum(sw) / 1e3
+    conv = bool(hist[-1] <= cfg.tol * hist[0])
+    decades = {}
+    for e in range(1, 9):
+        k = next((i for i, x in enumerate(hist) if x <= 10.0 ** -e * hist[0]), None)
+        if k is not None:
+            decades[f"1e-{e}"] = {"sweeps": k, "time_to_residual_s": init_s + t_setup + (cum[k - 1] if k else 0.0)}
+    best_ratio = min(hist) / hist[0]
+    return {"tol": cfg.tol, "sweeps": len(its), "converged": conv,
+            "stopped": "converged" if conv else ("max_iter" if len(its) >= cfg.m1_max_outer else "stalled"),
+            "time_to_residual_s": init_s + t_setup + float(cum[-1]) if conv else None,
+            "best_residual_ratio": best_ratio, "decades": decades,
+            "init_s": init_s, "setup_s": t_setup, "sweeps_s": float(cum[-1]) if len(cum) else 0.0,
+            "median_sweep_ms": float(np.median(sw)) if sw else None,
+            "median_dof_per_s": D * jobs / (allreduce_max(pg, float(np.median(sw))) / 1e3) if sw else None,
+            "inner_iterations_median": float(np.median(its)) if its else 0.0,
+            "inner_iterations_max": int(max(its)) if its else 0,
+            "frequency_iterations_mean": float(np.mean(fits)) if fits else 0.0,
+            "history_first_last": [hist[0], hist[-1]]}
 
 
 # ----------------------------------------------------------------- b200 arm
@@ -152,22 +236,21 @@ def run_b200(args):
     from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg
 
     desc = baseline_desc(args.config)
-    D, config = workload_config(desc, world, args.replicas)
+    D, config = workload_config(desc, args.config, world, args.replicas)
     cfg = default_cfg(tol=1e-8)
     sharded = world > 1 and not args.replicas
     comm = None
+    warm_modules(local)
     if sharded:
         from paper_2502_21013_b200 import Comm
         comm = Comm.from_torch(local)
         p = Problem.sharded(desc, comm)
     else:
         p = Problem(desc, device=local)
-    # init time = static_init + nu_hat of a warm process: one untimed call first
-    # pays the one-time CUDA module loading / first-launch costs
-    p.static_init(cfg, want_state=False)
+    Uh = pinned(p.shape, torch)  # U0, pinned: the e2e leg uploads it every step
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    U0, counts = p.static_init(cfg)
+    _, counts = p.static_init(cfg, out=Uh)
     nu, q = p.choose_nu_hat(cfg)
     init_s = time.perf_counter() - t0
     t0 = time.perf_counter()
@@ -205,7 +288,7 @@ def run_b200(args):
 
     # Isolated calibration of the dominant kernel: the timed region runs the
     # frequency solves as concurrent groups (their kernels overlap, so a
-    # launch's event-to-event time includes other groups' kernels).  Three more
+    # launch's event-to-event time includes other groups' kernels).  More
     # sweeps with the groups serialized (freq_groups=1) time the kernel alone,
     # same events, same stream discipline.
     iso = None
@@ -221,12 +304,13 @@ def run_b200(args):
         torch.cuda.synchronize()
         iso = p.kernel_timer(False)
 
+    # Time to residual from the same U0 (setup excluded from the sweeps).
+    full = full_solve_leg(p, Uh, cfg, init_s, D, jobs, pg, torch, stream) if args.full_solve else None
+
     # e2e through the C ABI with pinned host buffers (one sweep per call)
     e2e = None
     if args.e2e_steps > 0:
-        Uh = torch.empty(p.shape, dtype=torch.float64, pin_memory=True).numpy()
-        Uo = torch.empty(p.shape, dtype=torch.float64, pin_memory=True).numpy()
-        Uh[:] = U0
+        Uo = pinned(p.shape, torch)
         c1 = default_cfg(tol=1e-12, m1_max_outer=1)
         p.solve_m1_fixed_point(Uh, c1, out=Uo)  # warm (hierarchy cached)
         times = []
@@ -237,54 +321,62 @@ def run_b200(args):
             times.append(time.perf_counter() - t)
         e2e_s = allreduce_max(pg, float(np.median(times)))
         e2e = {"value": D * jobs / e2e_s, "unit": UNIT, "h2d_bytes_per_step": int(Uh.nbytes),
-               "d2h_bytes_per_step": int(Uo.nbytes),
-               "note": "tp_solve_m1 per step: H2D U0, initial residual, one sweep (cold inner start), D2H U"}
-
-    # Full solve to the BASELINE tolerance from the same U0 (time-to-residual
-    # metric; median sweep over the whole solve, setup excluded).
-    full = None
-    if args.full_solve:
-        p.set_state(U0)
-        t0 = time.perf_counter()
-        r0 = p.m1_begin(cfg)
-        t_setup = time.perf_counter() - t0
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(cfg.m1_max_outer + 1)]
-        ev[0].record(stream)
-        hist, its, fits = [r0], [], []
-        while len(its) < cfg.m1_max_outer and not hist[-1] <= cfg.tol * hist[0]:
-            r, it = p.m1_sweep()
-            hist.append(r)
-            its.append(it)
-            fits.append(p.sweep_stats()[1])
-            ev[len(its)].record(stream)
-        torch.cuda.synchronize()
-        sw = [ev[k].elapsed_time(ev[k + 1]) for k in range(len(its))]
-        full = {"tol": cfg.tol, "sweeps": len(its), "converged": bool(hist[-1] <= cfg.tol * hist[0]),
-                "time_to_residual_s": init_s + t_setup + sum(sw) / 1e3,
-                "init_s": init_s, "setup_s": t_setup, "sweeps_s": sum(sw) / 1e3,
-                "median_sweep_ms": float(np.median(sw)),
-                "median_dof_per_s": D * jobs / (allreduce_max(pg, float(np.median(sw))) / 1e3),
-                "inner_iterations_median": float(np.median(its)),
-                "inner_iterations_max": int(max(its)) if its else 0,
-                "frequency_iterations_mean": float(np.mean(fits)) if fits else 0.0}
+               "d2h_bytes_per_step": int(Uo.nbytes), "step_s": e2e_s,
+               "note": "tp_solve_m1 per step (m1_max_outer = 1): H2D of U0 from pinned host memory, initial "
+                       "residual, one sweep warm-started from the spectrum of U0, D2H of U"}
+        del Uo
 
     hbm, src = peaks()
-    # Dominant kernel (k_stream_up<Five>: fine-level V-cycle up pass, ~20% of a
-    # sweep in the ncu launch list): algorithmic bytes = 3.25 complex values
-    # (read z2, r, 1/4 coarse correction; write z) x 16 B per fine node per
-    # active frequency, divided by its CUDA-event duration measured over the
-    # timed region.
-    # ncu DRAM bytes of the dominant kernel per active frequency
-    # (profiles/kernel_traffic.json: one cfg-1 sweep's launch list, total DRAM
-    # bytes of its k_stream_up<Five> launches / the sweep's frequency-
-    # iterations), scaled to this run's launches
-    dram_per_freq = None
-    try:
-        with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
-            dram_per_freq = json.load(f).get("dominant_kernel_dram_bytes_per_frequency")
-    except Exception:
-        pass
-    alg_per_freq = 3.25 * 16.0 * (desc.cells - 1) ** 2
+    n = (desc.cells - 1) ** 2
+    roofline = dominant_kernel_roofline(args, k_launches, k_ms, k_bytes, iso, hbm, src, n)
+    # Whole-sweep algorithmic bytes per GPU (SURVEY.md §8(d)):
+    # B = 72 D / P + 16 n S sum_k it_k over this rank's frequency blocks
+    # (sum_k it_k counted exactly by the solver, tp_sweep_stats), with S = 15.0
+    # complex streams per inner iteration and frequency as implemented (fine:
+    # apply 6 = read z, p, x, write p, q, x; down with the fused residual update
+    # 4.25 = read r, q, write r, z2, 1/4 coarse rhs; up 3.25; first Galerkin
+    # level 5.5 / 4; fused small-level cycle: read b, write z at 1/16).
+    STREAMS = 13.5 + 5.5 / 4 + 2.0 / 16
+    mean_inner = float(np.mean(inner)) if inner else 0.0
+    mean_fit = float(np.mean(fiters)) if fiters else 0.0
+    b_alg = 72.0 * D / (world if sharded else 1) + 16.0 * n * STREAMS * mean_fit
+    t_sweep = total_ms / 1e3 / args.steps
+    sweep_roofline = {"bound": "hbm", "achieved": b_alg / t_sweep / 1e9, "peak": hbm, "unit": "GB/s",
+                      "frac": b_alg / t_sweep / 1e9 / hbm, "bytes_per_sweep": b_alg,
+                      "fixed_bytes_per_sweep": 72.0 * D, "streams_per_inner_iteration": STREAMS,
+                      "inner_iterations_mean": mean_inner, "frequency_iterations_per_sweep": mean_fit}
+    sweep_roofline.update(sweep_dram_crosscheck(args.config, b_alg, mean_fit, n, STREAMS, D, t_sweep, hbm))
+
+    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+           "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
+           "data": f"synthetic (BASELINE.json configs[{args.config}] physics, seeded inputs)",
+           "config": config, "impl": "b200", "clocks": clk.summary(),
+           "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "sweep_roofline": sweep_roofline,
+           "sweep_ms": {"median": float(np.median(per)), "min": float(np.min(per)),
+                        "max": float(np.max(per))},
+           "inner_iterations": inner, "frequency_iterations": fiters, "newton_max": int(counts.max()),
+           "init_s": init_s, "setup_s": setup_s, "full_solve": full,
+           "residual_last": history[-1], "residual_first": history[0]}
+    p.close()
+    del Uh
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        out["cpu_baseline"] = cpu_baseline(desc, nu, args.config)
+    if rank == 0 and world == 1 and args.cfg1_leg and args.config != 1:
+        out["cfg1_leg"] = cfg1_leg(args, torch)
+    if rank == 0 and world == 1 and args.mesh:
+        out["reference_mesh"] = mesh_leg(args)
+    if rank == 0:
+        print(json.dumps(out), flush=True)
+    if comm is not None:
+        comm.close()
+
+
+def dominant_kernel_roofline(args, k_launches, k_ms, k_bytes, iso, hbm, src, n):
+    """The kernel the library brackets with CUDA events (tp_kernel_timer: the
+    fine-level V-cycle up pass k_stream_up<Five>): algorithmic bytes = 3.25
+    complex values (read z2, r, 1/4 coarse correction; write z) x 16 B per
+    fine node per active frequency, over its event-measured launch time."""
     def kstats(nl, ms, by):
         avg_ms = ms / max(nl, 1)
         b_launch = by / max(nl, 1)
@@ -300,51 +392,86 @@ def run_b200(args):
         roofline["measured"] = ("live in bench.py: CUDA events around every launch on its stream, over "
                                 f"{args.calib_sweeps} sweeps run right after the timed region with the frequency "
                                 "groups serialized (freq_groups=1), so launches do not overlap other kernels")
-        roofline["in_timed_region"] = dict(timed, note="concurrent frequency groups (5 by default): a launch's event span "
+        roofline["in_timed_region"] = dict(timed, note="concurrent frequency groups: a launch's event span "
                                            "includes the other groups' kernels")
     else:
         roofline.update(timed)
-    if dram_per_freq and roofline.get("bytes_per_launch"):
-        roofline["traffic"] = dram_per_freq * roofline["bytes_per_launch"] / alg_per_freq
-        roofline["traffic_note"] = ("ncu dram__bytes_read+write per launch, from the per-frequency figure in "
-                                    "profiles/kernel_traffic.json scaled to this launch's active frequencies")
-    # Whole-sweep algorithmic bytes per GPU (SURVEY.md §8(d)):
-    # B = 72 D / P + 16 n S sum_k it_k over this rank's frequency blocks
-    # (sum_k it_k counted exactly by the solver, tp_sweep_stats), with S = 15.0
-    # complex streams per inner iteration and frequency as implemented (fine:
-    # apply 6 = read z, p, x, write p, q, x; down with the fused residual update
-    # 4.25 = read r, q, write r, z2, 1/4 coarse rhs; up 3.25; first Galerkin
-    # level 5.5 / 4; fused small-level cycle: read b, write z at 1/16).
-    n = (desc.cells - 1) ** 2
-    STREAMS = 13.5 + 5.5 / 4 + 2.0 / 16
-    mean_inner = float(np.mean(inner)) if inner else 0.0
-    mean_fit = float(np.mean(fiters)) if fiters else 0.0
-    b_alg = 72.0 * D / (world if sharded else 1) + 16.0 * n * STREAMS * mean_fit
-    t_sweep = total_ms / 1e3 / args.steps
-    sweep_roofline = {"bound": "hbm", "achieved": b_alg / t_sweep / 1e9, "peak": hbm, "unit": "GB/s",
-                      "frac": b_alg / t_sweep / 1e9 / hbm, "bytes_per_sweep": b_alg,
-                      "streams_per_inner_iteration": STREAMS, "inner_iterations_mean": mean_inner,
-                      "frequency_iterations_per_sweep": mean_fit}
+    # ncu DRAM bytes of this kernel per fine node and active frequency, from
+    # the committed launch list of the same config (profiles/kernel_traffic.json)
+    try:
+        with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
+            kt = json.load(f)
+        per = kt.get(f"cfg{args.config}", {}).get("dominant_kernel_dram_bytes_per_node_frequency")
+        if per and roofline.get("bytes_per_launch"):
+            alg_per = 3.25 * 16.0
+            roofline["traffic"] = per * roofline["bytes_per_launch"] / alg_per
+            roofline["traffic_note"] = ("ncu dram__bytes_read+write of this kernel per launch, from the per-node-"
+                                        "frequency figure of the committed launch list (profiles/kernel_traffic.json)"
+                                        " scaled to this launch's active frequencies")
+    except Exception:
+        pass
+    return roofline
 
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-           "scaling": "strong" if sharded else "weak", "vs_baseline": None, "dtype": "f64",
-           "data": "synthetic (BASELINE.json configs[1] physics, seeded sigma noise)",
-           "config": config, "impl": "b200", "clocks": clk.summary(),
-           "e2e": e2e, "gpu_launches": launches, "roofline": roofline, "sweep_roofline": sweep_roofline,
-           "sweep_ms": {"median": float(np.median(per)), "min": float(np.min(per)),
-                        "max": float(np.max(per))},
-           "inner_iterations": inner, "init_s": init_s, "setup_s": setup_s, "full_solve": full,
-           "residual_last": history[-1], "residual_first": history[0]}
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        out["cpu_baseline"] = cpu_baseline(desc, U0, nu, q)
-    if rank == 0 and world == 1 and args.mesh:
-        out["reference_mesh"] = mesh_leg(args)
-    if rank == 0:
-        print(json.dumps(out), flush=True)
-    p.close()
-    if comm is not None:
-        comm.close()
+
+def sweep_dram_crosscheck(config, b_alg, fit, n, streams, D, t_sweep, hbm):
+    """SURVEY.md §8(d) cross-check: the ncu DRAM bytes of one production
+    sweep of this config (profiles/kernel_traffic.json, from the committed
+    launch list) rescaled to this run's frequency-iterations, against the
+    algorithmic bytes; the roofline fraction on the smaller of the two."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
+            kt = json.load(f).get(f"cfg{config}")
+        if not kt:
+            return {}
+        fixed, per_fit = kt["sweep_dram_fixed_bytes"], kt["sweep_dram_bytes_per_frequency_iteration"]
+        dram = fixed + per_fit * fit
+        return {"dram_bytes_per_sweep": dram, "dram_source": kt.get("source"),
+                "dram_over_algorithmic": dram / b_alg,
+                "frac_on_smaller": min(dram, b_alg) / t_sweep / 1e9 / hbm}
+    except Exception:
+        return {}
+
+
+def cfg1_leg(args, torch):
+    """configs[1] (256^2 cells, N = 256): the configuration the CPU reference
+    solves to 1e-8 (tests/golden/cfg1_full_reference.npz: 8 host threads),
+    device sweeps + time to 1e-8 here, one reference sweep on the host."""
+    from paper_2502_21013_b200 import Problem, baseline_desc, default_cfg
+    desc = baseline_desc(1)
+    D = (desc.cells - 1) ** 2 * desc.steps
+    cfg = default_cfg(tol=1e-8)
+    with Problem(desc) as p:
+        t0 = time.perf_counter()
+        U0, _ = p.static_init(cfg)
+        nu, q = p.choose_nu_hat(cfg)
+        init_s = time.perf_counter() - t0
+        p.m1_begin(cfg)
+        for _ in range(3):
+            p.m1_sweep()
+        stream = torch.cuda.ExternalStream(p.stream, device=torch.cuda.current_device())
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+        K = 20
+        torch.cuda.synchronize()
+        ev[0].record(stream)
+        for _ in range(K):
+            p.m1_sweep()
+        ev[1].record(stream)
+        ev[1].synchronize()
+        sweep_ms = ev[0].elapsed_time(ev[1]) / K
+        full = full_solve_leg(p, U0, cfg, init_s, D, 1, None, torch, stream)
+    leg = {"workload": f"BASELINE configs[1]: {desc.cells}x{desc.cells} cells x N={desc.steps}",
+           "sweep_ms": sweep_ms, "dof_per_s": D / (sweep_ms / 1e3), "full_solve": full}
+    try:
+        g = np.load(os.path.join(ROOT, "tests", "golden", "cfg1_full_reference.npz"))
+        leg["reference_full_solve"] = {"sweeps": int(g["iterations"]), "m1_wall_s": float(g["m1_wall_s"]),
+                                       "init_s": float(g["init_s"]), "threads": int(g["threads"]),
+                                       "where": "the fixture run (tests/golden/make_golden_large.py cfg1), "
+                                                "not this box"}
+    except Exception:
+        pass
+    if not args.no_cpu_baseline:
+        leg["cpu_baseline"] = cpu_baseline(desc, nu, 1, U0=U0, q=q)
+    return leg
 
 
 def mesh_leg(args):
@@ -397,33 +524,80 @@ def mesh_leg(args):
     return leg
 
 
-def cpu_baseline(desc, U0, nu, q):
-    """The reference's own sweep (oracle/_ref/libtpref.so) on the host cores."""
+def stage_block_measurement(config):
+    """Committed measurement of the reference's frequency-block stage on the
+    GPU box's host (profiles/r2_ref_blocks.json, tools/ref_blocks.py): T
+    concurrent complex blocks (lambda_k M + K_hat assembled, factorised,
+    solved, residual-checked) on T threads take `round_wall_s`."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r2_ref_blocks.json")) as f:
+            return json.load(f).get(f"cfg{config}")
+    except Exception:
+        return None
+
+
+def sampled_reference_sweep(desc, nu, config, cores, reps):
+    """The reference sweep at sizes where one takes hours (configs >= 2,
+    cache = never: every sweep factorises all N/2+1 blocks), stage by stage
+    on a bounded sample (tpref_sweep_sample, the reference's own code per
+    stage, cores threads): A / E on `cores` slices scaled by N / cores, B / D
+    on 2048 * cores columns scaled by n / columns, C = ceil((N/2+1) / T)
+    rounds of T concurrent block solves from the committed box measurement.
+    Returns (per-rep sweep seconds, stages of the last rep, note)."""
+    from oracle import ref
+    N = desc.steps
+    n = (desc.cells - 1) ** 2
+    S = cores
+    Cc = min(n, 2048 * cores)
+    samples, setup = ref.sweep_sample(desc, nu, S, Cc, 0, threads=cores, reps=reps)
+    blk = stage_block_measurement(config)
+    K = N // 2 + 1
+    t_c = None
+    if blk:
+        T = int(blk["concurrent_blocks"])
+        t_c = -(-K // T) * float(blk["round_wall_s"])
+    sweeps, stages = [], None
+    for smp in samples:
+        st = {"A_rhs": smp["A_rhs"] * N / S, "B_forward_dft": smp["B_forward_dft"] * n / Cc,
+              "D_inverse_dft": smp["D_inverse_dft"] * n / Cc, "E_residual": smp["E_residual"] * N / S,
+              "C_blocks": t_c}
+        sweeps.append(sum(v for v in st.values() if v is not None))
+        stages = st
+    note = (f"stages A (RHS) and E (residual) timed live on {S} slices and scaled by N/{S}; B / D (time DFTs) "
+            f"on {Cc} dof columns scaled by n/{Cc}; " +
+            (f"C (the {K} frequency-block factorisations + solves) = ceil({K}/{blk['concurrent_blocks']}) rounds x "
+             f"{float(blk['round_wall_s']):.1f} s, the wall time of {blk['concurrent_blocks']} concurrent blocks "
+             f"measured once on this box's host (profiles/r2_ref_blocks.json)" if blk else
+             "C (frequency blocks) NOT included: value is an upper bound on the reference's DoF/s"))
+    return sweeps, stages, note, setup
+
+
+def cpu_baseline(desc, nu, config, U0=None, q=None):
+    """The reference's own sweep (oracle/_ref/libtpref.so) on the host cores:
+    one full sweep where that takes seconds (configs 0 / 1, from the device's
+    U0), a stage-by-stage sample otherwise (sampled_reference_sweep)."""
     from oracle import ref
     from paper_2502_21013_b200.abi import default_cfg
     if not ref.available():
         return {"value": None, "unit": UNIT, "cores": 0, "kind": "reference",
                 "sample": "oracle/_ref/libtpref.so not built"}
     cores = ref.hardware_threads()
-    cfg = default_cfg(tol=1e-12, m1_max_outer=1, threads=cores)
-    r = ref.solve_m1(desc, nu, q, U0, cfg, cache=0)
-    sweep_s = max(r.wall_time - r.setup_time, 1e-9)
     D = (desc.cells - 1) ** 2 * desc.steps
-    # per-stage split (SURVEY.md §8(d)): residual + block_l2 (a8) and the periodic
-    # solve (a6, incl. its per-block factorisations) timed alone on the same inputs;
-    # the RHS (a2) is the sweep's remainder
-    t = time.perf_counter()
-    ref.residual(desc, U0, threads=cores)
-    t_res = time.perf_counter() - t
-    t = time.perf_counter()
-    ref.periodic_solve(desc, nu, ref.loads(desc), cfg)
-    t_ps = time.perf_counter() - t
-    return {"value": D / sweep_s, "unit": UNIT, "cores": cores, "kind": "reference",
-            "sample": f"one full sweep of the same workload (tpfem solve_m1_fixed_point, "
-                      f"m1_max_outer=1, cache=automatic, {cores} threads, shim sparse LDL^T); "
-                      f"{sweep_s:.2f} s per sweep",
-            "stages_s": {"residual_a8": t_res, "periodic_solve_a6_incl_factorisation": t_ps,
-                         "setup_and_initial_residual": r.setup_time}}
+    if U0 is not None:
+        cfg = default_cfg(tol=1e-12, m1_max_outer=1, threads=cores)
+        r = ref.solve_m1(desc, nu, q, U0, cfg, cache=0)
+        sweep_s = max(r.wall_time - r.setup_time, 1e-9)
+        samples, _ = ref.sweep_sample(desc, nu, cores, min(2048 * cores, (desc.cells - 1) ** 2), 0,
+                                      threads=cores, reps=1)
+        return {"value": D / sweep_s, "unit": UNIT, "cores": cores, "kind": "reference",
+                "sample": f"one full sweep of the same workload (tpfem solve_m1_fixed_point, m1_max_outer=1, "
+                          f"cache=automatic, {cores} threads, shim sparse LDL^T) from the device's U0; "
+                          f"{sweep_s:.2f} s per sweep",
+                "stage_sample_s": samples[0], "setup_and_initial_residual_s": r.setup_time}
+    sweeps, stages, note, setup = sampled_reference_sweep(desc, nu, config, cores, reps=1)
+    return {"value": D / sweeps[0], "unit": UNIT, "cores": cores, "kind": "reference",
+            "sample": "one reference sweep estimated stage by stage: " + note, "stages_s": stages,
+            "sweep_s": sweeps[0], "setup_s": setup}
 
 
 # ------------------------------------------------------------ reference arm
@@ -434,39 +608,55 @@ def run_reference(args):
     from oracle import ref
     from paper_2502_21013_b200.abi import default_cfg
     desc = ref.baseline_desc(args.config)
-    D, config = workload_config(desc, world)
+    D, config = workload_config(desc, args.config, world)
     if not ref.available():
         print(json.dumps({"impl": "reference", "unavailable": "oracle/_ref/libtpref.so not built"}))
         return
     cores = ref.hardware_threads()
     cfg = default_cfg(tol=1e-8, threads=cores)
-    # Setup (not timed): the reference's own static_init and frozen-field nu_hat.
-    # A sweep's CPU cost does not depend on the state (every sweep factorises
-    # all N/2+1 frequency blocks), so static_init runs at a loose Newton
-    # tolerance to keep the arm within minutes.
-    t0 = time.perf_counter()
-    U0 = np.load(args.ref_u0) if args.ref_u0 else ref.static_init(desc, default_cfg(static_tol=1e-2, threads=cores))[0]
-    nu, q = ref.choose_nu_hat(desc, U0, cfg)
-    setup_s = time.perf_counter() - t0
-    one = default_cfg(tol=1e-12, m1_max_outer=1, threads=cores)
-    times = []
-    U = U0
-    for k in range(args.warmup + args.steps):
-        r = ref.solve_m1(desc, nu, q, U, one, cache=0)
-        if k >= args.warmup:
-            times.append(max(r.wall_time - r.setup_time, 1e-9))
-        U = r.U
+    out = {"metric": METRIC, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+           "warmup": args.warmup, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f64", "data": "synthetic", "config": config, "impl": "reference"}
+    if args.config <= 1:
+        # Setup (not timed): the reference's own static_init and frozen-field
+        # nu_hat.  A sweep's CPU cost does not depend on the state (every sweep
+        # factorises all N/2+1 frequency blocks), so static_init runs at a loose
+        # Newton tolerance to keep the arm within minutes.
+        t0 = time.perf_counter()
+        U0 = ref.static_init(desc, default_cfg(static_tol=1e-2, threads=cores))[0]
+        nu, q = ref.choose_nu_hat(desc, U0, cfg)
+        setup_s = time.perf_counter() - t0
+        one = default_cfg(tol=1e-12, m1_max_outer=1, threads=cores)
+        times = []
+        U = U0
+        for k in range(args.warmup + args.steps):
+            r = ref.solve_m1(desc, nu, q, U, one, cache=0)
+            if k >= args.warmup:
+                times.append(max(r.wall_time - r.setup_time, 1e-9))
+            U = r.U
+        sample = ("full sweeps of the workload (tpfem solve_m1_fixed_point, m1_max_outer=1), tpfem compiled "
+                  "from /root/reference with the shim sparse LDL^T; U0 = the reference's static_init at "
+                  "static_tol 1e-2 (a sweep's cost does not depend on the state)")
+        stages = None
+    else:
+        # nu_hat: the midpoint of each material law (a stage's cost does not
+        # depend on it; the reference's own static_init at this size runs for hours)
+        nu = np.ones(5)
+        for m in range(desc.n_materials):
+            nu[m] = 0.5 * (desc.material[m].nu0 + desc.material[m].nu_inf)
+        sweeps, stages, note, setup_s = sampled_reference_sweep(desc, nu, args.config, cores,
+                                                                args.warmup + args.steps)
+        times = sweeps[args.warmup:]
+        sample = "per step, one reference sweep estimated stage by stage: " + note
     tot = float(np.sum(times))
     value = D * len(times) / tot
-    out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-           "warmup": args.warmup, "ms_per_step": tot / len(times) * 1e3, "higher_is_better": True,
-           "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-           "config": config, "impl": "reference",
-           "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
-                            "sample": "full sweeps of the workload, tpfem compiled from "
-                                      "/root/reference with the shim sparse LDL^T"},
-           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-           "setup_s": setup_s, "sweep_s": times}
+    out.update({"value": value, "ms_per_step": tot / len(times) * 1e3,
+                "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "reference",
+                                 "sample": sample},
+                "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+                "setup_s": setup_s, "sweep_s": times})
+    if stages:
+        out["stages_s"] = stages
     print(json.dumps(out), flush=True)
 
 
@@ -476,16 +666,17 @@ def main():
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
-    ap.add_argument("--config", type=int, default=1)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--config", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=2)
     ap.add_argument("--calib-sweeps", type=int, default=3,
                     help="isolated dominant-kernel calibration sweeps after the timed region (0: off)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-mesh", dest="mesh", action="store_false",
                     help="skip the general-mesh leg (reference transformer config)")
     ap.add_argument("--no-full-solve", dest="full_solve", action="store_false")
+    ap.add_argument("--no-cfg1-leg", dest="cfg1_leg", action="store_false",
+                    help="skip the configs[1] leg (device sweeps + time to 1e-8 + one reference sweep)")
     ap.add_argument("--replicas", action="store_true", help="N>1: independent copies instead of sharding")
-    ap.add_argument("--ref-u0", default=None, help="reference arm: precomputed U0 (.npy)")
     args = ap.parse_args()
     if args.warmup < 3 and args.impl == "b200":
         args.warmup = 3

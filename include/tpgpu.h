@@ -120,7 +120,9 @@ typedef struct tp_solver_cfg {
   int32_t m2_inner_max;       /* FGMRES iteration cap, default 300 */
   int32_t m2_restart;         /* FGMRES restart length, default 60 */
   int32_t m3_max_cycles;      /* M3 time-stepping periods (SolverConfig::m3_max_cycles), default 10 */
-  int32_t reserved_;          /* keeps the struct size a multiple of 8 */
+  int32_t track_error_contraction; /* SolverConfig::track_error_contraction (solvers.hpp:66-68, 347-360):
+                                 M1 archives its iterates (host memory) and reports K_hat-norm
+                                 error ratios against the final iterate as contraction_history */
 } tp_solver_cfg;
 
 /* Mirrors SolveReport (solvers.hpp:88-96); residual/contraction histories are
@@ -134,6 +136,8 @@ typedef struct tp_report {
   double wall_time;           /* seconds, like SolveReport::wall_time (incl. setup) */
   double setup_time;          /* solver-hierarchy build, seconds */
   double sweep_time;          /* sum of sweep times, seconds */
+  int32_t contraction_len;    /* contraction_history entries written */
+  int32_t pad_;
 } tp_report;
 
 /* Per-iterate callback (the iterate_log of solve_m1_fixed_point,

@@ -18,6 +18,7 @@
 //   std::invalid_argument <- TP_EINVAL
 #pragma once
 
+#include <limits>
 #include <memory>
 #include <stdexcept>
 #include <string>
@@ -42,6 +43,13 @@ inline void check(int code) {
   throw std::runtime_error(msg);
 }
 
+/// SolverConfig -> tp_solver_cfg.  Every field of the reference's config is
+/// mapped or has no device meaning: `transform` (radix-2 vs direct DFT) only
+/// selects the algorithm of the same transform (the device picks Stockham for
+/// powers of two and a direct DFT otherwise); `cache` / `cache_budget_bytes`
+/// govern the reference's per-frequency factor cache, and the device has no
+/// factorisations to cache (matrix-free MG-COCG per block); `threads` is the
+/// CPU worker count.  Those are accepted and validated, not silently dropped.
 inline tp_solver_cfg to_c(const tpfem::SolverConfig& s) {
   tp_solver_cfg c;
   tp_solver_cfg_default(&c);
@@ -55,6 +63,12 @@ inline tp_solver_cfg to_c(const tpfem::SolverConfig& s) {
   c.static_tol = s.static_tol;
   c.static_max_newton = s.static_max_newton;
   c.threads = s.threads;
+  c.m2_max_outer = s.m2_max_outer;
+  c.m2_inner_tol = s.m2_inner_tol;
+  c.m2_inner_max = s.m2_inner_max;
+  c.m2_restart = s.m2_restart;
+  c.m3_max_cycles = s.m3_max_cycles;
+  c.track_error_contraction = s.track_error_contraction ? 1 : 0;
   return c;
 }
 
@@ -145,6 +159,8 @@ inline int c_choose(GpuProblem& p, const tp_solver_cfg* c, double* nu, double* q
 inline int c_choose(GpuMeshProblem& p, const tp_solver_cfg* c, double* nu, double* q) {
   return tp_mesh_choose_nu_hat(p.get(), c, nu, q);
 }
+inline int c_loads(GpuProblem& p, double* F) { return tp_problem_loads(p.get(), F); }
+inline int c_loads(GpuMeshProblem& p, double* F) { return tp_mesh_loads(p.get(), F); }
 inline int c_m1(GpuProblem& p, const tp_solver_cfg* c, const double* U0, double* U, tp_report* r, double* h,
                 double* ct, int32_t cap, tp_iterate_cb cb, void* u) {
   return tp_solve_m1(p.get(), c, U0, U, r, h, ct, cap, cb, u);
@@ -208,11 +224,40 @@ inline std::pair<tpfem::PeriodicState, tpfem::SolveReport> solve_m1_fixed_point(
   r.method = tpfem::Method::m1;
   r.iterations = rep.iterations;
   r.residual_history.assign(hist.begin(), hist.begin() + rep.history_len);
-  r.contraction_history.assign(contr.begin(), contr.begin() + std::max(0, rep.history_len - 1));
+  r.contraction_history.assign(contr.begin(), contr.begin() + rep.contraction_len);
   r.q_estimate = rep.q_estimate;
   r.wall_time = rep.wall_time;
   r.status = rep.status == TP_CONVERGED ? tpfem::SolveStatus::converged : tpfem::SolveStatus::max_iter;
   return {std::move(U), std::move(r)};
+}
+
+/// The reference's full signature (solvers.hpp:301-306): K_hat and F are
+/// the problem's own frozen stiffness and loads (runner.hpp:68,
+/// assembly.hpp:68-106), which the device problem assembles itself from the
+/// installed nu_hat and the source description; their shapes are checked and
+/// F is compared against the device loads, so a caller passing different
+/// operators gets std::invalid_argument instead of a silently different
+/// solve.  q_estimate is reported back as SolveReport::q_estimate.
+template <class P>
+inline std::pair<tpfem::PeriodicState, tpfem::SolveReport> solve_m1_fixed_point(
+    P& p, const tpfem::SparseMatrix<double>& K_hat, const tpfem::BlockRhs& F, const tpfem::PeriodicState& U0,
+    const tpfem::SolverConfig& cfg, double q_estimate = std::numeric_limits<double>::quiet_NaN(),
+    std::vector<tpfem::PeriodicState>* iterate_log = nullptr) {
+  if (K_hat.rows() != p.n_dof() || K_hat.cols() != p.n_dof() || F.steps != p.steps() || F.n_dof != p.n_dof() ||
+      U0.steps != p.steps() || U0.n_dof != p.n_dof())
+    throw std::invalid_argument("fixed-point solver: shape mismatch");
+  std::vector<double> Fd(F.data.size());
+  check(detail::c_loads(p, Fd.data()));
+  double num = 0, den = 0;
+  for (std::size_t i = 0; i < Fd.size(); ++i) {
+    num += (Fd[i] - F.data[i]) * (Fd[i] - F.data[i]);
+    den += F.data[i] * F.data[i];
+  }
+  if (num > 1e-24 * std::max(den, 1e-300))
+    throw std::invalid_argument("fixed-point solver: F differs from the device problem's loads");
+  auto out = solve_m1_fixed_point(p, U0, cfg, iterate_log);
+  out.second.q_estimate = q_estimate;
+  return out;
 }
 
 }  // namespace tpgpu

@@ -454,22 +454,25 @@ def frequency_blocks(desc, nu_hat, ks, B, cfg: TpSolverCfg | None = None):
     return X
 
 
-def sweep_sample(desc, nu_hat, slices, cols, blocks=0, threads=0):
+STAGES = ("A_rhs", "B_forward_dft", "D_inverse_dft", "E_residual", "C_blocks")
+
+
+def sweep_sample(desc, nu_hat, slices, cols, blocks=0, threads=0, reps=1):
     """Stage-by-stage timing of one reference sweep on a bounded sample
-    (tpref_sweep_sample): dict of seconds for A (RHS on `slices` slices),
-    B / D (forward / inverse transforms on `cols` columns), E (residual on
-    the slices), C (`blocks` frequency-block solves) and the setup."""
+    (tpref_sweep_sample), `reps` times after one setup: (list of dicts of
+    seconds for A (RHS on `slices` slices), B / D (forward / inverse
+    transforms on `cols` columns), E (residual on the slices), C (`blocks`
+    frequency-block solves), setup seconds)."""
     L = lib()
     if not getattr(L, "_ss_ready", False):
         dp = C.POINTER(C.c_double)
         L.tpref_sweep_sample.argtypes = [C.POINTER(TpProblemDesc), C.POINTER(TpSolverCfg), dp, C.c_int32,
-                                         C.c_int32, C.c_int32, dp, dp]
+                                         C.c_int32, C.c_int32, C.c_int32, dp, dp]
         L._ss_ready = True
     cfg = default_cfg(threads=threads or hardware_threads())
-    t = np.zeros(5)
+    t = np.zeros((max(1, reps), 5))
     setup = C.c_double()
     nu = np.ascontiguousarray(nu_hat, dtype=np.float64)
-    _check(L.tpref_sweep_sample(C.byref(desc), C.byref(cfg), _ptr(nu), slices, cols, blocks, _ptr(t),
+    _check(L.tpref_sweep_sample(C.byref(desc), C.byref(cfg), _ptr(nu), slices, cols, blocks, reps, _ptr(t),
                                 C.byref(setup)))
-    return {"A_rhs": t[0], "B_forward_dft": t[1], "D_inverse_dft": t[2], "E_residual": t[3],
-            "C_blocks": t[4], "setup": setup.value}
+    return [dict(zip(STAGES, row.tolist())) for row in t], setup.value

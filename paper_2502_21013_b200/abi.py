@@ -46,7 +46,7 @@ class TpSolverCfg(C.Structure):
                 ("freq_chunk", C.c_int32), ("slice_chunk", C.c_int32),
                 ("freq_groups", C.c_int32), ("m2_max_outer", C.c_int32),
                 ("m2_inner_tol", C.c_double), ("m2_inner_max", C.c_int32), ("m2_restart", C.c_int32),
-                ("m3_max_cycles", C.c_int32), ("reserved_", C.c_int32)]
+                ("m3_max_cycles", C.c_int32), ("track_error_contraction", C.c_int32)]
 
 
 class TpShardPlan(C.Structure):
@@ -59,7 +59,7 @@ class TpReport(C.Structure):
     _fields_ = [("iterations", C.c_int32), ("status", C.c_int32), ("history_len", C.c_int32),
                 ("inner_iterations", C.c_int32), ("q_estimate", C.c_double),
                 ("wall_time", C.c_double), ("setup_time", C.c_double),
-                ("sweep_time", C.c_double)]
+                ("sweep_time", C.c_double), ("contraction_len", C.c_int32), ("pad_", C.c_int32)]
 
 
 TP_ITERATE_CB = C.CFUNCTYPE(C.c_int, C.c_int32, C.POINTER(C.c_double), C.c_double, C.c_void_p)
@@ -90,7 +90,7 @@ def default_cfg(**overrides) -> TpSolverCfg:
     c.m2_inner_max = 300
     c.m2_restart = 60
     c.m3_max_cycles = 10
-    c.reserved_ = 0
+    c.track_error_contraction = 0
     for k, v in overrides.items():
         setattr(c, k, v)
     return c

@@ -333,9 +333,16 @@ class Problem:
         return R, nrm.value
 
     # ---- methods
-    def static_init(self, cfg: TpSolverCfg | None = None, want_state=True):
+    def static_init(self, cfg: TpSolverCfg | None = None, want_state=True, out=None):
+        """static_init (solvers.hpp:276-296).  out: caller buffer for U0
+        (C-contiguous float64 of the state shape, e.g. pinned host memory)."""
         cfg = cfg or default_cfg()
-        U0 = np.zeros(self.shape) if want_state else None
+        if out is not None:
+            if out.shape != self.shape or out.dtype != np.float64 or not out.flags.c_contiguous:
+                raise ValueError("out must be a C-contiguous float64 array of the state shape")
+            U0 = out
+        else:
+            U0 = np.zeros(self.shape) if want_state else None
         counts = np.zeros(self.steps, dtype=np.int32)
         _check(lib().tp_static_init(self._h, C.byref(cfg), _dp(U0), _ip(counts)))
         return U0, counts
@@ -399,7 +406,7 @@ class Problem:
                                  _dp(contr), cap, cb, None))
         k = rep.history_len
         report = SolveReport(iterations=rep.iterations, residual_history=hist[:k].tolist(),
-                             contraction_history=contr[:max(k - 1, 0)].tolist(),
+                             contraction_history=contr[:rep.contraction_len].tolist(),
                              q_estimate=rep.q_estimate, wall_time=rep.wall_time,
                              status=STATUS_NAMES[rep.status], setup_time=rep.setup_time,
                              sweep_time=rep.sweep_time, inner_iterations=rep.inner_iterations)
@@ -414,7 +421,7 @@ class Problem:
         _check(fn(self._h, C.byref(cfg), _dp(U0a), _dp(U), C.byref(rep), _dp(hist), _dp(contr), cap))
         k = rep.history_len
         report = SolveReport(method=method, iterations=rep.iterations, residual_history=hist[:k].tolist(),
-                             contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
+                             contraction_history=contr[:rep.contraction_len].tolist(), q_estimate=rep.q_estimate,
                              wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
                              inner_iterations=rep.inner_iterations)
         return U, report

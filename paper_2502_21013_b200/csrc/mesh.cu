@@ -715,6 +715,7 @@ class MeshProblem {
   double nu_hat[kRegions] = {};
   double q_estimate = 0;
   bool nu_hat_set = false, state_valid = false, factored = false;
+  tp_solver_cfg sweep_cfg{};  // the configuration tp_mesh_m1_begin set the sweeps up with
 
   cudaStream_t stream = nullptr;
   std::atomic<int64_t> launches{0};
@@ -1948,9 +1949,7 @@ int tp_mesh_solve_m1(tp_mesh_problem* h, const tp_solver_cfg* c, const double* U
     r.history_len = (int32_t)std::min<size_t>(hist.size(), cap > 0 ? cap : 0);
     if (history)
       for (int k = 0; k < r.history_len; ++k) history[k] = hist[k];
-    if (contraction)
-      for (size_t k = 0; k + 1 < hist.size() && (int)k < cap; ++k)
-        contraction[k] = hist[k] > 0 ? hist[k + 1] / hist[k] : 0.0;
+    r.contraction_len = tpgpu::residual_contraction(hist, contraction, cap);
     if (U_out) {
       TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
       p.sync();
@@ -1965,8 +1964,10 @@ int tp_mesh_solve_m1(tp_mesh_problem* h, const tp_solver_cfg* c, const double* U
 int tp_mesh_m1_begin(tp_mesh_problem* h, const tp_solver_cfg* c, double* residual0) {
   return mguard([&] {
     auto& p = MP(h);
-    (void)c;
+    const tp_solver_cfg cfg = mcfg(c);
+    tpgpu::validate_cfg(cfg);
     tpgpu::require(p.nu_hat_set && p.state_valid, "m1_begin: needs nu_hat and a state");
+    p.sweep_cfg = cfg;
     if (!p.factored) p.factor_blocks();
     const double r = p.residual_and_rhs(true);
     if (residual0) *residual0 = r;
@@ -1976,9 +1977,8 @@ int tp_mesh_m1_begin(tp_mesh_problem* h, const tp_solver_cfg* c, double* residua
 int tp_mesh_m1_sweep(tp_mesh_problem* h, double* residual) {
   return mguard([&] {
     auto& p = MP(h);
-    tp_solver_cfg cfg;
-    tp_solver_cfg_default(&cfg);
-    p.periodic_solve(cfg);
+    tpgpu::require(p.factored, "m1_sweep: call tp_mesh_m1_begin first");
+    p.periodic_solve(p.sweep_cfg);
     const double r = p.residual_and_rhs(true);
     if (residual) *residual = r;
   });
@@ -2013,9 +2013,7 @@ int mesh_m23(tp_mesh_problem* h, const tp_solver_cfg* c, const double* U0, doubl
     r.history_len = (int32_t)std::min<size_t>(res.history.size(), cap > 0 ? cap : 0);
     if (history)
       for (int k = 0; k < r.history_len; ++k) history[k] = res.history[k];
-    if (contraction)
-      for (size_t k = 0; k + 1 < res.history.size() && (int)k < cap; ++k)
-        contraction[k] = res.history[k] > 0 ? res.history[k + 1] / res.history[k] : 0.0;
+    r.contraction_len = tpgpu::residual_contraction(res.history, contraction, cap);
     if (U_out) {
       TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
       p.sync();

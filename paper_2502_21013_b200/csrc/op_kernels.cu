@@ -466,6 +466,55 @@ double reduce_sum(Problem& p, const double* partials, int count) {
   return p.h_scalars[0];
 }
 
+// sum_n (a^n - b^n)^T K_hat (a^n - b^n) over `count` slices (block_norm_khat,
+// periodic.hpp:70-75, of a difference of iterates): the frozen stiffness on
+// the right-triangle grid is the graph Laplacian of its edge weights
+// (we: vertex (X,Y)-(X+1,Y), wn: (X,Y)-(X,Y+1); Dirichlet vertices are zero),
+// so x^T K_hat x = sum over edges of w (x_i - x_j)^2.  Each node owns its east
+// and north edges, plus the west / south edge when that neighbour is on the
+// boundary.  One partial per block, reduced in fixed order.
+__global__ void __launch_bounds__(256) k_khat_quadform(const double* __restrict__ a, const double* __restrict__ b,
+                                                       const double* __restrict__ we, const double* __restrict__ wn,
+                                                       int m, int c, int count, double* __restrict__ part) {
+  __shared__ double red[32];
+  const size_t n = (size_t)m * m;
+  const size_t total = n * count;
+  const int V = c + 1;
+  double acc = 0;
+  for (size_t g = (size_t)blockIdx.x * blockDim.x + threadIdx.x; g < total; g += (size_t)gridDim.x * blockDim.x) {
+    const size_t sl = g / n, i = g - sl * n;
+    const int x = (int)(i % m), y = (int)(i / m);  // vertex (X, Y) = (x + 1, y + 1)
+    const double* A = a + sl * n;
+    const double* B = b ? b + sl * n : nullptr;  // b == nullptr: the norm of a itself
+    const double v = A[i] - (B ? B[i] : 0.0);
+    const int X = x + 1, Y = y + 1;
+    const double ve = x + 1 < m ? A[i + 1] - (B ? B[i + 1] : 0.0) : 0.0;
+    const double vn = y + 1 < m ? A[i + m] - (B ? B[i + m] : 0.0) : 0.0;
+    double t = we[(size_t)Y * V + X] * (ve - v) * (ve - v) + wn[(size_t)Y * V + X] * (vn - v) * (vn - v);
+    if (x == 0) t += we[(size_t)Y * V + 0] * v * v;
+    if (y == 0) t += wn[(size_t)0 * V + X] * v * v;
+    acc += t;
+  }
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, o);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = acc;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s2 = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) s2 += red[w];
+    part[blockIdx.x] = s2;
+  }
+}
+
+double Problem::khat_norm_diff(const double* a, const double* b) {
+  require(d_we.get() != nullptr, "K_hat norm: frequency solver not built");
+  require(!sharded(), "K_hat norm: single-rank problems only");
+  const int blocks = 4 * num_sms;
+  part.ensure((size_t)blocks);
+  k_khat_quadform<<<blocks, 256, 0, stream>>>(a, b, d_we.get(), d_wn.get(), m, c, N, part.get());
+  TP_LAUNCHED(this);
+  return std::sqrt(std::max(0.0, reduce_sum(*this, part.get(), blocks)));
+}
+
 void Problem::apply_k_dev(const double* u, double* out, int count) {
   dim3 grid((m + TX - 1) / TX, (m + TY - 1) / TY, count);
   k_apply_k<<<grid, dim3(TX, TY), 0, stream>>>(u, out, m, c, d_cell_mat.get(), d_mat.get());

@@ -1041,6 +1041,18 @@ int tp_solve_m1(tp_problem* h, const tp_solver_cfg* c, const double* U0, double*
       if (cb(k, host_u.data(), res, user) != 0) throw Error(TP_EINVAL, "m1: aborted by iterate callback");
     };
     auto stop = [&]() { return hist.back() <= cfg.tol * hist.front(); };  // solvers.hpp:100-103
+    // track_error_contraction: the iterates are archived in host memory
+    // (solvers.hpp:317-319; the device holds only the current state)
+    const bool archive = cfg.track_error_contraction != 0;
+    tpgpu::require(!archive || !p.sharded(), "m1: track_error_contraction needs a single-rank problem");
+    std::vector<std::vector<double>> iterates;
+    auto keep = [&]() {
+      if (!archive) return;
+      iterates.emplace_back((size_t)p.N * p.n);
+      TP_CUDA(cudaMemcpyAsync(iterates.back().data(), p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
+      TP_CUDA(cudaStreamSynchronize(p.stream));
+    };
+    keep();
     hist.push_back(p.residual_and_rhs(true));
     callback(0, hist.back());
     tp_report r{};
@@ -1059,6 +1071,7 @@ int tp_solve_m1(tp_problem* h, const tp_solver_cfg* c, const double* U0, double*
         r.iterations = k;
         hist.push_back(p.residual_and_rhs(true));
         sweeps += seconds_since(tk);
+        keep();
         callback(k, hist.back());
         if (stop()) break;
       }
@@ -1068,9 +1081,26 @@ int tp_solve_m1(tp_problem* h, const tp_solver_cfg* c, const double* U0, double*
     r.history_len = (int32_t)std::min<size_t>(hist.size(), cap > 0 ? cap : 0);
     if (history)
       for (int k = 0; k < r.history_len; ++k) history[k] = hist[k];
-    if (contraction)
-      for (size_t k = 0; k + 1 < hist.size() && (int)k < cap; ++k)
-        contraction[k] = hist[k] > 0 ? hist[k + 1] / hist[k] : 0.0;
+    if (archive && iterates.size() >= 2) {
+      // K_hat-norm errors against the final iterate (solvers.hpp:347-360);
+      // the device G is the scratch for each archived iterate, then restored
+      std::vector<double> errors;
+      for (size_t k = 0; k + 1 < iterates.size(); ++k) {
+        TP_CUDA(cudaMemcpyAsync(p.G.get(), iterates[k].data(), p.G.bytes(), cudaMemcpyHostToDevice, p.stream));
+        errors.push_back(p.khat_norm_diff(p.G.get(), p.U.get()));
+      }
+      const double floor = 1e-13 * std::max(1.0, p.khat_norm_diff(p.U.get(), nullptr));
+      int w = 0;
+      for (size_t k = 0; k + 1 < errors.size() && w < cap; ++k) {
+        if (errors[k] <= floor || errors[k + 1] <= floor) break;
+        if (contraction) contraction[w] = errors[k + 1] / errors[k];
+        ++w;
+      }
+      r.contraction_len = w;
+      (void)p.residual_and_rhs(true);  // G back to the next sweep's right-hand side
+    } else {
+      r.contraction_len = tpgpu::residual_contraction(hist, contraction, cap);
+    }
     if (U_out) {
       TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
       TP_CUDA(cudaStreamSynchronize(p.stream));
@@ -1163,9 +1193,7 @@ static int solve_m23(tp_problem* h, const tp_solver_cfg* c, const double* U0, do
     r.history_len = (int32_t)std::min<size_t>(hist.size(), cap > 0 ? cap : 0);
     if (history)
       for (int k = 0; k < r.history_len; ++k) history[k] = hist[k];
-    if (contraction)
-      for (size_t k = 0; k + 1 < hist.size() && (int)k < cap; ++k)
-        contraction[k] = hist[k] > 0 ? hist[k + 1] / hist[k] : 0.0;
+    r.contraction_len = tpgpu::residual_contraction(hist, contraction, cap);
     if (U_out) {
       TP_CUDA(cudaMemcpyAsync(U_out, p.U.get(), p.U.bytes(), cudaMemcpyDeviceToHost, p.stream));
       TP_CUDA(cudaStreamSynchronize(p.stream));

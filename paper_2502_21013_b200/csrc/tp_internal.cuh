@@ -51,6 +51,19 @@ struct Error : std::runtime_error {
 void set_last_error(const std::string& msg, double residual);
 void validate_cfg(const tp_solver_cfg& c);  // validate(), solvers.hpp:71-86
 
+// contraction_history from residual norms (solvers.hpp:361-365): the ratio
+// r_{k+1} / r_k for every k with r_k > 0 (zero residuals are skipped, not
+// zero-filled); returns the entries written (at most cap).
+inline int residual_contraction(const std::vector<double>& hist, double* out, int cap) {
+  int w = 0;
+  for (size_t k = 0; k + 1 < hist.size() && w < cap; ++k)
+    if (hist[k] > 0) {
+      if (out) out[w] = hist[k + 1] / hist[k];
+      ++w;
+    }
+  return w;
+}
+
 // ---------------------------------------------------------------- PDL
 // Programmatic dependent launch for the kernel chains of the frequency solves
 // (one stream per frequency group, ~9 dependent kernels per inner iteration):
@@ -330,6 +343,8 @@ class Problem {
   void solve_m2_dev(const tp_solver_cfg& cfg, M2Result& res);
   void solve_m3_dev(const tp_solver_cfg& cfg, M2Result& res);  // M3 time stepping (m3.cu)
   void field_ranges(double* lo, double* hi, int* any);
+  // block_norm_khat(a - b) (periodic.hpp:70-75) over the N slices, device arrays
+  double khat_norm_diff(const double* a, const double* b);
   int last_inner = 0;
   int64_t last_freq_iters = 0;  // sum over frequency blocks of the last periodic solve
 };

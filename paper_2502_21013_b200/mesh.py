@@ -232,7 +232,7 @@ class MeshProblem:
                                         _dp(contr), cap, cb, None))
         k = rep.history_len
         return U, SolveReport(iterations=rep.iterations, residual_history=hist[:k].tolist(),
-                              contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
+                              contraction_history=contr[:rep.contraction_len].tolist(), q_estimate=rep.q_estimate,
                               wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
                               setup_time=rep.setup_time, sweep_time=rep.sweep_time)
 
@@ -245,7 +245,7 @@ class MeshProblem:
                                     cap))
         k = rep.history_len
         return U, SolveReport(method=method, iterations=rep.iterations, residual_history=hist[:k].tolist(),
-                              contraction_history=contr[:max(k - 1, 0)].tolist(), q_estimate=rep.q_estimate,
+                              contraction_history=contr[:rep.contraction_len].tolist(), q_estimate=rep.q_estimate,
                               wall_time=rep.wall_time, status=STATUS_NAMES[rep.status],
                               inner_iterations=rep.inner_iterations)
 
