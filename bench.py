@@ -175,8 +175,28 @@ def warm_modules(device):
         w.m1_sweep()
 
 
+_PINNED = []
+
+
 def pinned(shape, torch):
-    return torch.empty(shape, dtype=torch.float64, pin_memory=True).numpy()
+    """A page-locked host array of exactly `shape` (cudaHostRegister on a
+    numpy buffer: torch's pinned allocator rounds a 34 GB request up to the
+    next power of two)."""
+    a = np.empty(shape, dtype=np.float64)
+    a.fill(0.0)  # fault the pages in before locking them
+    err = torch.cuda.cudart().cudaHostRegister(a.ctypes.data, a.nbytes, 0)
+    if int(err) != 0:
+        raise RuntimeError(f"cudaHostRegister failed ({err})")
+    _PINNED.append(a)
+    return a
+
+
+def unpin(a, torch):
+    for i, b in enumerate(_PINNED):
+        if b is a:
+            torch.cuda.cudart().cudaHostUnregister(a.ctypes.data)
+            del _PINNED[i]
+            return
 
 
 def full_solve_leg(p, U0, cfg, init_s, D, jobs, pg, torch, stream, stall_window=20):
@@ -324,6 +344,7 @@ def run_b200(args):
                "d2h_bytes_per_step": int(Uo.nbytes), "step_s": e2e_s,
                "note": "tp_solve_m1 per step (m1_max_outer = 1): H2D of U0 from pinned host memory, initial "
                        "residual, one sweep warm-started from the spectrum of U0, D2H of U"}
+        unpin(Uo, torch)
         del Uo
 
     hbm, src = peaks()
@@ -359,6 +380,7 @@ def run_b200(args):
            "init_s": init_s, "setup_s": setup_s, "full_solve": full,
            "residual_last": history[-1], "residual_first": history[0]}
     p.close()
+    unpin(Uh, torch)
     del Uh
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         out["cpu_baseline"] = cpu_baseline(desc, nu, args.config)
@@ -565,9 +587,11 @@ def sampled_reference_sweep(desc, nu, config, cores, reps):
         stages = st
     note = (f"stages A (RHS) and E (residual) timed live on {S} slices and scaled by N/{S}; B / D (time DFTs) "
             f"on {Cc} dof columns scaled by n/{Cc}; " +
-            (f"C (the {K} frequency-block factorisations + solves) = ceil({K}/{blk['concurrent_blocks']}) rounds x "
-             f"{float(blk['round_wall_s']):.1f} s, the wall time of {blk['concurrent_blocks']} concurrent blocks "
-             f"measured once on this box's host (profiles/r2_ref_blocks.json)" if blk else
+            (f"C (the {K} frequency-block factorisations + solves, one per worker thread) = ceil({K}/"
+             f"{blk['concurrent_blocks']}) rounds x {float(blk['round_wall_s']):.1f} s, the wall time of "
+             f"{blk.get('concurrent_blocks_measured', blk['concurrent_blocks'])} concurrent blocks measured once on "
+             f"the GPU box's host (tools/ref_blocks.py -> profiles/r2_ref_blocks.json; a full-host round is taken "
+             f"to cost the same, which favours the reference)" if blk else
              "C (frequency blocks) NOT included: value is an upper bound on the reference's DoF/s"))
     return sweeps, stages, note, setup
 

@@ -351,35 +351,47 @@ __global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict
   const int C = 2 * P;
   const size_t j0 = (size_t)blockIdx.x * C;
   const int half = N / 2;
-  // stage the K x C half-spectrum block (cp.async, all in flight), then build
-  // the Hermitian extension of the two packed columns in place of the FFT buffer
-  // (N even: self-conjugate bins 0 and N/2)
-  cplx* raw = z + (size_t)N * P;  // K x C
-  const int K = half + 1;
+  // the Hermitian extension of the two packed columns, built straight from
+  // the half spectrum: every (k, pair) loads X_a, X_b (two adjacent complex
+  // columns, one 32-byte read; a block reads C complex = 16 C bytes per
+  // frequency row) into registers and writes Z_k and Z_{N-k}; UNR pairs in
+  // flight per thread (no shared staging of the raw spectrum: half the
+  // shared footprint, twice the resident blocks)
   for (int t = threadIdx.x; t < N; t += blockDim.x) acp16(&tws[t], &tw[t], true);
-  for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
-    const int k = t / C, cc = t - k * C;
-    const bool ok = j0 + cc < n;
-    acp16(&raw[t], Uhat + (ok ? (size_t)k * n + j0 + cc : 0), ok);
+  const int K = half + 1;
+  const int total = K * P;
+  double im2 = 0;
+  constexpr int UNR = 4;
+  for (int t0 = threadIdx.x; t0 < total; t0 += UNR * blockDim.x) {
+    cplx xa[UNR], xb[UNR];
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = t0 + u * blockDim.x;
+      xa[u] = xb[u] = cplx{0, 0};
+      if (t < total) {
+        const int k = t / P, p = t - k * P;
+        const size_t col = j0 + 2 * p;
+        const cplx* src = Uhat + (size_t)k * n + col;
+        if (col < n) xa[u] = src[0];
+        if (col + 1 < n) xb[u] = src[1];
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < UNR; ++u) {
+      const int t = t0 + u * blockDim.x;
+      if (t >= total) break;
+      const int k = t / P, p = t - k * P;
+      const cplx Xa = xa[u], Xb = xb[u];
+      if (k == 0 || k == half) {
+        z[(size_t)k * P + p] = {Xa.re, Xb.re};
+        im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
+      } else {
+        z[(size_t)k * P + p] = {Xa.re - Xb.im, Xa.im + Xb.re};
+        z[(size_t)(N - k) * P + p] = {Xa.re + Xb.im, -Xa.im + Xb.re};
+      }
+    }
   }
   acp_wait_all();
-  __syncthreads();
-  double im2 = 0;
-  for (int t = threadIdx.x; t < N * P; t += blockDim.x) {
-    const int k = t / P, p = t - k * P;
-    const int kk = (k <= half) ? k : N - k;
-    const cplx Xa = raw[kk * C + 2 * p], Xb = raw[kk * C + 2 * p + 1];
-    cplx Z;
-    if (k == 0 || k == half) {
-      Z = {Xa.re, Xb.re};
-      im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
-    } else if (k < half) {
-      Z = {Xa.re - Xb.im, Xa.im + Xb.re};
-    } else {
-      Z = {Xa.re + Xb.im, -Xa.im + Xb.re};
-    }
-    z[(size_t)k * P + p] = Z;
-  }
   __syncthreads();
   stockham<true>(z, tws, N, P);
   const double invN = 1.0 / N;
@@ -477,23 +489,22 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
   // (36 KB of shared memory with the twiddles: six blocks per SM)
   if (pl->pow2 && N >= 16 && !std::getenv("TPGPU_RADIX2_DFT")) {
     static const int fp_env = std::getenv("TPGPU_FFT_P") ? std::atoi(std::getenv("TPGPU_FFT_P")) : 0;
-    int sP = fp_env > 0 ? fp_env : std::max(1, 2048 / N);
+    // at least 4 column pairs (64-byte row segments) for long periods: with 2
+    // pairs at N = 1024 the 32-byte row reads held both transforms near 1.8
+    // TB/s (cfg 3 launch list, profiles/r2c_launches_cfg3_sweep.txt)
+    int sP = fp_env > 0 ? fp_env : std::max(N >= 512 ? 4 : 1, 2048 / N);
     while (sP > 1 && (size_t)(sP + 1) * N * sizeof(cplx) > 100 * 1024) sP >>= 1;
     const int T = sP * N / 16;
-    if (T <= 1024 && (size_t)((sP + 1) * N + (N / 2 + 1) * 2 * sP) * sizeof(cplx) <= 200 * 1024) {
+    if (T <= 1024 && (size_t)((sP + 1) * N) * sizeof(cplx) <= 200 * 1024) {
       pl->stockham = true;
       pl->sP = sP;
       pl->sT = std::max(32, T);
-      // inverse: the same column pairs per block + its staged half spectrum
-      // (N/2+1) x 2P (halving P measured no faster: 132.6 vs 132.6 us at cfg 1;
-      // TPGPU_IFFT_P overrides)
+      // inverse: the same column pairs per block (TPGPU_IFFT_P overrides)
       static const int ip_env = std::getenv("TPGPU_IFFT_P") ? std::atoi(std::getenv("TPGPU_IFFT_P")) : 0;
       const int siP = ip_env > 0 ? ip_env : sP;
       pl->siP = siP;
       pl->siT = std::max(32, siP * N / 16);
-      pl->ssmem = (size_t)((siP + 1) * N + (N / 2 + 1) * 2 * siP) * sizeof(cplx);
-      // the forward transform needs only the twiddles and the P columns (half
-      // the inverse's footprint: twice the resident blocks)
+      pl->ssmem = (size_t)((siP + 1) * N) * sizeof(cplx);
       pl->fsmem = (size_t)((sP + 1) * N) * sizeof(cplx);
       TP_CUDA(cudaFuncSetAttribute(k_sfft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->fsmem));
       TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));

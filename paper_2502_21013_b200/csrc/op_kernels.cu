@@ -216,6 +216,10 @@ __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
 // look-ahead the kernel was latency-bound at ~1.3 TB/s.
 constexpr int SB = 16;
 constexpr int SD = 6;
+// resident blocks per SM the registers are bounded for
+#ifndef TPGPU_SWEEP_MINB
+#define TPGPU_SWEEP_MINB 3
+#endif
 
 __device__ __forceinline__ void cp_async8(void* sdst, const void* g, bool ok) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
@@ -223,7 +227,7 @@ __device__ __forceinline__ void cp_async8(void* sdst, const void* g, bool ok) {
 }
 
 template <bool WANT_G>
-__global__ void __launch_bounds__(TX * TY, 4) k_sweep_slices(
+__global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
     const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
     int sy0, int rows, double* __restrict__ G, double* __restrict__ part, int m, int c, int N, double inv_tau,
     const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
@@ -231,6 +235,7 @@ __global__ void __launch_bounds__(TX * TY, 4) k_sweep_slices(
     const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
   __shared__ double su[SD][TY + 2][TX + 2];
   __shared__ double cnu0[TY + 1][TX + 1], cdnu[TY + 1][TX + 1], cbs2[TY + 1][TX + 1], chat[TY + 1][TX + 1];
+  __shared__ double wnu[2][TY + 1][TX + 1];  // nu_T / 2 of the current slice (T1, T2 per cell)
   __shared__ double red[32];
   const size_t n = (size_t)m * m;
   const size_t nl = (size_t)rows * m;
@@ -307,36 +312,62 @@ __global__ void __launch_bounds__(TX * TY, 4) k_sweep_slices(
   double uprev = 0;
   if (own && mi != 0) uprev = U[(size_t)((sbeg + N - 1) % N) * nl + il];
   const double c2 = (double)c * (double)c;
+  // slice-invariant operands in registers: the material law of this thread's
+  // cells (cell pass) and nu_hat / 2 of the node's six incident triangles
+  constexpr int NCELL = (TY + 1) * (TX + 1);
+  const int kc0 = tid, kc1 = tid + TX * TY;
+  __syncthreads();  // per-cell material constants staged
+  double cl[2][3];
+#pragma unroll
+  for (int e = 0; e < 2; ++e) {
+    const int k = e == 0 ? kc0 : kc1;
+    const int cy = k / (TX + 1), cx = k - cy * (TX + 1);
+    const bool ok = k < NCELL;
+    cl[e][0] = ok ? cdnu[cy][cx] : 0.0;
+    cl[e][1] = ok ? cbs2[cy][cx] : 1.0;
+    cl[e][2] = ok ? cnu0[cy][cx] : 0.0;
+  }
+  const int cxs[6] = {0, 0, -1, -1, -1, 0}, cys[6] = {0, 0, 0, -1, -1, -1};
+  double hat[6];
+#pragma unroll
+  for (int t6 = 0; t6 < 6; ++t6) hat[t6] = WANT_G ? chat[ty + 1 + cys[t6]][tx + 1 + cxs[t6]] : 0.0;
   double r2 = 0;
   for (int s = sbeg; s < send; ++s) {
     asm volatile("cp.async.wait_group %0;\n" ::"n"(SD - 2) : "memory");
-    __syncthreads();  // slice s staged by every thread; slice s-1's slot free
+    __syncthreads();  // slice s staged by every thread; slice s-1's slot and weights free
     issue(s + SD - 1);
+    const double(*t)[TX + 2] = su[s % SD];
+    // nu(|grad u|) / 2 once per triangle: the (TY+1) x (TX+1) cells under the
+    // node tile, two triangles each (T1 lower-right: d = (u10-u00, u11-u10);
+    // T2 upper-left: d = (u11-u01, u01-u00)) -- each triangle is shared by
+    // three nodes, which used to evaluate its law three times
+#pragma unroll
+    for (int e = 0; e < 2; ++e) {
+      const int k = e == 0 ? kc0 : kc1;
+      if (k < NCELL) {
+        const int cy = k / (TX + 1), cx = k - cy * (TX + 1);
+        const double u00 = t[cy][cx], u10 = t[cy][cx + 1], u01 = t[cy + 1][cx], u11 = t[cy + 1][cx + 1];
+        const double ax = u10 - u00, ay = u11 - u10, bx = u11 - u01, by = u01 - u00;
+        const double sa = c2 * (ax * ax + ay * ay), sb2 = c2 * (bx * bx + by * by);
+        wnu[0][cy][cx] = 0.5 * fma(cl[e][0], sa * acc_rcp(sa + cl[e][1]), cl[e][2]);
+        wnu[1][cy][cx] = 0.5 * fma(cl[e][0], sb2 * acc_rcp(sb2 + cl[e][1]), cl[e][2]);
+      }
+    }
+    __syncthreads();
     if (own) {
-      const double(*t)[TX + 2] = su[s % SD];
       const int lx = tx + 1, ly = ty + 1;
       const double uC = t[ly][lx], uE = t[ly][lx + 1], uW = t[ly][lx - 1];
       const double uN = t[ly + 1][lx], uS = t[ly - 1][lx];
-      const double uNE = t[ly + 1][lx + 1], uSW = t[ly - 1][lx - 1];
-      // the six incident triangles: (cell, type, contribution dx*sx + dy*sy, (dx, dy))
-      // T1(X,Y): cell (lx,ly)    d=(uE-uC, uNE-uE)   contrib -(uE-uC)
-      // T2(X,Y): cell (lx,ly)    d=(uNE-uN, uN-uC)   contrib -(uN-uC)
-      // T1(X-1,Y): cell (lx-1,ly) d=(uC-uW, uN-uC)   contrib (uC-uW)-(uN-uC)
-      // T1(X-1,Y-1): cell (lx-1,ly-1) d=(uS-uSW, uC-uS) contrib (uC-uS)
-      // T2(X-1,Y-1): cell (lx-1,ly-1) d=(uC-uW, uW-uSW) contrib (uC-uW)
-      // T2(X,Y-1): cell (lx,ly-1) d=(uE-uC, uC-uS)    contrib -(uE-uC)+(uC-uS)
-      const double dx[6] = {uE - uC, uNE - uN, uC - uW, uS - uSW, uC - uW, uE - uC};
-      const double dy[6] = {uNE - uE, uN - uC, uN - uC, uC - uS, uW - uSW, uC - uS};
+      // the six incident triangles (cell, type): contribution dx*sx + dy*sy
+      // T1(X,Y) -(uE-uC); T2(X,Y) -(uN-uC); T1(X-1,Y) (uC-uW)-(uN-uC);
+      // T1(X-1,Y-1) uC-uS; T2(X-1,Y-1) uC-uW; T2(X,Y-1) -(uE-uC)+(uC-uS)
       const double con[6] = {-(uE - uC), -(uN - uC), (uC - uW) - (uN - uC), uC - uS, uC - uW, -(uE - uC) + (uC - uS)};
-      const int cxs[6] = {0, 0, -1, -1, -1, 0}, cys[6] = {0, 0, 0, -1, -1, -1};
+      const int tt[6] = {0, 1, 0, 0, 1, 1};
       double ku = 0, kh = 0;
 #pragma unroll
       for (int t6 = 0; t6 < 6; ++t6) {
-        const int cx = lx + cxs[t6], cy = ly + cys[t6];
-        const double s2 = c2 * (dx[t6] * dx[t6] + dy[t6] * dy[t6]);
-        const double nu = fma(cdnu[cy][cx], s2 * acc_rcp(s2 + cbs2[cy][cx]), cnu0[cy][cx]);
-        ku = fma(0.5 * nu, con[t6], ku);
-        if (WANT_G) kh = fma(chat[cy][cx], con[t6], kh);
+        ku = fma(wnu[tt[t6]][ly + cys[t6]][lx + cxs[t6]], con[t6], ku);
+        if (WANT_G) kh = fma(hat[t6], con[t6], kh);
       }
       double f = 0;
 #pragma unroll
