@@ -218,6 +218,16 @@ int tp_m1_sweep(tp_problem* p, double* residual, int32_t* inner_iterations);
  * count of any frequency block and the sum over blocks of their iteration
  * counts (the bench's algorithmic-byte count). */
 int tp_sweep_stats(const tp_problem* p, int32_t* max_iterations, int64_t* frequency_iterations);
+/* Achieved frequency-block residuals of the last periodic solve (the
+ * reference's SparseSolver residual contract, solve.hpp:54,79-89): the
+ * largest ||r_k|| / max(||g_k||, ||g|| / sqrt(K)) -- the stopping reference
+ * the device enforces (<= inner_rtol; a batch that ends above 1e-10 of it
+ * raises TP_ESOLVE) -- and the largest ||r_k|| / ||g_k|| against the block's
+ * own right-hand side, the reference's per-solve measure.  The two differ
+ * only for blocks whose right-hand side is below their equal share of the
+ * spectrum (round-off-sized even harmonics), which stop at the share
+ * (DESIGN.md §5). */
+int tp_solve_residuals(const tp_problem* p, double* max_rel_floored, double* max_rel_own);
 /* ---- multi-GPU (one process per GPU, NCCL over NVLink) ---------------
  * Partition of a sharded problem: node-row strip [row0,row1)
  * for K(u)/residual/RHS/DFT (all N slices local), frequency block
@@ -235,8 +245,13 @@ typedef struct tp_shard_plan {
 
 typedef struct tp_comm tp_comm;
 
-/* Pure host function (no GPU): the partition every rank computes. */
+/* Pure host function (no GPU): the partition every rank computes.  freq0/freq1
+ * are SLOTS of the half spectrum: frequencies are dealt to the ranks in snake
+ * order and stored so that each rank's are contiguous;
+ * tp_shard_freq_order gives the frequency held by every slot (N/2+1 entries;
+ * the identity for one rank). */
 int tp_shard_plan_make(int32_t cells, int32_t steps, int32_t nranks, int32_t rank, tp_shard_plan* out);
+int tp_shard_freq_order(int32_t cells, int32_t steps, int32_t nranks, int32_t* slot_to_freq);
 /* ncclGetUniqueId on one rank; the caller broadcasts the 128 bytes. */
 int tp_nccl_unique_id(unsigned char id[128]);
 int tp_comm_create(const unsigned char id[128], int32_t nranks, int32_t rank, int32_t device, tp_comm** out);

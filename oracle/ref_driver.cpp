@@ -71,6 +71,7 @@ tpfem::SolverConfig to_ref(const tp_solver_cfg* c) {
   if (c->m2_inner_max > 0) s.m2_inner_max = c->m2_inner_max;
   if (c->m2_restart > 0) s.m2_restart = c->m2_restart;
   if (c->m3_max_cycles > 0) s.m3_max_cycles = c->m3_max_cycles;
+  s.track_error_contraction = c->track_error_contraction != 0;
   s.threads = c->threads > 0 ? c->threads
                              : static_cast<int>(std::max(1u, std::thread::hardware_concurrency()));
   return s;

@@ -37,7 +37,7 @@ EXPORTS = [
     "tp_m1_begin", "tp_m1_sweep", "tp_sweep_stats", "tp_problem_stream", "tp_problem_launches",
     "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
     "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
-    "tp_kernel_timer", "tp_comm_create_host",
+    "tp_kernel_timer", "tp_comm_create_host", "tp_solve_residuals", "tp_shard_freq_order",
 ]
 
 # tp_host_exchange_fn (tpgpu.h)
@@ -92,12 +92,14 @@ def lib():
         L.tp_m1_begin.argtypes = [vp, G, dp]
         L.tp_m1_sweep.argtypes = [vp, dp, ip]
         L.tp_sweep_stats.argtypes = [vp, ip, C.POINTER(C.c_int64)]
+        L.tp_solve_residuals.argtypes = [vp, dp, dp]
         L.tp_problem_stream.argtypes = [vp]
         L.tp_problem_stream.restype = vp
         L.tp_problem_launches.argtypes = [vp]
         L.tp_problem_launches.restype = C.c_int64
         SP = C.POINTER(TpShardPlan)
         L.tp_shard_plan_make.argtypes = [C.c_int32, C.c_int32, C.c_int32, C.c_int32, SP]
+        L.tp_shard_freq_order.argtypes = [C.c_int32, C.c_int32, C.c_int32, ip]
         L.tp_nccl_unique_id.argtypes = [C.c_char_p]
         L.tp_comm_create.argtypes = [C.c_char_p, C.c_int32, C.c_int32, C.c_int32, C.POINTER(vp)]
         L.tp_comm_create_host.argtypes = [C.c_int32, C.c_int32, C.c_int32, HOST_EXCHANGE_FN, vp, C.POINTER(vp)]
@@ -174,6 +176,14 @@ def shard_plan(cells: int, steps: int, nranks: int, rank: int) -> TpShardPlan:
     p = TpShardPlan()
     _check(lib().tp_shard_plan_make(cells, steps, nranks, rank, C.byref(p)))
     return p
+
+
+def shard_freq_order(cells: int, steps: int, nranks: int) -> np.ndarray:
+    """Frequency held by every slot of the sharded half spectrum (snake order,
+    DESIGN.md §6; the identity for one rank).  No GPU needed."""
+    out = np.zeros(steps // 2 + 1, dtype=np.int32)
+    _check(lib().tp_shard_freq_order(cells, steps, nranks, _ip(out)))
+    return out
 
 
 def nccl_unique_id() -> bytes:
@@ -459,6 +469,13 @@ class Problem:
         mx, tot = C.c_int32(), C.c_int64()
         _check(lib().tp_sweep_stats(self._h, C.byref(mx), C.byref(tot)))
         return mx.value, tot.value
+
+    def solve_residuals(self):
+        """(largest ||r_k|| / max(||g_k||, ||g||/sqrt(K)), largest ||r_k|| / ||g_k||)
+        over the frequency blocks of the last periodic solve (tp_solve_residuals)."""
+        a, b = C.c_double(), C.c_double()
+        _check(lib().tp_solve_residuals(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def kernel_timer(self, enable: bool):
         """(launches, ms, algorithmic bytes) of the dominant kernel since the

@@ -96,7 +96,7 @@ __device__ void transform(cplx* z, cplx* tmp, const cplx* __restrict__ tw, int N
 
 __global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N,
                                int P, int bits, int pow2, const cplx* __restrict__ tw,
-                               double* __restrict__ sq) {
+                               double* __restrict__ sq, const int* __restrict__ kslot) {
   extern __shared__ cplx smem[];
   cplx* z = smem;
   cplx* tmp = smem + (size_t)P * N;
@@ -121,7 +121,7 @@ __global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ 
     cplx X;
     if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
     else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
-    Ghat[(size_t)k * n + j0 + cc] = X;
+    Ghat[(size_t)(kslot ? kslot[k] : k) * n + j0 + cc] = X;
     e = fma(X.re, X.re, fma(X.im, X.im, e));
   }
   if (sq) block_sum_to(e, sq + blockIdx.x);
@@ -129,7 +129,7 @@ __global__ void k_rdft_forward(const double* __restrict__ G, cplx* __restrict__ 
 
 __global__ void k_rdft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N,
                                int P, int bits, int pow2, const cplx* __restrict__ tw,
-                               double* __restrict__ part) {
+                               double* __restrict__ part, const int* __restrict__ kslot) {
   extern __shared__ cplx smem[];
   __shared__ double red[2][32];
   cplx* z = smem;
@@ -144,8 +144,9 @@ __global__ void k_rdft_inverse(const cplx* __restrict__ Uhat, double* __restrict
     const size_t ja = j0 + 2 * p, jb = ja + 1;
     cplx Xa{0, 0}, Xb{0, 0};
     const int kk = (k <= half) ? k : N - k;
-    if (ja < n) Xa = Uhat[(size_t)kk * n + ja];
-    if (jb < n) Xb = Uhat[(size_t)kk * n + jb];
+    const size_t row = (size_t)(kslot ? kslot[kk] : kk) * n;
+    if (ja < n) Xa = Uhat[row + ja];
+    if (jb < n) Xb = Uhat[row + jb];
     cplx Z;
     if (k == 0 || (even && k == half)) {
       // self-conjugate bins: the real parts form the Hermitian spectrum; the
@@ -218,6 +219,17 @@ __constant__ double kC16[16] = {1.0,
                                 0.70710678118654752440,
                                 0.92387953251128673848};
 
+// Shared layout of the Stockham columns: complex entry e = pos * P + p lives
+// at zx(e) = e + e / 64 -- one 16-byte pad per kilobyte, so the first pass's
+// stores (stride R P entries between the lanes of a warp) spread over the
+// banks instead of hitting the same 64 bytes eight times (ncu at cfg 3: 52 %
+// of the forward's shared stores were bank conflicts without it).
+#ifndef TPGPU_FFT_PAD
+#define TPGPU_FFT_PAD 1
+#endif
+__device__ __forceinline__ int zx(int e) { return TPGPU_FFT_PAD ? e + (e >> 6) : e; }
+__host__ __device__ constexpr int zx_size(int e) { return TPGPU_FFT_PAD ? e + (e >> 6) + 1 : e; }
+
 template <int R>
 __device__ __forceinline__ constexpr int rev_bits(int i) {
   int r = 0;
@@ -269,7 +281,7 @@ __device__ __forceinline__ void stockham_pass(cplx* z, const cplx* tw, int N, in
   for (int b = 0; b < B; ++b) {
     const int t = threadIdx.x + b * T, p = t % P, j = t / P;
 #pragma unroll
-    for (int r = 0; r < R; ++r) v[b][r] = z[(size_t)(j + r * NR) * P + p];
+    for (int r = 0; r < R; ++r) v[b][r] = z[zx((j + r * NR) * P + p)];
   }
   __syncthreads();
 #pragma unroll
@@ -288,7 +300,7 @@ __device__ __forceinline__ void stockham_pass(cplx* z, const cplx* tw, int N, in
     dft_reg<R, INV>(v[b]);
     const int base = (j / Ns) * Ns * R + k;
 #pragma unroll
-    for (int r = 0; r < R; ++r) z[(size_t)(base + r * Ns) * P + p] = v[b][r];
+    for (int r = 0; r < R; ++r) z[zx((base + r * Ns) * P + p)] = v[b][r];
   }
   __syncthreads();
 }
@@ -309,7 +321,8 @@ __device__ void stockham(cplx* z, const cplx* tw, int N, int P) {
 
 // shared layout: twiddles W_N^m (N), then the P interleaved columns (P N)
 __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N, int P,
-                               const cplx* __restrict__ tw, double* __restrict__ sq) {
+                               const cplx* __restrict__ tw, double* __restrict__ sq,
+                               const int* __restrict__ kslot) {
   extern __shared__ cplx smem[];
   cplx* tws = smem;
   cplx* z = smem + N;
@@ -321,7 +334,7 @@ __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ 
   for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
     const int i = t / C, cc = t - i * C;
     const bool ok = j0 + cc < n;
-    acp8(&zd[(size_t)i * C + cc], G + (ok ? (size_t)i * n + j0 + cc : 0), ok);  // = z[i P + cc/2].{re,im}
+    acp8(&zd[2 * zx(i * P + (cc >> 1)) + (cc & 1)], G + (ok ? (size_t)i * n + j0 + cc : 0), ok);  // z[i P + cc/2].{re,im}
   }
   acp_wait_all();
   __syncthreads();
@@ -332,18 +345,19 @@ __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ 
     const int k = t / C, cc = t - k * C;
     if (j0 + cc >= n) continue;
     const int p = cc >> 1;
-    const cplx Zk = z[(size_t)k * P + p], Zm = conj(z[(size_t)((N - k) % N) * P + p]);
+    const cplx Zk = z[zx(k * P + p)], Zm = conj(z[zx(((N - k) % N) * P + p)]);
     cplx X;
     if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
     else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
-    Ghat[(size_t)k * n + j0 + cc] = X;
+    Ghat[(size_t)(kslot ? kslot[k] : k) * n + j0 + cc] = X;
     e = fma(X.re, X.re, fma(X.im, X.im, e));
   }
   if (sq) block_sum_to(e, sq + blockIdx.x);
 }
 
 __global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N, int P,
-                               const cplx* __restrict__ tw, double* __restrict__ part) {
+                               const cplx* __restrict__ tw, double* __restrict__ part,
+                               const int* __restrict__ kslot) {
   extern __shared__ cplx smem[];
   __shared__ double red[2][32];
   cplx* tws = smem;
@@ -371,7 +385,7 @@ __global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict
       if (t < total) {
         const int k = t / P, p = t - k * P;
         const size_t col = j0 + 2 * p;
-        const cplx* src = Uhat + (size_t)k * n + col;
+        const cplx* src = Uhat + (size_t)(kslot ? kslot[k] : k) * n + col;
         if (col < n) xa[u] = src[0];
         if (col + 1 < n) xb[u] = src[1];
       }
@@ -383,11 +397,11 @@ __global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict
       const int k = t / P, p = t - k * P;
       const cplx Xa = xa[u], Xb = xb[u];
       if (k == 0 || k == half) {
-        z[(size_t)k * P + p] = {Xa.re, Xb.re};
+        z[zx(k * P + p)] = {Xa.re, Xb.re};
         im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
       } else {
-        z[(size_t)k * P + p] = {Xa.re - Xb.im, Xa.im + Xb.re};
-        z[(size_t)(N - k) * P + p] = {Xa.re + Xb.im, -Xa.im + Xb.re};
+        z[zx(k * P + p)] = {Xa.re - Xb.im, Xa.im + Xb.re};
+        z[zx((N - k) * P + p)] = {Xa.re + Xb.im, -Xa.im + Xb.re};
       }
     }
   }
@@ -400,7 +414,7 @@ __global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict
   for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
     const int i = t / C, cc = t - i * C;
     if (j0 + cc >= n) continue;
-    const double x = zd[(size_t)i * C + cc] * invN;
+    const double x = zd[2 * zx(i * P + (cc >> 1)) + (cc & 1)] * invN;
     U[(size_t)i * n + j0 + cc] = x;
     re2 += x * x;
   }
@@ -493,9 +507,9 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
     // pairs at N = 1024 the 32-byte row reads held both transforms near 1.8
     // TB/s (cfg 3 launch list, profiles/r2c_launches_cfg3_sweep.txt)
     int sP = fp_env > 0 ? fp_env : std::max(N >= 512 ? 4 : 1, 2048 / N);
-    while (sP > 1 && (size_t)(sP + 1) * N * sizeof(cplx) > 100 * 1024) sP >>= 1;
+    while (sP > 1 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) > (fp_env > 0 ? 200 : 100) * 1024) sP >>= 1;
     const int T = sP * N / 16;
-    if (T <= 1024 && (size_t)((sP + 1) * N) * sizeof(cplx) <= 200 * 1024) {
+    if (T <= 1024 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) <= 200 * 1024) {
       pl->stockham = true;
       pl->sP = sP;
       pl->sT = std::max(32, T);
@@ -504,8 +518,8 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
       const int siP = ip_env > 0 ? ip_env : sP;
       pl->siP = siP;
       pl->siT = std::max(32, siP * N / 16);
-      pl->ssmem = (size_t)((siP + 1) * N) * sizeof(cplx);
-      pl->fsmem = (size_t)((sP + 1) * N) * sizeof(cplx);
+      pl->ssmem = (size_t)(N + zx_size(siP * N)) * sizeof(cplx);
+      pl->fsmem = (size_t)(N + zx_size(sP * N)) * sizeof(cplx);
       TP_CUDA(cudaFuncSetAttribute(k_sfft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->fsmem));
       TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
     }
@@ -532,10 +546,10 @@ void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
   FftPlan& pl = plan_for(*c.plan, c.N);
   const int blocks = dft_forward_blocks(c);
   if (pl.stockham) {
-    k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq);
+    k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq, c.kslot);
   } else {
     k_rdft_forward<<<blocks, 256, pl.smem, c.stream>>>(G, Ghat, c.n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
-                                                       sq);
+                                                       sq, c.kslot);
   }
   launched(c);
 }
@@ -548,10 +562,10 @@ void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, doub
   c.red->ensure(16);
   if (pl.stockham) {
     k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.N, pl.siP, pl.tw.get(),
-                                                            c.part->get());
+                                                            c.part->get(), c.kslot);
   } else {
     k_rdft_inverse<<<blocks, 256, pl.smem, c.stream>>>(Uhat, U, c.n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
-                                                       c.part->get());
+                                                       c.part->get(), c.kslot);
   }
   launched(c);
   k_reduce_pairs<<<1, 1024, 0, c.stream>>>(c.part->get(), blocks, c.red->get());
@@ -567,7 +581,8 @@ void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, doub
 namespace {
 DftCtx ctx_of(Problem& p) {
   // columns of this rank's strip
-  return DftCtx{p.N, (size_t)p.sh.nr, p.stream, &p.fft_plan, &p.part, &p.red, p.h_scalars, &p.launches};
+  return DftCtx{p.N, (size_t)p.sh.nr, p.stream, &p.fft_plan, &p.part, &p.red, p.h_scalars, &p.launches,
+                p.d_kslot.get()};
 }
 }  // namespace
 

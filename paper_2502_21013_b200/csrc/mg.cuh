@@ -117,7 +117,7 @@ struct BatchSolver {
   DevBuf<T> rho, mu, alpha, beta;
   DevBuf<T> rho2;               // fused scalars: rho of the two most recent iterations (2B)
   DevBuf<double> partA, partD;  // fused scalars: apply / down partials (kept apart from the up pass's)
-  DevBuf<double> bn2, rn2;
+  DevBuf<double> bn2, rn2, bown;
   DevBuf<int> active;
   DevBuf<int> count;
   DevBuf<unsigned> done_ctr;  // blocks of the stopping-test kernel that finished (last one publishes)

@@ -142,8 +142,10 @@ struct Problem::FreqWork {
   int chunk = 0;  // frequencies per group
   int nL = 0;
   int req_chunk = 0, req_groups = 0;  // the configuration it was built for
+  std::unique_ptr<WorkerPool> pool;  // parts - 1 persistent helper threads
   BatchSolver<0>& group(int g) { return g == 0 ? solver : *extra[g - 1]; }
   ~FreqWork() {
+    pool.reset();
     for (auto& e : ev_out)
       if (e) cudaEventDestroy(e);
     if (ev_in) cudaEventDestroy(ev_in);
@@ -271,6 +273,12 @@ Problem::Problem(const tp_problem_desc& d, int dev, const ShardInfo* shard) : de
   if (sharded()) {
     Ghat_f.alloc((size_t)(sh.k1 - sh.k0) * n);
     Uhat_f.alloc((size_t)(sh.k1 - sh.k0) * n);
+    if (!sh.kperm.empty()) {
+      std::vector<int> slot(K);
+      for (int s2 = 0; s2 < K; ++s2) slot[sh.kperm[s2]] = s2;
+      d_kslot.alloc(K);
+      TP_CUDA(cudaMemcpy(d_kslot.get(), slot.data(), K * sizeof(int), cudaMemcpyHostToDevice));
+    }
   }
   red.alloc(4096);
   TP_CUDA(cudaMemsetAsync(U.get(), 0, U.bytes(), stream));
@@ -393,7 +401,7 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
   const int Kr = sh.k1 - sh.k0;
   std::vector<cplx> lam(Kr);
   for (int kk = 0; kk < Kr; ++kk) {
-    const int k = sh.k0 + kk;
+    const int k = freq_of_slot(sh.k0 + kk);
     cplx& lk = lam[kk];
     if (k == 0) lk = {0.0, 0.0};
     else if (2 * k == N) lk = {2.0 / tau, 0.0};
@@ -611,6 +619,7 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
     sv.coarse_inv = w.inv.get() + (size_t)k0 * w.nL * w.nL;
     return sv.solve(spec_in() + (size_t)k0 * n, spec_out() + (size_t)k0 * n, nb, warm, sst);
   };
+  double rel_f = 0, rel_o = 0;
   if (w.parts == 1) {
     for (int k0 = 0; k0 < Kr; k0 += w.chunk) {
       SolveStats cs;
@@ -621,6 +630,8 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
         st->batch_iterations += cs.batch_iterations;
         st->max_rel_residual = std::max(st->max_rel_residual, cs.max_rel_residual);
       }
+      rel_f = std::max(rel_f, cs.max_rel_residual);
+      rel_o = std::max(rel_o, cs.max_rel_residual_own);
     }
   } else {
     // groups of `parts` chunks: group 0 on hs[0] (this thread), the others on
@@ -659,10 +670,8 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
         tl_stream = nullptr;
         if (dbg_groups) gsec[g] = std::chrono::duration<double>(std::chrono::steady_clock::now() - tg0).count();
       };
-      std::vector<std::thread> helpers;
-      for (int g = 1; g < P; ++g) helpers.emplace_back(body, g);
-      body(0);
-      for (auto& t : helpers) t.join();
+      if (!w.pool || w.pool->helpers() != P - 1) w.pool = std::make_unique<WorkerPool>(P - 1);
+      w.pool->run(body);
       if (dbg_groups) {
         std::string line = "groups:";
         for (int g = 0; g < P; ++g)
@@ -684,11 +693,15 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
           st->batch_iterations += gst[g].batch_iterations;
           st->max_rel_residual = std::max(st->max_rel_residual, gst[g].max_rel_residual);
         }
+        rel_f = std::max(rel_f, gst[g].max_rel_residual);
+        rel_o = std::max(rel_o, gst[g].max_rel_residual_own);
       }
     }
   }
   last_inner = iters;
   last_freq_iters = fiters;
+  last_rel_floored = sharded() ? global_max(rel_f) : rel_f;
+  last_rel_own = sharded() ? global_max(rel_o) : rel_o;
   if (sharded()) alltoall_from_freq();
   double re2 = 0, im2 = 0;
   launch_rdft_inverse(*this, Uhat.get(), out, &re2, &im2);
@@ -1004,6 +1017,14 @@ int tp_m1_sweep(tp_problem* h, double* residual, int32_t* inner) {
     const double r = p.residual_and_rhs(true);
     if (residual) *residual = r;
     if (inner) *inner = st.iterations;
+  });
+}
+
+int tp_solve_residuals(const tp_problem* h, double* max_rel_floored, double* max_rel_own) {
+  return guarded([&] {
+    tpgpu::require(h && h->impl, "null problem handle");
+    if (max_rel_floored) *max_rel_floored = h->impl->last_rel_floored;
+    if (max_rel_own) *max_rel_own = h->impl->last_rel_own;
   });
 }
 

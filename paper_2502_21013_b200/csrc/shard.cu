@@ -181,6 +181,18 @@ static void comm_allgather(tp_comm* c, const void* src, void* dst, size_t bytes,
   comm_exchange(c, s, r, stream);
 }
 
+// Frequencies are dealt to the ranks in boustrophedon ("snake") order --
+// rounds of P consecutive frequencies, alternating direction: round 0 gives
+// k = 0..P-1 to ranks 0..P-1, round 1 gives k = P..2P-1 to ranks P-1..0 --
+// so every rank holds frequencies from the whole spectrum.  The block solves'
+// cost falls steeply with k (cfg 3, measured: k = 1..20 take 7-8 COCG
+// iterations, k > 140 none; odd-symmetric sources leave every even harmonic
+// at round-off, so those take none either): a contiguous split would give rank
+// 0 most of the work, and plain round-robin with an even P would give some
+// ranks only even (free) harmonics.  In memory the spectrum is stored in
+// slot order (slot s holds frequency kperm[s]): each rank's frequencies are
+// a contiguous slot block [ks[r], ks[r+1]), so the all-to-alls stay block
+// transfers; only the time-DFT kernels index by the permutation.
 void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh) {
   require(P >= 1 && r >= 0 && r < P, "shard: rank out of range");
   require(m >= P, "shard: more ranks than grid rows");
@@ -193,9 +205,20 @@ void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh) {
   sh.ss.resize(P + 1);
   for (int q = 0; q <= P; ++q) {
     sh.ys[q] = (int)((long)m * q / P);
-    sh.ks[q] = (int)((long)K * q / P);
     sh.ss[q] = (int)((long)N * q / P);
   }
+  std::vector<std::vector<int>> own(P);
+  for (int k = 0; k < K; ++k) {
+    const int round = k / P, pos = k % P;
+    own[(round & 1) ? P - 1 - pos : pos].push_back(k);
+  }
+  sh.kperm.clear();
+  sh.ks[0] = 0;
+  for (int q = 0; q < P; ++q) {
+    sh.kperm.insert(sh.kperm.end(), own[q].begin(), own[q].end());
+    sh.ks[q + 1] = sh.ks[q] + (int)own[q].size();
+  }
+  if (P == 1) sh.kperm.clear();  // identity
   sh.y0 = sh.ys[r];
   sh.y1 = sh.ys[r + 1];
   sh.k0 = sh.ks[r];
@@ -204,7 +227,6 @@ void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh) {
   sh.s1 = sh.ss[r + 1];
   sh.nr = (sh.y1 - sh.y0) * m;
 }
-
 
 // Halo rows of all N slices: my first owned row goes to rank r-1 (its hi),
 // my last to rank r+1 (its lo).
@@ -394,6 +416,21 @@ int tp_shard_plan_make(int32_t cells, int32_t steps, int32_t nranks, int32_t ran
     out->slice0 = sh.s0;
     out->slice1 = sh.s1;
     out->n_local = sh.nr;
+    return TP_OK;
+  } catch (const std::exception& e) {
+    tpgpu::set_last_error(e.what(), -1.0);
+    return TP_EINVAL;
+  }
+}
+
+int tp_shard_freq_order(int32_t cells, int32_t steps, int32_t nranks, int32_t* slot_to_freq) {
+  try {
+    tpgpu::require(slot_to_freq != nullptr, "null argument");
+    tpgpu::require(cells >= 2 && steps >= 1, "shard plan: bad sizes");
+    tpgpu::ShardInfo sh;
+    const int K = steps / 2 + 1;
+    tpgpu::make_partition(cells - 1, K, steps, nranks, 0, sh);
+    for (int s = 0; s < K; ++s) slot_to_freq[s] = sh.kperm.empty() ? s : sh.kperm[s];
     return TP_OK;
   } catch (const std::exception& e) {
     tpgpu::set_last_error(e.what(), -1.0);

@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 
 #include <atomic>
+#include <condition_variable>
 #include <cstdint>
+#include <functional>
+#include <thread>
 #include <memory>
 #include <mutex>
 #include <stdexcept>
@@ -200,7 +203,72 @@ class Problem;
 struct SolveStats {
   int iterations = 0;
   int64_t batch_iterations = 0;
-  double max_rel_residual = 0;
+  double max_rel_residual = 0;      // ||r_k|| / max(||g_k||, ||g|| / sqrt(K)): the enforced stopping reference
+  double max_rel_residual_own = 0;  // ||r_k|| / ||g_k||: the reference SparseSolver's per-solve measure
+};
+
+// ---------------------------------------------------------------- host workers
+// Persistent helper threads that drive concurrent frequency groups (each
+// group's kernels go to its own stream; the host thread of a group waits on
+// its own convergence counters).  run(f) calls f(0) on the caller and f(g),
+// g = 1..n, on the helpers, and returns when all have finished: no thread is
+// created per sweep.
+class WorkerPool {
+ public:
+  explicit WorkerPool(int helpers) {
+    for (int g = 1; g <= helpers; ++g) th_.emplace_back([this, g] { loop(g); });
+  }
+  ~WorkerPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+      ++gen_;
+    }
+    cv_.notify_all();
+    for (auto& t : th_) t.join();
+  }
+  int helpers() const { return (int)th_.size(); }
+  void run(const std::function<void(int)>& f) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &f;
+      pending_ = (int)th_.size();
+      ++gen_;
+    }
+    cv_.notify_all();
+    f(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_cv_.wait(lk, [this] { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int g) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&] { return gen_ != seen; });
+        seen = gen_;
+        if (stop_) return;
+        job = job_;
+      }
+      (*job)(g);  // f catches its own exceptions (problem.cu)
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        --pending_;
+      }
+      done_cv_.notify_one();
+    }
+  }
+  std::vector<std::thread> th_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_cv_;
+  const std::function<void(int)>* job_ = nullptr;
+  int pending_ = 0;
+  uint64_t gen_ = 0;
+  bool stop_ = false;
 };
 
 // ---------------------------------------------------------------- sharding
@@ -214,7 +282,8 @@ struct ShardInfo {
   int k0 = 0, k1 = 0;
   int s0 = 0, s1 = 0;
   int nr = 0;  // local dofs (y1-y0)*m
-  std::vector<int> ys, ks, ss;  // partition points, P+1 each
+  std::vector<int> ys, ks, ss;  // partition points, P+1 each (ks: frequency slots)
+  std::vector<int> kperm;       // slot -> frequency (empty: identity, P == 1)
   tp_comm* comm = nullptr;      // NCCL or host-staged transport (shard.cu)
 };
 void make_partition(int m, int K, int N, int P, int r, ShardInfo& sh);
@@ -281,6 +350,8 @@ class Problem {
   DevBuf<double> halo_lo, halo_hi, halo_send;  // N*m each
   DevBuf<cplx> Ghat_f, Uhat_f, xstage;         // (k1-k0)*n frequency blocks, staging
   DevBuf<double> red_all;                      // P doubles (allgather)
+  DevBuf<int> d_kslot;                         // frequency -> spectrum slot (sharded; else none)
+  int freq_of_slot(int s) const { return sh.kperm.empty() ? s : sh.kperm[s]; }
   DevBuf<cplx> uhat_prev;  // warm-start extrapolation: the spectrum of the sweep before
   bool uhat_prev_valid = false;
   double extrap_theta = 0.0;  // > 0: the next periodic_solve_with extrapolates its warm start
@@ -289,6 +360,11 @@ class Problem {
   void exchange_halo();
   double global_sum(double local);
   void global_minmax(double* lo, double* hi, int count);
+  double global_max(double v) {
+    double lo = v, hi = v;
+    global_minmax(&lo, &hi, 1);
+    return hi;
+  }
   void global_sum_ints(std::vector<int>& v);
   void alltoall_to_freq(const cplx* src = nullptr, cplx* dst = nullptr);  // Ghat (K x nr) -> Ghat_f ((k1-k0) x n)
   // warm start of the first sweep's frequency solves: the spectrum of the
@@ -347,6 +423,7 @@ class Problem {
   double khat_norm_diff(const double* a, const double* b);
   int last_inner = 0;
   int64_t last_freq_iters = 0;  // sum over frequency blocks of the last periodic solve
+  double last_rel_floored = 0, last_rel_own = 0;  // achieved block residuals of the last periodic solve
 };
 
 // kernels / helpers implemented in the .cu files
@@ -368,6 +445,7 @@ struct DftCtx {
   DevBuf<double>* red;
   double* h_scalars;
   std::atomic<int64_t>* launches;
+  const int* kslot = nullptr;  // frequency k -> row of the half spectrum (nullptr: k)
 };
 int dft_forward_blocks(const DftCtx& c);
 void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq = nullptr);

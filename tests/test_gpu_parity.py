@@ -315,3 +315,43 @@ def test_m3_timestepping_matches_reference(ref, cfg0_ref):
     np.testing.assert_allclose(h[1], hr[1], rtol=1e-8)
     np.testing.assert_allclose(h[2:], hr[2:], rtol=1e-2)
     assert rel(U, Ur) <= 1e-8
+
+
+def test_track_error_contraction_matches_reference(cfg0_ref, ref):
+    """SolverConfig::track_error_contraction (solvers.hpp:66-68, 347-360):
+    M1 archives its iterates and reports K_hat-norm error ratios against the
+    final iterate, cut where an error reaches 1e-13 max(1, ||U||_K_hat).
+    The ratios compare errors that shrink to that floor, so the late ones
+    carry the 1e-12 difference of the two final iterates: the leading half is
+    checked to 1e-6, the cut point to within three iterates."""
+    r = cfg0_ref
+    cfg = default_cfg(tol=1e-8, track_error_contraction=1)
+    mr = ref.solve_m1(r["desc"], r["nu"], r["q"], r["U0"], cfg)
+    with Problem(r["desc"]) as p:
+        p.set_state(r["U0"])
+        p.set_nu_hat(r["nu"], r["q"])
+        U, rep = p.solve_m1_fixed_point(r["U0"], cfg)
+    assert rep.iterations == mr.iterations
+    c, cr = np.asarray(rep.contraction_history), np.trim_zeros(np.asarray(mr.contraction), "b")
+    assert abs(len(c) - len(cr)) <= 3, (len(c), len(cr))
+    h = min(len(c), len(cr)) // 2
+    assert h >= 10
+    assert np.max(np.abs(c[:h] - cr[:h]) / cr[:h]) <= 1e-6
+
+
+def test_block_residual_contract_reported():
+    """tp_solve_residuals: the achieved relative residual of every frequency
+    block after a periodic solve, against the enforced stopping reference
+    (<= inner_rtol) and against the block's own right-hand side."""
+    d = baseline_desc(0)
+    cfg = default_cfg(tol=1e-8)
+    with Problem(d) as p:
+        p.static_init(cfg, want_state=False)
+        p.choose_nu_hat(cfg)
+        rng = np.random.default_rng(3)
+        G = rng.standard_normal(p.shape)
+        p.periodic_solve(G, cfg)
+        floored, own = p.solve_residuals()
+    assert 0 < floored <= cfg.inner_rtol * 1.0001
+    # random right-hand sides fill every frequency: no block is below its share
+    assert own <= 1e-10

@@ -55,6 +55,26 @@ def test_partition_covers_everything_once(cells, steps, P):
         assert p["n_local"] == (p["row1"] - p["row0"]) * m
 
 
+@pytest.mark.parametrize("steps,P", [(1024, 8), (1024, 2), (256, 4), (63, 3)])
+def test_frequency_order_is_a_balanced_permutation(steps, P):
+    """Snake-dealt frequencies: a permutation of 0..N/2, each
+    rank's slots contiguous, every rank a spread of the spectrum (its mean
+    frequency within one round of the global mean) and a balanced share of
+    odd harmonics (the only ones that iterate under odd-symmetric sources)."""
+    from paper_2502_21013_b200 import shard_freq_order
+    K = steps // 2 + 1
+    order = shard_freq_order(2049, steps, P)
+    assert sorted(order.tolist()) == list(range(K))
+    plans = [plan_of(2049, steps, P, r) for r in range(P)]
+    odd = []
+    for p in plans:
+        ks = order[p["freq0"]:p["freq1"]]
+        assert abs(ks.mean() - (K - 1) / 2) <= P
+        odd.append(int(np.sum(ks % 2)))
+    assert max(odd) - min(odd) <= 2
+    assert np.array_equal(shard_freq_order(2049, steps, 1), np.arange(K))
+
+
 def test_partition_rejects_too_many_ranks():
     from paper_2502_21013_b200 import shard_plan
     with pytest.raises(ValueError):
@@ -119,8 +139,11 @@ def _worker(rank, world, port, cells, steps, out_path):
     parts = [torch.zeros(1, dtype=torch.float64) for _ in range(world)]
     dist.all_gather(parts, r2)
     res_norm = float(np.sqrt(sum(float(p.item()) for p in parts)))  # rank order
-    # 3. forward DFT along time (local), half spectrum K x n_r
-    Gh = np.fft.fft(G, axis=0)[:K]
+    # 3. forward DFT along time (local), half spectrum K x n_r, stored in the
+    # library's slot order (snake-dealt frequencies, tp_shard_freq_order)
+    from paper_2502_21013_b200 import shard_freq_order
+    order = shard_freq_order(cells, steps, world)
+    Gh = np.fft.fft(G, axis=0)[:K][order]
     # 4. all-to-all strips -> frequency blocks
     Ghf = np.zeros((me["freq1"] - me["freq0"], n), dtype=complex)
     for q in range(world):
@@ -135,8 +158,8 @@ def _worker(rank, world, port, cells, steps, out_path):
         Ghf[:, pq["row0"] * m:pq["row1"] * m] = got
     # 5. solve my frequencies on the full grid
     Uhf = np.zeros_like(Ghf)
-    for kk, k in enumerate(range(me["freq0"], me["freq1"])):
-        lam = O.symbol(k, N, g.tau)
+    for kk, slot in enumerate(range(me["freq0"], me["freq1"])):
+        lam = O.symbol(int(order[slot]), N, g.tau)
         A = (lam * sp.diags(mass) + Kh).astype(complex).tocsc()
         Uhf[kk] = spla.spsolve(A, Ghf[kk])
     # 6. all-to-all back, inverse DFT of my strip
@@ -151,6 +174,7 @@ def _worker(rank, world, port, cells, steps, out_path):
             got = sendrecv(np.stack([blk.real, blk.imag], -1), q, sh)
             got = got[..., 0] + 1j * got[..., 1]
         Uh[pq["freq0"]:pq["freq1"]] = got
+    Uh = Uh[np.argsort(order)]  # slot order -> frequency order
     full = np.zeros((N, me["n_local"]), dtype=complex)
     full[:K] = Uh
     for k in range(1, (N + 1) // 2):
