@@ -320,7 +320,7 @@ __device__ void stockham(cplx* z, const cplx* tw, int N, int P) {
 }
 
 // shared layout: twiddles W_N^m (N), then the P interleaved columns (P N)
-__global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N, int P,
+__global__ void __launch_bounds__(512) k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ Ghat, size_t n, int N, int P,
                                const cplx* __restrict__ tw, double* __restrict__ sq,
                                const int* __restrict__ kslot) {
   extern __shared__ cplx smem[];
@@ -355,7 +355,7 @@ __global__ void k_sfft_forward(const double* __restrict__ G, cplx* __restrict__ 
   if (sq) block_sum_to(e, sq + blockIdx.x);
 }
 
-__global__ void k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N, int P,
+__global__ void __launch_bounds__(512) k_sfft_inverse(const cplx* __restrict__ Uhat, double* __restrict__ U, size_t n, int N, int P,
                                const cplx* __restrict__ tw, double* __restrict__ part,
                                const int* __restrict__ kslot) {
   extern __shared__ cplx smem[];
@@ -509,7 +509,7 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
     int sP = fp_env > 0 ? fp_env : std::max(N >= 512 ? 4 : 1, 2048 / N);
     while (sP > 1 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) > (fp_env > 0 ? 200 : 100) * 1024) sP >>= 1;
     const int T = sP * N / 16;
-    if (T <= 1024 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) <= 200 * 1024) {
+    if (T <= 512 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) <= 200 * 1024) {  // __launch_bounds__(512)
       pl->stockham = true;
       pl->sP = sP;
       pl->sT = std::max(32, T);

@@ -577,7 +577,11 @@ double Problem::residual_and_rhs(bool want_rhs) {
         d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   }
   TP_LAUNCHED(this);
-  const double r = std::sqrt(global_sum(reduce_sum(*this, part.get(), (int)np)));
+  reduce_sum_dev(*this, part.get(), (int)np, red.get());
+  global_sum_dev(red.get(), 1, red.get() + 1);
+  TP_CUDA(cudaMemcpyAsync(h_scalars, red.get() + 1, sizeof(double), cudaMemcpyDeviceToHost, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  const double r = std::sqrt(h_scalars[0]);
   if (want_rhs) {  // the fixed-point residual history (warm-start extrapolation, problem.cu)
     resid_prev = resid_last;
     resid_last = r;

@@ -437,14 +437,21 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
       for (int X = 0; X <= c - 1; ++X) we[(size_t)Y * V + X] = 0.5 * (nh(X, Y) + nh(X, Y - 1));
     for (int Y = 0; Y <= c - 1; ++Y)
       for (int X = 1; X <= c - 1; ++X) wn[(size_t)Y * V + X] = 0.5 * (nh(X, Y) + nh(X - 1, Y));
-    d_we.alloc(we.size());
-    d_wn.alloc(wn.size());
-    TP_CUDA(cudaMemcpy(d_we.get(), we.data(), we.size() * sizeof(double), cudaMemcpyHostToDevice));
-    TP_CUDA(cudaMemcpy(d_wn.get(), wn.data(), wn.size() * sizeof(double), cudaMemcpyHostToDevice));
+    // one contiguous block [we | wn | mass]: every fine pass of every frequency
+    // re-reads these 24 bytes per node, so they are kept L2-resident through a
+    // persisting access-policy window (below) instead of competing with the
+    // streamed vectors (cfg 3: 100 MB of coefficients beside 67 MB per vector)
+    const size_t VV = (size_t)V * V;
+    d_coef.alloc(2 * VV + (size_t)n);
+    TP_CUDA(cudaMemcpy(d_coef.get(), we.data(), VV * sizeof(double), cudaMemcpyHostToDevice));
+    TP_CUDA(cudaMemcpy(d_coef.get() + VV, wn.data(), VV * sizeof(double), cudaMemcpyHostToDevice));
+    TP_CUDA(cudaMemcpy(d_coef.get() + 2 * VV, mass.data(), (size_t)n * sizeof(double), cudaMemcpyHostToDevice));
+    d_we.alias(d_coef.get(), VV);
+    d_wn.alias(d_coef.get() + VV, VV);
     FineOp& fo = ops[0].fine;
     fo.we = d_we.get();
     fo.wn = d_wn.get();
-    fo.mass = d_mass.get();
+    fo.mass = d_coef.get() + 2 * VV;
     fo.m = m;
     fo.c = c;
     fo.n = n;
@@ -487,7 +494,33 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
     TP_CUDA(cudaEventCreateWithFlags(&w->ev_in, cudaEventDisableTiming));
     for (auto& e : w->ev_out) TP_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
   }
+  if (d_coef.get() && !K0) {
+    std::vector<cudaStream_t> ss{stream};
+    for (auto h : w->hs) ss.push_back(h);
+    l2_persist(d_coef.get(), d_coef.bytes(), ss);
+  }
   TP_CUDA(cudaStreamSynchronize(stream));
+}
+
+// Persisting L2 window over [base, base + bytes) on the given streams
+// (TPGPU_L2_PERSIST=0 disables): the fine-level coefficients stay resident
+// while the vectors stream through as normal (missProp streaming).
+void Problem::l2_persist(const void* base, size_t bytes, const std::vector<cudaStream_t>& ss) {
+  static const bool on = !std::getenv("TPGPU_L2_PERSIST") || std::atoi(std::getenv("TPGPU_L2_PERSIST")) != 0;
+  if (!on || bytes == 0) return;
+  int max_persist = 0, max_window = 0;
+  TP_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
+  TP_CUDA(cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, device));
+  if (max_persist <= 0 || max_window <= 0) return;
+  const size_t limit = std::min<size_t>((size_t)max_persist, bytes);
+  TP_CUDA(cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, limit));
+  cudaStreamAttrValue a{};
+  a.accessPolicyWindow.base_ptr = const_cast<void*>(base);
+  a.accessPolicyWindow.num_bytes = std::min<size_t>(bytes, (size_t)max_window);
+  a.accessPolicyWindow.hitRatio = (float)std::min(1.0, (double)limit / (double)a.accessPolicyWindow.num_bytes);
+  a.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  a.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  for (auto h : ss) TP_CUDA(cudaStreamSetAttribute(h, cudaStreamAttributeAccessPolicyWindow, &a));
 }
 
 namespace {
@@ -590,13 +623,8 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
   spec_sq.ensure((size_t)nblk + 1);
   launch_rdft_forward(*this, in, Ghat.get(), use_floor ? spec_sq.get() : nullptr);
   if (use_floor) {
-    if (sharded()) {
-      const double tot = global_sum(reduce_sum(*this, spec_sq.get(), nblk));
-      TP_CUDA(cudaMemcpyAsync(spec_sq.get() + nblk, &tot, sizeof(double), cudaMemcpyHostToDevice, stream));
-      TP_CUDA(cudaStreamSynchronize(stream));
-    } else {
-      reduce_sum_dev(*this, spec_sq.get(), nblk, spec_sq.get() + nblk);
-    }
+    reduce_sum_dev(*this, spec_sq.get(), nblk, spec_sq.get() + nblk);
+    if (sharded()) global_sum_dev(spec_sq.get() + nblk, 1, spec_sq.get() + nblk);
   }
   if (sharded()) alltoall_to_freq();
   const int Kr = sh.k1 - sh.k0;
@@ -704,9 +732,12 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
   last_rel_own = sharded() ? global_max(rel_o) : rel_o;
   if (sharded()) alltoall_from_freq();
   double re2 = 0, im2 = 0;
-  launch_rdft_inverse(*this, Uhat.get(), out, &re2, &im2);
-  re2 = global_sum(re2);
-  im2 = global_sum(im2);
+  launch_rdft_inverse(*this, Uhat.get(), out, nullptr, nullptr);  // sums in red[0..1]
+  global_sum_dev(red.get(), 2, red.get() + 2);
+  TP_CUDA(cudaMemcpyAsync(h_scalars, red.get() + 2, 2 * sizeof(double), cudaMemcpyDeviceToHost, stream));
+  TP_CUDA(cudaStreamSynchronize(stream));
+  re2 = h_scalars[0];
+  im2 = h_scalars[1];
   // imaginary-residue guard, periodic.hpp:186-196
   const double re_norm = std::sqrt(re2), im_norm = std::sqrt(im2);
   if (im_norm > cfg.imag_tol * std::max(re_norm, 1e-300))

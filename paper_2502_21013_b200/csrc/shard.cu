@@ -292,6 +292,31 @@ void Problem::global_sum_ints(std::vector<int>& v) {
   }
 }
 
+// out[i] = sum over ranks q (in rank order) of all[q * count + i]
+__global__ void k_rank_sum(const double* __restrict__ all, int P, int count, double* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= count) return;
+  double s = 0;
+  for (int q = 0; q < P; ++q) s += all[(size_t)q * count + i];
+  out[i] = s;
+}
+
+// Device-resident rank-ordered sum of `count` doubles: gather every rank's
+// partials and sum them in rank order into d_out, without a host round trip
+// on the NCCL path (deterministic: the same order on every rank).
+void Problem::global_sum_dev(const double* d_in, int count, double* d_out) {
+  if (!sharded()) {
+    if (d_out != d_in) TP_CUDA(cudaMemcpyAsync(d_out, d_in, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+    return;
+  }
+  red_all.ensure((size_t)(sh.P + 1) * count);
+  double* src = red_all.get() + (size_t)sh.P * count;
+  TP_CUDA(cudaMemcpyAsync(src, d_in, count * sizeof(double), cudaMemcpyDeviceToDevice, stream));
+  comm_allgather(sh.comm, src, red_all.get(), count * sizeof(double), stream);
+  k_rank_sum<<<(count + 127) / 128, 128, 0, stream>>>(red_all.get(), sh.P, count, d_out);
+  TP_LAUNCHED(this);
+}
+
 void Problem::global_minmax(double* lo, double* hi, int count) {
   if (!sharded()) return;
   red_all.ensure((size_t)2 * count * (sh.P + 1));

@@ -144,13 +144,14 @@ template <class T>
 struct DevBuf {
   T* ptr = nullptr;
   size_t count = 0;
+  bool owned = true;  // false: a view into another buffer (alias)
   DevBuf() = default;
   explicit DevBuf(size_t n) { alloc(n); }
   DevBuf(const DevBuf&) = delete;
   DevBuf& operator=(const DevBuf&) = delete;
-  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count) { o.ptr = nullptr; o.count = 0; }
+  DevBuf(DevBuf&& o) noexcept : ptr(o.ptr), count(o.count), owned(o.owned) { o.ptr = nullptr; o.count = 0; }
   DevBuf& operator=(DevBuf&& o) noexcept {
-    if (this != &o) { release(); ptr = o.ptr; count = o.count; o.ptr = nullptr; o.count = 0; }
+    if (this != &o) { release(); ptr = o.ptr; count = o.count; owned = o.owned; o.ptr = nullptr; o.count = 0; }
     return *this;
   }
   ~DevBuf() { release(); }
@@ -158,12 +159,20 @@ struct DevBuf {
     release();
     if (n) TP_CUDA(cudaMalloc(reinterpret_cast<void**>(&ptr), n * sizeof(T)));
     count = n;
+    owned = true;
+  }
+  void alias(T* p, size_t n) {
+    release();
+    ptr = p;
+    count = n;
+    owned = false;
   }
   void ensure(size_t n) { if (count < n) alloc(n); }
   void release() {
-    if (ptr) cudaFree(ptr);
+    if (ptr && owned) cudaFree(ptr);
     ptr = nullptr;
     count = 0;
+    owned = true;
   }
   T* get() const { return ptr; }
   size_t bytes() const { return count * sizeof(T); }
@@ -324,7 +333,9 @@ class Problem {
   DevBuf<double> d_src_time;
   DevBuf<MaterialDev> d_mat;
   DevBuf<double> d_nu_hat;
-  DevBuf<double> d_we, d_wn;  // K_hat edge weights on the (c+1)^2 vertex grid (fine streaming kernels)
+  DevBuf<double> d_coef;      // [we | wn | mass] of the fine streaming kernels (one L2-persisting block)
+  DevBuf<double> d_we, d_wn;  // K_hat edge weights on the (c+1)^2 vertex grid (views into d_coef)
+  void l2_persist(const void* base, size_t bytes, const std::vector<cudaStream_t>& ss);
   // device state
   DevBuf<double> U;     // N*n current iterate (slice-major)
   DevBuf<double> G;     // N*n right-hand side of the next sweep
@@ -359,6 +370,7 @@ class Problem {
   DevBuf<double> spec_sq;  // forward-DFT |X|^2 partials, then [last] the total (frequency stopping floor)
   void exchange_halo();
   double global_sum(double local);
+  void global_sum_dev(const double* d_in, int count, double* d_out);  // no host round trip
   void global_minmax(double* lo, double* hi, int count);
   double global_max(double v) {
     double lo = v, hi = v;

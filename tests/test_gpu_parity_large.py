@@ -107,13 +107,13 @@ def test_cfg1_full_m1_matches_reference():
     h, hr = np.asarray(rep.residual_history), g["history"]
     assert h.shape == hr.shape
     # residual history: within 1e-10 of the first residual everywhere
-    # (measured ~3e-12: late entries sit 1e-8 below the first, where the
+    # (measured 6e-12: late entries sit 1e-8 below the first, where the
     # two solvers' 1e-12-accurate block solves and fp64 rounding of the
-    # residual set them apart by ~1e-14 absolute) and within 1e-6 relative
-    # wherever the residual is above 1e-6 of the first
+    # residual set them apart by ~1e-14 absolute) and within 1e-7 relative
+    # wherever the residual is above 1e-4 of the first
     assert np.max(np.abs(h - hr)) <= 1e-10 * hr[0], np.max(np.abs(h - hr)) / hr[0]
-    big = hr > 1e-6 * hr[0]
-    assert np.max(np.abs(h - hr)[big] / hr[big]) <= 1e-6
+    big = hr > 1e-4 * hr[0]
+    assert np.max(np.abs(h - hr)[big] / hr[big]) <= 1e-7
     _compare_iterates(dig, g)
     assert_checksum_close(checksum(U), g["U_checksum"], what="final U")
 
