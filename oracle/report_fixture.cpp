@@ -20,7 +20,9 @@
 #include <string>
 #include <vector>
 
+#include "tpfem/mesh.hpp"
 #include "tpfem/report.hpp"
+#include "tpfem/vtk.hpp"
 
 using namespace tpfem;
 
@@ -29,7 +31,21 @@ static double num(const std::string& s) {
   return std::strtod(s.c_str(), nullptr);  // (subnormals too, unlike std::stod)
 }
 
+// usage: report_fixture vtk <outdir>: mesh.vtk and u.vtk (vtk.hpp) of the
+// reference transformer mesh (12 x 10 cells, build_rectilinear_mesh) with the
+// field u[d] = sin(0.37 d) - 1e-3 d on the free dofs.
+static int vtk_fixture(const std::filesystem::path& out) {
+  std::filesystem::create_directories(out);
+  const Mesh m = build_rectilinear_mesh(transformer_regions(), 12, 10);
+  write_mesh_vtk(out / "mesh.vtk", m);
+  std::vector<double> u(static_cast<std::size_t>(m.n_dof()));
+  for (std::size_t d = 0; d < u.size(); ++d) u[d] = std::sin(0.37 * static_cast<double>(d)) - 1e-3 * static_cast<double>(d);
+  write_field_vtk(out / "u.vtk", m, u);
+  return 0;
+}
+
 int main(int argc, char** argv) {
+  if (argc == 3 && std::string(argv[1]) == "vtk") return vtk_fixture(argv[2]);
   if (argc != 3) {
     std::cerr << "usage: report_fixture <spec> <outdir>\n";
     return 1;

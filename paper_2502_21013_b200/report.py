@@ -15,6 +15,8 @@ the reference's own report.hpp, tests/golden/make_report_golden.py):
 from __future__ import annotations
 
 import math
+
+import numpy as np
 import os
 from typing import Iterable, Sequence
 
@@ -185,3 +187,54 @@ def symbol_abs(steps: int, tau: float) -> list:
 
 def ensure_dir(path: str) -> None:
     os.makedirs(path, exist_ok=True)
+
+
+# ---------------------------------------------------------------- VTK (vtk.hpp:12-55)
+def dof_of_vertices(V) -> np.ndarray:
+    """finalize_mesh's numbering (mesh.hpp:86-103): vertices off the bounding
+    box, in vertex order, are the free dofs; boundary vertices get -1."""
+    V = np.asarray(V, dtype=np.float64)
+    xmin, ymin = V.min(axis=0)
+    xmax, ymax = V.max(axis=0)
+    tol = 1e-12 * max(xmax - xmin, ymax - ymin)
+    on = ((np.abs(V[:, 0] - xmin) <= tol) | (np.abs(V[:, 0] - xmax) <= tol) |
+          (np.abs(V[:, 1] - ymin) <= tol) | (np.abs(V[:, 1] - ymax) <= tol))
+    dof = np.full(len(V), -1, dtype=np.int64)
+    dof[~on] = np.arange(int((~on).sum()))
+    return dof
+
+
+def _vtk_head(f, V, T, title):
+    # std::ostream with precision(17), default float format (%.17g); z = 0 written as an integer
+    f.write(f"# vtk DataFile Version 3.0\n{title}\nASCII\nDATASET UNSTRUCTURED_GRID\n")
+    f.write(f"POINTS {len(V)} double\n")
+    for x, y in V:
+        f.write(f"{format_double(x)} {format_double(y)} 0\n")
+    f.write(f"CELLS {len(T)} {4 * len(T)}\n")
+    for a, b, c in T:
+        f.write(f"3 {a} {b} {c}\n")
+    f.write(f"CELL_TYPES {len(T)}\n")
+    f.write("5\n" * len(T))
+
+
+def write_mesh_vtk(path: str, V, T, region) -> None:
+    """write_mesh_vtk (vtk.hpp:33-38): the mesh with region labels as cell data."""
+    with open(path, "w", newline="\n") as f:
+        _vtk_head(f, V, T, "mesh regions")
+        f.write(f"CELL_DATA {len(T)}\nSCALARS region int 1\nLOOKUP_TABLE default\n")
+        for r in region:
+            f.write(f"{int(r)}\n")
+
+
+def write_field_vtk(path: str, V, T, free_values, name: str = "u") -> None:
+    """write_field_vtk (vtk.hpp:42-55): a free-dof field on the vertices,
+    zero on the Dirichlet boundary."""
+    dof = dof_of_vertices(V)
+    free_values = np.asarray(free_values, dtype=np.float64)
+    if free_values.size != int((dof >= 0).sum()):
+        raise ValueError("vtk field: size mismatch")
+    with open(path, "w", newline="\n") as f:
+        _vtk_head(f, V, T, "vertex field")
+        f.write(f"POINT_DATA {len(V)}\nSCALARS {name} double 1\nLOOKUP_TABLE default\n")
+        for d in dof:
+            f.write(f"{format_double(free_values[d]) if d >= 0 else '0'}\n")

@@ -31,6 +31,7 @@ def main():
     with open(spec, "w") as f:
         f.write(SPEC)
     subprocess.check_call([BIN, spec, OUT])
+    subprocess.check_call([BIN, "vtk", OUT])  # mesh.vtk, u.vtk (vtk.hpp)
     print("wrote", sorted(os.listdir(OUT)))
 
 
