@@ -438,9 +438,8 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
     for (int Y = 0; Y <= c - 1; ++Y)
       for (int X = 1; X <= c - 1; ++X) wn[(size_t)Y * V + X] = 0.5 * (nh(X, Y) + nh(X - 1, Y));
     // one contiguous block [we | wn | mass]: every fine pass of every frequency
-    // re-reads these 24 bytes per node, so they are kept L2-resident through a
-    // persisting access-policy window (below) instead of competing with the
-    // streamed vectors (cfg 3: 100 MB of coefficients beside 67 MB per vector)
+    // re-reads these 24 bytes per node; a persisting access-policy window over
+    // it is available (l2_persist, off by default: measured slower)
     const size_t VV = (size_t)V * V;
     d_coef.alloc(2 * VV + (size_t)n);
     TP_CUDA(cudaMemcpy(d_coef.get(), we.data(), VV * sizeof(double), cudaMemcpyHostToDevice));
@@ -503,10 +502,13 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
 }
 
 // Persisting L2 window over [base, base + bytes) on the given streams
-// (TPGPU_L2_PERSIST=0 disables): the fine-level coefficients stay resident
+// (TPGPU_L2_PERSIST=1 enables): the fine-level coefficients stay resident
 // while the vectors stream through as normal (missProp streaming).
 void Problem::l2_persist(const void* base, size_t bytes, const std::vector<cudaStream_t>& ss) {
-  static const bool on = !std::getenv("TPGPU_L2_PERSIST") || std::atoi(std::getenv("TPGPU_L2_PERSIST")) != 0;
+  // off by default: measured at cfg 3 the window made every sweep slower
+  // (398-402 vs 346-349 ms, profiles/r2g_ab.txt) -- the persisting lines
+  // shrink the L2 the streamed vectors and the coarse levels reuse
+  static const bool on = std::getenv("TPGPU_L2_PERSIST") && std::atoi(std::getenv("TPGPU_L2_PERSIST")) != 0;
   if (!on || bytes == 0) return;
   int max_persist = 0, max_window = 0;
   TP_CUDA(cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, device));
