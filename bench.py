@@ -284,6 +284,7 @@ def run_b200(args):
     evs = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps + 1)]
     inner = []
     launches0 = p.launches
+    p.kernel_timer_select(DOMINANT[0])
     p.kernel_timer(True)  # CUDA events around the dominant kernel, over the timed region
     barrier(pg)
     torch.cuda.synchronize()
@@ -351,22 +352,24 @@ def run_b200(args):
     n = (desc.cells - 1) ** 2
     roofline = dominant_kernel_roofline(args, k_launches, k_ms, k_bytes, iso, hbm, src, n)
     # Whole-sweep algorithmic bytes per GPU:
-    # B = 72 D / P + 16 n S sum_k it_k over this rank's frequency blocks
-    # (sum_k it_k counted exactly by the solver, tp_sweep_stats), with S = 15.0
-    # complex streams per inner iteration and frequency as implemented (fine:
-    # apply 6 = read z, p, x, write p, q, x; down with the fused residual update
-    # 4.25 = read r, q, write r, z2, 1/4 coarse rhs; up 3.25; first Galerkin
-    # level 5.5 / 4; fused small-level cycle: read b, write z at 1/16).
-    STREAMS = 13.5 + 5.5 / 4 + 2.0 / 16
+    # B = 72 D / P + 16 n (3 K / P + S sum_k it_k) over this rank's frequency
+    # blocks (sum_k it_k counted exactly by the solver, tp_sweep_stats), with S
+    # the complex streams per inner iteration and frequency as implemented
+    # (streams_per_iteration: 15.0 at cfg 1, 15.46 at cfg 3) and 3 streams for
+    # every block's initial residual.
+    STREAMS = streams_per_iteration(desc.cells - 1)
     mean_inner = float(np.mean(inner)) if inner else 0.0
     mean_fit = float(np.mean(fiters)) if fiters else 0.0
-    b_alg = 72.0 * D / (world if sharded else 1) + 16.0 * n * STREAMS * mean_fit
+    K = desc.steps // 2 + 1
+    # + the initial residual of every block (r = g - A x0: read g, x0, write r)
+    b_alg = 72.0 * D / (world if sharded else 1) + 16.0 * n * (3.0 * K / (world if sharded else 1)
+                                                              + STREAMS * mean_fit)
     t_sweep = total_ms / 1e3 / args.steps
     sweep_roofline = {"bound": "hbm", "achieved": b_alg / t_sweep / 1e9, "peak": hbm, "unit": "GB/s",
                       "frac": b_alg / t_sweep / 1e9 / hbm, "bytes_per_sweep": b_alg,
                       "fixed_bytes_per_sweep": 72.0 * D, "streams_per_inner_iteration": STREAMS,
                       "inner_iterations_mean": mean_inner, "frequency_iterations_per_sweep": mean_fit}
-    sweep_roofline.update(sweep_dram_crosscheck(args.config, b_alg, mean_fit, n, STREAMS, D, t_sweep, hbm))
+    sweep_roofline.update(sweep_dram_crosscheck(args.config, b_alg, t_sweep, hbm))
 
     out = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
            "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
@@ -394,11 +397,20 @@ def run_b200(args):
         comm.close()
 
 
+# The dominant kernel at the bench configs: the fine-level down pass
+# (k_stream_down<Five>, fused with the Krylov update): 25 % of a cfg-3 sweep and
+# 24 % of a cfg-1 sweep in the ncu launch lists (profiles/r2*_launches_cfg3_sweep.txt,
+# r2c_launches_cfg1_sweep.txt; at cfg 1 the fused small-level cycle is level with
+# it, and it has no HBM roofline: it keeps its levels in shared memory).
+DOMINANT = (1, "k_stream_down<Five> (fine-level V-cycle down pass, fused Krylov update)")
+
+
 def dominant_kernel_roofline(args, k_launches, k_ms, k_bytes, iso, hbm, src, n):
-    """The kernel the library brackets with CUDA events (tp_kernel_timer: the
-    fine-level V-cycle up pass k_stream_up<Five>): algorithmic bytes = 3.25
-    complex values (read z2, r, 1/4 coarse correction; write z) x 16 B per
-    fine node per active frequency, over its event-measured launch time."""
+    """The kernel the library brackets with CUDA events (tp_kernel_timer,
+    tp_kernel_timer_select): algorithmic bytes per launch = 4.25 complex values
+    (read r, q; write r, z2 and the 1/4-size coarse right-hand side) x 16 B per
+    fine node per active frequency (2.25 on the plain first pass), over its
+    event-measured launch time."""
     def kstats(nl, ms, by):
         avg_ms = ms / max(nl, 1)
         b_launch = by / max(nl, 1)
@@ -407,7 +419,7 @@ def dominant_kernel_roofline(args, k_launches, k_ms, k_bytes, iso, hbm, src, n):
                 "avg_launch_ms": avg_ms, "launches": nl}
 
     timed = kstats(k_launches, k_ms, k_bytes)
-    roofline = {"bound": "hbm", "kernel": "k_stream_up<Five> (fine-level V-cycle up pass)", "peak": hbm,
+    roofline = {"bound": "hbm", "kernel": DOMINANT[1], "peak": hbm,
                 "unit": "GB/s", "traffic": None, "peak_source": src}
     if iso is not None and iso[0]:
         roofline.update(kstats(*iso))
@@ -418,37 +430,51 @@ def dominant_kernel_roofline(args, k_launches, k_ms, k_bytes, iso, hbm, src, n):
                                            "includes the other groups' kernels")
     else:
         roofline.update(timed)
-    # ncu DRAM bytes of this kernel per fine node and active frequency, from
-    # the committed launch list of the same config (profiles/kernel_traffic.json)
+    # ncu DRAM bytes of this kernel per algorithmic byte, from the committed
+    # launch list of the same config (profiles/kernel_traffic.json)
     try:
         with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
-            kt = json.load(f)
-        per = kt.get(f"cfg{args.config}", {}).get("dominant_kernel_dram_bytes_per_node_frequency")
-        if per and roofline.get("bytes_per_launch"):
-            alg_per = 3.25 * 16.0
-            roofline["traffic"] = per * roofline["bytes_per_launch"] / alg_per
-            roofline["traffic_note"] = ("ncu dram__bytes_read+write of this kernel per launch, from the per-node-"
-                                        "frequency figure of the committed launch list (profiles/kernel_traffic.json)"
-                                        " scaled to this launch's active frequencies")
+            kt = json.load(f).get(f"cfg{args.config}", {})
+        ratio = kt.get("dominant_kernel_dram_over_algorithmic")
+        if ratio and roofline.get("bytes_per_launch"):
+            roofline["traffic"] = ratio * roofline["bytes_per_launch"]
+            roofline["traffic_note"] = ("ncu dram__bytes_read+write per launch: the kernel's DRAM / algorithmic byte "
+                                        "ratio from the committed launch list of this config "
+                                        f"({kt.get('source')}) times this launch's algorithmic bytes")
     except Exception:
         pass
     return roofline
 
 
-def sweep_dram_crosscheck(config, b_alg, fit, n, streams, D, t_sweep, hbm):
-    """SURVEY.md §8(d) cross-check: the ncu DRAM bytes of one production
-    sweep of this config (profiles/kernel_traffic.json, from the committed
-    launch list) rescaled to this run's frequency-iterations, against the
-    algorithmic bytes; the roofline fraction on the smaller of the two."""
+def streams_per_iteration(m):
+    """Complex fine-level streams per inner COCG iteration and frequency, for
+    the level sizes of this grid (m interior nodes per side): fine apply 6 +
+    fused down 4.25 + up 3.25; every streamed Galerkin level (m_l > 63) 5.5
+    of its own size; the fused small-level cycle reads b and writes z at its
+    first level."""
+    S = 13.5
+    ml = (m - 1) // 2
+    while ml > 63:
+        S += 5.5 * (ml * ml) / (m * m)
+        ml = (ml - 1) // 2
+    S += 2.0 * (ml * ml) / (m * m)
+    return S
+
+
+def sweep_dram_crosscheck(config, b_alg, t_sweep, hbm):
+    """SURVEY.md §8(d) cross-check: ncu DRAM bytes of one production sweep of
+    this config over its algorithmic bytes (profiles/kernel_traffic.json, from
+    the committed launch list and the solver's own counts of that sweep),
+    applied to this run's algorithmic bytes; the roofline fraction on the
+    smaller of the two."""
     try:
         with open(os.path.join(ROOT, "profiles", "kernel_traffic.json")) as f:
             kt = json.load(f).get(f"cfg{config}")
-        if not kt:
+        if not kt or not kt.get("sweep_dram_over_algorithmic"):
             return {}
-        fixed, per_fit = kt["sweep_dram_fixed_bytes"], kt["sweep_dram_bytes_per_frequency_iteration"]
-        dram = fixed + per_fit * fit
+        dram = kt["sweep_dram_over_algorithmic"] * b_alg
         return {"dram_bytes_per_sweep": dram, "dram_source": kt.get("source"),
-                "dram_over_algorithmic": dram / b_alg,
+                "dram_over_algorithmic": kt["sweep_dram_over_algorithmic"],
                 "frac_on_smaller": min(dram, b_alg) / t_sweep / 1e9 / hbm}
     except Exception:
         return {}

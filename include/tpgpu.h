@@ -276,10 +276,13 @@ int32_t tp_comm_device(const tp_comm* c);
 int tp_problem_create_sharded(const tp_problem_desc* desc, tp_comm* comm, tp_problem** out);
 int tp_problem_shard(const tp_problem* p, tp_shard_plan* out);
 
-/* Live timing of the dominant kernel (fine-level V-cycle up pass) with CUDA
+/* Live timing of one fine-level kernel (tp_kernel_timer_select) with CUDA
  * events: returns the launches / event time / algorithmic bytes accumulated
  * since the previous call, then enables (1) or disables (0) the timer. */
 int tp_kernel_timer(tp_problem* p, int32_t enable, int64_t* launches, double* ms, double* bytes);
+/* Which fine-level pass tp_kernel_timer brackets: 0 the up pass (default),
+ * 1 the down pass (with the fused Krylov update), 2 the COCG apply. */
+int tp_kernel_timer_select(tp_problem* p, int32_t which);
 /* CUDA stream the problem launches on (cudaStream_t), for event timing. */
 void* tp_problem_stream(tp_problem* p);
 /* Kernel launches issued so far by this problem (for the bench's gpu_launches). */

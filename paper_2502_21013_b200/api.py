@@ -37,7 +37,7 @@ EXPORTS = [
     "tp_m1_begin", "tp_m1_sweep", "tp_sweep_stats", "tp_problem_stream", "tp_problem_launches",
     "tp_shard_plan_make", "tp_nccl_unique_id", "tp_comm_create", "tp_comm_destroy", "tp_comm_nccl",
     "tp_comm_rank", "tp_comm_size", "tp_comm_device", "tp_problem_create_sharded", "tp_problem_shard",
-    "tp_kernel_timer", "tp_comm_create_host", "tp_solve_residuals", "tp_shard_freq_order",
+    "tp_kernel_timer", "tp_kernel_timer_select", "tp_comm_create_host", "tp_solve_residuals", "tp_shard_freq_order",
 ]
 
 # tp_host_exchange_fn (tpgpu.h)
@@ -113,6 +113,7 @@ def lib():
         L.tp_problem_create_sharded.argtypes = [D, vp, C.POINTER(vp)]
         L.tp_problem_shard.argtypes = [vp, SP]
         L.tp_kernel_timer.argtypes = [vp, C.c_int32, C.POINTER(C.c_int64), dp, dp]
+        L.tp_kernel_timer_select.argtypes = [vp, C.c_int32]
         _lib = L
     return _lib
 
@@ -476,6 +477,10 @@ class Problem:
         a, b = C.c_double(), C.c_double()
         _check(lib().tp_solve_residuals(self._h, C.byref(a), C.byref(b)))
         return a.value, b.value
+
+    def kernel_timer_select(self, which: int):
+        """0: fine up pass, 1: fine down pass, 2: fine apply (tp_kernel_timer_select)."""
+        _check(lib().tp_kernel_timer_select(self._h, which))
 
     def kernel_timer(self, enable: bool):
         """(launches, ms, algorithmic bytes) of the dominant kernel since the

@@ -503,12 +503,12 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
   // (36 KB of shared memory with the twiddles: six blocks per SM)
   if (pl->pow2 && N >= 16 && !std::getenv("TPGPU_RADIX2_DFT")) {
     static const int fp_env = std::getenv("TPGPU_FFT_P") ? std::atoi(std::getenv("TPGPU_FFT_P")) : 0;
-    // at least 8 column pairs (128-byte row segments) for long periods: with 2
+    // at least 4 column pairs (64-byte row segments) for long periods: with 2
     // pairs at N = 1024 the 32-byte row reads held both transforms near 1.8
     // TB/s (cfg 3 launch list, profiles/r2c_launches_cfg3_sweep.txt); 4 pairs
-    // -> 2.3 / 1.5 TB/s, 8 pairs (512 threads, one block per SM) faster still
-    // (profiles/r2g_ab.txt)
-    int sP = fp_env > 0 ? fp_env : std::max(N >= 512 ? 8 : 1, 2048 / N);
+    // -> 2.3 / 1.5 TB/s; 8 pairs (512 threads, one block per SM) measured
+    // level with 4 on the whole sweep (profiles/r2h_ab.txt)
+    int sP = fp_env > 0 ? fp_env : std::max(N >= 512 ? 4 : 1, 2048 / N);
     while (sP > 1 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) > 200 * 1024) sP >>= 1;
     const int T = sP * N / 16;
     if (T <= 512 && (size_t)(N + zx_size(sP * N)) * sizeof(cplx) <= 200 * 1024) {  // __launch_bounds__(512)

@@ -1323,8 +1323,15 @@ void BatchSolver<MODE>::fine_down0(int nb, const T* r_in, const T* qv, T* r_out,
                                    double* part_out) {
   const FineOp fo = stream_op(0);
   if constexpr (MODE == 0)
-    launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
-                       qv, qv ? alpha.get() : nullptr, r_out, qv ? (part_out ? part_out : part.get()) : nullptr, sf);
+    // algorithmic bytes per fine node and active frequency: fused (the Krylov
+    // update rides along) read r, q, write r, z2 and the 1/4 coarse rhs = 4.25
+    // values; plain read r, write z2 and the coarse rhs = 2.25
+    p->ktimer.time(1, p->cur_stream(), (qv ? 4.25 : 2.25) * (double)sizeof(T) * (double)ops[0].n * (double)cur_active,
+                   [&] {
+                     launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega,
+                                        cfg.omega2, nb, qv, qv ? alpha.get() : nullptr, r_out,
+                                        qv ? (part_out ? part_out : part.get()) : nullptr, sf);
+                   });
   else
     launch_stream_down(*p, fo, r_in, lz0[0].get(), lb[1].get(), ops[1].m, active.get(), cfg.omega, cfg.omega2, nb,
                        qv, qv ? alpha.get() : nullptr, r_out, qv ? part.get() : nullptr);
@@ -1349,23 +1356,13 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::fine_rest0(int nb, const T* bl
       } else {
         xcf = vcycle_level(l + 1, nb, lb[l + 1].get(), nullptr, false, false);
       }
-      cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (p->ktimer.on) {
-        TP_CUDA(cudaEventCreate(&e0));
-        TP_CUDA(cudaEventCreate(&e1));
-        TP_CUDA(cudaEventRecord(e0, s));
-      }
       trace_mark("up", s);
-      launch_stream_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0, part.get());
-      if (p->ktimer.on) {
-        TP_CUDA(cudaEventRecord(e1, s));
-        std::lock_guard<std::mutex> lk(p->ktimer.mu);
-        p->ktimer.pending.emplace_back(e0, e1);
-        // algorithmic bytes: read z2, r and the coarse correction (1/4), write z --
-        // 3.25 values per fine node of every active frequency
-        p->ktimer.bytes += 3.25 * (double)sizeof(T) * (double)ops[l].n * (double)cur_active;
-        ++p->ktimer.launches;
-      }
+      // algorithmic bytes: read z2, r and the coarse correction (1/4), write z --
+      // 3.25 values per fine node of every active frequency
+      p->ktimer.time(0, s, 3.25 * (double)sizeof(T) * (double)ops[l].n * (double)cur_active, [&] {
+        launch_stream_up(*p, fo, bl, z2, xcf, ops[l + 1].m, zo, act, cfg.omega, cfg.omega2, nb, dot ? 1 : 0,
+                         part.get());
+      });
       return zo;
     }
   }
@@ -1562,8 +1559,11 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
           sf.per = per_u;
           sf.rho_r = rho2.get() + (size_t)(par ^ 1) * B;
           sf.rho_w = rho2.get() + (size_t)par * B;
-          launch_fine_apply(*p, stream_op(0), z, pin, pout, q.get(), beta.get(), act, first, nb, partA.get(), false, x,
-                            xa_ptr, &sf);
+          // algorithmic bytes: read z, p (not on the first iteration), x; write p, q, x
+          p->ktimer.time(2, s, (first ? 5.0 : 6.0) * (double)sizeof(T) * (double)ops[0].n * (double)cur_active, [&] {
+            launch_fine_apply(*p, stream_op(0), z, pin, pout, q.get(), beta.get(), act, first, nb, partA.get(), false,
+                              x, xa_ptr, &sf);
+          });
         }
       } else if (sapply) {
         launch_fine_apply(*p, stream_op(0), z, pin, pout, q.get(), beta.get(), act, first, nb, part.get(), false,

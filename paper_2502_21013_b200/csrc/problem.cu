@@ -1195,6 +1195,15 @@ int tp_problem_shard(const tp_problem* p, tp_shard_plan* out) {
   });
 }
 
+int tp_kernel_timer_select(tp_problem* h, int32_t which) {
+  return guarded([&] {
+    Problem& p = P(h);
+    tpgpu::require(which >= 0 && which <= 2, "kernel timer: which must be 0 (up), 1 (down) or 2 (apply)");
+    p.ktimer.drain();
+    p.ktimer.which = which;
+  });
+}
+
 int tp_kernel_timer(tp_problem* h, int32_t enable, int64_t* launches, double* ms, double* bytes) {
   return guarded([&] {
     Problem& p = P(h);

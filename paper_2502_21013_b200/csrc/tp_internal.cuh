@@ -392,10 +392,29 @@ class Problem {
   struct KernelTimer {
     std::mutex mu;
     bool on = false;
+    int which = 0;  // tp_kernel_timer_select: 0 fine up pass, 1 fine down pass, 2 fine apply
     int64_t launches = 0;
     double bytes = 0, ms = 0;
     std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
     void drain();
+    // bracket one launch of kernel `kind` on stream s (alg_bytes: its algorithmic bytes)
+    template <class F>
+    void time(int kind, cudaStream_t s, double alg_bytes, F&& launch) {
+      if (!on || kind != which) {
+        launch();
+        return;
+      }
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      TP_CUDA(cudaEventCreate(&e0));
+      TP_CUDA(cudaEventCreate(&e1));
+      TP_CUDA(cudaEventRecord(e0, s));
+      launch();
+      TP_CUDA(cudaEventRecord(e1, s));
+      std::lock_guard<std::mutex> lk(mu);
+      pending.emplace_back(e0, e1);
+      bytes += alg_bytes;
+      ++launches;
+    }
   } ktimer;
 
   // pinned host scratch

@@ -182,6 +182,8 @@ def test_sweeps_from_zero_match_reference(config, name):
     assert rep.iterations == count
     h, hr = np.asarray(rep.residual_history), g["history"]
     assert h.shape == hr.shape
-    assert abs(h[0] - hr[0]) <= 1e-12 * hr[0]
+    # ||R(0)|| = ||F|| summed over 5e8 entries in two different orders:
+    # measured 1.2e-12 apart at cfg 5
+    assert abs(h[0] - hr[0]) <= 1e-11 * hr[0]
     assert np.max(np.abs(h - hr) / hr) <= 1e-6, (h, hr)
     _compare_iterates(dig, g)
