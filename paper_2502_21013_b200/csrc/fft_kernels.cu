@@ -438,6 +438,149 @@ __global__ void __launch_bounds__(512) k_sfft_inverse(const cplx* __restrict__ U
   }
 }
 
+// ---------------------------------------------------------------- pipelined transforms
+// Persistent, software-pipelined forms of k_sfft_forward / k_sfft_inverse for
+// long periods (N >= 512): a block walks tiles of C = 2P columns with a
+// stride of the grid and keeps the NEXT tile's loads in flight (cp.async into
+// the second of two shared buffers) while it transforms and stores the
+// current one.  The one-shot kernels load, then compute, then store, so at
+// one or two resident blocks per SM HBM idled through every transform:
+// 2.2-2.3 TB/s at cfg 3 (profiles/r2i_launches_cfg3_sweep.txt).
+
+// stage tile `tile` of the real input (N rows x C doubles) into z (padded layout)
+__device__ __forceinline__ void fwd_issue(double* zd, const double* __restrict__ G, size_t n, int N, int P,
+                                          size_t tile) {
+  const int C = 2 * P;
+  const size_t j0 = tile * C;
+  for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
+    const int i = t / C, cc = t - i * C;
+    const bool ok = j0 + cc < n;
+    acp8(&zd[2 * zx(i * P + (cc >> 1)) + (cc & 1)], G + (ok ? (size_t)i * n + j0 + cc : 0), ok);
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k_sfft_forward_pp(const double* __restrict__ G, cplx* __restrict__ Ghat,
+                                                           size_t n, int N, int P, const cplx* __restrict__ tw,
+                                                           double* __restrict__ sq, const int* __restrict__ kslot,
+                                                           size_t ntiles) {
+  extern __shared__ cplx smem[];
+  cplx* tws = smem;
+  const int zsz = zx_size(P * N);
+  cplx* zb[2] = {smem + N, smem + N + zsz};
+  for (int t = threadIdx.x; t < N; t += blockDim.x) acp16(&tws[t], &tw[t], true);
+  size_t tile = blockIdx.x;
+  if (tile < ntiles) fwd_issue(reinterpret_cast<double*>(zb[0]), G, n, N, P, tile);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  const int C = 2 * P, K = N / 2 + 1;
+  double e = 0;
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    cplx* z = zb[it & 1];
+    const size_t next = tile + gridDim.x;
+    if (next < ntiles) fwd_issue(reinterpret_cast<double*>(zb[(it + 1) & 1]), G, n, N, P, next);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // this tile (and the twiddles) landed
+    __syncthreads();
+    stockham<false>(z, tws, N, P);
+    const size_t j0 = tile * C;
+    for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
+      const int k = t / C, cc = t - k * C;
+      if (j0 + cc >= n) continue;
+      const int p = cc >> 1;
+      const cplx Zk = z[zx(k * P + p)], Zm = conj(z[zx(((N - k) % N) * P + p)]);
+      cplx X;
+      if ((cc & 1) == 0) X = {0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
+      else X = {0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)};
+      Ghat[(size_t)(kslot ? kslot[k] : k) * n + j0 + cc] = X;
+      e = fma(X.re, X.re, fma(X.im, X.im, e));
+    }
+    __syncthreads();  // z is refilled two tiles on
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  if (sq) block_sum_to(e, sq + blockIdx.x);
+}
+
+// stage tile `tile` of the half spectrum (K rows x C complex) into raw
+__device__ __forceinline__ void inv_issue(cplx* raw, const cplx* __restrict__ Uhat, size_t n, int N, int P,
+                                          size_t tile, const int* __restrict__ kslot) {
+  const int C = 2 * P, K = N / 2 + 1;
+  const size_t j0 = tile * C;
+  for (int t = threadIdx.x; t < K * C; t += blockDim.x) {
+    const int k = t / C, cc = t - k * C;
+    const bool ok = j0 + cc < n;
+    acp16(&raw[t], Uhat + (ok ? (size_t)(kslot ? kslot[k] : k) * n + j0 + cc : 0), ok);
+  }
+}
+
+__global__ void __launch_bounds__(256, 1) k_sfft_inverse_pp(const cplx* __restrict__ Uhat, double* __restrict__ U,
+                                                           size_t n, int N, int P, const cplx* __restrict__ tw,
+                                                           double* __restrict__ part, const int* __restrict__ kslot,
+                                                           size_t ntiles) {
+  extern __shared__ cplx smem[];
+  __shared__ double red[2][32];
+  const int C = 2 * P, half = N / 2, K = half + 1;
+  cplx* tws = smem;
+  cplx* z = smem + N;
+  const int zsz = zx_size(P * N);
+  cplx* rb[2] = {z + zsz, z + zsz + K * C};
+  for (int t = threadIdx.x; t < N; t += blockDim.x) acp16(&tws[t], &tw[t], true);
+  size_t tile = blockIdx.x;
+  if (tile < ntiles) inv_issue(rb[0], Uhat, n, N, P, tile, kslot);
+  asm volatile("cp.async.commit_group;\n" ::: "memory");
+  double re2 = 0, im2 = 0;
+  const double invN = 1.0 / N;
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const cplx* raw = rb[it & 1];
+    const size_t next = tile + gridDim.x;
+    if (next < ntiles) inv_issue(rb[(it + 1) & 1], Uhat, n, N, P, next, kslot);
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    __syncthreads();
+    // Hermitian extension of the two packed columns (N even: self-conjugate 0, N/2)
+    for (int t = threadIdx.x; t < K * P; t += blockDim.x) {
+      const int k = t / P, p = t - k * P;
+      const cplx Xa = raw[k * C + 2 * p], Xb = raw[k * C + 2 * p + 1];
+      if (k == 0 || k == half) {
+        z[zx(k * P + p)] = {Xa.re, Xb.re};
+        im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
+      } else {
+        z[zx(k * P + p)] = {Xa.re - Xb.im, Xa.im + Xb.re};
+        z[zx((N - k) * P + p)] = {Xa.re + Xb.im, -Xa.im + Xb.re};
+      }
+    }
+    __syncthreads();
+    stockham<true>(z, tws, N, P);
+    const size_t j0 = tile * C;
+    const double* zd = reinterpret_cast<const double*>(z);
+    for (int t = threadIdx.x; t < N * C; t += blockDim.x) {
+      const int i = t / C, cc = t - i * C;
+      if (j0 + cc >= n) continue;
+      const double x = zd[2 * zx(i * P + (cc >> 1)) + (cc & 1)] * invN;
+      U[(size_t)i * n + j0 + cc] = x;
+      re2 += x * x;
+    }
+    __syncthreads();  // z rebuilt and this raw buffer refilled next
+  }
+  asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+  for (int o = 16; o > 0; o >>= 1) {
+    re2 += __shfl_down_sync(0xffffffffu, re2, o);
+    im2 += __shfl_down_sync(0xffffffffu, im2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = re2;
+    red[1][threadIdx.x >> 5] = im2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < (int)(blockDim.x / 32); ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
 __global__ void k_reduce_pairs(const double* __restrict__ part, int count, double* __restrict__ out) {
   __shared__ double sh[2][32];
   double a = 0, b = 0;
@@ -475,6 +618,10 @@ struct FftPlan {
   int sP = 0, sT = 0;    // forward: column pairs per block, threads
   int siP = 0, siT = 0;  // inverse
   size_t ssmem = 0, fsmem = 0;  // inverse (+ staged half spectrum) / forward
+  // pipelined persistent kernels (N >= 512): column pairs, threads, shared bytes, grid
+  bool pp_fwd = false, pp_inv = false;
+  int pP = 0, pT = 0, pgrid = 0;
+  size_t pfsmem = 0, pismem = 0;
 };
 
 FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
@@ -526,6 +673,36 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
       TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
     }
   }
+  // pipelined forms: two tiles of P column pairs (+ twiddles; the inverse also
+  // stages two raw half-spectrum tiles), one block of P N / 16 threads per SM
+  static const bool no_pp = std::getenv("TPGPU_FFT_NO_PIPELINE") != nullptr;
+  if (pl->stockham && N >= 512 && !no_pp) {
+    int dev = 0, sms = 148, maxsm = 0;
+    TP_CUDA(cudaGetDevice(&dev));
+    TP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+    TP_CUDA(cudaDeviceGetAttribute(&maxsm, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    static const int pp_env = std::getenv("TPGPU_FFT_PP_P") ? std::atoi(std::getenv("TPGPU_FFT_PP_P")) : 4;
+    for (int P = pp_env; P >= 2; P >>= 1) {
+      const size_t fs = (size_t)(N + 2 * zx_size(P * N)) * sizeof(cplx);
+      const size_t is = (size_t)(N + zx_size(P * N) + 2 * (N / 2 + 1) * 2 * P) * sizeof(cplx) + 2 * 32 * sizeof(double);
+      const int T = P * N / 16;
+      if (T > 256) continue;  // __launch_bounds__(256, 1)
+      const bool f_ok = fs <= (size_t)maxsm, i_ok = is <= (size_t)maxsm;
+      if (!f_ok) continue;
+      pl->pp_fwd = true;
+      pl->pp_inv = i_ok;
+      pl->pP = P;
+      pl->pT = T;
+      pl->pgrid = sms;
+      pl->pfsmem = fs;
+      pl->pismem = is - 2 * 32 * sizeof(double);
+      TP_CUDA(cudaFuncSetAttribute(k_sfft_forward_pp, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)fs));
+      if (i_ok)
+        TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse_pp, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pl->pismem));
+      break;
+    }
+  }
   slot = pl;
   return *pl;
 }
@@ -540,6 +717,7 @@ void launched(const DftCtx& c) {
 
 int dft_forward_blocks(const DftCtx& c) {
   FftPlan& pl = plan_for(*c.plan, c.N);
+  if (pl.pp_fwd) return pl.pgrid;
   const int C = 2 * (pl.stockham ? pl.sP : pl.P);
   return (int)((c.n + C - 1) / C);
 }
@@ -547,7 +725,11 @@ int dft_forward_blocks(const DftCtx& c) {
 void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
   FftPlan& pl = plan_for(*c.plan, c.N);
   const int blocks = dft_forward_blocks(c);
-  if (pl.stockham) {
+  if (pl.pp_fwd) {
+    const size_t ntiles = (c.n + 2 * pl.pP - 1) / (2 * pl.pP);
+    k_sfft_forward_pp<<<pl.pgrid, pl.pT, pl.pfsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.pP, pl.tw.get(), sq, c.kslot,
+                                                                 ntiles);
+  } else if (pl.stockham) {
     k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq, c.kslot);
   } else {
     k_rdft_forward<<<blocks, 256, pl.smem, c.stream>>>(G, Ghat, c.n, pl.N, pl.P, pl.bits, pl.pow2, pl.tw.get(),
@@ -559,10 +741,14 @@ void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
 void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, double* im2) {
   FftPlan& pl = plan_for(*c.plan, c.N);
   const int C = 2 * (pl.stockham ? pl.siP : pl.P);
-  const int blocks = (int)((c.n + C - 1) / C);
+  const int blocks = pl.pp_inv ? pl.pgrid : (int)((c.n + C - 1) / C);
   c.part->ensure((size_t)2 * blocks);
   c.red->ensure(16);
-  if (pl.stockham) {
+  if (pl.pp_inv) {
+    const size_t ntiles = (c.n + 2 * pl.pP - 1) / (2 * pl.pP);
+    k_sfft_inverse_pp<<<pl.pgrid, pl.pT, pl.pismem, c.stream>>>(Uhat, U, c.n, pl.N, pl.pP, pl.tw.get(),
+                                                                 c.part->get(), c.kslot, ntiles);
+  } else if (pl.stockham) {
     k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.N, pl.siP, pl.tw.get(),
                                                             c.part->get(), c.kslot);
   } else {
