@@ -675,8 +675,11 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
   }
   // pipelined forms: two tiles of P column pairs (+ twiddles; the inverse also
   // stages two raw half-spectrum tiles), one block of P N / 16 threads per SM
-  static const bool no_pp = std::getenv("TPGPU_FFT_NO_PIPELINE") != nullptr;
-  if (pl->stockham && N >= 512 && !no_pp) {
+  // opt-in (TPGPU_FFT_PIPELINE=1): measured slower than the one-shot kernels
+  // at cfg 3 (378.6 vs 351.2 ms per sweep, profiles/r2j_ab.txt; the inverse
+  // moved 108 GB of DRAM for its 68.8 GB of data)
+  static const bool want_pp = std::getenv("TPGPU_FFT_PIPELINE") && std::atoi(std::getenv("TPGPU_FFT_PIPELINE")) != 0;
+  if (pl->stockham && N >= 512 && want_pp) {
     int dev = 0, sms = 148, maxsm = 0;
     TP_CUDA(cudaGetDevice(&dev));
     TP_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));

@@ -235,7 +235,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
     const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc) {
   __shared__ double su[SD][TY + 2][TX + 2];
   __shared__ double cnu0[TY + 1][TX + 1], cdnu[TY + 1][TX + 1], cbs2[TY + 1][TX + 1], chat[TY + 1][TX + 1];
-  __shared__ double wnu[2][TY + 1][TX + 1];  // nu_T / 2 of the current slice (T1, T2 per cell)
+  __shared__ double wnu[2][2][TY + 1][TX + 1];  // nu_T / 2 (T1, T2 per cell) of two slices
   __shared__ double red[32];
   const size_t n = (size_t)m * m;
   const size_t nl = (size_t)rows * m;
@@ -332,15 +332,15 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
 #pragma unroll
   for (int t6 = 0; t6 < 6; ++t6) hat[t6] = WANT_G ? chat[ty + 1 + cys[t6]][tx + 1 + cxs[t6]] : 0.0;
   double r2 = 0;
-  for (int s = sbeg; s < send; ++s) {
-    asm volatile("cp.async.wait_group %0;\n" ::"n"(SD - 2) : "memory");
-    __syncthreads();  // slice s staged by every thread; slice s-1's slot and weights free
-    issue(s + SD - 1);
-    const double(*t)[TX + 2] = su[s % SD];
-    // nu(|grad u|) / 2 once per triangle: the (TY+1) x (TX+1) cells under the
-    // node tile, two triangles each (T1 lower-right: d = (u10-u00, u11-u10);
-    // T2 upper-left: d = (u11-u01, u01-u00)) -- each triangle is shared by
-    // three nodes, which used to evaluate its law three times
+  // nu(|grad u|) / 2 once per triangle: the (TY+1) x (TX+1) cells under the
+  // node tile, two triangles each (T1 lower-right: d = (u10-u00, u11-u10);
+  // T2 upper-left: d = (u11-u01, u01-u00)) -- each triangle is shared by
+  // three nodes, which used to evaluate its law three times.  Software
+  // pipelined: iteration s evaluates the cells of slice s+1 and gathers the
+  // nodes of slice s, one barrier per slice (wnu double-buffered)
+  auto cell_pass = [&](int sl) {
+    const double(*t)[TX + 2] = su[sl % SD];
+    double(*w)[TY + 1][TX + 1] = wnu[sl & 1];
 #pragma unroll
     for (int e = 0; e < 2; ++e) {
       const int k = e == 0 ? kc0 : kc1;
@@ -349,12 +349,22 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
         const double u00 = t[cy][cx], u10 = t[cy][cx + 1], u01 = t[cy + 1][cx], u11 = t[cy + 1][cx + 1];
         const double ax = u10 - u00, ay = u11 - u10, bx = u11 - u01, by = u01 - u00;
         const double sa = c2 * (ax * ax + ay * ay), sb2 = c2 * (bx * bx + by * by);
-        wnu[0][cy][cx] = 0.5 * fma(cl[e][0], sa * acc_rcp(sa + cl[e][1]), cl[e][2]);
-        wnu[1][cy][cx] = 0.5 * fma(cl[e][0], sb2 * acc_rcp(sb2 + cl[e][1]), cl[e][2]);
+        w[0][cy][cx] = 0.5 * fma(cl[e][0], sa * acc_rcp(sa + cl[e][1]), cl[e][2]);
+        w[1][cy][cx] = 0.5 * fma(cl[e][0], sb2 * acc_rcp(sb2 + cl[e][1]), cl[e][2]);
       }
     }
-    __syncthreads();
+  };
+  asm volatile("cp.async.wait_group %0;\n" ::"n"(SD - 2) : "memory");
+  __syncthreads();  // slice sbeg staged
+  cell_pass(sbeg);
+  for (int s = sbeg; s < send; ++s) {
+    asm volatile("cp.async.wait_group %0;\n" ::"n"(SD - 3) : "memory");
+    __syncthreads();  // slice s+1 staged; the cells of slice s evaluated; slice s-1's slot and weights free
+    issue(s + SD - 1);
+    if (s + 1 < send) cell_pass(s + 1);
     if (own) {
+      const double(*t)[TX + 2] = su[s % SD];
+      const double(*w)[TY + 1][TX + 1] = wnu[s & 1];
       const int lx = tx + 1, ly = ty + 1;
       const double uC = t[ly][lx], uE = t[ly][lx + 1], uW = t[ly][lx - 1];
       const double uN = t[ly + 1][lx], uS = t[ly - 1][lx];
@@ -366,7 +376,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
       double ku = 0, kh = 0;
 #pragma unroll
       for (int t6 = 0; t6 < 6; ++t6) {
-        ku = fma(wnu[tt[t6]][ly + cys[t6]][lx + cxs[t6]], con[t6], ku);
+        ku = fma(w[tt[t6]][ly + cys[t6]][lx + cxs[t6]], con[t6], ku);
         if (WANT_G) kh = fma(hat[t6], con[t6], kh);
       }
       double f = 0;

@@ -270,3 +270,44 @@ def test_transformer_golden_fixture():
         assert rel(U0.reshape(-1)[::97], g[f"{tag}_U0_sample"]) <= ITERATE_TOL
         if tag == "small":
             assert rel(U, g["small_U"]) <= ITERATE_TOL and rel(U0, g["small_U0"]) <= ITERATE_TOL
+
+
+def test_reference_table_config_and_vtk(ref, tmp_path):
+    """`tpfem table` (run_table, runner.hpp:235-269) for a run config with a
+    "sweep": one table.csv row per (refinements, steps) entry in the
+    reference's format, with the reference's M1 iteration counts; and
+    `tpfem solve` with write_mesh / write_fields (runner.hpp:180,219-227):
+    mesh.vtk and one u_<i>.vtk per slice in vtk.hpp's format, the field of
+    the first method's state."""
+    import json
+    from paper_2502_21013_b200 import run
+    mats = {"winding_plus": {"j_amp": 950000.0}, "winding_minus": {"j_amp": -950000.0}}
+    conf = {"problem": "transformer", "nx": 12, "ny": 10, "period": 0.02, "output_dir": str(tmp_path / "t"),
+            "materials": mats, "solver": {"tol": 1e-6, "m3_max_cycles": 2},
+            "sweep": [{"refinements": 0, "steps": 8}, {"refinements": 0, "steps": 16}]}
+    path = tmp_path / "table.json"
+    path.write_text(json.dumps(conf))
+    assert run.main(["--ref-config", str(path)]) == 0
+    lines = (tmp_path / "t" / "table.csv").read_text().splitlines()
+    assert lines[0].startswith("steps,n_dof,init_seconds,m1_iterations") and len(lines) == 3
+    cfg = default_cfg(tol=1e-6, m3_max_cycles=2)
+    for line, steps in zip(lines[1:], (8, 16)):
+        f = line.split(",")
+        c = ref.tr_cfg(nx=12, ny=10, steps=steps, j_amp=9.5e5)
+        U0, _ = ref.tr_static_init(c, cfg)
+        m1 = ref.tr_solve_m1(c, *ref.tr_choose_nu_hat(c, U0, cfg), U0, cfg)
+        assert int(f[0]) == steps and int(f[3]) == m1.iterations
+    # solve with VTK output
+    conf2 = {"problem": "transformer", "method": "m1", "nx": 12, "ny": 10, "steps": 4, "period": 0.02,
+             "output_dir": str(tmp_path / "s"), "write_mesh": True, "write_fields": True, "materials": mats,
+             "solver": {"tol": 1e-6}}
+    path2 = tmp_path / "solve.json"
+    path2.write_text(json.dumps(conf2))
+    run.main(["--ref-config", str(path2)])
+    V, T, R, ndof = transformer_mesh(12, 10, 0)
+    mesh_vtk = (tmp_path / "s" / "mesh.vtk").read_text().splitlines()
+    assert mesh_vtk[4] == f"POINTS {len(V)} double" and f"CELL_DATA {len(T)}" in mesh_vtk
+    for i in range(1, 5):
+        u = (tmp_path / "s" / f"u_{i}.vtk").read_text().splitlines()
+        k = u.index(f"POINT_DATA {len(V)}")
+        assert len(u) == k + 3 + len(V)
