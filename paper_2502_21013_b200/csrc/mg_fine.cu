@@ -953,20 +953,6 @@ int rh_for(int m) {
   return m >= 200 ? 32 : m >= 100 ? 16 : m >= 50 ? 16 : 8;
 }
 
-// Galerkin levels of the frequency solver (Seven; no partial sums depend on
-// the item layout): the coarse passes are latency-bound -- each warp walks its
-// chunk row by row -- so the chunk height shrinks until the launch has enough
-// warps (>= TPGPU_SEVEN_WARPS, default 8192) to hide the per-row chain: cfg 3
-// levels 511 / 255 / 127 took 58 / 27 / 15 us per down pass at 32 / 32 / 16
-// rows (profiles/r2f_launches_cfg3_sweep.txt)
-int rh_seven(int m, int nb) {
-  static const int target = std::getenv("TPGPU_SEVEN_WARPS") ? std::atoi(std::getenv("TPGPU_SEVEN_WARPS")) : 8192;
-  int rh = rh_for(m);
-  const long strips = (m + 25) / 26;
-  while (rh > 4 && strips * ((m + rh - 1) / rh) * (long)nb < target) rh >>= 1;
-  return rh;
-}
-
 int env_int(const char* name, int dflt) {
   const char* v = std::getenv(name);
   return v ? std::atoi(v) : dflt;
@@ -983,7 +969,7 @@ void down_t(Problem& p, const FineOp& op, const T* r, T* z2, T* bc, int mc, cons
     return true;
   }();
   (void)attrs;
-  const int rh = std::is_same_v<S, Seven> ? rh_seven(op.m, nb) : rh_for(op.m);
+  const int rh = rh_for(op.m);
   launch_pdl(k_stream_down<S, NB, RA, WPBK, FUSED>, grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK),
              sm, p.cur_stream(), op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part,
              sf ? *sf : ScalFuse{});
@@ -998,7 +984,7 @@ void up_t(Problem& p, const FineOp& op, const T* r, const T* z2, const T* xc, in
     return true;
   }();
   (void)attrs;
-  const int rh = std::is_same_v<S, Seven> ? rh_seven(op.m, nb) : rh_for(op.m);
+  const int rh = rh_for(op.m);
   launch_pdl(k_stream_up<S, NB, RA, WPBK>, grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK), sm,
              p.cur_stream(), op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
