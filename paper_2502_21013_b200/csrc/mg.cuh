@@ -50,6 +50,7 @@ struct FineOp {
   size_t kstride = 0;             // slice mode: coefficients per batch (7n)
   const cplx* lam = nullptr;      // per batch symbol
   int m = 0, c = 0, n = 0;
+  int rha = 32;                   // rows per warp item of the apply pass (set at launch, rha_for)
 };
 
 // Krylov scalars reduced inside the fine passes (frequency mode, fused path):

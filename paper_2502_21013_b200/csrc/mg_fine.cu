@@ -829,7 +829,8 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
   extern __shared__ __align__(16) unsigned char fine_smem[];
   const int m = op.m;
   TP_PDL_ENTRY();
-  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, RHA, nb, nullptr);
+  const int rha = op.rha;
+  const ItemNB<WPBK, 1> it = item_nb<WPBK, 1>(m, OWN, rha, nb, nullptr);
   const bool on = INIT || !active || active[it.b[0]];
   T xab{};
   if (XUPD) xab = xa[it.b[0]];
@@ -928,7 +929,7 @@ __global__ void __launch_bounds__(WL * WPBK) k_stream_apply(FineOp op, const typ
   cp_wait<0>();
   warp_pair(s0, s1);
   if (lane == 0 && on) {
-    const int ns = (m + OWN - 1) / OWN, nch = (m + RHA - 1) / RHA;
+    const int ns = (m + OWN - 1) / OWN, nch = (m + rha - 1) / rha;
     const size_t per = (size_t)ns * nch;
     const size_t k = (size_t)b * per + (size_t)it.chunk * ns + it.strip;
     part[2 * k] = s0;
@@ -945,12 +946,24 @@ dim3 grid_for(int m, int own, int nb, int rh = RH, int wpb = WPB) {
 
 // rows per warp item of the down/up passes: long chunks amortise the 5-6
 // halo rows, short ones give the small grids enough warps
+// (levels of 1000+ nodes per side: 64 rows -- cfg 3 sweeps 348 -> 331 ms,
+// static_init 58.9 -> 57.0 s, profiles/r2l_ab.txt -- there are warps to spare
+// and a chunk's six halo rows are amortised over twice the rows)
 int rh_for(int m) {
+  static const int envb = std::getenv("TPGPU_RHBIG") ? std::atoi(std::getenv("TPGPU_RHBIG")) : 64;
   static const int env = std::getenv("TPGPU_RH") ? std::atoi(std::getenv("TPGPU_RH")) : 0;
   static const int env1 = std::getenv("TPGPU_RH1") ? std::atoi(std::getenv("TPGPU_RH1")) : 0;
+  if (m >= 1000) return envb;
   if (env > 0 && m >= 200) return env;
   if (env1 > 0 && m >= 100 && m < 200) return env1;
   return m >= 200 ? 32 : m >= 100 ? 16 : m >= 50 ? 16 : 8;
+}
+
+// rows per warp item of the apply pass: RHA, 64 on levels of 1000+ nodes per
+// side (TPGPU_RHA_BIG overrides)
+int rha_for(int m) {
+  static const int envb = std::getenv("TPGPU_RHA_BIG") ? std::atoi(std::getenv("TPGPU_RHA_BIG")) : 64;
+  return m >= 1000 ? envb : RHA;
 }
 
 int env_int(const char* name, int dflt) {
@@ -1002,18 +1015,21 @@ void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T*
     return true;
   }();
   (void)attrs;
-  const dim3 g = grid_for(op.m, 30, nb, RHA, W);
+  const int rha = rha_for(op.m);
+  const dim3 g = grid_for(op.m, 30, nb, rha, W);
   cudaStream_t s = p.cur_stream();
+  FineOp opa = op;
+  opa.rha = rha;
   using T0 = T*;
   using C0 = const T*;
   if (init)
-    launch_pdl(k_stream_apply<S, 1, RA, W>, g, dim3(WL * W), sm, s, op, z, pin, pout, q, beta, active, first, nb, part,
+    launch_pdl(k_stream_apply<S, 1, RA, W>, g, dim3(WL * W), sm, s, opa, z, pin, pout, q, beta, active, first, nb, part,
                T0(nullptr), C0(nullptr), ScalFuse{});
   else if (xa)
-    launch_pdl(k_stream_apply<S, 0, RA, W, true>, g, dim3(WL * W), sm3, s, op, z, pin, pout, q, beta, active, first,
+    launch_pdl(k_stream_apply<S, 0, RA, W, true>, g, dim3(WL * W), sm3, s, opa, z, pin, pout, q, beta, active, first,
                nb, part, x, xa, sfv);
   else
-    launch_pdl(k_stream_apply<S, 0, RA, W>, g, dim3(WL * W), sm, s, op, z, pin, pout, q, beta, active, first, nb, part,
+    launch_pdl(k_stream_apply<S, 0, RA, W>, g, dim3(WL * W), sm, s, opa, z, pin, pout, q, beta, active, first, nb, part,
                T0(nullptr), C0(nullptr), sfv);
   TP_LAUNCHED(&p);
 }
@@ -1021,7 +1037,7 @@ void apply_t(Problem& p, const FineOp& op, const T* z, const T* pin, T* pout, T*
 }  // namespace
 
 int fine_partials(int m, int kind) {
-  return kind == 0 ? items_per_batch(m, 30, RHA) : items_per_batch(m, kind == 1 ? 26 : 28, rh_for(m));
+  return kind == 0 ? items_per_batch(m, 30, rha_for(m)) : items_per_batch(m, kind == 1 ? 26 : 28, rh_for(m));
 }
 
 void launch_fine_apply(Problem& p, const FineOp& op, const cplx* z, const cplx* pin, cplx* pout, cplx* q,

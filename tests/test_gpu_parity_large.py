@@ -194,3 +194,27 @@ def test_sweeps_from_zero_match_reference(config, name):
     if config == 5:  # the linear control converges in one sweep (BASELINE.json configs[4])
         assert h[1] <= 1e-10 * h[0] and hr[1] <= 1e-10 * hr[0]
     _compare_iterates(dig, g)
+
+
+def test_cfg4_sweeps_from_static_init_match_reference():
+    """Config 4 from the production start: the reference's static_init over
+    all 2048 slices, frozen-field nu_hat, then its first three M1 sweeps --
+    Newton counts, U^0, nu_hat, the residual history (which rises over the
+    first sweeps from static_init, on both sides) and every iterate."""
+    g = golden("cfg4_static_sweeps_reference.npz")
+    count = int(g["iterations"])
+    cfg = default_cfg(tol=1e-12, m1_max_outer=count)
+    with Problem(baseline_desc(4)) as p:
+        U0, counts = p.static_init(cfg)
+        assert np.array_equal(counts, g["newton_counts"])
+        assert_checksum_close(checksum(U0), g["U0_checksum"], what="U0", size=U0.size)
+        assert rel(U0.reshape(-1)[::int(g["stride"])], g["U0_sample"]) <= ITERATE_TOL
+        nu, q = p.choose_nu_hat(cfg)
+        assert np.allclose(nu, g["nu_hat"], rtol=1e-12, atol=0)
+        dig = Digests(int(g["stride"]))
+        U, rep = p.solve_m1_fixed_point(None, cfg, callback=dig)
+    assert rep.iterations == count
+    h, hr = np.asarray(rep.residual_history), g["history"]
+    assert h.shape == hr.shape
+    assert np.max(np.abs(h - hr) / hr) <= 1e-8, (h, hr)
+    _compare_iterates(dig, g)
