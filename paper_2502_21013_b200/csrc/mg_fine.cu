@@ -946,11 +946,11 @@ dim3 grid_for(int m, int own, int nb, int rh = RH, int wpb = WPB) {
 
 // rows per warp item of the down/up passes: long chunks amortise the 5-6
 // halo rows, short ones give the small grids enough warps
-// (levels of 1000+ nodes per side: 64 rows -- cfg 3 sweeps 348 -> 331 ms,
+// (levels of 1000+ nodes per side: 128 rows -- cfg 3 sweeps 348 -> 331 ms at 64, 318 ms at 128,
 // static_init 58.9 -> 57.0 s, profiles/r2l_ab.txt -- there are warps to spare
 // and a chunk's six halo rows are amortised over twice the rows)
 int rh_for(int m) {
-  static const int envb = std::getenv("TPGPU_RHBIG") ? std::atoi(std::getenv("TPGPU_RHBIG")) : 64;
+  static const int envb = std::getenv("TPGPU_RHBIG") ? std::atoi(std::getenv("TPGPU_RHBIG")) : 128;
   static const int env = std::getenv("TPGPU_RH") ? std::atoi(std::getenv("TPGPU_RH")) : 0;
   static const int env1 = std::getenv("TPGPU_RH1") ? std::atoi(std::getenv("TPGPU_RH1")) : 0;
   if (m >= 1000) return envb;
