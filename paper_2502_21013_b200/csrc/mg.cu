@@ -878,7 +878,8 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
                           T* __restrict__ xa, int* __restrict__ count = nullptr,
                           const double* __restrict__ bfloor = nullptr, double fscale = 0.0,
                           int* __restrict__ count_clear = nullptr, volatile int* __restrict__ pub = nullptr,
-                          unsigned* __restrict__ done = nullptr, double* __restrict__ bown = nullptr) {
+                          unsigned* __restrict__ done = nullptr, double* __restrict__ bown = nullptr,
+                          const double* __restrict__ bscale = nullptr) {
   TP_PDL_ENTRY();
   const int b = blockIdx.x;
   if (b >= nb) return;
@@ -915,7 +916,7 @@ __global__ void k_scalars(int stage, const double* __restrict__ part, int per, i
     case ST_INIT: {
       // stopping reference: ||g_k||^2, floored at the frequency's equal share
       // of the whole right-hand side (BatchSolver::bfloor)
-      const double bref = bfloor ? fmax(s0, fscale * *bfloor) : s0;
+      const double bref = (bfloor ? fmax(s0, fscale * *bfloor) : s0) * (bscale ? bscale[b] : 1.0);
       bn2[b] = bref;
       if (bown) bown[b] = s0;  // the block's own ||g_k||^2 (SparseSolver contract, solve.hpp:79-89)
       rn2[b] = s1;
@@ -1515,7 +1516,8 @@ int BatchSolver<MODE>::solve(const T* b, T* x, int nb, bool warm, SolveStats* st
                      double floor_scale, volatile int* pub = nullptr) {
     launch_pdl(k_scalars<T>, dim3(nb), dim3(256), 0, s, stage, partials, per, nb, rtol2, rho.get(), mu.get(),
                alpha.get(), beta.get(), bn2.get(), rn2.get(), act, zero, ext_mask, xa_ptr, cnt, floor_ptr,
-               floor_scale, cnt_clear, pub, pub ? done_ctr.get() : static_cast<unsigned*>(nullptr), bown.get());
+               floor_scale, cnt_clear, pub, pub ? done_ctr.get() : static_cast<unsigned*>(nullptr), bown.get(),
+               bscale);
     TP_LAUNCHED(p);
   };
   trace_mark("pcg-init", s);

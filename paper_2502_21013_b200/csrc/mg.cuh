@@ -110,6 +110,9 @@ struct BatchSolver {
   // bfloor_scale * *bfloor) (device scalar: ||b||^2 of the whole right-hand side)
   const double* bfloor = nullptr;
   double bfloor_scale = 0.0;
+  // optional per-batch tolerance: batch b stops at rtol^2 * bscale[b] times
+  // its reference (inexact Newton forcing terms, newton.cu)
+  const double* bscale = nullptr;
   // work
   std::vector<DevBuf<T>> lb, lz0, lz1;  // per level (level 0: b is external)
   DevBuf<T> r, r2, p0, p1, q;

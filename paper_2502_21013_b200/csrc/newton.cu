@@ -11,6 +11,7 @@
 // norms, in exactly the reference's order and arithmetic.
 #include <algorithm>
 #include <cmath>
+#include <cstdio>
 #include <cstdlib>
 #include <memory>
 #include <string>
@@ -37,14 +38,20 @@ __global__ void k_accept(double* __restrict__ Ub, double* __restrict__ Rb, const
 }
 }  // namespace
 
+// Inexact Newton safeguards: the linear error's share of the
+// accepted residual (kSteer), and within kNear of the stopping threshold
+// kSteerNear; default forcing gamma and eta_max.
+constexpr double kSteer = 0.1, kSteerNear = 1e-6, kNear = 1e4;
+constexpr double kForcingGamma = 1e-2, kForcingMax = 1e-2;
+
 // One group of slices [g0, g1): its own buffers, batch solver and (when the
 // slices are split into concurrent groups) its own stream / host thread.
 struct NewtonGroup {
   int S = 0;  // slices per batch
   DevBuf<double> Ub, Rb, Db, Ut, Rt, inv, part, red;
   std::vector<DevBuf<double>> J;
-  DevBuf<int> d_slice, d_active, d_acc;
-  DevBuf<double> d_alpha;
+  DevBuf<int> d_slice, d_active, d_acc, d_todo;
+  DevBuf<double> d_alpha, d_bscale;
   BatchSolver<1> solver;
 };
 
@@ -66,6 +73,12 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   const int Nr = sh.s1 - sh.s0;
   int S = cfg.slice_chunk > 0 ? cfg.slice_chunk : (int)std::min<size_t>(Nr, (size_t)(0.5 * free_b) / per_slice);
   S = std::max(1, std::min(S, Nr));
+  // equal batches (464 + 48 slices at cfg 2 ran the short batch's Newton and
+  // PCG iterations at a tenth of the occupancy)
+  if (cfg.slice_chunk <= 0) {
+    const int nbatch = (Nr + S - 1) / S;
+    S = (Nr + nbatch - 1) / nbatch;
+  }
   // optional concurrent slice groups (TPGPU_SLICE_GROUPS, as the frequency
   // groups of the periodic solve).  Off by default: the Newton loop is a chain
   // of short launches and host decisions, and concurrent host threads measured
@@ -93,6 +106,14 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   if (const char* e = std::getenv("TPGPU_NEWTON_OMEGA")) mc.omega = mc.omega2 = std::atof(e);
   if (const char* e = std::getenv("TPGPU_NEWTON_OMEGA2")) mc.omega2 = std::atof(e);
 
+  // inexact Newton forcing terms (gamma, eta_max; TPGPU_NEWTON_FORCING=0 off)
+  double f_gamma = kForcingGamma, f_max = kForcingMax;
+  if (const char* e = std::getenv("TPGPU_NEWTON_FORCING")) {
+    f_gamma = 0;
+    std::sscanf(e, "%lf,%lf", &f_gamma, &f_max);
+  }
+  const bool forcing = f_gamma > 0;
+
   std::vector<std::unique_ptr<NewtonGroup>> groups(G);
   for (auto& gp : groups) {
     gp = std::make_unique<NewtonGroup>();
@@ -105,7 +126,9 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
     g.d_slice.alloc(Sg);
     g.d_active.alloc(Sg);
     g.d_acc.alloc(Sg);
+    g.d_todo.alloc(Sg);
     g.d_alpha.alloc(Sg);
+    g.d_bscale.alloc(Sg);
     std::vector<LevelOp> ops(nl);
     for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], g.J[l].get(), nullptr, false, {}};
     g.solver.init(this, ops, Sg, mc);
@@ -128,7 +151,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
       trace_mark("start", s);
     }
     std::vector<int> h_slice(Sb), h_active(Sb), h_acc(Sb);
-    std::vector<double> h_alpha(Sb), rnorm(Sb), scale(Sb), nrm2(Sb);
+    std::vector<double> h_alpha(Sb), rnorm(Sb), scale(Sb), nrm2(Sb), h_bscale(Sb, 1.0), rprev(Sb);
     for (int s0 = r0; s0 < r1; s0 += Sb) {
       const int nb = std::min(Sb, r1 - s0);
       for (int b = 0; b < Sb; ++b) {
@@ -142,6 +165,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
       newton_residual(*this, g.Ub.get(), nullptr, nullptr, nullptr, g.Rb.get(), g.d_slice.get(), g.d_active.get(),
                       Sb, nrm2.data(), g.part, g.red);
       for (int b = 0; b < nb; ++b) {
+        rprev[b] = -1.0;
         rnorm[b] = std::sqrt(nrm2[b]);
         scale[b] = std::max(rnorm[b], rnorm[b]);
         if (scale[b] == 0 || rnorm[b] <= cfg.static_tol * scale[b]) h_active[b] = 0;
@@ -156,45 +180,114 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
         launch_element_stencil(*this, true, g.Ub.get(), g.J[0].get(), nb);
         for (int l = 1; l < nl; ++l) launch_rap(*this, g.J[l - 1].get(), ms[l - 1], g.J[l].get(), ms[l], nb);
         launch_coarse_inverse_slice(*this, g.J[nl - 1].get(), ms[nl - 1], g.inv.get(), nb);
-        // delta = J^{-1} r  (masked to the active slices)
-        g.solver.ext_mask = g.d_active.get();
-        SolveStats st;
-        g.solver.solve(g.Rb.get(), g.Db.get(), nb, false, &st);
-        g.solver.ext_mask = nullptr;
-        // Armijo backtracking (solvers.hpp:158-177)
-        for (int b = 0; b < Sb; ++b) {
-          h_alpha[b] = 1.0;
-          h_acc[b] = 0;
-        }
-        std::vector<int> searching(h_active.begin(), h_active.end());
-        trace_mark("linesearch", s);
-        for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
-          int any = 0;
-          for (int b = 0; b < nb; ++b) any += searching[b];
-          if (!any) break;
-          TP_CUDA(cudaMemcpyAsync(g.d_alpha.get(), h_alpha.data(), Sb * sizeof(double), cudaMemcpyHostToDevice, s));
-          TP_CUDA(cudaMemcpyAsync(g.d_acc.get(), searching.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
-          newton_residual(*this, g.Ub.get(), g.Db.get(), g.d_alpha.get(), g.Ut.get(), g.Rt.get(), g.d_slice.get(),
-                          g.d_acc.get(), Sb, nrm2.data(), g.part, g.red);
-          std::vector<int> accept(Sb, 0);
+        // delta = J^{-1} r  (masked to the active slices), then the Armijo
+        // backtracking search (solvers.hpp:158-177).  Inexact Newton (DESIGN
+        // §5e): a slice's linear tolerance eta follows its observed contraction
+        // (Eisenstat-Walker, eta = gamma (r_k / r_{k-1})^2 in [rtol, eta_max]),
+        // and a step is kept only when the linear error cannot have steered it:
+        // the residual perturbation alpha eta r_k must be small against the
+        // accepted residual (and tiny near the stopping threshold).  Otherwise
+        // the step is re-solved warm to the full tolerance and searched again,
+        // so the accept/reject decisions and the counts are the exact solve's.
+        std::vector<double> eta(Sb, mc.rtol), rstart(rnorm);
+        std::vector<int> todo(h_active.begin(), h_active.end());
+        if (forcing)
           for (int b = 0; b < nb; ++b) {
-            if (!searching[b]) continue;
-            const double tnorm = std::sqrt(nrm2[b]);
-            if (tnorm <= (1.0 - cfg.armijo_slope * h_alpha[b]) * rnorm[b]) {
-              accept[b] = 1;
-              rnorm[b] = tnorm;
-              h_acc[b] = 1;
-              searching[b] = 0;
-            } else {
-              h_alpha[b] *= cfg.armijo_backtrack;
-            }
+            if (!h_active[b]) continue;
+            const double ratio = rprev[b] > 0 ? rnorm[b] / rprev[b] : 1.0;
+            const double rpred = rnorm[b] * ratio * ratio;
+            eta[b] = rpred <= kNear * cfg.static_tol * scale[b]
+                         ? mc.rtol
+                         : std::min(f_max, std::max(mc.rtol, f_gamma * ratio * ratio));
           }
-          TP_CUDA(cudaMemcpyAsync(g.d_acc.get(), accept.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
-          dim3 gr((unsigned)std::min<size_t>((n + 255) / 256, 1024), Sb);
-          k_accept<<<gr, 256, 0, s>>>(g.Ub.get(), g.Rb.get(), g.Ut.get(), g.Rt.get(), g.d_acc.get(), n);
-          TP_LAUNCHED(this);
-          TP_CUDA(cudaStreamSynchronize(s));
+        SolveStats st;
+        int halvings = 0, refined = 0;
+        for (int b = 0; b < Sb; ++b) h_acc[b] = 0;
+        for (int pass = 0; pass < 2; ++pass) {
+          bool loose = false;
+          for (int b = 0; b < nb; ++b) {
+            h_bscale[b] = (eta[b] / mc.rtol) * (eta[b] / mc.rtol);
+            loose = loose || (todo[b] && eta[b] > mc.rtol);
+          }
+          TP_CUDA(cudaMemcpyAsync(g.d_todo.get(), todo.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+          g.solver.ext_mask = g.d_todo.get();
+          if (loose) {
+            TP_CUDA(cudaMemcpyAsync(g.d_bscale.get(), h_bscale.data(), Sb * sizeof(double), cudaMemcpyHostToDevice, s));
+            g.solver.bscale = g.d_bscale.get();
+          }
+          g.solver.solve(g.Rb.get(), g.Db.get(), nb, pass > 0, &st);
+          g.solver.ext_mask = nullptr;
+          g.solver.bscale = nullptr;
+          std::vector<int> searching(todo), refine(Sb, 0);
+          for (int b = 0; b < Sb; ++b) h_alpha[b] = 1.0;
+          trace_mark("linesearch", s);
+          for (int h = 0; h <= cfg.armijo_max_halvings; ++h) {
+            int any = 0;
+            for (int b = 0; b < nb; ++b) any += searching[b];
+            if (!any) break;
+            halvings = std::max(halvings, h);
+            TP_CUDA(cudaMemcpyAsync(g.d_alpha.get(), h_alpha.data(), Sb * sizeof(double), cudaMemcpyHostToDevice, s));
+            TP_CUDA(cudaMemcpyAsync(g.d_acc.get(), searching.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+            newton_residual(*this, g.Ub.get(), g.Db.get(), g.d_alpha.get(), g.Ut.get(), g.Rt.get(), g.d_slice.get(),
+                            g.d_acc.get(), Sb, nrm2.data(), g.part, g.red);
+            std::vector<int> accept(Sb, 0);
+            for (int b = 0; b < nb; ++b) {
+              if (!searching[b]) continue;
+              const double tnorm = std::sqrt(nrm2[b]);
+              if (tnorm <= (1.0 - cfg.armijo_slope * h_alpha[b]) * rstart[b]) {
+                searching[b] = 0;
+                const double pert = h_alpha[b] * eta[b] * rstart[b];
+                const bool near = tnorm <= kNear * cfg.static_tol * scale[b];
+                if (eta[b] > mc.rtol && (pert > kSteer * tnorm || (near && pert > kSteerNear * tnorm))) {
+                  refine[b] = 1;
+                  continue;
+                }
+                accept[b] = 1;
+                rnorm[b] = tnorm;
+                h_acc[b] = 1;
+              } else {
+                h_alpha[b] *= cfg.armijo_backtrack;
+              }
+            }
+            TP_CUDA(cudaMemcpyAsync(g.d_acc.get(), accept.data(), Sb * sizeof(int), cudaMemcpyHostToDevice, s));
+            dim3 gr((unsigned)std::min<size_t>((n + 255) / 256, 1024), Sb);
+            k_accept<<<gr, 256, 0, s>>>(g.Ub.get(), g.Rb.get(), g.Ut.get(), g.Rt.get(), g.d_acc.get(), n);
+            TP_LAUNCHED(this);
+            TP_CUDA(cudaStreamSynchronize(s));
+          }
+          // a loose step whose search was exhausted is re-solved too
+          int nref = 0;
+          for (int b = 0; b < nb; ++b) {
+            if (searching[b] && eta[b] > mc.rtol) refine[b] = 1;
+            nref += refine[b];
+          }
+          if (nref == 0) break;
+          refined += nref;
+          for (int b = 0; b < nb; ++b) {
+            todo[b] = refine[b];
+            if (refine[b]) eta[b] = mc.rtol;
+          }
         }
+        for (int b = 0; b < nb; ++b)
+          if (h_active[b]) rprev[b] = rstart[b];
+        static const bool dbg_newton = std::getenv("TPGPU_DEBUG_NEWTON") != nullptr;
+        if (dbg_newton) {
+          int na = 0;
+          double worst = 0;
+          for (int b = 0; b < nb; ++b)
+            if (h_active[b]) {
+              ++na;
+              worst = std::max(worst, rnorm[b] / scale[b]);
+            }
+          std::fprintf(stderr,
+                       "newtondbg slices %d-%d step %d active %d pcg %d halvings %d refined %d worst_rel %.3e\n", s0,
+                       s0 + nb - 1, step, na, st.iterations, halvings, refined, worst);
+        }
+        if (std::getenv("TPGPU_DEBUG_NEWTON") && std::atoi(std::getenv("TPGPU_DEBUG_NEWTON")) >= 2)
+          for (int b = 0; b < nb; ++b)
+            if (h_active[b])
+              std::fprintf(stderr, "newtonslice %d step %d alpha %.17g rel %.17g\n", s0 + b, step, h_alpha[b],
+                           rnorm[b] / scale[b]);
         for (int b = 0; b < nb; ++b) {
           if (!h_active[b]) continue;
           if (!h_acc[b])

@@ -185,10 +185,16 @@ def test_sweeps_from_zero_match_reference(config, name):
     # ||R(0)|| = ||F|| summed over 5e8 entries in two different orders:
     # measured 1.2e-12 apart at cfg 5
     assert abs(h[0] - hr[0]) <= 1e-11 * hr[0]
-    # within 1e-10 of the first residual everywhere, 1e-6 relative where the
-    # residual is above 1e-6 of the first (config 5 lands at the rounding
-    # floor after its one sweep: 1.5e-11 vs 5.0e-12 against a first 2.6)
-    assert np.max(np.abs(h - hr)) <= 1e-10 * hr[0], (h, hr)
+    # within 1e-10 of the first residual everywhere (config 4: 1e-9), 1e-6
+    # relative where the residual is above 1e-6 of the first (config 5 lands
+    # at the rounding floor after its one sweep: 1.5e-11 vs 5.0e-12 against a
+    # first 2.6).  Config 4 (J0 = 200, Bs = 0.5, nu_inf = 50) evaluates
+    # R = F - K(U) with terms far above their sum: its history agrees to
+    # 2.0e-10 of the first residual while the iterates agree to 3e-14, for
+    # any block tolerance 1e-12..1e-14 (tools/zero_sweeps_diag.py,
+    # profiles/r2o_cfg4_diag.txt) -- the residual's own rounding
+    hist_tol = 1e-9 if config == 4 else 1e-10
+    assert np.max(np.abs(h - hr)) <= hist_tol * hr[0], (h, hr)
     big = hr > 1e-6 * hr[0]
     assert np.max(np.abs(h - hr)[big] / hr[big]) <= 1e-6, (h, hr)
     if config == 5:  # the linear control converges in one sweep (BASELINE.json configs[4])
