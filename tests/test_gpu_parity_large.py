@@ -183,8 +183,11 @@ def test_sweeps_from_zero_match_reference(config, name):
     h, hr = np.asarray(rep.residual_history), g["history"]
     assert h.shape == hr.shape
     # ||R(0)|| = ||F|| summed over 5e8 entries in two different orders:
-    # measured 1.2e-12 apart at cfg 5
-    assert abs(h[0] - hr[0]) <= 1e-11 * hr[0]
+    # measured 1.2e-12 apart at cfg 5, 1.1e-11 at cfg 2 (whose later
+    # residuals agree to 1.7e-13 and iterates to 7e-14: the difference is
+    # the summation of a norm dominated by few coil entries,
+    # profiles/r2o_cfg2_diag.txt)
+    assert abs(h[0] - hr[0]) <= (3e-11 if config == 2 else 1e-11) * hr[0]
     # within 1e-10 of the first residual everywhere (config 4: 1e-9), 1e-6
     # relative where the residual is above 1e-6 of the first (config 5 lands
     # at the rounding floor after its one sweep: 1.5e-11 vs 5.0e-12 against a
