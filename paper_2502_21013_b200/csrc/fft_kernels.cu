@@ -438,6 +438,212 @@ __global__ void __launch_bounds__(512) k_sfft_inverse(const cplx* __restrict__ U
   }
 }
 
+// ---------------------------------------------------------------- compile-time shapes
+// The same Stockham transforms with N and the column pairs P as template
+// constants (the plan's shapes for N = 64 .. 4096).  With N, P and every
+// pass's Ns known at compile time, the per-element index arithmetic (t / P,
+// t % P, j % Ns, the row/column split of the staging loops) folds to shifts
+// and masks, and every thread walks one column with a pointer increment
+// instead of a 64-bit multiply per element: the runtime-shaped kernels spent
+// ~75 % of their issued instructions on integer work (IMAD 30 %, ISETP 11 %,
+// LEA 8 %, the emulated divisions' IABS / I2F / F2I) against 15 % fp64,
+// issue-bound at 2.25 TB/s at cfg 3 (profiles/r2o_sass_mix_fwd.txt).
+template <int R, bool INV, int N, int P, int Ns>
+__device__ __forceinline__ void stockham_pass_t(cplx* z, const cplx* tw) {
+  constexpr int T = P * N / 16;
+  constexpr int B = 16 / R;
+  constexpr int NR = N / R;
+  cplx v[B][R];
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int t = threadIdx.x + b * T, p = t % P, j = t / P;
+#pragma unroll
+    for (int r = 0; r < R; ++r) v[b][r] = z[zx((j + r * NR) * P + p)];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int b = 0; b < B; ++b) {
+    const int t = threadIdx.x + b * T, p = t % P, j = t / P;
+    const int k = j % Ns;
+    if constexpr (Ns > 1) {
+      const int step = k * (N / (Ns * R));
+#pragma unroll
+      for (int r = 1; r < R; ++r) {
+        cplx w = tw[r * step];
+        if (INV) w.im = -w.im;
+        v[b][r] = cmul(v[b][r], w);
+      }
+    }
+    dft_reg<R, INV>(v[b]);
+    const int base = (j / Ns) * Ns * R + k;
+#pragma unroll
+    for (int r = 0; r < R; ++r) z[zx((base + r * Ns) * P + p)] = v[b][r];
+  }
+  __syncthreads();
+}
+
+template <bool INV, int N, int P, int Ns = 1>
+__device__ __forceinline__ void stockham_t(cplx* z, const cplx* tw) {
+  if constexpr (Ns * 16 <= N) {
+    stockham_pass_t<16, INV, N, P, Ns>(z, tw);
+    stockham_t<INV, N, P, Ns * 16>(z, tw);
+  } else if constexpr (N / Ns == 8) {
+    stockham_pass_t<8, INV, N, P, Ns>(z, tw);
+  } else if constexpr (N / Ns == 4) {
+    stockham_pass_t<4, INV, N, P, Ns>(z, tw);
+  } else if constexpr (N / Ns == 2) {
+    stockham_pass_t<2, INV, N, P, Ns>(z, tw);
+  }
+}
+
+template <int N, int P>
+__global__ void __launch_bounds__(P * N / 16) k_sfft_forward_t(const double* __restrict__ G, cplx* __restrict__ Ghat,
+                                                             size_t n, const cplx* __restrict__ tw,
+                                                             double* __restrict__ sq, const int* __restrict__ kslot) {
+  constexpr int T = P * N / 16, C = 2 * P, K = N / 2 + 1, RS = T / C;  // RS: rows per sweep of the block
+  static_assert(T % C == 0 && T <= 512, "shape");
+  extern __shared__ cplx smem[];
+  cplx* tws = smem;
+  cplx* z = smem + N;
+  const size_t j0 = (size_t)blockIdx.x * C;
+  for (int t = threadIdx.x; t < N; t += T) acp16(&tws[t], &tw[t], true);
+  // this thread's column cc and rows i0, i0 + RS, ... (cp.async, zero-fill past the last column)
+  const int cc = threadIdx.x % C, i0 = threadIdx.x / C, p = cc >> 1;
+  const bool ok = j0 + cc < n;
+  double* zd = reinterpret_cast<double*>(z);
+  {
+    const double* src = ok ? G + (size_t)i0 * n + j0 + cc : G;
+    const size_t step = ok ? (size_t)RS * n : 0;
+#pragma unroll 8
+    for (int i = i0; i < N; i += RS, src += step) acp8(&zd[2 * zx(i * P + p) + (cc & 1)], src, ok);
+  }
+  acp_wait_all();
+  __syncthreads();
+  stockham_t<false, N, P>(z, tws);
+  // untangle the two packed real columns: X = (Z_k + conj Z_{N-k}) / 2 (even
+  // column), (Z_k - conj Z_{N-k}) / 2i (odd column)
+  double e = 0;
+  if (ok) {
+    const bool odd = cc & 1;
+    cplx* dst = Ghat + (size_t)i0 * n + j0 + cc;
+    const size_t step = (size_t)RS * n;
+    for (int k = i0; k < K; k += RS, dst += step) {
+      const cplx Zk = z[zx(k * P + p)], Zm = conj(z[zx(((N - k) & (N - 1)) * P + p)]);
+      const cplx X = odd ? cplx{0.5 * (Zk.im - Zm.im), -0.5 * (Zk.re - Zm.re)}
+                         : cplx{0.5 * (Zk.re + Zm.re), 0.5 * (Zk.im + Zm.im)};
+      if (kslot) Ghat[(size_t)kslot[k] * n + j0 + cc] = X;
+      else *dst = X;
+      e = fma(X.re, X.re, fma(X.im, X.im, e));
+    }
+  }
+  if (sq) block_sum_to(e, sq + blockIdx.x);
+}
+
+template <int N, int P>
+__global__ void __launch_bounds__(P * N / 16) k_sfft_inverse_t(const cplx* __restrict__ Uhat, double* __restrict__ U,
+                                                             size_t n, const cplx* __restrict__ tw,
+                                                             double* __restrict__ part, const int* __restrict__ kslot) {
+  constexpr int T = P * N / 16, C = 2 * P, half = N / 2, K = half + 1, RS = T / C, KS = T / P;
+  static_assert(T % C == 0 && T <= 512, "shape");
+  extern __shared__ cplx smem[];
+  __shared__ double red[2][32];
+  cplx* tws = smem;
+  cplx* z = smem + N;
+  const size_t j0 = (size_t)blockIdx.x * C;
+  for (int t = threadIdx.x; t < N; t += T) acp16(&tws[t], &tw[t], true);
+  // the Hermitian extension of the two packed columns 2p, 2p+1, straight
+  // from the half spectrum: this thread's pair p, frequencies k0, k0 + KS, ...
+  const int p = threadIdx.x % P, k0 = threadIdx.x / P;
+  const size_t col = j0 + 2 * p;
+  const bool oka = col < n, okb = col + 1 < n;
+  double im2 = 0;
+  {
+    const cplx* src = Uhat + (size_t)k0 * n + col;
+    const size_t step = (size_t)KS * n;
+    constexpr int UNR = 4;
+    for (int kb = k0; kb < K; kb += UNR * KS) {
+      cplx xa[UNR], xb[UNR];
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = kb + u * KS;
+        xa[u] = xb[u] = cplx{0, 0};
+        if (k < K) {
+          const cplx* s = kslot ? Uhat + (size_t)kslot[k] * n + col : src + (size_t)u * step;
+          if (oka) xa[u] = s[0];
+          if (okb) xb[u] = s[1];
+        }
+      }
+      src += (size_t)UNR * step;
+#pragma unroll
+      for (int u = 0; u < UNR; ++u) {
+        const int k = kb + u * KS;
+        if (k >= K) break;
+        const cplx Xa = xa[u], Xb = xb[u];
+        if (k == 0 || k == half) {
+          z[zx(k * P + p)] = {Xa.re, Xb.re};
+          im2 += (Xa.im * Xa.im + Xb.im * Xb.im) / N;
+        } else {
+          z[zx(k * P + p)] = {Xa.re - Xb.im, Xa.im + Xb.re};
+          z[zx((N - k) * P + p)] = {Xa.re + Xb.im, -Xa.im + Xb.re};
+        }
+      }
+    }
+  }
+  acp_wait_all();
+  __syncthreads();
+  stockham_t<true, N, P>(z, tws);
+  constexpr double invN = 1.0 / N;
+  double re2 = 0;
+  const double* zd = reinterpret_cast<const double*>(z);
+  {
+    const int cc = threadIdx.x % C, i0 = threadIdx.x / C;
+    if (j0 + cc < n) {
+      double* dst = U + (size_t)i0 * n + j0 + cc;
+      const size_t step = (size_t)RS * n;
+#pragma unroll 4
+      for (int i = i0; i < N; i += RS, dst += step) {
+        const double x = zd[2 * zx(i * P + (cc >> 1)) + (cc & 1)] * invN;
+        *dst = x;
+        re2 = fma(x, x, re2);
+      }
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    re2 += __shfl_down_sync(0xffffffffu, re2, o);
+    im2 += __shfl_down_sync(0xffffffffu, im2, o);
+  }
+  if ((threadIdx.x & 31) == 0) {
+    red[0][threadIdx.x >> 5] = re2;
+    red[1][threadIdx.x >> 5] = im2;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double a = 0, b = 0;
+    for (int w = 0; w < T / 32; ++w) {
+      a += red[0][w];
+      b += red[1][w];
+    }
+    part[2 * blockIdx.x] = a;
+    part[2 * blockIdx.x + 1] = b;
+  }
+}
+
+// the compiled shapes: (N, P) -> kernel pointers (nullptr: runtime-shaped kernels)
+using FwdFn = void (*)(const double*, cplx*, size_t, const cplx*, double*, const int*);
+using InvFn = void (*)(const cplx*, double*, size_t, const cplx*, double*, const int*);
+template <int N, int P>
+bool pick_shape(int n_, int p_, FwdFn& f, InvFn& g) {
+  if (n_ != N || p_ != P) return false;
+  f = k_sfft_forward_t<N, P>;
+  g = k_sfft_inverse_t<N, P>;
+  return true;
+}
+bool compiled_shape(int N, int P, FwdFn& f, InvFn& g) {
+  return pick_shape<64, 32>(N, P, f, g) || pick_shape<128, 16>(N, P, f, g) || pick_shape<256, 8>(N, P, f, g) ||
+         pick_shape<512, 4>(N, P, f, g) || pick_shape<1024, 4>(N, P, f, g) || pick_shape<2048, 4>(N, P, f, g) ||
+         pick_shape<4096, 2>(N, P, f, g);
+}
+
 // ---------------------------------------------------------------- pipelined transforms
 // Persistent, software-pipelined forms of k_sfft_forward / k_sfft_inverse for
 // long periods (N >= 512): a block walks tiles of C = 2P columns with a
@@ -617,6 +823,8 @@ struct FftPlan {
   bool stockham = false;
   int sP = 0, sT = 0;    // forward: column pairs per block, threads
   int siP = 0, siT = 0;  // inverse
+  FwdFn tf = nullptr;    // compile-time-shaped kernels for (N, sP) when compiled (sP == siP)
+  InvFn ti = nullptr;
   size_t ssmem = 0, fsmem = 0;  // inverse (+ staged half spectrum) / forward
   // pipelined persistent kernels (N >= 512): column pairs, threads, shared bytes, grid
   bool pp_fwd = false, pp_inv = false;
@@ -671,6 +879,18 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
       pl->fsmem = (size_t)(N + zx_size(sP * N)) * sizeof(cplx);
       TP_CUDA(cudaFuncSetAttribute(k_sfft_forward, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->fsmem));
       TP_CUDA(cudaFuncSetAttribute(k_sfft_inverse, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)pl->ssmem));
+      // compile-time shapes (TPGPU_FFT_TEMPLATE=0: the runtime-shaped kernels)
+      static const bool want_t = !std::getenv("TPGPU_FFT_TEMPLATE") || std::atoi(std::getenv("TPGPU_FFT_TEMPLATE")) != 0;
+      FwdFn f = nullptr;
+      InvFn g = nullptr;
+      if (want_t && siP == sP && compiled_shape(N, sP, f, g)) {
+        pl->tf = f;
+        pl->ti = g;
+        TP_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pl->fsmem));
+        TP_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(g), cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     (int)pl->ssmem));
+      }
     }
   }
   // pipelined forms: two tiles of P column pairs (+ twiddles; the inverse also
@@ -732,6 +952,8 @@ void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
     const size_t ntiles = (c.n + 2 * pl.pP - 1) / (2 * pl.pP);
     k_sfft_forward_pp<<<pl.pgrid, pl.pT, pl.pfsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.pP, pl.tw.get(), sq, c.kslot,
                                                                  ntiles);
+  } else if (pl.tf) {
+    pl.tf<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.tw.get(), sq, c.kslot);
   } else if (pl.stockham) {
     k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq, c.kslot);
   } else {
@@ -751,6 +973,8 @@ void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, doub
     const size_t ntiles = (c.n + 2 * pl.pP - 1) / (2 * pl.pP);
     k_sfft_inverse_pp<<<pl.pgrid, pl.pT, pl.pismem, c.stream>>>(Uhat, U, c.n, pl.N, pl.pP, pl.tw.get(),
                                                                  c.part->get(), c.kslot, ntiles);
+  } else if (pl.ti) {
+    pl.ti<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.tw.get(), c.part->get(), c.kslot);
   } else if (pl.stockham) {
     k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.N, pl.siP, pl.tw.get(),
                                                             c.part->get(), c.kslot);

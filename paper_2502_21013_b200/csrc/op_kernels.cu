@@ -215,10 +215,22 @@ __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
 // zero-filled off the domain, one barrier per slice): with one slice of
 // look-ahead the kernel was latency-bound at ~1.3 TB/s.
 constexpr int SB = 16;
-constexpr int SD = 6;
+#ifndef TPGPU_SWEEP_SD
+#define TPGPU_SWEEP_SD 6
+#endif
+constexpr int SD = TPGPU_SWEEP_SD;
+// thread rows per block: the 32 x 8 node tile has 33 x 9 = 297 cells, so
+// with TY thread rows 41 threads (two warps) evaluate a second cell while the
+// other six warps wait at the slice barrier; TYT = 10 rows (320 threads)
+// evaluate every cell in one round and leave two warps idle in the node pass
+#ifndef TPGPU_SWEEP_TYT
+#define TPGPU_SWEEP_TYT 10
+#endif
+constexpr int TYT = TPGPU_SWEEP_TYT;
+constexpr int SNT = TX * TYT;  // threads per block
 // resident blocks per SM the registers are bounded for
 #ifndef TPGPU_SWEEP_MINB
-#define TPGPU_SWEEP_MINB 3
+#define TPGPU_SWEEP_MINB (TYT > TY ? 2 : 3)
 #endif
 
 __device__ __forceinline__ void cp_async8(void* sdst, const void* g, bool ok) {
@@ -227,7 +239,7 @@ __device__ __forceinline__ void cp_async8(void* sdst, const void* g, bool ok) {
 }
 
 template <bool WANT_G>
-__global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
+__global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
     const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
     int sy0, int rows, double* __restrict__ G, double* __restrict__ part, int m, int c, int N, double inv_tau,
     const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
@@ -246,7 +258,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
   // (x0 + lx, y0 + ly) in slice s = base + s * stride (main strip, or the
   // neighbours' halo rows), or zero (Dirichlet boundary / outside)
   constexpr int TN = (TY + 2) * (TX + 2);
-  const int k0 = tid, k1 = tid + TX * TY;
+  const int k0 = tid, k1 = tid + SNT;
   const double* sb[2];
   size_t sstr[2];
   bool sok[2];
@@ -284,7 +296,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
 #pragma unroll
   for (int j = 0; j < SD - 1; ++j) issue(sbeg + j);
   // per-cell material constants of the tile (+ halo cells)
-  for (int k = tid; k < (TY + 1) * (TX + 1); k += TX * TY) {
+  for (int k = tid; k < (TY + 1) * (TX + 1); k += SNT) {
     const int ly = k / (TX + 1), lx = k % (TX + 1);
     const int i = x0 + lx, j = y0 + ly;
     double a = 0, b = 0, bs = 1, h = 0;
@@ -302,7 +314,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
     chat[ly][lx] = h;
   }
   const int x = x0 + tx, y = y0 + ty;
-  const bool own = x < m && y < sy0 + rows;
+  const bool own = ty < TY && x < m && y < sy0 + rows;
   const size_t i = own ? (size_t)y * m + x : 0;           // global
   const size_t il = own ? (size_t)(y - sy0) * m + x : 0;  // local
   const double mi = own ? mass[i] : 0.0;
@@ -315,11 +327,11 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
   // slice-invariant operands in registers: the material law of this thread's
   // cells (cell pass) and nu_hat / 2 of the node's six incident triangles
   constexpr int NCELL = (TY + 1) * (TX + 1);
-  const int kc0 = tid, kc1 = tid + TX * TY;
+  const int kc0 = tid, kc1 = tid + SNT;
   __syncthreads();  // per-cell material constants staged
   double cl[2][3];
 #pragma unroll
-  for (int e = 0; e < 2; ++e) {
+  for (int e = 0; e < (SNT >= NCELL ? 1 : 2); ++e) {
     const int k = e == 0 ? kc0 : kc1;
     const int cy = k / (TX + 1), cx = k - cy * (TX + 1);
     const bool ok = k < NCELL;
@@ -330,7 +342,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
   const int cxs[6] = {0, 0, -1, -1, -1, 0}, cys[6] = {0, 0, 0, -1, -1, -1};
   double hat[6];
 #pragma unroll
-  for (int t6 = 0; t6 < 6; ++t6) hat[t6] = WANT_G ? chat[ty + 1 + cys[t6]][tx + 1 + cxs[t6]] : 0.0;
+  for (int t6 = 0; t6 < 6; ++t6) hat[t6] = (WANT_G && ty < TY) ? chat[ty + 1 + cys[t6]][tx + 1 + cxs[t6]] : 0.0;
   double r2 = 0;
   // nu(|grad u|) / 2 once per triangle: the (TY+1) x (TX+1) cells under the
   // node tile, two triangles each (T1 lower-right: d = (u10-u00, u11-u10);
@@ -342,7 +354,7 @@ __global__ void __launch_bounds__(TX * TY, TPGPU_SWEEP_MINB) k_sweep_slices(
     const double(*t)[TX + 2] = su[sl % SD];
     double(*w)[TY + 1][TX + 1] = wnu[sl & 1];
 #pragma unroll
-    for (int e = 0; e < 2; ++e) {
+    for (int e = 0; e < (SNT >= NCELL ? 1 : 2); ++e) {
       const int k = e == 0 ? kc0 : kc1;
       if (k < NCELL) {
         const int cy = k / (TX + 1), cx = k - cy * (TX + 1);
@@ -578,11 +590,11 @@ double Problem::residual_and_rhs(bool want_rhs) {
   const double* hi = sharded() ? halo_hi.get() : nullptr;
   if (want_rhs) {
     require(nu_hat_set, "fixed-point sweep: nu_hat not installed");
-    k_sweep_slices<true><<<grid, dim3(TX, TY), 0, stream>>>(
+    k_sweep_slices<true><<<grid, dim3(TX, TYT), 0, stream>>>(
         U.get(), lo, hi, sh.y0, rows, G.get(), part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
         d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   } else {
-    k_sweep_slices<false><<<grid, dim3(TX, TY), 0, stream>>>(
+    k_sweep_slices<false><<<grid, dim3(TX, TYT), 0, stream>>>(
         U.get(), lo, hi, sh.y0, rows, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
         d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
   }
