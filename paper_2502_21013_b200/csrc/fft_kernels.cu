@@ -448,6 +448,22 @@ __global__ void __launch_bounds__(512) k_sfft_inverse(const cplx* __restrict__ U
 // ~75 % of their issued instructions on integer work (IMAD 30 %, ISETP 11 %,
 // LEA 8 %, the emulated divisions' IABS / I2F / F2I) against 15 % fp64,
 // issue-bound at 2.25 TB/s at cfg 3 (profiles/r2o_sass_mix_fwd.txt).
+// Compact twiddle table of the compile-time-shaped kernels: W_N^m =
+// hi[m / 32] * lo[m % 32] from N/32 + 32 entries (1 KB at N = 1024 instead of
+// the 16 KB full table, so three blocks fit an SM; the product adds ~1 ulp)
+template <int N>
+constexpr int tw_count() { return N / 32 + 32; }
+// resident 256-thread blocks per SM the registers of the compile-time-shaped
+// kernels are bounded for (3: 80 registers with ~150 bytes of spills -- measured
+// slower, 310-346 vs 295-297 ms per cfg-3 sweep, profiles/r2u_ab.txt; 2: none)
+#ifndef TPGPU_FFT_MINB
+#define TPGPU_FFT_MINB 2
+#endif
+template <int N>
+__device__ __forceinline__ cplx tw_at(const cplx* tw, int m) {
+  return cmul(tw[m >> 5], tw[N / 32 + (m & 31)]);
+}
+
 template <int R, bool INV, int N, int P, int Ns>
 __device__ __forceinline__ void stockham_pass_t(cplx* z, const cplx* tw) {
   constexpr int T = P * N / 16;
@@ -469,7 +485,7 @@ __device__ __forceinline__ void stockham_pass_t(cplx* z, const cplx* tw) {
       const int step = k * (N / (Ns * R));
 #pragma unroll
       for (int r = 1; r < R; ++r) {
-        cplx w = tw[r * step];
+        cplx w = tw_at<N>(tw, r * step);
         if (INV) w.im = -w.im;
         v[b][r] = cmul(v[b][r], w);
       }
@@ -497,16 +513,16 @@ __device__ __forceinline__ void stockham_t(cplx* z, const cplx* tw) {
 }
 
 template <int N, int P>
-__global__ void __launch_bounds__(P * N / 16) k_sfft_forward_t(const double* __restrict__ G, cplx* __restrict__ Ghat,
+__global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB : 1) k_sfft_forward_t(const double* __restrict__ G, cplx* __restrict__ Ghat,
                                                              size_t n, const cplx* __restrict__ tw,
                                                              double* __restrict__ sq, const int* __restrict__ kslot) {
   constexpr int T = P * N / 16, C = 2 * P, K = N / 2 + 1, RS = T / C;  // RS: rows per sweep of the block
   static_assert(T % C == 0 && T <= 512, "shape");
   extern __shared__ cplx smem[];
   cplx* tws = smem;
-  cplx* z = smem + N;
+  cplx* z = smem + tw_count<N>();
   const size_t j0 = (size_t)blockIdx.x * C;
-  for (int t = threadIdx.x; t < N; t += T) acp16(&tws[t], &tw[t], true);
+  for (int t = threadIdx.x; t < tw_count<N>(); t += T) acp16(&tws[t], &tw[t], true);
   // this thread's column cc and rows i0, i0 + RS, ... (cp.async, zero-fill past the last column)
   const int cc = threadIdx.x % C, i0 = threadIdx.x / C, p = cc >> 1;
   const bool ok = j0 + cc < n;
@@ -540,7 +556,7 @@ __global__ void __launch_bounds__(P * N / 16) k_sfft_forward_t(const double* __r
 }
 
 template <int N, int P>
-__global__ void __launch_bounds__(P * N / 16) k_sfft_inverse_t(const cplx* __restrict__ Uhat, double* __restrict__ U,
+__global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB : 1) k_sfft_inverse_t(const cplx* __restrict__ Uhat, double* __restrict__ U,
                                                              size_t n, const cplx* __restrict__ tw,
                                                              double* __restrict__ part, const int* __restrict__ kslot) {
   constexpr int T = P * N / 16, C = 2 * P, half = N / 2, K = half + 1, RS = T / C, KS = T / P;
@@ -548,9 +564,9 @@ __global__ void __launch_bounds__(P * N / 16) k_sfft_inverse_t(const cplx* __res
   extern __shared__ cplx smem[];
   __shared__ double red[2][32];
   cplx* tws = smem;
-  cplx* z = smem + N;
+  cplx* z = smem + tw_count<N>();
   const size_t j0 = (size_t)blockIdx.x * C;
-  for (int t = threadIdx.x; t < N; t += T) acp16(&tws[t], &tw[t], true);
+  for (int t = threadIdx.x; t < tw_count<N>(); t += T) acp16(&tws[t], &tw[t], true);
   // the Hermitian extension of the two packed columns 2p, 2p+1, straight
   // from the half spectrum: this thread's pair p, frequencies k0, k0 + KS, ...
   const int p = threadIdx.x % P, k0 = threadIdx.x / P;
@@ -825,6 +841,8 @@ struct FftPlan {
   int siP = 0, siT = 0;  // inverse
   FwdFn tf = nullptr;    // compile-time-shaped kernels for (N, sP) when compiled (sP == siP)
   InvFn ti = nullptr;
+  DevBuf<cplx> tw2;      // their compact twiddle table (hi: W^{32j}, j < N/32; lo: W^i, i < 32)
+  size_t tsmem = 0;      // their shared bytes
   size_t ssmem = 0, fsmem = 0;  // inverse (+ staged half spectrum) / forward
   // pipelined persistent kernels (N >= 512): column pairs, threads, shared bytes, grid
   bool pp_fwd = false, pp_inv = false;
@@ -886,10 +904,23 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
       if (want_t && siP == sP && compiled_shape(N, sP, f, g)) {
         pl->tf = f;
         pl->ti = g;
+        const int nt = N / 32 + 32;
+        std::vector<cplx> t2(nt);
+        for (int j = 0; j < N / 32; ++j) {
+          const double a = -2.0 * std::numbers::pi * (32.0 * j) / N;
+          t2[j] = {std::cos(a), std::sin(a)};
+        }
+        for (int i = 0; i < 32; ++i) {
+          const double a = -2.0 * std::numbers::pi * i / N;
+          t2[N / 32 + i] = {std::cos(a), std::sin(a)};
+        }
+        pl->tw2.alloc(nt);
+        TP_CUDA(cudaMemcpy(pl->tw2.get(), t2.data(), nt * sizeof(cplx), cudaMemcpyHostToDevice));
+        pl->tsmem = (size_t)(nt + zx_size(sP * N)) * sizeof(cplx);
         TP_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(f), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)pl->fsmem));
+                                     (int)pl->tsmem));
         TP_CUDA(cudaFuncSetAttribute(reinterpret_cast<const void*>(g), cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     (int)pl->ssmem));
+                                     (int)pl->tsmem));
       }
     }
   }
@@ -953,7 +984,7 @@ void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
     k_sfft_forward_pp<<<pl.pgrid, pl.pT, pl.pfsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.pP, pl.tw.get(), sq, c.kslot,
                                                                  ntiles);
   } else if (pl.tf) {
-    pl.tf<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.tw.get(), sq, c.kslot);
+    pl.tf<<<blocks, pl.sT, pl.tsmem, c.stream>>>(G, Ghat, c.n, pl.tw2.get(), sq, c.kslot);
   } else if (pl.stockham) {
     k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq, c.kslot);
   } else {
@@ -974,7 +1005,7 @@ void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, doub
     k_sfft_inverse_pp<<<pl.pgrid, pl.pT, pl.pismem, c.stream>>>(Uhat, U, c.n, pl.N, pl.pP, pl.tw.get(),
                                                                  c.part->get(), c.kslot, ntiles);
   } else if (pl.ti) {
-    pl.ti<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.tw.get(), c.part->get(), c.kslot);
+    pl.ti<<<blocks, pl.siT, pl.tsmem, c.stream>>>(Uhat, U, c.n, pl.tw2.get(), c.part->get(), c.kslot);
   } else if (pl.stockham) {
     k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.N, pl.siP, pl.tw.get(),
                                                             c.part->get(), c.kslot);

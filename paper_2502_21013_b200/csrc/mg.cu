@@ -1413,7 +1413,7 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
     if (!ops[l].five && !j1 && !tile_coarse && ops[l].m >= 7) {
       FineOp so;
       so.K = ops[l].K;
-      so.M = ops[l].M;
+      so.M = ops[l].drop_m ? nullptr : ops[l].M;
       so.lam = lam;
       so.m = ops[l].m;
       so.n = ops[l].n;

@@ -20,12 +20,15 @@
 namespace tpgpu {
 
 // Slice-mode (Newton Jacobian) smoother: l1-Jacobi diagonal sum_j |J_ij| with
-// the degree-2 Chebyshev weights for D_l1^-1 J on [1/6, 1] (1: on; 0: plain
-// damped Jacobi, omega = 0.6 on the true diagonal)
+// the degree-2 Chebyshev weights for D_l1^-1 J on [1/15, 1] (1: on; 0: plain
+// damped Jacobi, omega = 0.6 on the true diagonal).  Interval measured on cfg 2
+// static_init (tools/init_omega_sweep.py, profiles/r2o_omega_sweep.txt,
+// r2t_omega.txt): [1/6, 1] 3.98-4.00 s, [1/10, 1] 3.77, [1/15, 1] 3.69-3.70,
+// [1/20, 1] 3.69, [1/25, 1] 4.05, [1/4, 1] 4.28; Newton counts equal
 #ifndef TPGPU_SLICE_L1
 #define TPGPU_SLICE_L1 1
 #endif
-constexpr double kL1Omega1 = 1.1387, kL1Omega2 = 3.4641;
+constexpr double kL1Omega1 = 1.1583, kL1Omega2 = 4.9169;
 
 struct MGConfig {
   int pre = 2, post = 2;    // smoothing sweeps
@@ -94,6 +97,8 @@ struct LevelOp {
   const double* M = nullptr;  // freq only
   bool five = false;          // freq mode: K 5-point and M diagonal (fine level)
   FineOp fine;                // freq mode level 0: streaming kernels (we != nullptr)
+  bool drop_m = false;        // freq mode Galerkin level: the V-cycle's level operator is K alone
+                              // (max |lambda| M negligible against K, Problem::build_freq_work)
 };
 
 template <int MODE>

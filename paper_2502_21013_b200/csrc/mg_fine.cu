@@ -301,6 +301,60 @@ struct Seven {  // coarse levels: Galerkin K and M, symmetric 7-point (C, E, N, 
   }
 };
 
+// Galerkin levels of the frequency solver where the shift is negligible
+// (max_k |lambda_k| M_l << K_l, measured per level when the hierarchy is
+// built, Problem::build_freq_work): the level operator of the V-cycle is K_l
+// alone -- four real planes instead of eight, a real diagonal.  Only the
+// preconditioner changes (the COCG residual is the fine operator's own), and
+// the V-cycle stays a fixed complex-symmetric operator.
+struct SevenK {
+  using T = cplx;
+  static constexpr int NW = 4;  // K C E N NE
+  struct Src {
+    const double* K;
+    unsigned n;
+    bool col;
+  };
+  static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int, int) {
+    Src s;
+    s.K = op.K + xc;
+    s.n = (unsigned)op.n;
+    s.col = x >= 0 && x < op.m;
+    return s;
+  }
+  static __device__ __forceinline__ void stage(WRow<NW>& st, const Src& s, int lane, int, unsigned moff,
+                                               bool rowok) {
+    const bool v = s.col && rowok;
+    const int dirs[4] = {SC, SE_, SN_, SNE};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) cp8(&st.w[q][lane], s.K + (dirs[q] * s.n + moff), v);
+  }
+  static constexpr int RETAIN = 3;
+  static constexpr bool XLANE = true;
+  struct Reg {
+    const WRow<NW>* p;
+    const WRow<NW>* pb;
+    int lane;
+  };
+  static __device__ __forceinline__ Reg load(const WRow<NW>& st, int lane, const Reg& below) {
+    return {&st, below.p, lane};
+  }
+  static __device__ __forceinline__ Reg first(const WRow<NW>& st, int lane) { return {&st, &st, lane}; }
+  static __device__ __forceinline__ cplx diag(const Reg& y, cplx) { return {y.p->w[0][y.lane], 0.0}; }
+  static __device__ __forceinline__ cplx sdiag(const Reg&, cplx d) { return d; }
+  static __device__ __forceinline__ cplx apply(const Reg& y, cplx, cplx d, cplx vs, cplx v, cplx vn) {
+    const int ln = y.lane, lw = ln > 0 ? ln - 1 : 0;
+    const cplx vw = shf_up(v), ve = shf_dn(v), vne = shf_dn(vn), vsw = shf_up(vs);
+    const WRow<NW>& a = *y.p;
+    const WRow<NW>& b = *y.pb;
+    const double kE = a.w[1][ln], kW = a.w[1][lw], kN = a.w[2][ln], kS = b.w[2][ln], kNE = a.w[3][ln],
+                 kSW = b.w[3][lw];
+    const double re = kE * ve.re + kW * vw.re + kN * vn.re + kS * vs.re + kNE * vne.re + kSW * vsw.re;
+    const double im = kE * ve.im + kW * vw.im + kN * vn.im + kS * vs.im + kNE * vne.im + kSW * vsw.im;
+    return {fma(d.re, v.re, re), fma(d.re, v.im, im)};
+  }
+};
+
 // slice mode (static_init Newton): per-slice symmetric 7-point Jacobians J_b
 // (planes C, E, N, NE of the 7n-per-slice stencil), real vectors
 struct SevenJ {
@@ -1069,6 +1123,8 @@ void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, c
     static const int ra = env_int("TPGPU_RA5", 6);
     if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
     else down_t<Five, 1, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+  } else if (!op.M) {
+    down_t<SevenK, 1, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   } else {
     static const int ra = env_int("TPGPU_RA7", 2), w = env_int("TPGPU_WPB7", 2);
     if (ra == 4) down_t<Seven, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
@@ -1085,6 +1141,8 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
     static const int ra = env_int("TPGPU_RA5U", 2);
     if (ra == 4) up_t<Five, 1, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else up_t<Five, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+  } else if (!op.M) {
+    up_t<SevenK, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   } else {
     static const int ra = env_int("TPGPU_RA7U", 2), w = env_int("TPGPU_WPB7", 2);
     if (ra == 4) up_t<Seven, 1, 4, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);

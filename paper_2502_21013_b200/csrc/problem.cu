@@ -340,6 +340,29 @@ void Problem::install_nu_hat(const double* nu, double q) {
   uhat_valid = false;
 }
 
+namespace {
+// max_i sum_d |M_d(i)| and min_i K_C(i) of one level's 7-point planes (stride
+// n), as ordered bit patterns of non-negative doubles
+__global__ void k_level_shift_ratio(const double* __restrict__ K, const double* __restrict__ M, size_t n,
+                                    unsigned long long* __restrict__ out) {
+  double mx = 0, mn = __longlong_as_double(0x7ff0000000000000ll);
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    double s = 0;
+    for (int d = 0; d < 7; ++d) s += fabs(M[d * n + i]);
+    mx = fmax(mx, s);
+    mn = fmin(mn, K[i]);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mx = fmax(mx, __shfl_down_sync(0xffffffffu, mx, o));
+    mn = fmin(mn, __shfl_down_sync(0xffffffffu, mn, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&out[0], (unsigned long long)__double_as_longlong(mx));
+    atomicMin(&out[1], (unsigned long long)__double_as_longlong(fmax(mn, 0.0)));
+  }
+}
+}  // namespace
+
 // PeriodicSolver ctor (periodic.hpp:128-139): symbols + multigrid hierarchy
 // for (lambda_k M + K_hat), all frequencies sharing the real stencils.
 void Problem::build_frequency_solver(const tp_solver_cfg& cfg) {
@@ -397,8 +420,60 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
   }
   out = std::make_unique<FreqWork>();
   FreqWork* w = out.get();
-  // symbols lambda_k (periodic.hpp:146-152) of this rank's frequencies
   const int Kr = sh.k1 - sh.k0;
+  // chunk: work ~ 7 complex vectors per frequency on the fine level (+1/3 coarse)
+  size_t free_b = 0, total_b = 0;
+  TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
+  const double per = 16.0 * 8.5 * n;
+  int chunk = cfg.freq_chunk > 0 ? cfg.freq_chunk : (int)std::min<double>(Kr, 0.6 * free_b / per);
+  chunk = std::max(1, std::min(chunk, Kr));
+  w->chunk = chunk;
+  // Single GPU, several frequency groups: deal the frequencies of every chunk
+  // to the groups in boustrophedon order (the sharded solver's slot
+  // permutation), so each group's contiguous slot block holds a
+  // spread of the spectrum instead of group 0 holding the lowest -- the
+  // slowest -- frequencies of every chunk.  Only the time DFTs index through
+  // the permutation (kslot).  Opt-in (TPGPU_GROUP_DEAL=1): measured level at
+  // cfg 3 and slower at cfg 1 (3.26 vs 3.01 ms per sweep: every group then
+  // runs the long iteration chain of its low frequencies, profiles/r2t_ab.txt)
+  if (!K0 && !sharded()) {
+    static const bool deal = std::getenv("TPGPU_GROUP_DEAL") && std::atoi(std::getenv("TPGPU_GROUP_DEAL")) != 0;
+    const int parts0 = std::max(1, std::min(want_groups, chunk));
+    const int per0 = (chunk + parts0 - 1) / parts0;
+    sh.kperm.clear();
+    d_kslot.release();
+    if (deal && parts0 > 1) {
+      const int span = parts0 * per0;
+      std::vector<int> perm(Kr, -1);
+      for (int c0 = 0; c0 < Kr; c0 += span) {
+        std::vector<int> cap(parts0), fill(parts0, 0);
+        for (int g = 0; g < parts0; ++g) cap[g] = std::max(0, std::min(per0, Kr - (c0 + g * per0)));
+        const int cnt = std::min(span, Kr - c0);
+        int g = 0, dir = 1;
+        for (int i = 0; i < cnt; ++i) {
+          while (fill[g] >= cap[g]) {  // next group in snake order with room
+            g += dir;
+            if (g == parts0 || g < 0) {
+              dir = -dir;
+              g += dir;
+            }
+          }
+          perm[c0 + g * per0 + fill[g]++] = c0 + i;  // slot -> frequency
+          g += dir;
+          if (g == parts0 || g < 0) {
+            dir = -dir;
+            g += dir;
+          }
+        }
+      }
+      sh.kperm = perm;
+      std::vector<int> slot(Kr);
+      for (int s2 = 0; s2 < Kr; ++s2) slot[perm[s2]] = s2;
+      d_kslot.alloc(Kr);
+      TP_CUDA(cudaMemcpy(d_kslot.get(), slot.data(), Kr * sizeof(int), cudaMemcpyHostToDevice));
+    }
+  }
+  // symbols lambda_k (periodic.hpp:146-152) of this rank's frequencies
   std::vector<cplx> lam(Kr);
   for (int kk = 0; kk < Kr; ++kk) {
     const int k = freq_of_slot(sh.k0 + kk);
@@ -417,15 +492,37 @@ void Problem::build_freq_work(std::vector<Level>& lv, std::unique_ptr<FreqWork>&
   w->nL = LC.n;
   w->inv.alloc((size_t)Kr * LC.n * LC.n);
   launch_coarse_inverse_freq(*this, LC.K.get(), LC.M.get(), LC.m, w->lam.get(), w->inv.get(), Kr);
-  // chunk: work ~ 7 complex vectors per frequency on the fine level (+1/3 coarse)
-  size_t free_b = 0, total_b = 0;
-  TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
-  const double per = 16.0 * 8.5 * n;
-  int chunk = cfg.freq_chunk > 0 ? cfg.freq_chunk : (int)std::min<double>(Kr, 0.6 * free_b / per);
-  chunk = std::max(1, std::min(chunk, Kr));
-  w->chunk = chunk;
   std::vector<LevelOp> ops(nl);
   for (int l = 0; l < nl; ++l) ops[l] = {lv[l].m, lv[l].n, lv[l].K.get(), lv[l].M.get(), l == 0 && !K0, {}};
+  // Galerkin levels whose shift is negligible: max_k |lambda_k| max_i sum_d
+  // |M_l,d(i)| <= 1e-2 min_i K_l,C(i) (|lambda_k| <= 2 / tau) -- the V-cycle
+  // uses K_l alone there (SevenK: half the coefficient planes; M_l grows 4x
+  // per level against K_l, so this holds on the fine Galerkin levels of the
+  // large grids: cfg 3 levels 1-4 at <= 3.7e-3, cfg 1 level 1 at 4.0e-3;
+  // 1e-2 against 1e-3: cfg 1 3.0 -> 2.9 ms per sweep, profiles/r2u_ab.txt).
+  // TPGPU_DROP_M=ratio overrides the threshold (0: keep M everywhere).
+  static const double drop_thr = std::getenv("TPGPU_DROP_M") ? std::atof(std::getenv("TPGPU_DROP_M")) : 1e-2;
+  if (drop_thr > 0) {
+    DevBuf<unsigned long long> mm;
+    mm.alloc(2);
+    for (int l = 1; l < nl; ++l) {
+      const unsigned long long init[2] = {0ull, 0x7ff0000000000000ull};  // max sum |M| = 0, min K_C = +inf
+      TP_CUDA(cudaMemcpyAsync(mm.get(), init, sizeof init, cudaMemcpyHostToDevice, stream));
+      const int blocks = (int)std::min<size_t>((lv[l].n + 255) / 256, 1024);
+      k_level_shift_ratio<<<blocks, 256, 0, stream>>>(lv[l].K.get(), lv[l].M.get(), (size_t)lv[l].n, mm.get());
+      TP_LAUNCHED(this);
+      unsigned long long h[2];
+      TP_CUDA(cudaMemcpyAsync(h, mm.get(), sizeof h, cudaMemcpyDeviceToHost, stream));
+      TP_CUDA(cudaStreamSynchronize(stream));
+      double msum, kmin;
+      std::memcpy(&msum, &h[0], sizeof msum);
+      std::memcpy(&kmin, &h[1], sizeof kmin);
+      ops[l].drop_m = kmin > 0 && (2.0 / tau) * msum <= drop_thr * kmin;
+      if (std::getenv("TPGPU_DEBUG_LEVELS"))
+        std::fprintf(stderr, "level %d m %d shift ratio %.3e drop_m %d\n", l, lv[l].m, (2.0 / tau) * msum / kmin,
+                     (int)ops[l].drop_m);
+    }
+  }
   if (!K0 && !std::getenv("TPGPU_NO_STREAM_FINE")) {
     // K_hat edge weights: we[Y][X] = (nu_hat(cell(X,Y)) + nu_hat(cell(X,Y-1)))/2,
     // wn[Y][X] = (nu_hat(cell(X,Y)) + nu_hat(cell(X-1,Y)))/2 (the two triangles
@@ -667,7 +764,15 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
     // groups of `parts` chunks: group 0 on hs[0] (this thread), the others on
     // hs[g] driven by helper threads
     const int P = w.parts;
-    for (int k0 = 0; k0 < Kr; k0 += P * w.chunk) {
+    // Each group walks its block of every chunk in turn, with no barrier
+    // between chunks: a group that finishes its block of chunk c starts on
+    // chunk c+1 while the others still iterate (the lowest frequencies of
+    // chunk 0 used to hold every group at the chunk boundary).
+    // TPGPU_CHUNK_BARRIER=1 restores the per-chunk join.
+    static const bool chunk_barrier = std::getenv("TPGPU_CHUNK_BARRIER") != nullptr;
+    const int span = P * w.chunk;
+    for (int c0 = 0; c0 < Kr; c0 += chunk_barrier ? span : Kr) {
+      const int c1 = chunk_barrier ? std::min(Kr, c0 + span) : Kr;
       TP_CUDA(cudaEventRecord(w.ev_in, stream));
       for (auto h : w.hs) TP_CUDA(cudaStreamWaitEvent(h, w.ev_in, 0));
       std::vector<SolveStats> gst(P);
@@ -677,8 +782,6 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
       std::vector<double> gsec(P, 0.0);
       const auto tg0 = std::chrono::steady_clock::now();
       auto body = [&](int g) {
-        const int kg = k0 + g * w.chunk, nbg = std::min(w.chunk, Kr - kg);
-        if (nbg <= 0) return;
         static const bool tracing = std::getenv("TPGPU_TRACE") != nullptr;
         StreamTrace trace;
         try {
@@ -688,7 +791,11 @@ void Problem::periodic_solve_with(FreqWork& w, const double* in, double* out, bo
             tl_trace = &trace;
             trace_mark("start", w.hs[g]);
           }
-          git[g] = run(w.group(g), kg, nbg, &gst[g]);
+          for (int k0 = c0; k0 < c1; k0 += span) {
+            const int kg = k0 + g * w.chunk, nbg = std::min(w.chunk, Kr - kg);
+            if (nbg <= 0) break;
+            git[g] = std::max(git[g], run(w.group(g), kg, nbg, &gst[g]));
+          }
           if (tracing) {
             trace_mark("end", w.hs[g]);
             tl_trace = nullptr;
