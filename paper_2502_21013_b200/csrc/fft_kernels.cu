@@ -656,7 +656,8 @@ bool pick_shape(int n_, int p_, FwdFn& f, InvFn& g) {
 }
 bool compiled_shape(int N, int P, FwdFn& f, InvFn& g) {
   return pick_shape<64, 32>(N, P, f, g) || pick_shape<128, 16>(N, P, f, g) || pick_shape<256, 8>(N, P, f, g) ||
-         pick_shape<512, 4>(N, P, f, g) || pick_shape<1024, 4>(N, P, f, g) || pick_shape<2048, 4>(N, P, f, g) ||
+         pick_shape<512, 4>(N, P, f, g) || pick_shape<1024, 4>(N, P, f, g) || pick_shape<1024, 2>(N, P, f, g) ||
+         pick_shape<1024, 8>(N, P, f, g) || pick_shape<2048, 4>(N, P, f, g) ||
          pick_shape<4096, 2>(N, P, f, g);
 }
 

@@ -1124,7 +1124,9 @@ void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, c
     if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
     else down_t<Five, 1, 6, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   } else if (!op.M) {
-    down_t<SevenK, 1, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    static const int nb7 = env_int("TPGPU_NB7", 1);
+    if (nb7 == 2) down_t<SevenK, 2, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
+    else down_t<SevenK, 1, 2, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   } else {
     static const int ra = env_int("TPGPU_RA7", 2), w = env_int("TPGPU_WPB7", 2);
     if (ra == 4) down_t<Seven, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
@@ -1142,7 +1144,9 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
     if (ra == 4) up_t<Five, 1, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else up_t<Five, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   } else if (!op.M) {
-    up_t<SevenK, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    static const int nb7 = env_int("TPGPU_NB7", 1);
+    if (nb7 == 2) up_t<SevenK, 2, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else up_t<SevenK, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   } else {
     static const int ra = env_int("TPGPU_RA7U", 2), w = env_int("TPGPU_WPB7", 2);
     if (ra == 4) up_t<Seven, 1, 4, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);

@@ -36,6 +36,13 @@ __global__ void k_accept(double* __restrict__ Ub, double* __restrict__ Rb, const
     Rb[b * n + i] = Rt[b * n + i];
   }
 }
+// x_b *= f_b (the warm start of the next Newton step's linear solve)
+__global__ void k_scale_batches(double* __restrict__ x, const double* __restrict__ f, size_t n) {
+  const double a = f[blockIdx.y];
+  double* xb = x + (size_t)blockIdx.y * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    xb[i] *= a;
+}
 }  // namespace
 
 // Inexact Newton safeguards: the linear error's share of the
@@ -51,7 +58,7 @@ struct NewtonGroup {
   DevBuf<double> Ub, Rb, Db, Ut, Rt, inv, part, red;
   std::vector<DevBuf<double>> J;
   DevBuf<int> d_slice, d_active, d_acc, d_todo;
-  DevBuf<double> d_alpha, d_bscale;
+  DevBuf<double> d_alpha, d_bscale, d_wscale;
   BatchSolver<1> solver;
 };
 
@@ -129,6 +136,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
     g.d_todo.alloc(Sg);
     g.d_alpha.alloc(Sg);
     g.d_bscale.alloc(Sg);
+    g.d_wscale.alloc(Sg);
     std::vector<LevelOp> ops(nl);
     for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], g.J[l].get(), nullptr, false, {}};
     g.solver.init(this, ops, Sg, mc);
@@ -151,7 +159,9 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
       trace_mark("start", s);
     }
     std::vector<int> h_slice(Sb), h_active(Sb), h_acc(Sb);
-    std::vector<double> h_alpha(Sb), rnorm(Sb), scale(Sb), nrm2(Sb), h_bscale(Sb, 1.0), rprev(Sb);
+    std::vector<double> h_alpha(Sb), rnorm(Sb), scale(Sb), nrm2(Sb), h_bscale(Sb, 1.0), rprev(Sb), h_wscale(Sb);
+    std::vector<double> acc_alpha(Sb, 1.0);
+    static const bool newton_warm = std::getenv("TPGPU_NEWTON_WARM") && std::atoi(std::getenv("TPGPU_NEWTON_WARM")) != 0;
     for (int s0 = r0; s0 < r1; s0 += Sb) {
       const int nb = std::min(Sb, r1 - s0);
       for (int b = 0; b < Sb; ++b) {
@@ -215,7 +225,19 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
             TP_CUDA(cudaMemcpyAsync(g.d_bscale.get(), h_bscale.data(), Sb * sizeof(double), cudaMemcpyHostToDevice, s));
             g.solver.bscale = g.d_bscale.get();
           }
-          g.solver.solve(g.Rb.get(), g.Db.get(), nb, pass > 0, &st);
+          // warm start of a new step (TPGPU_NEWTON_WARM=1): the part of the
+          // previous direction the line search left, (1 - alpha) delta_{k-1}
+          // -- only the linear solver's initial guess changes
+          bool warm_lin = pass > 0;
+          if (pass == 0 && newton_warm && step > 1) {
+            for (int b = 0; b < Sb; ++b) h_wscale[b] = (b < nb && h_active[b]) ? 1.0 - acc_alpha[b] : 0.0;
+            TP_CUDA(cudaMemcpyAsync(g.d_wscale.get(), h_wscale.data(), Sb * sizeof(double), cudaMemcpyHostToDevice, s));
+            dim3 gw((unsigned)std::min<size_t>((n + 255) / 256, 512), Sb);
+            k_scale_batches<<<gw, 256, 0, s>>>(g.Db.get(), g.d_wscale.get(), n);
+            TP_LAUNCHED(this);
+            warm_lin = true;
+          }
+          g.solver.solve(g.Rb.get(), g.Db.get(), nb, warm_lin, &st);
           g.solver.ext_mask = nullptr;
           g.solver.bscale = nullptr;
           std::vector<int> searching(todo), refine(Sb, 0);
@@ -245,6 +267,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
                 accept[b] = 1;
                 rnorm[b] = tnorm;
                 h_acc[b] = 1;
+                acc_alpha[b] = h_alpha[b];
               } else {
                 h_alpha[b] *= cfg.armijo_backtrack;
               }
