@@ -222,9 +222,12 @@ constexpr int SD = TPGPU_SWEEP_SD;
 // thread rows per block: the 32 x 8 node tile has 33 x 9 = 297 cells, so
 // with TY thread rows 41 threads (two warps) evaluate a second cell while the
 // other six warps wait at the slice barrier; TYT = 10 rows (320 threads)
-// evaluate every cell in one round and leave two warps idle in the node pass
+// evaluate every cell in one round and leave two warps idle in the node pass,
+// but fit two blocks per SM instead of three: 45.4 vs 42.7 ms per cfg-3 sweep
+// in the ncu launch lists (profiles/r2u_*, r2o_*), level in the sweep A/B
+// (profiles/r2q_ab.txt) -- 8 rows kept
 #ifndef TPGPU_SWEEP_TYT
-#define TPGPU_SWEEP_TYT 10
+#define TPGPU_SWEEP_TYT 8
 #endif
 constexpr int TYT = TPGPU_SWEEP_TYT;
 constexpr int SNT = TX * TYT;  // threads per block
