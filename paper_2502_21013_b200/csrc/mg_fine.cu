@@ -145,6 +145,39 @@ __device__ __forceinline__ void cp_wait() {
   asm volatile("cp.async.wait_group %0;\n" ::"n"(N) : "memory");
 }
 
+// ---- bulk row staging (TMA engine, cp.async.bulk -> UBLKCP): one elected
+// lane copies a warp's whole row segment of a vector (up to 32 x 16 bytes,
+// complex rows are 16-byte aligned) into its ring slot and the slot's
+// mbarrier counts the bytes in; the lanes wait on the barrier's phase.
+// resident 128-thread blocks per SM the bulk-staged passes are bounded for
+// (3: <= 168 registers, the cp.async passes' occupancy)
+#ifndef TPGPU_BULK_MINB
+#define TPGPU_BULK_MINB 3
+#endif
+__device__ __forceinline__ unsigned smem_u32(const void* p) { return (unsigned)__cvta_generic_to_shared(p); }
+__device__ __forceinline__ void mbar_init(uint64_t* b) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;\n" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint64_t* b, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n" ::"r"(smem_u32(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, unsigned parity) {
+  asm volatile(
+      "{\n\t.reg .pred P1;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n\t"
+      "@!P1 bra WAIT_%=;\n}\n" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* sdst, const void* g, unsigned bytes, uint64_t* b) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n" ::"r"(
+                   smem_u32(sdst)),
+               "l"(g), "r"(bytes), "r"(smem_u32(b))
+               : "memory");
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.shared::cta;\n" ::: "memory"); }
+
 template <class T, int NV>
 struct VRowT {  // NV values per lane of one staged row
   T v[NV][WL];
@@ -511,8 +544,8 @@ __device__ __forceinline__ ItemNB<WPBK, NB> item_nb(int m, int own, int rh, int 
 // right-hand side is r_new = r - alpha q (read r and q, write r_new to rout
 // for the owned rows, partial ||r_new||^2 per warp item), replacing the
 // separate x/r update pass (x is updated in the next apply).
-template <class S, int NB, int RA, int WPBK, bool FUSED = false>
-__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(FineOp op, const typename S::T* __restrict__ rv,
+template <class S, int NB, int RA, int WPBK, bool FUSED = false, bool BULK = false>
+__global__ void __launch_bounds__(WL * WPBK, BULK ? TPGPU_BULK_MINB : TP_MINB_S(S, WPBK)) k_stream_down(FineOp op, const typename S::T* __restrict__ rv,
                                                                          typename S::T* __restrict__ z2out,
                                                                          typename S::T* __restrict__ bc, int mc,
                                                                          int rh, const int* __restrict__ active,
@@ -535,6 +568,21 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
   VRowT<T, NVV>* const vring = reinterpret_cast<VRowT<T, NVV>*>(fine_smem) + wib * RV;
   WRow<S::NW>* const wring =
       reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRowT<T, NVV>)) + wib * RC;
+  // BULK: the warp's vector-row segments come in by cp.async.bulk, one
+  // mbarrier per vector ring slot (after the coefficient rings)
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(fine_smem + WPBK * RV * sizeof(VRowT<T, NVV>) +
+                                                     WPBK * RC * sizeof(WRow<S::NW>)) + wib * RV;
+  const int blo = max(0, H - it.xs);                        // first lane with a column in [0, m)
+  const int bhi = min(WL, m - (it.xs - H));                 // one past the last
+  const unsigned bbytes = bhi > blo ? (unsigned)(bhi - blo) * (unsigned)sizeof(T) : 0u;
+  unsigned bpar = 0, bpend = 0;  // per slot: parity of the last issued phase, issued-not-waited
+  if constexpr (BULK) {
+    if (lane == 0) {
+      for (int q = 0; q < RV; ++q) mbar_init(&bars[q]);
+      fence_proxy_async();
+    }
+    __syncwarp();
+  }
   const T* const qp = FUSED ? qv + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
   T* const ro = FUSED ? rout + (size_t)it.b[0] * op.n + min(max(it.xs - H + lane, 0), op.m - 1) : nullptr;
   T al{};
@@ -584,9 +632,29 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
     if (TPGPU_ISSUE_ALWAYS || yr <= ylast) {
       const bool rowok = (unsigned)yr < (unsigned)m, rin = colok && rowok;
       const unsigned off = (unsigned)min(max(yr, 0), m - 1) * (unsigned)m;
+      if constexpr (BULK) {
+        __syncwarp();  // every lane's reads of the slot (two rows ago) precede the refill
+        if (lane == 0) {
+          // the first staged row's vectors are never read: arrive without bytes
+          const unsigned by = (rowok && yr != y0) ? bbytes : 0u;
+          fence_proxy_async();  // the slot's earlier generic reads before the async writes
+          mbar_expect(&bars[vi], by * NVV);
+          if (by) {
+            // lane blo's pointer is the segment start (rp / qp are per-lane column pointers)
+            const size_t seg = (size_t)yr * m + (size_t)(it.xs - H + blo);
 #pragma unroll
-      for (int j = 0; j < NB; ++j) cpv(&vring[vi].v[j][lane], rp[j] + off, rin);
-      if (FUSED) cpv(&vring[vi].v[1][lane], qp + off, rin);
+            for (int j = 0; j < NB; ++j)
+              bulk_g2s(&vring[vi].v[j][blo], rv + (size_t)it.b[j] * op.n + seg, by, &bars[vi]);
+            if (FUSED) bulk_g2s(&vring[vi].v[1][blo], qv + (size_t)it.b[0] * op.n + seg, by, &bars[vi]);
+          }
+        }
+        bpar ^= 1u << vi;
+        bpend |= 1u << vi;
+      } else {
+#pragma unroll
+        for (int j = 0; j < NB; ++j) cpv(&vring[vi].v[j][lane], rp[j] + off, rin);
+        if (FUSED) cpv(&vring[vi].v[1][lane], qp + off, rin);
+      }
       S::stage(wring[wi], src, lane, yr, off, rowok);
       vi = wrap_inc(vi, RV);
       wi = wrap_inc(wi, RC);
@@ -622,6 +690,11 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
     if (S::XLANE) __syncwarp();
+    if constexpr (BULK) {
+      // the phase issued last for this slot: parity bit before that issue's flip
+      mbar_wait(&bars[vr], ((bpar >> vr) & 1u) ^ 1u);
+      bpend &= ~(1u << vr);
+    }
     k2 = k1; k1 = k0;
     k0 = S::load(wring[sr], lane, k1);
     const bool in0 = colok && (unsigned)yi < (unsigned)m;
@@ -630,9 +703,11 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
     const bool st1 = own && yi - 1 >= ys && yi - 1 < ye;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = vring[vr].v[j][lane];
+      // (BULK: lanes off the grid and rows off the grid read zero, the bulk
+      // copy fills only the segment inside it)
+      r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = (!BULK || in0) ? vring[vr].v[j][lane] : T{};
       if (FUSED) {
-        const T qq = vring[vr].v[1][lane];
+        const T qq = (!BULK || in0) ? vring[vr].v[1][lane] : T{};
         r0[j] = r0[j] - cm(al, qq);
         if (own && yi >= ys && yi < ye) {
           ro[(long)yi * m] = r0[j];
@@ -678,6 +753,11 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
     }
   }
   cp_wait<0>();
+  if constexpr (BULK) {
+    // copies issued but never consumed (the first staged row) land before exit
+    for (int q = 0; q < RV; ++q)
+      if ((bpend >> q) & 1u) mbar_wait(&bars[q], ((bpar >> q) & 1u) ^ 1u);
+  }
   if (FUSED) {
     double zz = 0;
     warp_pair(rn2, zz);
@@ -694,8 +774,8 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_down(F
 //   zc = z2 + P x_c ; z3, z4 = two Jacobi steps ; writes z4 (+ partial r^T z4)
 // Staged per row and frequency: r, z2 and the (up to two) coarse values P x_c
 // interpolates from at the lane's node; the coefficient row once.
-template <class S, int NB, int RA, int WPBK>
-__global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(FineOp op, const typename S::T* __restrict__ rv,
+template <class S, int NB, int RA, int WPBK, bool BULK = false>
+__global__ void __launch_bounds__(WL * WPBK, BULK ? TPGPU_BULK_MINB : TP_MINB_S(S, WPBK)) k_stream_up(FineOp op, const typename S::T* __restrict__ rv,
                                                                        const typename S::T* __restrict__ z2in,
                                                                        const typename S::T* __restrict__ xcv, int mc,
                                                                        int rh, typename S::T* __restrict__ zout,
@@ -714,6 +794,20 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
   VRowT<T, 4 * NB>* const vring = reinterpret_cast<VRowT<T, 4 * NB>*>(fine_smem) + wib * RV;
   WRow<S::NW>* const wring =
       reinterpret_cast<WRow<S::NW>*>(fine_smem + WPBK * RV * sizeof(VRowT<T, 4 * NB>)) + wib * RC;
+  // BULK: r and z2 rows by cp.async.bulk (the coarse values are gathered per lane)
+  uint64_t* const bars = reinterpret_cast<uint64_t*>(fine_smem + WPBK * RV * sizeof(VRowT<T, 4 * NB>) +
+                                                     WPBK * RC * sizeof(WRow<S::NW>)) + wib * RV;
+  const int blo = max(0, H - it.xs);
+  const int bhi = min(WL, m - (it.xs - H));
+  const unsigned bbytes = bhi > blo ? (unsigned)(bhi - blo) * (unsigned)sizeof(T) : 0u;
+  unsigned bpar = 0, bpend = 0;
+  if constexpr (BULK) {
+    if (lane == 0) {
+      for (int q = 0; q < RV; ++q) mbar_init(&bars[q]);
+      fence_proxy_async();
+    }
+    __syncwarp();
+  }
   const int x = it.xs - H + lane;
   const bool colok = x >= 0 && x < m;
   const bool own = lane >= H && lane < WL - H && colok;
@@ -755,10 +849,30 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
       const bool ok2 = rin && has2 && cA2 && B2 >= 1 && B2 <= mc;
       const unsigned c1 = ok1 ? (bh - 1) * mc + (ah - 1) : 0, c2 = ok2 ? (B2 - 1) * mc + (A2 - 1) : 0;
       VRowT<T, 4 * NB>& sv = vring[vi];
+      if constexpr (BULK) {
+        __syncwarp();
+        if (lane == 0) {
+          const unsigned by = (rowok && yr != y0) ? bbytes : 0u;
+          fence_proxy_async();
+          mbar_expect(&bars[vi], by * 2 * NB);
+          if (by) {
+            const size_t seg = (size_t)yr * m + (size_t)(it.xs - H + blo);
+#pragma unroll
+            for (int j = 0; j < NB; ++j) {
+              bulk_g2s(&sv.v[4 * j][blo], rv + (size_t)it.b[j] * op.n + seg, by, &bars[vi]);
+              bulk_g2s(&sv.v[4 * j + 1][blo], z2in + (size_t)it.b[j] * op.n + seg, by, &bars[vi]);
+            }
+          }
+        }
+        bpar ^= 1u << vi;
+        bpend |= 1u << vi;
+      }
 #pragma unroll
       for (int j = 0; j < NB; ++j) {
-        cpv(&sv.v[4 * j][lane], rp[j] + off, rin);
-        cpv(&sv.v[4 * j + 1][lane], zp[j] + off, rin);
+        if constexpr (!BULK) {
+          cpv(&sv.v[4 * j][lane], rp[j] + off, rin);
+          cpv(&sv.v[4 * j + 1][lane], zp[j] + off, rin);
+        }
         cpv(&sv.v[4 * j + 2][lane], xb[j] + c1, ok1);
         cpv(&sv.v[4 * j + 3][lane], xb[j] + c2, ok2);
       }
@@ -794,18 +908,24 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
     sr = wrap_inc(sr, RC);
     cp_wait<RA>();
     if (S::XLANE) __syncwarp();
+    if constexpr (BULK) {
+      mbar_wait(&bars[vr], ((bpar >> vr) & 1u) ^ 1u);
+      bpend &= ~(1u << vr);
+    }
     const VRowT<T, 4 * NB>& sv = vring[vr];
     const double wc1 = (!ao && !((yi + 1) & 1)) ? 1.0 : 0.5;
     k2 = k1; k1 = k0;
     k0 = S::load(wring[sr], lane, k1);
     const bool in1 = colok && (unsigned)(yi - 1) < (unsigned)m;
+    const bool in0 = colok && (unsigned)yi < (unsigned)m;
     const bool st2 = own && yi - 2 >= ys && yi - 2 < ye;
 #pragma unroll
     for (int j = 0; j < NB; ++j) {
-      const T zz = sv.v[4 * j + 1][lane], x1 = sv.v[4 * j + 2][lane], x2 = sv.v[4 * j + 3][lane];
+      const T zz = (!BULK || in0) ? sv.v[4 * j + 1][lane] : T{}, x1 = sv.v[4 * j + 2][lane],
+              x2 = sv.v[4 * j + 3][lane];
       const T ccur = fmav(wc1, x1, fmav(0.5, x2, zz));
       c2[j] = c1[j]; c1[j] = c0[j]; c0[j] = ccur;
-      r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = sv.v[4 * j][lane];
+      r2[j] = r1[j]; r1[j] = r0[j]; r0[j] = (!BULK || in0) ? sv.v[4 * j][lane] : T{};
       // z3 at row yi-1
       e3[j] = e2[j]; e2[j] = e1[j];
       {
@@ -830,6 +950,10 @@ __global__ void __launch_bounds__(WL * WPBK, TP_MINB_S(S, WPBK)) k_stream_up(Fin
     }
   }
   cp_wait<0>();
+  if constexpr (BULK) {
+    for (int q = 0; q < RV; ++q)
+      if ((bpend >> q) & 1u) mbar_wait(&bars[q], ((bpar >> q) & 1u) ^ 1u);
+  }
   if (dot) {
     const int ns = (m + OWN - 1) / OWN, nch = (m + rh - 1) / rh;
     const size_t per = (size_t)ns * nch;
@@ -1025,34 +1149,34 @@ int env_int(const char* name, int dflt) {
   return v ? std::atoi(v) : dflt;
 }
 
-template <class S, int NB, int RA, int WPBK, bool FUSED = false, class T = typename S::T>
+template <class S, int NB, int RA, int WPBK, bool FUSED = false, bool BULK = false, class T = typename S::T>
 void down_t(Problem& p, const FineOp& op, const T* r, T* z2, T* bc, int mc, const int* active, double om1,
             double om2, int nb, const T* q = nullptr, const T* alpha = nullptr, T* rout = nullptr,
             double* part = nullptr, const ScalFuse* sf = nullptr) {
-  constexpr size_t sm = ring_smem<S, FUSED ? 2 : NB, RA, WPBK>();
+  constexpr size_t sm = ring_smem<S, FUSED ? 2 : NB, RA, WPBK>() + (BULK ? (size_t)WPBK * (RA + 2) * 8 : 0);
   static bool attrs = [] {
-    cudaFuncSetAttribute(k_stream_down<S, NB, RA, WPBK, FUSED>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_stream_down<S, NB, RA, WPBK, FUSED, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          (int)sm);
     return true;
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  launch_pdl(k_stream_down<S, NB, RA, WPBK, FUSED>, grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK),
+  launch_pdl(k_stream_down<S, NB, RA, WPBK, FUSED, BULK>, grid_for(op.m, 26, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK),
              sm, p.cur_stream(), op, r, z2, bc, mc, rh, active, om1, om2, nb, q, alpha, rout, part,
              sf ? *sf : ScalFuse{});
 }
 
-template <class S, int NB, int RA, int WPBK, class T = typename S::T>
+template <class S, int NB, int RA, int WPBK, bool BULK = false, class T = typename S::T>
 void up_t(Problem& p, const FineOp& op, const T* r, const T* z2, const T* xc, int mc, T* z, const int* active,
           double om1, double om2, int nb, int dot, double* part) {
-  constexpr size_t sm = ring_smem<S, 4 * NB, RA, WPBK>();
+  constexpr size_t sm = ring_smem<S, 4 * NB, RA, WPBK>() + (BULK ? (size_t)WPBK * (RA + 2) * 8 : 0);
   static bool attrs = [] {
-    cudaFuncSetAttribute(k_stream_up<S, NB, RA, WPBK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    cudaFuncSetAttribute(k_stream_up<S, NB, RA, WPBK, BULK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     return true;
   }();
   (void)attrs;
   const int rh = rh_for(op.m);
-  launch_pdl(k_stream_up<S, NB, RA, WPBK>, grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK), sm,
+  launch_pdl(k_stream_up<S, NB, RA, WPBK, BULK>, grid_for(op.m, 28, (nb + NB - 1) / NB, rh, WPBK), dim3(WL * WPBK), sm,
              p.cur_stream(), op, r, z2, xc, mc, rh, z, active, om1, om2, nb, dot, part);
 }
 
@@ -1118,7 +1242,10 @@ void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, c
                         const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
                         cplx* rout, double* part, const ScalFuse* sf) {
   if (op.we && q) {
-    down_t<Five, 1, 6, 4, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part, sf);
+    // vector rows by bulk copies (TPGPU_BULK=0: per-lane cp.async)
+    static const int bulk = env_int("TPGPU_BULK", 1);
+    if (bulk) down_t<Five, 1, 6, 4, true, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part, sf);
+    else down_t<Five, 1, 6, 4, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part, sf);
   } else if (op.we) {
     static const int ra = env_int("TPGPU_RA5", 6);
     if (ra == 4) down_t<Five, 1, 4, 4>(p, op, r, z2, bc, mc, active, om1, om2, nb);
@@ -1141,7 +1268,9 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
   if (op.we) {
     static const int ra = env_int("TPGPU_RA5U", 2);
+    static const int bulk = env_int("TPGPU_BULK", 1);
     if (ra == 4) up_t<Five, 1, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+    else if (bulk) up_t<Five, 1, 2, 4, true>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else up_t<Five, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   } else if (!op.M) {
     static const int nb7 = env_int("TPGPU_NB7", 1);
