@@ -1242,8 +1242,12 @@ void launch_stream_down(Problem& p, const FineOp& op, const cplx* r, cplx* z2, c
                         const int* active, double om1, double om2, int nb, const cplx* q, const cplx* alpha,
                         cplx* rout, double* part, const ScalFuse* sf) {
   if (op.we && q) {
-    // vector rows by bulk copies (TPGPU_BULK=0: per-lane cp.async)
-    static const int bulk = env_int("TPGPU_BULK", 1);
+    // vector rows by bulk copies (TPGPU_BULK=1; measured slower than the
+    // per-lane cp.async rings: cfg 3 302-304 vs 294 ms per sweep, cfg 1 3.14
+    // vs 2.89 ms, the fine down / up passes 82 / 64 vs 73 / 60 ms of kernel,
+    // profiles/r2z_ab.txt -- one lane issuing after a __syncwarp and the
+    // mbarrier wait sit on each row's critical path; default off)
+    static const int bulk = env_int("TPGPU_BULK", 0);
     if (bulk) down_t<Five, 1, 6, 4, true, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part, sf);
     else down_t<Five, 1, 6, 4, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part, sf);
   } else if (op.we) {
@@ -1268,7 +1272,7 @@ void launch_stream_up(Problem& p, const FineOp& op, const cplx* r, const cplx* z
                       cplx* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
   if (op.we) {
     static const int ra = env_int("TPGPU_RA5U", 2);
-    static const int bulk = env_int("TPGPU_BULK", 1);
+    static const int bulk = env_int("TPGPU_BULK", 0);
     if (ra == 4) up_t<Five, 1, 4, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else if (bulk) up_t<Five, 1, 2, 4, true>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
     else up_t<Five, 1, 2, 4>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);

@@ -252,6 +252,7 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
   __shared__ double cnu0[TY + 1][TX + 1], cdnu[TY + 1][TX + 1], cbs2[TY + 1][TX + 1], chat[TY + 1][TX + 1];
   __shared__ double wnu[2][2][TY + 1][TX + 1];  // nu_T / 2 (T1, T2 per cell) of two slices
   __shared__ double red[32];
+  __shared__ double stime[SB * TP_MAX_MATERIALS];  // source amplitudes of the block's slices
   const size_t n = (size_t)m * m;
   const size_t nl = (size_t)rows * m;
   const int tx = threadIdx.x, ty = threadIdx.y, tid = ty * TX + tx;
@@ -288,16 +289,24 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
       }
     }
   }
+  // staged element pointers at slice sbeg, advanced by one slice per issue
+  // (issue is called for consecutive slices)
+  const double* sp0 = sok[0] ? sb[0] + (size_t)sbeg * sstr[0] : U;
+  const double* sp1 = sok[1] ? sb[1] + (size_t)sbeg * sstr[1] : U;
+  const size_t sst0 = sok[0] ? sstr[0] : 0, sst1 = sok[1] ? sstr[1] : 0;
   auto issue = [&](int sl) {
     if (sl < send) {
       double(*t)[TX + 2] = su[sl % SD];
-      cp_async8(&t[sly[0]][slx[0]], sok[0] ? sb[0] + (size_t)sl * sstr[0] : U, sok[0]);
-      if (k1 < TN) cp_async8(&t[sly[1]][slx[1]], sok[1] ? sb[1] + (size_t)sl * sstr[1] : U, sok[1]);
+      cp_async8(&t[sly[0]][slx[0]], sp0, sok[0]);
+      if (k1 < TN) cp_async8(&t[sly[1]][slx[1]], sp1, sok[1]);
+      sp0 += sst0;
+      sp1 += sst1;
     }
     asm volatile("cp.async.commit_group;\n" ::: "memory");
   };
 #pragma unroll
   for (int j = 0; j < SD - 1; ++j) issue(sbeg + j);
+  for (int k = tid; k < (send - sbeg) * nsrc; k += SNT) stime[k] = src_time[(size_t)sbeg * nsrc + k];
   // per-cell material constants of the tile (+ halo cells)
   for (int k = tid; k < (TY + 1) * (TX + 1); k += SNT) {
     const int ly = k / (TX + 1), lx = k % (TX + 1);
@@ -326,7 +335,8 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
   for (int r = 0; r < TP_MAX_MATERIALS; ++r) prof[r] = (own && r < nsrc) ? src_prof[r * n + i] : 0.0;
   double uprev = 0;
   if (own && mi != 0) uprev = U[(size_t)((sbeg + N - 1) % N) * nl + il];
-  const double c2 = (double)c * (double)c;
+  double* gp = WANT_G ? G + (size_t)sbeg * nl + il : nullptr;
+  const double inv_c2 = 1.0 / ((double)c * (double)c);
   // slice-invariant operands in registers: the material law of this thread's
   // cells (cell pass) and nu_hat / 2 of the node's six incident triangles
   constexpr int NCELL = (TY + 1) * (TX + 1);
@@ -338,9 +348,10 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
     const int k = e == 0 ? kc0 : kc1;
     const int cy = k / (TX + 1), cx = k - cy * (TX + 1);
     const bool ok = k < NCELL;
-    cl[e][0] = ok ? cdnu[cy][cx] : 0.0;
-    cl[e][1] = ok ? cbs2[cy][cx] : 1.0;
-    cl[e][2] = ok ? cnu0[cy][cx] : 0.0;
+    // folded: nu/2 = (dnu/2) q / (q + Bs^2/c^2) + nu0/2 with q = |grad u|^2 / c^2
+    cl[e][0] = ok ? 0.5 * cdnu[cy][cx] : 0.0;
+    cl[e][1] = ok ? cbs2[cy][cx] * inv_c2 : 1.0;
+    cl[e][2] = ok ? 0.5 * cnu0[cy][cx] : 0.0;
   }
   const int cxs[6] = {0, 0, -1, -1, -1, 0}, cys[6] = {0, 0, 0, -1, -1, -1};
   double hat[6];
@@ -363,9 +374,9 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
         const int cy = k / (TX + 1), cx = k - cy * (TX + 1);
         const double u00 = t[cy][cx], u10 = t[cy][cx + 1], u01 = t[cy + 1][cx], u11 = t[cy + 1][cx + 1];
         const double ax = u10 - u00, ay = u11 - u10, bx = u11 - u01, by = u01 - u00;
-        const double sa = c2 * (ax * ax + ay * ay), sb2 = c2 * (bx * bx + by * by);
-        w[0][cy][cx] = 0.5 * fma(cl[e][0], sa * acc_rcp(sa + cl[e][1]), cl[e][2]);
-        w[1][cy][cx] = 0.5 * fma(cl[e][0], sb2 * acc_rcp(sb2 + cl[e][1]), cl[e][2]);
+        const double qa = fma(ax, ax, ay * ay), qb = fma(bx, bx, by * by);
+        w[0][cy][cx] = fma(cl[e][0], qa * acc_rcp(qa + cl[e][1]), cl[e][2]);
+        w[1][cy][cx] = fma(cl[e][0], qb * acc_rcp(qb + cl[e][1]), cl[e][2]);
       }
     }
   };
@@ -397,8 +408,11 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
       double f = 0;
 #pragma unroll
       for (int r = 0; r < TP_MAX_MATERIALS; ++r)
-        if (r < nsrc) f = fma(src_time[s * nsrc + r], prof[r], f);
-      if (WANT_G) G[(size_t)s * nl + il] = f + kh - ku;
+        if (r < nsrc) f = fma(stime[(s - sbeg) * nsrc + r], prof[r], f);
+      if (WANT_G) {
+        *gp = f + kh - ku;
+        gp += nl;
+      }
       const double mdu = mi != 0 ? mi * ((uC - uprev) * inv_tau) : 0.0;
       const double res = f - mdu - ku;
       r2 = fma(res, res, r2);
