@@ -1087,6 +1087,27 @@ __global__ void k_dense_inverse(const double* __restrict__ K, const double* __re
 
 }  // namespace
 
+namespace {
+__global__ void k_planes_f32(const double* __restrict__ K, float* __restrict__ Kf, size_t n) {
+  const int b = blockIdx.y;
+  const double* Kb = K + (size_t)b * 7 * n;
+  float* Fb = Kf + (size_t)b * 4 * n;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    Fb[i] = (float)Kb[(size_t)SC * n + i];
+    Fb[n + i] = (float)Kb[(size_t)SE_ * n + i];
+    Fb[2 * n + i] = (float)Kb[(size_t)SN_ * n + i];
+    Fb[3 * n + i] = (float)Kb[(size_t)SNE * n + i];
+  }
+}
+}  // namespace
+
+void launch_planes_f32(Problem& p, const double* K, int m, float* Kf, int batches) {
+  const size_t n = (size_t)m * m;
+  const dim3 g((unsigned)std::min<size_t>((n + 255) / 256, 1024), batches);
+  k_planes_f32<<<g, 256, 0, p.cur_stream()>>>(K, Kf, n);
+  TP_LAUNCHED(&p);
+}
+
 void launch_rap(Problem& p, const double* Af, int mf, double* Ac, int mc, int batches) {
   const size_t nc = (size_t)mc * mc;
   dim3 grid((unsigned)((nc + 127) / 128), batches);
@@ -1392,6 +1413,8 @@ typename BatchSolver<MODE>::T* BatchSolver<MODE>::vcycle_generic(int l, int nb, 
       FineOp so;
       so.K = ops[l].K;
       so.kstride = (size_t)7 * ops[l].n;
+      so.Kf = ops[l].Kf;
+      so.kfstride = (size_t)4 * ops[l].n;
       so.m = ops[l].m;
       so.n = ops[l].n;
       launch_stream_down(*p, so, bl, z2, lb[l + 1].get(), ops[l + 1].m, act, cfg.omega, cfg.omega2, nb);

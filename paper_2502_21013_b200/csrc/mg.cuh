@@ -51,6 +51,8 @@ struct FineOp {
   const double* K = nullptr;      // Galerkin levels: 7n (slice mode: per-slice Jacobians, stride kstride)
   const double* M = nullptr;      // Galerkin levels: 7n
   size_t kstride = 0;             // slice mode: coefficients per batch (7n)
+  const float* Kf = nullptr;      // slice mode: fp32 C/E/N/NE planes for the V-cycle passes (optional)
+  size_t kfstride = 0;            // floats per batch (4n)
   const cplx* lam = nullptr;      // per batch symbol
   int m = 0, c = 0, n = 0;
   int rha = 32;                   // rows per warp item of the apply pass (set at launch, rha_for)
@@ -97,6 +99,7 @@ struct LevelOp {
   const double* M = nullptr;  // freq only
   bool five = false;          // freq mode: K 5-point and M diagonal (fine level)
   FineOp fine;                // freq mode level 0: streaming kernels (we != nullptr)
+  const float* Kf = nullptr;  // slice mode: fp32 copies of the C/E/N/NE planes (4n per batch) for the V-cycle
   bool drop_m = false;        // freq mode Galerkin level: the V-cycle's level operator is K alone
                               // (max |lambda| M negligible against K, Problem::build_freq_work)
 };
@@ -158,6 +161,9 @@ struct BatchSolver {
   T* fine_rest0(int nb, const T* bl, bool dot);
 };
 
+// fp32 copies of the C/E/N/NE planes of `batches` 7-point stencils (stride 7n
+// -> 4n floats per batch)
+void launch_planes_f32(Problem& p, const double* K, int m, float* Kf, int batches);
 // Galerkin coarse stencil Ac = P^T Af P for `batches` stencils (stride 7n).
 void launch_rap(Problem& p, const double* Af, int mf, double* Ac, int mc, int batches);
 // Dense inverse of the coarsest operator per batch.

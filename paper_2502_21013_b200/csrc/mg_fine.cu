@@ -139,6 +139,10 @@ __device__ __forceinline__ void cp8(void* sdst, const void* g, bool ok) {
   const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 8 : 0) : "memory");
 }
+__device__ __forceinline__ void cp4(void* sdst, const void* g, bool ok) {
+  const unsigned sa = (unsigned)__cvta_generic_to_shared(sdst);
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;\n" ::"r"(sa), "l"(g), "r"(ok ? 4 : 0) : "memory");
+}
 __device__ __forceinline__ void cp_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 template <int N>
 __device__ __forceinline__ void cp_wait() {
@@ -390,17 +394,23 @@ struct SevenK {
 
 // slice mode (static_init Newton): per-slice symmetric 7-point Jacobians J_b
 // (planes C, E, N, NE of the 7n-per-slice stencil), real vectors
-struct SevenJ {
+// C = double: the Jacobian planes as assembled; C = float: single-precision
+// copies of the four planes (FineOp::Kf, 4n floats per slice) for the V-cycle
+// passes -- the preconditioner reads half the coefficient bytes, the PCG
+// operator (the tile apply) keeps the fp64 Jacobian
+template <class C>
+struct SevenJT {
   using T = double;
   static constexpr int NW = 4;  // J C E N NE
   struct Src {
-    const double* J;  // lane column base of this slice's stencil
+    const C* J;  // lane column base of this slice's stencil
     unsigned n;
     bool col;
   };
   static __device__ __forceinline__ Src src(const FineOp& op, int x, int xc, int, int b) {
     Src s;
-    s.J = op.K + (size_t)b * op.kstride + xc;
+    if constexpr (std::is_same_v<C, float>) s.J = op.Kf + (size_t)b * op.kfstride + xc;
+    else s.J = op.K + (size_t)b * op.kstride + xc;
     s.n = (unsigned)op.n;
     s.col = x >= 0 && x < op.m;
     return s;
@@ -408,9 +418,19 @@ struct SevenJ {
   static __device__ __forceinline__ void stage(WRow<NW>& st, const Src& s, int lane, int, unsigned moff,
                                                bool rowok) {
     const bool v = s.col && rowok;
-    const int dirs[4] = {SC, SE_, SN_, SNE};
+    if constexpr (std::is_same_v<C, float>) {
 #pragma unroll
-    for (int q = 0; q < 4; ++q) cp8(&st.w[q][lane], s.J + (dirs[q] * s.n + moff), v);
+      for (int q = 0; q < 4; ++q) cp4(&st.w[q][lane], s.J + (q * s.n + moff), v);
+    } else {
+      const int dirs[4] = {SC, SE_, SN_, SNE};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) cp8(&st.w[q][lane], s.J + (dirs[q] * s.n + moff), v);
+    }
+  }
+  // coefficient q of lane ln from a staged row (floats sit in the first half of the slot)
+  static __device__ __forceinline__ double cf(const WRow<NW>& r, int q, int ln) {
+    if constexpr (std::is_same_v<C, float>) return (double)*reinterpret_cast<const float*>(&r.w[q][ln]);
+    else return r.w[q][ln];
   }
   static constexpr int RETAIN = 3;
   static constexpr bool XLANE = true;
@@ -423,7 +443,7 @@ struct SevenJ {
     return {&st, below.p, lane};
   }
   static __device__ __forceinline__ Reg first(const WRow<NW>& st, int lane) { return {&st, &st, lane}; }
-  static __device__ __forceinline__ double diag(const Reg& y, cplx) { return y.p->w[0][y.lane]; }
+  static __device__ __forceinline__ double diag(const Reg& y, cplx) { return cf(*y.p, 0, y.lane); }
   // the smoother's diagonal: the l1 row sum sum_j |J_ij| (TPGPU_SLICE_L1, mg.cuh)
   // -- D_l1^-1 J has its spectrum in (0, 1] for any SPD J, so the Chebyshev
   // pair of weights is safe despite the anisotropic rank-one Jacobian term
@@ -432,8 +452,8 @@ struct SevenJ {
     const int ln = y.lane, lw = ln > 0 ? ln - 1 : 0;
     const WRow<NW>& a = *y.p;
     const WRow<NW>& b = *y.pb;
-    return fabs(d) + fabs(a.w[1][ln]) + fabs(a.w[1][lw]) + fabs(a.w[2][ln]) + fabs(b.w[2][ln]) + fabs(a.w[3][ln]) +
-           fabs(b.w[3][lw]);
+    return fabs(d) + fabs(cf(a, 1, ln)) + fabs(cf(a, 1, lw)) + fabs(cf(a, 2, ln)) + fabs(cf(b, 2, ln)) +
+           fabs(cf(a, 3, ln)) + fabs(cf(b, 3, lw));
 #else
     return d;
 #endif
@@ -444,11 +464,13 @@ struct SevenJ {
     const double vw = shf_up(v), ve = shf_dn(v), vne = shf_dn(vn), vsw = shf_up(vs);
     const WRow<NW>& a = *y.p;
     const WRow<NW>& b = *y.pb;
-    const double off = a.w[1][ln] * ve + a.w[1][lw] * vw + a.w[2][ln] * vn + b.w[2][ln] * vs + a.w[3][ln] * vne +
-                       b.w[3][lw] * vsw;
+    const double off = cf(a, 1, ln) * ve + cf(a, 1, lw) * vw + cf(a, 2, ln) * vn + cf(b, 2, ln) * vs +
+                       cf(a, 3, ln) * vne + cf(b, 3, lw) * vsw;
     return fma(d, v, off);
   }
 };
+using SevenJ = SevenJT<double>;
+using SevenJF = SevenJT<float>;
 
 template <class S, int NV, int RA, int WPBK>
 constexpr size_t ring_smem() {
@@ -1297,6 +1319,8 @@ void launch_stream_down(Problem& p, const FineOp& op, const double* r, double* z
                         double* rout, double* part) {
   if (q)
     down_t<SevenJ, 1, 4, 2, true>(p, op, r, z2, bc, mc, active, om1, om2, nb, q, alpha, rout, part);
+  else if (op.Kf)
+    down_t<SevenJF, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   else
     down_t<SevenJ, 1, 4, 2>(p, op, r, z2, bc, mc, active, om1, om2, nb);
   TP_LAUNCHED(&p);
@@ -1304,7 +1328,8 @@ void launch_stream_down(Problem& p, const FineOp& op, const double* r, double* z
 
 void launch_stream_up(Problem& p, const FineOp& op, const double* r, const double* z2, const double* xc, int mc,
                       double* z, const int* active, double om1, double om2, int nb, int dot, double* part) {
-  up_t<SevenJ, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+  if (op.Kf) up_t<SevenJF, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
+  else up_t<SevenJ, 1, 2, 2>(p, op, r, z2, xc, mc, z, active, om1, om2, nb, dot, part);
   TP_LAUNCHED(&p);
 }
 

@@ -57,6 +57,7 @@ struct NewtonGroup {
   int S = 0;  // slices per batch
   DevBuf<double> Ub, Rb, Db, Ut, Rt, inv, part, red;
   std::vector<DevBuf<double>> J;
+  std::vector<DevBuf<float>> Jf;  // fp32 C/E/N/NE planes of the non-coarsest levels (V-cycle passes)
   DevBuf<int> d_slice, d_active, d_acc, d_todo;
   DevBuf<double> d_alpha, d_bscale, d_wscale;
   BatchSolver<1> solver;
@@ -73,7 +74,7 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   const int nl = (int)ms.size();
   const int nL = ms.back() * ms.back();
   size_t per_slice = 0;  // bytes
-  for (int l = 0; l < nl; ++l) per_slice += (size_t)ms[l] * ms[l] * 8 * (7 + 3);
+  for (int l = 0; l < nl; ++l) per_slice += (size_t)ms[l] * ms[l] * (8 * (7 + 3) + 4 * 4);
   per_slice += (size_t)n * 8 * 9 + (size_t)nL * nL * 8;
   size_t free_b = 0, total_b = 0;
   TP_CUDA(cudaMemGetInfo(&free_b, &total_b));
@@ -121,6 +122,11 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   }
   const bool forcing = f_gamma > 0;
 
+  // fp32 copies of the Jacobian planes for the V-cycle passes (the PCG
+  // operator stays fp64; only the preconditioner reads rounded coefficients;
+  // TPGPU_NEWTON_F32=0: fp64 planes)
+  const bool f32_planes = !std::getenv("TPGPU_NEWTON_F32") || std::atoi(std::getenv("TPGPU_NEWTON_F32")) != 0;
+
   std::vector<std::unique_ptr<NewtonGroup>> groups(G);
   for (auto& gp : groups) {
     gp = std::make_unique<NewtonGroup>();
@@ -129,6 +135,10 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
     for (auto* b : {&g.Ub, &g.Rb, &g.Db, &g.Ut, &g.Rt}) b->alloc((size_t)Sg * n);
     g.J.resize(nl);
     for (int l = 0; l < nl; ++l) g.J[l].alloc((size_t)Sg * 7 * ms[l] * ms[l]);
+    if (f32_planes) {
+      g.Jf.resize(nl);
+      for (int l = 0; l + 1 < nl; ++l) g.Jf[l].alloc((size_t)Sg * 4 * ms[l] * ms[l]);
+    }
     g.inv.alloc((size_t)Sg * nL * nL);
     g.d_slice.alloc(Sg);
     g.d_active.alloc(Sg);
@@ -138,7 +148,10 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
     g.d_bscale.alloc(Sg);
     g.d_wscale.alloc(Sg);
     std::vector<LevelOp> ops(nl);
-    for (int l = 0; l < nl; ++l) ops[l] = {ms[l], ms[l] * ms[l], g.J[l].get(), nullptr, false, {}};
+    for (int l = 0; l < nl; ++l) {
+      ops[l] = {ms[l], ms[l] * ms[l], g.J[l].get(), nullptr, false, {}};
+      if (f32_planes && l + 1 < nl) ops[l].Kf = g.Jf[l].get();
+    }
     g.solver.init(this, ops, Sg, mc);
     g.solver.coarse_inv = g.inv.get();
   }
@@ -190,6 +203,8 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
         launch_element_stencil(*this, true, g.Ub.get(), g.J[0].get(), nb);
         for (int l = 1; l < nl; ++l) launch_rap(*this, g.J[l - 1].get(), ms[l - 1], g.J[l].get(), ms[l], nb);
         launch_coarse_inverse_slice(*this, g.J[nl - 1].get(), ms[nl - 1], g.inv.get(), nb);
+        if (f32_planes)
+          for (int l = 0; l + 1 < nl; ++l) launch_planes_f32(*this, g.J[l].get(), ms[l], g.Jf[l].get(), nb);
         // delta = J^{-1} r  (masked to the active slices), then the Armijo
         // backtracking search (solvers.hpp:158-177).  Inexact Newton (DESIGN
         // §5e): a slice's linear tolerance eta follows its observed contraction

@@ -19,7 +19,7 @@ ap.add_argument("--config", type=int, default=2)
 ap.add_argument("--settings", nargs="+", default=[""])
 a = ap.parse_args()
 cfg = default_cfg(tol=1e-8)
-KEYS = ("TPGPU_NEWTON_FORCING", "TPGPU_NEWTON_WARM")
+KEYS = ("TPGPU_NEWTON_FORCING", "TPGPU_NEWTON_WARM", "TPGPU_NEWTON_F32")
 
 
 def apply(setting):
