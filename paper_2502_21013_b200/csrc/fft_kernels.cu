@@ -464,10 +464,10 @@ __device__ __forceinline__ cplx tw_at(const cplx* tw, int m) {
   return cmul(tw[m >> 5], tw[N / 32 + (m & 31)]);
 }
 
-template <int R, bool INV, int N, int P, int Ns>
+template <int R, bool INV, int N, int P, int Ns, int VPT>
 __device__ __forceinline__ void stockham_pass_t(cplx* z, const cplx* tw) {
-  constexpr int T = P * N / 16;
-  constexpr int B = 16 / R;
+  constexpr int T = P * N / VPT;
+  constexpr int B = VPT / R;
   constexpr int NR = N / R;
   cplx v[B][R];
 #pragma unroll
@@ -498,25 +498,30 @@ __device__ __forceinline__ void stockham_pass_t(cplx* z, const cplx* tw) {
   __syncthreads();
 }
 
-template <bool INV, int N, int P, int Ns = 1>
+// VPT values per thread: 16 (radix-16 passes, then one of 8, 4 or 2) or 8
+// (radix-8 passes, twice the threads at half the registers each)
+template <bool INV, int N, int P, int VPT, int Ns = 1>
 __device__ __forceinline__ void stockham_t(cplx* z, const cplx* tw) {
-  if constexpr (Ns * 16 <= N) {
-    stockham_pass_t<16, INV, N, P, Ns>(z, tw);
-    stockham_t<INV, N, P, Ns * 16>(z, tw);
+  if constexpr (VPT == 16 && Ns * 16 <= N) {
+    stockham_pass_t<16, INV, N, P, Ns, VPT>(z, tw);
+    stockham_t<INV, N, P, VPT, Ns * 16>(z, tw);
+  } else if constexpr (VPT == 8 && Ns * 8 <= N) {
+    stockham_pass_t<8, INV, N, P, Ns, VPT>(z, tw);
+    stockham_t<INV, N, P, VPT, Ns * 8>(z, tw);
   } else if constexpr (N / Ns == 8) {
-    stockham_pass_t<8, INV, N, P, Ns>(z, tw);
+    stockham_pass_t<8, INV, N, P, Ns, VPT>(z, tw);
   } else if constexpr (N / Ns == 4) {
-    stockham_pass_t<4, INV, N, P, Ns>(z, tw);
+    stockham_pass_t<4, INV, N, P, Ns, VPT>(z, tw);
   } else if constexpr (N / Ns == 2) {
-    stockham_pass_t<2, INV, N, P, Ns>(z, tw);
+    stockham_pass_t<2, INV, N, P, Ns, VPT>(z, tw);
   }
 }
 
-template <int N, int P>
-__global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB : 1) k_sfft_forward_t(const double* __restrict__ G, cplx* __restrict__ Ghat,
+template <int N, int P, int VPT = 16>
+__global__ void __launch_bounds__(P * N / VPT, P * N / VPT == 256 ? TPGPU_FFT_MINB : P * N / VPT == 512 ? 2 : 1) k_sfft_forward_t(const double* __restrict__ G, cplx* __restrict__ Ghat,
                                                              size_t n, const cplx* __restrict__ tw,
                                                              double* __restrict__ sq, const int* __restrict__ kslot) {
-  constexpr int T = P * N / 16, C = 2 * P, K = N / 2 + 1, RS = T / C;  // RS: rows per sweep of the block
+  constexpr int T = P * N / VPT, C = 2 * P, K = N / 2 + 1, RS = T / C;  // RS: rows per sweep of the block
   static_assert(T % C == 0 && T <= 512, "shape");
   extern __shared__ cplx smem[];
   cplx* tws = smem;
@@ -535,7 +540,7 @@ __global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB
   }
   acp_wait_all();
   __syncthreads();
-  stockham_t<false, N, P>(z, tws);
+  stockham_t<false, N, P, VPT>(z, tws);
   // untangle the two packed real columns: X = (Z_k + conj Z_{N-k}) / 2 (even
   // column), (Z_k - conj Z_{N-k}) / 2i (odd column)
   double e = 0;
@@ -555,11 +560,11 @@ __global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB
   if (sq) block_sum_to(e, sq + blockIdx.x);
 }
 
-template <int N, int P>
-__global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB : 1) k_sfft_inverse_t(const cplx* __restrict__ Uhat, double* __restrict__ U,
+template <int N, int P, int VPT = 16>
+__global__ void __launch_bounds__(P * N / VPT, P * N / VPT == 256 ? TPGPU_FFT_MINB : P * N / VPT == 512 ? 2 : 1) k_sfft_inverse_t(const cplx* __restrict__ Uhat, double* __restrict__ U,
                                                              size_t n, const cplx* __restrict__ tw,
                                                              double* __restrict__ part, const int* __restrict__ kslot) {
-  constexpr int T = P * N / 16, C = 2 * P, half = N / 2, K = half + 1, RS = T / C, KS = T / P;
+  constexpr int T = P * N / VPT, C = 2 * P, half = N / 2, K = half + 1, RS = T / C, KS = T / P;
   static_assert(T % C == 0 && T <= 512, "shape");
   extern __shared__ cplx smem[];
   __shared__ double red[2][32];
@@ -607,7 +612,7 @@ __global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB
   }
   acp_wait_all();
   __syncthreads();
-  stockham_t<true, N, P>(z, tws);
+  stockham_t<true, N, P, VPT>(z, tws);
   constexpr double invN = 1.0 / N;
   double re2 = 0;
   const double* zd = reinterpret_cast<const double*>(z);
@@ -647,14 +652,15 @@ __global__ void __launch_bounds__(P * N / 16, P * N / 16 == 256 ? TPGPU_FFT_MINB
 // the compiled shapes: (N, P) -> kernel pointers (nullptr: runtime-shaped kernels)
 using FwdFn = void (*)(const double*, cplx*, size_t, const cplx*, double*, const int*);
 using InvFn = void (*)(const cplx*, double*, size_t, const cplx*, double*, const int*);
-template <int N, int P>
-bool pick_shape(int n_, int p_, FwdFn& f, InvFn& g) {
-  if (n_ != N || p_ != P) return false;
-  f = k_sfft_forward_t<N, P>;
-  g = k_sfft_inverse_t<N, P>;
+template <int N, int P, int VPT = 16>
+bool pick_shape(int n_, int p_, FwdFn& f, InvFn& g, int vpt = 16) {
+  if (n_ != N || p_ != P || vpt != VPT) return false;
+  f = k_sfft_forward_t<N, P, VPT>;
+  g = k_sfft_inverse_t<N, P, VPT>;
   return true;
 }
-bool compiled_shape(int N, int P, FwdFn& f, InvFn& g) {
+bool compiled_shape(int N, int P, FwdFn& f, InvFn& g, int vpt) {
+  if (vpt == 8) return pick_shape<1024, 4, 8>(N, P, f, g, vpt) || pick_shape<512, 4, 8>(N, P, f, g, vpt);
   return pick_shape<64, 32>(N, P, f, g) || pick_shape<128, 16>(N, P, f, g) || pick_shape<256, 8>(N, P, f, g) ||
          pick_shape<512, 4>(N, P, f, g) || pick_shape<1024, 4>(N, P, f, g) || pick_shape<1024, 2>(N, P, f, g) ||
          pick_shape<1024, 8>(N, P, f, g) || pick_shape<2048, 4>(N, P, f, g) ||
@@ -844,6 +850,7 @@ struct FftPlan {
   InvFn ti = nullptr;
   DevBuf<cplx> tw2;      // their compact twiddle table (hi: W^{32j}, j < N/32; lo: W^i, i < 32)
   size_t tsmem = 0;      // their shared bytes
+  int tT = 0;            // their threads per block
   size_t ssmem = 0, fsmem = 0;  // inverse (+ staged half spectrum) / forward
   // pipelined persistent kernels (N >= 512): column pairs, threads, shared bytes, grid
   bool pp_fwd = false, pp_inv = false;
@@ -902,9 +909,14 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
       static const bool want_t = !std::getenv("TPGPU_FFT_TEMPLATE") || std::atoi(std::getenv("TPGPU_FFT_TEMPLATE")) != 0;
       FwdFn f = nullptr;
       InvFn g = nullptr;
-      if (want_t && siP == sP && compiled_shape(N, sP, f, g)) {
+      // values per thread of the compiled shapes (TPGPU_FFT_VPT=8: radix-8
+      // passes with twice the threads; 16 otherwise)
+      static const int vpt_env = std::getenv("TPGPU_FFT_VPT") ? std::atoi(std::getenv("TPGPU_FFT_VPT")) : 16;
+      int vpt = vpt_env == 8 && compiled_shape(N, sP, f, g, 8) ? 8 : 16;
+      if (want_t && siP == sP && compiled_shape(N, sP, f, g, vpt)) {
         pl->tf = f;
         pl->ti = g;
+        pl->tT = sP * N / vpt;
         const int nt = N / 32 + 32;
         std::vector<cplx> t2(nt);
         for (int j = 0; j < N / 32; ++j) {
@@ -985,7 +997,7 @@ void dft_forward(const DftCtx& c, const double* G, cplx* Ghat, double* sq) {
     k_sfft_forward_pp<<<pl.pgrid, pl.pT, pl.pfsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.pP, pl.tw.get(), sq, c.kslot,
                                                                  ntiles);
   } else if (pl.tf) {
-    pl.tf<<<blocks, pl.sT, pl.tsmem, c.stream>>>(G, Ghat, c.n, pl.tw2.get(), sq, c.kslot);
+    pl.tf<<<blocks, pl.tT, pl.tsmem, c.stream>>>(G, Ghat, c.n, pl.tw2.get(), sq, c.kslot);
   } else if (pl.stockham) {
     k_sfft_forward<<<blocks, pl.sT, pl.fsmem, c.stream>>>(G, Ghat, c.n, pl.N, pl.sP, pl.tw.get(), sq, c.kslot);
   } else {
@@ -1006,7 +1018,7 @@ void dft_inverse(const DftCtx& c, const cplx* Uhat, double* U, double* re2, doub
     k_sfft_inverse_pp<<<pl.pgrid, pl.pT, pl.pismem, c.stream>>>(Uhat, U, c.n, pl.N, pl.pP, pl.tw.get(),
                                                                  c.part->get(), c.kslot, ntiles);
   } else if (pl.ti) {
-    pl.ti<<<blocks, pl.siT, pl.tsmem, c.stream>>>(Uhat, U, c.n, pl.tw2.get(), c.part->get(), c.kslot);
+    pl.ti<<<blocks, pl.tT, pl.tsmem, c.stream>>>(Uhat, U, c.n, pl.tw2.get(), c.part->get(), c.kslot);
   } else if (pl.stockham) {
     k_sfft_inverse<<<blocks, pl.siT, pl.ssmem, c.stream>>>(Uhat, U, c.n, pl.N, pl.siP, pl.tw.get(),
                                                             c.part->get(), c.kslot);

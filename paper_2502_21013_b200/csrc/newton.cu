@@ -123,9 +123,11 @@ void Problem::static_init_dev(const tp_solver_cfg& cfg, int32_t* newton_counts) 
   const bool forcing = f_gamma > 0;
 
   // fp32 copies of the Jacobian planes for the V-cycle passes (the PCG
-  // operator stays fp64; only the preconditioner reads rounded coefficients;
-  // TPGPU_NEWTON_F32=0: fp64 planes)
-  const bool f32_planes = !std::getenv("TPGPU_NEWTON_F32") || std::atoi(std::getenv("TPGPU_NEWTON_F32")) != 0;
+  // operator stays fp64; only the preconditioner reads rounded coefficients).
+  // Opt-in (TPGPU_NEWTON_F32=1): no measurable change (cfg 2 4.55 vs 4.53 s,
+  // cfg 3 30.0 vs 30.0 s, profiles/r2zb_init_ab.txt) -- the slice-mode passes
+  // are latency-bound, not bound by their coefficient bytes
+  const bool f32_planes = std::getenv("TPGPU_NEWTON_F32") && std::atoi(std::getenv("TPGPU_NEWTON_F32")) != 0;
 
   std::vector<std::unique_ptr<NewtonGroup>> groups(G);
   for (auto& gp : groups) {
