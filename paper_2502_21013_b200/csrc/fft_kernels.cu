@@ -910,7 +910,10 @@ FftPlan& plan_for(std::shared_ptr<void>& slot, int N) {
       FwdFn f = nullptr;
       InvFn g = nullptr;
       // values per thread of the compiled shapes (TPGPU_FFT_VPT=8: radix-8
-      // passes with twice the threads; 16 otherwise)
+      // passes with twice the threads at 64 registers; measured slower at
+      // cfg 3: forward / inverse 22.1 / 24.4 vs 20.9 / 23.1 ms, 281 vs 277 ms
+      // per sweep, profiles/r2zc_ab.txt -- the fourth pass through shared
+      // memory and its barrier cost more than the doubled occupancy gains)
       static const int vpt_env = std::getenv("TPGPU_FFT_VPT") ? std::atoi(std::getenv("TPGPU_FFT_VPT")) : 16;
       int vpt = vpt_env == 8 && compiled_shape(N, sP, f, g, 8) ? 8 : 16;
       if (want_t && siP == sP && compiled_shape(N, sP, f, g, vpt)) {
