@@ -214,7 +214,10 @@ __global__ void __launch_bounds__(TX * TY) k_sweep_fused(
 // u tiles of the next SD-1 slices are in flight (cp.async ring of SD slots,
 // zero-filled off the domain, one barrier per slice): with one slice of
 // look-ahead the kernel was latency-bound at ~1.3 TB/s.
-constexpr int SB = 16;
+#ifndef TPGPU_SWEEP_SB
+#define TPGPU_SWEEP_SB 16
+#endif
+constexpr int SB = TPGPU_SWEEP_SB;  // slices per block
 #ifndef TPGPU_SWEEP_SD
 #define TPGPU_SWEEP_SD 6
 #endif
