@@ -427,6 +427,234 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
   if (tid == 0) part[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] = tot;
 }
 
+// Row-walking form of the sweep kernel (the default; TPGPU_SWEEP_TILE=1 keeps
+// k_sweep_slices): one warp owns a column strip of RW_LANES = 30 nodes (32
+// lanes: the strip plus one halo column on each side), a chunk of node rows
+// and SG consecutive slices, and walks its rows upward with u rows y-1, y,
+// y+1 (and y+2 in flight) of its slices in registers.  East/west
+// neighbours and the west triangles come by warp shuffles, the triangles of
+// the cell row below are carried from the previous row: no shared-memory
+// tile and no block barrier (k_sweep_slices is bound by its per-slice
+// barrier and its shared-memory wavefronts).  nu(|grad u|) is
+// evaluated once per triangle (the halo lanes' cells excepted) and skipped
+// where the material is linear: there the weight is nu0/2, exactly what the
+// fma gives with dnu = 0.  Slice-invariant row data (cell materials, lumped
+// mass, source profiles) is loaded once per row for the SG slices, and only
+// in the strips/chunks where it is nonzero (host-built region flags);
+// u^{s-1} is the previous slice's register row (the group's first slice
+// reads slice s0-1 where there is mass).  Per node the formulas and the
+// summation order are k_sweep_slices', so U-> G is bitwise the same; the
+// residual partials are summed per block in another fixed order.
+constexpr int RW_LANES = 30;
+constexpr int RW_WARPS = 4;  // warps per block: consecutive slice groups of one region
+#ifndef TPGPU_SWEEP_SG
+#define TPGPU_SWEEP_SG 4
+#endif
+#ifndef TPGPU_SWEEP_H
+#define TPGPU_SWEEP_H 64
+#endif
+
+// source row of node row y (global) for the lane's column: nullptr = zero
+// (Dirichlet boundary, outside the strip and its halo rows); `st` = stride
+// between consecutive slices
+__device__ __forceinline__ const double* rw_row(const double* U, const double* lo, const double* hi, int sy0,
+                                                int rows, int m, size_t nl, int y, int x, bool colok, size_t& st) {
+  st = 0;
+  if (!colok || y < 0 || y >= m) return nullptr;
+  const int ly = y - sy0;
+  if (ly >= 0 && ly < rows) {
+    st = nl;
+    return U + (size_t)ly * m + x;
+  }
+  if (ly == -1 && lo) {
+    st = m;
+    return lo + x;
+  }
+  if (ly == rows && hi) {
+    st = m;
+    return hi + x;
+  }
+  return nullptr;
+}
+
+#ifndef TPGPU_SWEEP_MINB_RW
+#define TPGPU_SWEEP_MINB_RW 4
+#endif
+template <bool WANT_G, int SG, int NS>  // NS: source profiles held per node (>= nsrc)
+__global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_rows(
+    const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
+    int sy0, int rows, double* __restrict__ G, double* __restrict__ part, int m, int c, int N, double inv_tau,
+    const uint8_t* __restrict__ cell_mat, const MaterialDev* __restrict__ mats,
+    const double* __restrict__ nu_hat, const double* __restrict__ mass,
+    const double* __restrict__ src_prof, const double* __restrict__ src_time, int nsrc,
+    const uint8_t* __restrict__ rflags, int H, int nstrips, int nsgb) {
+  __shared__ double tab[4][TP_MAX_MATERIALS];  // per material: dnu/2, Bs^2/c^2, nu0/2, nu_hat/2
+  __shared__ double stime[RW_WARPS][SG][TP_MAX_MATERIALS];
+  __shared__ double red[RW_WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const size_t n = (size_t)m * m;
+  const size_t nl = (size_t)rows * m;
+  const double inv_c2 = 1.0 / ((double)c * (double)c);
+  if (threadIdx.x < TP_MAX_MATERIALS) {
+    const MaterialDev md = mats[threadIdx.x];
+    tab[0][threadIdx.x] = md.linear ? 0.0 : 0.5 * (md.nu_inf - md.nu0);
+    tab[1][threadIdx.x] = md.bs2 * inv_c2;
+    tab[2][threadIdx.x] = 0.5 * md.nu0;
+    tab[3][threadIdx.x] = WANT_G ? 0.5 * nu_hat[threadIdx.x] : 0.0;
+  }
+  const int region = blockIdx.x / nsgb, sgb = blockIdx.x - region * nsgb;
+  const int strip = region % nstrips, chunk = region / nstrips;
+  const int s0 = (sgb * RW_WARPS + w) * SG;
+  const int ns = max(0, min(SG, N - s0));
+  for (int k = lane; k < SG * TP_MAX_MATERIALS; k += 32) {
+    const int sl = k / TP_MAX_MATERIALS, r = k - sl * TP_MAX_MATERIALS;
+    stime[w][sl][r] = (sl < ns && r < nsrc) ? src_time[(size_t)(s0 + sl) * nsrc + r] : 0.0;
+  }
+  __syncthreads();
+  const int flags = rflags[region];
+  const bool hasm = flags & 1, hasf = flags & 2;
+  const int X = strip * RW_LANES + lane;  // vertex column (node x = X - 1)
+  const int x = X - 1;
+  const bool colok = X >= 1 && X <= m;
+  const bool own = lane >= 1 && lane <= RW_LANES && colok;
+  const bool cellok = X <= c - 1;  // this lane's cell column exists
+  const int ya = sy0 + chunk * H, yb = min(sy0 + rows, ya + H);
+  double r2 = 0;
+  if (ns > 0) {
+    // u of row y for the group's slices (zero-filled), material of cell (X, j)
+    auto load_u = [&](int y, double (&v)[SG]) {
+      size_t st;
+      const double* p = rw_row(U, halo_lo, halo_hi, sy0, rows, m, nl, y, x, colok, st);
+#pragma unroll
+      for (int k = 0; k < SG; ++k) v[k] = (p && k < ns) ? __ldg(p + (size_t)(s0 + k) * st) : 0.0;
+    };
+    auto load_mat = [&](int j) -> int { return (cellok && j >= 0 && j < c) ? (int)__ldg(cell_mat + (size_t)j * c + X) : -1; };
+    // row-invariant per-node data for node row y (mass, source profiles, u^{s0-1})
+    auto load_node = [&](int y, double& mi, double (&pr)[NS], double& up) {
+      const bool ok = own && y < yb;
+      const size_t i = (size_t)y * m + x;
+      mi = 0.0;
+      up = 0.0;
+      if (hasm && ok) {
+        mi = __ldg(mass + i);
+        if (mi != 0.0) up = __ldg(U + (size_t)((s0 + N - 1) % N) * nl + (size_t)(y - sy0) * m + x);
+      }
+#pragma unroll
+      for (int r = 0; r < NS; ++r) pr[r] = (hasf && ok && r < nsrc) ? __ldg(src_prof + r * n + i) : 0.0;
+    };
+    // the two triangles of cell (X, j) from u at its corners
+    auto cell = [&](int mt, double u00, double u10, double u01, double u11, double& w1, double& w2) {
+      if (mt < 0) {
+        w1 = w2 = 0.0;
+        return;
+      }
+      const double c0 = tab[0][mt], c1 = tab[1][mt], c2 = tab[2][mt];
+      if (c0 == 0.0) {  // linear material: fma(0, finite, nu0/2) == nu0/2
+        w1 = w2 = c2;
+        return;
+      }
+      const double ax = u10 - u00, ay = u11 - u10, bx = u11 - u01, by = u01 - u00;
+      const double qa = fma(ax, ax, ay * ay), qb = fma(bx, bx, by * by);
+      w1 = fma(c0, qa * acc_rcp(qa + c1), c2);
+      w2 = fma(c0, qb * acc_rcp(qb + c1), c2);
+    };
+    constexpr unsigned FULL = 0xffffffffu;
+    double uS[SG], uC[SG], uN[SG], uQ[SG];
+    double b2[SG], t3[SG], t4[SG];  // lower cell row: own T2, west T1, west T2
+    load_u(ya - 1, uS);
+    load_u(ya, uC);
+    int matL = load_mat(ya);  // cell row below node row ya
+    load_u(ya + 1, uN);
+    int matU = load_mat(ya + 1);
+    double mi, pr[NS], up;
+    load_node(ya, mi, pr, up);
+    {
+#pragma unroll
+      for (int k = 0; k < SG; ++k) {
+        const double e0 = __shfl_down_sync(FULL, uS[k], 1), e1 = __shfl_down_sync(FULL, uC[k], 1);
+        double w1, w2;
+        cell(matL, uS[k], e0, uC[k], e1, w1, w2);
+        b2[k] = w2;
+        t3[k] = __shfl_up_sync(FULL, w1, 1);
+        t4[k] = __shfl_up_sync(FULL, w2, 1);
+      }
+    }
+    double hb = matL >= 0 ? tab[3][matL] : 0.0;
+    double h3 = __shfl_up_sync(FULL, hb, 1);
+    double* gp = WANT_G ? G + (size_t)(ya - sy0) * m + x : nullptr;
+    for (int y = ya; y < yb; ++y) {
+      // in flight: row y+2 and its cell row, the next row's node data
+      load_u(y + 2, uQ);
+      const int matQ = load_mat(y + 2);
+      double mi2, pr2[NS], up2;
+      load_node(y + 1, mi2, pr2, up2);
+      const double ha = matU >= 0 ? tab[3][matU] : 0.0;
+      const double hau = __shfl_up_sync(FULL, ha, 1);
+#pragma unroll
+      for (int k = 0; k < SG; ++k) {
+        const double uc = uC[k];
+        const double uE = __shfl_down_sync(FULL, uc, 1), uW = __shfl_up_sync(FULL, uc, 1);
+        const double uNE = __shfl_down_sync(FULL, uN[k], 1);
+        double a1, a2;
+        cell(matU, uc, uE, uN[k], uNE, a1, a2);
+        const double a1u = __shfl_up_sync(FULL, a1, 1), a2u = __shfl_up_sync(FULL, a2, 1);
+        if (own && y < yb && k < ns) {
+          const double un = uN[k], us = uS[k];
+          const double con[6] = {-(uE - uc), -(un - uc), (uc - uW) - (un - uc), uc - us, uc - uW,
+                                 -(uE - uc) + (uc - us)};
+          const double wt[6] = {a1, a2, a1u, t3[k], t4[k], b2[k]};
+          const double hh[6] = {ha, ha, hau, h3, h3, hb};
+          double ku = 0, kh = 0;
+#pragma unroll
+          for (int t6 = 0; t6 < 6; ++t6) {
+            ku = fma(wt[t6], con[t6], ku);
+            if (WANT_G) kh = fma(hh[t6], con[t6], kh);
+          }
+          double f = 0;
+          if (hasf) {
+#pragma unroll
+            for (int r = 0; r < NS; ++r)
+              if (r < nsrc) f = fma(stime[w][k][r], pr[r], f);
+          }
+          if (WANT_G) __stcs(gp + (size_t)(s0 + k) * nl, f + kh - ku);
+          const double uprev = k == 0 ? up : uC[k > 0 ? k - 1 : 0];
+          const double mdu = mi != 0 ? mi * ((uc - uprev) * inv_tau) : 0.0;
+          const double res = f - mdu - ku;
+          r2 = fma(res, res, r2);
+        }
+        b2[k] = a2;
+        t3[k] = a1u;
+        t4[k] = a2u;
+      }
+#pragma unroll
+      for (int k = 0; k < SG; ++k) {
+        uS[k] = uC[k];
+        uC[k] = uN[k];
+        uN[k] = uQ[k];
+      }
+      matU = matQ;
+      hb = ha;
+      h3 = hau;
+      mi = mi2;
+      up = up2;
+#pragma unroll
+      for (int r = 0; r < NS; ++r) pr[r] = pr2[r];
+      if (WANT_G) gp += m;
+    }
+  }
+  // fixed-order block reduction: butterfly within the warp, warps in order
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+  if (lane == 0) red[w] = r2;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0;
+#pragma unroll
+    for (int k = 0; k < RW_WARPS; ++k) s += red[k];
+    part[blockIdx.x] = s;
+  }
+}
+
 __global__ void k_reduce_sum(const double* __restrict__ in, int count, double* __restrict__ out) {
   __shared__ double sh[32];
   double v = 0;
@@ -598,25 +826,71 @@ static size_t sweep_partials(int m, int N) {
   return (size_t)((m + TX - 1) / TX) * ((m + TY - 1) / TY) * N;
 }
 
+// region flags of the row-walking sweep kernel: per (row chunk, column strip)
+// of this rank's node rows, bit 0 = some node has mass, bit 1 = some node
+// has a source profile
+static std::vector<uint8_t> sweep_region_flags(const Problem& p, int H, int nstrips, int nchunks) {
+  std::vector<uint8_t> f((size_t)nstrips * nchunks, 0);
+  const int nsrc = (int)p.src_mats.size();
+  for (int y = p.sh.y0; y < p.sh.y1; ++y)
+    for (int x = 0; x < p.m; ++x) {
+      const size_t i = (size_t)y * p.m + x;
+      uint8_t b = p.mass[i] != 0.0 ? 1 : 0;
+      for (int r = 0; r < nsrc; ++r)
+        if (p.src_prof[(size_t)r * p.n + i] != 0.0) b |= 2;
+      f[(size_t)((y - p.sh.y0) / H) * nstrips + x / RW_LANES] |= b;
+    }
+  return f;
+}
+
 double Problem::residual_and_rhs(bool want_rhs) {
   const int rows = sh.y1 - sh.y0;
   if (sharded()) exchange_halo();
-  dim3 grid((m + TX - 1) / TX, (rows + TY - 1) / TY, (N + SB - 1) / SB);
-  const size_t np = (size_t)grid.x * grid.y * grid.z;
-  part.ensure(np);
   const int nsrc = (int)src_mats.size();
   require(nsrc <= TP_MAX_MATERIALS, "sweep: too many source materials");
+  require(!want_rhs || nu_hat_set, "fixed-point sweep: nu_hat not installed");
   const double* lo = sharded() ? halo_lo.get() : nullptr;
   const double* hi = sharded() ? halo_hi.get() : nullptr;
-  if (want_rhs) {
-    require(nu_hat_set, "fixed-point sweep: nu_hat not installed");
-    k_sweep_slices<true><<<grid, dim3(TX, TYT), 0, stream>>>(
-        U.get(), lo, hi, sh.y0, rows, G.get(), part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
-        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+  // k_sweep_slices (32x8 node tiles in shared memory) on request
+  static const bool tile = std::getenv("TPGPU_SWEEP_TILE") != nullptr;
+  size_t np;
+  if (!tile) {
+    constexpr int SG = TPGPU_SWEEP_SG, H = TPGPU_SWEEP_H;
+    const int nstrips = (m + RW_LANES - 1) / RW_LANES, nchunks = (rows + H - 1) / H;
+    const int nsgb = (N + SG * RW_WARPS - 1) / (SG * RW_WARPS);
+    if (rflags_key != H) {
+      const std::vector<uint8_t> f = sweep_region_flags(*this, H, nstrips, nchunks);
+      d_rflags.alloc(f.size());
+      TP_CUDA(cudaMemcpy(d_rflags.get(), f.data(), f.size(), cudaMemcpyHostToDevice));
+      rflags_key = H;
+    }
+    const dim3 grid((unsigned)((size_t)nstrips * nchunks * nsgb));
+    np = grid.x;
+    part.ensure(np);
+#define TP_SWEEP_ROWS(WG, NS)                                                                                   \
+  k_sweep_rows<WG, SG, NS><<<grid, 32 * RW_WARPS, 0, stream>>>(                                                 \
+      U.get(), lo, hi, sh.y0, rows, WG ? G.get() : nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), \
+      d_mat.get(), d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc, d_rflags.get(), H,  \
+      nstrips, nsgb)
+    if (nsrc <= 2) {
+      if (want_rhs) TP_SWEEP_ROWS(true, 2); else TP_SWEEP_ROWS(false, 2);
+    } else {
+      if (want_rhs) TP_SWEEP_ROWS(true, TP_MAX_MATERIALS); else TP_SWEEP_ROWS(false, TP_MAX_MATERIALS);
+    }
+#undef TP_SWEEP_ROWS
   } else {
-    k_sweep_slices<false><<<grid, dim3(TX, TYT), 0, stream>>>(
-        U.get(), lo, hi, sh.y0, rows, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
-        d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+    dim3 grid((m + TX - 1) / TX, (rows + TY - 1) / TY, (N + SB - 1) / SB);
+    np = (size_t)grid.x * grid.y * grid.z;
+    part.ensure(np);
+    if (want_rhs) {
+      k_sweep_slices<true><<<grid, dim3(TX, TYT), 0, stream>>>(
+          U.get(), lo, hi, sh.y0, rows, G.get(), part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+          d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+    } else {
+      k_sweep_slices<false><<<grid, dim3(TX, TYT), 0, stream>>>(
+          U.get(), lo, hi, sh.y0, rows, nullptr, part.get(), m, c, N, 1.0 / tau, d_cell_mat.get(), d_mat.get(),
+          d_nu_hat.get(), d_mass.get(), d_src_prof.get(), d_src_time.get(), nsrc);
+    }
   }
   TP_LAUNCHED(this);
   reduce_sum_dev(*this, part.get(), (int)np, red.get());

@@ -333,6 +333,8 @@ class Problem {
   DevBuf<double> d_src_time;
   DevBuf<MaterialDev> d_mat;
   DevBuf<double> d_nu_hat;
+  DevBuf<uint8_t> d_rflags;  // region flags of the row-walking sweep kernel (op_kernels.cu)
+  int rflags_key = -1;       // the row-chunk height they were built for
   DevBuf<double> d_coef;      // [we | wn | mass] of the fine streaming kernels (one L2-persisting block)
   DevBuf<double> d_we, d_wn;  // K_hat edge weights on the (c+1)^2 vertex grid (views into d_coef)
   void l2_persist(const void* base, size_t bytes, const std::vector<cudaStream_t>& ss);
