@@ -59,11 +59,12 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--configs", type=int, nargs="+", default=[0, 1, 2])
     ap.add_argument("--reps", type=int, default=5)
+    ap.add_argument("--rows-env", nargs="*", default=[], help="KEY=VAL for the rows run (e.g. TPGPU_LIB=libtpgpu_ra8.so)")
     a = ap.parse_args()
     ok = True
     for cfgi in a.configs:
         pr, pt = f"/tmp/U_rows_{cfgi}.npy", f"/tmp/U_tile_{cfgi}.npy"
-        rows = run(cfgi, {}, a.reps, pr)
+        rows = run(cfgi, dict(e.split("=", 1) for e in a.rows_env), a.reps, pr)
         tile = run(cfgi, {"TPGPU_SWEEP_TILE": "1"}, a.reps, pt)
         d_r0 = abs(rows["r0"] - tile["r0"]) / tile["r0"]
         # sweep residuals against the first (near the fp64 floor of cfg >= 2 the
