@@ -480,6 +480,17 @@ __device__ __forceinline__ const double* rw_row(const double* U, const double* l
 #ifndef TPGPU_SWEEP_MINB_RW
 #define TPGPU_SWEEP_MINB_RW 4
 #endif
+// rows of u staged ahead through a private per-warp shared-memory ring by
+// per-lane cp.async copies (0: row y+2 is prefetched into registers instead).
+// A lane reads back only what it copied itself, so cp.async.wait_group is
+// the only synchronisation; RA + 2 slots, the overwritten slot was read two
+// rows earlier.  Zero rows (boundary, outside the strip) are zero-filled by
+// the copy (src-size 0).
+#ifndef TPGPU_SWEEP_RA
+#define TPGPU_SWEEP_RA 4
+#endif
+constexpr int RW_RA = TPGPU_SWEEP_RA;
+constexpr int RW_SLOTS = RW_RA > 0 ? RW_RA + 2 : 1;
 template <bool WANT_G, int SG, int NS>  // NS: source profiles held per node (>= nsrc)
 __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_rows(
     const double* __restrict__ U, const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
@@ -491,6 +502,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_ro
   __shared__ double tab[4][TP_MAX_MATERIALS];  // per material: dnu/2, Bs^2/c^2, nu0/2, nu_hat/2
   __shared__ double stime[RW_WARPS][SG][TP_MAX_MATERIALS];
   __shared__ double red[RW_WARPS];
+  __shared__ double ring[RW_RA > 0 ? RW_WARPS : 1][RW_SLOTS][RW_RA > 0 ? SG : 1][RW_RA > 0 ? 32 : 1];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const size_t n = (size_t)m * m;
   const size_t nl = (size_t)rows * m;
@@ -520,13 +532,48 @@ __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_ro
   const bool cellok = X <= c - 1;  // this lane's cell column exists
   const int ya = sy0 + chunk * H, yb = min(sy0 + rows, ya + H);
   double r2 = 0;
-  if (ns > 0) {
+#ifdef TPGPU_SWEEP_NSGUARD
+  if (ns > 0)
+#endif
+  {
+    // (no `ns > 0` guard: every access below is predicated on k < ns, and a
+    // branch on the warp index makes the compiler treat the whole row loop as
+    // possibly divergent -- a convergence check before every shuffle group)
     // u of row y for the group's slices (zero-filled), material of cell (X, j)
     auto load_u = [&](int y, double (&v)[SG]) {
       size_t st;
       const double* p = rw_row(U, halo_lo, halo_hi, sy0, rows, m, nl, y, x, colok, st);
 #pragma unroll
       for (int k = 0; k < SG; ++k) v[k] = (p && k < ns) ? __ldg(p + (size_t)(s0 + k) * st) : 0.0;
+    };
+    // the same row into the ring slot at byte offset `so` (asynchronous).
+    // Rows ya+2 .. yb-1 are interior rows of this rank's strip: a running
+    // pointer (`pint`, one row per call) and the slice stride nl; row yb can be
+    // a halo or boundary row (rw_row, selected by predicates: measured faster
+    // than a direct load of that row when it is due, 20.3 vs 21.6 ms at cfg 3);
+    // rows past yb are never read
+    const unsigned ring_lane = (unsigned)__cvta_generic_to_shared(&ring[w][0][0][RW_RA > 0 ? lane : 0]);
+    constexpr unsigned SLOT_B = SG * 32 * 8;
+    const double* pint = U + (size_t)s0 * nl + (size_t)(ya + 2 - sy0) * m + x;
+    auto stage_u = [&](int y, unsigned so) {
+      const double* q = pint;
+      size_t st = nl;
+      bool ok = colok && y < yb;
+      if (y == yb) {
+        q = rw_row(U, halo_lo, halo_hi, sy0, rows, m, nl, y, x, colok, st);
+        ok = q != nullptr;
+        if (ok) q += (size_t)s0 * st;
+      }
+      pint += m;
+#pragma unroll
+      for (int k = 0; k < SG; ++k) {
+        const bool okk = ok && k < ns;
+        asm volatile("cp.async.ca.shared.global [%0], [%1], 8, %2;\n" ::"r"(ring_lane + so + k * 256), "l"(okk ? q : U),
+                     "r"(okk ? 8 : 0)
+                     : "memory");
+        q += st;
+      }
+      asm volatile("cp.async.commit_group;\n" ::: "memory");
     };
     auto load_mat = [&](int j) -> int { return (cellok && j >= 0 && j < c) ? (int)__ldg(cell_mat + (size_t)j * c + X) : -1; };
     // row-invariant per-node data for node row y (mass, source profiles, u^{s0-1})
@@ -582,24 +629,52 @@ __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_ro
     double hb = matL >= 0 ? tab[3][matL] : 0.0;
     double h3 = __shfl_up_sync(FULL, hb, 1);
     double* gp = WANT_G ? G + (size_t)(ya - sy0) * m + x : nullptr;
+    unsigned slot_r = 0, slot_w = (RW_RA % RW_SLOTS) * SLOT_B;  // ring byte offset of row y+2 / of row y+2+RA
+    if constexpr (RW_RA > 0) {
+#pragma unroll
+      for (int j = 0; j < RW_RA; ++j) stage_u(ya + 2 + j, j * SLOT_B);
+    }
+    if (WANT_G) gp += (size_t)s0 * nl;
     for (int y = ya; y < yb; ++y) {
       // in flight: row y+2 and its cell row, the next row's node data
-      load_u(y + 2, uQ);
+      if constexpr (RW_RA > 0) {
+        asm volatile("cp.async.wait_group %0;\n" ::"n"(RW_RA > 0 ? RW_RA - 1 : 0) : "memory");
+        stage_u(y + 2 + RW_RA, slot_w);
+        slot_w = slot_w + SLOT_B == RW_SLOTS * SLOT_B ? 0 : slot_w + SLOT_B;
+      } else {
+        load_u(y + 2, uQ);
+      }
       const int matQ = load_mat(y + 2);
       double mi2, pr2[NS], up2;
       load_node(y + 1, mi2, pr2, up2);
       const double ha = matU >= 0 ? tab[3][matU] : 0.0;
       const double hau = __shfl_up_sync(FULL, ha, 1);
+      // the row's cell material is the same for the SG slices: coefficients
+      // once per row, and one warp-uniform branch around the material law
+      // (no lane of the strip in a nonlinear cell: weights are nu0/2)
+      const int mtc = max(matU, 0);
+      const double c0 = tab[0][mtc], c1 = tab[1][mtc], c2 = matU >= 0 ? tab[2][mtc] : 0.0;
+      const bool nlin = matU >= 0 && c0 != 0.0;
+      const bool anynl = __any_sync(FULL, nlin);
+      double* gk = gp;  // G of (slice s0 + k, row y)
 #pragma unroll
       for (int k = 0; k < SG; ++k) {
         const double uc = uC[k];
         const double uE = __shfl_down_sync(FULL, uc, 1), uW = __shfl_up_sync(FULL, uc, 1);
-        const double uNE = __shfl_down_sync(FULL, uN[k], 1);
-        double a1, a2;
-        cell(matU, uc, uE, uN[k], uNE, a1, a2);
+        const double un = uN[k], us = uS[k];
+        const double uNE = __shfl_down_sync(FULL, un, 1);
+        double a1 = c2, a2 = c2;
+        if (anynl) {
+          const double ax = uE - uc, ay = uNE - uE, bx = uNE - un, by = un - uc;
+          const double qa = fma(ax, ax, ay * ay), qb = fma(bx, bx, by * by);
+          const double n1 = fma(c0, qa * acc_rcp(qa + c1), c2), n2 = fma(c0, qb * acc_rcp(qb + c1), c2);
+          a1 = nlin ? n1 : c2;
+          a2 = nlin ? n2 : c2;
+        }
         const double a1u = __shfl_up_sync(FULL, a1, 1), a2u = __shfl_up_sync(FULL, a2, 1);
-        if (own && y < yb && k < ns) {
-          const double un = uN[k], us = uS[k];
+        {
+          // every lane evaluates its node (halo lanes and slices past N: values unused)
+          const bool act = own && k < ns;
           const double con[6] = {-(uE - uc), -(un - uc), (uc - uW) - (un - uc), uc - us, uc - uW,
                                  -(uE - uc) + (uc - us)};
           const double wt[6] = {a1, a2, a1u, t3[k], t4[k], b2[k]};
@@ -616,11 +691,12 @@ __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_ro
             for (int r = 0; r < NS; ++r)
               if (r < nsrc) f = fma(stime[w][k][r], pr[r], f);
           }
-          if (WANT_G) __stcs(gp + (size_t)(s0 + k) * nl, f + kh - ku);
+          if (WANT_G && act) __stcs(gk, f + kh - ku);
+          if (WANT_G) gk += nl;
           const double uprev = k == 0 ? up : uC[k > 0 ? k - 1 : 0];
           const double mdu = mi != 0 ? mi * ((uc - uprev) * inv_tau) : 0.0;
           const double res = f - mdu - ku;
-          r2 = fma(res, res, r2);
+          r2 = act ? fma(res, res, r2) : r2;
         }
         b2[k] = a2;
         t3[k] = a1u;
@@ -630,8 +706,13 @@ __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_ro
       for (int k = 0; k < SG; ++k) {
         uS[k] = uC[k];
         uC[k] = uN[k];
-        uN[k] = uQ[k];
+        if constexpr (RW_RA > 0) {  // row y+2, landed (wait_group above)
+          asm volatile("ld.shared.f64 %0, [%1];\n" : "=d"(uN[k]) : "r"(ring_lane + slot_r + k * 256) : "memory");
+        } else {
+          uN[k] = uQ[k];
+        }
       }
+      if constexpr (RW_RA > 0) slot_r = slot_r + SLOT_B == RW_SLOTS * SLOT_B ? 0 : slot_r + SLOT_B;
       matU = matQ;
       hb = ha;
       h3 = hau;
@@ -642,6 +723,7 @@ __global__ void __launch_bounds__(32 * RW_WARPS, TPGPU_SWEEP_MINB_RW) k_sweep_ro
       if (WANT_G) gp += m;
     }
   }
+  if constexpr (RW_RA > 0) asm volatile("cp.async.wait_group 0;\n" ::: "memory");
   // fixed-order block reduction: butterfly within the warp, warps in order
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) r2 += __shfl_xor_sync(0xffffffffu, r2, o);
