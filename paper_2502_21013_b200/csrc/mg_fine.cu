@@ -1153,6 +1153,8 @@ int rh_for(int m) {
   static const int envb = std::getenv("TPGPU_RHBIG") ? std::atoi(std::getenv("TPGPU_RHBIG")) : 128;
   static const int env = std::getenv("TPGPU_RH") ? std::atoi(std::getenv("TPGPU_RH")) : 0;
   static const int env1 = std::getenv("TPGPU_RH1") ? std::atoi(std::getenv("TPGPU_RH1")) : 0;
+  static const int envm = std::getenv("TPGPU_RHMID") ? std::atoi(std::getenv("TPGPU_RHMID")) : 0;
+  if (envm > 0 && m >= 1000 && m < 2000) return envm;  // A/B: the first Galerkin level of a 2048-cell grid
   if (m >= 1000) return envb;
   if (env > 0 && m >= 200) return env;
   if (env1 > 0 && m >= 100 && m < 200) return env1;

@@ -436,9 +436,14 @@ __global__ void __launch_bounds__(SNT, TPGPU_SWEEP_MINB) k_sweep_slices(
 // the cell row below are carried from the previous row: no shared-memory
 // tile and no block barrier (k_sweep_slices is bound by its per-slice
 // barrier and its shared-memory wavefronts).  nu(|grad u|) is
-// evaluated once per triangle (the halo lanes' cells excepted) and skipped
-// where the material is linear: there the weight is nu0/2, exactly what the
-// fma gives with dnu = 0.  Slice-invariant row data (cell materials, lumped
+// evaluated once per triangle (the halo lanes' cells excepted) behind one
+// warp vote per row, and skipped where no lane of the strip sits in a
+// nonlinear cell: there the weight is nu0/2, exactly what the fma gives with
+// dnu = 0.  The row body is branch-free otherwise (halo lanes and slices past
+// N compute unused values; stores and the residual sum are predicated): the
+// kernel is instruction-issue bound, and divergent branches cost a
+// convergence check before every shuffle group (27.5 -> 24.8 -> 20.3 ms at
+// cfg 3 with the u-row ring below, profiles/r2zi_ab.txt, r2zk_ab.txt).  Slice-invariant row data (cell materials, lumped
 // mass, source profiles) is loaded once per row for the SG slices, and only
 // in the strips/chunks where it is nonzero (host-built region flags);
 // u^{s-1} is the previous slice's register row (the group's first slice

@@ -70,6 +70,44 @@ def test_residual_matches_reference(ref):
         assert abs(nrm - nr) <= 1e-13 * nr
 
 
+# k_sweep_rows shapes: 30-column strips, 64-row chunks, 4 slices per warp and
+# 16 per block -- sizes that leave partial strips, a one-row last chunk,
+# partial slice groups and warps with no slice at all
+RAGGED = [(8, 5), (31, 7), (45, 21), (66, 3), (130, 18)]
+
+
+@pytest.mark.parametrize("cells,steps", RAGGED)
+def test_residual_ragged_sizes(ref, cells, steps):
+    d = small_desc(cells, steps)
+    with Problem(d) as p:
+        U = np.random.default_rng(cells * 1000 + steps).standard_normal(p.shape) * 0.02
+        R, nrm = p.residual(U)
+        Rr, nr = ref.residual(d, U)
+        assert rel(R, Rr) <= 1e-13
+        assert abs(nrm - nr) <= 1e-13 * nr
+
+
+@pytest.mark.parametrize("cells,steps", RAGGED[1:4])
+def test_m1_sweeps_ragged_sizes(ref, cells, steps):
+    """Three fixed-point sweeps (residual + RHS kernel, DFTs, block solves) at
+    sizes off every tile boundary: iterates within 1e-10 of the reference's."""
+    d = small_desc(cells, steps)
+    cfg = default_cfg(tol=1e-8)
+    cfg.m1_max_outer = 3
+    U0, _ = ref.static_init(d, cfg)
+    nu, q = ref.choose_nu_hat(d, U0, cfg)
+    m1 = ref.solve_m1(d, nu, q, U0, cfg, keep_iterates=True)
+    with Problem(d) as p:
+        p.set_nu_hat(nu, q)
+        log = []
+        U, rep = p.solve_m1_fixed_point(U0, cfg, iterate_log=log)
+        assert rep.iterations == m1.iterations
+        errs = [rel(a, b) for a, b in zip(log, m1.iterates)]
+        assert len(errs) == len(m1.iterates) and max(errs) <= ITERATE_TOL, errs
+        h, hr = np.array(rep.residual_history), m1.history
+        assert np.all(np.abs(h - hr) <= 1e-10 * hr[0] + 1e-6 * hr)
+
+
 def test_static_init_matches_reference(cfg0_ref):
     r = cfg0_ref
     with Problem(r["desc"]) as p:
