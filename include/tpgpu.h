@@ -156,6 +156,10 @@ void tp_solver_cfg_default(tp_solver_cfg* cfg);
 int tp_problem_desc_baseline(int32_t config, tp_problem_desc* desc);
 
 /* ---- setup (mesh, materials, sources; runner.hpp:46-73 up to static_init) */
+/* Grid sizes: K(u), the residual and the time transforms take any cells >= 2
+ * and any N >= 1; the solvers (tp_static_init, tp_periodic_solve, tp_solve_*)
+ * build a geometric hierarchy and need cells = 2^k * q with q <= 8
+ * (TP_EINVAL otherwise; every BASELINE configuration is a power of two). */
 int tp_problem_create(const tp_problem_desc* desc, int32_t device, tp_problem** out);
 void tp_problem_destroy(tp_problem* p);
 /* n_dof: dofs held by this problem (all free dofs; a sharded rank: its strip). */

@@ -87,10 +87,12 @@ def test_residual_ragged_sizes(ref, cells, steps):
         assert abs(nrm - nr) <= 1e-13 * nr
 
 
-@pytest.mark.parametrize("cells,steps", RAGGED[1:4])
+# the frequency solver's hierarchy needs cells = 2^k * q with q <= 8
+@pytest.mark.parametrize("cells,steps", [(40, 7), (56, 21), (160, 3)])
 def test_m1_sweeps_ragged_sizes(ref, cells, steps):
     """Three fixed-point sweeps (residual + RHS kernel, DFTs, block solves) at
-    sizes off every tile boundary: iterates within 1e-10 of the reference's."""
+    sizes off the sweep kernel's strip, chunk and slice-group boundaries:
+    iterates within 1e-10 of the reference's."""
     d = small_desc(cells, steps)
     cfg = default_cfg(tol=1e-8)
     cfg.m1_max_outer = 3
